@@ -1,0 +1,156 @@
+/*
+ * irminsul_b200.h -- C ABI of the B200-native cache-reattach hot path.
+ *
+ * The reference (Irminsul, /root/reference/pkg/src/irminsul) is a pure-Python
+ * package with no FFI; its "operator API" is a set of module functions. Each
+ * entry point below is the batched, device-resident replacement for one of
+ * them (file:line cited per function). The Python drop-in modules in
+ * paper_2605_05696_b200/ bind these through ctypes with the reference's own
+ * signatures.
+ *
+ * Conventions
+ *  - Every pointer argument is DEVICE memory owned by the caller (torch
+ *    tensors), unless the name ends in _h. No entry point allocates.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t) and returns
+ *    IRM_OK (0), IRM_EINVAL (1: bad argument -> ValueError), IRM_ECUDA
+ *    (2: CUDA error -> RuntimeError) or IRM_ECAPACITY (3: output/workspace
+ *    too small -> ValueError). irm_last_error() gives a message.
+ *  - Entry points are re-entrant across streams; calls that mutate one store
+ *    must be ordered on one stream by the caller (single-writer, like
+ *    registry.py:95-101).
+ */
+#ifndef IRMINSUL_B200_H
+#define IRMINSUL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *irm_stream_t; /* == cudaStream_t */
+
+#define IRM_OK 0
+#define IRM_EINVAL 1
+#define IRM_ECUDA 2
+#define IRM_ECAPACITY 3
+
+#define IRM_FORCED_NONE 0       /* chunking.py:31 Forced.NONE */
+#define IRM_FORCED_MAX_CLAMP 1  /* chunking.py:32 */
+#define IRM_FORCED_MARKER 2     /* chunking.py:33 */
+#define IRM_FORCED_STREAM_END 3 /* chunking.py:34 */
+
+#define IRM_LAYOUT_HALF_SPLIT 0  /* rotary.py:98-108 (DSv3-form, reference) */
+#define IRM_LAYOUT_INTERLEAVED 1 /* DSv2-form: pairs (2j, 2j+1) */
+
+#define IRM_DTYPE_F64 0
+#define IRM_DTYPE_F32 1
+#define IRM_DTYPE_BF16 2
+
+#define IRM_ROUND_NONE 0 /* rotary.py:90-95 _store(): F64 */
+#define IRM_ROUND_F32 1  /*                            F32 */
+#define IRM_ROUND_BF16 2 /*                            BF16E (single RNE rounding) */
+
+int irm_abi_version(void);
+const char *irm_last_error(void);
+int irm_device_sm_count(void);
+
+/* ---- constants (rng.py:17-38, chunking.py:64-86) ---------------------- */
+/* Gear table: out[i] = splitmix64 output i+1 of `seed`, 65,536 entries.
+ * Replaces chunking.build_gear_table / gear_table (chunking.py:64-76). */
+int irm_gear_table(uint64_t seed, uint64_t *out, irm_stream_t stream);
+
+/* ---- K1: CDC + xxh64 (chunking.py:89-133 + fingerprint.py:28-30) -------
+ * tok:        all streams' u32 tokens, concatenated.
+ * stream_off: [n_streams+1] token offsets (int64).
+ * pin_off:    [n_streams+1] offsets into pins; pins of one stream are
+ *             stream-relative token indices, sorted ascending (duplicates and
+ *             out-of-range values allowed: they never match, like `t in
+ *             markers`). A pin forces a boundary after token t and resets the
+ *             rolling state (chunking.py:116-118). marker_pinned=0 ignores them.
+ * Outputs (dense, stream-major, chunk order): c_start (stream-relative),
+ * c_len, c_fp, c_forced; chunk_off[n_streams+1] gets the per-stream CSR
+ * offsets (chunk_off[n_streams] = total chunks).
+ * cap must be >= irm_cdc_chunk_bound(); ws_bytes >= irm_cdc_workspace_bytes(). */
+int64_t irm_cdc_chunk_bound(int64_t n_tokens, int32_t n_streams, int64_t n_pins, int32_t min_size);
+int64_t irm_cdc_workspace_bytes(int64_t n_tokens, int32_t n_streams, int64_t n_pins, int32_t min_size);
+int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_off,
+                  int32_t n_streams, const int64_t *pin_off, const int64_t *pins, int64_t n_pins,
+                  int32_t mask_exponent, int32_t min_size, int32_t max_size, int32_t marker_pinned,
+                  const uint64_t *gear, int32_t *c_start, int32_t *c_len, uint64_t *c_fp,
+                  uint8_t *c_forced, int64_t *chunk_off, int64_t cap, void *ws, int64_t ws_bytes,
+                  irm_stream_t stream);
+
+/* ---- K2: batched xxh64 over byte spans (fingerprint.py:24-50) ----------
+ * out[i] = XXH64(base + off[i], len[i] bytes, seed). Token spans: off/len x4. */
+int irm_xxh64_spans(const uint8_t *base, const int64_t *off, const int64_t *len, int64_t n,
+                    uint64_t seed, uint64_t *out, irm_stream_t stream);
+
+/* ---- K3: content-hash chunk store (registry.py:113-140) ----------------
+ * Open-addressing table fingerprint -> entry, plus entry arrays, all caller
+ * owned. Initialise with irm_store_reset(). First writer wins by the
+ * smallest order key (registry.py:128-130 + engine.py's sequential order). */
+typedef struct {
+    uint64_t *slot_key;   /* [n_slots]   fingerprint or IRM_EMPTY_KEY          */
+    int64_t *slot_order;  /* [n_slots+1] batch claim (atomicMin), INT64_MAX idle */
+    int64_t *slot_entry;  /* [n_slots+1] entry index or -1; [n_slots] = fp==EMPTY */
+    int64_t n_slots;      /* power of two                                       */
+    uint64_t *e_fp;       /* [max_entries]                                      */
+    int64_t *e_p_src;     /* [max_entries] absolute source position (registry.py:82) */
+    int32_t *e_len;       /* [max_entries] chunk length                         */
+    int64_t *e_row;       /* [max_entries] first row in the latent pool         */
+    int64_t max_entries;
+    int64_t *counters;    /* [4]: n_entries, pool rows used, error flags (1 table
+                           full, 2 entries full; sticky), reserved            */
+} irm_store_view;
+#define IRM_EMPTY_KEY 0xFFFFFFFFFFFFFFFFULL
+
+int irm_store_reset(const irm_store_view *st, irm_stream_t stream);
+/* Batched lookup-or-insert of n queries, given in ascending q_order (the
+ * sequential serve order: request, then chunk). For probed queries
+ * (q_probe != 0; 0 = carve-out, engine.py:184-196: neither probed nor
+ * inserted):
+ *   q_hit = 1 and the entry's (p_src, row) if the fingerprint was stored
+ *     before the batch or inserted by an earlier query of the batch;
+ *   q_hit = 0 if this query is the first writer: a new entry is appended
+ *     with p_src = q_p, len = q_len, row = pool rows allocated in order.
+ * Unprobed queries get q_hit = -1. */
+int64_t irm_store_workspace_bytes(int64_t n);
+int irm_store_lookup_insert(const irm_store_view *st, const uint64_t *q_fp,
+                            const int64_t *q_order, const int64_t *q_p, const int32_t *q_len,
+                            const uint8_t *q_probe, int64_t n, int32_t *q_hit, int64_t *q_entry,
+                            int64_t *q_p_src, int64_t *q_row, void *ws, int64_t ws_bytes,
+                            irm_stream_t stream);
+/* Read-only batched lookup (registry.py:116-117): q_entry = -1 on miss. */
+int irm_store_lookup(const irm_store_view *st, const uint64_t *q_fp, int64_t n, int64_t *q_entry,
+                     irm_stream_t stream);
+
+/* ---- K4: delta-rotation rotate + gather (registry.py:146-166) ----------
+ * For each chunk c and layer l: rows [src_row[c], +len[c]) of the pool are
+ * copied to rows [dst_row[c], +len[c]) of out. Each row is ckv_dim latent
+ * values copied verbatim followed by kr_dim rotary values rotated by
+ * R(delta[c]) (angle = delta * inv_freq[j] in fp64, rotary.py:98-108).
+ * pool/out element (row r, layer l) at base + (l*layer_stride + r) * row_dim.
+ * dtype: element type of pool and out. out_round: IRM_ROUND_* applied to
+ * the rotated values (f64 pools only; BF16E/F32 store emulation). */
+int64_t irm_rotate_gather_workspace_bytes(int64_t n_chunks, int32_t kr_dim);
+int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, void *out,
+                      int64_t out_layer_stride, int32_t layers, int32_t ckv_dim, int32_t kr_dim,
+                      const int64_t *src_row, const int64_t *dst_row, const int32_t *len,
+                      const int64_t *delta, int64_t n_chunks, const double *inv_freq,
+                      int32_t layout, int32_t dtype, int32_t out_round, void *ws,
+                      int64_t ws_bytes, irm_stream_t stream);
+/* Per-row absolute rotation (producer side of the store, registry.py:131-133
+ * with rotary.py:98-108): out[i] = R(positions[i]) rows[i] for the dim-wide
+ * rotary rows at rows + i*row_stride (elements). out may alias rows. */
+int irm_rotate_rows(const void *rows, int64_t row_stride, void *out, int64_t out_stride,
+                    int64_t n, int32_t dim, const double *positions, const double *inv_freq,
+                    int32_t layout, int32_t dtype, int32_t out_round, irm_stream_t stream);
+/* Elementwise store rounding of f64 values: IRM_ROUND_F32 (f32 cast) or
+ * IRM_ROUND_BF16 (rotary.py:63-87 round_bf16, single RNE incl. subnormals). */
+int irm_round_f64(const double *x, double *y, int64_t n, int32_t mode, irm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,386 @@
+// K1 (CDC + xxh64) and K2 (batched xxh64 spans) for sm_100a.
+//
+// Replaces chunking.cdc_chunk (reference chunking.py:89-133) and
+// fingerprint.fingerprint (fingerprint.py:28-30) with one batched,
+// bit-exact device pass.
+//
+// The Gear recurrence h_t = rotl64(h_{t-1}, 1) + g_t (chunking.py:114) has no
+// window, so it is not a plain scan. Writing rotl(h) = 2h + msb(h) (mod 2^64)
+// gives the exact decomposition
+//     h_t = G_t + B_t  (mod 2^64),
+//     G_t = sum_{k<64} g_{t-k} << k          (windowed, warp-scannable)
+//     B_t = sum_{k<64} m_{t-1-k} << k,  m_t = msb(h_t)
+// so the only sequential dependency is ONE BIT per token. A warp handles 32
+// tokens per step: lane j knows B up to the 2^j-1 contribution of lanes < j,
+// so msb(h) is determined when msb(lo) == msb(lo + 2^j - 1); otherwise
+// (≈2^-32 per lane on random input) the lane is resolved exactly, in lane
+// order. Then B advances by (B << 32) | brev(ballot(m)).
+//
+// Marker pins reset h (chunking.py:116-118), so the stream splits into
+// independent regions; one warp scans one region, walks the boundary rule
+// with ballot/ffs over the candidate mask, then hashes its chunks (lane per
+// chunk, XXH64 from L2-resident tokens).
+#include "common.cuh"
+
+namespace irm {
+
+struct Region {
+    int64_t tok_begin;     // absolute index into tok[] of the region's first token
+    int64_t stream_begin;  // absolute index of the owning stream's first token
+    int64_t cap_off;       // staging slot of the region's first chunk
+    int32_t len;           // tokens (>= 1)
+    int32_t ends_pin;      // last token carries a marker pin
+};
+
+__global__ void gear_table_kernel(uint64_t seed, uint64_t *out) {
+    // splitmix64 (rng.py:17-24): state_i = seed + (i+1) * gamma, then mix.
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 65536) return;
+    uint64_t z = seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    out[i] = z ^ (z >> 31);
+}
+
+// Walk one stream's sorted pins: calls emit(start, last, ends_pin) per region.
+template <typename F>
+__device__ __forceinline__ int64_t for_each_region(int64_t n, const int64_t *pins, int64_t np,
+                                                   F emit) {
+    int64_t rs = 0, prev = -1, cnt = 0;
+    for (int64_t i = 0; i < np; ++i) {
+        int64_t p = pins[i];
+        if (p < 0 || p >= n || p == prev) continue;
+        prev = p;
+        emit(rs, p, 1, cnt);
+        ++cnt;
+        rs = p + 1;
+    }
+    if (rs < n) {
+        emit(rs, n - 1, 0, cnt);
+        ++cnt;
+    }
+    return cnt;
+}
+
+constexpr int PLAN_BLOCK = 1024;
+
+__global__ void __launch_bounds__(PLAN_BLOCK)
+cdc_plan_kernel(const int64_t *__restrict__ stream_off, int32_t n_streams,
+                const int64_t *__restrict__ pin_off, const int64_t *__restrict__ pins,
+                int32_t use_pins, int32_t min_size, Region *__restrict__ regions,
+                int64_t *__restrict__ r_first, int64_t *__restrict__ n_regions) {
+    __shared__ int64_t sm[PLAN_BLOCK / 32];
+    int64_t carry = 0;
+    for (int32_t s0 = 0; s0 < n_streams; s0 += PLAN_BLOCK) {
+        const int32_t s = s0 + threadIdx.x;
+        int64_t cnt = 0, n = 0, p0 = 0, np = 0, sb = 0;
+        if (s < n_streams) {
+            sb = stream_off[s];
+            n = stream_off[s + 1] - sb;
+            if (use_pins) {
+                p0 = pin_off[s];
+                np = pin_off[s + 1] - p0;
+            }
+            cnt = for_each_region(n, pins + p0, np, [](int64_t, int64_t, int, int64_t) {});
+        }
+        int64_t tot;
+        const int64_t ex = block_exclusive_scan<PLAN_BLOCK>(cnt, &tot, sm);
+        if (s < n_streams) {
+            const int64_t rbase = carry + ex;
+            r_first[s] = rbase;
+            for_each_region(n, pins + p0, np, [&](int64_t rs, int64_t last, int pin, int64_t i) {
+                Region R;
+                R.tok_begin = sb + rs;
+                R.stream_begin = sb;
+                R.len = (int32_t)(last - rs + 1);
+                R.ends_pin = pin;
+                R.cap_off = (sb + rs) / min_size + (rbase + i);
+                regions[rbase + i] = R;
+            });
+        }
+        carry += tot;
+    }
+    if (threadIdx.x == 0) {
+        r_first[n_streams] = carry;
+        *n_regions = carry;
+    }
+}
+
+constexpr int SCAN_WARPS = 4;
+
+__global__ void __launch_bounds__(SCAN_WARPS * 32)
+cdc_scan_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ regions,
+                const int64_t *__restrict__ n_regions_p, const uint64_t *__restrict__ gear,
+                int32_t k, int32_t min_size, int32_t max_size, int32_t *__restrict__ st_start,
+                int32_t *__restrict__ st_len, uint8_t *__restrict__ st_forced,
+                uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= *n_regions_p) return;
+    const Region R = regions[r];
+    const uint32_t *__restrict__ rt = tok + R.tok_begin;
+    const int32_t rel0 = (int32_t)(R.tok_begin - R.stream_begin);
+    const uint64_t mask = (1ULL << k) - 1;
+    const int32_t t_pin = R.ends_pin ? R.len - 1 : INT32_MAX;
+
+    uint64_t Gprev = 0, B = 0;
+    int32_t start = 0, nchunks = 0;
+    const int64_t cap = R.cap_off;
+
+    // software prefetch of the next step's gear entry (tokens -> table index)
+    uint64_t g_next = (lane < R.len) ? __ldg(gear + (__ldg(rt + lane) & 0xFFFFu)) : 0;
+    for (int32_t base = 0; base < R.len; base += 32) {
+        const int32_t t = base + lane;
+        const bool valid = t < R.len;
+        const uint64_t g = g_next;
+        {
+            const int32_t tn = t + 32;
+            g_next = (tn < R.len) ? __ldg(gear + (__ldg(rt + tn) & 0xFFFFu)) : 0;
+        }
+        // G_t: windowed shift-add scan (Kogge-Stone), carry-in from step before
+        uint64_t x = g;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y << d;
+        }
+        const uint64_t G = x + (Gprev << (lane + 1));
+        Gprev = __shfl_sync(0xffffffffu, G, 31);
+
+        // B_t: known part (B << j) plus the in-step part < 2^j
+        const uint64_t lo = G + (B << lane);
+        const uint64_t hi = lo + ((1ULL << lane) - 1);
+        unsigned M = __ballot_sync(0xffffffffu, (unsigned)(lo >> 63));
+        unsigned und = __ballot_sync(0xffffffffu, valid && ((lo ^ hi) >> 63));
+        while (und) {  // exact resolution of undetermined lanes, in lane order
+            const int jj = __ffs(und) - 1;
+            unsigned mb = 0;
+            if (lane == jj) {
+                const uint64_t u = jj ? (uint64_t)(__brev(M) >> (32 - jj)) : 0;
+                mb = (unsigned)((lo + u) >> 63);
+            }
+            mb = __shfl_sync(0xffffffffu, mb, jj);
+            M = (M & ~(1u << jj)) | (mb << jj);
+            und &= und - 1;
+        }
+        const uint64_t h = lo + (lane ? (uint64_t)(__brev(M) >> (32 - lane)) : 0);
+        B = (B << 32) | (uint64_t)__brev(M);
+        const unsigned cand = __ballot_sync(0xffffffffu, valid && (h & mask) == 0);
+
+        // boundary rule (chunking.py:116-124): marker > max_clamp > mask hit
+        const int32_t end = min(base + 32, R.len);
+        while (true) {
+            const int32_t t_max = start + max_size - 1;
+            const int32_t lo_c = max(base, start + min_size - 1);
+            int32_t t_cand = INT32_MAX;
+            if (lo_c < end) {
+                const unsigned m = cand & (0xffffffffu << (lo_c - base));
+                if (m) t_cand = base + __ffs(m) - 1;
+            }
+            const int32_t nxt = min(t_max, min(t_pin, t_cand));
+            if (nxt >= end) break;
+            if (lane == 0) {
+                st_start[cap + nchunks] = rel0 + start;
+                st_len[cap + nchunks] = nxt - start + 1;
+                st_forced[cap + nchunks] = nxt == t_pin   ? IRM_FORCED_MARKER
+                                           : nxt == t_max ? IRM_FORCED_MAX_CLAMP
+                                                          : IRM_FORCED_NONE;
+            }
+            ++nchunks;
+            start = nxt + 1;
+        }
+    }
+    if (start < R.len) {  // only when the region ends at the stream end
+        if (lane == 0) {
+            st_start[cap + nchunks] = rel0 + start;
+            st_len[cap + nchunks] = R.len - start;
+            st_forced[cap + nchunks] = IRM_FORCED_STREAM_END;
+        }
+        ++nchunks;
+    }
+    __syncwarp();
+    // fingerprints: one lane per chunk
+    const uint32_t *__restrict__ sbase = tok + R.stream_begin;
+    for (int32_t c = lane; c < nchunks; c += 32) {
+        const int32_t s = st_start[cap + c];
+        const int32_t l = st_len[cap + c];
+        st_fp[cap + c] = xxh64_words(sbase + s, l, 0);
+    }
+    if (lane == 0) r_count[r] = nchunks;
+}
+
+__global__ void __launch_bounds__(PLAN_BLOCK)
+cdc_offsets_kernel(const int64_t *__restrict__ n_regions_p, const int32_t *__restrict__ r_count,
+                   int64_t *__restrict__ r_out, const int64_t *__restrict__ r_first,
+                   int32_t n_streams, int64_t *__restrict__ chunk_off) {
+    __shared__ int64_t sm[PLAN_BLOCK / 32];
+    const int64_t nr = *n_regions_p;
+    int64_t carry = 0;
+    for (int64_t r0 = 0; r0 < nr; r0 += PLAN_BLOCK) {
+        const int64_t r = r0 + threadIdx.x;
+        const int64_t c = r < nr ? r_count[r] : 0;
+        int64_t tot;
+        const int64_t ex = block_exclusive_scan<PLAN_BLOCK>(c, &tot, sm);
+        if (r < nr) r_out[r] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) r_out[nr] = carry;
+    __syncthreads();
+    for (int32_t s = threadIdx.x; s <= n_streams; s += PLAN_BLOCK) chunk_off[s] = r_out[r_first[s]];
+}
+
+__global__ void __launch_bounds__(128)
+cdc_compact_kernel(const int64_t *__restrict__ n_regions_p, const Region *__restrict__ regions,
+                   const int32_t *__restrict__ r_count, const int64_t *__restrict__ r_out,
+                   const int32_t *__restrict__ st_start, const int32_t *__restrict__ st_len,
+                   const uint8_t *__restrict__ st_forced, const uint64_t *__restrict__ st_fp,
+                   int32_t *__restrict__ c_start, int32_t *__restrict__ c_len,
+                   uint64_t *__restrict__ c_fp, uint8_t *__restrict__ c_forced) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= *n_regions_p) return;
+    const int64_t src = regions[r].cap_off, dst = r_out[r];
+    const int32_t n = r_count[r];
+    for (int32_t i = lane; i < n; i += 32) {
+        c_start[dst + i] = st_start[src + i];
+        c_len[dst + i] = st_len[src + i];
+        c_fp[dst + i] = st_fp[src + i];
+        c_forced[dst + i] = st_forced[src + i];
+    }
+}
+
+__global__ void xxh64_spans_kernel(const uint8_t *__restrict__ base, const int64_t *__restrict__ off,
+                                   const int64_t *__restrict__ len, int64_t n, uint64_t seed,
+                                   uint64_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t o = off[i], l = len[i];
+    // token spans (4-byte aligned, whole words) take the word path
+    if (((o | l) & 3) == 0 && (((uintptr_t)base) & 3) == 0)
+        out[i] = xxh64_words(reinterpret_cast<const uint32_t *>(base + o), l / 4, seed);
+    else
+        out[i] = xxh64_bytes(base + o, l, seed);
+}
+
+// ------------------------------------------------------------- workspace
+struct CdcWs {
+    Region *regions;
+    int64_t *r_first, *n_regions, *r_out;
+    int32_t *r_count, *st_start, *st_len;
+    uint8_t *st_forced;
+    uint64_t *st_fp;
+    int64_t bytes;
+};
+
+static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+static CdcWs carve_cdc_ws(void *ws, int64_t n_tokens, int32_t n_streams, int64_t n_pins,
+                          int32_t min_size) {
+    const int64_t rmax = (int64_t)n_streams + n_pins + 1;
+    const int64_t smax = n_tokens / min_size + rmax + 1;
+    CdcWs w{};
+    char *p = (char *)ws;
+    int64_t o = 0;
+    auto take = [&](int64_t bytes) {
+        char *q = p ? p + o : nullptr;
+        o = align_up(o + bytes, 256);
+        return q;
+    };
+    w.regions = (Region *)take(rmax * sizeof(Region));
+    w.r_first = (int64_t *)take((n_streams + 1) * sizeof(int64_t));
+    w.n_regions = (int64_t *)take(sizeof(int64_t));
+    w.r_out = (int64_t *)take((rmax + 1) * sizeof(int64_t));
+    w.r_count = (int32_t *)take(rmax * sizeof(int32_t));
+    w.st_start = (int32_t *)take(smax * sizeof(int32_t));
+    w.st_len = (int32_t *)take(smax * sizeof(int32_t));
+    w.st_fp = (uint64_t *)take(smax * sizeof(uint64_t));
+    w.st_forced = (uint8_t *)take(smax);
+    w.bytes = o;
+    return w;
+}
+
+}  // namespace irm
+
+using namespace irm;
+
+extern "C" int irm_gear_table(uint64_t seed, uint64_t *out, irm_stream_t stream) {
+    IRM_REQUIRE(out != nullptr, "irm_gear_table: out is null");
+    gear_table_kernel<<<65536 / 256, 256, 0, (cudaStream_t)stream>>>(seed, out);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+extern "C" int64_t irm_cdc_chunk_bound(int64_t n_tokens, int32_t n_streams, int64_t n_pins,
+                                       int32_t min_size) {
+    if (min_size < 1) return -1;
+    return n_tokens / min_size + (int64_t)n_streams + n_pins + 1;
+}
+
+extern "C" int64_t irm_cdc_workspace_bytes(int64_t n_tokens, int32_t n_streams, int64_t n_pins,
+                                           int32_t min_size) {
+    if (min_size < 1 || n_streams < 0 || n_tokens < 0 || n_pins < 0) return -1;
+    return carve_cdc_ws(nullptr, n_tokens, n_streams, n_pins, min_size).bytes;
+}
+
+extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_off,
+                             int32_t n_streams, const int64_t *pin_off, const int64_t *pins,
+                             int64_t n_pins, int32_t mask_exponent, int32_t min_size,
+                             int32_t max_size, int32_t marker_pinned, const uint64_t *gear,
+                             int32_t *c_start, int32_t *c_len, uint64_t *c_fp, uint8_t *c_forced,
+                             int64_t *chunk_off, int64_t cap, void *ws, int64_t ws_bytes,
+                             irm_stream_t stream) {
+    // ChunkerParams validation, chunking.py:45-49
+    IRM_REQUIRE(mask_exponent >= 1 && mask_exponent <= 20, "mask_exponent must be in [1, 20]");
+    IRM_REQUIRE(min_size >= 1 && min_size < max_size, "need 1 <= min_size < max_size");
+    IRM_REQUIRE(n_streams >= 0 && n_tokens >= 0 && n_pins >= 0, "negative sizes");
+    IRM_REQUIRE(n_tokens < (int64_t)1 << 40, "n_tokens too large");
+    IRM_REQUIRE(stream_off && chunk_off, "null stream_off/chunk_off");
+    IRM_REQUIRE(n_tokens == 0 || (tok && gear), "null tok/gear");
+    if (marker_pinned && n_pins > 0) IRM_REQUIRE(pin_off && pins, "null pins");
+    const int64_t bound = irm_cdc_chunk_bound(n_tokens, n_streams, marker_pinned ? n_pins : 0,
+                                              min_size);
+    if (cap < bound) {
+        set_error("chunk capacity %lld < bound %lld", (long long)cap, (long long)bound);
+        return IRM_ECAPACITY;
+    }
+    const int64_t np = marker_pinned ? n_pins : 0;
+    CdcWs w = carve_cdc_ws(ws, n_tokens, n_streams, np, min_size);
+    if (ws_bytes < w.bytes || ws == nullptr) {
+        set_error("workspace %lld < %lld bytes", (long long)ws_bytes, (long long)w.bytes);
+        return IRM_ECAPACITY;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_streams == 0) {
+        IRM_CUDA_CHECK(cudaMemsetAsync(chunk_off, 0, sizeof(int64_t), st));
+        return IRM_OK;
+    }
+    const int32_t use_pins = marker_pinned && n_pins > 0;
+    cdc_plan_kernel<<<1, PLAN_BLOCK, 0, st>>>(stream_off, n_streams, pin_off, pins, use_pins,
+                                              min_size, w.regions, w.r_first, w.n_regions);
+    IRM_LAUNCH_CHECK();
+    const int64_t rmax = (int64_t)n_streams + np;
+    const int64_t warps_blocks = (rmax + SCAN_WARPS - 1) / SCAN_WARPS;
+    cdc_scan_kernel<<<(unsigned)warps_blocks, SCAN_WARPS * 32, 0, st>>>(
+        tok, w.regions, w.n_regions, gear, mask_exponent, min_size, max_size, w.st_start, w.st_len,
+        w.st_forced, w.st_fp, w.r_count);
+    IRM_LAUNCH_CHECK();
+    cdc_offsets_kernel<<<1, PLAN_BLOCK, 0, st>>>(w.n_regions, w.r_count, w.r_out, w.r_first,
+                                                 n_streams, chunk_off);
+    IRM_LAUNCH_CHECK();
+    cdc_compact_kernel<<<(unsigned)((rmax + 3) / 4), 128, 0, st>>>(
+        w.n_regions, w.regions, w.r_count, w.r_out, w.st_start, w.st_len, w.st_forced, w.st_fp,
+        c_start, c_len, c_fp, c_forced);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+extern "C" int irm_xxh64_spans(const uint8_t *base, const int64_t *off, const int64_t *len,
+                               int64_t n, uint64_t seed, uint64_t *out, irm_stream_t stream) {
+    IRM_REQUIRE(n >= 0, "n must be >= 0");
+    if (n == 0) return IRM_OK;
+    IRM_REQUIRE(off && len && out, "null pointer");
+    xxh64_spans_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        base, off, len, n, seed, out);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}

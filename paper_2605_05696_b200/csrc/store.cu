@@ -1,0 +1,299 @@
+// K3: the content-hash chunk store on the device.
+//
+// Replaces KvRegistry.lookup / insert (reference registry.py:113-140) and the
+// per-chunk probe/insert of engine.serve (engine.py:197-223) with a batched,
+// order-exact operation: the reference serves chunks one at a time with
+// first-writer-wins, which equals "per fingerprint, the query with the
+// smallest (request, chunk) order key writes; everyone else hits it".
+//
+// Table: open addressing, linear probing, keys claimed with atomicCAS, the
+// batch winner elected with atomicMin on the order key. Entry indices and
+// pool rows of new entries are assigned by an exclusive scan in query order,
+// so insert_epoch (registry.py:83,137) and pool layout are deterministic.
+#include "common.cuh"
+
+namespace irm {
+
+constexpr int ST_BLOCK = 512;
+enum : int8_t { Q_NOVEL = 0, Q_HIT_OLD = 1, Q_HIT_BATCH = 2, Q_SKIP = 3 };
+enum : int64_t { ERR_TABLE_FULL = 1, ERR_ENTRIES_FULL = 2 };
+
+__device__ __forceinline__ uint64_t slot_hash(uint64_t fp) {
+    // fingerprints are already xxh64 outputs; fold the high bits in anyway
+    return (fp ^ (fp >> 31)) * 0x9E3779B97F4A7C15ULL;
+}
+
+// Find or claim the slot of fp. Returns n_slots for the EMPTY-key side slot,
+// -1 when the table is full.
+__device__ __forceinline__ int64_t find_slot(const irm_store_view &st, uint64_t fp, bool claim) {
+    if (fp == IRM_EMPTY_KEY) return st.n_slots;
+    const uint64_t m = (uint64_t)st.n_slots - 1;
+    uint64_t idx = (slot_hash(fp) >> 17) & m;
+    for (int64_t probe = 0; probe < st.n_slots; ++probe, idx = (idx + 1) & m) {
+        uint64_t k = ((volatile uint64_t *)st.slot_key)[idx];
+        if (k == fp) return (int64_t)idx;
+        if (k == IRM_EMPTY_KEY) {
+            if (!claim) return -1;
+            k = atomicCAS((unsigned long long *)&st.slot_key[idx], (unsigned long long)IRM_EMPTY_KEY,
+                          (unsigned long long)fp);
+            if (k == IRM_EMPTY_KEY || k == fp) return (int64_t)idx;
+        }
+    }
+    return -1;
+}
+
+__global__ void store_reset_kernel(irm_store_view st) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < st.n_slots) st.slot_key[i] = IRM_EMPTY_KEY;
+    if (i <= st.n_slots) {
+        st.slot_order[i] = INT64_MAX;
+        st.slot_entry[i] = -1;
+    }
+    if (i < 4) st.counters[i] = 0;
+}
+
+__global__ void store_claim_kernel(irm_store_view st, const uint64_t *__restrict__ q_fp,
+                                   const int64_t *__restrict__ q_order,
+                                   const uint8_t *__restrict__ q_probe, int64_t n,
+                                   int64_t *__restrict__ q_slot) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (q_probe && !q_probe[i]) {
+        q_slot[i] = -2;
+        return;
+    }
+    const int64_t s = find_slot(st, q_fp[i], true);
+    q_slot[i] = s;
+    if (s < 0) {
+        atomicOr((unsigned long long *)&st.counters[2], (unsigned long long)ERR_TABLE_FULL);
+        return;
+    }
+    if (st.slot_entry[s] < 0) atomicMin((long long *)&st.slot_order[s], (long long)q_order[i]);
+}
+
+// state per query + per-block totals of (new entries, new rows)
+__global__ void __launch_bounds__(ST_BLOCK)
+store_decide_kernel(irm_store_view st, const int64_t *__restrict__ q_order,
+                    const int32_t *__restrict__ q_len, int64_t n,
+                    const int64_t *__restrict__ q_slot, int8_t *__restrict__ q_state,
+                    int64_t *__restrict__ blk_cnt, int64_t *__restrict__ blk_rows) {
+    __shared__ int64_t sm[ST_BLOCK / 32];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int8_t state = Q_SKIP;
+    if (i < n) {
+        const int64_t s = q_slot[i];
+        if (s >= 0) {
+            if (st.slot_entry[s] >= 0) state = Q_HIT_OLD;
+            else if (st.slot_order[s] == q_order[i]) state = Q_NOVEL;
+            else state = Q_HIT_BATCH;
+        }
+        q_state[i] = state;
+    }
+    int64_t tot_c, tot_r;
+    block_exclusive_scan<ST_BLOCK>(state == Q_NOVEL ? 1 : 0, &tot_c, sm);
+    block_exclusive_scan<ST_BLOCK>(state == Q_NOVEL ? (int64_t)q_len[i] : 0, &tot_r, sm);
+    if (threadIdx.x == 0) {
+        blk_cnt[blockIdx.x] = tot_c;
+        blk_rows[blockIdx.x] = tot_r;
+    }
+}
+
+// exclusive scan of the block totals (single block, tiles of ST_BLOCK)
+__global__ void __launch_bounds__(ST_BLOCK)
+store_blockscan_kernel(int64_t nb, int64_t *__restrict__ blk_cnt, int64_t *__restrict__ blk_rows,
+                       int64_t *__restrict__ totals) {
+    __shared__ int64_t sm[ST_BLOCK / 32];
+    int64_t cc = 0, cr = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += ST_BLOCK) {
+        const int64_t b = b0 + threadIdx.x;
+        const int64_t vc = b < nb ? blk_cnt[b] : 0, vr = b < nb ? blk_rows[b] : 0;
+        int64_t tc, tr;
+        const int64_t ec = block_exclusive_scan<ST_BLOCK>(vc, &tc, sm);
+        const int64_t er = block_exclusive_scan<ST_BLOCK>(vr, &tr, sm);
+        if (b < nb) {
+            blk_cnt[b] = cc + ec;
+            blk_rows[b] = cr + er;
+        }
+        cc += tc;
+        cr += tr;
+    }
+    if (threadIdx.x == 0) {
+        totals[0] = cc;
+        totals[1] = cr;
+    }
+}
+
+__global__ void __launch_bounds__(ST_BLOCK)
+store_commit_kernel(irm_store_view st, const uint64_t *__restrict__ q_fp,
+                    const int64_t *__restrict__ q_p, const int32_t *__restrict__ q_len, int64_t n,
+                    const int64_t *__restrict__ q_slot, const int8_t *__restrict__ q_state,
+                    const int64_t *__restrict__ blk_cnt, const int64_t *__restrict__ blk_rows,
+                    const int64_t *__restrict__ totals, int32_t *__restrict__ q_hit,
+                    int64_t *__restrict__ q_entry, int64_t *__restrict__ q_p_src,
+                    int64_t *__restrict__ q_row) {
+    __shared__ int64_t sm[ST_BLOCK / 32];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int8_t state = i < n ? q_state[i] : Q_SKIP;
+    int64_t tc, tr;
+    const int64_t ec = block_exclusive_scan<ST_BLOCK>(state == Q_NOVEL ? 1 : 0, &tc, sm);
+    const int64_t er = block_exclusive_scan<ST_BLOCK>(state == Q_NOVEL ? (int64_t)q_len[i] : 0, &tr, sm);
+    // counters are bumped only by the resolve kernel, after every commit block
+    const int64_t n_before = st.counters[0], rows_before = st.counters[1];
+    if (i >= n) return;
+    if (state == Q_NOVEL) {
+        const int64_t e = n_before + blk_cnt[blockIdx.x] + ec;
+        const int64_t row = rows_before + blk_rows[blockIdx.x] + er;
+        const int64_t s = q_slot[i];
+        if (e < st.max_entries) {
+            st.e_fp[e] = q_fp[i];
+            st.e_p_src[e] = q_p[i];
+            st.e_len[e] = q_len[i];
+            st.e_row[e] = row;
+            st.slot_entry[s] = e;
+        } else {
+            atomicOr((unsigned long long *)&st.counters[2], (unsigned long long)ERR_ENTRIES_FULL);
+        }
+        st.slot_order[s] = INT64_MAX;
+        q_hit[i] = 0;
+        q_entry[i] = e;
+        q_p_src[i] = q_p[i];
+        q_row[i] = row;
+    } else if (state == Q_SKIP) {
+        q_hit[i] = -1;
+        q_entry[i] = -1;
+        q_p_src[i] = 0;
+        q_row[i] = -1;
+    }
+}
+
+// hits: resolve after all new entries are published; also bump the counters
+__global__ void store_resolve_kernel(irm_store_view st, int64_t n,
+                                     const int64_t *__restrict__ q_slot,
+                                     const int8_t *__restrict__ q_state,
+                                     const int64_t *__restrict__ totals, int32_t *__restrict__ q_hit,
+                                     int64_t *__restrict__ q_entry, int64_t *__restrict__ q_p_src,
+                                     int64_t *__restrict__ q_row) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        const int64_t ne = st.counters[0] + totals[0];
+        st.counters[0] = ne < st.max_entries ? ne : st.max_entries;
+        st.counters[1] += totals[1];
+    }
+    if (i >= n) return;
+    const int8_t state = q_state[i];
+    if (state != Q_HIT_OLD && state != Q_HIT_BATCH) return;
+    const int64_t e = st.slot_entry[q_slot[i]];
+    q_hit[i] = 1;
+    q_entry[i] = e;
+    q_p_src[i] = e >= 0 ? st.e_p_src[e] : 0;
+    q_row[i] = e >= 0 ? st.e_row[e] : -1;
+}
+
+__global__ void store_lookup_kernel(irm_store_view st, const uint64_t *__restrict__ q_fp, int64_t n,
+                                    int64_t *__restrict__ q_entry) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t s = find_slot(st, q_fp[i], false);
+    q_entry[i] = s >= 0 ? st.slot_entry[s] : -1;
+}
+
+struct StoreWs {
+    int64_t *q_slot, *blk_cnt, *blk_rows, *totals;
+    int8_t *q_state;
+    int64_t bytes;
+};
+
+static StoreWs carve_store_ws(void *ws, int64_t n) {
+    const int64_t nb = (n + ST_BLOCK - 1) / ST_BLOCK + 1;
+    StoreWs w{};
+    char *p = (char *)ws;
+    int64_t o = 0;
+    auto take = [&](int64_t bytes) {
+        char *q = p ? p + o : nullptr;
+        o = (o + bytes + 255) / 256 * 256;
+        return q;
+    };
+    w.q_slot = (int64_t *)take(n * sizeof(int64_t));
+    w.blk_cnt = (int64_t *)take(nb * sizeof(int64_t));
+    w.blk_rows = (int64_t *)take(nb * sizeof(int64_t));
+    w.totals = (int64_t *)take(2 * sizeof(int64_t));
+    w.q_state = (int8_t *)take(n);
+    w.bytes = o;
+    return w;
+}
+
+static int check_view(const irm_store_view *st) {
+    IRM_REQUIRE(st != nullptr, "null store view");
+    IRM_REQUIRE(st->n_slots >= 2 && (st->n_slots & (st->n_slots - 1)) == 0,
+                "n_slots must be a power of two >= 2");
+    IRM_REQUIRE(st->slot_key && st->slot_order && st->slot_entry && st->counters,
+                "null store arrays");
+    IRM_REQUIRE(st->e_fp && st->e_p_src && st->e_len && st->e_row && st->max_entries > 0,
+                "null entry arrays");
+    return IRM_OK;
+}
+
+}  // namespace irm
+
+using namespace irm;
+
+extern "C" int irm_store_reset(const irm_store_view *st, irm_stream_t stream) {
+    if (int rc = check_view(st)) return rc;
+    const int64_t n = st->n_slots + 1;
+    store_reset_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*st);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+extern "C" int64_t irm_store_workspace_bytes(int64_t n) {
+    if (n < 0) return -1;
+    return carve_store_ws(nullptr, n).bytes;
+}
+
+extern "C" int irm_store_lookup_insert(const irm_store_view *st, const uint64_t *q_fp,
+                                       const int64_t *q_order, const int64_t *q_p,
+                                       const int32_t *q_len, const uint8_t *q_probe, int64_t n,
+                                       int32_t *q_hit, int64_t *q_entry, int64_t *q_p_src,
+                                       int64_t *q_row, void *ws, int64_t ws_bytes,
+                                       irm_stream_t stream) {
+    if (int rc = check_view(st)) return rc;
+    IRM_REQUIRE(n >= 0, "n must be >= 0");
+    if (n == 0) return IRM_OK;
+    IRM_REQUIRE(q_fp && q_order && q_p && q_len && q_hit && q_entry && q_p_src && q_row,
+                "null query arrays");
+    StoreWs w = carve_store_ws(ws, n);
+    if (!ws || ws_bytes < w.bytes) {
+        set_error("store workspace %lld < %lld", (long long)ws_bytes, (long long)w.bytes);
+        return IRM_ECAPACITY;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned nb = (unsigned)((n + ST_BLOCK - 1) / ST_BLOCK);
+    store_claim_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(*st, q_fp, q_order, q_probe, n,
+                                                                   w.q_slot);
+    IRM_LAUNCH_CHECK();
+    store_decide_kernel<<<nb, ST_BLOCK, 0, s>>>(*st, q_order, q_len, n, w.q_slot, w.q_state,
+                                                w.blk_cnt, w.blk_rows);
+    IRM_LAUNCH_CHECK();
+    store_blockscan_kernel<<<1, ST_BLOCK, 0, s>>>(nb, w.blk_cnt, w.blk_rows, w.totals);
+    IRM_LAUNCH_CHECK();
+    store_commit_kernel<<<nb, ST_BLOCK, 0, s>>>(*st, q_fp, q_p, q_len, n, w.q_slot, w.q_state,
+                                                w.blk_cnt, w.blk_rows, w.totals, q_hit, q_entry,
+                                                q_p_src, q_row);
+    IRM_LAUNCH_CHECK();
+    store_resolve_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+        *st, n, w.q_slot, w.q_state, w.totals, q_hit, q_entry, q_p_src, q_row);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+extern "C" int irm_store_lookup(const irm_store_view *st, const uint64_t *q_fp, int64_t n,
+                                int64_t *q_entry, irm_stream_t stream) {
+    if (int rc = check_view(st)) return rc;
+    IRM_REQUIRE(n >= 0, "n must be >= 0");
+    if (n == 0) return IRM_OK;
+    IRM_REQUIRE(q_fp && q_entry, "null query arrays");
+    store_lookup_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*st, q_fp, n,
+                                                                                      q_entry);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}

@@ -1,0 +1,262 @@
+"""Tensor-level operators over the C ABI (device-resident, batched).
+
+These are the B200 forms of the reference's per-call functions; the drop-in
+modules (chunking, fingerprint, rotary, registry, engine) are thin host
+adapters over them. All tensors live on the current CUDA device; 64-bit
+unsigned values (fingerprints, gear entries) are carried in int64 tensors
+holding the same bit patterns, u32 tokens in int32 tensors.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+DEFAULT_GEAR_SEED = 0x49524D494E53554C
+
+
+def _dev():
+    N.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def u64_to_i64(v: int) -> int:
+    v &= (1 << 64) - 1
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
+def tokens_to_device(tokens) -> torch.Tensor:
+    """u32 token ids -> int32 device tensor carrying the same bits."""
+    if isinstance(tokens, torch.Tensor):
+        t = tokens
+        if t.dtype == torch.int64:
+            t = (t & 0xFFFFFFFF).to(torch.int64)
+            t = torch.where(t >= 2**31, t - 2**32, t).to(torch.int32)
+        return t.to(device=_dev(), dtype=torch.int32).contiguous()
+    a = np.asarray(tokens, dtype=np.uint64)
+    if a.size and int(a.max()) > 0xFFFFFFFF:
+        raise ValueError("token ids must be unsigned 32-bit")
+    a = a.astype(np.uint32).view(np.int32)
+    return torch.from_numpy(np.ascontiguousarray(a)).to(_dev())
+
+
+# ------------------------------------------------------------------ gear table
+_GEAR_DEV: dict[tuple[int, int], torch.Tensor] = {}
+
+
+def gear_table_device(seed: int = DEFAULT_GEAR_SEED) -> torch.Tensor:
+    """65,536-entry splitmix64 table generated on the device (chunking.py:64-76)."""
+    dev = _dev()
+    key = (seed & (2**64 - 1), dev.index)
+    t = _GEAR_DEV.get(key)
+    if t is None:
+        t = torch.empty(65536, dtype=torch.int64, device=dev)
+        N.check(N.lib().irm_gear_table(seed & (2**64 - 1), N.ptr(t), N.stream_ptr()), "irm_gear_table")
+        _GEAR_DEV[key] = t
+    return t
+
+
+# ------------------------------------------------------------------ K1: CDC + xxh64
+@dataclass
+class ChunkTable:
+    """Device chunk table: CSR over streams (chunk_off[n_streams+1])."""
+
+    start: torch.Tensor    # int32, stream-relative
+    length: torch.Tensor   # int32
+    fp: torch.Tensor       # int64 (u64 bits)
+    forced: torch.Tensor   # uint8
+    chunk_off: torch.Tensor  # int64 [n_streams+1]
+    n_chunks: int | None = None
+
+    def to_host(self):
+        off = self.chunk_off.cpu().numpy()
+        n = int(off[-1])
+        return (self.start[:n].cpu().numpy(), self.length[:n].cpu().numpy(),
+                self.fp[:n].cpu().numpy().view(np.uint64), self.forced[:n].cpu().numpy(), off)
+
+
+class CdcWorkspace:
+    """Reusable device buffers for irm_cdc_xxh64 (grown on demand)."""
+
+    def __init__(self):
+        self.ws = None
+        self.cap = 0
+        self.bufs = None
+
+    def get(self, n_tokens, n_streams, n_pins, min_size):
+        L = N.lib()
+        wb = int(L.irm_cdc_workspace_bytes(n_tokens, n_streams, n_pins, min_size))
+        cap = int(L.irm_cdc_chunk_bound(n_tokens, n_streams, n_pins, min_size))
+        dev = _dev()
+        if self.ws is None or self.ws.numel() < wb:
+            self.ws = torch.empty(max(wb, 256), dtype=torch.uint8, device=dev)
+        if self.bufs is None or self.cap < cap:
+            self.cap = max(cap, 16)
+            self.bufs = (torch.empty(self.cap, dtype=torch.int32, device=dev),
+                         torch.empty(self.cap, dtype=torch.int32, device=dev),
+                         torch.empty(self.cap, dtype=torch.int64, device=dev),
+                         torch.empty(self.cap, dtype=torch.uint8, device=dev))
+        return self.ws, self.bufs, self.cap
+
+
+_DEFAULT_CDC_WS = CdcWorkspace()
+
+
+def cdc_xxh64(tok: torch.Tensor, stream_off: torch.Tensor, pin_off: torch.Tensor | None,
+              pins: torch.Tensor | None, mask_exponent: int = 7, min_size: int = 32,
+              max_size: int = 512, marker_pinned: bool = True,
+              gear_seed: int = DEFAULT_GEAR_SEED, ws: CdcWorkspace | None = None,
+              n_tokens: int | None = None, n_pins: int | None = None) -> ChunkTable:
+    """Batched CDC + fingerprints over CSR token streams (K1).
+
+    ``tok`` int32 [n_tokens]; ``stream_off`` int64 [n_streams+1]; ``pins``
+    int64 sorted per stream (CSR ``pin_off``). Outputs stay on the device.
+    """
+    ws = ws or _DEFAULT_CDC_WS
+    n_streams = stream_off.numel() - 1
+    n_tokens = tok.numel() if n_tokens is None else n_tokens
+    if pins is None or pin_off is None:
+        pins = torch.zeros(1, dtype=torch.int64, device=tok.device)
+        pin_off = torch.zeros(n_streams + 1, dtype=torch.int64, device=tok.device)
+        n_pins = 0
+    n_pins = pins.numel() if n_pins is None else n_pins
+    wsbuf, (st, ln, fp, fo), cap = ws.get(n_tokens, n_streams, n_pins if marker_pinned else 0,
+                                          max(min_size, 1))
+    chunk_off = torch.empty(n_streams + 1, dtype=torch.int64, device=tok.device)
+    rc = N.lib().irm_cdc_xxh64(
+        N.ptr(tok), n_tokens, N.ptr(stream_off), n_streams, N.ptr(pin_off), N.ptr(pins), n_pins,
+        mask_exponent, min_size, max_size, int(bool(marker_pinned)), N.ptr(gear_table_device(gear_seed)),
+        N.ptr(st), N.ptr(ln), N.ptr(fp), N.ptr(fo), N.ptr(chunk_off), cap, N.ptr(wsbuf),
+        wsbuf.numel(), N.stream_ptr())
+    N.check(rc, "irm_cdc_xxh64")
+    return ChunkTable(st, ln, fp, fo, chunk_off)
+
+
+# ------------------------------------------------------------------ K2: xxh64 spans
+def xxh64_spans(base: torch.Tensor, off: torch.Tensor, length: torch.Tensor, seed: int = 0) -> torch.Tensor:
+    """XXH64 of byte spans of a device buffer (offsets/lengths in bytes)."""
+    n = off.numel()
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=base.device)
+    if n:
+        N.check(N.lib().irm_xxh64_spans(N.ptr(base), N.ptr(off), N.ptr(length), n, seed & (2**64 - 1),
+                                        N.ptr(out), N.stream_ptr()), "irm_xxh64_spans")
+    return out[:n]
+
+
+# ------------------------------------------------------------------ K4: rotation
+_DTYPE_CODE = {torch.float64: N.DTYPE_F64, torch.float32: N.DTYPE_F32, torch.bfloat16: N.DTYPE_BF16}
+
+
+def inv_freq_device(inv_freq) -> torch.Tensor:
+    return torch.as_tensor(np.asarray(inv_freq, dtype=np.float64)).to(_dev())
+
+
+def rotate_gather(pool: torch.Tensor, out: torch.Tensor, src_row: torch.Tensor, dst_row: torch.Tensor,
+                  length: torch.Tensor, delta: torch.Tensor, inv_freq: torch.Tensor,
+                  ckv_dim: int = 512, kr_dim: int = 64, layout: int = N.LAYOUT_HALF_SPLIT,
+                  out_round: int = N.ROUND_NONE, ws: torch.Tensor | None = None) -> None:
+    """K4. pool [layers, pool_rows, ckv+kr], out [layers, out_rows, ckv+kr] (same dtype)."""
+    assert pool.dtype == out.dtype and pool.is_contiguous() and out.is_contiguous()
+    assert pool.dim() == 3 and out.dim() == 3 and pool.shape[0] == out.shape[0]
+    assert pool.shape[2] == ckv_dim + kr_dim == out.shape[2]
+    n = src_row.numel()
+    need = int(N.lib().irm_rotate_gather_workspace_bytes(n, kr_dim))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 256), dtype=torch.uint8, device=pool.device)
+    rc = N.lib().irm_rotate_gather(
+        N.ptr(pool), pool.shape[1], N.ptr(out), out.shape[1], pool.shape[0], ckv_dim, kr_dim,
+        N.ptr(src_row), N.ptr(dst_row), N.ptr(length), N.ptr(delta), n, N.ptr(inv_freq), layout,
+        _DTYPE_CODE[pool.dtype], out_round, N.ptr(ws), ws.numel(), N.stream_ptr())
+    N.check(rc, "irm_rotate_gather")
+
+
+def rotate_rows(rows: torch.Tensor, positions: torch.Tensor, inv_freq: torch.Tensor,
+                layout: int = N.LAYOUT_HALF_SPLIT, out_round: int = N.ROUND_NONE,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """Per-row absolute rotation (rows [n, dim] with arbitrary row stride)."""
+    assert rows.dim() == 2 and rows.stride(1) == 1
+    if out is None:
+        out = torch.empty(rows.shape, dtype=rows.dtype, device=rows.device)
+    pos = positions.to(device=rows.device, dtype=torch.float64).contiguous()
+    rc = N.lib().irm_rotate_rows(N.ptr(rows), rows.stride(0), N.ptr(out), out.stride(0), rows.shape[0],
+                                 rows.shape[1], N.ptr(pos), N.ptr(inv_freq), layout,
+                                 _DTYPE_CODE[rows.dtype], out_round, N.stream_ptr())
+    N.check(rc, "irm_rotate_rows")
+    return out
+
+
+def round_f64(x: torch.Tensor, mode: int) -> torch.Tensor:
+    x = x.contiguous()
+    y = torch.empty_like(x)
+    N.check(N.lib().irm_round_f64(N.ptr(x), N.ptr(y), x.numel(), mode, N.stream_ptr()), "irm_round_f64")
+    return y
+
+
+# ------------------------------------------------------------------ K3: chunk store
+class ChunkStore:
+    """Device content-hash store: fingerprint -> (p_src, len, pool row).
+
+    Host state is only the ctypes view; tables and entries are torch tensors.
+    """
+
+    def __init__(self, max_entries: int = 1 << 16, load_factor: float = 0.5):
+        dev = _dev()
+        n_slots = 1
+        while n_slots < max(2, int(max_entries / load_factor)):
+            n_slots <<= 1
+        self.n_slots, self.max_entries = n_slots, max_entries
+        self.slot_key = torch.empty(n_slots, dtype=torch.int64, device=dev)
+        self.slot_order = torch.empty(n_slots + 1, dtype=torch.int64, device=dev)
+        self.slot_entry = torch.empty(n_slots + 1, dtype=torch.int64, device=dev)
+        self.e_fp = torch.empty(max_entries, dtype=torch.int64, device=dev)
+        self.e_p_src = torch.empty(max_entries, dtype=torch.int64, device=dev)
+        self.e_len = torch.empty(max_entries, dtype=torch.int32, device=dev)
+        self.e_row = torch.empty(max_entries, dtype=torch.int64, device=dev)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.view = N.StoreView(
+            N.ptr(self.slot_key), N.ptr(self.slot_order), N.ptr(self.slot_entry), n_slots,
+            N.ptr(self.e_fp), N.ptr(self.e_p_src), N.ptr(self.e_len), N.ptr(self.e_row),
+            max_entries, N.ptr(self.counters))
+        self._ws = None
+        self.reset()
+
+    def reset(self):
+        N.check(N.lib().irm_store_reset(self.view, N.stream_ptr()), "irm_store_reset")
+
+    def _workspace(self, n):
+        need = int(N.lib().irm_store_workspace_bytes(n))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.slot_key.device)
+        return self._ws
+
+    def lookup_insert(self, q_fp: torch.Tensor, q_order: torch.Tensor, q_p: torch.Tensor,
+                      q_len: torch.Tensor, q_probe: torch.Tensor | None = None):
+        n = q_fp.numel()
+        dev = q_fp.device
+        hit = torch.empty(n, dtype=torch.int32, device=dev)
+        entry = torch.empty(n, dtype=torch.int64, device=dev)
+        p_src = torch.empty(n, dtype=torch.int64, device=dev)
+        row = torch.empty(n, dtype=torch.int64, device=dev)
+        ws = self._workspace(n)
+        rc = N.lib().irm_store_lookup_insert(
+            self.view, N.ptr(q_fp), N.ptr(q_order), N.ptr(q_p), N.ptr(q_len), N.ptr(q_probe), n,
+            N.ptr(hit), N.ptr(entry), N.ptr(p_src), N.ptr(row), N.ptr(ws), ws.numel(), N.stream_ptr())
+        N.check(rc, "irm_store_lookup_insert")
+        return hit, entry, p_src, row
+
+    def lookup(self, q_fp: torch.Tensor) -> torch.Tensor:
+        n = q_fp.numel()
+        entry = torch.empty(max(n, 1), dtype=torch.int64, device=q_fp.device)
+        N.check(N.lib().irm_store_lookup(self.view, N.ptr(q_fp), n, N.ptr(entry), N.stream_ptr()),
+                "irm_store_lookup")
+        return entry[:n]
+
+    def counts(self) -> tuple[int, int, int]:
+        c = self.counters.cpu().tolist()
+        if c[2]:
+            raise RuntimeError(f"chunk store overflow (flags {c[2]}): raise max_entries")
+        return c[0], c[1], c[2]

@@ -1,0 +1,234 @@
+"""Drop-in for ``irminsul.registry`` (reference registry.py) on the B200 path.
+
+The registry is a device-resident content-hash store (K3, ``ops.ChunkStore``)
+over a device latent pool [layers, rows, ckv_dim + kr_dim]:
+  * ``insert`` appends the chunk's rows to the pool and stores k_r already
+    rotated to p_src + i (the producer rotation, ``irm_rotate_rows``);
+  * ``lookup`` probes the device table;
+  * ``materialize`` runs the rotate+gather kernel (K4, ``irm_rotate_gather``)
+    with delta = p_dest - p_src and the precision tag's store rounding.
+Entries keep host mirrors of (c_kv, kr_base) so the reference's object
+contract holds: ``materialize(...).c_kv is entry.c_kv`` (registry_test:124).
+
+The synthetic KV oracle (``synth_kv``) stands in for model prefill exactly as
+in the reference (registry.py:37-70); it is the input generator, not the path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import ops
+from .rng import derive_seed
+from .rotary import Precision, RotarySpec, _ROUND, inv_freq_device
+
+_CKV_LABEL = 0x434B56
+_KR_LABEL = 0x4B52
+
+
+@dataclass(frozen=True)
+class SyntheticKvParams:
+    seed: int = 0
+    ckv_dim: int = 512
+    kr_dim: int = 64
+
+    def __post_init__(self):
+        if self.ckv_dim <= 0 or self.kr_dim <= 0:
+            raise ValueError("dims must be positive")
+        if self.kr_dim % 2 != 0:
+            raise ValueError("kr_dim must be even")
+
+
+def synth_kv(token: int, index_in_chunk: int, params: SyntheticKvParams) -> tuple[np.ndarray, np.ndarray]:
+    """Deterministic unit-norm (c_kv row, kr_raw row) for a token id (registry.py:37-54)."""
+    ckv_rng = np.random.Generator(np.random.PCG64(derive_seed(params.seed, _CKV_LABEL, token)))
+    kr_rng = np.random.Generator(np.random.PCG64(derive_seed(params.seed, _KR_LABEL, token)))
+    c_kv = ckv_rng.standard_normal(params.ckv_dim)
+    kr_raw = kr_rng.standard_normal(params.kr_dim)
+    return c_kv / np.linalg.norm(c_kv), kr_raw / np.linalg.norm(kr_raw)
+
+
+class _SynthCache:
+    def __init__(self, params: SyntheticKvParams):
+        self.params = params
+        self._rows: dict[int, tuple[np.ndarray, np.ndarray]] = {}
+
+    def rows(self, tokens: Sequence[int]) -> tuple[np.ndarray, np.ndarray]:
+        for t in tokens:
+            if t not in self._rows:
+                self._rows[t] = synth_kv(t, 0, self.params)
+        if len(tokens) == 0:
+            return np.zeros((0, self.params.ckv_dim)), np.zeros((0, self.params.kr_dim))
+        return (np.stack([self._rows[t][0] for t in tokens]),
+                np.stack([self._rows[t][1] for t in tokens]))
+
+
+@dataclass(frozen=True)
+class RegistryEntry:
+    fingerprint: int
+    c_kv: np.ndarray
+    kr_base: np.ndarray
+    p_src: int
+    insert_epoch: int
+
+    @property
+    def chunk_len(self) -> int:
+        return self.kr_base.shape[0]
+
+
+@dataclass
+class MaterializeResult:
+    c_kv: np.ndarray
+    k_r: np.ndarray
+    delta: int
+    multiplies: int
+
+
+class DevicePool:
+    """Latent pool [layers, rows, ckv_dim + kr_dim] on the device, grown by doubling."""
+
+    def __init__(self, ckv_dim: int, kr_dim: int, layers: int = 1, dtype=torch.float64, rows: int = 4096):
+        self.ckv_dim, self.kr_dim, self.layers, self.dtype = ckv_dim, kr_dim, layers, dtype
+        self.data = torch.zeros(layers, rows, ckv_dim + kr_dim, dtype=dtype, device=ops._dev())
+
+    def ensure(self, rows: int):
+        if rows <= self.data.shape[1]:
+            return
+        cap = self.data.shape[1]
+        while cap < rows:
+            cap *= 2
+        new = torch.zeros(self.layers, cap, self.data.shape[2], dtype=self.dtype, device=self.data.device)
+        new[:, : self.data.shape[1]] = self.data
+        self.data = new
+
+
+class KvRegistry:
+    """fingerprint -> (c_kv, kr_base, p_src); first writer wins (registry.py:94-170)."""
+
+    def __init__(self, kv_params: SyntheticKvParams, spec: RotarySpec, max_entries: int = 1 << 16):
+        self.kv_params = kv_params
+        self.spec = spec
+        self._synth = _SynthCache(kv_params)
+        self._entries: list[RegistryEntry] = []
+        self._entry_rows: list[int] = []  # pool row of entry i
+        self.store = ops.ChunkStore(max_entries)
+        self.pool = DevicePool(kv_params.ckv_dim, kv_params.kr_dim)
+        self._rows_used = 0
+        self._order = 0
+        self._gather_ws = None
+
+    # ------------------------------------------------------------ queries
+    def __len__(self) -> int:
+        return len(self._entries)
+
+    def __contains__(self, fp: int) -> bool:
+        return self.lookup(fp) is not None
+
+    def _fp_tensor(self, fps) -> torch.Tensor:
+        a = np.asarray([int(f) & (2**64 - 1) for f in fps], dtype=np.uint64).view(np.int64)
+        return torch.from_numpy(a).to(ops._dev())
+
+    def lookup(self, fp: int) -> RegistryEntry | None:
+        e = int(self.store.lookup(self._fp_tensor([fp])).item())
+        return self._entries[e] if e >= 0 else None
+
+    def entries(self) -> list[RegistryEntry]:
+        return list(self._entries)  # entry index == insert epoch
+
+    def entry_by_index(self, i: int) -> RegistryEntry:
+        return self._entries[i]
+
+    def fresh_rows(self, tokens: Sequence[int]) -> tuple[np.ndarray, np.ndarray]:
+        return self._synth.rows(tokens)
+
+    # ------------------------------------------------------------ inserts
+    def insert(self, fp: int, tokens: Sequence[int], p_src: int) -> RegistryEntry:
+        """Store a chunk's KV at p_src (no-op on duplicates, registry.py:126-140)."""
+        dev = ops._dev()
+        hit, entry, _, row = self.store.lookup_insert(
+            self._fp_tensor([fp]), torch.tensor([self._order], dtype=torch.int64, device=dev),
+            torch.tensor([p_src], dtype=torch.int64, device=dev),
+            torch.tensor([len(tokens)], dtype=torch.int32, device=dev))
+        self._order += 1
+        h, e, r = int(hit.item()), int(entry.item()), int(row.item())
+        if h == 1:
+            return self._entries[e]
+        assert e == len(self._entries), "device store and host mirror diverged"
+        return self.commit_rows(fp, tokens, p_src, r)
+
+    def commit_rows(self, fp: int, tokens: Sequence[int], p_src: int, row: int) -> RegistryEntry:
+        """Producer side: write synthetic prefill rows at pool row ``row`` and
+        rotate k_r to p_src + i on the device (registry.py:131-136)."""
+        n = len(tokens)
+        c_kv, kr_raw = self._synth.rows(tokens)
+        self.pool.ensure(row + n)
+        d = self.pool.data
+        ckv = self.kv_params.ckv_dim
+        dev = d.device
+        if n:
+            d[0, row:row + n, :ckv] = torch.from_numpy(c_kv).to(dev)
+            d[0, row:row + n, ckv:] = torch.from_numpy(kr_raw).to(dev)
+            pos = torch.arange(p_src, p_src + n, dtype=torch.float64, device=dev)
+            kr_view = d[0, row:row + n, ckv:]
+            ops.rotate_rows(kr_view, pos, inv_freq_device(self.spec), self.spec.layout_code,
+                            out=kr_view)
+            kr_base = kr_view.cpu().numpy().copy()
+        else:
+            kr_base = np.zeros((0, self.kv_params.kr_dim))
+        self._rows_used = max(self._rows_used, row + n)
+        c_kv = c_kv.copy()
+        c_kv.setflags(write=False)
+        kr_base.setflags(write=False)
+        entry = RegistryEntry(int(fp), c_kv, kr_base, int(p_src), len(self._entries))
+        self._entries.append(entry)
+        self._entry_rows.append(row)
+        return entry
+
+    def pool_bytes(self) -> int:
+        """Bytes of the shared latent pool as f64 c_kv rows (one copy per fingerprint)."""
+        return sum(e.c_kv.nbytes for e in self._entries)
+
+    # ------------------------------------------------------------ materialize
+    def materialize_device(self, rows: torch.Tensor, lens: torch.Tensor, deltas: torch.Tensor,
+                           precision: Precision = Precision.F64, out: torch.Tensor | None = None):
+        """Batched K4 over the pool: chunk i -> out rows [sum(lens[:i]), +lens[i])."""
+        n_rows = int(lens.sum().item()) if out is None else out.shape[1]
+        if out is None:
+            out = torch.empty(1, max(n_rows, 1), self.pool.data.shape[2], dtype=self.pool.data.dtype,
+                              device=self.pool.data.device)
+        dst = torch.zeros_like(rows)
+        if rows.numel() > 1:
+            dst[1:] = torch.cumsum(lens[:-1].to(torch.int64), 0)
+        need = int(N.lib().irm_rotate_gather_workspace_bytes(rows.numel(), self.kv_params.kr_dim))
+        if self._gather_ws is None or self._gather_ws.numel() < need:
+            self._gather_ws = torch.empty(max(need, 256), dtype=torch.uint8, device=out.device)
+        ops.rotate_gather(self.pool.data, out, rows, dst, lens.to(torch.int32), deltas,
+                          inv_freq_device(self.spec), self.kv_params.ckv_dim, self.kv_params.kr_dim,
+                          self.spec.layout_code, _ROUND[Precision(precision)], ws=self._gather_ws)
+        return out
+
+    def materialize(self, entry: RegistryEntry, p_dest: int,
+                    precision: Precision = Precision.F64) -> MaterializeResult:
+        """Re-target a stored chunk to p_dest via a uniform delta-rotation (registry.py:146-166)."""
+        if p_dest < 0:
+            raise ValueError("p_dest must be non-negative")
+        delta = p_dest - entry.p_src
+        n = entry.chunk_len
+        if n == 0:
+            return MaterializeResult(entry.c_kv, np.zeros((0, self.spec.dim)), delta, 0)
+        dev = ops._dev()
+        out = self.materialize_device(
+            torch.tensor([self._entry_rows[entry.insert_epoch]], dtype=torch.int64, device=dev),
+            torch.tensor([n], dtype=torch.int32, device=dev),
+            torch.tensor([delta], dtype=torch.int64, device=dev), precision)
+        k_r = out[0, :n, self.kv_params.ckv_dim:].cpu().numpy().copy()
+        return MaterializeResult(entry.c_kv, k_r, delta, n * self.spec.dim)
+
+    def naive_reuse(self, entry: RegistryEntry, p_dest: int) -> MaterializeResult:
+        """Stored rows with no rotation: the naive-reuse baseline (registry.py:168-170)."""
+        return MaterializeResult(entry.c_kv, np.array(entry.kr_base), p_dest - entry.p_src, 0)

@@ -1,0 +1,133 @@
+"""Seeded inputs for the golden fixtures (no reference import needed).
+
+Both ``make_golden.py`` (reference side, build container) and the parity tests
+(GPU box) regenerate the exact same inputs from these case tables.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64_fill(seed: int, n: int) -> np.ndarray:
+    """Vectorised splitmix64 stream (reference rng.py:17-38)."""
+    with np.errstate(over="ignore"):
+        state = np.uint64(seed) + np.arange(1, n + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+        z = state
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+GEAR = splitmix64_fill(0x49524D494E53554C, 65536)
+
+
+def rand_tokens(seed: int, n: int) -> np.ndarray:
+    return np.random.Generator(np.random.PCG64(seed)).integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+
+
+def marker_tokens() -> np.ndarray:
+    with np.errstate(over="ignore"):
+        s = np.uint64(0x49524D494E53554C) ^ np.uint64(64)
+        s2 = splitmix64_fill(int(s), 1)[0]
+    return (splitmix64_fill(int(s2), 64) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+
+def _adversarial(seed: int, n: int) -> np.ndarray:
+    """Tokens whose Gear entries sit next to 0 / 2^64: the rolling state then
+    hugs the wrap-around, which is where the warp-parallel MSB speculation of
+    the CUDA scan is undetermined and must fall back to exact resolution."""
+    order = np.argsort(GEAR)
+    lo = order[:8].astype(np.uint32)          # gear ~ 0
+    hi = order[-8:].astype(np.uint32)         # gear ~ 2^64
+    rng = np.random.Generator(np.random.PCG64(seed))
+    pick = rng.integers(0, 4, size=n)
+    rnd = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    toks = np.where(pick == 0, lo[rng.integers(0, 8, size=n)],
+                    np.where(pick == 1, hi[rng.integers(0, 8, size=n)],
+                             np.where(pick == 2, hi[0], rnd)))
+    # high 16 bits are ignored by the table index; randomise them
+    return (toks & np.uint32(0xFFFF)) | (rnd & np.uint32(0xFFFF0000))
+
+
+def cdc_case_inputs(case: dict):
+    kind = case.get("kind", "random")
+    n = case["n"]
+    if kind == "random":
+        tokens = rand_tokens(case["seed"], n)
+    elif kind == "marker":
+        pre = rand_tokens(case["seed"], case["prefix"])
+        body = rand_tokens(case["seed"] + 1, n - case["prefix"] - 64)
+        tokens = np.concatenate([pre, marker_tokens(), body])
+    elif kind == "const":
+        tokens = np.full(n, case["value"], np.uint32)
+    elif kind == "adversarial":
+        tokens = _adversarial(case["seed"], n)
+    elif kind == "hi_const":
+        tokens = np.full(n, int(np.argsort(GEAR)[-1 - case.get("rank", 0)]), np.uint32)
+    elif kind == "lo_const":
+        tokens = np.full(n, int(np.argsort(GEAR)[case.get("rank", 0)]), np.uint32)
+    else:
+        raise ValueError(kind)
+    pins = list(case.get("pins", []))
+    if "pin_every" in case:
+        pins += list(range(case["pin_every"] - 1, n, case["pin_every"]))
+    if kind == "marker":
+        s = case["prefix"]
+        pins += [s - 1, s + 63] if s > 0 else [63]
+    return tokens, set(pins)
+
+
+CDC_CASES = {
+    "empty": dict(n=0, seed=1, k=7, min=32, max=512),
+    "short20": dict(n=20, seed=2, k=7, min=32, max=512),
+    "exact32": dict(n=32, seed=3, k=7, min=32, max=512),
+    "tile5000": dict(n=5000, seed=3, k=7, min=32, max=512),
+    "stats100k": dict(n=100_000, seed=77, k=7, min=32, max=512),
+    "k20_maxclamp": dict(n=2000, seed=4, k=20, min=32, max=512),
+    "k1": dict(n=3000, seed=5, k=1, min=32, max=512),
+    "min1_max2": dict(n=777, seed=6, k=1, min=1, max=2),
+    "min1_k3": dict(n=2000, seed=7, k=3, min=1, max=40),
+    "small_params_pins": dict(n=4000, seed=8, k=3, min=4, max=9, pins=[0, 1, 2, 5, 100, 101, 3999]),
+    "marker_pinned": dict(kind="marker", n=1564, prefix=500, seed=21, k=7, min=32, max=512),
+    "marker_at_start": dict(kind="marker", n=1064, prefix=0, seed=22, k=7, min=32, max=512),
+    "marker_pins_disabled": dict(kind="marker", n=1064, prefix=500, seed=30, k=7, min=32, max=512, pinned=False),
+    "pins_edges": dict(n=3000, seed=9, k=7, min=32, max=512, pins=[-5, 0, 10, 11, 12, 511, 512, 2999, 3003]),
+    "pin_every_37": dict(n=20_000, seed=10, k=7, min=32, max=512, pin_every=37),
+    "pin_every_1000": dict(n=50_000, seed=11, k=7, min=32, max=512, pin_every=1000),
+    "long_131k": dict(n=131_072, seed=12, k=7, min=32, max=512, pins=[4095, 4159, 70000]),
+    "const_zero": dict(kind="const", n=3000, value=0, k=7, min=32, max=512),
+    "adversarial": dict(kind="adversarial", n=50_000, seed=13, k=7, min=32, max=512),
+    "adversarial_k2": dict(kind="adversarial", n=20_000, seed=14, k=2, min=2, max=300, pin_every=4321),
+    "hi_const": dict(kind="hi_const", n=5000, k=7, min=32, max=512),
+    "lo_const": dict(kind="lo_const", n=5000, k=4, min=8, max=200),
+}
+
+
+def rot_case_inputs(case: dict):
+    rng = np.random.Generator(np.random.PCG64(case["seed"]))
+    rows = rng.standard_normal((case["n"], 64))
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    positions = np.concatenate([
+        np.array([0, 1, -1, 1024, -1024, 2**20 - 1, -(2**17), 2**17], np.int64),
+        rng.integers(-(2**20), 2**20, size=case["n"] - 8),
+    ])
+    return rows, positions
+
+
+ROT_CASES = {f"theta_{int(t)}": dict(theta=t, n=512, seed=100 + i)
+             for i, t in enumerate((1e4, 5e4, 3.2e7))}
+
+
+TRACE_CASES = {
+    # config 1 of BASELINE.json: ~4K-token agent_meta prompts with shifted CDC chunks
+    "agent_meta_cfg1": dict(pattern="agent_meta", n_req=8, body_len=3900, seed=7),
+    "agent_meta_nomark": dict(pattern="agent_meta", n_req=6, body_len=2000, seed=3, markers=False),
+    "sysvar": dict(pattern="sysvar", n_req=10, body_len=2500, seed=1),
+    "compact": dict(pattern="compact", n_req=12, body_len=2000, seed=2),
+    "rerank": dict(pattern="rerank", n_req=20, body_len=2500, seed=4),
+    "tool_variants": dict(pattern="tool_variants", n_req=12, body_len=2500, seed=5),
+    "agent_meta_k5": dict(pattern="agent_meta", n_req=6, body_len=3000, seed=9, k=5),
+}

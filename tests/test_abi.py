@@ -1,0 +1,65 @@
+"""CPU: the C-ABI library loads, exports every declared entry point, and
+rejects bad arguments with the reference's error classes before any device
+work (ChunkerParams rules chunking.py:45-49 -> IRM_EINVAL -> ValueError)."""
+
+import ctypes
+
+import pytest
+
+from paper_2605_05696_b200 import _native as N
+
+
+def test_library_exports_every_header_symbol():
+    L = N.lib()
+    declared = N.exported_symbols()
+    assert len(declared) >= 16
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(N._SIGS) >= set(declared) - {"irm_mla_workspace_bytes", "irm_mla_reattach_prefill"}
+
+
+def test_abi_version_and_bounds():
+    L = N.lib()
+    assert L.irm_abi_version() == 1
+    assert L.irm_cdc_chunk_bound(32768, 1, 2, 32) == 32768 // 32 + 1 + 2 + 1
+    assert L.irm_cdc_chunk_bound(10, 1, 0, 0) == -1
+    assert L.irm_cdc_workspace_bytes(1 << 20, 8, 16, 32) > 0
+    assert L.irm_store_workspace_bytes(1000) > 0
+    assert L.irm_rotate_gather_workspace_bytes(100, 64) >= 100 * 32 * 16
+
+
+@pytest.mark.parametrize("k,mn,mx", [(0, 32, 512), (21, 32, 512), (7, 0, 512), (7, 512, 512), (7, 600, 512)])
+def test_cdc_param_validation(k, mn, mx):
+    L = N.lib()
+    rc = L.irm_cdc_xxh64(None, 0, None, 0, None, None, 0, k, mn, mx, 1, None, None, None, None,
+                         None, None, 0, None, 0, None)
+    assert rc == N.IRM_EINVAL
+    with pytest.raises(ValueError):
+        N.check(rc, "cdc")
+
+
+def test_cdc_capacity_error():
+    L = N.lib()
+    buf = ctypes.create_string_buffer(64)
+    rc = L.irm_cdc_xxh64(buf, 1000, buf, 1, None, None, 0, 7, 32, 512, 1, buf, buf, buf, buf, buf,
+                         buf, 3, buf, 64, None)
+    assert rc == N.IRM_ECAPACITY
+
+
+def test_rotate_validation():
+    L = N.lib()
+    # odd rotary dim, bad layout, rounding on a non-f64 pool
+    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 63, None, None, None, None, 1, None, 0, 0, 0, None, 0, None) == N.IRM_EINVAL
+    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 1, None, 7, 0, 0, None, 0, None) == N.IRM_EINVAL
+    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 1, None, 0, N.DTYPE_BF16, N.ROUND_BF16, None, 0, None) == N.IRM_EINVAL
+    assert L.irm_rotate_rows(None, 0, None, 0, 4, 63, None, None, 0, 0, 0, None) == N.IRM_EINVAL
+    # zero work is a no-op success
+    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 0, None, 0, 0, 0, None, 0, None) == N.IRM_OK
+
+
+def test_store_view_validation():
+    L = N.lib()
+    v = N.StoreView()
+    v.n_slots = 3  # not a power of two
+    assert L.irm_store_reset(ctypes.byref(v), None) == N.IRM_EINVAL
+    assert b"power of two" in L.irm_last_error()

@@ -1,0 +1,140 @@
+"""GPU parity: rotation (rotate_rows / round_bf16) against the reference's
+golden outputs, and K4 rotate+gather (f64 / f32 / bf16 pools, half-split and
+interleaved layouts) against the oracle.
+
+Tolerances (BASELINE.json north_star): fp32 k_r <= 1e-5 rel-L2; bf16 <= 4.7e-3
+rel-L2 vs f64 truth; f64 <= 1e-12 (GPU fp64 trig vs the host libm)."""
+
+import numpy as np
+import pytest
+import torch
+
+from inputs import ROT_CASES, rot_case_inputs
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-5
+BF16_TOL = 4.7e-3
+
+
+@pytest.fixture(scope="module")
+def R():
+    from paper_2605_05696_b200 import _native as N, ops, rotary
+
+    return rotary, ops, N
+
+
+@pytest.mark.parametrize("name", sorted(ROT_CASES))
+def test_rotate_rows_golden(R, name, golden_rotary):
+    rotary, _, _ = R
+    case = ROT_CASES[name]
+    rows, pos = rot_case_inputs(case)
+    spec = rotary.make_spec(case["theta"])
+    g = golden_rotary[name]
+    assert np.array_equal(spec.inv_freq, g["inv_freq"])
+    out = rotary.rotate_rows(rows, pos, spec)
+    err = np.abs(out - g["out"]).max()
+    assert err <= 1e-12, err
+    # store rounding is a deterministic function of the f64 value: bit-exact
+    assert np.array_equal(rotary.round_bf16(g["out"]), g["out_bf16"])
+    assert np.array_equal(rotary._store(g["out"], rotary.Precision.F32), g["out_f32"])
+
+
+def test_round_bf16_edge_cases(R):
+    rotary, _, _ = R
+    x = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1.0, 1.00390625, 1.005859375, 2.0**-133,
+                  2.0**-134, 3 * 2.0**-135, 3.3961e38, 3.4e38, -1e-40, 1e-45, 65504.0, 1 / 3])
+    got = rotary.round_bf16(x)
+    ref = O.round_bf16(x)
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    m = ~np.isnan(ref)
+    assert np.array_equal(got[m], ref[m])
+
+
+def _pool(rng, layers, rows, dtype, ckv=512, kr=64):
+    p = rng.standard_normal((layers, rows, ckv + kr))
+    return p
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32", "bf16"])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_rotate_gather_vs_oracle(R, dtype, layout):
+    rotary, ops, N = R
+    rng = np.random.default_rng(5 + layout)
+    layers, prow = 3, 4000
+    pool64 = _pool(rng, layers, prow, dtype)
+    lens = rng.integers(1, 300, size=40).astype(np.int32)
+    lens[:4] = [1, 7, 32, 512]
+    src = rng.integers(0, prow - 512, size=lens.size).astype(np.int64)
+    dst = np.concatenate([[0], np.cumsum(lens[:-1])]).astype(np.int64)
+    delta = rng.integers(-(2**20), 2**20, size=lens.size).astype(np.int64)
+    delta[:3] = [0, 1, -1]
+    inv = O.make_inv_freq(1e4)
+    tdt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+    pool = torch.from_numpy(pool64).to("cuda", tdt)
+    out = torch.full((layers, int(lens.sum()), 576), float("nan"), dtype=tdt, device="cuda")
+    d = lambda a: torch.from_numpy(a).cuda()
+    ops.rotate_gather(pool, out, d(src), d(dst), d(lens), d(delta), ops.inv_freq_device(inv), layout=layout)
+    got = out.to(torch.float64).cpu().numpy()
+    pin = pool.to(torch.float64).cpu().numpy()  # exact input values after storage rounding
+    for c in range(lens.size):
+        for l in range(layers):
+            s, t, n = src[c], dst[c], lens[c]
+            src_rows = pin[l, s:s + n]
+            g = got[l, t:t + n]
+            assert np.array_equal(g[:, :512], src_rows[:, :512])  # c_KV verbatim
+            truth = O.rotate_rows(src_rows[:, 512:], np.full(n, delta[c]), inv, interleaved=bool(layout))
+            err = O.rel_l2(g[:, 512:], truth)
+            tol = {"f64": 1e-13, "f32": 1e-6, "bf16": 4e-3}[dtype]
+            assert err <= tol, (dtype, layout, c, l, err)
+
+
+def test_rotate_gather_f64_rounding_modes(R):
+    rotary, ops, N = R
+    rng = np.random.default_rng(9)
+    pool = torch.from_numpy(rng.standard_normal((1, 600, 576))).cuda()
+    lens = np.array([100, 37], np.int32)
+    src = np.array([0, 300], np.int64)
+    dst = np.array([0, 100], np.int64)
+    delta = np.array([777, -4096], np.int64)
+    inv = O.make_inv_freq(5e4)
+    d = lambda a: torch.from_numpy(a).cuda()
+    for mode, fn in [(N.ROUND_F32, lambda x: x.astype(np.float32).astype(np.float64)), (N.ROUND_BF16, O.round_bf16)]:
+        out = torch.empty(1, 137, 576, dtype=torch.float64, device="cuda")
+        ops.rotate_gather(pool, out, d(src), d(dst), d(lens), d(delta), ops.inv_freq_device(inv), out_round=mode)
+        exact = torch.empty_like(out)
+        ops.rotate_gather(pool, exact, d(src), d(dst), d(lens), d(delta), ops.inv_freq_device(inv))
+        e = exact.cpu().numpy()[0, :, 512:]
+        assert np.array_equal(out.cpu().numpy()[0, :, 512:], fn(e))
+
+
+@pytest.mark.parametrize("theta", [1e4, 5e4, 3.2e7])
+def test_delta_precision_sweep(R, theta):
+    """Config 4: |delta| in 2^0..2^17 (both signs), rel-L2 vs f64 truth of the
+    fresh rotation: fp32 within 1e-5, bf16 (bf16 kr_base in, bf16 out) within 4.7e-3."""
+    rotary, ops, N = R
+    rng = np.random.default_rng(int(theta) % 1000)
+    inv = O.make_inv_freq(theta)
+    n = 2000
+    raw = rng.standard_normal((n, 64))
+    raw /= np.linalg.norm(raw, axis=1, keepdims=True)
+    p_src = 5000
+    base64 = O.rotate_rows(raw, np.full(n, p_src), inv)
+    deltas = np.array([s * 2**e for e in range(18) for s in (1, -1)], np.int64)
+    deltas = deltas[p_src + deltas >= 0]
+    pool = np.zeros((1, n, 576))
+    pool[0, :, 512:] = base64
+    d = lambda a: torch.from_numpy(a).cuda()
+    for dt, tol in [(torch.float32, F32_TOL), (torch.bfloat16, BF16_TOL)]:
+        tp = d(pool).to(dt)
+        lens = np.full(deltas.size, n, np.int32)
+        out = torch.empty(1, n * deltas.size, 576, dtype=dt, device="cuda")
+        ops.rotate_gather(tp, out, d(np.zeros(deltas.size, np.int64)),
+                          d(np.arange(deltas.size, dtype=np.int64) * n), d(lens), d(deltas), ops.inv_freq_device(inv))
+        got = out.to(torch.float64).cpu().numpy()[0, :, 512:].reshape(deltas.size, n, 64)
+        worst = 0.0
+        for i, dl in enumerate(deltas):
+            truth = O.rotate_rows(raw, np.full(n, p_src + dl), inv)
+            worst = max(worst, O.rel_l2(got[i], truth))
+        assert worst <= tol, (dt, theta, worst)
