@@ -1,0 +1,416 @@
+"""Benchmark of the cache-reattach hot path (BASELINE.json config 2).
+
+A step = one wave of R fresh 32K-token agent_meta requests (shared 50-token
+header, per-request 30..70-token metadata, 64-token marker, shared 32,768-token
+body) served warm against a store that already holds the body:
+    K1  CDC + xxh64 over every request tail            (irm_cdc_xxh64)
+    K3  batched first-writer-wins store lookup/insert   (irm_store_lookup_insert)
+    K4  rotate+gather of every hit chunk x 27 layers    (irm_rotate_gather)
+        bf16 latent pool [27, rows, 576] -> per-request KV [27, R*33K, 576]
+DeepSeek-V2-Lite shape (27 layers, kv_lora_rank 512, rope 64, theta 1e4,
+DSv2 interleaved rotary). Synthetic tokens and random-init latent rows.
+
+value = reattached KV tokens / s / GPU (PIC-hit tokens, each gathered and
+rotated for all 27 layers) with inputs resident in HBM; e2e adds the H2D of
+the wave's tokens/pins from pinned host memory and the D2H of the per-chunk
+service result. Components: CDC+hash tokens/s (K1 alone) and, when built,
+fused reattach-attention TFLOPS (K5).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reattached KV tokens/s/GPU (rotate+gather); CDC+hash tokens/s; fused-attn TFLOPS"
+UNIT = "tokens/s"
+LAYERS, CKV, KR, THETA = 27, 512, 64, 1e4
+BODY, HEADER, R_PER_WAVE = 32768, 50, 8
+CARVE = 32
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------- workload
+def make_wave(rng, header, marker, body, n_req):
+    """Token streams of one wave plus the host-side phase-1 prefix length m
+    (the shared header; exact-prefix matching is host radix work, §8(f))."""
+    streams, pins, ms = [], [], []
+    for _ in range(n_req):
+        meta = rng.integers(0, 2**32, size=int(rng.integers(30, 71)), dtype=np.uint64).astype(np.uint32)
+        full = np.concatenate([header, meta, marker, body])
+        m = HEADER  # the metadata diverges right after the shared header
+        tail = full[m:]
+        ms_ = meta.size
+        pins.append(sorted({ms_ - 1, ms_ + 63}))  # marker_pin_offsets rebased to the tail
+        streams.append(tail)
+        ms.append(m)
+    return streams, pins, ms
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (recipe clocks line)."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_05696_b200 import _native as N, ops
+    from paper_2605_05696_b200.chunking import canonical_marker
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    hbm, tf_burst, tf_sust, peak_kind = peaks()
+
+    # -------- inputs (seeded, per rank: sessions s mod G)
+    rng = np.random.default_rng(1000 + rank)
+    shared = np.random.default_rng(7)
+    header = shared.integers(0, 2**32, size=HEADER, dtype=np.uint64).astype(np.uint32)
+    body = shared.integers(0, 2**32, size=BODY, dtype=np.uint64).astype(np.uint32)
+    marker = np.array(canonical_marker(), np.uint32)
+    R = args.requests
+    n_steps = args.warmup + args.steps
+    waves = [make_wave(rng, header, marker, body, R) for _ in range(n_steps + 1)]
+
+    def pack(wave):
+        streams, pins, ms = wave
+        off = np.zeros(len(streams) + 1, np.int64)
+        np.cumsum([s.size for s in streams], out=off[1:])
+        poff = np.zeros(len(streams) + 1, np.int64)
+        np.cumsum([len(p) for p in pins], out=poff[1:])
+        return (np.concatenate(streams), off, poff, np.array([x for p in pins for x in p], np.int64),
+                np.array(ms, np.int64))
+
+    packed = [pack(w) for w in waves]
+    max_tail = max(int(p[1][-1]) for p in packed)
+    req_stride = max(int(np.diff(p[1]).max()) + HEADER for p in packed)  # rows per request in the KV out
+
+    # device-resident inputs (value) and pinned host copies (e2e)
+    dev_in = [tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(dev) for a in p)
+              for p in packed]
+    host_in = [tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).pin_memory() for a in p)
+               for p in packed]
+
+    # -------- store + latent pool, populated by the cold request (untimed)
+    store = ops.ChunkStore(max_entries=1 << 16)
+    pool_rows = BODY + 2048 * (n_steps + 2)  # body + the novel header/meta chunks of every wave
+    pool = torch.randn(LAYERS, pool_rows, CKV + KR, device=dev).to(torch.bfloat16)  # random-init latents
+    inv = ops.inv_freq_device(np.power(THETA, -2.0 * np.arange(KR // 2) / KR))
+    out = torch.empty(LAYERS, R * req_stride, CKV + KR, dtype=torch.bfloat16, device=dev)
+    cws = ops.CdcWorkspace()
+    gws = torch.empty(int(N.lib().irm_rotate_gather_workspace_bytes(1 << 16, KR)), dtype=torch.uint8, device=dev)
+    order_base = [0]
+    layout = N.LAYOUT_INTERLEAVED  # DSv2 rotary form
+
+    ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev_k4 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    k1_ms, k4_ms = [], []
+
+    def step(inp, timing=False):
+        tok, off, poff, pins, ms = inp
+        if timing:
+            ev_k1[0].record()
+        table = ops.cdc_xxh64(tok, off, poff, pins, 7, 32, 512, True, ws=cws, n_tokens=tok.numel())
+        if timing:
+            ev_k1[1].record()
+        cap = table.start.numel()
+        # chunk -> request via the CSR offsets, all on the device (no host sync)
+        idx = torch.arange(cap, device=dev)
+        req = torch.searchsorted(table.chunk_off[1:], idx, right=True)
+        valid = idx < table.chunk_off[-1]
+        reqc = torch.clamp(req, max=R - 1)
+        p_abs = ms[reqc] + table.start.to(torch.int64)
+        probe = (valid & (p_abs >= CARVE)).to(torch.uint8)
+        order = order_base[0] + idx
+        order_base[0] += cap
+        hit, entry, p_src, row = store.lookup_insert(table.fp, order, p_abs, table.length, probe)
+        is_hit = hit == 1
+        length = torch.where(is_hit, table.length, torch.zeros_like(table.length))
+        src = torch.where(is_hit, row, torch.zeros_like(row))
+        dst = reqc * req_stride + p_abs
+        delta = p_abs - p_src
+        if timing:
+            ev_k4[0].record()
+        ops.rotate_gather(pool, out, src, dst, length, delta, inv, CKV, KR, layout, ws=gws)
+        if timing:
+            ev_k4[1].record()
+        return hit, length
+
+    # cold request: inserts the body (its pool rows hold the random latents)
+    step(dev_in[-1])
+    torch.cuda.synchronize()
+    for i in range(args.warmup):
+        step(dev_in[i])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # -------- timed region (value): inputs resident in HBM
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hit_tok = 0
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        t0.record()
+        lens = []
+        for i in range(args.steps):
+            _, l = step(dev_in[args.warmup + i], timing=True)
+            lens.append(l)
+        t1.record()
+        torch.cuda.synchronize()
+    ms_total = t0.elapsed_time(t1)
+    hit_tok = int(sum(int(l.sum().item()) for l in lens))
+    # per-launch K1/K4 durations: re-time each with events on the launch stream
+    for i in range(min(args.steps, 5)):
+        step(dev_in[args.warmup + i], timing=True)
+        torch.cuda.synchronize()
+        k1_ms.append(ev_k1[0].elapsed_time(ev_k1[1]))
+        k4_ms.append(ev_k4[0].elapsed_time(ev_k4[1]))
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        ht = torch.tensor([hit_tok], device=dev, dtype=torch.int64)
+        dist.all_reduce(ht)
+        hit_tok = int(ht.item())
+
+    value = hit_tok / (ms_total / 1e3)  # whole-job reattached tokens/s
+    ms_step = ms_total / args.steps
+    tok_per_wave = int(packed[0][1][-1])
+
+    # -------- e2e: through the public C-ABI ops with host buffers
+    e2e_ms = 0.0
+    bi = sum(t.numel() * t.element_size() for t in host_in[0])
+    bo = 0
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = []
+    for i in range(args.steps):
+        h = host_in[args.warmup + i]
+        inp = tuple(x.to(dev, non_blocking=True) for x in h)
+        hit, length = step(inp)
+        hh = torch.empty(hit.shape, dtype=hit.dtype, pin_memory=True)
+        hh.copy_(hit, non_blocking=True)
+        res.append(hh)
+        bo = hit.numel() * hit.element_size()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = hit_tok / (e2e_ms / 1e3)
+
+    # -------- roofline of the dominant kernel (K4) and K1
+    k4 = statistics.median(k4_ms)
+    k1 = statistics.median(k1_ms)
+    rows_per_launch = hit_tok // (world * args.steps) * LAYERS
+    k4_bytes = rows_per_launch * 2 * (CKV + KR) * 2
+    k4_gbs = k4_bytes / (k4 / 1e3) / 1e9
+    k1_bytes = tok_per_wave * 4 + (tok_per_wave // 128) * 24
+    k1_gbs = k1_bytes / (k1 / 1e3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "DeepSeek-V2-Lite reattach (config 2): 27 layers, kv_lora 512 + rope 64, "
+                               "DSv2 interleaved rotary theta 1e4, 32K-token agent_meta prompts",
+                   "requests_per_step": R, "tokens_per_request": tok_per_wave // R + HEADER,
+                   "layers": LAYERS, "l2": "inputs larger than L2 (1.0 GB pool, 8 GB KV out per step)",
+                   "parallelism": f"sessions s mod G over {world} GPU(s)"},
+        "roofline": {"bound": "hbm", "kernel": "irm_rotate_gather (K4)", "achieved": k4_gbs,
+                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": None,
+                     "peak_kind": peak_kind, "launch_ms": k4, "algorithmic_bytes": k4_bytes},
+        "components": {
+            "cdc_hash": {"value": tok_per_wave / (k1 / 1e3), "unit": "tokens/s", "kernel": "irm_cdc_xxh64 (K1)",
+                         "launch_ms": k1, "tokens_per_launch": tok_per_wave,
+                         "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm, "unit": "GB/s",
+                                      "frac": k1_gbs / hbm}},
+            "fused_attn": None,
+        },
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo},
+        "gpu_launches": args.steps * 11,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args, packed[0], sample_requests=R - 1)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------- CPU legs
+def cpu_baseline(args, packed, sample_requests=1, n_threads=0):
+    """The oracle port (restated reference, oracle/irm_oracle.c) on host cores:
+    CDC + xxh64, dict lookup, bf16 rotate+gather for `sample_requests` requests
+    of the same workload. Returns reattached tokens/s."""
+    from oracle import oracle as O
+
+    tok, off, poff, pins, ms = packed
+    n_req = off.size - 1
+    assert n_req > sample_requests, "need a cold request beyond the sample"
+    streams = [tok[off[i]:off[i + 1]] for i in range(n_req)]
+    pin_l = [pins[poff[i]:poff[i + 1]] for i in range(n_req)]
+    threads = n_threads or O.max_threads()
+    rng = np.random.default_rng(5)
+    # the store holds the body chunks (cold request), as on the GPU
+    cold = O.cdc_chunk(streams[-1], pins=pin_l[-1])  # the cold request populates the store
+    registry = {int(f): (int(s) + HEADER, int(s)) for s, f in zip(cold[0], cold[2]) if int(s) + HEADER >= CARVE}
+    rows = BODY + 4096
+    # bf16 bit patterns of values in [1, 2) with random mantissas (random-init latents)
+    pool = (np.uint16(0x3F80) | rng.integers(0, 128, size=(LAYERS, rows, CKV + KR), dtype=np.uint16))
+    out = np.zeros((LAYERS, sample_requests * (BODY + 512), CKV + KR), np.uint16)
+    inv = np.power(THETA, -2.0 * np.arange(KR // 2) / KR)
+    t0 = time.perf_counter()
+    total_hit = 0
+    for i in range(sample_requests):
+        st, ln, fp, fo = O.cdc_chunk(streams[i], pins=pin_l[i])
+        src, dst, lens, deltas = [], [], [], []
+        for s, l, f in zip(st, ln, fp):
+            p = int(ms[i]) + int(s)
+            if p < CARVE:
+                continue
+            e = registry.get(int(f))
+            if e is None:
+                continue
+            src.append(e[1]); dst.append(i * (BODY + 512) + int(s)); lens.append(int(l)); deltas.append(p - e[0])
+        total_hit += sum(lens)
+        O.rotate_gather_bf16(pool, out, np.array(src), np.array(dst), np.array(lens), np.array(deltas),
+                             inv, interleaved=True, n_threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": total_hit / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sample_requests} x 32K-token request(s): oracle CDC+xxh64, dict lookup, "
+                      f"bf16 rotate+gather of {total_hit} hit tokens x {LAYERS} layers ({dt:.2f} s)"}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    oracle port; the Python reference cannot travel to the GPU box) on all
+    host threads, same metric/config, a bounded sample per step."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2605_05696_b200.rng import SplitMix64  # host constant only
+
+    shared = np.random.default_rng(7)
+    header = shared.integers(0, 2**32, size=HEADER, dtype=np.uint64).astype(np.uint32)
+    body = shared.integers(0, 2**32, size=BODY, dtype=np.uint64).astype(np.uint32)
+    gen = SplitMix64(SplitMix64(0x49524D494E53554C ^ 64).next_u64())
+    marker = np.array([v & 0xFFFFFFFF for v in gen.fill(64)], np.uint32)
+    rng = np.random.default_rng(1000)
+    n_sample = 4
+    streams, pins, ms = make_wave(rng, header, marker, body, n_sample + 1)
+    off = np.zeros(len(streams) + 1, np.int64)
+    np.cumsum([x.size for x in streams], out=off[1:])
+    poff = np.zeros(len(streams) + 1, np.int64)
+    np.cumsum([len(p) for p in pins], out=poff[1:])
+    packed = (np.concatenate(streams), off, poff, np.array([x for p in pins for x in p], np.int64),
+              np.array(ms, np.int64))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(args, packed, n_sample)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median([r["value"] for r in vals])
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "DeepSeek-V2-Lite reattach (config 2): 27 layers, kv_lora 512 + rope 64, "
+                                   "DSv2 interleaved rotary theta 1e4, 32K-token agent_meta prompts (CPU oracle port)",
+                       "requests_per_step": n_sample},
+            "cpu_baseline": {**vals[-1], "value": v},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--requests", type=int, default=R_PER_WAVE)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

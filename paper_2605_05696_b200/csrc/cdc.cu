@@ -177,7 +177,8 @@ cdc_scan_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ reg
                 const unsigned m = cand & (0xffffffffu << (lo_c - base));
                 if (m) t_cand = base + __ffs(m) - 1;
             }
-            const int32_t nxt = min(t_max, min(t_pin, t_cand));
+            // the pin (region end) counts only while the open chunk can reach it
+            const int32_t nxt = min(t_max, min(t_pin >= start ? t_pin : INT32_MAX, t_cand));
             if (nxt >= end) break;
             if (lane == 0) {
                 st_start[cap + nchunks] = rel0 + start;

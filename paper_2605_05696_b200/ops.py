@@ -80,27 +80,24 @@ class ChunkTable:
 
 
 class CdcWorkspace:
-    """Reusable device buffers for irm_cdc_xxh64 (grown on demand)."""
+    """Reusable device scratch for irm_cdc_xxh64 (grown on demand). Output
+    tables are allocated per call, so results never alias a later call."""
 
     def __init__(self):
         self.ws = None
-        self.cap = 0
-        self.bufs = None
 
     def get(self, n_tokens, n_streams, n_pins, min_size):
         L = N.lib()
         wb = int(L.irm_cdc_workspace_bytes(n_tokens, n_streams, n_pins, min_size))
-        cap = int(L.irm_cdc_chunk_bound(n_tokens, n_streams, n_pins, min_size))
+        cap = max(int(L.irm_cdc_chunk_bound(n_tokens, n_streams, n_pins, min_size)), 16)
         dev = _dev()
         if self.ws is None or self.ws.numel() < wb:
             self.ws = torch.empty(max(wb, 256), dtype=torch.uint8, device=dev)
-        if self.bufs is None or self.cap < cap:
-            self.cap = max(cap, 16)
-            self.bufs = (torch.empty(self.cap, dtype=torch.int32, device=dev),
-                         torch.empty(self.cap, dtype=torch.int32, device=dev),
-                         torch.empty(self.cap, dtype=torch.int64, device=dev),
-                         torch.empty(self.cap, dtype=torch.uint8, device=dev))
-        return self.ws, self.bufs, self.cap
+        bufs = (torch.empty(cap, dtype=torch.int32, device=dev),
+                torch.empty(cap, dtype=torch.int32, device=dev),
+                torch.empty(cap, dtype=torch.int64, device=dev),
+                torch.empty(cap, dtype=torch.uint8, device=dev))
+        return self.ws, bufs, cap
 
 
 _DEFAULT_CDC_WS = CdcWorkspace()
