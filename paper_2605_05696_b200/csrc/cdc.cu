@@ -106,53 +106,98 @@ cdc_plan_kernel(const int64_t *__restrict__ stream_off, int32_t n_streams,
     }
 }
 
-constexpr int SCAN_WARPS = 4;
+// One CTA per region: a chain warp runs the sequential MSB recurrence and the
+// boundary walk tile by tile, while the producer warps compute the windowed
+// G_t of the next tile (gear loads have high MLP there, not on the chain).
+constexpr int RG_THREADS = 256;
+constexpr int RG_TILE = 1024;                 // tokens per pipeline tile
+constexpr int RG_SUB = RG_TILE / 32;          // 32-token sub-blocks (chain steps) per tile
+constexpr int RG_PRODUCERS = RG_THREADS / 32 - 1;
+constexpr int RG_PER = (RG_SUB + RG_PRODUCERS - 1) / RG_PRODUCERS;
 
-__global__ void __launch_bounds__(SCAN_WARPS * 32)
-cdc_scan_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ regions,
-                const int64_t *__restrict__ n_regions_p, const uint64_t *__restrict__ gear,
-                int32_t k, int32_t min_size, int32_t max_size, int32_t *__restrict__ st_start,
-                int32_t *__restrict__ st_len, uint8_t *__restrict__ st_forced,
-                uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count) {
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (r >= *n_regions_p) return;
-    const Region R = regions[r];
-    const uint32_t *__restrict__ rt = tok + R.tok_begin;
-    const int32_t rel0 = (int32_t)(R.tok_begin - R.stream_begin);
-    const uint64_t mask = (1ULL << k) - 1;
-    const int32_t t_pin = R.ends_pin ? R.len - 1 : INT32_MAX;
+__device__ __forceinline__ void producer_bar() {
+    asm volatile("bar.sync 1, %0;" ::"n"(RG_PRODUCERS * 32) : "memory");
+}
 
-    uint64_t Gprev = 0, B = 0;
-    int32_t start = 0, nchunks = 0;
-    const int64_t cap = R.cap_off;
-
-    // software prefetch of the next step's gear entry (tokens -> table index)
-    uint64_t g_next = (lane < R.len) ? __ldg(gear + (__ldg(rt + lane) & 0xFFFFu)) : 0;
-    for (int32_t base = 0; base < R.len; base += 32) {
-        const int32_t t = base + lane;
-        const bool valid = t < R.len;
-        const uint64_t g = g_next;
-        {
-            const int32_t tn = t + 32;
-            g_next = (tn < R.len) ? __ldg(gear + (__ldg(rt + tn) & 0xFFFFu)) : 0;
-        }
-        // G_t: windowed shift-add scan (Kogge-Stone), carry-in from step before
-        uint64_t x = g;
+// G_t for tokens [tile_start, tile_start + RG_TILE) of a region into sGdst.
+__device__ __forceinline__ void produce_tile(const uint32_t *__restrict__ rt, int32_t len,
+                                             int32_t tile_start, const uint64_t *__restrict__ gear,
+                                             uint64_t *sGdst, const uint64_t *sGprev,
+                                             uint64_t *sS31, int pw, int lane) {
+    uint32_t tk[RG_PER];
+    uint64_t g[RG_PER];
+#pragma unroll
+    for (int q = 0; q < RG_PER; ++q) {  // all token loads first, then all gear loads (MLP)
+        const int c = pw + q * RG_PRODUCERS;
+        const int32_t t = tile_start + c * 32 + lane;
+        tk[q] = (c < RG_SUB && t < len) ? __ldg(rt + t) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < RG_PER; ++q) {
+        const int c = pw + q * RG_PRODUCERS;
+        const int32_t t = tile_start + c * 32 + lane;
+        g[q] = (c < RG_SUB && t < len) ? __ldg(gear + (tk[q] & 0xFFFFu)) : 0ULL;
+    }
+#pragma unroll
+    for (int q = 0; q < RG_PER; ++q) {
+        const int c = pw + q * RG_PRODUCERS;
+        if (c >= RG_SUB) break;
+        uint64_t x = g[q];  // in-block windowed scan S_j = sum_{i<=j} g_i << (j-i)
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
             if (lane >= d) x += y << d;
         }
-        const uint64_t G = x + (Gprev << (lane + 1));
-        Gprev = __shfl_sync(0xffffffffu, G, 31);
+        sGdst[c * 32 + lane] = x;
+        if (lane == 31) sS31[c] = x;
+    }
+    producer_bar();
+    // carry-in G_{base-1} = G of the previous sub-block's last token:
+    // G_last(c) = S31(c) + (G_last(c-1) << 32), so two sub-blocks suffice
+    const uint64_t prevG = sGprev ? sGprev[RG_TILE - 1] : 0ULL;
+#pragma unroll
+    for (int q = 0; q < RG_PER; ++q) {
+        const int c = pw + q * RG_PRODUCERS;
+        if (c >= RG_SUB) break;
+        const uint64_t gb = c == 0 ? prevG
+                          : c == 1 ? sS31[0] + (prevG << 32)
+                                   : sS31[c - 1] + (sS31[c - 2] << 32);
+        sGdst[c * 32 + lane] += gb << (lane + 1);
+    }
+}
 
-        // B_t: known part (B << j) plus the in-step part < 2^j
+struct ChunkSink {
+    int32_t *st_start, *st_len;
+    uint8_t *st_forced;
+    int64_t cap;
+    int32_t rel0;
+    __device__ __forceinline__ void emit(int lane, int32_t n, int32_t start, int32_t len, uint8_t f) const {
+        if (lane == 0) {
+            st_start[cap + n] = rel0 + start;
+            st_len[cap + n] = len;
+            st_forced[cap + n] = f;
+        }
+    }
+};
+
+// chain warp: MSB recurrence over one tile (h_t, candidate mask), then the
+// boundary rule (chunking.py:116-124: marker > max_clamp > mask hit)
+__device__ __forceinline__ void chain_walk_tile(const uint64_t *sG, int32_t tile_start, int32_t len,
+                                                uint64_t mask, int32_t min_size, int32_t max_size,
+                                                int32_t t_pin, uint64_t &B, int32_t &start,
+                                                int32_t &nch, const ChunkSink &sink, int lane) {
+    const int nsteps = min(RG_SUB, (len - tile_start + 31) / 32);
+    unsigned my_cand = 0;  // lane s keeps the candidate word of step s
+    uint64_t Gn = sG[lane];
+    for (int s = 0; s < nsteps; ++s) {
+        const uint64_t G = Gn;
+        if (s + 1 < nsteps) Gn = sG[(s + 1) * 32 + lane];
+        const bool valid = tile_start + 32 * s + lane < len;
         const uint64_t lo = G + (B << lane);
         const uint64_t hi = lo + ((1ULL << lane) - 1);
         unsigned M = __ballot_sync(0xffffffffu, (unsigned)(lo >> 63));
         unsigned und = __ballot_sync(0xffffffffu, valid && ((lo ^ hi) >> 63));
-        while (und) {  // exact resolution of undetermined lanes, in lane order
+        while (und) {  // exact resolution of undetermined lanes, in lane order (rare)
             const int jj = __ffs(und) - 1;
             unsigned mb = 0;
             if (lane == jj) {
@@ -166,48 +211,80 @@ cdc_scan_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ reg
         const uint64_t h = lo + (lane ? (uint64_t)(__brev(M) >> (32 - lane)) : 0);
         B = (B << 32) | (uint64_t)__brev(M);
         const unsigned cand = __ballot_sync(0xffffffffu, valid && (h & mask) == 0);
+        if (lane == s) my_cand = cand;
+    }
+    const int32_t tile_end = min(tile_start + RG_TILE, len);
+    const int32_t word_lo = tile_start + 32 * lane;
+    while (true) {
+        const int32_t t_max = start + max_size - 1;
+        const int32_t lo_c = max(tile_start, start + min_size - 1);
+        unsigned mw = 0;
+        if (lo_c < word_lo + 32) mw = lo_c <= word_lo ? my_cand : my_cand & (0xffffffffu << (lo_c - word_lo));
+        const unsigned found = __ballot_sync(0xffffffffu, mw != 0);
+        int32_t t_cand = INT32_MAX;
+        if (found) {
+            const int w = __ffs(found) - 1;
+            const unsigned fw = __shfl_sync(0xffffffffu, mw, w);
+            t_cand = tile_start + 32 * w + __ffs(fw) - 1;
+        }
+        // the pin (region end) counts only while the open chunk can reach it
+        const int32_t nxt = min(t_max, min(t_pin >= start ? t_pin : INT32_MAX, t_cand));
+        if (nxt >= tile_end) break;
+        sink.emit(lane, nch, start, nxt - start + 1,
+                  nxt == t_pin ? IRM_FORCED_MARKER : nxt == t_max ? IRM_FORCED_MAX_CLAMP : IRM_FORCED_NONE);
+        ++nch;
+        start = nxt + 1;
+    }
+}
 
-        // boundary rule (chunking.py:116-124): marker > max_clamp > mask hit
-        const int32_t end = min(base + 32, R.len);
-        while (true) {
-            const int32_t t_max = start + max_size - 1;
-            const int32_t lo_c = max(base, start + min_size - 1);
-            int32_t t_cand = INT32_MAX;
-            if (lo_c < end) {
-                const unsigned m = cand & (0xffffffffu << (lo_c - base));
-                if (m) t_cand = base + __ffs(m) - 1;
-            }
-            // the pin (region end) counts only while the open chunk can reach it
-            const int32_t nxt = min(t_max, min(t_pin >= start ? t_pin : INT32_MAX, t_cand));
-            if (nxt >= end) break;
-            if (lane == 0) {
-                st_start[cap + nchunks] = rel0 + start;
-                st_len[cap + nchunks] = nxt - start + 1;
-                st_forced[cap + nchunks] = nxt == t_pin   ? IRM_FORCED_MARKER
-                                           : nxt == t_max ? IRM_FORCED_MAX_CLAMP
-                                                          : IRM_FORCED_NONE;
-            }
-            ++nchunks;
-            start = nxt + 1;
+__global__ void __launch_bounds__(RG_THREADS)
+cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ regions,
+                  const int64_t *__restrict__ n_regions_p, const uint64_t *__restrict__ gear,
+                  int32_t k, int32_t min_size, int32_t max_size, int32_t *__restrict__ st_start,
+                  int32_t *__restrict__ st_len, uint8_t *__restrict__ st_forced,
+                  uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count) {
+    __shared__ uint64_t sG[2][RG_TILE];
+    __shared__ uint64_t sS31[RG_SUB];
+    __shared__ int32_t sCount;
+    const int64_t r = blockIdx.x;
+    if (r >= *n_regions_p) return;  // uniform per CTA
+    const Region R = regions[r];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t *__restrict__ rt = tok + R.tok_begin;
+    const uint64_t mask = (1ULL << k) - 1;
+    const int32_t t_pin = R.ends_pin ? R.len - 1 : INT32_MAX;
+    const ChunkSink sink{st_start, st_len, st_forced, R.cap_off, (int32_t)(R.tok_begin - R.stream_begin)};
+    const int ntiles = (R.len + RG_TILE - 1) / RG_TILE;
+
+    uint64_t B = 0;  // chain-warp state: the previous 64 MSBs
+    int32_t start = 0, nch = 0;
+    for (int i = 0; i <= ntiles; ++i) {
+        if (warp == 0) {
+            if (i >= 1)
+                chain_walk_tile(sG[(i - 1) & 1], (i - 1) * RG_TILE, R.len, mask, min_size, max_size,
+                                t_pin, B, start, nch, sink, lane);
+        } else if (i < ntiles) {
+            produce_tile(rt, R.len, i * RG_TILE, gear, sG[i & 1], i ? sG[(i - 1) & 1] : nullptr, sS31,
+                         warp - 1, lane);
         }
+        __syncthreads();
     }
-    if (start < R.len) {  // only when the region ends at the stream end
+    if (warp == 0) {
+        if (start < R.len) {  // only when the region ends at the stream end
+            sink.emit(lane, nch, start, R.len - start, IRM_FORCED_STREAM_END);
+            ++nch;
+        }
         if (lane == 0) {
-            st_start[cap + nchunks] = rel0 + start;
-            st_len[cap + nchunks] = R.len - start;
-            st_forced[cap + nchunks] = IRM_FORCED_STREAM_END;
+            sCount = nch;
+            r_count[r] = nch;
         }
-        ++nchunks;
     }
-    __syncwarp();
-    // fingerprints: one lane per chunk
+    __syncthreads();
+    // fingerprints (fingerprint.py:28-30): one thread per chunk, tokens from L2
     const uint32_t *__restrict__ sbase = tok + R.stream_begin;
-    for (int32_t c = lane; c < nchunks; c += 32) {
-        const int32_t s = st_start[cap + c];
-        const int32_t l = st_len[cap + c];
-        st_fp[cap + c] = xxh64_words(sbase + s, l, 0);
-    }
-    if (lane == 0) r_count[r] = nchunks;
+    const int64_t cap = R.cap_off;
+    for (int32_t c = threadIdx.x; c < sCount; c += RG_THREADS)
+        st_fp[cap + c] = xxh64_words(sbase + st_start[cap + c], st_len[cap + c], 0);
 }
 
 __global__ void __launch_bounds__(PLAN_BLOCK)
@@ -360,8 +437,7 @@ extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_
                                               min_size, w.regions, w.r_first, w.n_regions);
     IRM_LAUNCH_CHECK();
     const int64_t rmax = (int64_t)n_streams + np;
-    const int64_t warps_blocks = (rmax + SCAN_WARPS - 1) / SCAN_WARPS;
-    cdc_scan_kernel<<<(unsigned)warps_blocks, SCAN_WARPS * 32, 0, st>>>(
+    cdc_region_kernel<<<(unsigned)rmax, RG_THREADS, 0, st>>>(
         tok, w.regions, w.n_regions, gear, mask_exponent, min_size, max_size, w.st_start, w.st_len,
         w.st_forced, w.st_fp, w.r_count);
     IRM_LAUNCH_CHECK();
