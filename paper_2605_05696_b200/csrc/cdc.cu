@@ -21,6 +21,7 @@
 // with ballot/ffs over the candidate mask, then hashes its chunks (lane per
 // chunk, XXH64 from L2-resident tokens).
 #include "common.cuh"
+#include <stdlib.h>
 
 namespace irm {
 
@@ -242,7 +243,7 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
                   const int64_t *__restrict__ n_regions_p, const uint64_t *__restrict__ gear,
                   int32_t k, int32_t min_size, int32_t max_size, int32_t *__restrict__ st_start,
                   int32_t *__restrict__ st_len, uint8_t *__restrict__ st_forced,
-                  uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count) {
+                  uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count, int dbg) {
     __shared__ uint64_t sG[2][RG_TILE];
     __shared__ uint64_t sS31[RG_SUB];
     __shared__ int32_t sCount;
@@ -258,7 +259,9 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
 
     uint64_t B = 0;  // chain-warp state: the previous 64 MSBs
     int32_t start = 0, nch = 0;
+    long long t_work = 0, t_all = clock64();
     for (int i = 0; i <= ntiles; ++i) {
+        const long long t0 = clock64();
         if (warp == 0) {
             if (i >= 1)
                 chain_walk_tile(sG[(i - 1) & 1], (i - 1) * RG_TILE, R.len, mask, min_size, max_size,
@@ -267,8 +270,12 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
             produce_tile(rt, R.len, i * RG_TILE, gear, sG[i & 1], i ? sG[(i - 1) & 1] : nullptr, sS31,
                          warp - 1, lane);
         }
+        t_work += clock64() - t0;
         __syncthreads();
     }
+    if (dbg && (threadIdx.x == 0 || threadIdx.x == 32) && R.len > 10000)  // IRM_CDC_DEBUG=1
+        printf("region %lld warp %d work %lld total %lld tiles %d\n", (long long)r, warp, t_work,
+               clock64() - t_all, ntiles);
     if (warp == 0) {
         if (start < R.len) {  // only when the region ends at the stream end
             sink.emit(lane, nch, start, R.len - start, IRM_FORCED_STREAM_END);
@@ -439,7 +446,7 @@ extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_
     const int64_t rmax = (int64_t)n_streams + np;
     cdc_region_kernel<<<(unsigned)rmax, RG_THREADS, 0, st>>>(
         tok, w.regions, w.n_regions, gear, mask_exponent, min_size, max_size, w.st_start, w.st_len,
-        w.st_forced, w.st_fp, w.r_count);
+        w.st_forced, w.st_fp, w.r_count, getenv("IRM_CDC_DEBUG") != nullptr);
     IRM_LAUNCH_CHECK();
     cdc_offsets_kernel<<<1, PLAN_BLOCK, 0, st>>>(w.n_regions, w.r_count, w.r_out, w.r_first,
                                                  n_streams, chunk_off);
