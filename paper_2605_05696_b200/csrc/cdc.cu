@@ -17,9 +17,9 @@
 // order. Then B advances by (B << 32) | brev(ballot(m)).
 //
 // Marker pins reset h (chunking.py:116-118), so the stream splits into
-// independent regions; one warp scans one region, walks the boundary rule
-// with ballot/ffs over the candidate mask, then hashes its chunks (lane per
-// chunk, XXH64 from L2-resident tokens).
+// independent regions; one CTA scans one region (producer / chain / walker
+// warps, see cdc_region_kernel), walks the boundary rule with ballot/ffs over
+// the candidate words, then hashes its chunks (XXH64 from L2-resident tokens).
 #include "common.cuh"
 #include <stdlib.h>
 
@@ -107,32 +107,40 @@ cdc_plan_kernel(const int64_t *__restrict__ stream_off, int32_t n_streams,
     }
 }
 
-// One CTA per region: a chain warp runs the sequential MSB recurrence and the
-// boundary walk tile by tile, while the producer warps compute the windowed
-// G_t of the next tile (gear loads have high MLP there, not on the chain).
-constexpr int RG_THREADS = 256;
+// One CTA per region, three warp roles pipelined over 1024-token tiles:
+//   producers (warps 2..15): windowed G_t of tile i (token loads one tile ahead)
+//   chain     (warp 0):      the sequential MSB recurrence over tile i-1
+//   walker    (warp 1):      the boundary rule over the candidate words of tile i-2
+// The chain's loop-carried path is kept to ~6 dependent instructions: msb(h)
+// is decided on the high 32-bit words alone (the low words can carry at most
+// 2 into them), the rare ambiguous lanes are resolved exactly in lane order.
+constexpr int RG_THREADS = 512;
 constexpr int RG_TILE = 1024;                 // tokens per pipeline tile
 constexpr int RG_SUB = RG_TILE / 32;          // 32-token sub-blocks (chain steps) per tile
-constexpr int RG_PRODUCERS = RG_THREADS / 32 - 1;
+constexpr int RG_PRODUCERS = RG_THREADS / 32 - 2;
 constexpr int RG_PER = (RG_SUB + RG_PRODUCERS - 1) / RG_PRODUCERS;
 
 __device__ __forceinline__ void producer_bar() {
     asm volatile("bar.sync 1, %0;" ::"n"(RG_PRODUCERS * 32) : "memory");
 }
 
-// G_t for tokens [tile_start, tile_start + RG_TILE) of a region into sGdst.
-__device__ __forceinline__ void produce_tile(const uint32_t *__restrict__ rt, int32_t len,
-                                             int32_t tile_start, const uint64_t *__restrict__ gear,
-                                             uint64_t *sGdst, const uint64_t *sGprev,
-                                             uint64_t *sS31, int pw, int lane) {
-    uint32_t tk[RG_PER];
-    uint64_t g[RG_PER];
+__device__ __forceinline__ void load_tile_tokens(const uint32_t *__restrict__ rt, int32_t len,
+                                                 int32_t tile_start, int pw, int lane,
+                                                 uint32_t (&tk)[RG_PER]) {
 #pragma unroll
-    for (int q = 0; q < RG_PER; ++q) {  // all token loads first, then all gear loads (MLP)
+    for (int q = 0; q < RG_PER; ++q) {
         const int c = pw + q * RG_PRODUCERS;
         const int32_t t = tile_start + c * 32 + lane;
         tk[q] = (c < RG_SUB && t < len) ? __ldg(rt + t) : 0u;
     }
+}
+
+// G_t for tokens [tile_start, tile_start + RG_TILE) of a region into sGdst.
+__device__ __forceinline__ void produce_tile(const uint32_t (&tk)[RG_PER], int32_t len,
+                                             int32_t tile_start, const uint64_t *__restrict__ gear,
+                                             uint64_t *sGdst, const uint64_t *sGprev,
+                                             uint64_t *sS31, int pw, int lane) {
+    uint64_t g[RG_PER];
 #pragma unroll
     for (int q = 0; q < RG_PER; ++q) {
         const int c = pw + q * RG_PRODUCERS;
@@ -167,6 +175,49 @@ __device__ __forceinline__ void produce_tile(const uint32_t *__restrict__ rt, in
     }
 }
 
+// chain warp: m_t = msb(h_t), h_t = G_t + B_t, over one tile; writes the
+// candidate words ((h & mask) == 0, chunking.py:121) to sCand[step].
+__device__ __forceinline__ void chain_tile(const uint64_t *sG, unsigned *sCand, int32_t tile_start,
+                                           int32_t len, uint32_t mask, uint32_t &Blo, uint32_t &Bhi,
+                                           int lane) {
+    const int nsteps = min(RG_SUB, (len - tile_start + 31) / 32);
+    unsigned my_cand = 0;  // lane s keeps the candidate word of step s
+    uint64_t Gn = sG[lane];
+    for (int s = 0; s < nsteps; ++s) {
+        const uint64_t G = Gn;
+        if (s + 1 < nsteps) Gn = sG[(s + 1) * 32 + lane];
+        const bool valid = tile_start + 32 * s + lane < len;
+        const uint32_t Glo = (uint32_t)G, Ghi = (uint32_t)(G >> 32);
+        const uint32_t Xlo = Blo << lane;                       // (B << j) low word
+        const uint32_t Xhi = __funnelshift_l(Blo, Bhi, lane);   // (B << j) high word
+        const uint32_t hs = Ghi + Xhi;  // high word of h up to a carry c in {0, 1, 2}
+        unsigned M = __ballot_sync(0xffffffffu, hs >> 31);
+        const unsigned und = __ballot_sync(0xffffffffu, valid && (hs & 0x7FFFFFFEu) == 0x7FFFFFFEu);
+        if (und) {  // exact resolution of ambiguous lanes, in lane order (~2^-30 per lane)
+            const uint64_t lo = G + ((((uint64_t)Bhi << 32) | Blo) << lane);
+            unsigned u2 = und;
+            while (u2) {
+                const int jj = __ffs(u2) - 1;
+                unsigned mb = 0;
+                if (lane == jj) {
+                    const uint64_t u = (uint64_t)((__brev(M) >> (31 - jj)) >> 1);
+                    mb = (unsigned)((lo + u) >> 63);
+                }
+                mb = __shfl_sync(0xffffffffu, mb, jj);
+                M = (M & ~(1u << jj)) | (mb << jj);
+                u2 &= u2 - 1;
+            }
+        }
+        Bhi = Blo;
+        Blo = __brev(M);
+        // low word of h: G_lo + (B << j)_lo + sum_{i<j} m_i << (j-1-i)
+        const uint32_t hlo = Glo + Xlo + ((Blo >> (31 - lane)) >> 1);
+        const unsigned cand = __ballot_sync(0xffffffffu, valid && (hlo & mask) == 0);
+        if (lane == s) my_cand = cand;
+    }
+    sCand[lane] = lane < nsteps ? my_cand : 0u;
+}
+
 struct ChunkSink {
     int32_t *st_start, *st_len;
     uint8_t *st_forced;
@@ -181,39 +232,13 @@ struct ChunkSink {
     }
 };
 
-// chain warp: MSB recurrence over one tile (h_t, candidate mask), then the
-// boundary rule (chunking.py:116-124: marker > max_clamp > mask hit)
-__device__ __forceinline__ void chain_walk_tile(const uint64_t *sG, int32_t tile_start, int32_t len,
-                                                uint64_t mask, int32_t min_size, int32_t max_size,
-                                                int32_t t_pin, uint64_t &B, int32_t &start,
-                                                int32_t &nch, const ChunkSink &sink, int lane) {
-    const int nsteps = min(RG_SUB, (len - tile_start + 31) / 32);
-    unsigned my_cand = 0;  // lane s keeps the candidate word of step s
-    uint64_t Gn = sG[lane];
-    for (int s = 0; s < nsteps; ++s) {
-        const uint64_t G = Gn;
-        if (s + 1 < nsteps) Gn = sG[(s + 1) * 32 + lane];
-        const bool valid = tile_start + 32 * s + lane < len;
-        const uint64_t lo = G + (B << lane);
-        const uint64_t hi = lo + ((1ULL << lane) - 1);
-        unsigned M = __ballot_sync(0xffffffffu, (unsigned)(lo >> 63));
-        unsigned und = __ballot_sync(0xffffffffu, valid && ((lo ^ hi) >> 63));
-        while (und) {  // exact resolution of undetermined lanes, in lane order (rare)
-            const int jj = __ffs(und) - 1;
-            unsigned mb = 0;
-            if (lane == jj) {
-                const uint64_t u = jj ? (uint64_t)(__brev(M) >> (32 - jj)) : 0;
-                mb = (unsigned)((lo + u) >> 63);
-            }
-            mb = __shfl_sync(0xffffffffu, mb, jj);
-            M = (M & ~(1u << jj)) | (mb << jj);
-            und &= und - 1;
-        }
-        const uint64_t h = lo + (lane ? (uint64_t)(__brev(M) >> (32 - lane)) : 0);
-        B = (B << 32) | (uint64_t)__brev(M);
-        const unsigned cand = __ballot_sync(0xffffffffu, valid && (h & mask) == 0);
-        if (lane == s) my_cand = cand;
-    }
+// walker warp: boundary rule over one tile (chunking.py:116-124:
+// marker > max_clamp > mask hit); lane w holds the candidate word of sub-block w
+__device__ __forceinline__ void walk_tile(const unsigned *sCand, int32_t tile_start, int32_t len,
+                                          int32_t min_size, int32_t max_size, int32_t t_pin,
+                                          int32_t &start, int32_t &nch, const ChunkSink &sink,
+                                          int lane) {
+    const unsigned my_cand = sCand[lane];
     const int32_t tile_end = min(tile_start + RG_TILE, len);
     const int32_t word_lo = tile_start + 32 * lane;
     while (true) {
@@ -246,37 +271,48 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
                   uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count, int dbg) {
     __shared__ uint64_t sG[2][RG_TILE];
     __shared__ uint64_t sS31[RG_SUB];
+    __shared__ unsigned sCand[2][RG_SUB];
     __shared__ int32_t sCount;
     const int64_t r = blockIdx.x;
     if (r >= *n_regions_p) return;  // uniform per CTA
     const Region R = regions[r];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t *__restrict__ rt = tok + R.tok_begin;
-    const uint64_t mask = (1ULL << k) - 1;
+    const uint32_t mask = (1u << k) - 1;  // k <= 20: the low word of h decides
     const int32_t t_pin = R.ends_pin ? R.len - 1 : INT32_MAX;
     const ChunkSink sink{st_start, st_len, st_forced, R.cap_off, (int32_t)(R.tok_begin - R.stream_begin)};
     const int ntiles = (R.len + RG_TILE - 1) / RG_TILE;
 
-    uint64_t B = 0;  // chain-warp state: the previous 64 MSBs
-    int32_t start = 0, nch = 0;
+    uint32_t Blo = 0, Bhi = 0;  // chain state: the previous 64 MSBs
+    int32_t start = 0, nch = 0;  // walker state
+    uint32_t tk[RG_PER];         // producer: tokens of the tile being produced
+    const int pw = warp - 2;
+    if (warp >= 2) load_tile_tokens(rt, R.len, 0, pw, lane, tk);
     long long t_work = 0, t_all = clock64();
-    for (int i = 0; i <= ntiles; ++i) {
+    for (int i = 0; i <= ntiles + 1; ++i) {
         const long long t0 = clock64();
         if (warp == 0) {
-            if (i >= 1)
-                chain_walk_tile(sG[(i - 1) & 1], (i - 1) * RG_TILE, R.len, mask, min_size, max_size,
-                                t_pin, B, start, nch, sink, lane);
+            if (i >= 1 && i <= ntiles)
+                chain_tile(sG[(i - 1) & 1], sCand[(i - 1) & 1], (i - 1) * RG_TILE, R.len, mask, Blo, Bhi, lane);
+        } else if (warp == 1) {
+            if (i >= 2)
+                walk_tile(sCand[i & 1], (i - 2) * RG_TILE, R.len, min_size, max_size, t_pin, start, nch,
+                          sink, lane);
         } else if (i < ntiles) {
-            produce_tile(rt, R.len, i * RG_TILE, gear, sG[i & 1], i ? sG[(i - 1) & 1] : nullptr, sS31,
-                         warp - 1, lane);
+            uint32_t tkn[RG_PER];
+            if (i + 1 < ntiles) load_tile_tokens(rt, R.len, (i + 1) * RG_TILE, pw, lane, tkn);
+            produce_tile(tk, R.len, i * RG_TILE, gear, sG[i & 1], i ? sG[(i - 1) & 1] : nullptr, sS31,
+                         pw, lane);
+#pragma unroll
+            for (int q = 0; q < RG_PER; ++q) tk[q] = tkn[q];
         }
         t_work += clock64() - t0;
         __syncthreads();
     }
-    if (dbg && (threadIdx.x == 0 || threadIdx.x == 32) && R.len > 10000)  // IRM_CDC_DEBUG=1
+    if (dbg && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64) && R.len > 10000)  // IRM_CDC_DEBUG=1
         printf("region %lld warp %d work %lld total %lld tiles %d\n", (long long)r, warp, t_work,
                clock64() - t_all, ntiles);
-    if (warp == 0) {
+    if (warp == 1) {
         if (start < R.len) {  // only when the region ends at the stream end
             sink.emit(lane, nch, start, R.len - start, IRM_FORCED_STREAM_END);
             ++nch;
