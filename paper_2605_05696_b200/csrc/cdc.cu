@@ -21,6 +21,7 @@
 // warps, see cdc_region_kernel), walks the boundary rule with ballot/ffs over
 // the candidate words, then hashes its chunks (XXH64 from L2-resident tokens).
 #include "common.cuh"
+#include "tma.cuh"
 #include <stdlib.h>
 
 namespace irm {
@@ -107,45 +108,50 @@ cdc_plan_kernel(const int64_t *__restrict__ stream_off, int32_t n_streams,
     }
 }
 
-// One CTA per region, three warp roles pipelined over 1024-token tiles:
-//   producers (warps 2..15): windowed G_t of tile i (token loads one tile ahead)
-//   chain     (warp 0):      the sequential MSB recurrence over tile i-1
-//   walker    (warp 1):      the boundary rule over the candidate words of tile i-2
-// The chain's loop-carried path is kept to ~6 dependent instructions: msb(h)
-// is decided on the high 32-bit words alone (the low words can carry at most
-// 2 into them), the rare ambiguous lanes are resolved exactly in lane order.
+// One CTA per region, four warp roles pipelined over 1024-token tiles:
+//   producers (warps 3..15): windowed G_t of tile i (tokens staged by cp.async
+//                            two tiles ahead)
+//   chain     (warp 0):      the sequential MSB recurrence over tile i-1 -- ONLY
+//                            m_t, ~6 dependent instructions per 32 tokens
+//   cand      (warp 1):      h_t and the mask candidates of tile i-2 (parallel
+//                            over steps: B at every step is known from the m's)
+//   walker    (warp 2):      the boundary rule over the candidate words of tile i-3
+// msb(h) is decided on the high 32-bit words alone (the low words carry at
+// most 2 into them); the rare ambiguous lanes are resolved exactly in lane order.
 constexpr int RG_THREADS = 512;
 constexpr int RG_TILE = 1024;                 // tokens per pipeline tile
 constexpr int RG_SUB = RG_TILE / 32;          // 32-token sub-blocks (chain steps) per tile
-constexpr int RG_PRODUCERS = RG_THREADS / 32 - 2;
+constexpr int RG_PRODUCERS = RG_THREADS / 32 - 3;
 constexpr int RG_PER = (RG_SUB + RG_PRODUCERS - 1) / RG_PRODUCERS;
 
 __device__ __forceinline__ void producer_bar() {
     asm volatile("bar.sync 1, %0;" ::"n"(RG_PRODUCERS * 32) : "memory");
 }
 
-__device__ __forceinline__ void load_tile_tokens(const uint32_t *__restrict__ rt, int32_t len,
-                                                 int32_t tile_start, int pw, int lane,
-                                                 uint32_t (&tk)[RG_PER]) {
-#pragma unroll
-    for (int q = 0; q < RG_PER; ++q) {
-        const int c = pw + q * RG_PRODUCERS;
-        const int32_t t = tile_start + c * 32 + lane;
-        tk[q] = (c < RG_SUB && t < len) ? __ldg(rt + t) : 0u;
+// stage tile `tile` tokens into sTok with 4-byte cp.async (regions are not 16-B aligned)
+__device__ __forceinline__ void stage_tokens(const uint32_t *__restrict__ rt, int32_t len, int32_t tile,
+                                             uint32_t *sTok, int ptid) {
+    const int32_t base = tile * RG_TILE;
+    for (int i = ptid; i < RG_TILE; i += RG_PRODUCERS * 32) {
+        if (base + i < len) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sTok + i)),
+                         "l"(rt + base + i)
+                         : "memory");
+        }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 // G_t for tokens [tile_start, tile_start + RG_TILE) of a region into sGdst.
-__device__ __forceinline__ void produce_tile(const uint32_t (&tk)[RG_PER], int32_t len,
-                                             int32_t tile_start, const uint64_t *__restrict__ gear,
-                                             uint64_t *sGdst, const uint64_t *sGprev,
-                                             uint64_t *sS31, int pw, int lane) {
+__device__ __forceinline__ void produce_tile(const uint32_t *sTok, int32_t len, int32_t tile_start,
+                                             const uint64_t *__restrict__ gear, uint64_t *sGdst,
+                                             const uint64_t *sGprev, uint64_t *sS31, int pw, int lane) {
     uint64_t g[RG_PER];
 #pragma unroll
     for (int q = 0; q < RG_PER; ++q) {
         const int c = pw + q * RG_PRODUCERS;
         const int32_t t = tile_start + c * 32 + lane;
-        g[q] = (c < RG_SUB && t < len) ? __ldg(gear + (tk[q] & 0xFFFFu)) : 0ULL;
+        g[q] = (c < RG_SUB && t < len) ? __ldg(gear + (sTok[c * 32 + lane] & 0xFFFFu)) : 0ULL;
     }
 #pragma unroll
     for (int q = 0; q < RG_PER; ++q) {
@@ -175,25 +181,22 @@ __device__ __forceinline__ void produce_tile(const uint32_t (&tk)[RG_PER], int32
     }
 }
 
-// chain warp: m_t = msb(h_t), h_t = G_t + B_t, over one tile; writes the
-// candidate words ((h & mask) == 0, chunking.py:121) to sCand[step].
-__device__ __forceinline__ void chain_tile(const uint64_t *sG, unsigned *sCand, int32_t tile_start,
-                                           int32_t len, uint32_t mask, uint32_t &Blo, uint32_t &Bhi,
-                                           int lane) {
+// chain warp: M_s = ballot(m_t) for the 32 tokens of each step of one tile.
+// sBm[s] = brev(M_s) is the low word of B after step s (bit 31-i = m_i).
+__device__ __forceinline__ void chain_tile(const uint64_t *sG, uint32_t *sBm, int32_t tile_start,
+                                           int32_t len, uint32_t &Blo, uint32_t &Bhi, int lane) {
     const int nsteps = min(RG_SUB, (len - tile_start + 31) / 32);
-    unsigned my_cand = 0;  // lane s keeps the candidate word of step s
-    uint64_t Gn = sG[lane];
+    uint32_t Ghn = (uint32_t)(sG[lane] >> 32);
     for (int s = 0; s < nsteps; ++s) {
-        const uint64_t G = Gn;
-        if (s + 1 < nsteps) Gn = sG[(s + 1) * 32 + lane];
-        const bool valid = tile_start + 32 * s + lane < len;
-        const uint32_t Glo = (uint32_t)G, Ghi = (uint32_t)(G >> 32);
-        const uint32_t Xlo = Blo << lane;                       // (B << j) low word
-        const uint32_t Xhi = __funnelshift_l(Blo, Bhi, lane);   // (B << j) high word
-        const uint32_t hs = Ghi + Xhi;  // high word of h up to a carry c in {0, 1, 2}
+        const uint32_t Ghi = Ghn;
+        if (s + 1 < nsteps) Ghn = (uint32_t)(sG[(s + 1) * 32 + lane] >> 32);
+        const uint32_t hs = Ghi + __funnelshift_l(Blo, Bhi, lane);  // high word of h, carry c in {0,1,2} pending
         unsigned M = __ballot_sync(0xffffffffu, hs >> 31);
+        const bool valid = tile_start + 32 * s + lane < len;
         const unsigned und = __ballot_sync(0xffffffffu, valid && (hs & 0x7FFFFFFEu) == 0x7FFFFFFEu);
+        uint32_t nb = __brev(M);
         if (und) {  // exact resolution of ambiguous lanes, in lane order (~2^-30 per lane)
+            const uint64_t G = sG[s * 32 + lane];
             const uint64_t lo = G + ((((uint64_t)Bhi << 32) | Blo) << lane);
             unsigned u2 = und;
             while (u2) {
@@ -207,15 +210,40 @@ __device__ __forceinline__ void chain_tile(const uint64_t *sG, unsigned *sCand, 
                 M = (M & ~(1u << jj)) | (mb << jj);
                 u2 &= u2 - 1;
             }
+            nb = __brev(M);
         }
         Bhi = Blo;
-        Blo = __brev(M);
-        // low word of h: G_lo + (B << j)_lo + sum_{i<j} m_i << (j-1-i)
-        const uint32_t hlo = Glo + Xlo + ((Blo >> (31 - lane)) >> 1);
+        Blo = nb;
+        if (lane == 0) sBm[s] = nb;
+    }
+}
+
+// cand warp: candidate words ((h & mask) == 0, chunking.py:121) of one tile.
+// Step s needs B before it: low word sBm[s-1], high word sBm[s-2] (previous
+// tile's last words in Bprev0/Bprev1 at s = 0, 1).
+__device__ __forceinline__ void cand_tile(const uint64_t *sG, const uint32_t *sBm, unsigned *sCand,
+                                          int32_t tile_start, int32_t len, uint32_t mask,
+                                          uint32_t &Bprev_lo, uint32_t &Bprev_hi, int lane) {
+    const int nsteps = min(RG_SUB, (len - tile_start + 31) / 32);
+    unsigned my_cand = 0;
+#pragma unroll 4
+    for (int s = 0; s < nsteps; ++s) {
+        const uint32_t b_lo = s >= 1 ? sBm[s - 1] : Bprev_lo;  // B before step s (low word)
+        const uint32_t mnew = sBm[s];                          // brev(M_s)
+        const uint32_t Glo = (uint32_t)sG[s * 32 + lane];
+        const uint32_t hlo = Glo + (b_lo << lane) + ((mnew >> (31 - lane)) >> 1);
+        const bool valid = tile_start + 32 * s + lane < len;
         const unsigned cand = __ballot_sync(0xffffffffu, valid && (hlo & mask) == 0);
         if (lane == s) my_cand = cand;
     }
     sCand[lane] = lane < nsteps ? my_cand : 0u;
+    if (nsteps >= 2) {
+        Bprev_hi = sBm[nsteps - 2];
+        Bprev_lo = sBm[nsteps - 1];
+    } else if (nsteps == 1) {
+        Bprev_hi = Bprev_lo;
+        Bprev_lo = sBm[0];
+    }
 }
 
 struct ChunkSink {
@@ -269,8 +297,10 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
                   int32_t k, int32_t min_size, int32_t max_size, int32_t *__restrict__ st_start,
                   int32_t *__restrict__ st_len, uint8_t *__restrict__ st_forced,
                   uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count, int dbg) {
-    __shared__ uint64_t sG[2][RG_TILE];
+    __shared__ uint64_t sG[3][RG_TILE];
+    __shared__ uint32_t sTok[3][RG_TILE];
     __shared__ uint64_t sS31[RG_SUB];
+    __shared__ uint32_t sBm[2][RG_SUB];
     __shared__ unsigned sCand[2][RG_SUB];
     __shared__ int32_t sCount;
     const int64_t r = blockIdx.x;
@@ -283,36 +313,42 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
     const ChunkSink sink{st_start, st_len, st_forced, R.cap_off, (int32_t)(R.tok_begin - R.stream_begin)};
     const int ntiles = (R.len + RG_TILE - 1) / RG_TILE;
 
-    uint32_t Blo = 0, Bhi = 0;  // chain state: the previous 64 MSBs
-    int32_t start = 0, nch = 0;  // walker state
-    uint32_t tk[RG_PER];         // producer: tokens of the tile being produced
-    const int pw = warp - 2;
-    if (warp >= 2) load_tile_tokens(rt, R.len, 0, pw, lane, tk);
+    uint32_t Blo = 0, Bhi = 0;          // chain: the previous 64 MSBs
+    uint32_t Cprev_lo = 0, Cprev_hi = 0;  // cand: B words at the end of the previous tile
+    int32_t start = 0, nch = 0;         // walker
+    const int pw = warp - 3, ptid = threadIdx.x - 96;
+    if (warp >= 3) {
+        stage_tokens(rt, R.len, 0, sTok[0], ptid);
+        stage_tokens(rt, R.len, 1, sTok[1], ptid);
+    }
     long long t_work = 0, t_all = clock64();
-    for (int i = 0; i <= ntiles + 1; ++i) {
+    for (int i = 0; i <= ntiles + 2; ++i) {
         const long long t0 = clock64();
         if (warp == 0) {
             if (i >= 1 && i <= ntiles)
-                chain_tile(sG[(i - 1) & 1], sCand[(i - 1) & 1], (i - 1) * RG_TILE, R.len, mask, Blo, Bhi, lane);
+                chain_tile(sG[(i - 1) % 3], sBm[(i - 1) & 1], (i - 1) * RG_TILE, R.len, Blo, Bhi, lane);
         } else if (warp == 1) {
-            if (i >= 2)
-                walk_tile(sCand[i & 1], (i - 2) * RG_TILE, R.len, min_size, max_size, t_pin, start, nch,
-                          sink, lane);
+            if (i >= 2 && i <= ntiles + 1)
+                cand_tile(sG[(i - 2) % 3], sBm[i & 1], sCand[i & 1], (i - 2) * RG_TILE, R.len, mask,
+                          Cprev_lo, Cprev_hi, lane);
+        } else if (warp == 2) {
+            if (i >= 3)
+                walk_tile(sCand[(i - 3) & 1], (i - 3) * RG_TILE, R.len, min_size, max_size, t_pin, start,
+                          nch, sink, lane);
         } else if (i < ntiles) {
-            uint32_t tkn[RG_PER];
-            if (i + 1 < ntiles) load_tile_tokens(rt, R.len, (i + 1) * RG_TILE, pw, lane, tkn);
-            produce_tile(tk, R.len, i * RG_TILE, gear, sG[i & 1], i ? sG[(i - 1) & 1] : nullptr, sS31,
-                         pw, lane);
-#pragma unroll
-            for (int q = 0; q < RG_PER; ++q) tk[q] = tkn[q];
+            stage_tokens(rt, R.len, i + 2, sTok[(i + 2) % 3], ptid);  // empty group past the end
+            asm volatile("cp.async.wait_group 2;" ::: "memory");       // tile i's tokens landed
+            producer_bar();
+            produce_tile(sTok[i % 3], R.len, i * RG_TILE, gear, sG[i % 3], i ? sG[(i - 1) % 3] : nullptr,
+                         sS31, pw, lane);
         }
         t_work += clock64() - t0;
         __syncthreads();
     }
-    if (dbg && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64) && R.len > 10000)  // IRM_CDC_DEBUG=1
+    if (dbg && (threadIdx.x & 31) == 0 && threadIdx.x < 128 && R.len > 10000)  // IRM_CDC_DEBUG=1
         printf("region %lld warp %d work %lld total %lld tiles %d\n", (long long)r, warp, t_work,
                clock64() - t_all, ntiles);
-    if (warp == 1) {
+    if (warp == 2) {
         if (start < R.len) {  // only when the region ends at the stream end
             sink.emit(lane, nch, start, R.len - start, IRM_FORCED_STREAM_END);
             ++nch;
@@ -328,6 +364,8 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
     const int64_t cap = R.cap_off;
     for (int32_t c = threadIdx.x; c < sCount; c += RG_THREADS)
         st_fp[cap + c] = xxh64_words(sbase + st_start[cap + c], st_len[cap + c], 0);
+    if (dbg && threadIdx.x == 0 && R.len > 10000)
+        printf("region %lld with hash %lld\n", (long long)r, clock64() - t_all);
 }
 
 __global__ void __launch_bounds__(PLAN_BLOCK)
