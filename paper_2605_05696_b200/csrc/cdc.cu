@@ -182,24 +182,41 @@ __device__ __forceinline__ void produce_tile(const uint32_t *sTok, int32_t len, 
     }
 }
 
-// chain warp: M_s = ballot(m_t) for the 32 tokens of each step of one tile.
-// sBm[s] = brev(M_s) is the low word of B after step s (bit 31-i = m_i).
+// chain warp: sBm[s] = W_s, the low word of B after step s of one tile
+// (bit 31-i = m_i of the step's token i). Lane L handles token j = 31 - L, so
+// the ballot itself is the bit-reversed word and the loop-carried path is
+// funnel-shift -> add -> vote (~30 cycles per 32 tokens, microbenchmarked:
+// a BREV or an ambiguity branch on the path costs ~20-25 cycles each).
+// Ambiguous lanes (high word at a carry boundary, ~2^-30 per token) are only
+// accumulated; a tile that saw one is recomputed exactly (64-bit, lane order).
 __device__ __forceinline__ void chain_tile(const uint64_t *sG, uint32_t *sBm, int32_t tile_start,
                                            int32_t len, uint32_t &Blo, uint32_t &Bhi, int lane) {
     const int nsteps = min(RG_SUB, (len - tile_start + 31) / 32);
-    uint32_t Ghn = (uint32_t)(sG[lane] >> 32);
+    const int j = 31 - lane;
+    const uint32_t Blo0 = Blo, Bhi0 = Bhi;
+    uint32_t myW = 0;  // lane s keeps W_s
+    unsigned und_acc = 0;
+    uint32_t Ghn = (uint32_t)(sG[j] >> 32);
     for (int s = 0; s < nsteps; ++s) {
         const uint32_t Ghi = Ghn;
-        if (s + 1 < nsteps) Ghn = (uint32_t)(sG[(s + 1) * 32 + lane] >> 32);
-        const uint32_t hs = Ghi + __funnelshift_l(Blo, Bhi, lane);  // high word of h, carry c in {0,1,2} pending
-        unsigned M = __ballot_sync(0xffffffffu, hs >> 31);
-        const bool valid = tile_start + 32 * s + lane < len;
-        const unsigned und = __ballot_sync(0xffffffffu, valid && (hs & 0x7FFFFFFEu) == 0x7FFFFFFEu);
-        uint32_t nb = __brev(M);
-        if (und) {  // exact resolution of ambiguous lanes, in lane order (~2^-30 per lane)
-            const uint64_t G = sG[s * 32 + lane];
-            const uint64_t lo = G + ((((uint64_t)Bhi << 32) | Blo) << lane);
-            unsigned u2 = und;
+        if (s + 1 < nsteps) Ghn = (uint32_t)(sG[(s + 1) * 32 + j] >> 32);
+        const uint32_t hs = Ghi + __funnelshift_l(Blo, Bhi, j);  // high word of h, carry c in {0,1,2} pending
+        const unsigned W = __ballot_sync(0xffffffffu, hs >> 31);
+        const bool valid = tile_start + 32 * s + j < len;
+        und_acc |= __ballot_sync(0xffffffffu, valid && (hs & 0x7FFFFFFEu) == 0x7FFFFFFEu);
+        myW = lane == s ? W : myW;
+        Bhi = Blo;
+        Blo = W;
+    }
+    if (und_acc) {  // rare: redo the tile with exact 64-bit arithmetic, lanes in token order
+        Blo = Blo0;
+        Bhi = Bhi0;
+        for (int s = 0; s < nsteps; ++s) {
+            const bool valid = tile_start + 32 * s + lane < len;
+            const uint64_t lo = sG[s * 32 + lane] + ((((uint64_t)Bhi << 32) | Blo) << lane);
+            const uint64_t hi = lo + ((1ULL << lane) - 1);
+            unsigned M = __ballot_sync(0xffffffffu, (unsigned)(lo >> 63));
+            unsigned u2 = __ballot_sync(0xffffffffu, valid && ((lo ^ hi) >> 63));
             while (u2) {
                 const int jj = __ffs(u2) - 1;
                 unsigned mb = 0;
@@ -211,12 +228,13 @@ __device__ __forceinline__ void chain_tile(const uint64_t *sG, uint32_t *sBm, in
                 M = (M & ~(1u << jj)) | (mb << jj);
                 u2 &= u2 - 1;
             }
-            nb = __brev(M);
+            const uint32_t W = __brev(M);
+            myW = lane == s ? W : myW;
+            Bhi = Blo;
+            Blo = W;
         }
-        Bhi = Blo;
-        Blo = nb;
-        if (lane == 0) sBm[s] = nb;
     }
+    sBm[lane] = myW;
 }
 
 // cand warp: candidate words ((h & mask) == 0, chunking.py:121) of one tile.
