@@ -118,11 +118,11 @@ cdc_plan_kernel(const int64_t *__restrict__ stream_off, int32_t n_streams,
 //   walker    (warp 2):      the boundary rule over the candidate words of tile i-3
 // msb(h) is decided on the high 32-bit words alone (the low words carry at
 // most 2 into them); the rare ambiguous lanes are resolved exactly in lane order.
-constexpr int RG_THREADS = 512;
+constexpr int RG_THREADS = 1024;
 constexpr int RG_TILE = 1024;                 // tokens per pipeline tile
 constexpr int RG_SUB = RG_TILE / 32;          // 32-token sub-blocks (chain steps) per tile
-constexpr int RG_PRODUCERS = RG_THREADS / 32 - 3;  // warps 0..12
-constexpr int W_WALK = RG_PRODUCERS, W_CAND = RG_PRODUCERS + 1, W_CHAIN = RG_PRODUCERS + 2;
+constexpr int RG_PRODUCERS = RG_THREADS / 32 - 4;  // warps 0..27
+constexpr int W_WALK = RG_PRODUCERS, W_CAND = RG_PRODUCERS + 1, W_CHAIN = RG_PRODUCERS + 3;
 constexpr int RG_PER = (RG_SUB + RG_PRODUCERS - 1) / RG_PRODUCERS;
 
 __device__ __forceinline__ void producer_bar() {
@@ -195,20 +195,19 @@ __device__ __forceinline__ void chain_tile(const uint64_t *sG, uint32_t *sBm, in
     const int j = 31 - lane;
     const uint32_t Blo0 = Blo, Bhi0 = Bhi;
     uint32_t myW = 0;  // lane s keeps W_s
-    unsigned und_acc = 0;
+    bool amb = false;  // per lane: some step's high word sat at a carry boundary
     uint32_t Ghn = (uint32_t)(sG[j] >> 32);
     for (int s = 0; s < nsteps; ++s) {
         const uint32_t Ghi = Ghn;
         if (s + 1 < nsteps) Ghn = (uint32_t)(sG[(s + 1) * 32 + j] >> 32);
         const uint32_t hs = Ghi + __funnelshift_l(Blo, Bhi, j);  // high word of h, carry c in {0,1,2} pending
         const unsigned W = __ballot_sync(0xffffffffu, hs >> 31);
-        const bool valid = tile_start + 32 * s + j < len;
-        und_acc |= __ballot_sync(0xffffffffu, valid && (hs & 0x7FFFFFFEu) == 0x7FFFFFFEu);
+        amb |= (hs & 0x7FFFFFFEu) == 0x7FFFFFFEu;  // (past-the-end lanes may trigger a harmless redo)
         myW = lane == s ? W : myW;
         Bhi = Blo;
         Blo = W;
     }
-    if (und_acc) {  // rare: redo the tile with exact 64-bit arithmetic, lanes in token order
+    if (__any_sync(0xffffffffu, amb)) {  // rare: redo the tile with exact 64-bit arithmetic, lanes in token order
         Blo = Blo0;
         Bhi = Bhi0;
         for (int s = 0; s < nsteps; ++s) {
@@ -240,29 +239,25 @@ __device__ __forceinline__ void chain_tile(const uint64_t *sG, uint32_t *sBm, in
 // cand warp: candidate words ((h & mask) == 0, chunking.py:121) of one tile.
 // Step s needs B before it: low word sBm[s-1], high word sBm[s-2] (previous
 // tile's last words in Bprev0/Bprev1 at s = 0, 1).
+// Two cand warps split the steps by parity; only B's low word matters for
+// (h & mask) with mask < 2^32.
 __device__ __forceinline__ void cand_tile(const uint64_t *sG, const uint32_t *sBm, unsigned *sCand,
                                           int32_t tile_start, int32_t len, uint32_t mask,
-                                          uint32_t &Bprev_lo, uint32_t &Bprev_hi, int lane) {
+                                          uint32_t &Bprev_lo, int parity, int lane) {
     const int nsteps = min(RG_SUB, (len - tile_start + 31) / 32);
     unsigned my_cand = 0;
 #pragma unroll 4
-    for (int s = 0; s < nsteps; ++s) {
+    for (int s = parity; s < nsteps; s += 2) {
         const uint32_t b_lo = s >= 1 ? sBm[s - 1] : Bprev_lo;  // B before step s (low word)
-        const uint32_t mnew = sBm[s];                          // brev(M_s)
+        const uint32_t mnew = sBm[s];                          // W_s: bit 31-i = m_i
         const uint32_t Glo = (uint32_t)sG[s * 32 + lane];
         const uint32_t hlo = Glo + (b_lo << lane) + ((mnew >> (31 - lane)) >> 1);
         const bool valid = tile_start + 32 * s + lane < len;
         const unsigned cand = __ballot_sync(0xffffffffu, valid && (hlo & mask) == 0);
-        if (lane == s) my_cand = cand;
+        my_cand = lane == s ? cand : my_cand;
     }
-    sCand[lane] = lane < nsteps ? my_cand : 0u;
-    if (nsteps >= 2) {
-        Bprev_hi = sBm[nsteps - 2];
-        Bprev_lo = sBm[nsteps - 1];
-    } else if (nsteps == 1) {
-        Bprev_hi = Bprev_lo;
-        Bprev_lo = sBm[0];
-    }
+    if ((lane & 1) == parity) sCand[lane] = lane < nsteps ? my_cand : 0u;
+    if (nsteps >= 1) Bprev_lo = sBm[nsteps - 1];
 }
 
 struct ChunkSink {
@@ -332,9 +327,9 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
     const ChunkSink sink{st_start, st_len, st_forced, R.cap_off, (int32_t)(R.tok_begin - R.stream_begin)};
     const int ntiles = (R.len + RG_TILE - 1) / RG_TILE;
 
-    uint32_t Blo = 0, Bhi = 0;          // chain: the previous 64 MSBs
-    uint32_t Cprev_lo = 0, Cprev_hi = 0;  // cand: B words at the end of the previous tile
-    int32_t start = 0, nch = 0;         // walker
+    uint32_t Blo = 0, Bhi = 0;  // chain: the previous 64 MSBs
+    uint32_t Cprev_lo = 0;      // cand: B low word at the end of the previous tile
+    int32_t start = 0, nch = 0; // walker
     // role warps take the HIGHEST warp ids: the SMSP arbiter issues
     // highest-warp-id-first, so the chain warp is never starved by producers
     const int pw = warp, ptid = threadIdx.x;
@@ -348,10 +343,10 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
         if (warp == W_CHAIN) {
             if (i >= 1 && i <= ntiles)
                 chain_tile(sG[(i - 1) % 3], sBm[(i - 1) & 1], (i - 1) * RG_TILE, R.len, Blo, Bhi, lane);
-        } else if (warp == W_CAND) {
+        } else if (warp == W_CAND || warp == W_CAND + 1) {
             if (i >= 2 && i <= ntiles + 1)
                 cand_tile(sG[(i - 2) % 3], sBm[i & 1], sCand[i & 1], (i - 2) * RG_TILE, R.len, mask,
-                          Cprev_lo, Cprev_hi, lane);
+                          Cprev_lo, warp - W_CAND, lane);
         } else if (warp == W_WALK) {
             if (i >= 3)
                 walk_tile(sCand[(i - 3) & 1], (i - 3) * RG_TILE, R.len, min_size, max_size, t_pin, start,
@@ -366,9 +361,7 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
         t_work += clock64() - t0;
         __syncthreads();
     }
-    if (dbg && (threadIdx.x & 31) == 0 && (warp >= W_WALK || warp == 0) && R.len > 10000)  // IRM_CDC_DEBUG=1
-        printf("region %lld warp %d work %lld total %lld tiles %d\n", (long long)r, warp, t_work,
-               clock64() - t_all, ntiles);
+    const long long t_loop = clock64() - t_all;
     if (warp == W_WALK) {
         if (start < R.len) {  // only when the region ends at the stream end
             sink.emit(lane, nch, start, R.len - start, IRM_FORCED_STREAM_END);
@@ -380,13 +373,20 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
         }
     }
     __syncthreads();
-    // fingerprints (fingerprint.py:28-30): one thread per chunk, tokens from L2
+    // fingerprints (fingerprint.py:28-30): a quad of lanes per chunk, tokens from L2
     const uint32_t *__restrict__ sbase = tok + R.stream_begin;
     const int64_t cap = R.cap_off;
-    for (int32_t c = threadIdx.x; c < sCount; c += RG_THREADS)
-        st_fp[cap + c] = xxh64_words(sbase + st_start[cap + c], st_len[cap + c], 0);
-    if (dbg && threadIdx.x == 0 && R.len > 10000)
-        printf("region %lld with hash %lld\n", (long long)r, clock64() - t_all);
+    const int n_chunks = sCount;
+    for (int c0 = warp * 8; c0 < n_chunks; c0 += RG_THREADS / 4) {  // warp-uniform trip count
+        const int c = c0 + (lane >> 2);
+        const bool ok = c < n_chunks;
+        const uint64_t h = xxh64_words_quad(sbase + (ok ? st_start[cap + c] : 0), ok ? st_len[cap + c] : 0,
+                                            0, lane);
+        if (ok && (lane & 3) == 0) st_fp[cap + c] = h;
+    }
+    if (dbg && (threadIdx.x & 31) == 0 && (warp >= W_WALK || warp == 0) && R.len > 10000)  // IRM_CDC_DEBUG=1
+        printf("region %lld warp %d work %lld loop %lld with-hash %lld tiles %d\n", (long long)r, warp,
+               t_work, t_loop, clock64() - t_all, ntiles);
 }
 
 __global__ void __launch_bounds__(PLAN_BLOCK)

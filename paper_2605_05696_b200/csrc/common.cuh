@@ -106,6 +106,54 @@ __device__ __forceinline__ uint64_t xxh64_words(const uint32_t *__restrict__ w, 
     return xxh_avalanche(h);
 }
 
+// XXH64 of n 32-bit words computed by the 4 lanes of a quad: lane q of the
+// quad runs accumulator v_{q+1} over every 32-byte stripe (the four lanes of
+// a stripe are independent in XXH64), loads unrolled 4 stripes deep. Every
+// lane of the warp must call this (shuffles), quads with n == 0 included;
+// all 4 lanes of a quad return the hash.
+__device__ __forceinline__ uint64_t xxh64_words_quad(const uint32_t *__restrict__ w, int64_t n,
+                                                     uint64_t seed, int lane) {
+    const int q = lane & 3, qb = lane & ~3;
+    const int64_t stripes = n / 8;
+    uint64_t v = q == 0 ? seed + XP1 + XP2 : q == 1 ? seed + XP2 : q == 2 ? seed : seed - XP1;
+    const uint32_t *__restrict__ p = w + 2 * q;
+    auto rd = [&](int64_t s) -> uint64_t {
+        return (uint64_t)__ldg(p + 8 * s) | ((uint64_t)__ldg(p + 8 * s + 1) << 32);
+    };
+    int64_t s = 0;
+    for (; s + 4 <= stripes; s += 4) {
+        const uint64_t d0 = rd(s), d1 = rd(s + 1), d2 = rd(s + 2), d3 = rd(s + 3);
+        v = xxh_round(v, d0);
+        v = xxh_round(v, d1);
+        v = xxh_round(v, d2);
+        v = xxh_round(v, d3);
+    }
+    for (; s < stripes; ++s) v = xxh_round(v, rd(s));
+    const uint64_t v1 = __shfl_sync(0xffffffffu, v, qb), v2 = __shfl_sync(0xffffffffu, v, qb + 1);
+    const uint64_t v3 = __shfl_sync(0xffffffffu, v, qb + 2), v4 = __shfl_sync(0xffffffffu, v, qb + 3);
+    uint64_t h;
+    if (stripes > 0) {
+        h = rotl64(v1, 1) + rotl64(v2, 7) + rotl64(v3, 12) + rotl64(v4, 18);
+        h = xxh_merge(h, v1);
+        h = xxh_merge(h, v2);
+        h = xxh_merge(h, v3);
+        h = xxh_merge(h, v4);
+    } else {
+        h = seed + XP5;
+    }
+    h += (uint64_t)(4 * n);
+    int64_t i = stripes * 8;
+    for (; i + 2 <= n; i += 2) {
+        h ^= xxh_round(0, (uint64_t)__ldg(w + i) | ((uint64_t)__ldg(w + i + 1) << 32));
+        h = rotl64(h, 27) * XP1 + XP4;
+    }
+    if (i < n) {
+        h ^= (uint64_t)__ldg(w + i) * XP1;
+        h = rotl64(h, 23) * XP2 + XP3;
+    }
+    return xxh_avalanche(h);
+}
+
 // XXH64 over an arbitrary byte span (K2's byte entry point, for the KATs).
 __device__ __forceinline__ uint64_t xxh64_bytes(const uint8_t *__restrict__ p, int64_t len,
                                                 uint64_t seed) {
