@@ -154,18 +154,35 @@ __device__ __forceinline__ void produce_tile(const uint32_t *sTok, int32_t len, 
         const int32_t t = tile_start + c * 32 + lane;
         g[q] = (c < RG_SUB && t < len) ? __ldg(gear + (sTok[c * 32 + lane] & 0xFFFFu)) : 0ULL;
     }
+    // in-block windowed scan S_j = sum_{i<=j} g_i << (j-i), Kogge-Stone through
+    // shared memory: the warp-shuffle unit is left to the chain/cand warps'
+    // votes, which sit on the CTA's critical path
 #pragma unroll
     for (int q = 0; q < RG_PER; ++q) {
         const int c = pw + q * RG_PRODUCERS;
-        if (c >= RG_SUB) break;
-        uint64_t x = g[q];  // in-block windowed scan S_j = sum_{i<=j} g_i << (j-i)
+        if (c < RG_SUB) sGdst[c * 32 + lane] = g[q];
+    }
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += y << d;
+    for (int d = 1; d < 32; d <<= 1) {
+        __syncwarp();
+        uint64_t y[RG_PER];
+#pragma unroll
+        for (int q = 0; q < RG_PER; ++q) {
+            const int c = pw + q * RG_PRODUCERS;
+            y[q] = (c < RG_SUB && lane >= d) ? sGdst[c * 32 + lane - d] : 0ULL;
         }
-        sGdst[c * 32 + lane] = x;
-        if (lane == 31) sS31[c] = x;
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < RG_PER; ++q) {
+            const int c = pw + q * RG_PRODUCERS;
+            g[q] += y[q] << d;
+            if (c < RG_SUB) sGdst[c * 32 + lane] = g[q];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < RG_PER; ++q) {
+        const int c = pw + q * RG_PRODUCERS;
+        if (c < RG_SUB && lane == 31) sS31[c] = g[q];
     }
     producer_bar();
     // carry-in G_{base-1} = G of the previous sub-block's last token:
