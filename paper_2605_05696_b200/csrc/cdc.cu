@@ -358,7 +358,7 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
     for (int i = 0; i <= ntiles + 2; ++i) {
         const long long t0 = clock64();
         if (warp == W_CHAIN) {
-            if (i >= 1 && i <= ntiles)
+            if (i >= 1 && i <= ntiles && !(dbg & 4))
                 chain_tile(sG[(i - 1) % 3], sBm[(i - 1) & 1], (i - 1) * RG_TILE, R.len, Blo, Bhi, lane);
         } else if (warp == W_CAND || warp == W_CAND + 1) {
             if (i >= 2 && i <= ntiles + 1)
@@ -368,7 +368,7 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
             if (i >= 3)
                 walk_tile(sCand[(i - 3) & 1], (i - 3) * RG_TILE, R.len, min_size, max_size, t_pin, start,
                           nch, sink, lane);
-        } else if (i < ntiles) {
+        } else if (i < ntiles && !(dbg & 2)) {
             stage_tokens(rt, R.len, i + 2, sTok[(i + 2) % 3], ptid);  // empty group past the end
             asm volatile("cp.async.wait_group 2;" ::: "memory");       // tile i's tokens landed
             producer_bar();
@@ -558,7 +558,7 @@ extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_
     const int64_t rmax = (int64_t)n_streams + np;
     cdc_region_kernel<<<(unsigned)rmax, RG_THREADS, 0, st>>>(
         tok, w.regions, w.n_regions, gear, mask_exponent, min_size, max_size, w.st_start, w.st_len,
-        w.st_forced, w.st_fp, w.r_count, getenv("IRM_CDC_DEBUG") != nullptr);
+        w.st_forced, w.st_fp, w.r_count, getenv("IRM_CDC_DEBUG") ? atoi(getenv("IRM_CDC_DEBUG")) : 0);
     IRM_LAUNCH_CHECK();
     cdc_offsets_kernel<<<1, PLAN_BLOCK, 0, st>>>(w.n_regions, w.r_count, w.r_out, w.r_first,
                                                  n_streams, chunk_off);
