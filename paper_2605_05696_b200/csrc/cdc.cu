@@ -118,10 +118,10 @@ cdc_plan_kernel(const int64_t *__restrict__ stream_off, int32_t n_streams,
 //   walker    (warp 2):      the boundary rule over the candidate words of tile i-3
 // msb(h) is decided on the high 32-bit words alone (the low words carry at
 // most 2 into them); the rare ambiguous lanes are resolved exactly in lane order.
-constexpr int RG_THREADS = 1024;
+constexpr int RG_THREADS = 512;
 constexpr int RG_TILE = 1024;                 // tokens per pipeline tile
 constexpr int RG_SUB = RG_TILE / 32;          // 32-token sub-blocks (chain steps) per tile
-constexpr int RG_PRODUCERS = RG_THREADS / 32 - 4;  // warps 0..27
+constexpr int RG_PRODUCERS = RG_THREADS / 32 - 4;  // warps 0..11
 constexpr int W_WALK = RG_PRODUCERS, W_CAND = RG_PRODUCERS + 1, W_CHAIN = RG_PRODUCERS + 3;
 constexpr int RG_PER = (RG_SUB + RG_PRODUCERS - 1) / RG_PRODUCERS;
 
