@@ -166,79 +166,44 @@ def run_ours(args):
                for p in packed]
 
     # -------- store + latent pool, populated by the cold request (untimed)
+    from paper_2605_05696_b200.pipeline import ReattachPipeline
+
     store = ops.ChunkStore(max_entries=1 << 16)
     pool_rows = BODY + 2048 * (n_steps + 2)  # body + the novel header/meta chunks of every wave
     pool = torch.randn(LAYERS, pool_rows, CKV + KR, device=dev).to(torch.bfloat16)  # random-init latents
     inv = ops.inv_freq_device(np.power(THETA, -2.0 * np.arange(KR // 2) / KR))
-    out = torch.empty(LAYERS, R * req_stride, CKV + KR, dtype=torch.bfloat16, device=dev)
-    cws = ops.CdcWorkspace()
-    gws = torch.empty(int(N.lib().irm_rotate_gather_workspace_bytes(1 << 16, KR)), dtype=torch.uint8, device=dev)
-    order_base = [0]
-    layout = N.LAYOUT_INTERLEAVED  # DSv2 rotary form
+    max_tok = max(int(p[1][-1]) for p in packed)
+    max_pins = max(int(p[2][-1]) for p in packed)
+    pipe = ReattachPipeline(store, pool, inv, R, max_tok, max_pins, req_stride, layout=N.LAYOUT_INTERLEAVED)
 
-    ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    ev_k4 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    k1_ms, k4_ms = [], []
-
-    def step(inp, timing=False):
-        tok, off, poff, pins, ms = inp
-        if timing:
-            ev_k1[0].record()
-        table = ops.cdc_xxh64(tok, off, poff, pins, 7, 32, 512, True, ws=cws, n_tokens=tok.numel())
-        if timing:
-            ev_k1[1].record()
-        cap = table.start.numel()
-        # chunk -> request via the CSR offsets, all on the device (no host sync)
-        idx = torch.arange(cap, device=dev)
-        req = torch.searchsorted(table.chunk_off[1:], idx, right=True)
-        valid = idx < table.chunk_off[-1]
-        reqc = torch.clamp(req, max=R - 1)
-        p_abs = ms[reqc] + table.start.to(torch.int64)
-        probe = (valid & (p_abs >= CARVE)).to(torch.uint8)
-        order = order_base[0] + idx
-        order_base[0] += cap
-        hit, entry, p_src, row = store.lookup_insert(table.fp, order, p_abs, table.length, probe)
-        is_hit = hit == 1
-        length = torch.where(is_hit, table.length, torch.zeros_like(table.length))
-        src = torch.where(is_hit, row, torch.zeros_like(row))
-        dst = reqc * req_stride + p_abs
-        delta = p_abs - p_src
-        if timing:
-            ev_k4[0].record()
-        ops.rotate_gather(pool, out, src, dst, length, delta, inv, CKV, KR, layout, ws=gws)
-        if timing:
-            ev_k4[1].record()
-        return hit, length
-
-    # cold request: inserts the body (its pool rows hold the random latents)
-    step(dev_in[-1])
+    # cold request wave: inserts the body (its pool rows hold the random latents)
+    pipe.load(*dev_in[-1])
+    pipe.step_eager()
     torch.cuda.synchronize()
+    pipe.capture()  # one CUDA graph per step (+ K1-only / K4-only graphs for component timing)
     for i in range(args.warmup):
-        step(dev_in[i])
+        pipe.load(*dev_in[i])
+        pipe.replay()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
-    # -------- timed region (value): inputs resident in HBM
+    # -------- timed region (value): inputs resident in HBM, one graph replay per wave
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    hit_tok = 0
+    lens = []
     with Clocks(local) as clk:
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0.record()
-        lens = []
         for i in range(args.steps):
-            _, l = step(dev_in[args.warmup + i], timing=True)
-            lens.append(l)
+            pipe.load(*dev_in[args.warmup + i])
+            pipe.replay()
+            lens.append(pipe.length.sum())  # device-side reduction, read after the timed region
         t1.record()
         torch.cuda.synchronize()
     ms_total = t0.elapsed_time(t1)
-    hit_tok = int(sum(int(l.sum().item()) for l in lens))
-    # per-launch K1/K4 durations: re-time each with events on the launch stream
-    for i in range(min(args.steps, 5)):
-        step(dev_in[args.warmup + i], timing=True)
-        torch.cuda.synchronize()
-        k1_ms.append(ev_k1[0].elapsed_time(ev_k1[1]))
-        k4_ms.append(ev_k4[0].elapsed_time(ev_k4[1]))
+    hit_tok = int(torch.stack(lens).sum().item())
     if world > 1:
         t = torch.tensor([ms_total], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -246,27 +211,39 @@ def run_ours(args):
         ht = torch.tensor([hit_tok], device=dev, dtype=torch.int64)
         dist.all_reduce(ht)
         hit_tok = int(ht.item())
-
     value = hit_tok / (ms_total / 1e3)  # whole-job reattached tokens/s
     ms_step = ms_total / args.steps
     tok_per_wave = int(packed[0][1][-1])
 
-    # -------- e2e: through the public C-ABI ops with host buffers
-    e2e_ms = 0.0
+    # -------- per-launch K1 / K4 durations: graph replays between events (no host gaps)
+    def time_graph(g, n=20):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(n):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    pipe.load(*dev_in[args.warmup])
+    pipe.replay()
+    k4_rows = int(pipe.length.sum().item()) * LAYERS
+    k1 = time_graph(pipe.graph_k1)
+    k4 = time_graph(pipe.graph_k4)
+
+    # -------- e2e: the same pipeline fed from pinned host buffers, result read back
     bi = sum(t.numel() * t.element_size() for t in host_in[0])
     bo = 0
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = [torch.empty(pipe.hit.shape, dtype=pipe.hit.dtype, pin_memory=True) for _ in range(args.steps)]
     e0.record()
-    res = []
     for i in range(args.steps):
-        h = host_in[args.warmup + i]
-        inp = tuple(x.to(dev, non_blocking=True) for x in h)
-        hit, length = step(inp)
-        hh = torch.empty(hit.shape, dtype=hit.dtype, pin_memory=True)
-        hh.copy_(hit, non_blocking=True)
-        res.append(hh)
-        bo = hit.numel() * hit.element_size()
+        pipe.load(*host_in[args.warmup + i])  # H2D from pinned memory
+        pipe.replay()
+        res[i].copy_(pipe.hit, non_blocking=True)  # D2H of the per-chunk service result
+        bo = pipe.hit.numel() * pipe.hit.element_size()
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
@@ -277,9 +254,7 @@ def run_ours(args):
     e2e_value = hit_tok / (e2e_ms / 1e3)
 
     # -------- roofline of the dominant kernel (K4) and K1
-    k4 = statistics.median(k4_ms)
-    k1 = statistics.median(k1_ms)
-    rows_per_launch = hit_tok // (world * args.steps) * LAYERS
+    rows_per_launch = k4_rows
     k4_bytes = rows_per_launch * 2 * (CKV + KR) * 2
     k4_gbs = k4_bytes / (k4 / 1e3) / 1e9
     k1_bytes = tok_per_wave * 4 + (tok_per_wave // 128) * 24

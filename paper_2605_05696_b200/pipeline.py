@@ -1,0 +1,126 @@
+"""The warm-serve reattach step as one CUDA graph (B200 production path).
+
+For a wave of requests whose phase-1 prefix lengths ``m`` are known (host
+radix, engine.py:170), one step is
+
+    K1  CDC + xxh64 over every request tail          (irm_cdc_xxh64)
+    K3  first-writer-wins lookup/insert of all chunks (irm_store_lookup_insert)
+        -- carve-out chunks (p < 32) neither probed nor inserted (engine.py:184-196)
+    K4  rotate+gather of every PIC hit chunk into the per-request KV buffer
+        out[l, r * req_stride + p, :] for all layers l (registry.py:146-166)
+
+with no host synchronisation anywhere: every shape is capacity-bounded, the
+chunk -> request map comes from the device CSR offsets, and non-hit chunks
+are masked to zero rows for K4. That makes the whole step capturable as a
+single CUDA graph (no tracing compiler), replayed per wave after the inputs
+are copied into the static buffers.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native as N
+from . import ops
+
+
+class ReattachPipeline:
+    def __init__(self, store: ops.ChunkStore, pool: torch.Tensor, inv_freq: torch.Tensor,
+                 max_requests: int, max_tokens: int, max_pins: int, req_stride: int,
+                 layout: int = N.LAYOUT_INTERLEAVED, mask_exponent: int = 7, min_size: int = 32,
+                 max_size: int = 512, carve: int = 32, ckv_dim: int = 512, kr_dim: int = 64):
+        dev = pool.device
+        self.store, self.pool, self.inv = store, pool, inv_freq
+        self.R, self.req_stride, self.carve = max_requests, req_stride, carve
+        self.params = (mask_exponent, min_size, max_size)
+        self.layout, self.ckv, self.kr = layout, ckv_dim, kr_dim
+        self.max_tokens, self.max_pins = max_tokens, max_pins
+        # static inputs
+        self.tok = torch.zeros(max_tokens, dtype=torch.int32, device=dev)
+        self.stream_off = torch.zeros(max_requests + 1, dtype=torch.int64, device=dev)
+        self.pin_off = torch.zeros(max_requests + 1, dtype=torch.int64, device=dev)
+        self.pins = torch.zeros(max(max_pins, 1), dtype=torch.int64, device=dev)
+        self.m = torch.zeros(max_requests, dtype=torch.int64, device=dev)
+        # static outputs: per-request KV and the chunk service table
+        self.out = torch.empty(pool.shape[0], max_requests * req_stride, pool.shape[2], dtype=pool.dtype,
+                               device=dev)
+        self.cdc_ws = ops.CdcWorkspace()
+        bound = int(N.lib().irm_cdc_chunk_bound(max_tokens, max_requests, max_pins, min_size))
+        self.gather_ws = torch.empty(int(N.lib().irm_rotate_gather_workspace_bytes(bound, kr_dim)),
+                                     dtype=torch.uint8, device=dev)
+        self.order0 = 0
+        self.graph = None
+        self.table = self.hit = self.length = self.delta = None
+
+    # ------------------------------------------------------------ device step
+    def k1(self):
+        k, mn, mx = self.params
+        self.table = ops.cdc_xxh64(self.tok, self.stream_off, self.pin_off, self.pins, k, mn, mx, True,
+                                   ws=self.cdc_ws, n_tokens=self.max_tokens, n_pins=self.max_pins)
+
+    def k3(self):
+        t = self.table
+        cap = t.start.numel()
+        idx = torch.arange(cap, device=t.start.device)
+        req = torch.searchsorted(t.chunk_off[1:], idx, right=True)
+        valid = idx < t.chunk_off[-1]
+        self.reqc = torch.clamp(req, max=self.R - 1)
+        self.p_abs = self.m[self.reqc] + t.start.to(torch.int64)
+        probe = (valid & (self.p_abs >= self.carve)).to(torch.uint8)
+        order = self.order0 + idx
+        self.hit, self.entry, self.p_src, self.row = self.store.lookup_insert(t.fp, order, self.p_abs,
+                                                                              t.length, probe)
+        is_hit = self.hit == 1
+        self.length = torch.where(is_hit, t.length, torch.zeros_like(t.length))
+        self.src = torch.where(is_hit, self.row, torch.zeros_like(self.row))
+        self.dst = self.reqc * self.req_stride + self.p_abs
+        self.delta = self.p_abs - self.p_src
+
+    def k4(self):
+        ops.rotate_gather(self.pool, self.out, self.src, self.dst, self.length, self.delta, self.inv,
+                          self.ckv, self.kr, self.layout, ws=self.gather_ws)
+
+    def step_eager(self):
+        self.k1()
+        self.k3()
+        self.k4()
+
+    # ------------------------------------------------------------ graphs
+    def capture(self, warmup: int = 2):
+        """Capture the step (and K1-only / K4-only graphs for component timing)."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.step_eager()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        pool = torch.cuda.graph_pool_handle()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, pool=pool):
+            self.step_eager()
+        self.graph_k1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph_k1, pool=pool):
+            self.k1()
+        self.graph_k4 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph_k4, pool=pool):
+            self.k4()
+        torch.cuda.synchronize()
+
+    def load(self, tok, stream_off, pin_off, pins, m):
+        """Copy one wave's inputs (device-resident or pinned host) into the static buffers."""
+        n = tok.numel()
+        if n > self.max_tokens or pins.numel() > self.max_pins or m.numel() > self.R:
+            raise ValueError("wave exceeds the pipeline's static capacity")
+        self.tok[:n].copy_(tok, non_blocking=True)
+        r = stream_off.numel()
+        self.stream_off[:r].copy_(stream_off, non_blocking=True)
+        self.pin_off[:r].copy_(pin_off, non_blocking=True)
+        if r < self.R + 1:  # unused request slots are empty streams
+            self.stream_off[r:].copy_(self.stream_off[r - 1:r].expand(self.R + 1 - r))
+            self.pin_off[r:].copy_(self.pin_off[r - 1:r].expand(self.R + 1 - r))
+        self.pins[:pins.numel()].copy_(pins, non_blocking=True)
+        self.m[:m.numel()].copy_(m, non_blocking=True)
+
+    def replay(self):
+        self.graph.replay()
