@@ -150,6 +150,26 @@ int irm_rotate_rows(const void *rows, int64_t row_stride, void *out, int64_t out
  * IRM_ROUND_BF16 (rotary.py:63-87 round_bf16, single RNE incl. subnormals). */
 int irm_round_f64(const double *x, double *y, int64_t n, int32_t mode, irm_stream_t stream);
 
+/* ---- K5: fused absorbed-MLA reattach prefill ----
+ * No reference implementation exists ("deliberate
+ * follow-up"); semantics restated in oracle/mla_ref.py:
+ *   S[r,k] = (q[r,:512] . c_KV[k] + q[r,512:] . R(delta_k) kr_base[k]) * scale
+ *   causal (key k visible to query position P iff k <= P), O = softmax(S) c_KV
+ * q    [n_q, heads, 576] bf16 (absorbed q_nope || rotated q_pe); query i at
+ *      position q_pos0 + i (q_pos0 + n_q <= n_kv)
+ * pool [*, 576] bf16 latent rows (c_KV || kr_base); key k at pool row
+ *      kv_rows[k] (NULL: row k)
+ * kv_chunk [n_kv] chunk of key k and chunk_cs [n_chunks*32] float2 from
+ *      irm_chunk_cossin(): k_r is rotated by R(delta) in shared memory on its
+ *      way to the tensor cores and never written back (NULL: no rotation)
+ * out  [n_q, heads, 512] bf16; lse [n_q, heads] fp32 natural log (nullable) */
+int irm_chunk_cossin(const int64_t *delta, int64_t n_chunks, const double *inv_freq, void *cs,
+                     irm_stream_t stream);
+int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t heads, int64_t q_pos0,
+                             const void *pool, const int32_t *kv_rows, int32_t n_kv,
+                             const int32_t *kv_chunk, const void *chunk_cs, int32_t layout,
+                             float scale, void *out, float *lse, irm_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

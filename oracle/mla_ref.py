@@ -1,0 +1,47 @@
+"""TEST INFRASTRUCTURE ONLY -- fp64 restatement of the fused reattach attention (K5).
+
+No reference implementation exists (the fused
+kernel is a "deliberate follow-up"); parity for K5 is therefore UNPINNED by
+the reference and this oracle restates the semantics from the paper:
+  * absorbed MLA: attention runs on the 512-dim latent
+    c_KV with the 64-dim decoupled rotary key, scores over the 576-wide key;
+  * reattach: the cached k_r is kr_base rotated by
+    R(delta) = R(p - p_src) (rotary.py:98-108 math, fp64 angles);
+  * causal prefill of the query positions q_pos0 .. q_pos0 + n_q - 1.
+Everything in float64 on the CPU from the same bf16 inputs the kernel sees.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+try:
+    from . import oracle as O
+except ImportError:  # pragma: no cover
+    import oracle as O
+
+
+def rotate_kr(kr_base: np.ndarray, delta_per_key: np.ndarray, inv_freq: np.ndarray, interleaved: bool):
+    return O.rotate_rows(kr_base, delta_per_key, inv_freq, interleaved=interleaved)
+
+
+def mla_reattach_ref(q: torch.Tensor, kv: torch.Tensor, q_pos0: int, scale: float,
+                     delta_per_key: np.ndarray | None = None, inv_freq: np.ndarray | None = None,
+                     interleaved: bool = False):
+    """q [n_q, H, 576], kv [n_kv, 576] (c_KV || kr_base). Returns (out [n_q,H,512], lse [n_q,H]) float64."""
+    q64 = q.to(torch.float64).cpu()
+    kv64 = kv.to(torch.float64).cpu().numpy().copy()
+    if delta_per_key is not None:
+        kv64[:, 512:] = rotate_kr(kv64[:, 512:], delta_per_key, inv_freq, interleaved)
+    kvt = torch.from_numpy(kv64)
+    n_q, H, _ = q64.shape
+    n_kv = kvt.shape[0]
+    s = torch.einsum("qhd,kd->qhk", q64, kvt) * scale
+    pos = q_pos0 + torch.arange(n_q).view(n_q, 1, 1)
+    keys = torch.arange(n_kv).view(1, 1, n_kv)
+    s = s.masked_fill(keys > pos, float("-inf"))
+    lse = torch.logsumexp(s, dim=-1)
+    p = torch.exp(s - lse.unsqueeze(-1))
+    out = torch.einsum("qhk,kd->qhd", p, kvt[:, :512])
+    return out, lse

@@ -1,0 +1,403 @@
+// K5: fused absorbed-MLA reattach prefill on tcgen05 / TMEM (sm_100a).
+//
+// Absent from the reference ("R(delta)R(p_src) = R(p), fused in
+// FlashMLA"; PAPER.md:469-476, 788-791 describe the production variant that
+// fuses the rotation into the load path so the rotated k_r never reaches
+// HBM). Semantics, restated in oracle/mla_ref.py:
+//   S[r, k] = (q_c[r] . c_KV[k] + q_pe[r] . R(delta_k) kr_base[k]) * scale
+//   causal: key k visible to the row of query position P iff k <= P
+//   O[r] = softmax_k(S[r, :]) @ c_KV           (512-dim latent output)
+// All heads share the single latent KV head, so rows are (query, head) pairs:
+// one CTA owns 64 rows (4 queries x 16 heads) and streams 64-key KV tiles.
+//
+// Tensor-core mapping (cta_group::1, M = 64):
+//   QK : D = S  [64 x 64]  fp32 in TMEM (the half-subpartition lanes +16)
+//        A = Q  [64 x 576] bf16 smem, K-major SW128 (9 pieces of 64 dims)
+//        B = KV [64 x 576] bf16 smem, K-major SW128; piece 8 (k_r) is
+//            rotated by R(delta) on its way into smem, in fp32 from an fp64
+//            per-chunk angle table -- never written back to HBM
+//   PV : D = O  [64 x 512] fp32 in TMEM (lanes +0, all 512 columns)
+//        A = P  [64 x 64]  bf16 smem (softmax output), K-major SW128
+//        B = V  = the same KV pieces 0..7 read MN-major (keys x dims)
+// Warp roles: 0-3 softmax / O-correction (lazy rescale, threshold 2^8),
+// 4-7 producers (cp.async + rotate), 8 the single-thread MMA issuer.
+#include "common.cuh"
+#include "tcgen05.cuh"
+#include <cuda_bf16.h>
+
+namespace irm {
+namespace mla {
+
+constexpr int BM = 64;           // q-rows per CTA
+constexpr int BN = 64;           // keys per tile
+constexpr int DQK = 576, DV = 512;
+constexpr int NPIECE = 9;        // 64-dim pieces of a 576-wide row
+constexpr int PIECE = BM * 128;  // 8 KB: 64 rows x 128 B
+constexpr int TILE = NPIECE * PIECE;
+constexpr int SMEM_Q = 0, SMEM_KV = TILE, SMEM_P = 3 * TILE, SMEM_BYTES = 3 * TILE + PIECE;
+constexpr int THREADS = 288;
+constexpr uint32_t S_LANE = 16;  // S lives in the upper half-subpartition lanes
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+
+struct Params {
+    const __nv_bfloat16 *q;
+    const __nv_bfloat16 *pool;
+    const int32_t *kv_rows;   // [n_kv] pool row of key k (nullptr: identity)
+    const int32_t *kv_chunk;  // [n_kv] chunk of key k (nullptr: no rotation)
+    const float2 *chunk_cs;   // [n_chunks * 32] (cos, sin)(delta_c * inv_freq[j])
+    __nv_bfloat16 *out;
+    float *lse;
+    int64_t n_rows;           // n_q * heads
+    int32_t heads, n_kv, layout;
+    int64_t q_pos0;
+    float scale_log2;         // softmax scale * log2(e)
+};
+
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {  // SW128 byte offset in a piece
+    return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&v);
+}
+
+// producers: KV tile `t` into `tile` (128 threads)
+__device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int t, int ptid) {
+    const uint32_t base = smem_u32(tile);
+    // c_KV: 64 rows x 64 chunks of 16 B, verbatim
+    for (int i = ptid; i < BN * 64; i += 128) {
+        const int r = i >> 6, c = i & 63;
+        const int k = t * BN + r;
+        const bool ok = k < p.n_kv;
+        const int64_t prow = ok ? (p.kv_rows ? (int64_t)p.kv_rows[k] : (int64_t)k) : 0;
+        cp_async16(base + (c >> 3) * PIECE + swz(r, c & 7), p.pool + prow * DQK + c * 8, ok ? 16u : 0u);
+    }
+    // k_r: load, rotate by R(delta) in fp32, store bf16 (piece 8)
+    const uint32_t rope = base + 8 * PIECE;
+    if (p.layout == IRM_LAYOUT_HALF_SPLIT) {
+        for (int i = ptid; i < BN * 4; i += 128) {  // (row, g): dims j = 8g..8g+7 pair with j + 32
+            const int r = i >> 2, g = i & 3;
+            const int k = t * BN + r;
+            uint4 a = make_uint4(0, 0, 0, 0), b = a;
+            if (k < p.n_kv) {
+                const int64_t prow = p.kv_rows ? (int64_t)p.kv_rows[k] : (int64_t)k;
+                const uint4 *src = reinterpret_cast<const uint4 *>(p.pool + prow * DQK + DV);
+                a = __ldg(src + g);
+                b = __ldg(src + g + 4);
+                if (p.kv_chunk) {
+                    const float2 *cs = p.chunk_cs + (int64_t)p.kv_chunk[k] * 32 + 8 * g;
+                    uint32_t *aw = reinterpret_cast<uint32_t *>(&a), *bw = reinterpret_cast<uint32_t *>(&b);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 c0 = __ldg(cs + 2 * e), c1 = __ldg(cs + 2 * e + 1);
+                        const float l0 = bf_lo(aw[e]), l1 = bf_hi(aw[e]), h0 = bf_lo(bw[e]), h1 = bf_hi(bw[e]);
+                        aw[e] = pack_bf2(l0 * c0.x - h0 * c0.y, l1 * c1.x - h1 * c1.y);
+                        bw[e] = pack_bf2(l0 * c0.y + h0 * c0.x, l1 * c1.y + h1 * c1.x);
+                    }
+                }
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rope + swz(r, g)), "r"(a.x), "r"(a.y),
+                         "r"(a.z), "r"(a.w)
+                         : "memory");
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rope + swz(r, g + 4)), "r"(b.x), "r"(b.y),
+                         "r"(b.z), "r"(b.w)
+                         : "memory");
+        }
+    } else {
+        for (int i = ptid; i < BN * 8; i += 128) {  // (row, c): pairs (2j, 2j+1), j = 4c..4c+3
+            const int r = i >> 3, c = i & 7;
+            const int k = t * BN + r;
+            uint4 a = make_uint4(0, 0, 0, 0);
+            if (k < p.n_kv) {
+                const int64_t prow = p.kv_rows ? (int64_t)p.kv_rows[k] : (int64_t)k;
+                a = __ldg(reinterpret_cast<const uint4 *>(p.pool + prow * DQK + DV) + c);
+                if (p.kv_chunk) {
+                    const float2 *cs = p.chunk_cs + (int64_t)p.kv_chunk[k] * 32 + 4 * c;
+                    uint32_t *aw = reinterpret_cast<uint32_t *>(&a);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 cc = __ldg(cs + e);
+                        const float lo = bf_lo(aw[e]), hi = bf_hi(aw[e]);
+                        aw[e] = pack_bf2(lo * cc.x - hi * cc.y, lo * cc.y + hi * cc.x);
+                    }
+                }
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rope + swz(r, c)), "r"(a.x), "r"(a.y),
+                         "r"(a.z), "r"(a.w)
+                         : "memory");
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    fence_proxy_async_smem();
+}
+
+__global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t bar_q, bar_kv_full[2], bar_kv_empty[2], bar_s_full[2], bar_p_full, bar_o_done;
+    __shared__ uint32_t tmem_base;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = (int64_t)blockIdx.x * BM;
+    const int64_t last_row = min(p.n_rows, row0 + BM) - 1;
+    const int64_t max_pos = p.q_pos0 + last_row / p.heads;
+    const int n_keys = (int)min((int64_t)p.n_kv, max_pos + 1);
+    const int T = (n_keys + BN - 1) / BN;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bar_q, 128);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bar_kv_full[s], 128);
+            mbar_init(&bar_kv_empty[s], 1);
+            mbar_init(&bar_s_full[s], 1);
+        }
+        mbar_init(&bar_p_full, 128);
+        mbar_init(&bar_o_done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 8) tc::tmem_alloc(&tmem_base, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = tmem_base;
+
+    if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------------ producers
+        const int ptid = threadIdx.x - 128;
+        const uint32_t qbase = smem_u32(smem + SMEM_Q);
+        for (int i = ptid; i < BM * 72; i += 128) {
+            const int r = i / 72, c = i % 72;
+            const int64_t grow = row0 + r;
+            const bool ok = grow < p.n_rows;
+            cp_async16(qbase + (c >> 3) * PIECE + swz(r, c & 7), p.q + (ok ? grow : 0) * DQK + c * 8, ok ? 16u : 0u);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        fence_proxy_async_smem();
+        mbar_arrive(&bar_q);
+        for (int t = 0; t < T; ++t) {
+            const int st = t & 1;
+            if (t >= 2) mbar_wait(&bar_kv_empty[st], ((t >> 1) - 1) & 1);
+            load_kv_tile(p, smem + SMEM_KV + st * TILE, t, ptid);
+            mbar_arrive(&bar_kv_full[st]);
+        }
+    } else if (warp == 8) {
+        // ------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc_qk = tc::idesc_bf16(BM, BN, false, false);
+            const uint32_t idesc_pv = tc::idesc_bf16(BM, 256, false, true);
+            const uint32_t q_addr = smem_u32(smem + SMEM_Q), kv_addr = smem_u32(smem + SMEM_KV);
+            const uint32_t p_addr = smem_u32(smem + SMEM_P);
+            mbar_wait(&bar_q, 0);
+            for (int t = 0; t <= T; ++t) {
+                if (t < T) {
+                    const int st = t & 1;
+                    mbar_wait(&bar_kv_full[st], (t >> 1) & 1);
+                    tc::fence_after();
+                    const uint32_t d = tbase + (S_LANE << 16) + st * BN;
+#pragma unroll 1
+                    for (int pc = 0; pc < NPIECE; ++pc) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint64_t a = tc::smem_desc_sw128(q_addr + pc * PIECE + k * 32, 16, 1024);
+                            const uint64_t b = tc::smem_desc_sw128(kv_addr + st * TILE + pc * PIECE + k * 32, 16, 1024);
+                            tc::mma_bf16_ss(d, a, b, idesc_qk, (pc | k) != 0);
+                        }
+                    }
+                    tc::commit(&bar_s_full[st]);
+                }
+                if (t >= 1) {
+                    const int u = t - 1, su = u & 1;
+                    mbar_wait(&bar_p_full, u & 1);
+                    tc::fence_after();
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint64_t a = tc::smem_desc_sw128(p_addr + k * 32, 16, 1024);
+                            const uint64_t b = tc::smem_desc_sw128(kv_addr + su * TILE + 4 * h * PIECE + k * 2048,
+                                                                   PIECE, 1024);
+                            tc::mma_bf16_ss(tbase + h * 256, a, b, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
+                        }
+                    }
+                    tc::commit(&bar_kv_empty[su]);
+                    tc::commit(&bar_o_done);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------ softmax / correction (warps 0-3)
+        const int w = warp;
+        const int L = (lane >> 2) + 8 * (lane & 1);  // TMEM lane within the 16-lane group
+        const int b = (lane >> 1) & 1;               // column parity of this thread
+        const int r = 16 * w + L;                    // tile row
+        const int64_t grow = row0 + r;
+        const bool row_ok = grow < p.n_rows;
+        const int64_t qpos = p.q_pos0 + (row_ok ? grow / p.heads : 0);
+        const uint32_t s_lane = tbase + ((uint32_t)(32 * w) + S_LANE << 16);
+        const uint32_t o_lane = tbase + ((uint32_t)(32 * w) << 16);
+        const uint32_t p_base = smem_u32(smem + SMEM_P);
+        float m = -INFINITY, l = 0.f;
+        for (int t = 0; t < T; ++t) {
+            const int st = t & 1;
+            mbar_wait(&bar_s_full[st], (t >> 1) & 1);
+            tc::fence_after();
+            uint32_t v[32];
+            tc::ld_16x64b_x32(s_lane + st * BN, v);
+            tc::wait_ld();
+            float s[32];
+            float mt = -INFINITY;
+            const int64_t kbase = (int64_t)t * BN + b;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int64_t key = kbase + 2 * i;
+                const bool ok = row_ok && key <= qpos && key < p.n_kv;
+                s[i] = ok ? __uint_as_float(v[i]) * p.scale_log2 : -INFINITY;
+                mt = fmaxf(mt, s[i]);
+            }
+            mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+            float alpha = 1.f;
+            const float m_new = fmaxf(m, mt);
+            if (m_new > m + RESCALE_THRESHOLD) {  // lazy rescale: only when the max grows by > 2^8
+                alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
+                m = m_new;
+            }
+            float lsum = 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                s[i] = (s[i] == -INFINITY) ? 0.f : exp2f(s[i] - m);
+                lsum += s[i];
+            }
+            lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+            l = l * alpha + lsum;
+            // pack P: pairs of adjacent keys, thread b = 0 takes keys 0..31, b = 1 keys 32..63
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const float other = __shfl_xor_sync(0xffffffffu, s[i], 2);
+                const uint32_t pr = b == 0 ? pack_bf2(s[i], other) : pack_bf2(other, s[i]);
+                if ((i >> 4) == b) pk[i & 15] = pr;
+            }
+            if (t >= 1) {  // PV(t-1) has finished: O is stable and the P tile is free
+                mbar_wait(&bar_o_done, (t - 1) & 1);
+                tc::fence_after();
+                if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+                    for (int c = 0; c < DV / 64; ++c) {
+                        uint32_t o[32];
+                        tc::ld_16x64b_x32(o_lane + c * 64, o);
+                        tc::wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                        tc::st_16x64b_x32(o_lane + c * 64, o);
+                    }
+                    tc::wait_st();
+                }
+            }
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(p_base + swz(r, 4 * b + q4)),
+                             "r"(pk[4 * q4]), "r"(pk[4 * q4 + 1]), "r"(pk[4 * q4 + 2]), "r"(pk[4 * q4 + 3])
+                             : "memory");
+            }
+            fence_proxy_async_smem();
+            tc::fence_before();
+            mbar_arrive(&bar_p_full);
+        }
+        // epilogue: O / l -> bf16, lse
+        mbar_wait(&bar_o_done, (T - 1) & 1);
+        tc::fence_after();
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+        for (int c = 0; c < DV / 64; ++c) {
+            uint32_t o[32];
+            tc::ld_16x64b_x32(o_lane + c * 64, o);
+            tc::wait_ld();
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const float mine = __uint_as_float(o[i]) * inv_l;
+                const float other = __shfl_xor_sync(0xffffffffu, mine, 2);
+                const uint32_t pr = b == 0 ? pack_bf2(mine, other) : pack_bf2(other, mine);
+                if ((i >> 4) == b) pk[i & 15] = pr;
+            }
+            if (row_ok) {
+                uint4 *dst = reinterpret_cast<uint4 *>(p.out + grow * DV + c * 64 + 32 * b);
+                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                dst[2] = make_uint4(pk[8], pk[9], pk[10], pk[11]);
+                dst[3] = make_uint4(pk[12], pk[13], pk[14], pk[15]);
+            }
+        }
+        if (row_ok && b == 0 && p.lse) p.lse[grow] = (m + log2f(l)) * 0.69314718055994531f;
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == 8) tc::tmem_dealloc(tbase, 512);
+}
+
+__global__ void cossin_kernel(const int64_t *__restrict__ delta, int64_t n_chunks,
+                              const double *__restrict__ inv_freq, float2 *__restrict__ cs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_chunks * 32) return;
+    double s, c;
+    sincos((double)delta[i / 32] * inv_freq[i % 32], &s, &c);  // fp64 angle (|delta| up to 2^20)
+    cs[i] = make_float2((float)c, (float)s);
+}
+
+}  // namespace mla
+}  // namespace irm
+
+using namespace irm;
+
+extern "C" int irm_chunk_cossin(const int64_t *delta, int64_t n_chunks, const double *inv_freq, void *cs,
+                                irm_stream_t stream) {
+    IRM_REQUIRE(n_chunks >= 0, "n_chunks must be >= 0");
+    if (n_chunks == 0) return IRM_OK;
+    IRM_REQUIRE(delta && inv_freq && cs, "null pointer");
+    mla::cossin_kernel<<<(unsigned)((n_chunks * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        delta, n_chunks, inv_freq, (float2 *)cs);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t heads, int64_t q_pos0,
+                                        const void *pool, const int32_t *kv_rows, int32_t n_kv,
+                                        const int32_t *kv_chunk, const void *chunk_cs, int32_t layout,
+                                        float scale, void *out, float *lse, irm_stream_t stream) {
+    IRM_REQUIRE(n_q >= 0 && heads >= 1 && n_kv >= 1 && q_pos0 >= 0, "bad sizes");
+    IRM_REQUIRE(q_pos0 + n_q <= (int64_t)n_kv, "queries must be positions < n_kv (q_pos0 + n_q <= n_kv)");
+    IRM_REQUIRE(layout == IRM_LAYOUT_HALF_SPLIT || layout == IRM_LAYOUT_INTERLEAVED, "bad layout");
+    IRM_REQUIRE(!kv_chunk || chunk_cs, "kv_chunk requires chunk_cs");
+    if (n_q == 0) return IRM_OK;
+    IRM_REQUIRE(q && pool && out, "null pointer");
+    IRM_REQUIRE((((uintptr_t)q | (uintptr_t)pool | (uintptr_t)out) & 15) == 0, "16-byte alignment required");
+    mla::Params p{};
+    p.q = (const __nv_bfloat16 *)q;
+    p.pool = (const __nv_bfloat16 *)pool;
+    p.kv_rows = kv_rows;
+    p.kv_chunk = kv_chunk;
+    p.chunk_cs = (const float2 *)chunk_cs;
+    p.out = (__nv_bfloat16 *)out;
+    p.lse = lse;
+    p.n_rows = n_q * heads;
+    p.heads = heads;
+    p.n_kv = n_kv;
+    p.layout = layout;
+    p.q_pos0 = q_pos0;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    const int smem = mla::SMEM_BYTES + 1024;
+    IRM_CUDA_CHECK(cudaFuncSetAttribute(mla::mla_reattach_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t grid = (p.n_rows + mla::BM - 1) / mla::BM;
+    mla::mla_reattach_kernel<<<(unsigned)grid, mla::THREADS, smem, (cudaStream_t)stream>>>(p);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}

@@ -257,3 +257,37 @@ class ChunkStore:
         if c[2]:
             raise RuntimeError(f"chunk store overflow (flags {c[2]}): raise max_entries")
         return c[0], c[1], c[2]
+
+
+# ------------------------------------------------------------------ K5: fused MLA reattach prefill
+def chunk_cossin(delta: torch.Tensor, inv_freq: torch.Tensor) -> torch.Tensor:
+    """Per-chunk (cos, sin)(delta * inv_freq[j]) from fp64 angles -> float32 [n_chunks, 32, 2]."""
+    n = delta.numel()
+    cs = torch.empty(max(n, 1), inv_freq.numel(), 2, dtype=torch.float32, device=delta.device)
+    if n:
+        N.check(N.lib().irm_chunk_cossin(N.ptr(delta.contiguous()), n, N.ptr(inv_freq), N.ptr(cs),
+                                         N.stream_ptr()), "irm_chunk_cossin")
+    return cs[:n]
+
+
+def mla_reattach_prefill(q: torch.Tensor, pool: torch.Tensor, n_kv: int, q_pos0: int, scale: float,
+                         kv_rows: torch.Tensor | None = None, kv_chunk: torch.Tensor | None = None,
+                         chunk_cs: torch.Tensor | None = None, layout: int = N.LAYOUT_HALF_SPLIT,
+                         out: torch.Tensor | None = None, lse: torch.Tensor | None = None):
+    """K5: absorbed-MLA causal prefill over the 576-wide latent key with the
+    reattach rotation of k_r fused into the shared-memory load.
+
+    q [n_q, H, 576] bf16; pool [rows, 576] bf16; returns (out [n_q, H, 512] bf16, lse [n_q, H] fp32).
+    """
+    assert q.dtype == torch.bfloat16 and pool.dtype == torch.bfloat16 and q.shape[-1] == 576
+    q = q.contiguous()
+    n_q, heads = q.shape[0], q.shape[1]
+    if out is None:
+        out = torch.empty(n_q, heads, 512, dtype=torch.bfloat16, device=q.device)
+    if lse is None:
+        lse = torch.empty(n_q, heads, dtype=torch.float32, device=q.device)
+    rc = N.lib().irm_mla_reattach_prefill(
+        N.ptr(q), n_q, heads, q_pos0, N.ptr(pool), N.ptr(kv_rows), n_kv, N.ptr(kv_chunk), N.ptr(chunk_cs),
+        layout, float(scale), N.ptr(out), N.ptr(lse), N.stream_ptr())
+    N.check(rc, "irm_mla_reattach_prefill")
+    return out, lse

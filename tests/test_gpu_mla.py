@@ -1,0 +1,95 @@
+"""GPU parity: K5 fused MLA reattach prefill (tcgen05/TMEM) vs the fp64 oracle
+(oracle/mla_ref.py) on the same bf16 inputs.
+
+Tolerance (BASELINE.json north_star): fused attention output within the
+paper's 4.7e-3 relative L2; lse within 2e-2 absolute.
+K5 parity is unpinned by the reference (no reference implementation exists)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from oracle.mla_ref import mla_reattach_ref
+
+pytestmark = pytest.mark.gpu
+TOL = 4.7e-3
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2605_05696_b200 import _native as N, ops
+
+    return ops, N
+
+
+def run_case(ops, N, n_kv, n_q, heads=16, q_pos0=None, rotate=False, paged=False, layout=0, q_gain=1.0, seed=0,
+             theta=1e4):
+    rng = np.random.default_rng(seed)
+    q_pos0 = n_kv - n_q if q_pos0 is None else q_pos0
+    q = (torch.from_numpy(rng.standard_normal((n_q, heads, 576)) * q_gain)).to("cuda", torch.bfloat16)
+    kv = torch.from_numpy(rng.standard_normal((n_kv, 576))).to("cuda", torch.bfloat16)
+    scale = 192 ** -0.5
+    kv_rows = kv_chunk = cs = None
+    pool = kv
+    delta_per_key = inv = None
+    if paged:
+        perm = rng.permutation(n_kv + 37)[:n_kv]
+        pool = torch.zeros(n_kv + 37, 576, dtype=torch.bfloat16, device="cuda")
+        pool[torch.from_numpy(perm).cuda()] = kv
+        kv_rows = torch.from_numpy(perm.astype(np.int32)).cuda()
+    if rotate:
+        bounds = np.sort(rng.choice(np.arange(1, n_kv), size=min(n_kv - 1, max(1, n_kv // 40)), replace=False))
+        chunk_of_key = np.searchsorted(bounds, np.arange(n_kv), side="right").astype(np.int32)
+        n_chunks = int(chunk_of_key.max()) + 1
+        deltas = rng.integers(-(2**17), 2**17, size=n_chunks).astype(np.int64)
+        deltas[0] = 0
+        inv = O.make_inv_freq(theta)
+        cs = ops.chunk_cossin(torch.from_numpy(deltas).cuda(), ops.inv_freq_device(inv))
+        kv_chunk = torch.from_numpy(chunk_of_key).cuda()
+        delta_per_key = deltas[chunk_of_key]
+    out, lse = ops.mla_reattach_prefill(q, pool, n_kv, q_pos0, scale, kv_rows=kv_rows, kv_chunk=kv_chunk,
+                                        chunk_cs=cs, layout=layout)
+    torch.cuda.synchronize()
+    ref, ref_lse = mla_reattach_ref(q, kv, q_pos0, scale, delta_per_key, inv, interleaved=bool(layout))
+    got = out.to(torch.float64).cpu()
+    err = float((got - ref).norm() / ref.norm())
+    row_err = ((got - ref).norm(dim=-1) / ref.norm(dim=-1).clamp_min(1e-30)).max().item()
+    lse_err = float((lse.cpu().double() - ref_lse).abs().max())
+    return err, row_err, lse_err
+
+
+@pytest.mark.parametrize("n_kv,n_q", [(64, 4), (300, 50), (1000, 1000), (4096, 256)])
+def test_mla_plain(ops, n_kv, n_q):
+    o, N = ops
+    err, row_err, lse_err = run_case(o, N, n_kv, n_q)
+    assert err <= TOL and row_err <= 2 * TOL and lse_err <= 2e-2, (err, row_err, lse_err)
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("paged", [False, True])
+def test_mla_reattach_rotation(ops, layout, paged):
+    o, N = ops
+    err, row_err, lse_err = run_case(o, N, 2048, 128, rotate=True, paged=paged, layout=layout, seed=3 + layout)
+    assert err <= TOL and row_err <= 2 * TOL and lse_err <= 2e-2, (err, row_err, lse_err)
+
+
+def test_mla_rescale_stress(ops):
+    """Large score magnitudes force repeated max increases (lazy O rescale path)."""
+    o, N = ops
+    err, row_err, lse_err = run_case(o, N, 3000, 64, q_gain=6.0, seed=7)
+    assert err <= TOL and lse_err <= 5e-2, (err, row_err, lse_err)
+
+
+def test_mla_other_heads_and_offsets(ops):
+    o, N = ops
+    err, row_err, lse_err = run_case(o, N, 700, 33, heads=5, q_pos0=100, seed=9)
+    assert err <= TOL and lse_err <= 2e-2, (err, row_err, lse_err)
+
+
+def test_mla_validation(ops):
+    o, N = ops
+    q = torch.zeros(4, 16, 576, dtype=torch.bfloat16, device="cuda")
+    kv = torch.zeros(8, 576, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        o.mla_reattach_prefill(q, kv, 8, 6, 0.1)  # q_pos0 + n_q > n_kv
