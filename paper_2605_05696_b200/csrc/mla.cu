@@ -8,19 +8,20 @@
 //   causal: key k visible to the row of query position P iff k <= P
 //   O[r] = softmax_k(S[r, :]) @ c_KV           (512-dim latent output)
 // All heads share the single latent KV head, so rows are (query, head) pairs:
-// one CTA owns 64 rows (4 queries x 16 heads) and streams 64-key KV tiles.
+// one CTA owns 64 rows (4 queries x 16 heads) and streams 32-key KV tiles
+// through a 4-stage ring.
 //
 // Tensor-core mapping (cta_group::1, M = 64):
-//   QK : D = S  [64 x 64]  fp32 in TMEM (the half-subpartition lanes +16)
+//   QK : D = S  [64 x 32]  fp32 in TMEM (the half-subpartition lanes +16)
 //        A = Q  [64 x 576] bf16 smem, K-major SW128 (9 pieces of 64 dims)
-//        B = KV [64 x 576] bf16 smem, K-major SW128; piece 8 (k_r) is
+//        B = KV [32 x 576] bf16 smem, K-major SW128; piece 8 (k_r) is
 //            rotated by R(delta) on its way into smem, in fp32 from an fp64
 //            per-chunk angle table -- never written back to HBM
 //   PV : D = O  [64 x 512] fp32 in TMEM (lanes +0, all 512 columns)
-//        A = P  [64 x 64]  bf16 smem (softmax output), K-major SW128
+//        A = P  [64 x 32]  bf16 smem (softmax output), K-major SW64
 //        B = V  = the same KV pieces 0..7 read MN-major (keys x dims)
 // Warp roles: 0-3 softmax / O-correction (lazy rescale, threshold 2^8),
-// 4-7 producers (cp.async + rotate), 8 the single-thread MMA issuer.
+// 4-11 producers (cp.async + rotate), 12 the single-thread MMA issuer.
 #include "common.cuh"
 #include "tcgen05.cuh"
 #include <cuda_bf16.h>
@@ -28,15 +29,21 @@
 namespace irm {
 namespace mla {
 
-constexpr int BM = 64;           // q-rows per CTA
-constexpr int BN = 64;           // keys per tile
+constexpr int BM = 64;               // q-rows per CTA
+constexpr int BN = 32;               // keys per KV tile
+constexpr int NST = 4;               // KV ring stages
 constexpr int DQK = 576, DV = 512;
-constexpr int NPIECE = 9;        // 64-dim pieces of a 576-wide row
-constexpr int PIECE = BM * 128;  // 8 KB: 64 rows x 128 B
-constexpr int TILE = NPIECE * PIECE;
-constexpr int SMEM_Q = 0, SMEM_KV = TILE, SMEM_P = 3 * TILE, SMEM_BYTES = 3 * TILE + PIECE;
-constexpr int THREADS = 288;
-constexpr uint32_t S_LANE = 16;  // S lives in the upper half-subpartition lanes
+constexpr int NPIECE = 9;            // 64-dim pieces of a 576-wide row
+constexpr int QPIECE = BM * 128;     // 8 KB
+constexpr int KPIECE = BN * 128;     // 4 KB
+constexpr int KTILE = NPIECE * KPIECE;
+constexpr int PTILE = BM * BN * 2;   // 4 KB, 64-byte rows (SW64)
+constexpr int SMEM_Q = 0, SMEM_KV = NPIECE * QPIECE, SMEM_P = SMEM_KV + NST * KTILE;
+constexpr int SMEM_BYTES = SMEM_P + 2 * PTILE;
+constexpr int N_PROD = 256;          // producer threads (warps 4..11)
+constexpr int W_MMA = 12;
+constexpr int THREADS = 32 * (W_MMA + 1);
+constexpr uint32_t S_LANE = 16;      // S lives in the upper half-subpartition lanes
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 struct Params {
@@ -53,12 +60,19 @@ struct Params {
     float scale_log2;         // softmax scale * log2(e)
 };
 
-__device__ __forceinline__ uint32_t swz(int row, int chunk) {  // SW128 byte offset in a piece
+__device__ __forceinline__ uint32_t swz128(int row, int chunk) {  // SW128 byte offset (128-B rows)
     return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ uint32_t swz64(int row, int chunk) {   // SW64 byte offset (64-B rows)
+    return (uint32_t)(row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4));
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
 }
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -68,70 +82,67 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
     return *reinterpret_cast<uint32_t *>(&v);
 }
 
-// producers: KV tile `t` into `tile` (128 threads)
+// producers: KV tile `t` into `tile` (N_PROD threads)
 __device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int t, int ptid) {
     const uint32_t base = smem_u32(tile);
-    // c_KV: 64 rows x 64 chunks of 16 B, verbatim
-    for (int i = ptid; i < BN * 64; i += 128) {
+    // c_KV: BN rows x 64 chunks of 16 B, verbatim
+#pragma unroll 4
+    for (int i = ptid; i < BN * 64; i += N_PROD) {
         const int r = i >> 6, c = i & 63;
         const int k = t * BN + r;
         const bool ok = k < p.n_kv;
-        const int64_t prow = ok ? (p.kv_rows ? (int64_t)p.kv_rows[k] : (int64_t)k) : 0;
-        cp_async16(base + (c >> 3) * PIECE + swz(r, c & 7), p.pool + prow * DQK + c * 8, ok ? 16u : 0u);
+        const int64_t prow = ok ? (p.kv_rows ? (int64_t)__ldg(p.kv_rows + k) : (int64_t)k) : 0;
+        cp_async16(base + (c >> 3) * KPIECE + swz128(r, c & 7), p.pool + prow * DQK + c * 8, ok ? 16u : 0u);
     }
     // k_r: load, rotate by R(delta) in fp32, store bf16 (piece 8)
-    const uint32_t rope = base + 8 * PIECE;
+    const uint32_t rope = base + 8 * KPIECE;
     if (p.layout == IRM_LAYOUT_HALF_SPLIT) {
-        for (int i = ptid; i < BN * 4; i += 128) {  // (row, g): dims j = 8g..8g+7 pair with j + 32
-            const int r = i >> 2, g = i & 3;
+        if (ptid < BN * 4) {  // (row, g): dims j = 8g..8g+7 pair with j + 32
+            const int r = ptid >> 2, g = ptid & 3;
             const int k = t * BN + r;
             uint4 a = make_uint4(0, 0, 0, 0), b = a;
             if (k < p.n_kv) {
-                const int64_t prow = p.kv_rows ? (int64_t)p.kv_rows[k] : (int64_t)k;
+                const int64_t prow = p.kv_rows ? (int64_t)__ldg(p.kv_rows + k) : (int64_t)k;
                 const uint4 *src = reinterpret_cast<const uint4 *>(p.pool + prow * DQK + DV);
                 a = __ldg(src + g);
                 b = __ldg(src + g + 4);
                 if (p.kv_chunk) {
-                    const float2 *cs = p.chunk_cs + (int64_t)p.kv_chunk[k] * 32 + 8 * g;
+                    const float4 *cs = reinterpret_cast<const float4 *>(p.chunk_cs + (int64_t)__ldg(p.kv_chunk + k) * 32 + 8 * g);
                     uint32_t *aw = reinterpret_cast<uint32_t *>(&a), *bw = reinterpret_cast<uint32_t *>(&b);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const float2 c0 = __ldg(cs + 2 * e), c1 = __ldg(cs + 2 * e + 1);
+                        const float4 c = __ldg(cs + e);  // (cos, sin) of pairs 2e and 2e + 1
                         const float l0 = bf_lo(aw[e]), l1 = bf_hi(aw[e]), h0 = bf_lo(bw[e]), h1 = bf_hi(bw[e]);
-                        aw[e] = pack_bf2(l0 * c0.x - h0 * c0.y, l1 * c1.x - h1 * c1.y);
-                        bw[e] = pack_bf2(l0 * c0.y + h0 * c0.x, l1 * c1.y + h1 * c1.x);
+                        aw[e] = pack_bf2(l0 * c.x - h0 * c.y, l1 * c.z - h1 * c.w);
+                        bw[e] = pack_bf2(l0 * c.y + h0 * c.x, l1 * c.w + h1 * c.z);
                     }
                 }
             }
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rope + swz(r, g)), "r"(a.x), "r"(a.y),
-                         "r"(a.z), "r"(a.w)
-                         : "memory");
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rope + swz(r, g + 4)), "r"(b.x), "r"(b.y),
-                         "r"(b.z), "r"(b.w)
-                         : "memory");
+            sts128(rope + swz128(r, g), a);
+            sts128(rope + swz128(r, g + 4), b);
         }
     } else {
-        for (int i = ptid; i < BN * 8; i += 128) {  // (row, c): pairs (2j, 2j+1), j = 4c..4c+3
-            const int r = i >> 3, c = i & 7;
+        if (ptid < BN * 8) {  // (row, c): pairs (2j, 2j+1), j = 4c..4c+3
+            const int r = ptid >> 3, c = ptid & 7;
             const int k = t * BN + r;
             uint4 a = make_uint4(0, 0, 0, 0);
             if (k < p.n_kv) {
-                const int64_t prow = p.kv_rows ? (int64_t)p.kv_rows[k] : (int64_t)k;
+                const int64_t prow = p.kv_rows ? (int64_t)__ldg(p.kv_rows + k) : (int64_t)k;
                 a = __ldg(reinterpret_cast<const uint4 *>(p.pool + prow * DQK + DV) + c);
                 if (p.kv_chunk) {
-                    const float2 *cs = p.chunk_cs + (int64_t)p.kv_chunk[k] * 32 + 4 * c;
+                    const float4 *cs = reinterpret_cast<const float4 *>(p.chunk_cs + (int64_t)__ldg(p.kv_chunk + k) * 32 + 4 * c);
                     uint32_t *aw = reinterpret_cast<uint32_t *>(&a);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 cc = __ldg(cs + e);
-                        const float lo = bf_lo(aw[e]), hi = bf_hi(aw[e]);
-                        aw[e] = pack_bf2(lo * cc.x - hi * cc.y, lo * cc.y + hi * cc.x);
+                    for (int e = 0; e < 2; ++e) {
+                        const float4 cc = __ldg(cs + e);
+                        const float l0 = bf_lo(aw[2 * e]), h0 = bf_hi(aw[2 * e]);
+                        const float l1 = bf_lo(aw[2 * e + 1]), h1 = bf_hi(aw[2 * e + 1]);
+                        aw[2 * e] = pack_bf2(l0 * cc.x - h0 * cc.y, l0 * cc.y + h0 * cc.x);
+                        aw[2 * e + 1] = pack_bf2(l1 * cc.z - h1 * cc.w, l1 * cc.w + h1 * cc.z);
                     }
                 }
             }
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rope + swz(r, c)), "r"(a.x), "r"(a.y),
-                         "r"(a.z), "r"(a.w)
-                         : "memory");
+            sts128(rope + swz128(r, c), a);
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -141,7 +152,8 @@ __device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int
 __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    __shared__ __align__(8) uint64_t bar_q, bar_kv_full[2], bar_kv_empty[2], bar_s_full[2], bar_p_full, bar_o_done;
+    __shared__ __align__(8) uint64_t bar_q, bar_kv_full[NST], bar_kv_empty[NST], bar_s_full[2], bar_p_full[2],
+        bar_o_done[2];
     __shared__ uint32_t tmem_base;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -152,83 +164,86 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
     const int T = (n_keys + BN - 1) / BN;
 
     if (threadIdx.x == 0) {
-        mbar_init(&bar_q, 128);
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&bar_kv_full[s], 128);
+        mbar_init(&bar_q, N_PROD);
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&bar_kv_full[s], N_PROD);
             mbar_init(&bar_kv_empty[s], 1);
-            mbar_init(&bar_s_full[s], 1);
         }
-        mbar_init(&bar_p_full, 128);
-        mbar_init(&bar_o_done, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bar_s_full[s], 1);
+            mbar_init(&bar_p_full[s], 128);
+            mbar_init(&bar_o_done[s], 1);
+        }
         fence_mbar_init();
     }
-    if (warp == 8) tc::tmem_alloc(&tmem_base, 512);
+    if (warp == W_MMA) tc::tmem_alloc(&tmem_base, 512);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = tmem_base;
 
-    if (warp >= 4 && warp < 8) {
+    if (warp >= 4 && warp < W_MMA) {
         // ------------------------------------------------------ producers
         const int ptid = threadIdx.x - 128;
         const uint32_t qbase = smem_u32(smem + SMEM_Q);
-        for (int i = ptid; i < BM * 72; i += 128) {
+        for (int i = ptid; i < BM * 72; i += N_PROD) {
             const int r = i / 72, c = i % 72;
             const int64_t grow = row0 + r;
             const bool ok = grow < p.n_rows;
-            cp_async16(qbase + (c >> 3) * PIECE + swz(r, c & 7), p.q + (ok ? grow : 0) * DQK + c * 8, ok ? 16u : 0u);
+            cp_async16(qbase + (c >> 3) * QPIECE + swz128(r, c & 7), p.q + (ok ? grow : 0) * DQK + c * 8, ok ? 16u : 0u);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         fence_proxy_async_smem();
         mbar_arrive(&bar_q);
         for (int t = 0; t < T; ++t) {
-            const int st = t & 1;
-            if (t >= 2) mbar_wait(&bar_kv_empty[st], ((t >> 1) - 1) & 1);
-            load_kv_tile(p, smem + SMEM_KV + st * TILE, t, ptid);
+            const int st = t % NST;
+            if (t >= NST) mbar_wait(&bar_kv_empty[st], ((t / NST) - 1) & 1);
+            load_kv_tile(p, smem + SMEM_KV + st * KTILE, t, ptid);
             mbar_arrive(&bar_kv_full[st]);
         }
-    } else if (warp == 8) {
-        // ------------------------------------------------------ MMA issuer
+    } else if (warp == W_MMA) {
+        // ------------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
             const uint32_t idesc_qk = tc::idesc_bf16(BM, BN, false, false);
             const uint32_t idesc_pv = tc::idesc_bf16(BM, 256, false, true);
             const uint32_t q_addr = smem_u32(smem + SMEM_Q), kv_addr = smem_u32(smem + SMEM_KV);
             const uint32_t p_addr = smem_u32(smem + SMEM_P);
-            mbar_wait(&bar_q, 0);
-            for (int t = 0; t <= T; ++t) {
-                if (t < T) {
-                    const int st = t & 1;
-                    mbar_wait(&bar_kv_full[st], (t >> 1) & 1);
-                    tc::fence_after();
-                    const uint32_t d = tbase + (S_LANE << 16) + st * BN;
+            auto issue_qk = [&](int t) {
+                const int st = t % NST;
+                mbar_wait(&bar_kv_full[st], (t / NST) & 1);
+                tc::fence_after();
+                const uint32_t d = tbase + (S_LANE << 16) + (t & 1) * BN;
 #pragma unroll 1
-                    for (int pc = 0; pc < NPIECE; ++pc) {
+                for (int pc = 0; pc < NPIECE; ++pc) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint64_t a = tc::smem_desc_sw128(q_addr + pc * PIECE + k * 32, 16, 1024);
-                            const uint64_t b = tc::smem_desc_sw128(kv_addr + st * TILE + pc * PIECE + k * 32, 16, 1024);
-                            tc::mma_bf16_ss(d, a, b, idesc_qk, (pc | k) != 0);
-                        }
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t a = tc::smem_desc_sw128(q_addr + pc * QPIECE + k * 32, 16, 1024);
+                        const uint64_t b = tc::smem_desc_sw128(kv_addr + st * KTILE + pc * KPIECE + k * 32, 16, 1024);
+                        tc::mma_bf16_ss(d, a, b, idesc_qk, (pc | k) != 0);
                     }
-                    tc::commit(&bar_s_full[st]);
                 }
-                if (t >= 1) {
-                    const int u = t - 1, su = u & 1;
-                    mbar_wait(&bar_p_full, u & 1);
-                    tc::fence_after();
+                tc::commit(&bar_s_full[t & 1]);
+            };
+            mbar_wait(&bar_q, 0);
+            issue_qk(0);
+            for (int t = 0; t < T; ++t) {
+                // S buffer (t+1)&1 was consumed by softmax(t-1): its P(t-1) arrived before PV(t-1)
+                if (t + 1 < T) issue_qk(t + 1);
+                const int st = t % NST;
+                mbar_wait(&bar_p_full[t & 1], (t >> 1) & 1);
+                tc::fence_after();
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < 2; ++h) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint64_t a = tc::smem_desc_sw128(p_addr + k * 32, 16, 1024);
-                            const uint64_t b = tc::smem_desc_sw128(kv_addr + su * TILE + 4 * h * PIECE + k * 2048,
-                                                                   PIECE, 1024);
-                            tc::mma_bf16_ss(tbase + h * 256, a, b, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
-                        }
+                    for (int k = 0; k < BN / 16; ++k) {
+                        const uint64_t a = tc::smem_desc_sw64(p_addr + (t & 1) * PTILE + k * 32, 16, 512);
+                        const uint64_t b = tc::smem_desc_sw128(kv_addr + st * KTILE + 4 * h * KPIECE + k * 2048,
+                                                               KPIECE, 1024);
+                        tc::mma_bf16_ss(tbase + h * 256, a, b, idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
                     }
-                    tc::commit(&bar_kv_empty[su]);
-                    tc::commit(&bar_o_done);
                 }
+                tc::commit(&bar_kv_empty[st]);
+                tc::commit(&bar_o_done[t & 1]);
             }
         }
         __syncwarp();
@@ -241,22 +256,21 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
         const int64_t grow = row0 + r;
         const bool row_ok = grow < p.n_rows;
         const int64_t qpos = p.q_pos0 + (row_ok ? grow / p.heads : 0);
-        const uint32_t s_lane = tbase + ((uint32_t)(32 * w) + S_LANE << 16);
+        const uint32_t s_lane = tbase + (((uint32_t)(32 * w) + S_LANE) << 16);
         const uint32_t o_lane = tbase + ((uint32_t)(32 * w) << 16);
         const uint32_t p_base = smem_u32(smem + SMEM_P);
         float m = -INFINITY, l = 0.f;
         for (int t = 0; t < T; ++t) {
-            const int st = t & 1;
-            mbar_wait(&bar_s_full[st], (t >> 1) & 1);
+            mbar_wait(&bar_s_full[t & 1], (t >> 1) & 1);
             tc::fence_after();
-            uint32_t v[32];
-            tc::ld_16x64b_x32(s_lane + st * BN, v);
+            uint32_t v[16];
+            tc::ld_16x64b_x16(s_lane + (t & 1) * BN, v);
             tc::wait_ld();
-            float s[32];
+            float s[16];
             float mt = -INFINITY;
             const int64_t kbase = (int64_t)t * BN + b;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < 16; ++i) {
                 const int64_t key = kbase + 2 * i;
                 const bool ok = row_ok && key <= qpos && key < p.n_kv;
                 s[i] = ok ? __uint_as_float(v[i]) * p.scale_log2 : -INFINITY;
@@ -271,48 +285,45 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
             }
             float lsum = 0.f;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < 16; ++i) {
                 s[i] = (s[i] == -INFINITY) ? 0.f : exp2f(s[i] - m);
                 lsum += s[i];
             }
             lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
             l = l * alpha + lsum;
-            // pack P: pairs of adjacent keys, thread b = 0 takes keys 0..31, b = 1 keys 32..63
-            uint32_t pk[16];
+            // pack P: pairs of adjacent keys, thread b = 0 takes keys 0..15, b = 1 keys 16..31
+            uint32_t pk[8];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < 16; ++i) {
                 const float other = __shfl_xor_sync(0xffffffffu, s[i], 2);
                 const uint32_t pr = b == 0 ? pack_bf2(s[i], other) : pack_bf2(other, s[i]);
-                if ((i >> 4) == b) pk[i & 15] = pr;
+                if ((i >> 3) == b) pk[i & 7] = pr;
             }
-            if (t >= 1) {  // PV(t-1) has finished: O is stable and the P tile is free
-                mbar_wait(&bar_o_done, (t - 1) & 1);
+            // P buffer t&1 is free once PV(t-2) completed
+            if (t >= 2) mbar_wait(&bar_o_done[t & 1], ((t >> 1) - 1) & 1);
+            if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
+                mbar_wait(&bar_o_done[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV(0..t-1)
                 tc::fence_after();
-                if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-                    for (int c = 0; c < DV / 64; ++c) {
-                        uint32_t o[32];
-                        tc::ld_16x64b_x32(o_lane + c * 64, o);
-                        tc::wait_ld();
+                for (int c = 0; c < DV / 64; ++c) {
+                    uint32_t o[32];
+                    tc::ld_16x64b_x32(o_lane + c * 64, o);
+                    tc::wait_ld();
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                        tc::st_16x64b_x32(o_lane + c * 64, o);
-                    }
-                    tc::wait_st();
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    tc::st_16x64b_x32(o_lane + c * 64, o);
                 }
+                tc::wait_st();
             }
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(p_base + swz(r, 4 * b + q4)),
-                             "r"(pk[4 * q4]), "r"(pk[4 * q4 + 1]), "r"(pk[4 * q4 + 2]), "r"(pk[4 * q4 + 3])
-                             : "memory");
-            }
+            const uint32_t pt = p_base + (t & 1) * PTILE;
+            sts128(pt + swz64(r, 2 * b), make_uint4(pk[0], pk[1], pk[2], pk[3]));
+            sts128(pt + swz64(r, 2 * b + 1), make_uint4(pk[4], pk[5], pk[6], pk[7]));
             fence_proxy_async_smem();
             tc::fence_before();
-            mbar_arrive(&bar_p_full);
+            mbar_arrive(&bar_p_full[t & 1]);
         }
         // epilogue: O / l -> bf16, lse
-        mbar_wait(&bar_o_done, (T - 1) & 1);
+        mbar_wait(&bar_o_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
         tc::fence_after();
         const float inv_l = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
@@ -341,7 +352,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if (warp == 8) tc::tmem_dealloc(tbase, 512);
+    if (warp == W_MMA) tc::tmem_dealloc(tbase, 512);
 }
 
 __global__ void cossin_kernel(const int64_t *__restrict__ delta, int64_t n_chunks,
@@ -380,6 +391,7 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
     if (n_q == 0) return IRM_OK;
     IRM_REQUIRE(q && pool && out, "null pointer");
     IRM_REQUIRE((((uintptr_t)q | (uintptr_t)pool | (uintptr_t)out) & 15) == 0, "16-byte alignment required");
+    IRM_REQUIRE(!chunk_cs || ((uintptr_t)chunk_cs & 15) == 0, "chunk_cs must be 16-byte aligned");
     mla::Params p{};
     p.q = (const __nv_bfloat16 *)q;
     p.pool = (const __nv_bfloat16 *)pool;
