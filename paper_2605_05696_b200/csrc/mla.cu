@@ -41,6 +41,7 @@ constexpr int PTILE = BM * BN * 2;   // 4 KB, 64-byte rows (SW64)
 constexpr int SMEM_Q = 0, SMEM_KV = NPIECE * QPIECE, SMEM_P = SMEM_KV + NST * KTILE;
 constexpr int SMEM_BYTES = SMEM_P + 2 * PTILE;
 constexpr int N_PROD = 256;          // producer threads (warps 4..11)
+constexpr int GROUP = N_PROD / NST;  // producer group g (64 threads) owns ring stage g
 constexpr int W_MMA = 12;
 constexpr int THREADS = 32 * (W_MMA + 1);
 constexpr uint32_t S_LANE = 16;      // S lives in the upper half-subpartition lanes
@@ -82,12 +83,12 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
     return *reinterpret_cast<uint32_t *>(&v);
 }
 
-// producers: KV tile `t` into `tile` (N_PROD threads)
+// producers: KV tile `t` into `tile` (one GROUP of threads)
 __device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int t, int ptid) {
     const uint32_t base = smem_u32(tile);
     // c_KV: BN rows x 64 chunks of 16 B, verbatim
 #pragma unroll 4
-    for (int i = ptid; i < BN * 64; i += N_PROD) {
+    for (int i = ptid; i < BN * 64; i += GROUP) {
         const int r = i >> 6, c = i & 63;
         const int k = t * BN + r;
         const bool ok = k < p.n_kv;
@@ -97,8 +98,8 @@ __device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int
     // k_r: load, rotate by R(delta) in fp32, store bf16 (piece 8)
     const uint32_t rope = base + 8 * KPIECE;
     if (p.layout == IRM_LAYOUT_HALF_SPLIT) {
-        if (ptid < BN * 4) {  // (row, g): dims j = 8g..8g+7 pair with j + 32
-            const int r = ptid >> 2, g = ptid & 3;
+        for (int it = ptid; it < BN * 4; it += GROUP) {  // (row, g): dims j = 8g..8g+7 pair with j + 32
+            const int r = it >> 2, g = it & 3;
             const int k = t * BN + r;
             uint4 a = make_uint4(0, 0, 0, 0), b = a;
             if (k < p.n_kv) {
@@ -122,8 +123,8 @@ __device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int
             sts128(rope + swz128(r, g + 4), b);
         }
     } else {
-        if (ptid < BN * 8) {  // (row, c): pairs (2j, 2j+1), j = 4c..4c+3
-            const int r = ptid >> 3, c = ptid & 7;
+        for (int it = ptid; it < BN * 8; it += GROUP) {  // (row, c): pairs (2j, 2j+1), j = 4c..4c+3
+            const int r = it >> 3, c = it & 7;
             const int k = t * BN + r;
             uint4 a = make_uint4(0, 0, 0, 0);
             if (k < p.n_kv) {
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
     if (threadIdx.x == 0) {
         mbar_init(&bar_q, N_PROD);
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&bar_kv_full[s], N_PROD);
+            mbar_init(&bar_kv_full[s], GROUP);
             mbar_init(&bar_kv_empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -195,11 +196,13 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
         asm volatile("cp.async.wait_all;" ::: "memory");
         fence_proxy_async_smem();
         mbar_arrive(&bar_q);
-        for (int t = 0; t < T; ++t) {
-            const int st = t % NST;
-            if (t >= NST) mbar_wait(&bar_kv_empty[st], ((t / NST) - 1) & 1);
-            load_kv_tile(p, smem + SMEM_KV + st * KTILE, t, ptid);
-            mbar_arrive(&bar_kv_full[st]);
+        // NST independent producer groups: group g streams tiles g, g + NST, ... into stage g,
+        // so NST tiles are in flight while each group waits only for its own copies
+        const int g = ptid / GROUP, gtid = ptid % GROUP;
+        for (int t = g; t < T; t += NST) {
+            if (t >= NST) mbar_wait(&bar_kv_empty[g], ((t / NST) - 1) & 1);
+            load_kv_tile(p, smem + SMEM_KV + g * KTILE, t, gtid);
+            mbar_arrive(&bar_kv_full[g]);
         }
     } else if (warp == W_MMA) {
         // ------------------------------------------------------ MMA issuer (one thread)
