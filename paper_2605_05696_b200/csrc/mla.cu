@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "tcgen05.cuh"
 #include <cuda_bf16.h>
+#include <stdlib.h>
 
 namespace irm {
 namespace mla {
@@ -59,6 +60,7 @@ struct Params {
     int32_t heads, n_kv, layout;
     int64_t q_pos0;
     float scale_log2;         // softmax scale * log2(e)
+    int dbg;                  // IRM_MLA_DEBUG: per-role cycle breakdown of CTA 0
 };
 
 __device__ __forceinline__ uint32_t swz128(int row, int chunk) {  // SW128 byte offset (128-B rows)
@@ -199,11 +201,18 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
         // NST independent producer groups: group g streams tiles g, g + NST, ... into stage g,
         // so NST tiles are in flight while each group waits only for its own copies
         const int g = ptid / GROUP, gtid = ptid % GROUP;
+        long long c_wait = 0, c_load = 0, c0 = clock64();
         for (int t = g; t < T; t += NST) {
+            long long a = clock64();
             if (t >= NST) mbar_wait(&bar_kv_empty[g], ((t / NST) - 1) & 1);
+            long long b2 = clock64();
             load_kv_tile(p, smem + SMEM_KV + g * KTILE, t, gtid);
             mbar_arrive(&bar_kv_full[g]);
+            c_wait += b2 - a;
+            c_load += clock64() - b2;
         }
+        if (p.dbg && blockIdx.x == 0 && gtid == 0)
+            printf("producer g%d: wait_empty %lld load %lld total %lld (T=%d)\n", g, c_wait, c_load, clock64() - c0, T);
     } else if (warp == W_MMA) {
         // ------------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
@@ -211,9 +220,12 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
             const uint32_t idesc_pv = tc::idesc_bf16(BM, 256, false, true);
             const uint32_t q_addr = smem_u32(smem + SMEM_Q), kv_addr = smem_u32(smem + SMEM_KV);
             const uint32_t p_addr = smem_u32(smem + SMEM_P);
+            long long c_kv = 0, c_p = 0, c0 = clock64();
             auto issue_qk = [&](int t) {
                 const int st = t % NST;
+                long long a = clock64();
                 mbar_wait(&bar_kv_full[st], (t / NST) & 1);
+                c_kv += clock64() - a;
                 tc::fence_after();
                 const uint32_t d = tbase + (S_LANE << 16) + (t & 1) * BN;
 #pragma unroll 1
@@ -233,7 +245,9 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
                 // S buffer (t+1)&1 was consumed by softmax(t-1): its P(t-1) arrived before PV(t-1)
                 if (t + 1 < T) issue_qk(t + 1);
                 const int st = t % NST;
+                long long a = clock64();
                 mbar_wait(&bar_p_full[t & 1], (t >> 1) & 1);
+                c_p += clock64() - a;
                 tc::fence_after();
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -248,6 +262,8 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
                 tc::commit(&bar_kv_empty[st]);
                 tc::commit(&bar_o_done[t & 1]);
             }
+            if (p.dbg && blockIdx.x == 0)
+                printf("mma: wait_kv %lld wait_p %lld total %lld\n", c_kv, c_p, clock64() - c0);
         }
         __syncwarp();
     } else {
@@ -263,8 +279,11 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
         const uint32_t o_lane = tbase + ((uint32_t)(32 * w) << 16);
         const uint32_t p_base = smem_u32(smem + SMEM_P);
         float m = -INFINITY, l = 0.f;
+        long long c_s = 0, c_o = 0, c_r = 0, c0 = clock64();
         for (int t = 0; t < T; ++t) {
+            long long a = clock64();
             mbar_wait(&bar_s_full[t & 1], (t >> 1) & 1);
+            c_s += clock64() - a;
             tc::fence_after();
             uint32_t v[16];
             tc::ld_16x64b_x16(s_lane + (t & 1) * BN, v);
@@ -303,7 +322,10 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
                 if ((i >> 3) == b) pk[i & 7] = pr;
             }
             // P buffer t&1 is free once PV(t-2) completed
+            a = clock64();
             if (t >= 2) mbar_wait(&bar_o_done[t & 1], ((t >> 1) - 1) & 1);
+            c_o += clock64() - a;
+            a = clock64();
             if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
                 mbar_wait(&bar_o_done[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV(0..t-1)
                 tc::fence_after();
@@ -318,6 +340,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
                 }
                 tc::wait_st();
             }
+            c_r += clock64() - a;
             const uint32_t pt = p_base + (t & 1) * PTILE;
             sts128(pt + swz64(r, 2 * b), make_uint4(pk[0], pk[1], pk[2], pk[3]));
             sts128(pt + swz64(r, 2 * b + 1), make_uint4(pk[4], pk[5], pk[6], pk[7]));
@@ -325,6 +348,8 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
             tc::fence_before();
             mbar_arrive(&bar_p_full[t & 1]);
         }
+        if (p.dbg && blockIdx.x == 0 && lane == 0)
+            printf("softmax w%d: wait_s %lld wait_o %lld rescale %lld total %lld\n", w, c_s, c_o, c_r, clock64() - c0);
         // epilogue: O / l -> bf16, lse
         mbar_wait(&bar_o_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
         tc::fence_after();
@@ -409,6 +434,7 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
     p.layout = layout;
     p.q_pos0 = q_pos0;
     p.scale_log2 = scale * 1.4426950408889634f;
+    p.dbg = getenv("IRM_MLA_DEBUG") != nullptr;
     const int smem = mla::SMEM_BYTES + 1024;
     IRM_CUDA_CHECK(cudaFuncSetAttribute(mla::mla_reattach_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t grid = (p.n_rows + mla::BM - 1) / mla::BM;
