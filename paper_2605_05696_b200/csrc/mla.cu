@@ -214,58 +214,68 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
         if (p.dbg && blockIdx.x == 0 && gtid == 0)
             printf("producer g%d: wait_empty %lld load %lld total %lld (T=%d)\n", g, c_wait, c_load, clock64() - c0, T);
     } else if (warp == W_MMA) {
-        // ------------------------------------------------------ MMA issuer (one thread)
-        if (lane == 0) {
-            const uint32_t idesc_qk = tc::idesc_bf16(BM, BN, false, false);
-            const uint32_t idesc_pv = tc::idesc_bf16(BM, 256, false, true);
-            const uint32_t q_addr = smem_u32(smem + SMEM_Q), kv_addr = smem_u32(smem + SMEM_KV);
-            const uint32_t p_addr = smem_u32(smem + SMEM_P);
-            long long c_kv = 0, c_p = 0, c0 = clock64();
-            auto issue_qk = [&](int t) {
-                const int st = t % NST;
-                long long a = clock64();
-                mbar_wait(&bar_kv_full[st], (t / NST) & 1);
-                c_kv += clock64() - a;
-                tc::fence_after();
-                const uint32_t d = tbase + (S_LANE << 16) + (t & 1) * BN;
-#pragma unroll 1
+        // ------------------------------------------------------ MMA issuer
+        // The warp stays converged (barrier waits by all lanes); one elected lane
+        // issues each unrolled batch. Descriptors are built once: per MMA only the
+        // 14-bit start-address field (bytes >> 4) advances, so a batch is a run of
+        // UTCHMMA with immediate offsets.
+        const uint32_t idesc_qk = tc::idesc_bf16(BM, BN, false, false);
+        const uint32_t idesc_pv = tc::idesc_bf16(BM, 256, false, true);
+        const uint64_t q_desc = tc::smem_desc_sw128(smem_u32(smem + SMEM_Q), 16, 1024);
+        const uint64_t kv_desc = tc::smem_desc_sw128(smem_u32(smem + SMEM_KV), 16, 1024);
+        const uint64_t v_desc = tc::smem_desc_sw128(smem_u32(smem + SMEM_KV), KPIECE, 1024);
+        const uint64_t p_desc = tc::smem_desc_sw64(smem_u32(smem + SMEM_P), 16, 512);
+        long long c_kv = 0, c_p = 0, c0 = clock64();
+        auto issue_qk = [&](int t) {
+            const int st = t % NST;
+            long long a = clock64();
+            mbar_wait(&bar_kv_full[st], (t / NST) & 1);
+            c_kv += clock64() - a;
+            tc::fence_after();
+            const uint32_t d = tbase + (S_LANE << 16) + (t & 1) * BN;
+            const uint64_t kd = kv_desc + (uint64_t)((st * KTILE) >> 4);
+            if (tc::elect_one()) {
+#pragma unroll
                 for (int pc = 0; pc < NPIECE; ++pc) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const uint64_t a = tc::smem_desc_sw128(q_addr + pc * QPIECE + k * 32, 16, 1024);
-                        const uint64_t b = tc::smem_desc_sw128(kv_addr + st * KTILE + pc * KPIECE + k * 32, 16, 1024);
-                        tc::mma_bf16_ss(d, a, b, idesc_qk, (pc | k) != 0);
+                        tc::mma_bf16_ss(d, q_desc + (uint64_t)((pc * QPIECE + k * 32) >> 4),
+                                        kd + (uint64_t)((pc * KPIECE + k * 32) >> 4), idesc_qk, (pc | k) != 0);
                     }
                 }
                 tc::commit(&bar_s_full[t & 1]);
-            };
-            mbar_wait(&bar_q, 0);
-            issue_qk(0);
-            for (int t = 0; t < T; ++t) {
-                // S buffer (t+1)&1 was consumed by softmax(t-1): its P(t-1) arrived before PV(t-1)
-                if (t + 1 < T) issue_qk(t + 1);
-                const int st = t % NST;
-                long long a = clock64();
-                mbar_wait(&bar_p_full[t & 1], (t >> 1) & 1);
-                c_p += clock64() - a;
-                tc::fence_after();
+            }
+            __syncwarp();
+        };
+        mbar_wait(&bar_q, 0);
+        issue_qk(0);
+        for (int t = 0; t < T; ++t) {
+            // S buffer (t+1)&1 was consumed by softmax(t-1): its P(t-1) arrived before PV(t-1)
+            if (t + 1 < T) issue_qk(t + 1);
+            const int st = t % NST;
+            long long a = clock64();
+            mbar_wait(&bar_p_full[t & 1], (t >> 1) & 1);
+            c_p += clock64() - a;
+            tc::fence_after();
+            const uint64_t pd = p_desc + (uint64_t)(((t & 1) * PTILE) >> 4);
+            const uint64_t vd = v_desc + (uint64_t)((st * KTILE) >> 4);
+            if (tc::elect_one()) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
 #pragma unroll
                     for (int k = 0; k < BN / 16; ++k) {
-                        const uint64_t a = tc::smem_desc_sw64(p_addr + (t & 1) * PTILE + k * 32, 16, 512);
-                        const uint64_t b = tc::smem_desc_sw128(kv_addr + st * KTILE + 4 * h * KPIECE + k * 2048,
-                                                               KPIECE, 1024);
-                        tc::mma_bf16_ss(tbase + h * 256, a, b, idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
+                        tc::mma_bf16_ss(tbase + h * 256, pd + (uint64_t)((k * 32) >> 4),
+                                        vd + (uint64_t)((4 * h * KPIECE + k * 2048) >> 4), idesc_pv,
+                                        (t > 0 || k > 0) ? 1u : 0u);
                     }
                 }
                 tc::commit(&bar_kv_empty[st]);
                 tc::commit(&bar_o_done[t & 1]);
             }
-            if (p.dbg && blockIdx.x == 0)
-                printf("mma: wait_kv %lld wait_p %lld total %lld\n", c_kv, c_p, clock64() - c0);
+            __syncwarp();
         }
-        __syncwarp();
+        if (p.dbg && blockIdx.x == 0 && lane == 0)
+            printf("mma: wait_kv %lld wait_p %lld total %lld\n", c_kv, c_p, clock64() - c0);
     } else {
         // ------------------------------------------------------ softmax / correction (warps 0-3)
         const int w = warp;
