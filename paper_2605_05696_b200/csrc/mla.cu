@@ -165,6 +165,9 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
     const int64_t max_pos = p.q_pos0 + last_row / p.heads;
     const int n_keys = (int)min((int64_t)p.n_kv, max_pos + 1);
     const int T = (n_keys + BN - 1) / BN;
+    // CTAs of a wave start at scattered key tiles (any order is exact under the
+    // online softmax), so concurrent CTAs do not hammer the same L2 lines
+    const int toff = (int)(((uint32_t)blockIdx.x * 2654435761u) % (uint32_t)T);
 
     if (threadIdx.x == 0) {
         mbar_init(&bar_q, N_PROD);
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
             long long a = clock64();
             if (t >= NST) mbar_wait(&bar_kv_empty[g], ((t / NST) - 1) & 1);
             long long b2 = clock64();
-            load_kv_tile(p, smem + SMEM_KV + g * KTILE, t, gtid);
+            load_kv_tile(p, smem + SMEM_KV + g * KTILE, (t + toff) % T, gtid);
             mbar_arrive(&bar_kv_full[g]);
             c_wait += b2 - a;
             c_load += clock64() - b2;
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
             tc::wait_ld();
             float s[16];
             float mt = -INFINITY;
-            const int64_t kbase = (int64_t)t * BN + b;
+            const int64_t kbase = (int64_t)((t + toff) % T) * BN + b;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 const int64_t key = kbase + 2 * i;
