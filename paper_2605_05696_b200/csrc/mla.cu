@@ -85,23 +85,19 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
     return *reinterpret_cast<uint32_t *>(&v);
 }
 
-// producers: KV tile `t` into `tile` (one GROUP of threads)
-__device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int t, int ptid) {
-    const uint32_t base = smem_u32(tile);
-    // c_KV: BN rows x 64 chunks of 16 B, verbatim
-#pragma unroll 4
-    for (int i = ptid; i < BN * 64; i += GROUP) {
-        const int r = i >> 6, c = i & 63;
-        const int k = t * BN + r;
-        const bool ok = k < p.n_kv;
-        const int64_t prow = ok ? (p.kv_rows ? (int64_t)__ldg(p.kv_rows + k) : (int64_t)k) : 0;
-        cp_async16(base + (c >> 3) * KPIECE + swz128(r, c & 7), p.pool + prow * DQK + c * 8, ok ? 16u : 0u);
-    }
-    // k_r: load, rotate by R(delta) in fp32, store bf16 (piece 8)
-    const uint32_t rope = base + 8 * KPIECE;
+// producers: the k_r part of KV tile `t` -- load kr_base, rotate by R(delta) in
+// fp32 (cos/sin from the per-chunk fp64-angle table) -- into registers. Runs
+// before the ring slot is free, so its two dependent L2 round trips
+// (kv_chunk -> cs) overlap the wait.
+struct RopeRegs {
+    uint4 v[4];
+};
+
+__device__ __forceinline__ void rope_fetch(const Params &p, int t, int ptid, RopeRegs &rr) {
     if (p.layout == IRM_LAYOUT_HALF_SPLIT) {
-        for (int it = ptid; it < BN * 4; it += GROUP) {  // (row, g): dims j = 8g..8g+7 pair with j + 32
-            const int r = it >> 2, g = it & 3;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {  // (row, g): dims j = 8g..8g+7 pair with j + 32
+            const int it = ptid + q * GROUP, r = it >> 2, g = it & 3;
             const int k = t * BN + r;
             uint4 a = make_uint4(0, 0, 0, 0), b = a;
             if (k < p.n_kv) {
@@ -121,12 +117,13 @@ __device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int
                     }
                 }
             }
-            sts128(rope + swz128(r, g), a);
-            sts128(rope + swz128(r, g + 4), b);
+            rr.v[2 * q] = a;
+            rr.v[2 * q + 1] = b;
         }
     } else {
-        for (int it = ptid; it < BN * 8; it += GROUP) {  // (row, c): pairs (2j, 2j+1), j = 4c..4c+3
-            const int r = it >> 3, c = it & 7;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // (row, c): pairs (2j, 2j+1), j = 4c..4c+3
+            const int it = ptid + q * GROUP, r = it >> 3, c = it & 7;
             const int k = t * BN + r;
             uint4 a = make_uint4(0, 0, 0, 0);
             if (k < p.n_kv) {
@@ -145,12 +142,43 @@ __device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int
                     }
                 }
             }
-            sts128(rope + swz128(r, c), a);
+            rr.v[q] = a;
+        }
+    }
+}
+
+// producers: KV tile `t` into ring slot `tile`: c_KV verbatim by cp.async, the
+// rotated k_r from registers (piece 8), then publish to the async proxy
+__device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int t, int ptid, const RopeRegs &rr) {
+    const uint32_t base = smem_u32(tile);
+#pragma unroll 4
+    for (int i = ptid; i < BN * 64; i += GROUP) {
+        const int r = i >> 6, c = i & 63;
+        const int k = t * BN + r;
+        const bool ok = k < p.n_kv;
+        const int64_t prow = ok ? (p.kv_rows ? (int64_t)__ldg(p.kv_rows + k) : (int64_t)k) : 0;
+        cp_async16(base + (c >> 3) * KPIECE + swz128(r, c & 7), p.pool + prow * DQK + c * 8, ok ? 16u : 0u);
+    }
+    const uint32_t rope = base + 8 * KPIECE;
+    if (p.layout == IRM_LAYOUT_HALF_SPLIT) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int it = ptid + q * GROUP, r = it >> 2, g = it & 3;
+            sts128(rope + swz128(r, g), rr.v[2 * q]);
+            sts128(rope + swz128(r, g + 4), rr.v[2 * q + 1]);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int it = ptid + q * GROUP, r = it >> 3, c = it & 7;
+            sts128(rope + swz128(r, c), rr.v[q]);
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     fence_proxy_async_smem();
 }
+
+static_assert(BN * 4 == 2 * GROUP && BN * 8 == 4 * GROUP, "rope work split assumes 2 / 4 items per producer");
 
 __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -206,10 +234,13 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
         const int g = ptid / GROUP, gtid = ptid % GROUP;
         long long c_wait = 0, c_load = 0, c0 = clock64();
         for (int t = g; t < T; t += NST) {
+            const int kt = (t + toff) % T;
+            RopeRegs rr;
+            rope_fetch(p, kt, gtid, rr);
             long long a = clock64();
             if (t >= NST) mbar_wait(&bar_kv_empty[g], ((t / NST) - 1) & 1);
             long long b2 = clock64();
-            load_kv_tile(p, smem + SMEM_KV + g * KTILE, (t + toff) % T, gtid);
+            load_kv_tile(p, smem + SMEM_KV + g * KTILE, kt, gtid, rr);
             mbar_arrive(&bar_kv_full[g]);
             c_wait += b2 - a;
             c_load += clock64() - b2;
