@@ -157,8 +157,8 @@ int irm_round_f64(const double *x, double *y, int64_t n, int32_t mode, irm_strea
  *   causal (key k visible to query position P iff k <= P), O = softmax(S) c_KV
  * q    [n_q, heads, 576] bf16 (absorbed q_nope || rotated q_pe); query i at
  *      position q_pos0 + i (q_pos0 + n_q <= n_kv)
- * pool [*, 576] bf16 latent rows (c_KV || kr_base); key k at pool row
- *      kv_rows[k] (NULL: row k)
+ * pool [pool_rows, 576] bf16 latent rows (c_KV || kr_base); key k at pool
+ *      row kv_rows[k] (NULL: row k), gathered by TMA (tile::gather4)
  * kv_chunk [n_kv] chunk of key k and chunk_cs [n_chunks*32] float2 from
  *      irm_chunk_cossin(): k_r is rotated by R(delta) in shared memory on its
  *      way to the tensor cores and never written back (NULL: no rotation)
@@ -166,7 +166,7 @@ int irm_round_f64(const double *x, double *y, int64_t n, int32_t mode, irm_strea
 int irm_chunk_cossin(const int64_t *delta, int64_t n_chunks, const double *inv_freq, void *cs,
                      irm_stream_t stream);
 int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t heads, int64_t q_pos0,
-                             const void *pool, const int32_t *kv_rows, int32_t n_kv,
+                             const void *pool, int64_t pool_rows, const int32_t *kv_rows, int32_t n_kv,
                              const int32_t *kv_chunk, const void *chunk_cs, int32_t layout,
                              float scale, void *out, float *lse, irm_stream_t stream);
 

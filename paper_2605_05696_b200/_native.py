@@ -54,7 +54,7 @@ _SIGS = {
     "irm_rotate_rows": ([P, i64, P, i64, i64, i32, P, P, i32, i32, i32, P], i32),
     "irm_round_f64": ([P, P, i64, i32, P], i32),
     "irm_chunk_cossin": ([P, i64, P, P, P], i32),
-    "irm_mla_reattach_prefill": ([P, i64, i32, i64, P, P, i32, P, P, i32, f32, P, P, P], i32),
+    "irm_mla_reattach_prefill": ([P, i64, i32, i64, P, i64, P, i32, P, P, i32, f32, P, P, P], i32),
 }
 
 _lib = None

@@ -25,6 +25,8 @@
 #include "common.cuh"
 #include "tcgen05.cuh"
 #include <cuda_bf16.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <stdlib.h>
 
 namespace irm {
@@ -41,9 +43,11 @@ constexpr int KTILE = NPIECE * KPIECE;
 constexpr int PTILE = BM * BN * 2;   // 4 KB, 64-byte rows (SW64)
 constexpr int SMEM_Q = 0, SMEM_KV = NPIECE * QPIECE, SMEM_P = SMEM_KV + NST * KTILE;
 constexpr int SMEM_BYTES = SMEM_P + 2 * PTILE;
-constexpr int N_PROD = 256;          // producer threads (warps 4..11)
-constexpr int GROUP = N_PROD / NST;  // producer group g (64 threads) owns ring stage g
-constexpr int W_MMA = 12;
+constexpr int N_PROD = 256;          // rope producer threads (warps 4..11)
+constexpr int GROUP = N_PROD / NST;  // rope group g (64 threads) owns ring stage g
+constexpr int W_TMA = 12;            // c_KV gather warp (TMA tile::gather4)
+constexpr int W_MMA = 13;
+constexpr uint32_t CKV_TX = BN * DV * 2;  // c_KV bytes landed by TMA per tile
 constexpr int THREADS = 32 * (W_MMA + 1);
 constexpr uint32_t S_LANE = 16;      // S lives in the upper half-subpartition lanes
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
@@ -147,19 +151,10 @@ __device__ __forceinline__ void rope_fetch(const Params &p, int t, int ptid, Rop
     }
 }
 
-// producers: KV tile `t` into ring slot `tile`: c_KV verbatim by cp.async, the
-// rotated k_r from registers (piece 8), then publish to the async proxy
-__device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int t, int ptid, const RopeRegs &rr) {
-    const uint32_t base = smem_u32(tile);
-#pragma unroll 4
-    for (int i = ptid; i < BN * 64; i += GROUP) {
-        const int r = i >> 6, c = i & 63;
-        const int k = t * BN + r;
-        const bool ok = k < p.n_kv;
-        const int64_t prow = ok ? (p.kv_rows ? (int64_t)__ldg(p.kv_rows + k) : (int64_t)k) : 0;
-        cp_async16(base + (c >> 3) * KPIECE + swz128(r, c & 7), p.pool + prow * DQK + c * 8, ok ? 16u : 0u);
-    }
-    const uint32_t rope = base + 8 * KPIECE;
+// rope producers: write the rotated k_r (piece 8) of KV tile `t` into ring slot
+// `tile` and publish it to the async proxy (c_KV arrives by TMA gather4)
+__device__ __forceinline__ void store_rope(const Params &p, uint8_t *tile, int ptid, const RopeRegs &rr) {
+    const uint32_t rope = smem_u32(tile) + 8 * KPIECE;
     if (p.layout == IRM_LAYOUT_HALF_SPLIT) {
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -174,13 +169,22 @@ __device__ __forceinline__ void load_kv_tile(const Params &p, uint8_t *tile, int
             sts128(rope + swz128(r, c), rr.v[q]);
         }
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
     fence_proxy_async_smem();
+}
+
+// 4 arbitrary pool rows x 64 columns (128 B each) -> 512 B of a SW128 piece
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tmap, int col, int r0, int r1, int r2,
+                                            int r3, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(tmap), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
 }
 
 static_assert(BN * 4 == 2 * GROUP && BN * 8 == 4 * GROUP, "rope work split assumes 2 / 4 items per producer");
 
-__global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
+__global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     __shared__ __align__(8) uint64_t bar_q, bar_kv_full[NST], bar_kv_empty[NST], bar_s_full[2], bar_p_full[2],
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
     if (threadIdx.x == 0) {
         mbar_init(&bar_q, N_PROD);
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&bar_kv_full[s], GROUP);
+            mbar_init(&bar_kv_full[s], GROUP + 1);  // rope group + the TMA thread's expect_tx
             mbar_init(&bar_kv_empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -216,8 +220,8 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
     tc::fence_after();
     const uint32_t tbase = tmem_base;
 
-    if (warp >= 4 && warp < W_MMA) {
-        // ------------------------------------------------------ producers
+    if (warp >= 4 && warp < W_TMA) {
+        // ------------------------------------------------------ Q (cp.async, once) + rope producers
         const int ptid = threadIdx.x - 128;
         const uint32_t qbase = smem_u32(smem + SMEM_Q);
         for (int i = ptid; i < BM * 72; i += N_PROD) {
@@ -229,8 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
         asm volatile("cp.async.wait_all;" ::: "memory");
         fence_proxy_async_smem();
         mbar_arrive(&bar_q);
-        // NST independent producer groups: group g streams tiles g, g + NST, ... into stage g,
-        // so NST tiles are in flight while each group waits only for its own copies
+        // NST independent rope groups: group g handles tiles g, g + NST, ... (ring stage g)
         const int g = ptid / GROUP, gtid = ptid % GROUP;
         long long c_wait = 0, c_load = 0, c0 = clock64();
         for (int t = g; t < T; t += NST) {
@@ -240,13 +243,40 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p) {
             long long a = clock64();
             if (t >= NST) mbar_wait(&bar_kv_empty[g], ((t / NST) - 1) & 1);
             long long b2 = clock64();
-            load_kv_tile(p, smem + SMEM_KV + g * KTILE, kt, gtid, rr);
+            store_rope(p, smem + SMEM_KV + g * KTILE, gtid, rr);
             mbar_arrive(&bar_kv_full[g]);
             c_wait += b2 - a;
             c_load += clock64() - b2;
         }
         if (p.dbg && blockIdx.x == 0 && gtid == 0)
-            printf("producer g%d: wait_empty %lld load %lld total %lld (T=%d)\n", g, c_wait, c_load, clock64() - c0, T);
+            printf("rope g%d: wait_empty %lld store %lld total %lld (T=%d)\n", g, c_wait, c_load, clock64() - c0, T);
+    } else if (warp == W_TMA) {
+        // ------------------------------------------------------ c_KV by TMA gather4 (paged rows)
+        // lane i resolves the pool row of key i of the tile; lanes 0..7 each issue the
+        // 8 gather4 (pieces 0..7) of rows 4i..4i+3
+        long long c_wait = 0, c0 = clock64();
+        for (int t = 0; t < T; ++t) {
+            const int st = t % NST, kt = (t + toff) % T;
+            const int k = kt * BN + lane;
+            const int row = k < p.n_kv ? (p.kv_rows ? __ldg(p.kv_rows + k) : k) : -1;  // -1: OOB, zero-filled
+            long long a = clock64();
+            if (t >= NST) mbar_wait(&bar_kv_empty[st], ((t / NST) - 1) & 1);
+            c_wait += clock64() - a;
+            if (lane == 0) mbar_arrive_expect_tx(&bar_kv_full[st], CKV_TX);
+            __syncwarp();
+            const int r0 = __shfl_sync(0xffffffffu, row, 4 * (lane & 7));
+            const int r1 = __shfl_sync(0xffffffffu, row, 4 * (lane & 7) + 1);
+            const int r2 = __shfl_sync(0xffffffffu, row, 4 * (lane & 7) + 2);
+            const int r3 = __shfl_sync(0xffffffffu, row, 4 * (lane & 7) + 3);
+            if (lane < BN / 4) {
+                const uint32_t dst = smem_u32(smem + SMEM_KV + st * KTILE) + lane * 512;
+#pragma unroll
+                for (int pc = 0; pc < 8; ++pc)
+                    tma_gather4(dst + pc * KPIECE, &tmap_pool, 64 * pc, r0, r1, r2, r3, &bar_kv_full[st]);
+            }
+        }
+        if (p.dbg && blockIdx.x == 0 && lane == 0)
+            printf("tma: wait_empty %lld total %lld\n", c_wait, clock64() - c0);
     } else if (warp == W_MMA) {
         // ------------------------------------------------------ MMA issuer
         // The warp stays converged (barrier waits by all lanes); one elected lane
@@ -452,18 +482,50 @@ extern "C" int irm_chunk_cossin(const int64_t *delta, int64_t n_chunks, const do
     return IRM_OK;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+    }
+    return fn;
+}
+
 extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t heads, int64_t q_pos0,
-                                        const void *pool, const int32_t *kv_rows, int32_t n_kv,
-                                        const int32_t *kv_chunk, const void *chunk_cs, int32_t layout,
-                                        float scale, void *out, float *lse, irm_stream_t stream) {
+                                        const void *pool, int64_t pool_rows, const int32_t *kv_rows,
+                                        int32_t n_kv, const int32_t *kv_chunk, const void *chunk_cs,
+                                        int32_t layout, float scale, void *out, float *lse, irm_stream_t stream) {
     IRM_REQUIRE(n_q >= 0 && heads >= 1 && n_kv >= 1 && q_pos0 >= 0, "bad sizes");
     IRM_REQUIRE(q_pos0 + n_q <= (int64_t)n_kv, "queries must be positions < n_kv (q_pos0 + n_q <= n_kv)");
     IRM_REQUIRE(layout == IRM_LAYOUT_HALF_SPLIT || layout == IRM_LAYOUT_INTERLEAVED, "bad layout");
     IRM_REQUIRE(!kv_chunk || chunk_cs, "kv_chunk requires chunk_cs");
+    IRM_REQUIRE(pool_rows >= 1 && pool_rows < ((int64_t)1 << 31), "bad pool_rows");
+    IRM_REQUIRE(kv_rows || pool_rows >= n_kv, "pool_rows < n_kv with identity kv_rows");
     if (n_q == 0) return IRM_OK;
     IRM_REQUIRE(q && pool && out, "null pointer");
     IRM_REQUIRE((((uintptr_t)q | (uintptr_t)pool | (uintptr_t)out) & 15) == 0, "16-byte alignment required");
     IRM_REQUIRE(!chunk_cs || ((uintptr_t)chunk_cs & 15) == 0, "chunk_cs must be 16-byte aligned");
+    // pool as a 2-D tensor [pool_rows, 576] bf16 for TMA gather4: box = 64 columns x 1 row, SW128
+    auto encode = get_encode_fn();
+    if (!encode) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return IRM_ECUDA;
+    }
+    CUtensorMap tmap;
+    const cuuint64_t dims[2] = {(cuuint64_t)mla::DQK, (cuuint64_t)pool_rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)mla::DQK * 2};
+    const cuuint32_t box[2] = {64, 1};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(pool), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)cr);
+        return IRM_ECUDA;
+    }
     mla::Params p{};
     p.q = (const __nv_bfloat16 *)q;
     p.pool = (const __nv_bfloat16 *)pool;
@@ -482,7 +544,7 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
     const int smem = mla::SMEM_BYTES + 1024;
     IRM_CUDA_CHECK(cudaFuncSetAttribute(mla::mla_reattach_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t grid = (p.n_rows + mla::BM - 1) / mla::BM;
-    mla::mla_reattach_kernel<<<(unsigned)grid, mla::THREADS, smem, (cudaStream_t)stream>>>(p);
+    mla::mla_reattach_kernel<<<(unsigned)grid, mla::THREADS, smem, (cudaStream_t)stream>>>(p, tmap);
     IRM_LAUNCH_CHECK();
     return IRM_OK;
 }

@@ -287,7 +287,7 @@ def mla_reattach_prefill(q: torch.Tensor, pool: torch.Tensor, n_kv: int, q_pos0:
     if lse is None:
         lse = torch.empty(n_q, heads, dtype=torch.float32, device=q.device)
     rc = N.lib().irm_mla_reattach_prefill(
-        N.ptr(q), n_q, heads, q_pos0, N.ptr(pool), N.ptr(kv_rows), n_kv, N.ptr(kv_chunk), N.ptr(chunk_cs),
+        N.ptr(q), n_q, heads, q_pos0, N.ptr(pool), pool.shape[0], N.ptr(kv_rows), n_kv, N.ptr(kv_chunk), N.ptr(chunk_cs),
         layout, float(scale), N.ptr(out), N.ptr(lse), N.stream_ptr())
     N.check(rc, "irm_mla_reattach_prefill")
     return out, lse
