@@ -172,6 +172,15 @@ __device__ __forceinline__ void store_rope(const Params &p, uint8_t *tile, int p
     fence_proxy_async_smem();
 }
 
+// BN consecutive pool rows x 64 columns -> one SW128 piece
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *tmap, int col, int row, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(tmap), "r"(col), "r"(row), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // 4 arbitrary pool rows x 64 columns (128 B each) -> 512 B of a SW128 piece
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tmap, int col, int r0, int r1, int r2,
                                             int r3, uint64_t *bar) {
@@ -184,7 +193,8 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tma
 
 static_assert(BN * 4 == 2 * GROUP && BN * 8 == 4 * GROUP, "rope work split assumes 2 / 4 items per producer");
 
-__global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool) {
+__global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
+                                                                    const __grid_constant__ CUtensorMap tmap_tile) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     __shared__ __align__(8) uint64_t bar_q, bar_kv_full[NST], bar_kv_empty[NST], bar_s_full[2], bar_p_full[2],
@@ -264,6 +274,18 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
             c_wait += clock64() - a;
             if (lane == 0) mbar_arrive_expect_tx(&bar_kv_full[st], CKV_TX);
             __syncwarp();
+            // a run of BN consecutive pool rows (the common case: chunks are contiguous in
+            // the pool) goes as 8 tiled boxes; anything else as 64 gather4
+            const int row0 = __shfl_sync(0xffffffffu, row, 0);
+            if (__all_sync(0xffffffffu, row0 >= 0 && row == row0 + lane)) {
+                if (lane == 0) {
+                    const uint32_t dst = smem_u32(smem + SMEM_KV + st * KTILE);
+#pragma unroll
+                    for (int pc = 0; pc < 8; ++pc)
+                        tma_load_2d(dst + pc * KPIECE, &tmap_tile, 64 * pc, row0, &bar_kv_full[st]);
+                }
+                continue;
+            }
             const int r0 = __shfl_sync(0xffffffffu, row, 4 * (lane & 7));
             const int r1 = __shfl_sync(0xffffffffu, row, 4 * (lane & 7) + 1);
             const int r2 = __shfl_sync(0xffffffffu, row, 4 * (lane & 7) + 2);
@@ -514,17 +536,23 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
         set_error("cuTensorMapEncodeTiled unavailable");
         return IRM_ECUDA;
     }
-    CUtensorMap tmap;
-    const cuuint64_t dims[2] = {(cuuint64_t)mla::DQK, (cuuint64_t)pool_rows};
+    CUtensorMap tmap, tmap_tile;
     const cuuint64_t strides[1] = {(cuuint64_t)mla::DQK * 2};
-    const cuuint32_t box[2] = {64, 1};
     const cuuint32_t estr[2] = {1, 1};
-    CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(pool), dims, strides, box,
-                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed (%d)", (int)cr);
-        return IRM_ECUDA;
+    for (int which = 0; which < 2; ++which) {
+        // gather4 map: 64 columns x 1 row over the whole pool; tile map: 64 x BN rows over
+        // the keys' row range (identity map: n_kv rows, so rows past the end are zero-filled)
+        const cuuint64_t rows = which == 0 ? (cuuint64_t)pool_rows : (cuuint64_t)(kv_rows ? pool_rows : n_kv);
+        const cuuint64_t dims[2] = {(cuuint64_t)mla::DQK, rows};
+        const cuuint32_t box[2] = {64, which == 0 ? 1u : (cuuint32_t)mla::BN};
+        CUresult cr = encode(which == 0 ? &tmap : &tmap_tile, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                             const_cast<void *>(pool), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled failed (%d)", (int)cr);
+            return IRM_ECUDA;
+        }
     }
     mla::Params p{};
     p.q = (const __nv_bfloat16 *)q;
@@ -544,7 +572,7 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
     const int smem = mla::SMEM_BYTES + 1024;
     IRM_CUDA_CHECK(cudaFuncSetAttribute(mla::mla_reattach_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t grid = (p.n_rows + mla::BM - 1) / mla::BM;
-    mla::mla_reattach_kernel<<<(unsigned)grid, mla::THREADS, smem, (cudaStream_t)stream>>>(p, tmap);
+    mla::mla_reattach_kernel<<<(unsigned)grid, mla::THREADS, smem, (cudaStream_t)stream>>>(p, tmap, tmap_tile);
     IRM_LAUNCH_CHECK();
     return IRM_OK;
 }
