@@ -306,7 +306,7 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
     from paper_2605_05696_b200 import _native as N, ops
 
     rng = np.random.default_rng(35)
-    doc, n_docs, prefix = 1024, 63, 512
+    doc, n_docs, prefix = 960, 63, 512  # 63 x (960 + 64-token marker) + 512 = 65,024; 512 novel tail
     seg = doc + 64
     src_start = prefix + np.arange(n_docs) * seg  # cached layout
     perm = rng.permutation(n_docs)
