@@ -131,7 +131,12 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.sharded:
+        if world == 1:  # single-rank group for the K6 path at N=1
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     hbm, tf_burst, tf_sust, peak_kind = peaks()
@@ -176,14 +181,22 @@ def run_ours(args):
     max_pins = max(int(p[2][-1]) for p in packed)
     pipe = ReattachPipeline(store, pool, inv, R, max_tok, max_pins, req_stride, layout=N.LAYOUT_INTERLEAVED)
 
+    sharded = world > 1 or args.sharded
+    if sharded:  # K6: hash-sharded store + replica cache, eager steps (host all-to-all splits)
+        from paper_2605_05696_b200 import shard
+
+        pipe.enable_sharding(shard.ShardedStore(store), shard.ReplicaCache(pool, replica_base=pool_rows // 2),
+                             rank, world)
+        step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_sharded(i, allocate_rows=cold))
+    else:
+        step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_eager() if cold else pipe.replay())
     # cold request wave: inserts the body (its pool rows hold the random latents)
-    pipe.load(*dev_in[-1])
-    pipe.step_eager()
+    step(len(dev_in) - 1, cold=True)
     torch.cuda.synchronize()
-    pipe.capture()  # one CUDA graph per step (+ K1-only / K4-only graphs for component timing)
+    if not sharded:
+        pipe.capture()  # one CUDA graph per step (+ K1-only / K4-only graphs for component timing)
     for i in range(args.warmup):
-        pipe.load(*dev_in[i])
-        pipe.replay()
+        step(i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -197,8 +210,7 @@ def run_ours(args):
             dist.barrier()
         t0.record()
         for i in range(args.steps):
-            pipe.load(*dev_in[args.warmup + i])
-            pipe.replay()
+            step(args.warmup + i)
             lens.append(pipe.length.sum())  # device-side reduction, read after the timed region
         t1.record()
         torch.cuda.synchronize()
@@ -226,11 +238,22 @@ def run_ours(args):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / n
 
-    pipe.load(*dev_in[args.warmup])
-    pipe.replay()
+    step(args.warmup)
+    torch.cuda.synchronize()
     k4_rows = int(pipe.length.sum().item()) * LAYERS
-    k1 = time_graph(pipe.graph_k1)
-    k4 = time_graph(pipe.graph_k4)
+    if sharded:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        pipe.k1()
+        ev[1].record()
+        ev[2].record()
+        pipe.k4()
+        ev[3].record()
+        torch.cuda.synchronize()
+        k1, k4 = ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])
+    else:
+        k1 = time_graph(pipe.graph_k1)
+        k4 = time_graph(pipe.graph_k4)
 
     # -------- e2e: the same pipeline fed from pinned host buffers, result read back
     bi = sum(t.numel() * t.element_size() for t in host_in[0])
@@ -241,7 +264,7 @@ def run_ours(args):
     e0.record()
     for i in range(args.steps):
         pipe.load(*host_in[args.warmup + i])  # H2D from pinned memory
-        pipe.replay()
+        pipe.step_sharded(args.warmup + i) if sharded else pipe.replay()
         res[i].copy_(pipe.hit, non_blocking=True)  # D2H of the per-chunk service result
         bo = pipe.hit.numel() * pipe.hit.element_size()
     e1.record()
@@ -268,7 +291,7 @@ def run_ours(args):
                                "DSv2 interleaved rotary theta 1e4, 32K-token agent_meta prompts",
                    "requests_per_step": R, "tokens_per_request": tok_per_wave // R + HEADER,
                    "layers": LAYERS, "l2": "inputs larger than L2 (1.0 GB pool, 8 GB KV out per step)",
-                   "parallelism": f"sessions s mod G over {world} GPU(s)"},
+                   "parallelism": f"sessions s mod G over {world} GPU(s)" + (", store sharded by fp prefix, NCCL all-to-all lookup" if sharded else "")},
         "roofline": {"bound": "hbm", "kernel": "irm_rotate_gather (K4)", "achieved": k4_gbs,
                      "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": None,
                      "peak_kind": peak_kind, "launch_ms": k4, "algorithmic_bytes": k4_bytes},
@@ -287,7 +310,7 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(args, packed[0], sample_requests=R - 1)
     if rank == 0:
         print(json.dumps(line))
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -443,6 +466,7 @@ def main():
     ap.add_argument("--requests", type=int, default=R_PER_WAVE)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-attn", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="K6 sharded-store path even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -85,6 +85,49 @@ class ReattachPipeline:
         self.k3()
         self.k4()
 
+    # ------------------------------------------------------------ multi-GPU (K6)
+    def enable_sharding(self, sharded_store, replica_cache, rank: int, world: int):
+        """Route K3 through the hash-sharded store (shard.ShardedStore) and K4's
+        sources through the replica cache. Steps then run eagerly: the
+        all-to-all split sizes are host values."""
+        self.sharded, self.replica, self.rank, self.world = sharded_store, replica_cache, rank, world
+        self.hint_next = 0
+
+    def k3_sharded(self, wave: int, allocate_rows: bool):
+        from . import shard
+
+        t = self.table
+        cap = t.start.numel()
+        dev = t.start.device
+        idx = torch.arange(cap, device=dev)
+        req = torch.searchsorted(t.chunk_off[1:], idx, right=True)
+        valid = idx < t.chunk_off[-1]
+        self.reqc = torch.clamp(req, max=self.R - 1)
+        self.p_abs = self.m[self.reqc] + t.start.to(torch.int64)
+        probe = valid & (self.p_abs >= self.carve)
+        # global order: (global request = (wave * R + r) * G + rank, chunk index within the request)
+        g_req = (wave * self.R + self.reqc) * self.world + self.rank
+        order = (g_req << 20) | (idx - t.chunk_off[self.reqc])
+        ln = t.length.to(torch.int64) * probe
+        if allocate_rows:  # this rank keeps the KV of chunks it may be first to write
+            local = self.hint_next + torch.cumsum(ln, 0) - ln
+            self.hint_next += int(ln.sum().item())
+        else:
+            local = torch.zeros_like(ln)
+        hint = shard.encode_row(self.rank, local)
+        hit, self.p_src, grow, _own = self.sharded.lookup_insert(t.fp, order, self.p_abs, t.length, probe, hint)
+        self.hit = hit
+        is_hit = hit == 1
+        self.length = torch.where(is_hit, t.length, torch.zeros_like(t.length))
+        self.src = self.replica.localize(torch.where(is_hit, grow, torch.full_like(grow, -1)), self.length)
+        self.dst = self.reqc * self.req_stride + self.p_abs
+        self.delta = self.p_abs - self.p_src
+
+    def step_sharded(self, wave: int, allocate_rows: bool = False):
+        self.k1()
+        self.k3_sharded(wave, allocate_rows)
+        self.k4()
+
     # ------------------------------------------------------------ graphs
     def capture(self, warmup: int = 2):
         """Capture the step (and K1-only / K4-only graphs for component timing)."""

@@ -155,3 +155,40 @@ def test_detect_spec(M):
     wrong = rotary.make_spec(5e4)
     bad = rotary.detect_spec(spec, lambda p: rotary.rotate(rotary.KrVector(rotary.probe_base_vector(64)), p, wrong))
     assert not bad.ok and bad.best_fit_theta == 5e4
+
+
+def test_sharded_store_single_rank_nccl(M):
+    """K6 exchange over NCCL (world 1) reproduces the plain device store."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2605_05696_b200 import shard
+
+    _, _, _, ops = M
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29537")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(8)
+        pool_fps = rng.integers(0, 2**64, size=50, dtype=np.uint64)
+        fps = pool_fps[rng.integers(0, 50, size=400)].view(np.int64)
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        order = np.arange(400, dtype=np.int64) * 3
+        p = rng.integers(0, 9999, size=400).astype(np.int64)
+        ln = rng.integers(1, 100, size=400).astype(np.int32)
+        plain = ops.ChunkStore(1024)
+        hit_a, _, ps_a, _ = plain.lookup_insert(d(fps), d(order), d(p), d(ln))
+        sh = shard.ShardedStore(ops.ChunkStore(1024))
+        hint = shard.encode_row(0, torch.arange(400, device="cuda") * 10)
+        hit_b, ps_b, row_b, own = sh.lookup_insert(d(fps), d(order), d(p), d(ln), None, hint)
+        assert torch.equal(hit_a.cpu(), hit_b.cpu()) and torch.equal(ps_a.cpu(), ps_b.cpu())
+        assert (own == 0).all()
+        first = {}
+        for i, (f, h, r) in enumerate(zip(fps.tolist(), hit_b.cpu().tolist(), row_b.cpu().tolist())):
+            if h == 0:
+                first[f] = int(hint[i])
+            assert r == first[f]
+    finally:
+        dist.destroy_process_group()

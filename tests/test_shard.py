@@ -1,0 +1,114 @@
+"""CPU, world size 2 over gloo: the hash-sharded store exchange (K6 host logic)
+equals one sequential first-writer-wins store over the union of all ranks'
+queries in global order (engine.py:197-223), and the replica cache fetches
+remote latent rows once with the right contents."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2605_05696_b200 import shard
+
+WORLD = 2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _queries(seed, n_total=600):
+    g = torch.Generator().manual_seed(seed)
+    pool = torch.randint(-(2**62), 2**62, (120,), generator=g, dtype=torch.int64)
+    pool[0] = -1  # the all-ones fingerprint (EMPTY sentinel of the device table) is legal
+    fp = pool[torch.randint(0, 120, (n_total,), generator=g)]
+    order = torch.arange(n_total, dtype=torch.int64) * 7 + 3
+    p = torch.randint(0, 100000, (n_total,), generator=g)
+    ln = torch.randint(1, 300, (n_total,), generator=g, dtype=torch.int32)
+    probe = torch.rand(n_total, generator=g) > 0.1
+    rank_of = torch.arange(n_total) % WORLD  # sessions round-robin over ranks
+    return fp, order, p, ln, probe, rank_of
+
+
+def _worker(rank, port, seed, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    from dict_store import DictStore
+
+    try:
+        fp, order, p, ln, probe, rank_of = _queries(seed)
+        mine = torch.nonzero(rank_of == rank).flatten()
+        store = shard.ShardedStore(DictStore())
+        hint = shard.encode_row(rank, torch.arange(mine.numel(), dtype=torch.int64) * 1000)
+        res = []
+        for wave in range(3):  # three waves hitting the same sharded store
+            sl = mine[wave::3]
+            h, ps, row, own = store.lookup_insert(fp[sl], order[sl] + wave * 10**7, p[sl], ln[sl], probe[sl],
+                                                  hint[wave::3])
+            res.append((sl, h, ps, row, own))
+
+        # replica cache: pool rows hold (rank, row) stamps
+        pool = torch.zeros(2, 64, 3)
+        pool[:, :, 0] = rank
+        pool[:, :, 1] = torch.arange(64, dtype=torch.float32)
+        cache = shard.ReplicaCache(pool, replica_base=32)
+        other = 1 - rank
+        grow = shard.encode_row(other, torch.tensor([3, 10, 3, -1], dtype=torch.int64))
+        grow[3] = -1
+        local = cache.localize(grow, torch.tensor([4, 2, 4, 1]))
+        ok = bool(local[0] == local[2]) and cache.fetched_rows == 6
+        ok = ok and bool((pool[:, local[0]:local[0] + 4, 0] == other).all())
+        ok = ok and bool((pool[:, local[0]:local[0] + 4, 1] == torch.arange(3, 7).float()).all())
+        ok = ok and bool((pool[:, local[1]:local[1] + 2, 1] == torch.tensor([10.0, 11.0])).all())
+        again = cache.localize(grow, torch.tensor([4, 2, 4, 1]))  # cached: no new rows
+        ok = ok and cache.fetched_rows == 6 and bool((again == local).all())
+        out_q.put((rank, res, hint, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_sharded_store_matches_sequential(seed):
+    from dict_store import DictStore
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, seed, q)) for r in range(WORLD)]
+    for pr in procs:
+        pr.start()
+    outs = [q.get(timeout=240) for _ in range(WORLD)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    fp, order, p, ln, probe, rank_of = _queries(seed)
+    # sequential reference over the union, in global order (waves are time-ordered)
+    rows = []
+    for rank, res, hint, ok in outs:
+        assert ok, f"replica cache check failed on rank {rank}"
+        for wave, (sl, h, ps, row, own) in enumerate(res):
+            for k, i in enumerate(sl.tolist()):
+                rows.append((int(order[i]) + wave * 10**7, i, rank, int(h[k]), int(ps[k]), int(row[k]),
+                             int(hint[wave::3][k]), int(own[k])))
+    rows.sort()
+    ref = DictStore()
+    first_hint: dict[int, int] = {}
+    for ordk, i, rank, h, ps, row, hnt, own in rows:
+        if not probe[i]:
+            assert h == -1
+            continue
+        f = int(fp[i])
+        eh, _, eps, _ = ref.lookup_insert(fp[i:i + 1], torch.tensor([ordk]), p[i:i + 1], ln[i:i + 1])
+        assert h == int(eh[0]) and ps == int(eps[0]), (i, h, int(eh[0]))
+        if h == 0:
+            first_hint[f] = hnt
+        assert row == first_hint[f]  # every hit reads the first writer's rows
+        assert own == int(shard.owner_of(fp[i:i + 1], WORLD)[0])
