@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "tma.cuh"
 #include <cuda_bf16.h>
+#include <stdlib.h>
 
 namespace irm {
 
@@ -237,10 +238,10 @@ __global__ void rotate_rows_kernel(const T *__restrict__ rows, int64_t rs, T *__
 constexpr int RG_THREADS = 256;
 constexpr int RG_STAGES = 4;
 
-template <typename T, int ROWS>
+template <typename T, int ROWS, int STAGES = RG_STAGES>
 static int launch_tma(const GatherArgs &a, const typename Elem<T>::CS *cs, cudaStream_t st) {
-    auto kern = rotate_gather_tma_kernel<T, ROWS, RG_STAGES, RG_THREADS>;
-    const int smem = RG_STAGES * ROWS * a.row_bytes;
+    auto kern = rotate_gather_tma_kernel<T, ROWS, STAGES, RG_THREADS>;
+    const int smem = STAGES * ROWS * a.row_bytes;
     IRM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
     IRM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RG_THREADS, smem));
@@ -268,6 +269,15 @@ static int launch_gather(const GatherArgs &a, void *ws, const int64_t *delta, co
     if (tma_ok) {
         // rows per tile so that one pipeline stage is ~18 KB
         const int rows_fit = 18432 / a.row_bytes;
+        if (const char *v = getenv("IRM_RG_VARIANT")) {  // tuning hook: rows x stages
+            const int var = atoi(v);
+            if (var == 1) return launch_tma<T, 8, 8>(a, cs, st);
+            if (var == 2) return launch_tma<T, 16, 6>(a, cs, st);
+            if (var == 3) return launch_tma<T, 32, 3>(a, cs, st);
+            if (var == 4) return launch_tma<T, 32, 4>(a, cs, st);
+            if (var == 5) return launch_tma<T, 8, 12>(a, cs, st);
+            if (var == 6) return launch_tma<T, 16, 8>(a, cs, st);
+        }
         if (rows_fit >= 32) return launch_tma<T, 32>(a, cs, st);
         if (rows_fit >= 16) return launch_tma<T, 16>(a, cs, st);
         if (rows_fit >= 8) return launch_tma<T, 8>(a, cs, st);
