@@ -132,14 +132,16 @@ int irm_store_lookup(const irm_store_view *st, const uint64_t *q_fp, int64_t n, 
  * R(delta[c]) (angle = delta * inv_freq[j] in fp64, rotary.py:98-108).
  * pool/out element (row r, layer l) at base + (l*layer_stride + r) * row_dim.
  * dtype: element type of pool and out. out_round: IRM_ROUND_* applied to
- * the rotated values (f64 pools only; BF16E/F32 store emulation). */
+ * the rotated values (f64 pools only; BF16E/F32 store emulation).
+ * n_chunks_dev (nullable): device-side count of the leading chunks to process
+ * (<= n_chunks), so a compacted hit list needs no host synchronisation. */
 int64_t irm_rotate_gather_workspace_bytes(int64_t n_chunks, int32_t kr_dim);
 int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, void *out,
                       int64_t out_layer_stride, int32_t layers, int32_t ckv_dim, int32_t kr_dim,
                       const int64_t *src_row, const int64_t *dst_row, const int32_t *len,
-                      const int64_t *delta, int64_t n_chunks, const double *inv_freq,
-                      int32_t layout, int32_t dtype, int32_t out_round, void *ws,
-                      int64_t ws_bytes, irm_stream_t stream);
+                      const int64_t *delta, int64_t n_chunks, const int64_t *n_chunks_dev,
+                      const double *inv_freq, int32_t layout, int32_t dtype, int32_t out_round,
+                      void *ws, int64_t ws_bytes, irm_stream_t stream);
 /* Per-row absolute rotation (producer side of the store, registry.py:131-133
  * with rotary.py:98-108): out[i] = R(positions[i]) rows[i] for the dim-wide
  * rotary rows at rows + i*row_stride (elements). out may alias rows. */

@@ -102,6 +102,7 @@ struct GatherArgs {
     const int64_t *src_row, *dst_row, *delta;
     const int32_t *len;
     int64_t n_chunks, n_items;
+    const int64_t *n_dev;  // optional device-side chunk count (<= n_chunks): graph-friendly compaction
     int32_t layout, round;
 };
 
@@ -136,6 +137,7 @@ struct TileIter {
 template <typename T, int ROWS, int STAGES, int THREADS>
 __global__ void __launch_bounds__(THREADS)
 rotate_gather_tma_kernel(GatherArgs a, const typename Elem<T>::CS *__restrict__ cs) {
+    if (a.n_dev) a.n_items = min(a.n_chunks, *a.n_dev) * a.layers;
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t full[STAGES];
     const int64_t stage_bytes = (int64_t)ROWS * a.row_bytes;
@@ -199,6 +201,7 @@ rotate_gather_tma_kernel(GatherArgs a, const typename Elem<T>::CS *__restrict__ 
 // any dims / alignment: one CTA per (chunk, layer) item, one warp per row
 template <typename T>
 __global__ void rotate_gather_generic_kernel(GatherArgs a, const typename Elem<T>::CS *__restrict__ cs) {
+    if (a.n_dev) a.n_items = min(a.n_chunks, *a.n_dev) * a.layers;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const int row_elems = a.ckv + a.kr, half = a.kr / 2;
     for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -304,8 +307,9 @@ extern "C" int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, vo
                                  int64_t out_layer_stride, int32_t layers, int32_t ckv_dim,
                                  int32_t kr_dim, const int64_t *src_row, const int64_t *dst_row,
                                  const int32_t *len, const int64_t *delta, int64_t n_chunks,
-                                 const double *inv_freq, int32_t layout, int32_t dtype,
-                                 int32_t out_round, void *ws, int64_t ws_bytes, irm_stream_t stream) {
+                                 const int64_t *n_chunks_dev, const double *inv_freq, int32_t layout,
+                                 int32_t dtype, int32_t out_round, void *ws, int64_t ws_bytes,
+                                 irm_stream_t stream) {
     IRM_REQUIRE(n_chunks >= 0 && layers >= 1 && ckv_dim >= 0 && kr_dim >= 0 && kr_dim % 2 == 0,
                 "bad sizes (layers >= 1, kr_dim even)");
     IRM_REQUIRE(layout == IRM_LAYOUT_HALF_SPLIT || layout == IRM_LAYOUT_INTERLEAVED, "bad layout");
@@ -335,6 +339,7 @@ extern "C" int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, vo
     a.len = len;
     a.n_chunks = n_chunks;
     a.n_items = n_chunks * layers;
+    a.n_dev = n_chunks_dev;
     a.layout = layout;
     a.round = out_round;
     cudaStream_t st = (cudaStream_t)stream;

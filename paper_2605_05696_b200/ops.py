@@ -155,8 +155,10 @@ def inv_freq_device(inv_freq) -> torch.Tensor:
 def rotate_gather(pool: torch.Tensor, out: torch.Tensor, src_row: torch.Tensor, dst_row: torch.Tensor,
                   length: torch.Tensor, delta: torch.Tensor, inv_freq: torch.Tensor,
                   ckv_dim: int = 512, kr_dim: int = 64, layout: int = N.LAYOUT_HALF_SPLIT,
-                  out_round: int = N.ROUND_NONE, ws: torch.Tensor | None = None) -> None:
-    """K4. pool [layers, pool_rows, ckv+kr], out [layers, out_rows, ckv+kr] (same dtype)."""
+                  out_round: int = N.ROUND_NONE, ws: torch.Tensor | None = None,
+                  n_dev: torch.Tensor | None = None) -> None:
+    """K4. pool [layers, pool_rows, ckv+kr], out [layers, out_rows, ckv+kr] (same dtype).
+    ``n_dev`` (int64 [1], device): process only the first n_dev[0] chunks."""
     assert pool.dtype == out.dtype and pool.is_contiguous() and out.is_contiguous()
     assert pool.dim() == 3 and out.dim() == 3 and pool.shape[0] == out.shape[0]
     assert pool.shape[2] == ckv_dim + kr_dim == out.shape[2]
@@ -166,7 +168,7 @@ def rotate_gather(pool: torch.Tensor, out: torch.Tensor, src_row: torch.Tensor, 
         ws = torch.empty(max(need, 256), dtype=torch.uint8, device=pool.device)
     rc = N.lib().irm_rotate_gather(
         N.ptr(pool), pool.shape[1], N.ptr(out), out.shape[1], pool.shape[0], ckv_dim, kr_dim,
-        N.ptr(src_row), N.ptr(dst_row), N.ptr(length), N.ptr(delta), n, N.ptr(inv_freq), layout,
+        N.ptr(src_row), N.ptr(dst_row), N.ptr(length), N.ptr(delta), n, N.ptr(n_dev), N.ptr(inv_freq), layout,
         _DTYPE_CODE[pool.dtype], out_round, N.ptr(ws), ws.numel(), N.stream_ptr())
     N.check(rc, "irm_rotate_gather")
 

@@ -72,13 +72,19 @@ class ReattachPipeline:
                                                                               t.length, probe)
         is_hit = self.hit == 1
         self.length = torch.where(is_hit, t.length, torch.zeros_like(t.length))
-        self.src = torch.where(is_hit, self.row, torch.zeros_like(self.row))
-        self.dst = self.reqc * self.req_stride + self.p_abs
-        self.delta = self.p_abs - self.p_src
+        self._compact(is_hit, self.row, self.reqc * self.req_stride + self.p_abs, self.p_abs - self.p_src)
+
+    def _compact(self, is_hit, src, dst, delta):
+        """PIC hits first (stable), with their count left on the device: K4 then
+        walks only real work and the step stays free of host synchronisation."""
+        perm = torch.argsort((~is_hit).to(torch.int8), stable=True)
+        self.k4_src, self.k4_dst = src[perm], dst[perm]
+        self.k4_len, self.k4_delta = self.length[perm], delta[perm]
+        self.n_hit = is_hit.sum().reshape(1).to(torch.int64)
 
     def k4(self):
-        ops.rotate_gather(self.pool, self.out, self.src, self.dst, self.length, self.delta, self.inv,
-                          self.ckv, self.kr, self.layout, ws=self.gather_ws)
+        ops.rotate_gather(self.pool, self.out, self.k4_src, self.k4_dst, self.k4_len, self.k4_delta, self.inv,
+                          self.ckv, self.kr, self.layout, ws=self.gather_ws, n_dev=self.n_hit)
 
     def step_eager(self):
         self.k1()
@@ -119,9 +125,8 @@ class ReattachPipeline:
         self.hit = hit
         is_hit = hit == 1
         self.length = torch.where(is_hit, t.length, torch.zeros_like(t.length))
-        self.src = self.replica.localize(torch.where(is_hit, grow, torch.full_like(grow, -1)), self.length)
-        self.dst = self.reqc * self.req_stride + self.p_abs
-        self.delta = self.p_abs - self.p_src
+        src = self.replica.localize(torch.where(is_hit, grow, torch.full_like(grow, -1)), self.length)
+        self._compact(is_hit, src, self.reqc * self.req_stride + self.p_abs, self.p_abs - self.p_src)
 
     def step_sharded(self, wave: int, allocate_rows: bool = False):
         self.k1()

@@ -49,12 +49,12 @@ def test_cdc_capacity_error():
 def test_rotate_validation():
     L = N.lib()
     # odd rotary dim, bad layout, rounding on a non-f64 pool
-    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 63, None, None, None, None, 1, None, 0, 0, 0, None, 0, None) == N.IRM_EINVAL
-    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 1, None, 7, 0, 0, None, 0, None) == N.IRM_EINVAL
-    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 1, None, 0, N.DTYPE_BF16, N.ROUND_BF16, None, 0, None) == N.IRM_EINVAL
+    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 63, None, None, None, None, 1, None, None, 0, 0, 0, None, 0, None) == N.IRM_EINVAL
+    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 1, None, None, 7, 0, 0, None, 0, None) == N.IRM_EINVAL
+    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 1, None, None, 0, N.DTYPE_BF16, N.ROUND_BF16, None, 0, None) == N.IRM_EINVAL
     assert L.irm_rotate_rows(None, 0, None, 0, 4, 63, None, None, 0, 0, 0, None) == N.IRM_EINVAL
     # zero work is a no-op success
-    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 0, None, 0, 0, 0, None, 0, None) == N.IRM_OK
+    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 0, None, None, 0, 0, 0, None, 0, None) == N.IRM_OK
 
 
 def test_store_view_validation():
