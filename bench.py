@@ -51,6 +51,16 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per K4 launch, from the committed
+    ncu --set full capture of this same workload (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return float(json.load(f)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------- workload
 def make_wave(rng, header, marker, body, n_req):
     """Token streams of one wave plus the host-side phase-1 prefix length m
@@ -293,7 +303,7 @@ def run_ours(args):
                    "layers": LAYERS, "l2": "inputs larger than L2 (1.0 GB pool, 8 GB KV out per step)",
                    "parallelism": f"sessions s mod G over {world} GPU(s)" + (", store sharded by fp prefix, NCCL all-to-all lookup" if sharded else "")},
         "roofline": {"bound": "hbm", "kernel": "irm_rotate_gather (K4)", "achieved": k4_gbs,
-                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": None,
+                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": ncu_traffic(),
                      "peak_kind": peak_kind, "launch_ms": k4, "algorithmic_bytes": k4_bytes},
         "components": {
             "cdc_hash": {"value": tok_per_wave / (k1 / 1e3), "unit": "tokens/s", "kernel": "irm_cdc_xxh64 (K1)",
