@@ -132,17 +132,16 @@ class ReplicaCache:
     def localize(self, grow: torch.Tensor, length: torch.Tensor) -> torch.Tensor:
         """grow [n] global rows (or -1), length [n] -> local rows (int64)."""
         dev = grow.device
-        g = grow.cpu().tolist()
-        ln = length.cpu().tolist()
         need: list[list[tuple[int, int]]] = [[] for _ in range(self.world)]
-        seen = set()
-        for gr, l in zip(g, ln):
-            if gr < 0:
-                continue
-            rk = gr >> ROW_SHIFT
-            if rk != self.rank and gr not in self.map and gr not in seen:
-                need[rk].append((gr & ROW_MASK, l))
-                seen.add(gr)
+        gt = grow.to(torch.int64)
+        remote = (gt >= 0) & ((gt >> ROW_SHIFT) != self.rank)
+        if bool(remote.any()):
+            uniq, inv = torch.unique(gt[remote], return_inverse=True)
+            first = torch.full((uniq.numel(),), -1, dtype=torch.int64, device=dev)
+            first.scatter_reduce_(0, inv, length.to(torch.int64)[remote], reduce="amax", include_self=False)
+            for gr, l in zip(uniq.cpu().tolist(), first.cpu().tolist()):
+                if gr not in self.map:
+                    need[gr >> ROW_SHIFT].append((gr & ROW_MASK, l))
         # 1. request counts and (row, len) requests
         counts = torch.tensor([len(x) for x in need], dtype=torch.int64, device=dev)
         recv_counts = torch.empty_like(counts)
@@ -186,13 +185,14 @@ class ReplicaCache:
                 off += l
         self.next += total
         self.fetched_rows += total
-        # 5. map every hit to a local row
-        out = []
-        for gr in g:
-            if gr < 0:
-                out.append(0)
-            elif (gr >> ROW_SHIFT) == self.rank:
-                out.append(gr & ROW_MASK)
-            else:
-                out.append(self.map[gr])
-        return torch.tensor(out, dtype=torch.int64, device=dev)
+        # 5. map every hit to a local row (vectorised: own rows pass through, remote run
+        #    starts are translated with one searchsorted over the replica map)
+        gt = grow.to(torch.int64)
+        out = torch.where((gt >> ROW_SHIFT) == self.rank, gt & ROW_MASK, torch.zeros_like(gt))
+        remote = (gt >= 0) & ((gt >> ROW_SHIFT) != self.rank)
+        if bool(remote.any()):
+            keys = torch.tensor(sorted(self.map), dtype=torch.int64, device=dev)
+            vals = torch.tensor([self.map[k] for k in sorted(self.map)], dtype=torch.int64, device=dev)
+            pos = torch.searchsorted(keys, gt[remote]).clamp_max(keys.numel() - 1)
+            out[remote] = vals[pos]
+        return out
