@@ -24,6 +24,7 @@
 // 4-11 producers (cp.async + rotate), 12 the single-thread MMA issuer.
 #include "common.cuh"
 #include "tcgen05.cuh"
+#include "cluster.cuh"
 #include <cuda_bf16.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -479,6 +480,322 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
     if (warp == W_MMA) tc::tmem_dealloc(tbase, 512);
 }
 
+// ============================================================================
+// CTA-pair (cta_group::2) variant: one cluster of 2 CTAs owns 128 rows and a
+// 64-key tile per step. The leader CTA issues M = 128 MMAs whose A operand is
+// split by rows (each CTA holds its 64 Q / P rows) and whose B operand is split
+// by N (QK: each CTA holds 32 of the 64 keys; PV: each CTA holds 128 of each
+// 256 latent dims). D lands in each CTA's TMEM in the 2x2 layout: S [64 x 64]
+// in 32 columns (lanes 0-63 keys 0-31, lanes 64-127 keys 32-63), O [64 x 512]
+// in 256 columns. Full tensor-core rate per SM, half the smem operand traffic
+// per FLOP of the M = 64 kernel.
+namespace p2 {
+
+constexpr int PBN = 64;                     // keys per pair tile (QK N)
+constexpr int VPIECE = PBN * 128;           // 8 KB: 64 keys x 64 dims
+constexpr int VTILE = 4 * VPIECE;           // this CTA's 256 latent dims of the tile
+constexpr int KST = 2, VST = 2;             // ring stages
+constexpr int PTILE2 = 64 * 128;            // P [64 rows x 64 keys] bf16, SW128
+constexpr int S_Q = 0, S_K = NPIECE * QPIECE, S_V = S_K + KST * KTILE, S_P = S_V + VST * VTILE;
+constexpr int SMEM2 = S_P + 2 * PTILE2;     // 224 KB
+constexpr int W_KTMA = 8, W_MMA2 = 9, W_VTMA = 10;
+constexpr int THREADS2 = 32 * 11;
+constexpr uint32_t COL_S = 0, COL_O = 64;   // TMEM columns: S[2] x 32, O 2 x 128
+
+__device__ __forceinline__ void arrive_leader(uint64_t *bar, uint32_t rank) {
+    if (rank == 0) mbar_arrive(bar);
+    else cl::remote_arrive(cl::map_to(smem_u32(bar), 0));
+}
+
+// TMA of rows [k0, k0 + 32) of column piece `col_piece` into dst (a 32-row SW128 box)
+__device__ __forceinline__ void tma_rows32(const Params &p, const CUtensorMap *tm_g4, const CUtensorMap *tm_tile,
+                                           uint32_t dst, int col_piece, int k0, int lane, uint64_t *bar) {
+    const int k = k0 + lane;
+    const int row = k < p.n_kv ? (p.kv_rows ? __ldg(p.kv_rows + k) : k) : -1;
+    const int row0 = __shfl_sync(0xffffffffu, row, 0);
+    if (__all_sync(0xffffffffu, row0 >= 0 && row == row0 + lane)) {
+        if (lane == 0) tma_load_2d(dst, tm_tile, 64 * col_piece, row0, bar);
+        return;
+    }
+    const int g = lane & 7;
+    const int r0 = __shfl_sync(0xffffffffu, row, 4 * g), r1 = __shfl_sync(0xffffffffu, row, 4 * g + 1);
+    const int r2 = __shfl_sync(0xffffffffu, row, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, row, 4 * g + 3);
+    if (lane < 8) tma_gather4(dst + lane * 512, tm_g4, 64 * col_piece, r0, r1, r2, r3, bar);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
+mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
+                        const __grid_constant__ CUtensorMap tmap_tile) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t b_q, b_qpair, b_kfull[KST], b_kpair[KST], b_vfull[VST], b_vpair[VST],
+        b_kempty[KST], b_vempty[VST], b_sfull[2], b_pfull[2], b_odone[2];
+    __shared__ float sx[2][2][64];  // row-max exchange between the two key halves
+    __shared__ float sl[2][64];     // final row-sum exchange
+    __shared__ uint32_t tmem_base;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cl::cta_rank();
+    const int64_t prow0 = (int64_t)(blockIdx.x >> 1) * 128;  // first row of the pair
+    const int64_t row0 = prow0 + 64 * rank;                 // first row of this CTA
+    const int64_t last_row = min(p.n_rows, prow0 + 128) - 1;
+    const int64_t max_pos = p.q_pos0 + last_row / p.heads;
+    const int n_keys = (int)min((int64_t)p.n_kv, max_pos + 1);
+    const int T = (n_keys + PBN - 1) / PBN;
+    const int toff = (int)(((uint32_t)(blockIdx.x >> 1) * 2654435761u) % (uint32_t)T);
+
+    if (threadIdx.x == 0) {
+        mbar_init(&b_q, 128);
+        mbar_init(&b_qpair, 1);
+        for (int s = 0; s < KST; ++s) {
+            mbar_init(&b_kfull[s], 1 + GROUP);  // TMA expect_tx + the rope group
+            mbar_init(&b_kpair[s], 1);
+            mbar_init(&b_kempty[s], 1);
+        }
+        for (int s = 0; s < VST; ++s) {
+            mbar_init(&b_vfull[s], 1);
+            mbar_init(&b_vpair[s], 1);
+            mbar_init(&b_vempty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&b_sfull[s], 1);
+            mbar_init(&b_pfull[s], 256);  // both CTAs' softmax threads (leader's barrier)
+            mbar_init(&b_odone[s], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == W_MMA2) tc2::tmem_alloc(&tmem_base, 512);
+    tc::fence_before();
+    cl::cluster_sync();
+    tc::fence_after();
+    const uint32_t tbase = tmem_base;
+
+    if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------ Q (once) + rope of this CTA's 32 keys
+        const int ptid = threadIdx.x - 128;
+        const uint32_t qbase = smem_u32(smem + S_Q);
+        for (int i = ptid; i < 64 * 72; i += 128) {
+            const int r = i / 72, c = i % 72;
+            const int64_t grow = row0 + r;
+            const bool ok = grow < p.n_rows;
+            cp_async16(qbase + (c >> 3) * QPIECE + swz128(r, c & 7), p.q + (ok ? grow : 0) * DQK + c * 8, ok ? 16u : 0u);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        fence_proxy_async_smem();
+        mbar_arrive(&b_q);
+        const int g = ptid / GROUP, gtid = ptid % GROUP;  // group g owns K stage g
+        for (int t = g; t < T; t += KST) {
+            const int kt = (t + toff) % T;
+            RopeRegs rr;
+            rope_fetch(p, 2 * kt + (int)rank, gtid, rr);  // keys kt*64 + 32*rank + [0, 32)
+            if (t >= KST) mbar_wait(&b_kempty[g], ((t / KST) - 1) & 1);
+            store_rope(p, smem + S_K + g * KTILE, gtid, rr);
+            mbar_arrive(&b_kfull[g]);
+        }
+    } else if (warp == W_KTMA) {
+        // ------------------------------------------------ c_KV of this CTA's 32 keys (QK operand)
+        for (int t = 0; t < T; ++t) {
+            const int st = t % KST, kt = (t + toff) % T;
+            if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
+            if (lane == 0) mbar_arrive_expect_tx(&b_kfull[st], CKV_TX);
+            __syncwarp();
+            const uint32_t dst = smem_u32(smem + S_K + st * KTILE);
+            for (int pc = 0; pc < 8; ++pc)
+                tma_rows32(p, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, kt * PBN + 32 * rank, lane, &b_kfull[st]);
+        }
+    } else if (warp == W_VTMA) {
+        // ------------------------------------------------ V: all 64 keys x this CTA's 256 latent dims
+        for (int t = 0; t < T; ++t) {
+            const int st = t % VST, kt = (t + toff) % T;
+            if (t >= VST) mbar_wait(&b_vempty[st], ((t / VST) - 1) & 1);
+            if (lane == 0) mbar_arrive_expect_tx(&b_vfull[st], (uint32_t)VTILE);
+            __syncwarp();
+            const uint32_t dst = smem_u32(smem + S_V + st * VTILE);
+            for (int j = 0; j < 4; ++j) {
+                const int cpiece = (j >> 1) * 4 + 2 * (int)rank + (j & 1);  // dims [256h + 128 rank, +128)
+                for (int half = 0; half < 2; ++half)
+                    tma_rows32(p, &tmap_pool, &tmap_tile, dst + j * VPIECE + half * 4096, cpiece,
+                               kt * PBN + 32 * half, lane, &b_vfull[st]);
+            }
+        }
+    } else if (warp == W_MMA2) {
+        if (rank != 0) {
+            // ------------------------------------------------ peer: relay local data readiness to the leader
+            const uint32_t q_l = cl::map_to(smem_u32(&b_qpair), 0);
+            mbar_wait(&b_q, 0);
+            if (lane == 0) cl::remote_arrive(q_l);
+            auto relay_k = [&](int t) {
+                mbar_wait(&b_kfull[t % KST], (t / KST) & 1);
+                if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_kpair[t % KST]), 0));
+            };
+            relay_k(0);
+            for (int t = 0; t < T; ++t) {
+                if (t + 1 < T) relay_k(t + 1);
+                mbar_wait(&b_vfull[t % VST], (t / VST) & 1);
+                if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_vpair[t % VST]), 0));
+            }
+        } else {
+            // ------------------------------------------------ leader: MMA issue for the pair
+            const uint32_t idesc_qk = tc::idesc_bf16(128, PBN, false, false);
+            const uint32_t idesc_pv = tc::idesc_bf16(128, 256, false, true);
+            const uint64_t q_desc = tc::smem_desc_sw128(smem_u32(smem + S_Q), 16, 1024);
+            const uint64_t k_desc = tc::smem_desc_sw128(smem_u32(smem + S_K), 16, 1024);
+            const uint64_t v_desc = tc::smem_desc_sw128(smem_u32(smem + S_V), VPIECE, 1024);
+            const uint64_t p_desc = tc::smem_desc_sw128(smem_u32(smem + S_P), 16, 1024);
+            mbar_wait(&b_q, 0);
+            cl::mbar_wait_cluster(&b_qpair, 0);
+            auto issue_qk = [&](int t) {
+                const int st = t % KST;
+                mbar_wait(&b_kfull[st], (t / KST) & 1);
+                cl::mbar_wait_cluster(&b_kpair[st], (t / KST) & 1);
+                tc::fence_after();
+                const uint64_t kd = k_desc + (uint64_t)((st * KTILE) >> 4);
+                if (tc::elect_one()) {
+#pragma unroll
+                    for (int pc = 0; pc < NPIECE; ++pc) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            tc2::mma_bf16_ss(tbase + COL_S + (t & 1) * 32, q_desc + (uint64_t)((pc * QPIECE + k * 32) >> 4),
+                                             kd + (uint64_t)((pc * KPIECE + k * 32) >> 4), idesc_qk, (pc | k) != 0);
+                    }
+                    tc2::commit_both(&b_sfull[t & 1]);
+                    tc2::commit_both(&b_kempty[st]);
+                }
+                __syncwarp();
+            };
+            issue_qk(0);
+            for (int t = 0; t < T; ++t) {
+                if (t + 1 < T) issue_qk(t + 1);
+                const int vs = t % VST;
+                cl::mbar_wait_cluster(&b_pfull[t & 1], (t >> 1) & 1);
+                mbar_wait(&b_vfull[vs], (t / VST) & 1);
+                cl::mbar_wait_cluster(&b_vpair[vs], (t / VST) & 1);
+                tc::fence_after();
+                const uint64_t pd = p_desc + (uint64_t)(((t & 1) * PTILE2) >> 4);
+                const uint64_t vd = v_desc + (uint64_t)((vs * VTILE) >> 4);
+                if (tc::elect_one()) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                        for (int k = 0; k < PBN / 16; ++k)
+                            tc2::mma_bf16_ss(tbase + COL_O + h * 128, pd + (uint64_t)((k * 32) >> 4),
+                                             vd + (uint64_t)((2 * h * VPIECE + k * 2048) >> 4), idesc_pv,
+                                             (t > 0 || k > 0) ? 1u : 0u);
+                    }
+                    tc2::commit_both(&b_vempty[vs]);
+                    tc2::commit_both(&b_odone[t & 1]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ------------------------------------------------ softmax / correction (warps 0-3)
+        const int w = warp;
+        const int r = 32 * (w & 1) + lane;  // row of this CTA
+        const int kh = w >> 1;              // key half (S) / latent-dim half (O)
+        const int64_t grow = row0 + r;
+        const bool row_ok = grow < p.n_rows;
+        const int64_t qpos = p.q_pos0 + (row_ok ? grow / p.heads : 0);
+        const uint32_t lane_base = tbase + ((uint32_t)(32 * w) << 16);
+        const uint32_t p_base = smem_u32(smem + S_P);
+        const uint32_t pfull_leader0 = cl::map_to(smem_u32(&b_pfull[0]), 0);
+        const uint32_t pfull_leader1 = cl::map_to(smem_u32(&b_pfull[1]), 0);
+        float m = -INFINITY, l = 0.f;
+        for (int t = 0; t < T; ++t) {
+            cl::mbar_wait_cluster(&b_sfull[t & 1], (t >> 1) & 1);
+            tc::fence_after();
+            uint32_t v[32];
+            tc2::ld_32x32b_x32(lane_base + COL_S + (t & 1) * 32, v);
+            tc::wait_ld();
+            const int64_t kbase = (int64_t)((t + toff) % T) * PBN + 32 * kh;
+            float s[32];
+            float mt = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int64_t key = kbase + i;
+                const bool ok = row_ok && key <= qpos && key < p.n_kv;
+                s[i] = ok ? __uint_as_float(v[i]) * p.scale_log2 : -INFINITY;
+                mt = fmaxf(mt, s[i]);
+            }
+            sx[t & 1][kh][r] = mt;  // exchange with the thread holding the other key half
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            mt = fmaxf(mt, sx[t & 1][kh ^ 1][r]);
+            float alpha = 1.f;
+            const float m_new = fmaxf(m, mt);
+            if (m_new > m + RESCALE_THRESHOLD) {
+                alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
+                m = m_new;
+            }
+            float lsum = 0.f;
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+                const float e0 = (s[i] == -INFINITY) ? 0.f : exp2f(s[i] - m);
+                const float e1 = (s[i + 1] == -INFINITY) ? 0.f : exp2f(s[i + 1] - m);
+                lsum += e0 + e1;
+                pk[i >> 1] = pack_bf2(e0, e1);
+            }
+            l = l * alpha + lsum;
+            if (t >= 2) cl::mbar_wait_cluster(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
+            if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
+                cl::mbar_wait_cluster(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV(0..t-1)
+                tc::fence_after();
+#pragma unroll 1
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t o[32];
+                    const uint32_t a = lane_base + COL_O + (c >> 2) * 128 + (c & 3) * 32;
+                    tc2::ld_32x32b_x32(a, o);
+                    tc::wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    tc2::st_32x32b_x32(a, o);
+                }
+                tc::wait_st();
+            }
+            const uint32_t pt = p_base + (t & 1) * PTILE2;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                sts128(pt + swz128(r, 4 * kh + j), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
+            fence_proxy_async_smem();
+            tc::fence_before();
+            if (rank == 0) mbar_arrive(&b_pfull[t & 1]);
+            else cl::remote_arrive((t & 1) ? pfull_leader1 : pfull_leader0);
+        }
+        // epilogue: O / l -> bf16, lse (l summed over the two key halves)
+        sl[kh][r] = l;
+        cl::mbar_wait_cluster(&b_odone[(T - 1) & 1], ((T - 1) >> 1) & 1);
+        tc::fence_after();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        l += sl[kh ^ 1][r];
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+            const int h = c >> 2, q = c & 3;
+            uint32_t o[32];
+            tc2::ld_32x32b_x32(lane_base + COL_O + h * 128 + q * 32, o);
+            tc::wait_ld();
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2)
+                pk[i >> 1] = pack_bf2(__uint_as_float(o[i]) * inv_l, __uint_as_float(o[i + 1]) * inv_l);
+            if (row_ok) {
+                uint4 *dst = reinterpret_cast<uint4 *>(p.out + grow * DV + 256 * h + 128 * kh + 32 * q);
+                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                dst[2] = make_uint4(pk[8], pk[9], pk[10], pk[11]);
+                dst[3] = make_uint4(pk[12], pk[13], pk[14], pk[15]);
+            }
+        }
+        if (row_ok && kh == 0 && p.lse) p.lse[grow] = (m + log2f(l)) * 0.69314718055994531f;
+    }
+    tc::fence_before();
+    cl::cluster_sync();
+    tc::fence_after();
+    if (warp == W_MMA2) tc2::tmem_dealloc(tbase, 512);
+}
+
+}  // namespace p2
+
 __global__ void cossin_kernel(const int64_t *__restrict__ delta, int64_t n_chunks,
                               const double *__restrict__ inv_freq, float2 *__restrict__ cs) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -569,6 +886,14 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
     p.q_pos0 = q_pos0;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.dbg = getenv("IRM_MLA_DEBUG") != nullptr;
+    if (getenv("IRM_MLA_1SM") == nullptr) {  // CTA-pair (cta_group::2) kernel: 128 rows per cluster
+        const int smem = mla::p2::SMEM2 + 1024;
+        IRM_CUDA_CHECK(cudaFuncSetAttribute(mla::p2::mla_reattach_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        const int64_t grid = 2 * ((p.n_rows + 127) / 128);
+        mla::p2::mla_reattach_2sm_kernel<<<(unsigned)grid, mla::p2::THREADS2, smem, (cudaStream_t)stream>>>(p, tmap, tmap_tile);
+        IRM_LAUNCH_CHECK();
+        return IRM_OK;
+    }
     const int smem = mla::SMEM_BYTES + 1024;
     IRM_CUDA_CHECK(cudaFuncSetAttribute(mla::mla_reattach_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t grid = (p.n_rows + mla::BM - 1) / mla::BM;
