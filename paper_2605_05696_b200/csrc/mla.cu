@@ -594,15 +594,20 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         }
     } else if (warp == W_KTMA) {
         // ------------------------------------------------ c_KV of this CTA's 32 keys (QK operand)
+        long long c_e = 0, c0 = clock64();
         for (int t = 0; t < T; ++t) {
             const int st = t % KST, kt = (t + toff) % T;
+            long long a0 = clock64();
             if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
+            c_e += clock64() - a0;
             if (lane == 0) mbar_arrive_expect_tx(&b_kfull[st], CKV_TX);
             __syncwarp();
             const uint32_t dst = smem_u32(smem + S_K + st * KTILE);
             for (int pc = 0; pc < 8; ++pc)
                 tma_rows32(p, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, kt * PBN + 32 * rank, lane, &b_kfull[st]);
         }
+        if (p.dbg && blockIdx.x < 2 && lane == 0)
+            printf("2sm ktma cta%d: wait_empty %lld total %lld\n", (int)rank, c_e, clock64() - c0);
     } else if (warp == W_VTMA) {
         // ------------------------------------------------ V: all 64 keys x this CTA's 256 latent dims
         for (int t = 0; t < T; ++t) {
@@ -644,10 +649,15 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             const uint64_t p_desc = tc::smem_desc_sw128(smem_u32(smem + S_P), 16, 1024);
             mbar_wait(&b_q, 0);
             cl::mbar_wait_cluster(&b_qpair, 0);
+            long long c_k = 0, c_kp = 0, c_p = 0, c_v = 0, c0 = clock64();
             auto issue_qk = [&](int t) {
                 const int st = t % KST;
+                long long a0 = clock64();
                 mbar_wait(&b_kfull[st], (t / KST) & 1);
+                long long a1 = clock64();
                 cl::mbar_wait_cluster(&b_kpair[st], (t / KST) & 1);
+                c_k += a1 - a0;
+                c_kp += clock64() - a1;
                 tc::fence_after();
                 const uint64_t kd = k_desc + (uint64_t)((st * KTILE) >> 4);
                 if (tc::elect_one()) {
@@ -667,9 +677,13 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             for (int t = 0; t < T; ++t) {
                 if (t + 1 < T) issue_qk(t + 1);
                 const int vs = t % VST;
+                long long a0 = clock64();
                 cl::mbar_wait_cluster(&b_pfull[t & 1], (t >> 1) & 1);
+                long long a1 = clock64();
                 mbar_wait(&b_vfull[vs], (t / VST) & 1);
                 cl::mbar_wait_cluster(&b_vpair[vs], (t / VST) & 1);
+                c_p += a1 - a0;
+                c_v += clock64() - a1;
                 tc::fence_after();
                 const uint64_t pd = p_desc + (uint64_t)(((t & 1) * PTILE2) >> 4);
                 const uint64_t vd = v_desc + (uint64_t)((vs * VTILE) >> 4);
@@ -687,6 +701,9 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 }
                 __syncwarp();
             }
+            if (p.dbg && blockIdx.x == 0 && lane == 0)
+                printf("2sm mma: wait_k %lld wait_kpair %lld wait_p %lld wait_v %lld total %lld T=%d\n", c_k, c_kp, c_p,
+                       c_v, clock64() - c0, T);
         }
     } else {
         // ------------------------------------------------ softmax / correction (warps 0-3)
@@ -701,8 +718,11 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         const uint32_t pfull_leader0 = cl::map_to(smem_u32(&b_pfull[0]), 0);
         const uint32_t pfull_leader1 = cl::map_to(smem_u32(&b_pfull[1]), 0);
         float m = -INFINITY, l = 0.f;
+        long long c_s = 0, c_o = 0, c_x = 0, c0 = clock64();
         for (int t = 0; t < T; ++t) {
+            long long a0 = clock64();
             cl::mbar_wait_cluster(&b_sfull[t & 1], (t >> 1) & 1);
+            c_s += clock64() - a0;
             tc::fence_after();
             uint32_t v[32];
             tc2::ld_32x32b_x32(lane_base + COL_S + (t & 1) * 32, v);
@@ -718,7 +738,9 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 mt = fmaxf(mt, s[i]);
             }
             sx[t & 1][kh][r] = mt;  // exchange with the thread holding the other key half
+            long long a1 = clock64();
             asm volatile("bar.sync 1, 128;" ::: "memory");
+            c_x += clock64() - a1;
             mt = fmaxf(mt, sx[t & 1][kh ^ 1][r]);
             float alpha = 1.f;
             const float m_new = fmaxf(m, mt);
@@ -736,7 +758,9 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 pk[i >> 1] = pack_bf2(e0, e1);
             }
             l = l * alpha + lsum;
+            long long a2 = clock64();
             if (t >= 2) cl::mbar_wait_cluster(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
+            c_o += clock64() - a2;
             if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
                 cl::mbar_wait_cluster(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV(0..t-1)
                 tc::fence_after();
@@ -761,6 +785,8 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             if (rank == 0) mbar_arrive(&b_pfull[t & 1]);
             else cl::remote_arrive((t & 1) ? pfull_leader1 : pfull_leader0);
         }
+        if (p.dbg && blockIdx.x < 2 && lane == 0 && w == 0)
+            printf("2sm softmax cta%d: wait_s %lld wait_o %lld xchg %lld total %lld\n", (int)rank, c_s, c_o, c_x, clock64() - c0);
         // epilogue: O / l -> bf16, lse (l summed over the two key halves)
         sl[kh][r] = l;
         cl::mbar_wait_cluster(&b_odone[(T - 1) & 1], ((T - 1) >> 1) & 1);
