@@ -559,7 +559,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&b_sfull[s], 1);
-            mbar_init(&b_pfull[s], 256);  // both CTAs' softmax threads (leader's barrier)
+            mbar_init(&b_pfull[s], 128 + 4);  // leader's 128 softmax threads + one per peer softmax warp
             mbar_init(&b_odone[s], 1);
         }
         fence_mbar_init();
@@ -782,8 +782,12 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 sts128(pt + swz128(r, 4 * kh + j), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
             fence_proxy_async_smem();
             tc::fence_before();
-            if (rank == 0) mbar_arrive(&b_pfull[t & 1]);
-            else cl::remote_arrive((t & 1) ? pfull_leader1 : pfull_leader0);
+            if (rank == 0) {
+                mbar_arrive(&b_pfull[t & 1]);
+            } else {  // one cluster-scope release per warp (a per-thread remote arrive serialises)
+                __syncwarp();
+                if (lane == 0) cl::remote_arrive((t & 1) ? pfull_leader1 : pfull_leader0);
+            }
         }
         if (p.dbg && blockIdx.x < 2 && lane == 0 && w == 0)
             printf("2sm softmax cta%d: wait_s %lld wait_o %lld xchg %lld total %lld\n", (int)rank, c_s, c_o, c_x, clock64() - c0);
