@@ -559,7 +559,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&b_sfull[s], 1);
-            mbar_init(&b_pfull[s], 128 + 4);  // leader's 128 softmax threads + one per peer softmax warp
+            mbar_init(&b_pfull[s], rank == 0 ? 128 + 1 : 128);  // local softmax threads (+ the peer's relay)
             mbar_init(&b_odone[s], 1);
         }
         fence_mbar_init();
@@ -634,8 +634,12 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_kpair[t % KST]), 0));
             };
             relay_k(0);
+            // forwarded in the leader's consumption order: K(t+1) for QK, then P(t) and V(t) for PV.
+            // A cluster-scope release costs ~1.5K cycles; doing it here keeps it off the softmax path.
             for (int t = 0; t < T; ++t) {
                 if (t + 1 < T) relay_k(t + 1);
+                mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
+                if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_pfull[t & 1]), 0));
                 mbar_wait(&b_vfull[t % VST], (t / VST) & 1);
                 if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_vpair[t % VST]), 0));
             }
@@ -718,7 +722,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         const uint32_t pfull_leader0 = cl::map_to(smem_u32(&b_pfull[0]), 0);
         const uint32_t pfull_leader1 = cl::map_to(smem_u32(&b_pfull[1]), 0);
         float m = -INFINITY, l = 0.f;
-        long long c_s = 0, c_o = 0, c_x = 0, c0 = clock64();
+        long long c_s = 0, c_o = 0, c_x = 0, c_r = 0, c_e = 0, c0 = clock64();
         for (int t = 0; t < T; ++t) {
             long long a0 = clock64();
             cl::mbar_wait_cluster(&b_sfull[t & 1], (t >> 1) & 1);
@@ -761,6 +765,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             long long a2 = clock64();
             if (t >= 2) cl::mbar_wait_cluster(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
             c_o += clock64() - a2;
+            long long a3 = clock64();
             if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
                 cl::mbar_wait_cluster(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV(0..t-1)
                 tc::fence_after();
@@ -776,21 +781,20 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 }
                 tc::wait_st();
             }
+            long long a4 = clock64();
+            c_r += a4 - a3;
             const uint32_t pt = p_base + (t & 1) * PTILE2;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 sts128(pt + swz128(r, 4 * kh + j), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
             fence_proxy_async_smem();
             tc::fence_before();
-            if (rank == 0) {
-                mbar_arrive(&b_pfull[t & 1]);
-            } else {  // one cluster-scope release per warp (a per-thread remote arrive serialises)
-                __syncwarp();
-                if (lane == 0) cl::remote_arrive((t & 1) ? pfull_leader1 : pfull_leader0);
-            }
+            mbar_arrive(&b_pfull[t & 1]);  // local; the peer's relay forwards it to the leader
+            c_e += clock64() - a4;
         }
         if (p.dbg && blockIdx.x < 2 && lane == 0 && w == 0)
-            printf("2sm softmax cta%d: wait_s %lld wait_o %lld xchg %lld total %lld\n", (int)rank, c_s, c_o, c_x, clock64() - c0);
+            printf("2sm softmax cta%d: wait_s %lld wait_o %lld xchg %lld rescale %lld pstore %lld total %lld\n", (int)rank,
+                   c_s, c_o, c_x, c_r, c_e, clock64() - c0);
         // epilogue: O / l -> bf16, lse (l summed over the two key halves)
         sl[kh][r] = l;
         cl::mbar_wait_cluster(&b_odone[(T - 1) & 1], ((T - 1) >> 1) & 1);
