@@ -85,6 +85,16 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ float ex2(float x) {  // 2^x, flush-to-zero; ex2(-inf) = 0
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Row max of raw scores with masked keys forced to -inf. Scores are scaled after the
+// max (scale > 0), so the exponent is one FFMA per element: ex2(v * scale_log2 - m).
+constexpr uint32_t NEG_INF_BITS = 0xff800000u;
+
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t *>(&v);
@@ -386,28 +396,34 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
             tc::ld_16x64b_x16(s_lane + (t & 1) * BN, v);
             tc::wait_ld();
             float s[16];
-            float mt = -INFINITY;
             const int64_t kbase = (int64_t)((t + toff) % T) * BN + b;
+            // the causal / length mask only touches diagonal and tail tiles
+            if (!__all_sync(0xffffffffu, row_ok && kbase + 30 <= qpos && kbase + 30 < p.n_kv)) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int64_t key = kbase + 2 * i;
-                const bool ok = row_ok && key <= qpos && key < p.n_kv;
-                s[i] = ok ? __uint_as_float(v[i]) * p.scale_log2 : -INFINITY;
-                mt = fmaxf(mt, s[i]);
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t key = kbase + 2 * i;
+                    if (!(row_ok && key <= qpos && key < p.n_kv)) v[i] = NEG_INF_BITS;
+                }
             }
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(v[i]));
+            float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
             mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
             float alpha = 1.f;
             const float m_new = fmaxf(m, mt);
             if (m_new > m + RESCALE_THRESHOLD) {  // lazy rescale: only when the max grows by > 2^8
-                alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
+                alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
                 m = m_new;
             }
-            float lsum = 0.f;
+            const float nm = (m == -INFINITY) ? 0.f : -m;  // fully masked so far: every v is -inf
+            float ls[2] = {0.f, 0.f};
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                s[i] = (s[i] == -INFINITY) ? 0.f : exp2f(s[i] - m);
-                lsum += s[i];
+                s[i] = ex2(fmaf(__uint_as_float(v[i]), p.scale_log2, nm));
+                ls[i & 1] += s[i];
             }
+            float lsum = ls[0] + ls[1];
             lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
             l = l * alpha + lsum;
             // pack P: pairs of adjacent keys, thread b = 0 takes keys 0..15, b = 1 keys 16..31
@@ -722,47 +738,55 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         const uint32_t pfull_leader0 = cl::map_to(smem_u32(&b_pfull[0]), 0);
         const uint32_t pfull_leader1 = cl::map_to(smem_u32(&b_pfull[1]), 0);
         float m = -INFINITY, l = 0.f;
-        long long c_s = 0, c_o = 0, c_x = 0, c_r = 0, c_e = 0, c0 = clock64();
+        long long c_s = 0, c_o = 0, c_x = 0, c_r = 0, c_e = 0, c_ld = 0, c_mx = 0, c_ex = 0, c0 = clock64();
         for (int t = 0; t < T; ++t) {
             long long a0 = clock64();
             cl::mbar_wait_cluster(&b_sfull[t & 1], (t >> 1) & 1);
             c_s += clock64() - a0;
             tc::fence_after();
             uint32_t v[32];
+            long long b0 = clock64();
             tc2::ld_32x32b_x32(lane_base + COL_S + (t & 1) * 32, v);
             tc::wait_ld();
+            long long b1 = clock64();
+            c_ld += b1 - b0;
             const int64_t kbase = (int64_t)((t + toff) % T) * PBN + 32 * kh;
-            float s[32];
-            float mt = -INFINITY;
+            if (!__all_sync(0xffffffffu, row_ok && kbase + 31 <= qpos && kbase + 31 < p.n_kv)) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int64_t key = kbase + i;
-                const bool ok = row_ok && key <= qpos && key < p.n_kv;
-                s[i] = ok ? __uint_as_float(v[i]) * p.scale_log2 : -INFINITY;
-                mt = fmaxf(mt, s[i]);
+                for (int i = 0; i < 32; ++i) {
+                    const int64_t key = kbase + i;
+                    if (!(row_ok && key <= qpos && key < p.n_kv)) v[i] = NEG_INF_BITS;
+                }
             }
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(v[i]));
+            float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
             sx[t & 1][kh][r] = mt;  // exchange with the thread holding the other key half
             long long a1 = clock64();
+            c_mx += a1 - b1;
             asm volatile("bar.sync 1, 128;" ::: "memory");
             c_x += clock64() - a1;
             mt = fmaxf(mt, sx[t & 1][kh ^ 1][r]);
             float alpha = 1.f;
             const float m_new = fmaxf(m, mt);
             if (m_new > m + RESCALE_THRESHOLD) {
-                alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
+                alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
                 m = m_new;
             }
-            float lsum = 0.f;
+            const float nm = (m == -INFINITY) ? 0.f : -m;  // fully masked so far: every v is -inf
+            float ls[2] = {0.f, 0.f};
             uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
-                const float e0 = (s[i] == -INFINITY) ? 0.f : exp2f(s[i] - m);
-                const float e1 = (s[i + 1] == -INFINITY) ? 0.f : exp2f(s[i + 1] - m);
-                lsum += e0 + e1;
+                const float e0 = ex2(fmaf(__uint_as_float(v[i]), p.scale_log2, nm));
+                const float e1 = ex2(fmaf(__uint_as_float(v[i + 1]), p.scale_log2, nm));
+                ls[(i >> 1) & 1] += e0 + e1;
                 pk[i >> 1] = pack_bf2(e0, e1);
             }
-            l = l * alpha + lsum;
+            l = l * alpha + (ls[0] + ls[1]);
             long long a2 = clock64();
+            c_ex += a2 - a1;
             if (t >= 2) cl::mbar_wait_cluster(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
             c_o += clock64() - a2;
             long long a3 = clock64();
@@ -793,8 +817,8 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             c_e += clock64() - a4;
         }
         if (p.dbg && blockIdx.x < 2 && lane == 0 && w == 0)
-            printf("2sm softmax cta%d: wait_s %lld wait_o %lld xchg %lld rescale %lld pstore %lld total %lld\n", (int)rank,
-                   c_s, c_o, c_x, c_r, c_e, clock64() - c0);
+            printf("2sm softmax cta%d: wait_s %lld ld %lld mask %lld xchg+exp %lld wait_o %lld rescale %lld pstore %lld "
+                   "total %lld\n", (int)rank, c_s, c_ld, c_mx, c_ex, c_o, c_r, c_e, clock64() - c0);
         // epilogue: O / l -> bf16, lse (l summed over the two key halves)
         sl[kh][r] = l;
         cl::mbar_wait_cluster(&b_odone[(T - 1) & 1], ((T - 1) >> 1) & 1);
