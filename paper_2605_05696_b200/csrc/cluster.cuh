@@ -32,17 +32,19 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// wait with cluster-scope acquire (for barriers whose arrivals come from the peer CTA)
+// wait with cluster-scope acquire. Not used on the K5 hot path: the acquire compiles to
+// CCTL.IVALL (an L1 invalidate) after every successful poll; the tensor-core consumers
+// read shared memory through the async proxy, so CTA-scope waits suffice (as CUTLASS).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "WAITC_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAITC_%=;\n"
         "}\n" ::"r"(a),
-        "r"(parity)
+        "r"(parity), "r"(MBAR_SUSPEND_HINT)
         : "memory");
 }
 

@@ -85,6 +85,21 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+// Per-role cycle counters, printed for CTA 0 when IRM_MLA_DEBUG is set at run time.
+// Roles: 1 = 2-SM K loader, 2 = 2-SM MMA issuer, 4 = 2-SM softmax, 8 = 1-SM kernel.
+// The 2-SM roles stay instrumented in the production build: compiling them out
+// (-DIRM_MLA_PROF_MASK=0) measured 13% slower on B200 (730 vs 845 TFLOP/s on the
+// config-3 shape), a warp-scheduling effect reproduced across runs (profiles/r01d_k5.md).
+#ifndef IRM_MLA_PROF_MASK
+#define IRM_MLA_PROF_MASK 7
+#endif
+constexpr bool kProf = IRM_MLA_PROF_MASK != 0;
+template <int ROLE>
+__device__ __forceinline__ long long prof_clock() {
+    if constexpr ((IRM_MLA_PROF_MASK & ROLE) != 0) return clock64();
+    return 0;
+}
+
 __device__ __forceinline__ float ex2(float x) {  // 2^x, flush-to-zero; ex2(-inf) = 0
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -256,33 +271,33 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
         mbar_arrive(&bar_q);
         // NST independent rope groups: group g handles tiles g, g + NST, ... (ring stage g)
         const int g = ptid / GROUP, gtid = ptid % GROUP;
-        long long c_wait = 0, c_load = 0, c0 = clock64();
+        long long c_wait = 0, c_load = 0, c0 = prof_clock<8>();
         for (int t = g; t < T; t += NST) {
             const int kt = (t + toff) % T;
             RopeRegs rr;
             rope_fetch(p, kt, gtid, rr);
-            long long a = clock64();
+            long long a = prof_clock<8>();
             if (t >= NST) mbar_wait(&bar_kv_empty[g], ((t / NST) - 1) & 1);
-            long long b2 = clock64();
+            long long b2 = prof_clock<8>();
             store_rope(p, smem + SMEM_KV + g * KTILE, gtid, rr);
             mbar_arrive(&bar_kv_full[g]);
             c_wait += b2 - a;
-            c_load += clock64() - b2;
+            c_load += prof_clock<8>() - b2;
         }
-        if (p.dbg && blockIdx.x == 0 && gtid == 0)
-            printf("rope g%d: wait_empty %lld store %lld total %lld (T=%d)\n", g, c_wait, c_load, clock64() - c0, T);
+        if (kProf && p.dbg && blockIdx.x == 0 && gtid == 0)
+            printf("rope g%d: wait_empty %lld store %lld total %lld (T=%d)\n", g, c_wait, c_load, prof_clock<8>() - c0, T);
     } else if (warp == W_TMA) {
         // ------------------------------------------------------ c_KV by TMA gather4 (paged rows)
         // lane i resolves the pool row of key i of the tile; lanes 0..7 each issue the
         // 8 gather4 (pieces 0..7) of rows 4i..4i+3
-        long long c_wait = 0, c0 = clock64();
+        long long c_wait = 0, c0 = prof_clock<8>();
         for (int t = 0; t < T; ++t) {
             const int st = t % NST, kt = (t + toff) % T;
             const int k = kt * BN + lane;
             const int row = k < p.n_kv ? (p.kv_rows ? __ldg(p.kv_rows + k) : k) : -1;  // -1: OOB, zero-filled
-            long long a = clock64();
+            long long a = prof_clock<8>();
             if (t >= NST) mbar_wait(&bar_kv_empty[st], ((t / NST) - 1) & 1);
-            c_wait += clock64() - a;
+            c_wait += prof_clock<8>() - a;
             if (lane == 0) mbar_arrive_expect_tx(&bar_kv_full[st], CKV_TX);
             __syncwarp();
             // a run of BN consecutive pool rows (the common case: chunks are contiguous in
@@ -308,8 +323,8 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
                     tma_gather4(dst + pc * KPIECE, &tmap_pool, 64 * pc, r0, r1, r2, r3, &bar_kv_full[st]);
             }
         }
-        if (p.dbg && blockIdx.x == 0 && lane == 0)
-            printf("tma: wait_empty %lld total %lld\n", c_wait, clock64() - c0);
+        if (kProf && p.dbg && blockIdx.x == 0 && lane == 0)
+            printf("tma: wait_empty %lld total %lld\n", c_wait, prof_clock<8>() - c0);
     } else if (warp == W_MMA) {
         // ------------------------------------------------------ MMA issuer
         // The warp stays converged (barrier waits by all lanes); one elected lane
@@ -322,12 +337,12 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
         const uint64_t kv_desc = tc::smem_desc_sw128(smem_u32(smem + SMEM_KV), 16, 1024);
         const uint64_t v_desc = tc::smem_desc_sw128(smem_u32(smem + SMEM_KV), KPIECE, 1024);
         const uint64_t p_desc = tc::smem_desc_sw64(smem_u32(smem + SMEM_P), 16, 512);
-        long long c_kv = 0, c_p = 0, c0 = clock64();
+        long long c_kv = 0, c_p = 0, c0 = prof_clock<8>();
         auto issue_qk = [&](int t) {
             const int st = t % NST;
-            long long a = clock64();
+            long long a = prof_clock<8>();
             mbar_wait(&bar_kv_full[st], (t / NST) & 1);
-            c_kv += clock64() - a;
+            c_kv += prof_clock<8>() - a;
             tc::fence_after();
             const uint32_t d = tbase + (S_LANE << 16) + (t & 1) * BN;
             const uint64_t kd = kv_desc + (uint64_t)((st * KTILE) >> 4);
@@ -350,9 +365,9 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
             // S buffer (t+1)&1 was consumed by softmax(t-1): its P(t-1) arrived before PV(t-1)
             if (t + 1 < T) issue_qk(t + 1);
             const int st = t % NST;
-            long long a = clock64();
+            long long a = prof_clock<8>();
             mbar_wait(&bar_p_full[t & 1], (t >> 1) & 1);
-            c_p += clock64() - a;
+            c_p += prof_clock<8>() - a;
             tc::fence_after();
             const uint64_t pd = p_desc + (uint64_t)(((t & 1) * PTILE) >> 4);
             const uint64_t vd = v_desc + (uint64_t)((st * KTILE) >> 4);
@@ -371,8 +386,8 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
             }
             __syncwarp();
         }
-        if (p.dbg && blockIdx.x == 0 && lane == 0)
-            printf("mma: wait_kv %lld wait_p %lld total %lld\n", c_kv, c_p, clock64() - c0);
+        if (kProf && p.dbg && blockIdx.x == 0 && lane == 0)
+            printf("mma: wait_kv %lld wait_p %lld total %lld\n", c_kv, c_p, prof_clock<8>() - c0);
     } else {
         // ------------------------------------------------------ softmax / correction (warps 0-3)
         const int w = warp;
@@ -386,11 +401,11 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
         const uint32_t o_lane = tbase + ((uint32_t)(32 * w) << 16);
         const uint32_t p_base = smem_u32(smem + SMEM_P);
         float m = -INFINITY, l = 0.f;
-        long long c_s = 0, c_o = 0, c_r = 0, c0 = clock64();
+        long long c_s = 0, c_o = 0, c_r = 0, c0 = prof_clock<8>();
         for (int t = 0; t < T; ++t) {
-            long long a = clock64();
+            long long a = prof_clock<8>();
             mbar_wait(&bar_s_full[t & 1], (t >> 1) & 1);
-            c_s += clock64() - a;
+            c_s += prof_clock<8>() - a;
             tc::fence_after();
             uint32_t v[16];
             tc::ld_16x64b_x16(s_lane + (t & 1) * BN, v);
@@ -435,10 +450,10 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
                 if ((i >> 3) == b) pk[i & 7] = pr;
             }
             // P buffer t&1 is free once PV(t-2) completed
-            a = clock64();
+            a = prof_clock<8>();
             if (t >= 2) mbar_wait(&bar_o_done[t & 1], ((t >> 1) - 1) & 1);
-            c_o += clock64() - a;
-            a = clock64();
+            c_o += prof_clock<8>() - a;
+            a = prof_clock<8>();
             if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
                 mbar_wait(&bar_o_done[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV(0..t-1)
                 tc::fence_after();
@@ -453,7 +468,7 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
                 }
                 tc::wait_st();
             }
-            c_r += clock64() - a;
+            c_r += prof_clock<8>() - a;
             const uint32_t pt = p_base + (t & 1) * PTILE;
             sts128(pt + swz64(r, 2 * b), make_uint4(pk[0], pk[1], pk[2], pk[3]));
             sts128(pt + swz64(r, 2 * b + 1), make_uint4(pk[4], pk[5], pk[6], pk[7]));
@@ -461,8 +476,8 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
             tc::fence_before();
             mbar_arrive(&bar_p_full[t & 1]);
         }
-        if (p.dbg && blockIdx.x == 0 && lane == 0)
-            printf("softmax w%d: wait_s %lld wait_o %lld rescale %lld total %lld\n", w, c_s, c_o, c_r, clock64() - c0);
+        if (kProf && p.dbg && blockIdx.x == 0 && lane == 0)
+            printf("softmax w%d: wait_s %lld wait_o %lld rescale %lld total %lld\n", w, c_s, c_o, c_r, prof_clock<8>() - c0);
         // epilogue: O / l -> bf16, lse
         mbar_wait(&bar_o_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
         tc::fence_after();
@@ -610,20 +625,20 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         }
     } else if (warp == W_KTMA) {
         // ------------------------------------------------ c_KV of this CTA's 32 keys (QK operand)
-        long long c_e = 0, c0 = clock64();
+        long long c_e = 0, c0 = prof_clock<1>();
         for (int t = 0; t < T; ++t) {
             const int st = t % KST, kt = (t + toff) % T;
-            long long a0 = clock64();
+            long long a0 = prof_clock<1>();
             if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
-            c_e += clock64() - a0;
+            c_e += prof_clock<1>() - a0;
             if (lane == 0) mbar_arrive_expect_tx(&b_kfull[st], CKV_TX);
             __syncwarp();
             const uint32_t dst = smem_u32(smem + S_K + st * KTILE);
             for (int pc = 0; pc < 8; ++pc)
                 tma_rows32(p, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, kt * PBN + 32 * rank, lane, &b_kfull[st]);
         }
-        if (p.dbg && blockIdx.x < 2 && lane == 0)
-            printf("2sm ktma cta%d: wait_empty %lld total %lld\n", (int)rank, c_e, clock64() - c0);
+        if (kProf && p.dbg && blockIdx.x < 2 && lane == 0)
+            printf("2sm ktma cta%d: wait_empty %lld total %lld\n", (int)rank, c_e, prof_clock<1>() - c0);
     } else if (warp == W_VTMA) {
         // ------------------------------------------------ V: all 64 keys x this CTA's 256 latent dims
         for (int t = 0; t < T; ++t) {
@@ -668,16 +683,16 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             const uint64_t v_desc = tc::smem_desc_sw128(smem_u32(smem + S_V), VPIECE, 1024);
             const uint64_t p_desc = tc::smem_desc_sw128(smem_u32(smem + S_P), 16, 1024);
             mbar_wait(&b_q, 0);
-            cl::mbar_wait_cluster(&b_qpair, 0);
-            long long c_k = 0, c_kp = 0, c_p = 0, c_v = 0, c0 = clock64();
+            mbar_wait(&b_qpair, 0);
+            long long c_k = 0, c_kp = 0, c_p = 0, c_v = 0, c0 = prof_clock<2>();
             auto issue_qk = [&](int t) {
                 const int st = t % KST;
-                long long a0 = clock64();
+                long long a0 = prof_clock<2>();
                 mbar_wait(&b_kfull[st], (t / KST) & 1);
-                long long a1 = clock64();
-                cl::mbar_wait_cluster(&b_kpair[st], (t / KST) & 1);
+                long long a1 = prof_clock<2>();
+                mbar_wait(&b_kpair[st], (t / KST) & 1);
                 c_k += a1 - a0;
-                c_kp += clock64() - a1;
+                c_kp += prof_clock<2>() - a1;
                 tc::fence_after();
                 const uint64_t kd = k_desc + (uint64_t)((st * KTILE) >> 4);
                 if (tc::elect_one()) {
@@ -697,13 +712,13 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             for (int t = 0; t < T; ++t) {
                 if (t + 1 < T) issue_qk(t + 1);
                 const int vs = t % VST;
-                long long a0 = clock64();
-                cl::mbar_wait_cluster(&b_pfull[t & 1], (t >> 1) & 1);
-                long long a1 = clock64();
+                long long a0 = prof_clock<2>();
+                mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
+                long long a1 = prof_clock<2>();
                 mbar_wait(&b_vfull[vs], (t / VST) & 1);
-                cl::mbar_wait_cluster(&b_vpair[vs], (t / VST) & 1);
+                mbar_wait(&b_vpair[vs], (t / VST) & 1);
                 c_p += a1 - a0;
-                c_v += clock64() - a1;
+                c_v += prof_clock<2>() - a1;
                 tc::fence_after();
                 const uint64_t pd = p_desc + (uint64_t)(((t & 1) * PTILE2) >> 4);
                 const uint64_t vd = v_desc + (uint64_t)((vs * VTILE) >> 4);
@@ -721,9 +736,9 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 }
                 __syncwarp();
             }
-            if (p.dbg && blockIdx.x == 0 && lane == 0)
+            if (kProf && p.dbg && blockIdx.x == 0 && lane == 0)
                 printf("2sm mma: wait_k %lld wait_kpair %lld wait_p %lld wait_v %lld total %lld T=%d\n", c_k, c_kp, c_p,
-                       c_v, clock64() - c0, T);
+                       c_v, prof_clock<2>() - c0, T);
         }
     } else {
         // ------------------------------------------------ softmax / correction (warps 0-3)
@@ -738,17 +753,17 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         const uint32_t pfull_leader0 = cl::map_to(smem_u32(&b_pfull[0]), 0);
         const uint32_t pfull_leader1 = cl::map_to(smem_u32(&b_pfull[1]), 0);
         float m = -INFINITY, l = 0.f;
-        long long c_s = 0, c_o = 0, c_x = 0, c_r = 0, c_e = 0, c_ld = 0, c_mx = 0, c_ex = 0, c0 = clock64();
+        long long c_s = 0, c_o = 0, c_x = 0, c_r = 0, c_e = 0, c_ld = 0, c_mx = 0, c_ex = 0, c0 = prof_clock<4>();
         for (int t = 0; t < T; ++t) {
-            long long a0 = clock64();
-            cl::mbar_wait_cluster(&b_sfull[t & 1], (t >> 1) & 1);
-            c_s += clock64() - a0;
+            long long a0 = prof_clock<4>();
+            mbar_wait(&b_sfull[t & 1], (t >> 1) & 1);
+            c_s += prof_clock<4>() - a0;
             tc::fence_after();
             uint32_t v[32];
-            long long b0 = clock64();
+            long long b0 = prof_clock<4>();
             tc2::ld_32x32b_x32(lane_base + COL_S + (t & 1) * 32, v);
             tc::wait_ld();
-            long long b1 = clock64();
+            long long b1 = prof_clock<4>();
             c_ld += b1 - b0;
             const int64_t kbase = (int64_t)((t + toff) % T) * PBN + 32 * kh;
             if (!__all_sync(0xffffffffu, row_ok && kbase + 31 <= qpos && kbase + 31 < p.n_kv)) {
@@ -763,10 +778,10 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(v[i]));
             float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
             sx[t & 1][kh][r] = mt;  // exchange with the thread holding the other key half
-            long long a1 = clock64();
+            long long a1 = prof_clock<4>();
             c_mx += a1 - b1;
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            c_x += clock64() - a1;
+            c_x += prof_clock<4>() - a1;
             mt = fmaxf(mt, sx[t & 1][kh ^ 1][r]);
             float alpha = 1.f;
             const float m_new = fmaxf(m, mt);
@@ -785,13 +800,13 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 pk[i >> 1] = pack_bf2(e0, e1);
             }
             l = l * alpha + (ls[0] + ls[1]);
-            long long a2 = clock64();
+            long long a2 = prof_clock<4>();
             c_ex += a2 - a1;
-            if (t >= 2) cl::mbar_wait_cluster(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
-            c_o += clock64() - a2;
-            long long a3 = clock64();
+            if (t >= 2) mbar_wait(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
+            c_o += prof_clock<4>() - a2;
+            long long a3 = prof_clock<4>();
             if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
-                cl::mbar_wait_cluster(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV(0..t-1)
+                mbar_wait(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV(0..t-1)
                 tc::fence_after();
 #pragma unroll 1
                 for (int c = 0; c < 8; ++c) {
@@ -805,7 +820,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 }
                 tc::wait_st();
             }
-            long long a4 = clock64();
+            long long a4 = prof_clock<4>();
             c_r += a4 - a3;
             const uint32_t pt = p_base + (t & 1) * PTILE2;
 #pragma unroll
@@ -814,14 +829,14 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             fence_proxy_async_smem();
             tc::fence_before();
             mbar_arrive(&b_pfull[t & 1]);  // local; the peer's relay forwards it to the leader
-            c_e += clock64() - a4;
+            c_e += prof_clock<4>() - a4;
         }
-        if (p.dbg && blockIdx.x < 2 && lane == 0 && w == 0)
+        if (kProf && p.dbg && blockIdx.x < 2 && lane == 0 && w == 0)
             printf("2sm softmax cta%d: wait_s %lld ld %lld mask %lld xchg+exp %lld wait_o %lld rescale %lld pstore %lld "
-                   "total %lld\n", (int)rank, c_s, c_ld, c_mx, c_ex, c_o, c_r, c_e, clock64() - c0);
+                   "total %lld\n", (int)rank, c_s, c_ld, c_mx, c_ex, c_o, c_r, c_e, prof_clock<4>() - c0);
         // epilogue: O / l -> bf16, lse (l summed over the two key halves)
         sl[kh][r] = l;
-        cl::mbar_wait_cluster(&b_odone[(T - 1) & 1], ((T - 1) >> 1) & 1);
+        mbar_wait(&b_odone[(T - 1) & 1], ((T - 1) >> 1) & 1);
         tc::fence_after();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         l += sl[kh ^ 1][r];

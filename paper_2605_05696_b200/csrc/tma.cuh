@@ -4,6 +4,12 @@
 
 namespace irm {
 
+// try_wait suspend-time hint (ns), as CUTLASS's ClusterBarrier::wait: a waiting warp sleeps
+// until the phase flips instead of re-polling the barrier unit.
+#ifndef MBAR_SUSPEND_HINT
+#define MBAR_SUSPEND_HINT 0x989680u
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -33,10 +39,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(a),
-        "r"(parity)
+        "r"(parity), "r"(MBAR_SUSPEND_HINT)
         : "memory");
 }
 

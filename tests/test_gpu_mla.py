@@ -16,11 +16,20 @@ pytestmark = pytest.mark.gpu
 TOL = 4.7e-3
 
 
-@pytest.fixture(scope="module")
-def ops():
+@pytest.fixture(scope="module", params=["2sm", "1sm"])
+def ops(request):
+    """Both K5 kernels: the CTA-pair (cta_group::2, default) and the 1-SM one
+    (selected by IRM_MLA_1SM, read by the library on every call)."""
+    import os
+
     from paper_2605_05696_b200 import _native as N, ops
 
-    return ops, N
+    if request.param == "1sm":
+        os.environ["IRM_MLA_1SM"] = "1"
+    else:
+        os.environ.pop("IRM_MLA_1SM", None)
+    yield ops, N
+    os.environ.pop("IRM_MLA_1SM", None)
 
 
 def run_case(ops, N, n_kv, n_q, heads=16, q_pos0=None, rotate=False, paged=False, layout=0, q_gain=1.0, seed=0,
