@@ -523,9 +523,9 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
 namespace p2 {
 
 constexpr int PBN = 64;                     // keys per pair tile (QK N)
-constexpr int VPIECE = PBN * 128;           // 8 KB: 64 keys x 64 dims
-constexpr int VTILE = 4 * VPIECE;           // this CTA's 256 latent dims of the tile
-constexpr int KST = 2, VST = 2;             // ring stages
+constexpr int VPIECE = 32 * 128;            // 4 KB: 32 keys x 64 dims (SW128)
+constexpr int VTILE = 4 * VPIECE;           // V half-tile: 32 keys x this CTA's 256 latent dims
+constexpr int KST = 2, VST = 4;             // ring stages (V in half-tiles: PV(t) is two K=32 halves)
 constexpr int PTILE2 = 64 * 128;            // P [64 rows x 64 keys] bf16, SW128
 constexpr int S_Q = 0, S_K = NPIECE * QPIECE, S_V = S_K + KST * KTILE, S_P = S_V + VST * VTILE;
 constexpr int SMEM2 = S_P + 2 * PTILE2;     // 224 KB
@@ -642,17 +642,18 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
     } else if (warp == W_VTMA) {
         // ------------------------------------------------ V: all 64 keys x this CTA's 256 latent dims
         for (int t = 0; t < T; ++t) {
-            const int st = t % VST, kt = (t + toff) % T;
-            if (t >= VST) mbar_wait(&b_vempty[st], ((t / VST) - 1) & 1);
+          for (int a = 0; a < 2; ++a) {  // key halves [32a, 32a + 32) of tile t
+            const int u = 2 * t + a, st = u % VST, kt = (t + toff) % T;
+            if (u >= VST) mbar_wait(&b_vempty[st], ((u / VST) - 1) & 1);
             if (lane == 0) mbar_arrive_expect_tx(&b_vfull[st], (uint32_t)VTILE);
             __syncwarp();
             const uint32_t dst = smem_u32(smem + S_V + st * VTILE);
             for (int j = 0; j < 4; ++j) {
                 const int cpiece = (j >> 1) * 4 + 2 * (int)rank + (j & 1);  // dims [256h + 128 rank, +128)
-                for (int half = 0; half < 2; ++half)
-                    tma_rows32(p, &tmap_pool, &tmap_tile, dst + j * VPIECE + half * 4096, cpiece,
-                               kt * PBN + 32 * half, lane, &b_vfull[st]);
+                tma_rows32(p, &tmap_pool, &tmap_tile, dst + j * VPIECE, cpiece, kt * PBN + 32 * a, lane,
+                           &b_vfull[st]);
             }
+          }
         }
     } else if (warp == W_MMA2) {
         if (rank != 0) {
@@ -671,8 +672,10 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 if (t + 1 < T) relay_k(t + 1);
                 mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
                 if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_pfull[t & 1]), 0));
-                mbar_wait(&b_vfull[t % VST], (t / VST) & 1);
-                if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_vpair[t % VST]), 0));
+                for (int u = 2 * t; u < 2 * t + 2; ++u) {
+                    mbar_wait(&b_vfull[u % VST], (u / VST) & 1);
+                    if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_vpair[u % VST]), 0));
+                }
             }
         } else {
             // ------------------------------------------------ leader: MMA issue for the pair
@@ -711,30 +714,33 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             issue_qk(0);
             for (int t = 0; t < T; ++t) {
                 if (t + 1 < T) issue_qk(t + 1);
-                const int vs = t % VST;
                 long long a0 = prof_clock<2>();
                 mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
-                long long a1 = prof_clock<2>();
-                mbar_wait(&b_vfull[vs], (t / VST) & 1);
-                mbar_wait(&b_vpair[vs], (t / VST) & 1);
-                c_p += a1 - a0;
-                c_v += prof_clock<2>() - a1;
-                tc::fence_after();
+                c_p += prof_clock<2>() - a0;
                 const uint64_t pd = p_desc + (uint64_t)(((t & 1) * PTILE2) >> 4);
-                const uint64_t vd = v_desc + (uint64_t)((vs * VTILE) >> 4);
-                if (tc::elect_one()) {
+#pragma unroll 1
+                for (int a = 0; a < 2; ++a) {  // PV over key half a, as soon as its V half-tile lands
+                    const int u = 2 * t + a, vs = u % VST;
+                    long long a1 = prof_clock<2>();
+                    mbar_wait(&b_vfull[vs], (u / VST) & 1);
+                    mbar_wait(&b_vpair[vs], (u / VST) & 1);
+                    c_v += prof_clock<2>() - a1;
+                    tc::fence_after();
+                    const uint64_t vd = v_desc + (uint64_t)((vs * VTILE) >> 4);
+                    if (tc::elect_one()) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                        for (int h = 0; h < 2; ++h) {
 #pragma unroll
-                        for (int k = 0; k < PBN / 16; ++k)
-                            tc2::mma_bf16_ss(tbase + COL_O + h * 128, pd + (uint64_t)((k * 32) >> 4),
-                                             vd + (uint64_t)((2 * h * VPIECE + k * 2048) >> 4), idesc_pv,
-                                             (t > 0 || k > 0) ? 1u : 0u);
+                            for (int k = 0; k < 2; ++k)
+                                tc2::mma_bf16_ss(tbase + COL_O + h * 128, pd + (uint64_t)(((2 * a + k) * 32) >> 4),
+                                                 vd + (uint64_t)((2 * h * VPIECE + k * 2048) >> 4), idesc_pv,
+                                                 (t > 0 || a > 0 || k > 0) ? 1u : 0u);
+                        }
+                        tc2::commit_both(&b_vempty[vs]);
+                        if (a == 1) tc2::commit_both(&b_odone[t & 1]);
                     }
-                    tc2::commit_both(&b_vempty[vs]);
-                    tc2::commit_both(&b_odone[t & 1]);
+                    __syncwarp();
                 }
-                __syncwarp();
             }
             if (kProf && p.dbg && blockIdx.x == 0 && lane == 0)
                 printf("2sm mma: wait_k %lld wait_kpair %lld wait_p %lld wait_v %lld total %lld T=%d\n", c_k, c_kp, c_p,
