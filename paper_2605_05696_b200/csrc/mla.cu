@@ -685,6 +685,10 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             const uint64_t k_desc = tc::smem_desc_sw128(smem_u32(smem + S_K), 16, 1024);
             const uint64_t v_desc = tc::smem_desc_sw128(smem_u32(smem + S_V), VPIECE, 1024);
             const uint64_t p_desc = tc::smem_desc_sw128(smem_u32(smem + S_P), 16, 1024);
+            const uint32_t q_lo = (uint32_t)q_desc, q_hi = (uint32_t)(q_desc >> 32);
+            const uint32_t k_lo = (uint32_t)k_desc, k_hi = (uint32_t)(k_desc >> 32);
+            const uint32_t v_lo = (uint32_t)v_desc, v_hi = (uint32_t)(v_desc >> 32);
+            const uint32_t p_lo = (uint32_t)p_desc, p_hi = (uint32_t)(p_desc >> 32);
             mbar_wait(&b_q, 0);
             mbar_wait(&b_qpair, 0);
             long long c_k = 0, c_kp = 0, c_p = 0, c_v = 0, c0 = prof_clock<2>();
@@ -697,14 +701,19 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 c_k += a1 - a0;
                 c_kp += prof_clock<2>() - a1;
                 tc::fence_after();
-                const uint64_t kd = k_desc + (uint64_t)((st * KTILE) >> 4);
+                const uint32_t kd = k_lo + ((st * KTILE) >> 4);
+                const uint32_t ds = tbase + COL_S + (t & 1) * 32;
                 if (tc::elect_one()) {
-#pragma unroll
+                    // one 64-dim piece per iteration, descriptors advanced incrementally: a fully
+                    // unrolled loop hoists all 72 descriptors into uniform registers and spills
+                    uint32_t qa = q_lo, kb = kd;
+#pragma unroll 1
                     for (int pc = 0; pc < NPIECE; ++pc) {
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
-                            tc2::mma_bf16_ss(tbase + COL_S + (t & 1) * 32, q_desc + (uint64_t)((pc * QPIECE + k * 32) >> 4),
-                                             kd + (uint64_t)((pc * KPIECE + k * 32) >> 4), idesc_qk, (pc | k) != 0);
+                            tc2::mma_bf16_ss_w(ds, qa + 2 * k, q_hi, kb + 2 * k, k_hi, idesc_qk, (pc | k) != 0);
+                        qa += QPIECE >> 4;
+                        kb += KPIECE >> 4;
                     }
                     tc2::commit_both(&b_sfull[t & 1]);
                     tc2::commit_both(&b_kempty[st]);
@@ -717,7 +726,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 long long a0 = prof_clock<2>();
                 mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
                 c_p += prof_clock<2>() - a0;
-                const uint64_t pd = p_desc + (uint64_t)(((t & 1) * PTILE2) >> 4);
+                const uint32_t pd = p_lo + (((t & 1) * PTILE2) >> 4);
 #pragma unroll 1
                 for (int a = 0; a < 2; ++a) {  // PV over key half a, as soon as its V half-tile lands
                     const int u = 2 * t + a, vs = u % VST;
@@ -726,15 +735,15 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                     mbar_wait(&b_vpair[vs], (u / VST) & 1);
                     c_v += prof_clock<2>() - a1;
                     tc::fence_after();
-                    const uint64_t vd = v_desc + (uint64_t)((vs * VTILE) >> 4);
+                    const uint32_t vd = v_lo + ((vs * VTILE) >> 4);
                     if (tc::elect_one()) {
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
 #pragma unroll
                             for (int k = 0; k < 2; ++k)
-                                tc2::mma_bf16_ss(tbase + COL_O + h * 128, pd + (uint64_t)(((2 * a + k) * 32) >> 4),
-                                                 vd + (uint64_t)((2 * h * VPIECE + k * 2048) >> 4), idesc_pv,
-                                                 (t > 0 || a > 0 || k > 0) ? 1u : 0u);
+                                tc2::mma_bf16_ss_w(tbase + COL_O + h * 128, pd + (((2 * a + k) * 32) >> 4), p_hi,
+                                                   vd + ((2 * h * VPIECE + k * 2048) >> 4), v_hi, idesc_pv,
+                                                   (t > 0 || a > 0 || k > 0) ? 1u : 0u);
                         }
                         tc2::commit_both(&b_vempty[vs]);
                         if (a == 1) tc2::commit_both(&b_odone[t & 1]);
