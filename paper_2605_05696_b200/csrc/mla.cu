@@ -85,13 +85,11 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
-// Per-role cycle counters, printed for CTA 0 when IRM_MLA_DEBUG is set at run time.
+// Per-role cycle counters, printed for CTA 0 when IRM_MLA_DEBUG is set at run time, exist
+// only in builds with -DIRM_MLA_PROF_MASK=<roles> (make EXTRA=-DIRM_MLA_PROF_MASK=15).
 // Roles: 1 = 2-SM K loader, 2 = 2-SM MMA issuer, 4 = 2-SM softmax, 8 = 1-SM kernel.
-// The 2-SM roles stay instrumented in the production build: compiling them out
-// (-DIRM_MLA_PROF_MASK=0) measured 13% slower on B200 (730 vs 845 TFLOP/s on the
-// config-3 shape), a warp-scheduling effect reproduced across runs (profiles/r01d_k5.md).
 #ifndef IRM_MLA_PROF_MASK
-#define IRM_MLA_PROF_MASK 7
+#define IRM_MLA_PROF_MASK 0
 #endif
 constexpr bool kProf = IRM_MLA_PROF_MASK != 0;
 template <int ROLE>
