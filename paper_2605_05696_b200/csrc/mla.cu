@@ -335,6 +335,10 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
         const uint64_t kv_desc = tc::smem_desc_sw128(smem_u32(smem + SMEM_KV), 16, 1024);
         const uint64_t v_desc = tc::smem_desc_sw128(smem_u32(smem + SMEM_KV), KPIECE, 1024);
         const uint64_t p_desc = tc::smem_desc_sw64(smem_u32(smem + SMEM_P), 16, 512);
+        const uint32_t q_lo = (uint32_t)q_desc, q_hi = (uint32_t)(q_desc >> 32);
+        const uint32_t kv_lo = (uint32_t)kv_desc, kv_hi = (uint32_t)(kv_desc >> 32);
+        const uint32_t v_lo = (uint32_t)v_desc, v_hi = (uint32_t)(v_desc >> 32);
+        const uint32_t p_lo = (uint32_t)p_desc, p_hi = (uint32_t)(p_desc >> 32);
         long long c_kv = 0, c_p = 0, c0 = prof_clock<8>();
         auto issue_qk = [&](int t) {
             const int st = t % NST;
@@ -343,15 +347,15 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
             c_kv += prof_clock<8>() - a;
             tc::fence_after();
             const uint32_t d = tbase + (S_LANE << 16) + (t & 1) * BN;
-            const uint64_t kd = kv_desc + (uint64_t)((st * KTILE) >> 4);
             if (tc::elect_one()) {
-#pragma unroll
+                uint32_t qa = q_lo, kb = kv_lo + ((st * KTILE) >> 4);  // see the 2-SM issue loop
+#pragma unroll 1
                 for (int pc = 0; pc < NPIECE; ++pc) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        tc::mma_bf16_ss(d, q_desc + (uint64_t)((pc * QPIECE + k * 32) >> 4),
-                                        kd + (uint64_t)((pc * KPIECE + k * 32) >> 4), idesc_qk, (pc | k) != 0);
-                    }
+                    for (int k = 0; k < 4; ++k)
+                        tc::mma_bf16_ss_w(d, qa + 2 * k, q_hi, kb + 2 * k, kv_hi, idesc_qk, (pc | k) != 0);
+                    qa += QPIECE >> 4;
+                    kb += KPIECE >> 4;
                 }
                 tc::commit(&bar_s_full[t & 1]);
             }
@@ -367,17 +371,16 @@ __global__ void __launch_bounds__(THREADS, 1) mla_reattach_kernel(Params p, cons
             mbar_wait(&bar_p_full[t & 1], (t >> 1) & 1);
             c_p += prof_clock<8>() - a;
             tc::fence_after();
-            const uint64_t pd = p_desc + (uint64_t)(((t & 1) * PTILE) >> 4);
-            const uint64_t vd = v_desc + (uint64_t)((st * KTILE) >> 4);
+            const uint32_t pd = p_lo + (((t & 1) * PTILE) >> 4);
+            const uint32_t vd = v_lo + ((st * KTILE) >> 4);
             if (tc::elect_one()) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
 #pragma unroll
-                    for (int k = 0; k < BN / 16; ++k) {
-                        tc::mma_bf16_ss(tbase + h * 256, pd + (uint64_t)((k * 32) >> 4),
-                                        vd + (uint64_t)((4 * h * KPIECE + k * 2048) >> 4), idesc_pv,
-                                        (t > 0 || k > 0) ? 1u : 0u);
-                    }
+                    for (int k = 0; k < BN / 16; ++k)
+                        tc::mma_bf16_ss_w(tbase + h * 256, pd + ((k * 32) >> 4), p_hi,
+                                          vd + ((4 * h * KPIECE + k * 2048) >> 4), v_hi, idesc_pv,
+                                          (t > 0 || k > 0) ? 1u : 0u);
                 }
                 tc::commit(&bar_kv_empty[st]);
                 tc::commit(&bar_o_done[t & 1]);
@@ -536,19 +539,36 @@ __device__ __forceinline__ void arrive_leader(uint64_t *bar, uint32_t rank) {
     else cl::remote_arrive(cl::map_to(smem_u32(bar), 0));
 }
 
-// TMA of rows [k0, k0 + 32) of column piece `col_piece` into dst (a 32-row SW128 box)
-__device__ __forceinline__ void tma_rows32(const Params &p, const CUtensorMap *tm_g4, const CUtensorMap *tm_tile,
-                                           uint32_t dst, int col_piece, int k0, int lane, uint64_t *bar) {
-    const int k = k0 + lane;
-    const int row = k < p.n_kv ? (p.kv_rows ? __ldg(p.kv_rows + k) : k) : -1;
-    const int row0 = __shfl_sync(0xffffffffu, row, 0);
-    if (__all_sync(0xffffffffu, row0 >= 0 && row == row0 + lane)) {
-        if (lane == 0) tma_load_2d(dst, tm_tile, 64 * col_piece, row0, bar);
+// Rows of keys [k0, k0 + 32): one kv_rows read per lane, reused for every column piece.
+struct Rows32 {
+    int row;     // this lane's pool row (-1 past n_kv)
+    int row0;    // lane 0's row
+    bool contig; // all 32 rows form one ascending run -> one tiled TMA box per piece
+};
+
+__device__ __forceinline__ int key_row(const Params &p, int k) {
+    return k < p.n_kv ? (p.kv_rows ? __ldg(p.kv_rows + k) : k) : -1;
+}
+
+__device__ __forceinline__ Rows32 rows32_resolve(int row, int lane) {
+    Rows32 r;
+    r.row = row;
+    r.row0 = __shfl_sync(0xffffffffu, row, 0);
+    r.contig = __all_sync(0xffffffffu, r.row0 >= 0 && row == r.row0 + lane);
+    return r;
+}
+
+// TMA of the 32 rows of column piece `col_piece` into dst (a 32-row SW128 box): a tiled box
+// for a contiguous run, else eight tile::gather4 ops (lanes 0-7, four rows each)
+__device__ __forceinline__ void tma_rows32(const Rows32 &r, const CUtensorMap *tm_g4, const CUtensorMap *tm_tile,
+                                           uint32_t dst, int col_piece, int lane, uint64_t *bar) {
+    if (r.contig) {
+        if (lane == 0) tma_load_2d(dst, tm_tile, 64 * col_piece, r.row0, bar);
         return;
     }
     const int g = lane & 7;
-    const int r0 = __shfl_sync(0xffffffffu, row, 4 * g), r1 = __shfl_sync(0xffffffffu, row, 4 * g + 1);
-    const int r2 = __shfl_sync(0xffffffffu, row, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, row, 4 * g + 3);
+    const int r0 = __shfl_sync(0xffffffffu, r.row, 4 * g), r1 = __shfl_sync(0xffffffffu, r.row, 4 * g + 1);
+    const int r2 = __shfl_sync(0xffffffffu, r.row, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, r.row, 4 * g + 3);
     if (lane < 8) tma_gather4(dst + lane * 512, tm_g4, 64 * col_piece, r0, r1, r2, r3, bar);
 }
 
@@ -624,34 +644,37 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
     } else if (warp == W_KTMA) {
         // ------------------------------------------------ c_KV of this CTA's 32 keys (QK operand)
         long long c_e = 0, c0 = prof_clock<1>();
+        int row_next = key_row(p, (toff % T) * PBN + 32 * (int)rank + lane);  // rows read one tile ahead
         for (int t = 0; t < T; ++t) {
-            const int st = t % KST, kt = (t + toff) % T;
+            const int st = t % KST;
+            const Rows32 rr = rows32_resolve(row_next, lane);
+            if (t + 1 < T) row_next = key_row(p, ((t + 1 + toff) % T) * PBN + 32 * (int)rank + lane);
             long long a0 = prof_clock<1>();
             if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
             c_e += prof_clock<1>() - a0;
             if (lane == 0) mbar_arrive_expect_tx(&b_kfull[st], CKV_TX);
             __syncwarp();
             const uint32_t dst = smem_u32(smem + S_K + st * KTILE);
-            for (int pc = 0; pc < 8; ++pc)
-                tma_rows32(p, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, kt * PBN + 32 * rank, lane, &b_kfull[st]);
+            for (int pc = 0; pc < 8; ++pc) tma_rows32(rr, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, lane, &b_kfull[st]);
         }
         if (kProf && p.dbg && blockIdx.x < 2 && lane == 0)
             printf("2sm ktma cta%d: wait_empty %lld total %lld\n", (int)rank, c_e, prof_clock<1>() - c0);
     } else if (warp == W_VTMA) {
         // ------------------------------------------------ V: all 64 keys x this CTA's 256 latent dims
-        for (int t = 0; t < T; ++t) {
-          for (int a = 0; a < 2; ++a) {  // key halves [32a, 32a + 32) of tile t
-            const int u = 2 * t + a, st = u % VST, kt = (t + toff) % T;
+        // key half-tiles u = 2t + a: keys [64 kt + 32a, +32), rows read one half-tile ahead
+        int row_next = key_row(p, (toff % T) * PBN + lane);
+        for (int u = 0; u < 2 * T; ++u) {
+            const int st = u % VST;
+            const Rows32 rr = rows32_resolve(row_next, lane);
+            if (u + 1 < 2 * T) row_next = key_row(p, (((u + 1) / 2 + toff) % T) * PBN + 32 * ((u + 1) & 1) + lane);
             if (u >= VST) mbar_wait(&b_vempty[st], ((u / VST) - 1) & 1);
             if (lane == 0) mbar_arrive_expect_tx(&b_vfull[st], (uint32_t)VTILE);
             __syncwarp();
             const uint32_t dst = smem_u32(smem + S_V + st * VTILE);
             for (int j = 0; j < 4; ++j) {
                 const int cpiece = (j >> 1) * 4 + 2 * (int)rank + (j & 1);  // dims [256h + 128 rank, +128)
-                tma_rows32(p, &tmap_pool, &tmap_tile, dst + j * VPIECE, cpiece, kt * PBN + 32 * a, lane,
-                           &b_vfull[st]);
+                tma_rows32(rr, &tmap_pool, &tmap_tile, dst + j * VPIECE, cpiece, lane, &b_vfull[st]);
             }
-          }
         }
     } else if (warp == W_MMA2) {
         if (rank != 0) {
