@@ -142,6 +142,12 @@ int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, void *out,
                       const int64_t *delta, int64_t n_chunks, const int64_t *n_chunks_dev,
                       const double *inv_freq, int32_t layout, int32_t dtype, int32_t out_round,
                       void *ws, int64_t ws_bytes, irm_stream_t stream);
+/* Limit the SMs a subsequent irm_rotate_gather launch spreads its persistent
+ * CTAs over (0 = all SMs; process-wide, read at launch, so a captured CUDA graph
+ * keeps the value it was captured with). The reattach pipeline leaves ~20 SMs to
+ * CDC/lookup of the next wave running concurrently; the gather stays at the HBM
+ * roofline down to ~128 SMs (profiles/r01d_k4_sms.md). */
+int irm_rotate_gather_set_sm_limit(int32_t n_sms);
 /* Per-row absolute rotation (producer side of the store, registry.py:131-133
  * with rotary.py:98-108): out[i] = R(positions[i]) rows[i] for the dim-wide
  * rotary rows at rows + i*row_stride (elements). out may alias rows. */

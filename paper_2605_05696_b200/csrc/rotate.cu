@@ -11,6 +11,7 @@
 // the k_r columns in shared memory in fp32 (cos/sin from an fp64 angle per
 // chunk: fp32 angles fail the 1e-5 bar at |delta| ~ 2^20), and writes the tile
 // back with a bulk store. STAGES tiles are in flight per CTA.
+#include <algorithm>
 #include "common.cuh"
 #include "tma.cuh"
 #include <cuda_bf16.h>
@@ -238,6 +239,7 @@ __global__ void rotate_rows_kernel(const T *__restrict__ rows, int64_t rs, T *__
 }
 
 // ------------------------------------------------------------ host launchers
+static int g_rg_sm_limit = 0;  // irm_rotate_gather_set_sm_limit
 constexpr int RG_THREADS = 256;
 constexpr int RG_STAGES = 4;
 
@@ -249,7 +251,9 @@ static int launch_tma(const GatherArgs &a, const typename Elem<T>::CS *cs, cudaS
     int per_sm = 0;
     IRM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RG_THREADS, smem));
     if (per_sm < 1) per_sm = 1;
-    int64_t grid = (int64_t)sm_count() * per_sm;
+    int sms = sm_count();
+    if (g_rg_sm_limit > 0) sms = std::min(sms, g_rg_sm_limit);
+    int64_t grid = (int64_t)sms * per_sm;
     if (grid > a.n_items) grid = a.n_items;
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, RG_THREADS, smem, st>>>(a, cs);
@@ -296,6 +300,12 @@ static int launch_gather(const GatherArgs &a, void *ws, const int64_t *delta, co
 }  // namespace irm
 
 using namespace irm;
+
+extern "C" int irm_rotate_gather_set_sm_limit(int32_t n_sms) {
+    IRM_REQUIRE(n_sms >= 0, "n_sms must be >= 0");
+    g_rg_sm_limit = n_sms;
+    return IRM_OK;
+}
 
 extern "C" int64_t irm_rotate_gather_workspace_bytes(int64_t n_chunks, int32_t kr_dim) {
     if (n_chunks < 0 || kr_dim < 0) return -1;

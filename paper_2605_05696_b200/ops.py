@@ -173,6 +173,11 @@ def rotate_gather(pool: torch.Tensor, out: torch.Tensor, src_row: torch.Tensor, 
     N.check(rc, "irm_rotate_gather")
 
 
+def set_rotate_gather_sm_limit(n_sms: int) -> None:
+    """Spread later K4 launches over at most ``n_sms`` SMs (0 = all)."""
+    N.check(N.lib().irm_rotate_gather_set_sm_limit(int(n_sms)), "irm_rotate_gather_set_sm_limit")
+
+
 def rotate_rows(rows: torch.Tensor, positions: torch.Tensor, inv_freq: torch.Tensor,
                 layout: int = N.LAYOUT_HALF_SPLIT, out_round: int = N.ROUND_NONE,
                 out: torch.Tensor | None = None) -> torch.Tensor:

@@ -14,6 +14,11 @@ chunk -> request map comes from the device CSR offsets, and non-hit chunks
 are masked to zero rows for K4. That makes the whole step capturable as a
 single CUDA graph (no tracing compiler), replayed per wave after the inputs
 are copied into the static buffers.
+
+``capture_overlapped`` adds a two-wave software pipeline: one graph per slot
+runs K4 of wave i (slot i % 2, on ~128 SMs) while K1 + K3 of wave i + 1 run on
+a forked stream over the remaining SMs and fill the other slot. K3 waves stay
+in order on that stream, so first-writer-wins across waves is unchanged.
 """
 
 from __future__ import annotations
@@ -49,6 +54,8 @@ class ReattachPipeline:
         self.gather_ws = torch.empty(int(N.lib().irm_rotate_gather_workspace_bytes(bound, kr_dim)),
                                      dtype=torch.uint8, device=dev)
         self.order0 = 0
+        self.fill_slot = None  # overlapped mode: the slot K3 compacts into
+        self.slots = None
         self.graph = None
         self.table = self.hit = self.length = self.delta = None
 
@@ -78,13 +85,28 @@ class ReattachPipeline:
         """PIC hits first (stable), with their count left on the device: K4 then
         walks only real work and the step stays free of host synchronisation."""
         perm = torch.argsort((~is_hit).to(torch.int8), stable=True)
-        self.k4_src, self.k4_dst = src[perm], dst[perm]
-        self.k4_len, self.k4_delta = self.length[perm], delta[perm]
-        self.n_hit = is_hit.sum().reshape(1).to(torch.int64)
+        if self.fill_slot is None:
+            self.k4_src, self.k4_dst = src[perm], dst[perm]
+            self.k4_len, self.k4_delta = self.length[perm], delta[perm]
+            self.n_hit = is_hit.sum().reshape(1).to(torch.int64)
+            return
+        sl = self.slots[self.fill_slot]  # overlapped mode: static per-slot buffers
+        torch.index_select(src, 0, perm, out=sl["src"])
+        torch.index_select(dst, 0, perm, out=sl["dst"])
+        torch.index_select(self.length, 0, perm, out=sl["len"])
+        torch.index_select(delta, 0, perm, out=sl["delta"])
+        sl["n_hit"].copy_(is_hit.sum().reshape(1))
+        sl["hit"].copy_(self.hit)
+        self.hit_tokens += self.length.sum(dtype=torch.int64)
 
-    def k4(self):
-        ops.rotate_gather(self.pool, self.out, self.k4_src, self.k4_dst, self.k4_len, self.k4_delta, self.inv,
-                          self.ckv, self.kr, self.layout, ws=self.gather_ws, n_dev=self.n_hit)
+    def k4(self, slot: int | None = None):
+        if slot is None:
+            ops.rotate_gather(self.pool, self.out, self.k4_src, self.k4_dst, self.k4_len, self.k4_delta, self.inv,
+                              self.ckv, self.kr, self.layout, ws=self.gather_ws, n_dev=self.n_hit)
+            return
+        sl = self.slots[slot]
+        ops.rotate_gather(self.pool, sl["out"], sl["src"], sl["dst"], sl["len"], sl["delta"], self.inv, self.ckv,
+                          self.kr, self.layout, ws=self.gather_ws, n_dev=sl["n_hit"])
 
     def step_eager(self):
         self.k1()
@@ -154,6 +176,105 @@ class ReattachPipeline:
         with torch.cuda.graph(self.graph_k4, pool=pool):
             self.k4()
         torch.cuda.synchronize()
+
+    def capture_overlapped(self, k4_sms: int = 128, warmup: int = 2):
+        """Capture the two-wave pipeline: ``front[s]`` = K1 + K3 of a wave into
+        slot s; ``overlap[s]`` = K4 of slot s on ``k4_sms`` SMs, concurrently with
+        front[1 - s] on a forked stream; ``drain[s]`` = K4 of slot s alone.
+        Per-slot outputs: ``slots[s]["out"]`` (KV), ``["hit"]`` (service map);
+        ``hit_tokens`` accumulates reattached tokens on the device."""
+        if self.table is None:
+            self.k1()
+        cap = self.table.start.numel()
+        dev = self.pool.device
+        i64 = dict(dtype=torch.int64, device=dev)
+        self.slots = []
+        for s in range(2):
+            self.slots.append(dict(
+                src=torch.zeros(cap, **i64), dst=torch.zeros(cap, **i64), delta=torch.zeros(cap, **i64),
+                len=torch.zeros(cap, dtype=torch.int32, device=dev), n_hit=torch.zeros(1, **i64),
+                hit=torch.zeros(cap, dtype=torch.int32, device=dev),
+                out=self.out if s == 0 else torch.empty_like(self.out)))
+        self.hit_tokens = torch.zeros((), **i64)
+        side = torch.cuda.Stream()
+
+        def front(s):
+            self.fill_slot = s
+            self.k1()
+            self.k3()
+            self.fill_slot = None
+
+        def overlap(s):
+            cur = torch.cuda.current_stream()
+            side.wait_stream(cur)
+            self.k4(s)
+            with torch.cuda.stream(side):
+                front(1 - s)
+            cur.wait_stream(side)
+
+        # warm up and capture over empty streams: no store side effects (nothing is
+        # probed or inserted), and every shape is capacity-bounded anyway
+        saved = (self.stream_off.clone(), self.pin_off.clone())
+        self.stream_off.zero_()
+        self.pin_off.zero_()
+        s0 = torch.cuda.Stream()
+        s0.wait_stream(torch.cuda.current_stream())
+        ops.set_rotate_gather_sm_limit(k4_sms)
+        try:
+            with torch.cuda.stream(s0):
+                for _ in range(warmup):
+                    front(0)
+                    overlap(0)
+                    self.k4(1)
+            torch.cuda.current_stream().wait_stream(s0)
+            torch.cuda.synchronize()
+            mp = torch.cuda.graph_pool_handle()
+            self.g_front, self.g_overlap, self.g_drain = [], [], []
+            for s in range(2):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, pool=mp):
+                    front(s)
+                self.g_front.append(g)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, pool=mp):
+                    overlap(s)
+                self.g_overlap.append(g)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, pool=mp):
+                    self.k4(s)
+                self.g_drain.append(g)
+        finally:
+            ops.set_rotate_gather_sm_limit(0)
+            torch.cuda.synchronize()
+            self.stream_off.copy_(saved[0])
+            self.pin_off.copy_(saved[1])
+        torch.cuda.synchronize()
+        self.hit_tokens.zero_()
+
+    def run_overlapped(self, n_waves: int, load_wave, after_front=None, after_k4=None):
+        """Process waves 0..n_waves-1 through the two-wave pipeline.
+        ``load_wave(i)`` copies wave i's inputs into the static buffers (called on
+        the current stream, after the previous graph that read them);
+        ``after_front(i, slot)`` is called once wave i's lookup results are in
+        ``slots[slot]`` (stream-ordered), e.g. to read the service map back;
+        ``after_k4(i, slot)`` once wave i's KV is in ``slots[slot]["out"]``."""
+        if n_waves <= 0:
+            return
+        load_wave(0)
+        self.g_front[0].replay()
+        if after_front:
+            after_front(0, 0)
+        for i in range(n_waves):
+            s = i & 1
+            if i + 1 < n_waves:
+                load_wave(i + 1)
+                self.g_overlap[s].replay()  # K4(i) || K1 + K3(i + 1) -> slot 1 - s
+                if after_front:
+                    after_front(i + 1, 1 - s)
+            else:
+                self.g_drain[s].replay()
+            if after_k4:
+                after_k4(i, s)
 
     def load(self, tok, stream_off, pin_off, pins, m):
         """Copy one wave's inputs (device-resident or pinned host) into the static buffers."""

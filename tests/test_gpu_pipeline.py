@@ -1,0 +1,160 @@
+"""GPU parity: the production reattach step (pipeline.ReattachPipeline, the path
+bench.py times) against the sequential oracle, for the serial CUDA graph and
+for the two-wave overlapped pipeline.
+
+Per wave of agent_meta-shaped requests (shared header = the phase-1 prefix,
+random metadata, the canonical marker, a shared body), the oracle runs
+oracle/irm_oracle.c's CDC + xxh64 per request and a sequential first-writer-wins
+dict in (wave, request, chunk) order, with carve-out chunks (p < 32) neither
+probed nor inserted (engine.py:181-226). New entries take pool rows in query
+order (store.cu). Checked bit-exact: the per-chunk service map (hit / novel /
+carve) of every wave. Checked against the oracle's bf16 rotate+gather
+(registry.py:146-166): every hit row of the per-request KV output, c_KV
+bit-exact, k_r within bf16 rounding."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+HEADER, BODY, R, WAVES, LAYERS, CARVE = 96, 5000, 3, 5, 2, 32
+
+
+def make_waves(seed=11):
+    shared = np.random.default_rng(7)
+    header = shared.integers(0, 2**32, size=HEADER, dtype=np.uint64).astype(np.uint32)
+    body = shared.integers(0, 2**32, size=BODY, dtype=np.uint64).astype(np.uint32)
+    marker = np.array(O.canonical_marker(), np.uint32)
+    rng = np.random.default_rng(seed)
+    waves = []
+    for w in range(WAVES + 1):  # wave 0 is the cold wave (one request: stores the body)
+        streams, pins, ms = [], [], []
+        for _ in range(1 if w == 0 else R):
+            meta = rng.integers(0, 2**32, size=int(rng.integers(30, 71)), dtype=np.uint64).astype(np.uint32)
+            if w > 0 and rng.random() < 0.3:  # some requests also edit the body
+                body_w = body.copy()
+                body_w[int(rng.integers(0, BODY))] ^= 1
+            else:
+                body_w = body
+            streams.append(np.concatenate([meta, marker, body_w]))
+            pins.append(sorted({meta.size - 1, meta.size + 63}))
+            ms.append(HEADER)
+        off = np.zeros(len(streams) + 1, np.int64)
+        np.cumsum([s.size for s in streams], out=off[1:])
+        poff = np.zeros(len(streams) + 1, np.int64)
+        np.cumsum([len(p) for p in pins], out=poff[1:])
+        waves.append((np.concatenate(streams), off, poff, np.array([x for p in pins for x in p], np.int64),
+                      np.array(ms, np.int64)))
+    return waves
+
+
+def oracle_waves(waves):
+    """Sequential reference: per wave, per chunk (hit code, p_src, row, p, len, request)."""
+    reg, rows_next, out = {}, 0, []
+    for tok, off, poff, pins, ms in waves:
+        recs = []
+        for r in range(off.size - 1):
+            st, ln, fp, _ = O.cdc_chunk(tok[off[r]:off[r + 1]], pins=pins[poff[r]:poff[r + 1]])
+            for s, l, f in zip(st.tolist(), ln.tolist(), fp.tolist()):
+                p = int(ms[r]) + s
+                if p < CARVE:
+                    recs.append((-1, 0, -1, p, l, r))
+                elif f in reg:
+                    recs.append((1, reg[f][0], reg[f][1], p, l, r))
+                else:
+                    reg[f] = (p, rows_next)
+                    recs.append((0, p, rows_next, p, l, r))
+                    rows_next += l
+        out.append(recs)
+    return out, rows_next
+
+
+def to_dev(wave):
+    return tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).cuda() for a in wave)
+
+
+@pytest.fixture(scope="module")
+def setup():
+    from paper_2605_05696_b200 import _native as N, ops
+
+    waves = make_waves()
+    ref, rows_used = oracle_waves(waves)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    pool = torch.randn(LAYERS, rows_used + 64, 576, device="cuda", generator=gen).to(torch.bfloat16)
+    inv = O.make_inv_freq(1e4)
+    max_tok = max(int(w[1][-1]) for w in waves)
+    max_pins = max(int(w[2][-1]) for w in waves)
+    req_stride = max(int(np.diff(w[1]).max()) for w in waves) + HEADER
+    return dict(N=N, ops=ops, waves=waves, ref=ref, pool=pool, inv=inv, max_tok=max_tok, max_pins=max_pins,
+                req_stride=req_stride)
+
+
+def new_pipe(S):
+    from paper_2605_05696_b200.pipeline import ReattachPipeline
+
+    ops = S["ops"]
+    store = ops.ChunkStore(max_entries=1 << 12)
+    return ReattachPipeline(store, S["pool"], ops.inv_freq_device(S["inv"]), R, S["max_tok"], S["max_pins"],
+                            S["req_stride"], layout=S["N"].LAYOUT_INTERLEAVED)
+
+
+def check_wave(S, w, hit, out):
+    """hit: service map (chunk order), out: [L, R * req_stride, 576] bf16 (host)."""
+    recs = S["ref"][w]
+    n = len(recs)
+    want = np.array([r[0] for r in recs], np.int64)
+    got = hit[:n].astype(np.int64)
+    assert np.array_equal(got, want), (w, np.nonzero(got != want)[0][:10])
+    hits = [r for r in recs if r[0] == 1]
+    assert hits, "workload must reattach something"
+    src = np.array([r[2] for r in hits], np.int64)
+    dst = np.array([r[5] * S["req_stride"] + r[3] for r in hits], np.int64)
+    ln = np.array([r[4] for r in hits], np.int32)
+    delta = np.array([r[3] - r[1] for r in hits], np.int64)
+    pool_u16 = S["pool"].view(torch.int16).cpu().numpy().view(np.uint16)
+    exp = np.zeros((LAYERS, out.shape[1], 576), np.uint16)
+    O.rotate_gather_bf16(pool_u16, exp, src, dst, ln, delta, S["inv"], interleaved=True)
+    got_u16 = out.view(torch.int16).numpy().view(np.uint16)
+    rows = np.concatenate([np.arange(d, d + l) for d, l in zip(dst, ln)])
+    assert np.array_equal(got_u16[:, rows, :512], exp[:, rows, :512])  # c_KV verbatim
+    f = lambda u: (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    g, e = f(got_u16[:, rows, 512:]), f(exp[:, rows, 512:])
+    assert np.abs(g - e).max() <= 2.0 ** -7 * np.abs(e).max(), "k_r beyond bf16 rounding"
+
+
+def test_pipeline_serial_graph(setup):
+    S = setup
+    pipe = new_pipe(S)
+    dev = [to_dev(w) for w in S["waves"]]
+    pipe.load(*dev[0])
+    pipe.step_eager()  # cold wave: inserts the body
+    torch.cuda.synchronize()
+    pipe.capture()  # its warm-up re-runs the cold wave: all hits, no new entries
+    for w in range(1, WAVES + 1):
+        pipe.load(*dev[w])
+        pipe.replay()
+        torch.cuda.synchronize()
+        check_wave(S, w, pipe.hit.cpu().numpy(), pipe.out.cpu())
+
+
+def test_pipeline_overlapped_matches_oracle(setup):
+    S = setup
+    pipe = new_pipe(S)
+    dev = [to_dev(w) for w in S["waves"]]
+    pipe.load(*dev[0])
+    pipe.step_eager()
+    torch.cuda.synchronize()
+    pipe.capture_overlapped(k4_sms=100)
+    hits, outs = {}, {}
+    pipe.run_overlapped(WAVES, lambda i: pipe.load(*dev[1 + i]),
+                        after_front=lambda i, s: hits.__setitem__(i, pipe.slots[s]["hit"].clone()),
+                        after_k4=lambda i, s: outs.__setitem__(i, pipe.slots[s]["out"].clone()))
+    torch.cuda.synchronize()
+    n_tok = 0
+    for i in range(WAVES):
+        check_wave(S, 1 + i, hits[i].cpu().numpy(), outs[i].cpu())
+        n_tok += sum(r[4] for r in S["ref"][1 + i] if r[0] == 1)
+    assert int(pipe.hit_tokens.item()) == n_tok

@@ -70,7 +70,9 @@ def _worker(rank, port, seed, out_q):
         ok = ok and bool((pool[:, local[1]:local[1] + 2, 1] == torch.tensor([10.0, 11.0])).all())
         again = cache.localize(grow, torch.tensor([4, 2, 4, 1]))  # cached: no new rows
         ok = ok and cache.fetched_rows == 6 and bool((again == local).all())
-        out_q.put((rank, res, hint, ok))
+        # plain lists: tensors would travel as shared-memory handles that vanish with this process
+        res = [tuple(x.tolist() for x in r) for r in res]
+        out_q.put((rank, res, hint.tolist(), ok))
     finally:
         dist.destroy_process_group()
 
@@ -95,7 +97,7 @@ def test_sharded_store_matches_sequential(seed):
     for rank, res, hint, ok in outs:
         assert ok, f"replica cache check failed on rank {rank}"
         for wave, (sl, h, ps, row, own) in enumerate(res):
-            for k, i in enumerate(sl.tolist()):
+            for k, i in enumerate(sl):
                 rows.append((int(order[i]) + wave * 10**7, i, rank, int(h[k]), int(ps[k]), int(row[k]),
                              int(hint[wave::3][k]), int(own[k])))
     rows.sort()
