@@ -1,3 +1,4 @@
+"""K4 (bf16, config-2 sized) HBM bandwidth vs the number of SMs it spreads over (irm_rotate_gather_set_sm_limit)."""
 import os, sys
 import numpy as np, torch
 sys.path.insert(0, ".")
@@ -14,7 +15,7 @@ ln = torch.from_numpy(lens).cuda()
 delta = torch.from_numpy(rng.integers(-5000, 5000, size=lens.size)).cuda()
 inv = ops.inv_freq_device(np.power(1e4, -2.0 * np.arange(32) / 64))
 for sms in [148, 144, 140, 136, 132, 128, 120, 112]:
-    os.environ["IRM_RG_SMS"] = str(sms)
+    ops.set_rotate_gather_sm_limit(sms)
     for _ in range(3):
         ops.rotate_gather(pool, out, src, dst, ln, delta, inv, layout=1)
     torch.cuda.synchronize()
