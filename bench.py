@@ -193,25 +193,29 @@ def run_ours(args):
     pipe = ReattachPipeline(store, pool, inv, R, max_tok, max_pins, req_stride, layout=N.LAYOUT_INTERLEAVED)
 
     sharded = world > 1 or args.sharded
-    if sharded:  # K6: hash-sharded store + replica cache, eager steps (host all-to-all splits)
+    if sharded:  # K6: hash-sharded store (fixed-capacity NCCL all-to-all) + peer replica cache
         from paper_2605_05696_b200 import shard
 
-        pipe.enable_sharding(shard.ShardedStore(store), shard.ReplicaCache(pool, replica_base=pool_rows // 2),
-                             rank, world)
+        cache = shard.ReplicaCache(pool, pool_rows // 2, shard.map_peer_pools(pool), rank,
+                                   ops.ChunkStore(max_entries=1 << 16))
+        pipe.enable_sharding(shard.ShardedStore(store), cache, rank, world)
         step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_sharded(i, allocate_rows=cold))
     else:
         step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_eager() if cold else pipe.replay())
     # cold request wave: inserts the body (its pool rows hold the random latents)
     step(len(dev_in) - 1, cold=True)
     torch.cuda.synchronize()
-    overlapped = not sharded and not args.serial
+    overlapped = not args.serial
     if not sharded:
         pipe.capture()  # one CUDA graph per step (+ K1-only / K4-only graphs for component timing)
     for i in range(args.warmup):
         step(i)
-    if overlapped:  # two-wave pipeline graphs (K4 on 128 SMs || K1 + K3 of the next wave)
+    if overlapped and not sharded:  # two-wave pipeline graphs (K4 on 128 SMs || K1 + K3 of the next wave)
         pipe.capture_overlapped(k4_sms=K4_SMS)
         pipe.run_overlapped(args.warmup, lambda i: pipe.load(*dev_in[i]))
+    if overlapped and sharded:  # the same pipeline on streams (NCCL all-to-all inside the front)
+        pipe.run_overlapped_sharded(args.warmup, lambda i: pipe.load(*dev_in[i]), wave0=n_steps + 2,
+                                    k4_sms=K4_SMS)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -226,7 +230,11 @@ def run_ours(args):
         if overlapped:
             pipe.hit_tokens.zero_()
             t0.record()
-            pipe.run_overlapped(args.steps, lambda i: pipe.load(*dev_in[args.warmup + i]))
+            if sharded:
+                pipe.run_overlapped_sharded(args.steps, lambda i: pipe.load(*dev_in[args.warmup + i]),
+                                            wave0=2 * n_steps + 4, k4_sms=K4_SMS)
+            else:
+                pipe.run_overlapped(args.steps, lambda i: pipe.load(*dev_in[args.warmup + i]))
             t1.record()
         else:
             t0.record()
@@ -288,7 +296,11 @@ def run_ours(args):
         def d2h(i, slot):  # D2H of wave i's per-chunk service result
             res[i].copy_(pipe.slots[slot]["hit"], non_blocking=True)
 
-        pipe.run_overlapped(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]), after_front=d2h)
+        if sharded:
+            pipe.run_overlapped_sharded(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]),
+                                        wave0=3 * n_steps + 6, k4_sms=K4_SMS, after_front=d2h)
+        else:
+            pipe.run_overlapped(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]), after_front=d2h)
         bo = pipe.slots[0]["hit"].numel() * pipe.slots[0]["hit"].element_size()
     else:
         for i in range(args.steps):
@@ -320,7 +332,8 @@ def run_ours(args):
                                "DSv2 interleaved rotary theta 1e4, 32K-token agent_meta prompts",
                    "requests_per_step": R, "tokens_per_request": tok_per_wave // R + HEADER,
                    "layers": LAYERS, "l2": "inputs larger than L2 (1.0 GB pool, 8 GB KV out per step)",
-                   "pipeline": ("two-wave overlap: K4 of wave i on %d SMs || K1 + K3 of wave i+1" % K4_SMS)
+                   "pipeline": ("two-wave overlap: K4 of wave i on %d SMs || K1 + K3 of wave i+1" % K4_SMS
+                                + (" (streams; sharded lookup + peer replica fetch)" if sharded else " (CUDA graphs)"))
                                if overlapped else "serial K1 -> K3 -> K4 per wave",
                    "parallelism": f"sessions s mod G over {world} GPU(s)" + (", store sharded by fp prefix, NCCL all-to-all lookup" if sharded else "")},
         "roofline": {"bound": "hbm", "kernel": "irm_rotate_gather (K4)", "achieved": k4_gbs,

@@ -148,6 +148,15 @@ int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, void *out,
  * CDC/lookup of the next wave running concurrently; the gather stays at the HBM
  * roofline down to ~128 SMs (profiles/r01d_k4_sms.md). */
 int irm_rotate_gather_set_sm_limit(int32_t n_sms);
+/* K6 replica fetch: for run c < min(n_runs, *n_runs_dev), copy len[c] rows of
+ * row_bytes from src_addr[c] + l * src_layer_stride (a device address, normally
+ * inside a peer GPU's pool mapped through CUDA IPC over NVLink) to
+ * dst + l * dst_layer_stride + dst_row[c] * row_bytes, for every layer l.
+ * Replaces the reference's in-process dict sharing of registry rows
+ * (registry.py:126-140) when the store is sharded across GPUs. */
+int irm_copy_runs(const int64_t *src_addr, int64_t src_layer_stride, void *dst, int64_t dst_layer_stride,
+                  const int64_t *dst_row, const int32_t *len, int64_t n_runs, const int64_t *n_runs_dev,
+                  int32_t layers, int32_t row_bytes, irm_stream_t stream);
 /* Per-row absolute rotation (producer side of the store, registry.py:131-133
  * with rotary.py:98-108): out[i] = R(positions[i]) rows[i] for the dim-wide
  * rotary rows at rows + i*row_stride (elements). out may alias rows. */

@@ -51,6 +51,7 @@ _SIGS = {
     "irm_store_lookup": ([ctypes.POINTER(StoreView), P, i64, P, P], i32),
     "irm_rotate_gather_workspace_bytes": ([i64, i32], i64),
     "irm_rotate_gather_set_sm_limit": ([i32], i32),
+    "irm_copy_runs": ([P, i64, P, i64, P, P, i64, P, i32, i32, P], i32),
     "irm_rotate_gather": ([P, i64, P, i64, i32, i32, i32, P, P, P, P, i64, P, P, i32, i32, i32, P, i64, P], i32),
     "irm_rotate_rows": ([P, i64, P, i64, i64, i32, P, P, i32, i32, i32, P], i32),
     "irm_round_f64": ([P, P, i64, i32, P], i32),

@@ -398,3 +398,39 @@ extern "C" int irm_round_f64(const double *x, double *y, int64_t n, int32_t mode
     IRM_LAUNCH_CHECK();
     return IRM_OK;
 }
+
+// Replica fetch (K6): copy runs of latent rows whose source lives in another GPU's pool,
+// addressed through peer (CUDA IPC / NVLink) mappings. One CTA per (run, layer) item,
+// grid-stride; 16-byte loads straight from peer memory, 16-byte stores to the local pool.
+namespace irm {
+__global__ void copy_runs_kernel(const int64_t *__restrict__ src_addr, int64_t src_ls, char *__restrict__ dst,
+                                 int64_t dst_ls, const int64_t *__restrict__ dst_row, const int32_t *__restrict__ len,
+                                 int64_t n_runs, const int64_t *__restrict__ n_runs_dev, int layers, int row_bytes) {
+    if (n_runs_dev) n_runs = min(n_runs, *n_runs_dev);
+    const int64_t items = n_runs * layers;
+    const int vec = row_bytes / 16;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int64_t c = it / layers;
+        const int l = (int)(it - c * layers);
+        const int64_t n16 = (int64_t)__ldg(len + c) * vec;
+        const uint4 *s = reinterpret_cast<const uint4 *>((const char *)__ldg(src_addr + c) + l * src_ls);
+        uint4 *d = reinterpret_cast<uint4 *>(dst + l * dst_ls + __ldg(dst_row + c) * (int64_t)row_bytes);
+        for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
+    }
+}
+}  // namespace irm
+
+extern "C" int irm_copy_runs(const int64_t *src_addr, int64_t src_layer_stride, void *dst, int64_t dst_layer_stride,
+                             const int64_t *dst_row, const int32_t *len, int64_t n_runs, const int64_t *n_runs_dev,
+                             int32_t layers, int32_t row_bytes, irm_stream_t stream) {
+    IRM_REQUIRE(n_runs >= 0 && layers >= 1 && row_bytes > 0 && row_bytes % 16 == 0, "bad sizes");
+    IRM_REQUIRE(src_layer_stride % 16 == 0 && dst_layer_stride % 16 == 0, "layer strides must be 16-byte multiples");
+    if (n_runs == 0) return IRM_OK;
+    IRM_REQUIRE(src_addr && dst && dst_row && len, "null pointer");
+    IRM_REQUIRE(((uintptr_t)dst & 15) == 0, "dst must be 16-byte aligned");
+    int64_t grid = std::min<int64_t>(n_runs * layers, (int64_t)sm_count() * 8);
+    irm::copy_runs_kernel<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, (cudaStream_t)stream>>>(
+        src_addr, src_layer_stride, (char *)dst, dst_layer_stride, dst_row, len, n_runs, n_runs_dev, layers, row_bytes);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}

@@ -173,6 +173,18 @@ def rotate_gather(pool: torch.Tensor, out: torch.Tensor, src_row: torch.Tensor, 
     N.check(rc, "irm_rotate_gather")
 
 
+def copy_runs(src_addr: torch.Tensor, src_layer_stride: int, dst_pool: torch.Tensor, dst_row: torch.Tensor,
+              length: torch.Tensor, n_dev: torch.Tensor | None = None) -> None:
+    """K6 replica fetch: runs of rows from device addresses (peer pools mapped
+    over NVLink) into ``dst_pool`` [layers, rows, width]; strides in bytes."""
+    assert dst_pool.dim() == 3 and dst_pool.is_contiguous()
+    row_bytes = dst_pool.shape[2] * dst_pool.element_size()
+    rc = N.lib().irm_copy_runs(N.ptr(src_addr), int(src_layer_stride), N.ptr(dst_pool),
+                               dst_pool.stride(0) * dst_pool.element_size(), N.ptr(dst_row), N.ptr(length),
+                               src_addr.numel(), N.ptr(n_dev), dst_pool.shape[0], row_bytes, N.stream_ptr())
+    N.check(rc, "irm_copy_runs")
+
+
 def set_rotate_gather_sm_limit(n_sms: int) -> None:
     """Spread later K4 launches over at most ``n_sms`` SMs (0 = all)."""
     N.check(N.lib().irm_rotate_gather_set_sm_limit(int(n_sms)), "irm_rotate_gather_set_sm_limit")

@@ -116,10 +116,11 @@ class ReattachPipeline:
     # ------------------------------------------------------------ multi-GPU (K6)
     def enable_sharding(self, sharded_store, replica_cache, rank: int, world: int):
         """Route K3 through the hash-sharded store (shard.ShardedStore) and K4's
-        sources through the replica cache. Steps then run eagerly: the
-        all-to-all split sizes are host values."""
+        sources through the replica cache. Sharded steps run eagerly (NCCL
+        all-to-alls between the kernels) but never wait for the host: every
+        buffer is capacity-bounded, so the CPU runs ahead of the GPU."""
         self.sharded, self.replica, self.rank, self.world = sharded_store, replica_cache, rank, world
-        self.hint_next = 0
+        self.hint_next = torch.zeros((), dtype=torch.int64, device=self.pool.device)
 
     def k3_sharded(self, wave: int, allocate_rows: bool):
         from . import shard
@@ -139,7 +140,7 @@ class ReattachPipeline:
         ln = t.length.to(torch.int64) * probe
         if allocate_rows:  # this rank keeps the KV of chunks it may be first to write
             local = self.hint_next + torch.cumsum(ln, 0) - ln
-            self.hint_next += int(ln.sum().item())
+            self.hint_next += ln.sum()
         else:
             local = torch.zeros_like(ln)
         hint = shard.encode_row(self.rank, local)
@@ -154,6 +155,47 @@ class ReattachPipeline:
         self.k1()
         self.k3_sharded(wave, allocate_rows)
         self.k4()
+
+    def run_overlapped_sharded(self, n_waves: int, load_wave, wave0: int = 0, k4_sms: int = 128,
+                               after_front=None, after_k4=None):
+        """The two-wave pipeline of ``run_overlapped`` for the sharded store, on
+        streams instead of graphs: K4 of wave i (main stream, ``k4_sms`` SMs)
+        runs while K1 + the sharded lookup + replica fetch of wave i + 1 run on a
+        side stream. Waves are numbered ``wave0 + i`` in the global order key."""
+        if n_waves <= 0:
+            return
+        self._alloc_slots()
+        main = torch.cuda.current_stream()
+        side = self._side if getattr(self, "_side", None) is not None else torch.cuda.Stream()
+        self._side = side
+
+        def front(i, s):
+            self.fill_slot = s
+            self.k1()
+            self.k3_sharded(wave0 + i, False)
+            self.fill_slot = None
+
+        ops.set_rotate_gather_sm_limit(k4_sms)
+        try:
+            load_wave(0)
+            front(0, 0)
+            if after_front:
+                after_front(0, 0)
+            for i in range(n_waves):
+                s = i & 1
+                if i + 1 < n_waves:
+                    load_wave(i + 1)
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        front(i + 1, 1 - s)
+                self.k4(s)
+                main.wait_stream(side)
+                if after_front and i + 1 < n_waves:
+                    after_front(i + 1, 1 - s)
+                if after_k4:
+                    after_k4(i, s)
+        finally:
+            ops.set_rotate_gather_sm_limit(0)
 
     # ------------------------------------------------------------ graphs
     def capture(self, warmup: int = 2):
@@ -177,12 +219,9 @@ class ReattachPipeline:
             self.k4()
         torch.cuda.synchronize()
 
-    def capture_overlapped(self, k4_sms: int = 128, warmup: int = 2):
-        """Capture the two-wave pipeline: ``front[s]`` = K1 + K3 of a wave into
-        slot s; ``overlap[s]`` = K4 of slot s on ``k4_sms`` SMs, concurrently with
-        front[1 - s] on a forked stream; ``drain[s]`` = K4 of slot s alone.
-        Per-slot outputs: ``slots[s]["out"]`` (KV), ``["hit"]`` (service map);
-        ``hit_tokens`` accumulates reattached tokens on the device."""
+    def _alloc_slots(self):
+        if self.slots is not None:
+            return
         if self.table is None:
             self.k1()
         cap = self.table.start.numel()
@@ -196,6 +235,14 @@ class ReattachPipeline:
                 hit=torch.zeros(cap, dtype=torch.int32, device=dev),
                 out=self.out if s == 0 else torch.empty_like(self.out)))
         self.hit_tokens = torch.zeros((), **i64)
+
+    def capture_overlapped(self, k4_sms: int = 128, warmup: int = 2):
+        """Capture the two-wave pipeline: ``front[s]`` = K1 + K3 of a wave into
+        slot s; ``overlap[s]`` = K4 of slot s on ``k4_sms`` SMs, concurrently with
+        front[1 - s] on a forked stream; ``drain[s]`` = K4 of slot s alone.
+        Per-slot outputs: ``slots[s]["out"]`` (KV), ``["hit"]`` (service map);
+        ``hit_tokens`` accumulates reattached tokens on the device."""
+        self._alloc_slots()
         side = torch.cuda.Stream()
 
         def front(s):

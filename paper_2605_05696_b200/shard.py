@@ -4,19 +4,24 @@ Sessions are data-parallel (session s on rank s mod G). The content store is
 sharded by fingerprint prefix: the owner of fp is ``(fp >> 32) * G >> 32``,
 which equals ``fp >> (64 - log2 G)`` for a power-of-two G. A lookup wave is one
 exchange over ``torch.distributed`` (NCCL over NVLink on B200, gloo in the CPU
-tests):
+tests), with fixed-capacity buffers so nothing on the path waits for the host:
 
-  1. all-to-all of per-owner query counts
-  2. all-to-all of the queries (fp, order key, p, len, row hint)
+  1. every probed query goes to slot (owner, position in the owner's bucket)
+     of a [G, cap, 5] send buffer (fp, order key, p, len, row hint); unused
+     slots carry padding order keys that sort after every real key
+  2. all-to-all of equal splits
   3. the owner sorts what it received by the global order key (request,
      chunk) and runs the first-writer-wins batch on its shard (K3), so the
      winner is the globally earliest query, exactly as the sequential
      reference (engine.py:197-223)
-  4. reverse all-to-all of (hit, p_src, row) to the asking rank
+  4. reverse all-to-all of (hit, p_src, row) into the same slots
 
 Rows are named globally: ``row = rank << 40 | local_row``. A hit whose rows
-live on another rank is fetched once into this rank's replica pool
-(``ReplicaCache``), so the rotate+gather (K4) always reads local HBM.
+live on another rank is fetched once into this rank's replica region of its
+pool (``ReplicaCache``): the peer pools are mapped into every process (CUDA
+IPC over NVLink), a second store keyed by the global row dedupes runs and
+assigns replica rows, and ``irm_copy_runs`` pulls the rows peer-to-peer. K4
+then always reads local HBM.
 """
 
 from __future__ import annotations
@@ -26,6 +31,7 @@ import torch.distributed as dist
 
 ROW_SHIFT = 40
 ROW_MASK = (1 << ROW_SHIFT) - 1
+PAD_ORDER = 1 << 62  # order keys of padding slots: above every (request << 20 | chunk) key
 
 
 def owner_of(fp: torch.Tensor, world: int) -> torch.Tensor:
@@ -42,157 +48,158 @@ def decode_row(grow: torch.Tensor):
     return grow >> ROW_SHIFT, grow & ROW_MASK
 
 
-def _a2a(output: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group):
-    dist.all_to_all_single(output, inp, out_splits, in_splits, group=group)
-
-
 class ShardedStore:
     """Wraps a local store shard (``ops.ChunkStore`` on GPU; any object with
-    the same ``lookup_insert`` contract, e.g. a test dict store on CPU)."""
+    the same ``lookup_insert`` contract and an ``e_row`` entry array, e.g. a
+    test dict store on CPU)."""
 
     def __init__(self, local_store, group=None):
         self.local = local_store
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        e_row = local_store.e_row
+        # global row of every entry of this shard (+1: scatter sink for non-novel queries)
+        self.e_grow = torch.full((e_row.numel() + 1,), -1, dtype=torch.int64, device=e_row.device)
         self.last_exchange_bytes = 0
 
     def lookup_insert(self, q_fp, q_order, q_p, q_len, q_probe=None, q_row_hint=None):
         """Same contract as ops.ChunkStore.lookup_insert, over the sharded store.
 
-        q_order must be globally unique (e.g. (global request << 20) | chunk).
-        q_row_hint: global row (encode_row) where this rank keeps the chunk's
-        KV if it is the first writer. Returns (hit, p_src, row, owner)."""
+        q_order must be globally unique and < 2^62 (e.g. (global request << 20) |
+        chunk). q_row_hint: global row (encode_row) where this rank keeps the
+        chunk's KV if it is the first writer. Returns (hit, p_src, row, owner).
+        No host synchronisation: every buffer has a fixed capacity of
+        q_fp.numel() slots per owner."""
         dev = q_fp.device
-        n = q_fp.numel()
+        n, G = q_fp.numel(), self.world
+        i64 = dict(dtype=torch.int64, device=dev)
         probe = torch.ones(n, dtype=torch.bool, device=dev) if q_probe is None else q_probe.to(torch.bool)
-        if q_row_hint is None:
-            q_row_hint = torch.full((n,), -1, dtype=torch.int64, device=dev)
-        sel = torch.nonzero(probe).flatten()
-        own = owner_of(q_fp[sel], self.world)
+        hint = torch.full((n,), -1, **i64) if q_row_hint is None else q_row_hint.to(torch.int64)
+        cap = max(n, 1)
+        own = torch.where(probe, owner_of(q_fp, G), torch.full_like(q_fp, G))  # bucket G: not probed
         perm = torch.argsort(own, stable=True)
-        sel = sel[perm]
-        own = own[perm]
-        send = torch.stack([q_fp[sel], q_order[sel], q_p[sel].to(torch.int64), q_len[sel].to(torch.int64),
-                            q_row_hint[sel]], dim=1).contiguous()
-        counts = torch.bincount(own, minlength=self.world).to(torch.int64)
-        recv_counts = torch.empty_like(counts)
-        dist.all_to_all_single(recv_counts, counts, group=self.group)
-        in_splits = counts.cpu().tolist()
-        out_splits = recv_counts.cpu().tolist()
-        recv = torch.empty(sum(out_splits), 5, dtype=torch.int64, device=dev)
-        _a2a(recv, send, out_splits, in_splits, self.group)
+        own_s = own[perm]
+        counts = torch.zeros(G + 1, **i64).scatter_add_(0, own, torch.ones(n, **i64))
+        start = torch.cumsum(counts, 0) - counts
+        valid = own_s < G
+        dest = torch.where(valid, own_s * cap + torch.arange(n, **i64) - start[own_s], G * cap)
+        send = torch.zeros(G * cap + 1, 5, **i64)  # last row: sink for unprobed queries
+        send[:, 1] = PAD_ORDER + self.rank * G * cap + torch.arange(G * cap + 1, **i64)  # unique padding keys
+        send[:, 4] = -1
+        send.index_copy_(0, dest, torch.stack([q_fp, q_order, q_p.to(torch.int64), q_len.to(torch.int64), hint],
+                                              dim=1)[perm])
+        send = send[:G * cap].contiguous()
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=self.group)
 
-        # owner side: the global first writer is the smallest order key
+        # owner side: the global first writer is the smallest order key (padding sorts last)
         o = torch.argsort(recv[:, 1])
         r = recv[o]
+        real = r[:, 1] < PAD_ORDER
         hit, entry, p_src, _row = self.local.lookup_insert(
-            r[:, 0].contiguous(), r[:, 1].contiguous(), r[:, 2].contiguous(), r[:, 3].to(torch.int32).contiguous())
+            r[:, 0].contiguous(), r[:, 1].contiguous(), r[:, 2].contiguous(), r[:, 3].to(torch.int32).contiguous(),
+            real)
         novel = hit == 0
-        # the new entry's rows are the winner's (row hint); hits read the entry's row
-        e_row = self.local.e_row
-        e_row[entry[novel]] = r[novel, 4]
-        rows = e_row[entry.clamp_min(0)]
-        reply_sorted = torch.stack([hit.to(torch.int64), p_src, rows], dim=1)
-        reply = torch.empty_like(reply_sorted)
-        reply[o] = reply_sorted
-        back = torch.empty(len(sel), 3, dtype=torch.int64, device=dev)
-        _a2a(back, reply.contiguous(), in_splits, out_splits, self.group)
-        self.last_exchange_bytes = 8 * (5 * (sum(in_splits) + sum(out_splits)) + 3 * (sum(in_splits) + sum(out_splits)))
+        sink = self.e_grow.numel() - 1
+        # the new entry's rows are its first writer's (row hint); each entry has one novel query
+        self.e_grow.index_copy_(0, torch.where(novel, entry, torch.full_like(entry, sink)), r[:, 4].contiguous())
+        rows = torch.where(entry >= 0, self.e_grow[entry.clamp_min(0)], torch.full_like(entry, -1))
+        reply = torch.empty(G * cap, 3, **i64)
+        reply.index_copy_(0, o, torch.stack([hit.to(torch.int64), p_src.to(torch.int64), rows], dim=1))
+        back = torch.empty_like(reply)
+        dist.all_to_all_single(back, reply, group=self.group)
+        self.last_exchange_bytes = 2 * G * cap * (5 + 3) * 8
 
+        res = back[torch.where(valid, dest, torch.zeros_like(dest))]  # sorted position k -> its slot
         out_hit = torch.full((n,), -1, dtype=torch.int32, device=dev)
-        out_psrc = torch.zeros(n, dtype=torch.int64, device=dev)
-        out_row = torch.full((n,), -1, dtype=torch.int64, device=dev)
-        out_owner = torch.full((n,), -1, dtype=torch.int64, device=dev)
-        out_hit[sel] = back[:, 0].to(torch.int32)
-        out_psrc[sel] = back[:, 1]
-        out_row[sel] = back[:, 2]
-        out_owner[sel] = own
+        out_psrc = torch.zeros(n, **i64)
+        out_row = torch.full((n,), -1, **i64)
+        out_owner = torch.full((n,), -1, **i64)
+        out_hit.index_copy_(0, perm, torch.where(valid, res[:, 0], -1).to(torch.int32))
+        out_psrc.index_copy_(0, perm, torch.where(valid, res[:, 1], 0))
+        out_row.index_copy_(0, perm, torch.where(valid, res[:, 2], -1))
+        out_owner.index_copy_(0, perm, torch.where(valid, own_s, -1))
         return out_hit, out_psrc, out_row, out_owner
+
+
+def map_peer_pools(pool: torch.Tensor, group=None) -> list[torch.Tensor]:
+    """Every rank's latent pool, mapped into this process (CUDA IPC; peer access
+    over NVLink is enabled lazily on first touch). Index = rank."""
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if world == 1:
+        return [pool]
+    objs = [None] * world
+    dist.all_gather_object(objs, reduce_tensor(pool), group=group)
+    return [pool if r == rank else objs[r][0](*objs[r][1]) for r in range(world)]
 
 
 class ReplicaCache:
     """Per-rank replica of remote latent rows, keyed by global row.
 
     ``pool`` is this rank's latent pool [layers, rows, width]; the replica
-    region starts at ``replica_base`` and grows. ``localize`` turns global
-    rows (encode_row) of hit chunks into local rows, fetching every missing
-    remote run once via one all-to-all of row requests and one of row data."""
+    region starts at ``replica_base``. ``peer_pools[r]`` is rank r's pool as
+    seen from this process (``map_peer_pools``; same shape on every rank).
+    ``map_store`` is a first-writer-wins store (``ops.ChunkStore``) keyed by the
+    global row of a run start: a novel key allocates replica rows by the
+    store's exclusive scan of run lengths, which is exactly a bump allocator
+    that dedupes runs within and across waves."""
 
-    def __init__(self, pool: torch.Tensor, replica_base: int, group=None):
-        self.pool = pool
-        self.base = replica_base
-        self.next = replica_base
-        self.map: dict[int, int] = {}  # global row of a run start -> local row
-        self.group = group
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        self.fetched_rows = 0
+    def __init__(self, pool: torch.Tensor, replica_base: int, peer_pools: list[torch.Tensor], rank: int,
+                 map_store):
+        self.pool, self.base, self.peers, self.rank, self.map = pool, replica_base, peer_pools, rank, map_store
+        for pp in peer_pools:
+            assert pp.shape == pool.shape and pp.dtype == pool.dtype and pp.is_contiguous()
+        dev = pool.device
+        self.row_bytes = pool.shape[2] * pool.element_size()
+        self.layer_bytes = pool.stride(0) * pool.element_size()
+        self.peer_base = torch.tensor([pp.data_ptr() for pp in peer_pools], dtype=torch.int64, device=dev)
+        self.overflow = torch.zeros((), dtype=torch.bool, device=dev)
+        self.fetched_runs = torch.zeros((), dtype=torch.int64, device=dev)
+        self.fetched_rows = torch.zeros((), dtype=torch.int64, device=dev)
 
     def localize(self, grow: torch.Tensor, length: torch.Tensor) -> torch.Tensor:
-        """grow [n] global rows (or -1), length [n] -> local rows (int64)."""
+        """grow [n] global rows (or -1), length [n] -> local rows (int64).
+        Missing remote runs are fetched peer-to-peer first (stream-ordered)."""
         dev = grow.device
-        need: list[list[tuple[int, int]]] = [[] for _ in range(self.world)]
+        n = grow.numel()
+        i64 = dict(dtype=torch.int64, device=dev)
         gt = grow.to(torch.int64)
-        remote = (gt >= 0) & ((gt >> ROW_SHIFT) != self.rank)
-        if bool(remote.any()):
-            uniq, inv = torch.unique(gt[remote], return_inverse=True)
-            first = torch.full((uniq.numel(),), -1, dtype=torch.int64, device=dev)
-            first.scatter_reduce_(0, inv, length.to(torch.int64)[remote], reduce="amax", include_self=False)
-            for gr, l in zip(uniq.cpu().tolist(), first.cpu().tolist()):
-                if gr not in self.map:
-                    need[gr >> ROW_SHIFT].append((gr & ROW_MASK, l))
-        # 1. request counts and (row, len) requests
-        counts = torch.tensor([len(x) for x in need], dtype=torch.int64, device=dev)
-        recv_counts = torch.empty_like(counts)
-        dist.all_to_all_single(recv_counts, counts, group=self.group)
-        in_splits, out_splits = counts.cpu().tolist(), recv_counts.cpu().tolist()
-        req = torch.tensor([x for lst in need for x in lst], dtype=torch.int64, device=dev).reshape(-1, 2)
-        got = torch.empty(sum(out_splits), 2, dtype=torch.int64, device=dev)
-        _a2a(got, req, out_splits, in_splits, self.group)
-        # 2. serve: gather the requested runs of my pool, row-major [rows, layers, width]
-        L, _, W = self.pool.shape
-        g_rows = got[:, 0].cpu().tolist()
-        g_len = got[:, 1].cpu().tolist()
-        send_rows_per_peer = []
-        pieces = []
-        pos = 0
-        for peer in range(self.world):
-            cnt = 0
-            for i in range(pos, pos + out_splits[peer]):
-                pieces.append(self.pool[:, g_rows[i]:g_rows[i] + g_len[i]].transpose(0, 1))
-                cnt += g_len[i]
-            pos += out_splits[peer]
-            send_rows_per_peer.append(cnt)
-        send = (torch.cat(pieces) if pieces else torch.empty(0, L, W, dtype=self.pool.dtype, device=dev)).contiguous()
-        # 3. row counts back, then the rows
-        send_counts = torch.tensor(send_rows_per_peer, dtype=torch.int64, device=dev)
-        recv_rows = torch.empty_like(send_counts)
-        dist.all_to_all_single(recv_rows, send_counts, group=self.group)
-        rr = recv_rows.cpu().tolist()
-        data = torch.empty(sum(rr), L, W, dtype=self.pool.dtype, device=dev)
-        _a2a(data, send, rr, send_rows_per_peer, self.group)
-        # 4. install replicas (requests were issued owner-major, in `need` order)
-        total = int(sum(rr))
-        if self.next + total > self.pool.shape[1]:
+        ln = length.to(torch.int64)
+        src_rank = gt >> ROW_SHIFT
+        remote = (gt >= 0) & (src_rank != self.rank)
+        hit, _e, _p, row = self.map.lookup_insert(gt.contiguous(), torch.arange(n, **i64), torch.zeros(n, **i64),
+                                                  ln.to(torch.int32).contiguous(), remote)
+        local = self.base + row
+        fits = local + ln <= self.pool.shape[1]
+        new = remote & (hit == 0)
+        self.overflow |= (new & ~fits).any()
+        fetch = new & fits
+        perm = torch.argsort((~fetch).to(torch.int8), stable=True)  # runs to fetch first
+        n_fetch = fetch.sum().reshape(1)
+        self.fetched_runs += n_fetch[0]
+        self.fetched_rows += (ln * fetch).sum()
+        src_addr = (self.peer_base[src_rank.clamp(0, len(self.peers) - 1)] +
+                    (gt & ROW_MASK) * self.row_bytes)[perm].contiguous()
+        self._copy(src_addr, src_rank[perm], (gt & ROW_MASK)[perm], local[perm].contiguous(),
+                   ln[perm].to(torch.int32).contiguous(), n_fetch)
+        return torch.where(remote, local, torch.where(gt >= 0, gt & ROW_MASK, torch.zeros_like(gt)))
+
+    def _copy(self, src_addr, src_rank, src_row, dst_row, length, n_fetch):
+        if self.pool.is_cuda:
+            from . import ops
+
+            ops.copy_runs(src_addr, self.layer_bytes, self.pool, dst_row, length, n_dev=n_fetch)
+            return
+        # CPU tensors (the gloo tests, with shared-memory pools standing in for peer mappings):
+        # the same copy, run by torch on the host
+        for c in range(int(n_fetch[0])):
+            r, s, d, l = int(src_rank[c]), int(src_row[c]), int(dst_row[c]), int(length[c])
+            self.pool[:, d:d + l] = self.peers[r][:, s:s + l]
+
+    def check(self):
+        """Host check (call outside timed regions): the replica region held every fetch."""
+        if bool(self.overflow):
             raise RuntimeError("replica region of the pool is full")
-        if total:
-            self.pool[:, self.next:self.next + total] = data.transpose(0, 1)
-        off = self.next
-        for rk in range(self.world):
-            for row, l in need[rk]:
-                self.map[(rk << ROW_SHIFT) | row] = off
-                off += l
-        self.next += total
-        self.fetched_rows += total
-        # 5. map every hit to a local row (vectorised: own rows pass through, remote run
-        #    starts are translated with one searchsorted over the replica map)
-        gt = grow.to(torch.int64)
-        out = torch.where((gt >> ROW_SHIFT) == self.rank, gt & ROW_MASK, torch.zeros_like(gt))
-        remote = (gt >= 0) & ((gt >> ROW_SHIFT) != self.rank)
-        if bool(remote.any()):
-            keys = torch.tensor(sorted(self.map), dtype=torch.int64, device=dev)
-            vals = torch.tensor([self.map[k] for k in sorted(self.map)], dtype=torch.int64, device=dev)
-            pos = torch.searchsorted(keys, gt[remote]).clamp_max(keys.numel() - 1)
-            out[remote] = vals[pos]
-        return out

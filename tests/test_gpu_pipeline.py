@@ -158,3 +158,70 @@ def test_pipeline_overlapped_matches_oracle(setup):
         check_wave(S, 1 + i, hits[i].cpu().numpy(), outs[i].cpu())
         n_tok += sum(r[4] for r in S["ref"][1 + i] if r[0] == 1)
     assert int(pipe.hit_tokens.item()) == n_tok
+
+
+def test_replica_fetch_peer_pools():
+    """K6 replica fetch on one GPU: a second pool stands in for a peer's
+    (shard.map_peer_pools gives the same kind of tensor for another GPU). Runs
+    are fetched once by irm_copy_runs, duplicates and later waves reuse them."""
+    from paper_2605_05696_b200 import ops, shard
+
+    L, rows = 3, 4096
+    pools = [torch.randn(L, rows, 576, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    cache = shard.ReplicaCache(pools[0], 2048, pools, 0, ops.ChunkStore(1 << 10))
+    rng = np.random.default_rng(4)
+    starts = rng.choice(np.arange(0, 1500, 64), size=12, replace=False)
+    lens = rng.integers(1, 64, size=12)
+    sel = np.concatenate([np.arange(12), [0, 5, 5]])  # runs 0 and 5 asked for again in the same wave
+    grow = shard.encode_row(1, torch.from_numpy(starts[sel]).cuda())
+    grow = torch.cat([grow, shard.encode_row(0, torch.tensor([7], device="cuda")),
+                      torch.tensor([-1], device="cuda")])
+    ln = torch.from_numpy(np.concatenate([lens[sel], [5, 3]]).astype(np.int32)).cuda()
+    local = cache.localize(grow, ln).cpu().numpy()
+    torch.cuda.synchronize()
+    assert int(cache.fetched_runs) == 12 and int(cache.fetched_rows) == int(lens.sum())
+    assert local[12] == local[0] and local[13] == local[14] == local[5]
+    assert local[15] == 7  # own rows pass through
+    p0, p1 = pools[0].cpu(), pools[1].cpu()
+    for k in range(12):
+        a, l = int(local[k]), int(lens[k])
+        assert a >= 2048 and torch.equal(p0[:, a:a + l], p1[:, starts[k]:starts[k] + l])
+    again = cache.localize(grow[:12], ln[:12]).cpu().numpy()
+    assert np.array_equal(again, local[:12]) and int(cache.fetched_runs) == 12
+    cache.check()
+
+
+def test_pipeline_sharded_single_rank(setup):
+    """The sharded step (NCCL all-to-all lookup, world 1) in the overlapped
+    stream pipeline reproduces the oracle like the unsharded graph path."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2605_05696_b200 import shard
+
+    S = setup
+    ops = S["ops"]
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29541")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        pipe = new_pipe(S)
+        peers = shard.map_peer_pools(S["pool"])
+        pipe.enable_sharding(shard.ShardedStore(pipe.store), shard.ReplicaCache(
+            S["pool"], S["pool"].shape[1] - 32, peers, 0, ops.ChunkStore(1 << 10)), 0, 1)
+        dev = [to_dev(w) for w in S["waves"]]
+        pipe.load(*dev[0])
+        pipe.step_sharded(0, allocate_rows=True)  # cold wave: hints give the oracle's rows
+        torch.cuda.synchronize()
+        hits, outs = {}, {}
+        pipe.run_overlapped_sharded(WAVES, lambda i: pipe.load(*dev[1 + i]), wave0=1, k4_sms=100,
+                                    after_front=lambda i, s: hits.__setitem__(i, pipe.slots[s]["hit"].clone()),
+                                    after_k4=lambda i, s: outs.__setitem__(i, pipe.slots[s]["out"].clone()))
+        torch.cuda.synchronize()
+        for i in range(WAVES):
+            check_wave(S, 1 + i, hits[i].cpu().numpy(), outs[i].cpu())
+        pipe.replica.check()
+    finally:
+        dist.destroy_process_group()

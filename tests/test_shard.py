@@ -37,7 +37,7 @@ def _queries(seed, n_total=600):
     return fp, order, p, ln, probe, rank_of
 
 
-def _worker(rank, port, seed, out_q):
+def _worker(rank, port, seed, out_q, pools):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
@@ -55,21 +55,21 @@ def _worker(rank, port, seed, out_q):
                                                   hint[wave::3])
             res.append((sl, h, ps, row, own))
 
-        # replica cache: pool rows hold (rank, row) stamps
-        pool = torch.zeros(2, 64, 3)
-        pool[:, :, 0] = rank
-        pool[:, :, 1] = torch.arange(64, dtype=torch.float32)
-        cache = shard.ReplicaCache(pool, replica_base=32)
+        # replica cache: pool rows hold (rank, row) stamps; the shared-memory pools of
+        # both ranks stand in for the CUDA-IPC peer mappings of shard.map_peer_pools
+        pool = pools[rank]
+        cache = shard.ReplicaCache(pool, 32, pools, rank, DictStore())
         other = 1 - rank
         grow = shard.encode_row(other, torch.tensor([3, 10, 3, -1], dtype=torch.int64))
         grow[3] = -1
         local = cache.localize(grow, torch.tensor([4, 2, 4, 1]))
-        ok = bool(local[0] == local[2]) and cache.fetched_rows == 6
+        ok = bool(local[0] == local[2]) and int(cache.fetched_rows) == 6 and int(cache.fetched_runs) == 2
         ok = ok and bool((pool[:, local[0]:local[0] + 4, 0] == other).all())
         ok = ok and bool((pool[:, local[0]:local[0] + 4, 1] == torch.arange(3, 7).float()).all())
         ok = ok and bool((pool[:, local[1]:local[1] + 2, 1] == torch.tensor([10.0, 11.0])).all())
         again = cache.localize(grow, torch.tensor([4, 2, 4, 1]))  # cached: no new rows
-        ok = ok and cache.fetched_rows == 6 and bool((again == local).all())
+        ok = ok and int(cache.fetched_rows) == 6 and bool((again == local).all())
+        cache.check()
         # plain lists: tensors would travel as shared-memory handles that vanish with this process
         res = [tuple(x.tolist() for x in r) for r in res]
         out_q.put((rank, res, hint.tolist(), ok))
@@ -84,7 +84,13 @@ def test_sharded_store_matches_sequential(seed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, seed, q)) for r in range(WORLD)]
+    pools = []
+    for r in range(WORLD):
+        pool = torch.zeros(2, 64, 3)
+        pool[:, :, 0] = r
+        pool[:, :, 1] = torch.arange(64, dtype=torch.float32)
+        pools.append(pool.share_memory_())
+    procs = [ctx.Process(target=_worker, args=(r, port, seed, q, pools)) for r in range(WORLD)]
     for pr in procs:
         pr.start()
     outs = [q.get(timeout=240) for _ in range(WORLD)]
