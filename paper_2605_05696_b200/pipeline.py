@@ -40,12 +40,13 @@ class ReattachPipeline:
         self.params = (mask_exponent, min_size, max_size)
         self.layout, self.ckv, self.kr = layout, ckv_dim, kr_dim
         self.max_tokens, self.max_pins = max_tokens, max_pins
-        # static inputs
-        self.tok = torch.zeros(max_tokens, dtype=torch.int32, device=dev)
-        self.stream_off = torch.zeros(max_requests + 1, dtype=torch.int64, device=dev)
-        self.pin_off = torch.zeros(max_requests + 1, dtype=torch.int64, device=dev)
-        self.pins = torch.zeros(max(max_pins, 1), dtype=torch.int64, device=dev)
-        self.m = torch.zeros(max_requests, dtype=torch.int64, device=dev)
+        # static inputs, two sets: the overlapped pipeline loads wave i + 2 while wave i + 1 reads the other
+        self.inputs = [dict(tok=torch.zeros(max_tokens, dtype=torch.int32, device=dev),
+                            stream_off=torch.zeros(max_requests + 1, dtype=torch.int64, device=dev),
+                            pin_off=torch.zeros(max_requests + 1, dtype=torch.int64, device=dev),
+                            pins=torch.zeros(max(max_pins, 1), dtype=torch.int64, device=dev),
+                            m=torch.zeros(max_requests, dtype=torch.int64, device=dev)) for _ in range(2)]
+        self.cur_in = 0  # the input set K1 / K3 read and load() writes
         # static outputs: per-request KV and the chunk service table
         self.out = torch.empty(pool.shape[0], max_requests * req_stride, pool.shape[2], dtype=pool.dtype,
                                device=dev)
@@ -58,6 +59,12 @@ class ReattachPipeline:
         self.slots = None
         self.graph = None
         self.table = self.hit = self.length = self.delta = None
+
+    tok = property(lambda self: self.inputs[self.cur_in]["tok"])
+    stream_off = property(lambda self: self.inputs[self.cur_in]["stream_off"])
+    pin_off = property(lambda self: self.inputs[self.cur_in]["pin_off"])
+    pins = property(lambda self: self.inputs[self.cur_in]["pins"])
+    m = property(lambda self: self.inputs[self.cur_in]["m"])
 
     # ------------------------------------------------------------ device step
     def k1(self):
@@ -170,26 +177,32 @@ class ReattachPipeline:
         self._side = side
 
         def front(i, s):
-            self.fill_slot = s
+            self.fill_slot, self.cur_in = s, s
             self.k1()
             self.k3_sharded(wave0 + i, False)
-            self.fill_slot = None
+            self.fill_slot, self.cur_in = None, 0
 
+        loader = _Loader(self, load_wave)
         ops.set_rotate_gather_sm_limit(k4_sms)
         try:
-            load_wave(0)
+            loader.load(0, main)
             front(0, 0)
+            loader.read_done(0, main)
             if after_front:
                 after_front(0, 0)
+            if n_waves > 1:
+                loader.load(1, side)
             for i in range(n_waves):
                 s = i & 1
                 if i + 1 < n_waves:
-                    load_wave(i + 1)
                     side.wait_stream(main)
                     with torch.cuda.stream(side):
                         front(i + 1, 1 - s)
+                        loader.read_done(i + 1, side)
                 self.k4(s)
                 main.wait_stream(side)
+                if i + 2 < n_waves:
+                    loader.load(i + 2, side)  # H2D under K4(i + 1); front(i + 2) waits for it
                 if after_front and i + 1 < n_waves:
                     after_front(i + 1, 1 - s)
                 if after_k4:
@@ -246,10 +259,10 @@ class ReattachPipeline:
         side = torch.cuda.Stream()
 
         def front(s):
-            self.fill_slot = s
+            self.fill_slot, self.cur_in = s, s
             self.k1()
             self.k3()
-            self.fill_slot = None
+            self.fill_slot, self.cur_in = None, 0
 
         def overlap(s):
             cur = torch.cuda.current_stream()
@@ -261,9 +274,10 @@ class ReattachPipeline:
 
         # warm up and capture over empty streams: no store side effects (nothing is
         # probed or inserted), and every shape is capacity-bounded anyway
-        saved = (self.stream_off.clone(), self.pin_off.clone())
-        self.stream_off.zero_()
-        self.pin_off.zero_()
+        saved = [(ins["stream_off"].clone(), ins["pin_off"].clone()) for ins in self.inputs]
+        for ins in self.inputs:
+            ins["stream_off"].zero_()
+            ins["pin_off"].zero_()
         s0 = torch.cuda.Stream()
         s0.wait_stream(torch.cuda.current_stream())
         ops.set_rotate_gather_sm_limit(k4_sms)
@@ -293,8 +307,9 @@ class ReattachPipeline:
         finally:
             ops.set_rotate_gather_sm_limit(0)
             torch.cuda.synchronize()
-            self.stream_off.copy_(saved[0])
-            self.pin_off.copy_(saved[1])
+            for ins, (so, po) in zip(self.inputs, saved):
+                ins["stream_off"].copy_(so)
+                ins["pin_off"].copy_(po)
         torch.cuda.synchronize()
         self.hit_tokens.zero_()
 
@@ -307,15 +322,22 @@ class ReattachPipeline:
         ``after_k4(i, slot)`` once wave i's KV is in ``slots[slot]["out"]``."""
         if n_waves <= 0:
             return
-        load_wave(0)
+        main = torch.cuda.current_stream()
+        loader = _Loader(self, load_wave)
+        loader.load(0, main)
         self.g_front[0].replay()
+        loader.read_done(0, main)
         if after_front:
             after_front(0, 0)
+        if n_waves > 1:
+            loader.load(1, main)
         for i in range(n_waves):
             s = i & 1
             if i + 1 < n_waves:
-                load_wave(i + 1)
                 self.g_overlap[s].replay()  # K4(i) || K1 + K3(i + 1) -> slot 1 - s
+                loader.read_done(i + 1, main)
+                if i + 2 < n_waves:
+                    loader.load(i + 2, main)  # H2D under the next graph (other input set)
                 if after_front:
                     after_front(i + 1, 1 - s)
             else:
@@ -324,7 +346,8 @@ class ReattachPipeline:
                 after_k4(i, s)
 
     def load(self, tok, stream_off, pin_off, pins, m):
-        """Copy one wave's inputs (device-resident or pinned host) into the static buffers."""
+        """Copy one wave's inputs (device-resident or pinned host) into the static
+        buffers of the current input set (``cur_in``), on the current stream."""
         n = tok.numel()
         if n > self.max_tokens or pins.numel() > self.max_pins or m.numel() > self.R:
             raise ValueError("wave exceeds the pipeline's static capacity")
@@ -340,3 +363,35 @@ class ReattachPipeline:
 
     def replay(self):
         self.graph.replay()
+
+
+class _Loader:
+    """Input loads of the overlapped pipelines on a copy stream. Wave j lands in
+    input set j % 2 once the front of wave j - 2 (the set's last reader) is done;
+    the stream that runs wave j's front waits for the copy."""
+
+    _stream = None
+
+    def __init__(self, pipe: ReattachPipeline, load_wave):
+        self.pipe, self.load_wave = pipe, load_wave
+        if _Loader._stream is None:
+            _Loader._stream = torch.cuda.Stream()
+        self.copy = _Loader._stream
+        self.read_ev = [None, None]
+
+    def load(self, j: int, consumer: torch.cuda.Stream):
+        s = j & 1
+        if self.read_ev[s] is not None:
+            self.copy.wait_event(self.read_ev[s])
+        else:
+            self.copy.wait_stream(consumer)
+        with torch.cuda.stream(self.copy):
+            self.pipe.cur_in = s
+            self.load_wave(j)
+            self.pipe.cur_in = 0
+        consumer.wait_stream(self.copy)
+
+    def read_done(self, j: int, stream: torch.cuda.Stream):
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.read_ev[j & 1] = ev
