@@ -141,6 +141,11 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # IRM_BENCH_ONE_DEVICE=1 + IRM_BENCH_BACKEND=gloo: every rank on cuda:0, a check of the
+    # N-rank code path on a one-GPU box (NCCL cannot put two ranks on one GPU; timings are not valid)
+    if os.environ.get("IRM_BENCH_ONE_DEVICE") == "1":
+        local = 0
+    backend = os.environ.get("IRM_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1 or args.sharded:
         if world == 1:  # single-rank group for the K6 path at N=1
@@ -148,7 +153,10 @@ def run_ours(args):
             os.environ.setdefault("MASTER_PORT", "29531")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     hbm, tf_burst, tf_sust, peak_kind = peaks()
 
@@ -185,21 +193,26 @@ def run_ours(args):
     from paper_2605_05696_b200.pipeline import ReattachPipeline
 
     store = ops.ChunkStore(max_entries=1 << 16)
+    sharded = world > 1 or args.sharded
     pool_rows = BODY + 2048 * (n_steps + 2)  # body + the novel header/meta chunks of every wave
+    if sharded:
+        # rows [0, novel) hold first-writer KV (split among the G owners), [novel, pool_rows) the replicas
+        n_waves_total = 3 * n_steps + 8
+        novel_rows = 2 * (BODY + 80 * R * n_waves_total)
+        pool_rows = novel_rows + BODY + 80 * R * n_waves_total + 4096
     pool = torch.randn(LAYERS, pool_rows, CKV + KR, device=dev).to(torch.bfloat16)  # random-init latents
     inv = ops.inv_freq_device(np.power(THETA, -2.0 * np.arange(KR // 2) / KR))
     max_tok = max(int(p[1][-1]) for p in packed)
     max_pins = max(int(p[2][-1]) for p in packed)
     pipe = ReattachPipeline(store, pool, inv, R, max_tok, max_pins, req_stride, layout=N.LAYOUT_INTERLEAVED)
 
-    sharded = world > 1 or args.sharded
     if sharded:  # K6: hash-sharded store (fixed-capacity NCCL all-to-all) + peer replica cache
         from paper_2605_05696_b200 import shard
 
-        cache = shard.ReplicaCache(pool, pool_rows // 2, shard.map_peer_pools(pool), rank,
+        cache = shard.ReplicaCache(pool, novel_rows, shard.map_peer_pools(pool), rank,
                                    ops.ChunkStore(max_entries=1 << 16))
-        pipe.enable_sharding(shard.ShardedStore(store), cache, rank, world)
-        step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_sharded(i, allocate_rows=cold))
+        pipe.enable_sharding(shard.ShardedStore(store, novel_rows), cache, rank, world)
+        step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_sharded(i))
     else:
         step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_eager() if cold else pipe.replay())
     # cold request wave: inserts the body (its pool rows hold the random latents)
@@ -316,6 +329,9 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = hit_tok / (e2e_ms / 1e3)
+    if sharded:  # host checks, outside the timed regions: first-writer rows and replicas all fit
+        pipe.sharded.check()
+        pipe.replica.check()
 
     # -------- roofline of the dominant kernel (K4) and K1
     rows_per_launch = k4_rows

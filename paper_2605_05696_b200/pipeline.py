@@ -127,11 +127,8 @@ class ReattachPipeline:
         all-to-alls between the kernels) but never wait for the host: every
         buffer is capacity-bounded, so the CPU runs ahead of the GPU."""
         self.sharded, self.replica, self.rank, self.world = sharded_store, replica_cache, rank, world
-        self.hint_next = torch.zeros((), dtype=torch.int64, device=self.pool.device)
 
-    def k3_sharded(self, wave: int, allocate_rows: bool):
-        from . import shard
-
+    def k3_sharded(self, wave: int):
         t = self.table
         cap = t.start.numel()
         dev = t.start.device
@@ -144,23 +141,17 @@ class ReattachPipeline:
         # global order: (global request = (wave * R + r) * G + rank, chunk index within the request)
         g_req = (wave * self.R + self.reqc) * self.world + self.rank
         order = (g_req << 20) | (idx - t.chunk_off[self.reqc])
-        ln = t.length.to(torch.int64) * probe
-        if allocate_rows:  # this rank keeps the KV of chunks it may be first to write
-            local = self.hint_next + torch.cumsum(ln, 0) - ln
-            self.hint_next += ln.sum()
-        else:
-            local = torch.zeros_like(ln)
-        hint = shard.encode_row(self.rank, local)
-        hit, self.p_src, grow, _own = self.sharded.lookup_insert(t.fp, order, self.p_abs, t.length, probe, hint)
+        hit, self.p_src, grow, _own = self.sharded.lookup_insert(t.fp, order, self.p_abs, t.length, probe)
         self.hit = hit
+        self.grow = grow  # novel chunks: the rows of this rank's pool that keep their KV (prefill writes them)
         is_hit = hit == 1
         self.length = torch.where(is_hit, t.length, torch.zeros_like(t.length))
         src = self.replica.localize(torch.where(is_hit, grow, torch.full_like(grow, -1)), self.length)
         self._compact(is_hit, src, self.reqc * self.req_stride + self.p_abs, self.p_abs - self.p_src)
 
-    def step_sharded(self, wave: int, allocate_rows: bool = False):
+    def step_sharded(self, wave: int):
         self.k1()
-        self.k3_sharded(wave, allocate_rows)
+        self.k3_sharded(wave)
         self.k4()
 
     def run_overlapped_sharded(self, n_waves: int, load_wave, wave0: int = 0, k4_sms: int = 128,
@@ -179,7 +170,7 @@ class ReattachPipeline:
         def front(i, s):
             self.fill_slot, self.cur_in = s, s
             self.k1()
-            self.k3_sharded(wave0 + i, False)
+            self.k3_sharded(wave0 + i)
             self.fill_slot, self.cur_in = None, 0
 
         loader = _Loader(self, load_wave)

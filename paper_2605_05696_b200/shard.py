@@ -7,13 +7,14 @@ exchange over ``torch.distributed`` (NCCL over NVLink on B200, gloo in the CPU
 tests), with fixed-capacity buffers so nothing on the path waits for the host:
 
   1. every probed query goes to slot (owner, position in the owner's bucket)
-     of a [G, cap, 5] send buffer (fp, order key, p, len, row hint); unused
+     of a [G, cap, 4] send buffer (fp, order key, p, len); unused
      slots carry padding order keys that sort after every real key
   2. all-to-all of equal splits
   3. the owner sorts what it received by the global order key (request,
      chunk) and runs the first-writer-wins batch on its shard (K3), so the
      winner is the globally earliest query, exactly as the sequential
-     reference (engine.py:197-223)
+     reference (engine.py:197-223); a new entry's rows are allocated by the
+     owner in its sub-range of the first writer's pool
   4. reverse all-to-all of (hit, p_src, row) into the same slots
 
 Rows are named globally: ``row = rank << 40 | local_row``. A hit whose rows
@@ -53,29 +54,39 @@ class ShardedStore:
     the same ``lookup_insert`` contract and an ``e_row`` entry array, e.g. a
     test dict store on CPU)."""
 
-    def __init__(self, local_store, group=None):
+    def __init__(self, local_store, novel_rows: int, group=None):
+        """novel_rows: rows [0, novel_rows) of every rank's latent pool hold the
+        KV of chunks that rank writes first. Owner o hands out rows of the
+        sub-range [o * novel_rows // G, (o + 1) * novel_rows // G) of each
+        writer's pool, with one bump counter per writer, so a first writer's
+        rows are known in the same exchange that decides it is first."""
         self.local = local_store
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         e_row = local_store.e_row
+        dev = e_row.device
         # global row of every entry of this shard (+1: scatter sink for non-novel queries)
-        self.e_grow = torch.full((e_row.numel() + 1,), -1, dtype=torch.int64, device=e_row.device)
+        self.e_grow = torch.full((e_row.numel() + 1,), -1, dtype=torch.int64, device=dev)
+        self.region = novel_rows // self.world
+        self.base = self.rank * self.region
+        self.next = torch.zeros(self.world, dtype=torch.int64, device=dev)  # per-writer bump counters
+        self.overflow = torch.zeros((), dtype=torch.bool, device=dev)
         self.last_exchange_bytes = 0
 
-    def lookup_insert(self, q_fp, q_order, q_p, q_len, q_probe=None, q_row_hint=None):
+    def lookup_insert(self, q_fp, q_order, q_p, q_len, q_probe=None):
         """Same contract as ops.ChunkStore.lookup_insert, over the sharded store.
 
         q_order must be globally unique and < 2^62 (e.g. (global request << 20) |
-        chunk). q_row_hint: global row (encode_row) where this rank keeps the
-        chunk's KV if it is the first writer. Returns (hit, p_src, row, owner).
+        chunk). Returns (hit, p_src, row, owner); row is the global row
+        (encode_row) of the entry's KV: for a novel query, where this rank must
+        keep the chunk's KV (a row of its own pool, assigned by the owner).
         No host synchronisation: every buffer has a fixed capacity of
         q_fp.numel() slots per owner."""
         dev = q_fp.device
         n, G = q_fp.numel(), self.world
         i64 = dict(dtype=torch.int64, device=dev)
         probe = torch.ones(n, dtype=torch.bool, device=dev) if q_probe is None else q_probe.to(torch.bool)
-        hint = torch.full((n,), -1, **i64) if q_row_hint is None else q_row_hint.to(torch.int64)
         cap = max(n, 1)
         own = torch.where(probe, owner_of(q_fp, G), torch.full_like(q_fp, G))  # bucket G: not probed
         perm = torch.argsort(own, stable=True)
@@ -84,10 +95,9 @@ class ShardedStore:
         start = torch.cumsum(counts, 0) - counts
         valid = own_s < G
         dest = torch.where(valid, own_s * cap + torch.arange(n, **i64) - start[own_s], G * cap)
-        send = torch.zeros(G * cap + 1, 5, **i64)  # last row: sink for unprobed queries
+        send = torch.zeros(G * cap + 1, 4, **i64)  # last row: sink for unprobed queries
         send[:, 1] = PAD_ORDER + self.rank * G * cap + torch.arange(G * cap + 1, **i64)  # unique padding keys
-        send[:, 4] = -1
-        send.index_copy_(0, dest, torch.stack([q_fp, q_order, q_p.to(torch.int64), q_len.to(torch.int64), hint],
+        send.index_copy_(0, dest, torch.stack([q_fp, q_order, q_p.to(torch.int64), q_len.to(torch.int64)],
                                               dim=1)[perm])
         send = send[:G * cap].contiguous()
         recv = torch.empty_like(send)
@@ -101,15 +111,23 @@ class ShardedStore:
             r[:, 0].contiguous(), r[:, 1].contiguous(), r[:, 2].contiguous(), r[:, 3].to(torch.int32).contiguous(),
             real)
         novel = hit == 0
+        # the first writer keeps the new entry's KV: rows of this owner's sub-range of the
+        # writer's pool, bump-allocated per writer in slot (= the writer's query) order
+        nov_slot = torch.zeros(G * cap, dtype=torch.bool, device=dev).index_copy_(0, o, novel)
+        L = torch.where(nov_slot, recv[:, 3], torch.zeros_like(recv[:, 3])).view(G, cap)
+        lrow = self.base + self.next[:, None] + torch.cumsum(L, 1) - L
+        self.next += L.sum(1)
+        self.overflow |= (self.next > self.region).any()
+        grow = ((torch.arange(G, **i64)[:, None] << ROW_SHIFT) | lrow).view(-1)[o]
         sink = self.e_grow.numel() - 1
-        # the new entry's rows are its first writer's (row hint); each entry has one novel query
-        self.e_grow.index_copy_(0, torch.where(novel, entry, torch.full_like(entry, sink)), r[:, 4].contiguous())
+        # each entry has exactly one novel query
+        self.e_grow.index_copy_(0, torch.where(novel, entry, torch.full_like(entry, sink)), grow)
         rows = torch.where(entry >= 0, self.e_grow[entry.clamp_min(0)], torch.full_like(entry, -1))
         reply = torch.empty(G * cap, 3, **i64)
         reply.index_copy_(0, o, torch.stack([hit.to(torch.int64), p_src.to(torch.int64), rows], dim=1))
         back = torch.empty_like(reply)
         dist.all_to_all_single(back, reply, group=self.group)
-        self.last_exchange_bytes = 2 * G * cap * (5 + 3) * 8
+        self.last_exchange_bytes = 2 * G * cap * (4 + 3) * 8
 
         res = back[torch.where(valid, dest, torch.zeros_like(dest))]  # sorted position k -> its slot
         out_hit = torch.full((n,), -1, dtype=torch.int32, device=dev)
@@ -121,6 +139,11 @@ class ShardedStore:
         out_row.index_copy_(0, perm, torch.where(valid, res[:, 2], -1))
         out_owner.index_copy_(0, perm, torch.where(valid, own_s, -1))
         return out_hit, out_psrc, out_row, out_owner
+
+    def check(self):
+        """Host check (call outside timed regions): every first writer got its rows."""
+        if bool(self.overflow):
+            raise RuntimeError("first-writer row range of the pool is full: raise novel_rows")
 
 
 def map_peer_pools(pool: torch.Tensor, group=None) -> list[torch.Tensor]:

@@ -209,11 +209,11 @@ def test_pipeline_sharded_single_rank(setup):
     try:
         pipe = new_pipe(S)
         peers = shard.map_peer_pools(S["pool"])
-        pipe.enable_sharding(shard.ShardedStore(pipe.store), shard.ReplicaCache(
+        pipe.enable_sharding(shard.ShardedStore(pipe.store, S["pool"].shape[1] - 32), shard.ReplicaCache(
             S["pool"], S["pool"].shape[1] - 32, peers, 0, ops.ChunkStore(1 << 10)), 0, 1)
         dev = [to_dev(w) for w in S["waves"]]
         pipe.load(*dev[0])
-        pipe.step_sharded(0, allocate_rows=True)  # cold wave: hints give the oracle's rows
+        pipe.step_sharded(0)  # cold wave (world 1: owner-allocated rows are the oracle's rows)
         torch.cuda.synchronize()
         hits, outs = {}, {}
         pipe.run_overlapped_sharded(WAVES, lambda i: pipe.load(*dev[1 + i]), wave0=1, k4_sms=100,
@@ -223,5 +223,6 @@ def test_pipeline_sharded_single_rank(setup):
         for i in range(WAVES):
             check_wave(S, 1 + i, hits[i].cpu().numpy(), outs[i].cpu())
         pipe.replica.check()
+        pipe.sharded.check()
     finally:
         dist.destroy_process_group()

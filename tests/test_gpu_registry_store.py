@@ -179,16 +179,13 @@ def test_sharded_store_single_rank_nccl(M):
         p = rng.integers(0, 9999, size=400).astype(np.int64)
         ln = rng.integers(1, 100, size=400).astype(np.int32)
         plain = ops.ChunkStore(1024)
-        hit_a, _, ps_a, _ = plain.lookup_insert(d(fps), d(order), d(p), d(ln))
-        sh = shard.ShardedStore(ops.ChunkStore(1024))
-        hint = shard.encode_row(0, torch.arange(400, device="cuda") * 10)
-        hit_b, ps_b, row_b, own = sh.lookup_insert(d(fps), d(order), d(p), d(ln), None, hint)
+        hit_a, _, ps_a, row_a = plain.lookup_insert(d(fps), d(order), d(p), d(ln))
+        sh = shard.ShardedStore(ops.ChunkStore(1024), novel_rows=1 << 20)
+        hit_b, ps_b, row_b, own = sh.lookup_insert(d(fps), d(order), d(p), d(ln))
         assert torch.equal(hit_a.cpu(), hit_b.cpu()) and torch.equal(ps_a.cpu(), ps_b.cpu())
         assert (own == 0).all()
-        first = {}
-        for i, (f, h, r) in enumerate(zip(fps.tolist(), hit_b.cpu().tolist(), row_b.cpu().tolist())):
-            if h == 0:
-                first[f] = int(hint[i])
-            assert r == first[f]
+        # world 1: the owner's per-writer bump allocator is the plain store's row scan
+        assert torch.equal(row_a.cpu(), row_b.cpu())
+        sh.check()
     finally:
         dist.destroy_process_group()

@@ -14,6 +14,7 @@ import torch.multiprocessing as mp
 from paper_2605_05696_b200 import shard
 
 WORLD = 2
+NOVEL_ROWS = 1 << 30
 
 
 def _free_port():
@@ -46,14 +47,13 @@ def _worker(rank, port, seed, out_q, pools):
     try:
         fp, order, p, ln, probe, rank_of = _queries(seed)
         mine = torch.nonzero(rank_of == rank).flatten()
-        store = shard.ShardedStore(DictStore())
-        hint = shard.encode_row(rank, torch.arange(mine.numel(), dtype=torch.int64) * 1000)
+        store = shard.ShardedStore(DictStore(), novel_rows=NOVEL_ROWS)
         res = []
         for wave in range(3):  # three waves hitting the same sharded store
             sl = mine[wave::3]
-            h, ps, row, own = store.lookup_insert(fp[sl], order[sl] + wave * 10**7, p[sl], ln[sl], probe[sl],
-                                                  hint[wave::3])
+            h, ps, row, own = store.lookup_insert(fp[sl], order[sl] + wave * 10**7, p[sl], ln[sl], probe[sl])
             res.append((sl, h, ps, row, own))
+        store.check()
 
         # replica cache: pool rows hold (rank, row) stamps; the shared-memory pools of
         # both ranks stand in for the CUDA-IPC peer mappings of shard.map_peer_pools
@@ -72,7 +72,7 @@ def _worker(rank, port, seed, out_q, pools):
         cache.check()
         # plain lists: tensors would travel as shared-memory handles that vanish with this process
         res = [tuple(x.tolist() for x in r) for r in res]
-        out_q.put((rank, res, hint.tolist(), ok))
+        out_q.put((rank, res, ok))
     finally:
         dist.destroy_process_group()
 
@@ -100,16 +100,16 @@ def test_sharded_store_matches_sequential(seed):
     fp, order, p, ln, probe, rank_of = _queries(seed)
     # sequential reference over the union, in global order (waves are time-ordered)
     rows = []
-    for rank, res, hint, ok in outs:
+    for rank, res, ok in outs:
         assert ok, f"replica cache check failed on rank {rank}"
         for wave, (sl, h, ps, row, own) in enumerate(res):
             for k, i in enumerate(sl):
-                rows.append((int(order[i]) + wave * 10**7, i, rank, int(h[k]), int(ps[k]), int(row[k]),
-                             int(hint[wave::3][k]), int(own[k])))
+                rows.append((int(order[i]) + wave * 10**7, i, rank, wave, k, int(h[k]), int(ps[k]), int(row[k]),
+                             int(own[k])))
     rows.sort()
     ref = DictStore()
-    first_hint: dict[int, int] = {}
-    for ordk, i, rank, h, ps, row, hnt, own in rows:
+    first: dict[int, tuple] = {}  # fp -> (writer rank, wave, position in the writer's wave)
+    for ordk, i, rank, wave, k, h, ps, row, own in rows:
         if not probe[i]:
             assert h == -1
             continue
@@ -117,6 +117,20 @@ def test_sharded_store_matches_sequential(seed):
         eh, _, eps, _ = ref.lookup_insert(fp[i:i + 1], torch.tensor([ordk]), p[i:i + 1], ln[i:i + 1])
         assert h == int(eh[0]) and ps == int(eps[0]), (i, h, int(eh[0]))
         if h == 0:
-            first_hint[f] = hnt
-        assert row == first_hint[f]  # every hit reads the first writer's rows
+            first[f] = (rank, wave, k)
         assert own == int(shard.owner_of(fp[i:i + 1], WORLD)[0])
+    # first-writer rows: owner o bump-allocates in [o * region, (o + 1) * region) of the writer's
+    # pool, per writer, in the writer's (wave, query) order
+    region = NOVEL_ROWS // WORLD
+    nxt = {}
+    grow = {}
+    for rank, res, ok in sorted(outs):
+        for wave, (sl, h, ps, row, own) in enumerate(res):
+            for k, i in enumerate(sl):
+                if h[k] == 0:
+                    o = own[k]
+                    grow[(rank, wave, k)] = (rank << shard.ROW_SHIFT) | (o * region + nxt.get((o, rank), 0))
+                    nxt[(o, rank)] = nxt.get((o, rank), 0) + int(ln[i])
+    for ordk, i, rank, wave, k, h, ps, row, own in rows:
+        if probe[i]:
+            assert row == grow[first[int(fp[i])]], (i, row)  # every query reads its first writer's rows
