@@ -226,9 +226,13 @@ def run_ours(args):
     if overlapped and not sharded:  # two-wave pipeline graphs (K4 on 128 SMs || K1 + K3 of the next wave)
         pipe.capture_overlapped(k4_sms=K4_SMS)
         pipe.run_overlapped(args.warmup, lambda i: pipe.load(*dev_in[i]))
-    if overlapped and sharded:  # the same pipeline on streams (NCCL all-to-all inside the front)
-        pipe.run_overlapped_sharded(args.warmup, lambda i: pipe.load(*dev_in[i]), wave0=n_steps + 2,
-                                    k4_sms=K4_SMS)
+    # sharded: the same two-wave graphs with the NCCL all-to-alls captured inside the front
+    # (eager streams when the backend cannot be captured, e.g. the gloo one-device check)
+    graphs = not sharded or backend == "nccl"
+    if overlapped and sharded and graphs:
+        pipe.capture_overlapped(k4_sms=K4_SMS, sharded=True)
+    if overlapped and sharded:
+        run_sharded(pipe, args.warmup, lambda i: pipe.load(*dev_in[i]), n_steps + 2, graphs)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -244,8 +248,8 @@ def run_ours(args):
             pipe.hit_tokens.zero_()
             t0.record()
             if sharded:
-                pipe.run_overlapped_sharded(args.steps, lambda i: pipe.load(*dev_in[args.warmup + i]),
-                                            wave0=2 * n_steps + 4, k4_sms=K4_SMS)
+                run_sharded(pipe, args.steps, lambda i: pipe.load(*dev_in[args.warmup + i]), 2 * n_steps + 4,
+                            graphs)
             else:
                 pipe.run_overlapped(args.steps, lambda i: pipe.load(*dev_in[args.warmup + i]))
             t1.record()
@@ -310,8 +314,8 @@ def run_ours(args):
             res[i].copy_(pipe.slots[slot]["hit"], non_blocking=True)
 
         if sharded:
-            pipe.run_overlapped_sharded(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]),
-                                        wave0=3 * n_steps + 6, k4_sms=K4_SMS, after_front=d2h)
+            run_sharded(pipe, args.steps, lambda i: pipe.load(*host_in[args.warmup + i]), 3 * n_steps + 6,
+                        graphs, after_front=d2h)
         else:
             pipe.run_overlapped(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]), after_front=d2h)
         bo = pipe.slots[0]["hit"].numel() * pipe.slots[0]["hit"].element_size()
@@ -349,7 +353,9 @@ def run_ours(args):
                    "requests_per_step": R, "tokens_per_request": tok_per_wave // R + HEADER,
                    "layers": LAYERS, "l2": "inputs larger than L2 (1.0 GB pool, 8 GB KV out per step)",
                    "pipeline": ("two-wave overlap: K4 of wave i on %d SMs || K1 + K3 of wave i+1" % K4_SMS
-                                + (" (streams; sharded lookup + peer replica fetch)" if sharded else " (CUDA graphs)"))
+                                + (" (CUDA graphs; sharded lookup: NCCL all-to-alls captured in the graph, peer replica fetch)"
+                                   if sharded and graphs else
+                                   " (streams; sharded lookup + peer replica fetch)" if sharded else " (CUDA graphs)"))
                                if overlapped else "serial K1 -> K3 -> K4 per wave",
                    "parallelism": f"sessions s mod G over {world} GPU(s)" + (", store sharded by fp prefix, NCCL all-to-all lookup" if sharded else "")},
         "roofline": {"bound": "hbm", "kernel": "irm_rotate_gather (K4)", "achieved": k4_gbs,
@@ -372,6 +378,13 @@ def run_ours(args):
         print(json.dumps(line))
     if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def run_sharded(pipe, n, load, wave0, graphs, after_front=None):
+    if graphs:
+        pipe.run_overlapped(n, load, after_front=after_front, wave0=wave0)
+    else:
+        pipe.run_overlapped_sharded(n, load, wave0=wave0, k4_sms=K4_SMS, after_front=after_front)
 
 
 # ----------------------------------------------------------------- K5 component

@@ -138,7 +138,8 @@ class ReattachPipeline:
         self.reqc = torch.clamp(req, max=self.R - 1)
         self.p_abs = self.m[self.reqc] + t.start.to(torch.int64)
         probe = valid & (self.p_abs >= self.carve)
-        # global order: (global request = (wave * R + r) * G + rank, chunk index within the request)
+        # global order: (global request = (wave * R + r) * G + rank, chunk index within the request);
+        # wave: an int, or a device scalar (graph-captured fronts advance it on the device)
         g_req = (wave * self.R + self.reqc) * self.world + self.rank
         order = (g_req << 20) | (idx - t.chunk_off[self.reqc])
         hit, self.p_src, grow, _own = self.sharded.lookup_insert(t.fp, order, self.p_abs, t.length, probe)
@@ -240,19 +241,31 @@ class ReattachPipeline:
                 out=self.out if s == 0 else torch.empty_like(self.out)))
         self.hit_tokens = torch.zeros((), **i64)
 
-    def capture_overlapped(self, k4_sms: int = 128, warmup: int = 2):
+    def capture_overlapped(self, k4_sms: int = 128, warmup: int = 2, sharded: bool = False):
         """Capture the two-wave pipeline: ``front[s]`` = K1 + K3 of a wave into
         slot s; ``overlap[s]`` = K4 of slot s on ``k4_sms`` SMs, concurrently with
         front[1 - s] on a forked stream; ``drain[s]`` = K4 of slot s alone.
         Per-slot outputs: ``slots[s]["out"]`` (KV), ``["hit"]`` (service map);
-        ``hit_tokens`` accumulates reattached tokens on the device."""
+        ``hit_tokens`` accumulates reattached tokens on the device.
+
+        ``sharded``: the front is K1 + the sharded lookup (NCCL all-to-alls
+        captured into the graph) + the replica fetch, as in
+        ``run_overlapped_sharded``; the wave number of the global order key is a
+        device scalar (``wave_t``) each front advances. Every rank captures the
+        same sequence of collectives, so replays stay matched across ranks."""
         self._alloc_slots()
         side = torch.cuda.Stream()
+        if sharded:
+            self.wave_t = torch.zeros((), dtype=torch.int64, device=self.pool.device)
 
         def front(s):
             self.fill_slot, self.cur_in = s, s
             self.k1()
-            self.k3()
+            if sharded:
+                self.k3_sharded(self.wave_t)
+                self.wave_t += 1
+            else:
+                self.k3()
             self.fill_slot, self.cur_in = None, 0
 
         def overlap(s):
@@ -304,16 +317,19 @@ class ReattachPipeline:
         torch.cuda.synchronize()
         self.hit_tokens.zero_()
 
-    def run_overlapped(self, n_waves: int, load_wave, after_front=None, after_k4=None):
+    def run_overlapped(self, n_waves: int, load_wave, after_front=None, after_k4=None, wave0: int = 0):
         """Process waves 0..n_waves-1 through the two-wave pipeline.
         ``load_wave(i)`` copies wave i's inputs into the static buffers (called on
         the current stream, after the previous graph that read them);
         ``after_front(i, slot)`` is called once wave i's lookup results are in
         ``slots[slot]`` (stream-ordered), e.g. to read the service map back;
-        ``after_k4(i, slot)`` once wave i's KV is in ``slots[slot]["out"]``."""
+        ``after_k4(i, slot)`` once wave i's KV is in ``slots[slot]["out"]``.
+        Sharded graphs number the waves ``wave0 + i`` in the global order key."""
         if n_waves <= 0:
             return
         main = torch.cuda.current_stream()
+        if getattr(self, "wave_t", None) is not None:
+            self.wave_t.fill_(wave0)
         loader = _Loader(self, load_wave)
         loader.load(0, main)
         self.g_front[0].replay()

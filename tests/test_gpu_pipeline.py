@@ -191,9 +191,11 @@ def test_replica_fetch_peer_pools():
     cache.check()
 
 
-def test_pipeline_sharded_single_rank(setup):
+@pytest.mark.parametrize("graphs", [False, True])
+def test_pipeline_sharded_single_rank(setup, graphs):
     """The sharded step (NCCL all-to-all lookup, world 1) in the overlapped
-    stream pipeline reproduces the oracle like the unsharded graph path."""
+    pipeline reproduces the oracle like the unsharded graph path: on streams,
+    and as captured graphs with the all-to-alls inside."""
     import os
 
     import torch.distributed as dist
@@ -216,9 +218,14 @@ def test_pipeline_sharded_single_rank(setup):
         pipe.step_sharded(0)  # cold wave (world 1: owner-allocated rows are the oracle's rows)
         torch.cuda.synchronize()
         hits, outs = {}, {}
-        pipe.run_overlapped_sharded(WAVES, lambda i: pipe.load(*dev[1 + i]), wave0=1, k4_sms=100,
-                                    after_front=lambda i, s: hits.__setitem__(i, pipe.slots[s]["hit"].clone()),
-                                    after_k4=lambda i, s: outs.__setitem__(i, pipe.slots[s]["out"].clone()))
+        af = lambda i, s: hits.__setitem__(i, pipe.slots[s]["hit"].clone())
+        ak = lambda i, s: outs.__setitem__(i, pipe.slots[s]["out"].clone())
+        if graphs:
+            pipe.capture_overlapped(k4_sms=100, sharded=True)
+            pipe.run_overlapped(WAVES, lambda i: pipe.load(*dev[1 + i]), after_front=af, after_k4=ak, wave0=1)
+        else:
+            pipe.run_overlapped_sharded(WAVES, lambda i: pipe.load(*dev[1 + i]), wave0=1, k4_sms=100,
+                                        after_front=af, after_k4=ak)
         torch.cuda.synchronize()
         for i in range(WAVES):
             check_wave(S, 1 + i, hits[i].cpu().numpy(), outs[i].cpu())
