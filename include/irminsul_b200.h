@@ -86,6 +86,37 @@ int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_o
 int irm_xxh64_spans(const uint8_t *base, const int64_t *off, const int64_t *len, int64_t n,
                     uint64_t seed, uint64_t *out, irm_stream_t stream);
 
+/* ---- K0: exact-prefix index (radix.py:31-89; engine.py:170, 228) -------
+ * Every prefix of every inserted sequence is a key of an open-addressing
+ * table holding the smallest insert epoch that reaches it (the radix tree's
+ * earliest-inserted witness). Caller-owned; initialise with irm_prefix_reset(). */
+typedef struct {
+    uint64_t *slot_key;   /* [n_slots] prefix key or IRM_EMPTY_KEY               */
+    int64_t *slot_epoch;  /* [n_slots] smallest insert epoch with this prefix    */
+    int64_t n_slots;      /* power of two, >= 2 x the distinct prefixes stored  */
+    int64_t *counters;    /* [2]: slots used, error flags (1 table full, 2 a
+                           match failed token verification; sticky)            */
+} irm_prefix_view;
+
+int irm_prefix_reset(const irm_prefix_view *ix, irm_stream_t stream);
+int64_t irm_prefix_workspace_bytes(int64_t n_tokens, int32_t n_seq);
+/* A batch of n_seq operations, in order, on sequences tok[seq_off[i],
+ * seq_off[i+1]) (seq_off relative to tok; n_tokens = seq_off[n_seq]).
+ *   op_insert[i] != 0: insert sequence i with epoch op_epoch[i]
+ *     (RadixTree.insert, radix.py:31-58);
+ *   op_query[i] != 0 (nullptr: all): m[i] = the longest prefix of sequence i
+ *     shared with a sequence inserted with an epoch < op_epoch[i] (before the
+ *     batch or earlier in it), wit[i] = the smallest such epoch reaching depth
+ *     m[i]; m = 0, wit = -1 when nothing matches (match_prefix, radix.py:60-83).
+ * Every answer is checked token by token against the witness's tokens at
+ * arena + wit_off[wit] (wit_len[wit] tokens; the caller keeps each inserted
+ * sequence there, including this batch's); a mismatch sets error flag 2. */
+int irm_prefix_match_insert(const irm_prefix_view *ix, const uint32_t *tok, const int64_t *seq_off,
+                            int32_t n_seq, int64_t n_tokens, const int64_t *op_epoch,
+                            const uint8_t *op_insert, const uint8_t *op_query, const uint32_t *arena,
+                            const int64_t *wit_off, const int64_t *wit_len, int64_t *m, int64_t *wit,
+                            void *ws, int64_t ws_bytes, irm_stream_t stream);
+
 /* ---- K3: content-hash chunk store (registry.py:113-140) ----------------
  * Open-addressing table fingerprint -> entry, plus entry arrays, all caller
  * owned. Initialise with irm_store_reset(). First writer wins by the

@@ -253,3 +253,21 @@ def rotate_gather_bf16(pool_u16: np.ndarray, out_u16: np.ndarray, src_row, dst_r
 
 def max_threads() -> int:
     return int(lib().oracle_max_threads())
+
+
+# ----------------------------------------------------------------- K0: exact-prefix match
+def prefix_match(inserted, seq):
+    """Longest common prefix of ``seq`` with any inserted sequence and the
+    earliest-inserted witness reaching it: the brute force the reference pins
+    RadixTree with (tests/test_radix.py:15-23, :75-90; radix.py:60-83).
+    ``inserted``: list of (handle, tokens) in insert order."""
+    q = np.asarray(seq, dtype=np.uint32)
+    best, who = 0, None
+    for handle, stored in inserted:
+        s = np.asarray(stored, dtype=np.uint32)
+        n = min(s.size, q.size)
+        neq = np.nonzero(s[:n] != q[:n])[0]
+        m = int(neq[0]) if neq.size else n
+        if m > best:
+            best, who = m, handle
+    return best, who

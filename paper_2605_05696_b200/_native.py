@@ -36,6 +36,12 @@ class StoreView(ctypes.Structure):
     ]
 
 
+class PrefixView(ctypes.Structure):
+    """irm_prefix_view (include/irminsul_b200.h)."""
+
+    _fields_ = [("slot_key", P), ("slot_epoch", P), ("n_slots", i64), ("counters", P)]
+
+
 _SIGS = {
     "irm_abi_version": ([], i32),
     "irm_last_error": ([], ctypes.c_char_p),
@@ -56,6 +62,9 @@ _SIGS = {
     "irm_rotate_rows": ([P, i64, P, i64, i64, i32, P, P, i32, i32, i32, P], i32),
     "irm_round_f64": ([P, P, i64, i32, P], i32),
     "irm_chunk_cossin": ([P, i64, P, P, P], i32),
+    "irm_prefix_reset": ([ctypes.POINTER(PrefixView), P], i32),
+    "irm_prefix_workspace_bytes": ([i64, i32], i64),
+    "irm_prefix_match_insert": ([ctypes.POINTER(PrefixView), P, P, i32, i64, P, P, P, P, P, P, P, P, P, i64, P], i32),
     "irm_mla_reattach_prefill": ([P, i64, i32, i64, P, i64, P, i32, P, P, i32, f32, P, P, P], i32),
 }
 

@@ -1,0 +1,343 @@
+// K0: batched exact-prefix index on the device (phase 1 of the serve path).
+//
+// Replaces RadixTree.insert / match_prefix (reference radix.py:31-89, called
+// by engine.serve at engine.py:170 and :228) for a batch of operations. The
+// reference walks a compressed radix tree per request; here every prefix of
+// every inserted sequence is one key of an open-addressing table:
+//
+//   key(s, d) = fmix64(H(s[0:d]) + d * phi),  H = polynomial hash mod 2^61 - 1
+//   slot value = the smallest insert epoch whose sequence has that prefix
+//
+// "some sequence inserted before epoch e shares the first d tokens of q" is
+// then one lookup (slot epoch < e), and it is monotone in d (a sequence that
+// shares d tokens shares every shorter prefix), so the longest match is a
+// binary search over d. The earliest-inserted witness at that depth is the
+// slot's epoch (radix.py:85-89 keeps the earliest handle on every node).
+// All prefix hashes of a batch come from one segmented scan of affine maps
+// x -> B x + (t + 1) (mod 2^61 - 1), so the work is O(tokens) and parallel.
+//
+// Exactness: a hash collision could only make a prefix look present. The
+// final answer of every query is verified token by token against the
+// witness's stored tokens; a mismatch raises error flag 2 (loud, never a
+// silent wrong answer). Deeper-prefix false negatives cannot happen.
+#include "common.cuh"
+
+namespace irm {
+namespace prefix {
+
+constexpr uint64_t P61 = (1ULL << 61) - 1;
+constexpr uint64_t BASE = 0x0F3D5B79A2C4E68DULL % P61;  // fixed odd base < p
+constexpr int CH = 1024;       // tokens per chunk (one CTA)
+constexpr int PT = 256;        // threads per CTA
+constexpr int TPT = CH / PT;   // tokens per thread
+enum : int64_t { ERR_TABLE_FULL = 1, ERR_VERIFY = 2 };
+
+struct Aff {  // x -> a x + b (mod p)
+    uint64_t a, b;
+};
+
+__device__ __forceinline__ uint64_t mulmod(uint64_t x, uint64_t y) {
+    const uint64_t lo = x * y, hi = __umul64hi(x, y);
+    uint64_t r = (lo & P61) + ((lo >> 61) | (hi << 3));
+    r = (r & P61) + (r >> 61);
+    return r >= P61 ? r - P61 : r;
+}
+__device__ __forceinline__ uint64_t addmod(uint64_t x, uint64_t y) {
+    const uint64_t r = x + y;
+    return r >= P61 ? r - P61 : r;
+}
+// f then g
+__device__ __forceinline__ Aff compose(Aff f, Aff g) { return {mulmod(f.a, g.a), addmod(mulmod(g.a, f.b), g.b)}; }
+__device__ __forceinline__ Aff tok_aff(uint32_t t) { return {BASE, (uint64_t)t + 1}; }
+
+__device__ __forceinline__ uint64_t fmix64(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xFF51AFD7ED558CCDULL;
+    k ^= k >> 33;
+    k *= 0xC4CEB9FE1A85EC53ULL;
+    k ^= k >> 33;
+    return k;
+}
+__device__ __forceinline__ uint64_t prefix_key(uint64_t h, int64_t d) {
+    const uint64_t k = fmix64(h + (uint64_t)d * 0x9E3779B97F4A7C15ULL);
+    return k == IRM_EMPTY_KEY ? k - 1 : k;
+}
+
+__device__ __forceinline__ int64_t find(const irm_prefix_view &ix, uint64_t key) {
+    const uint64_t m = (uint64_t)ix.n_slots - 1;
+    uint64_t idx = (key >> 20) & m;
+    for (int64_t probe = 0; probe < ix.n_slots; ++probe, idx = (idx + 1) & m) {
+        const uint64_t k = ((volatile uint64_t *)ix.slot_key)[idx];
+        if (k == key) return (int64_t)idx;
+        if (k == IRM_EMPTY_KEY) return -1;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ void insert(const irm_prefix_view &ix, uint64_t key, int64_t epoch) {
+    const uint64_t m = (uint64_t)ix.n_slots - 1;
+    uint64_t idx = (key >> 20) & m;
+    for (int64_t probe = 0; probe < ix.n_slots; ++probe, idx = (idx + 1) & m) {
+        uint64_t k = ((volatile uint64_t *)ix.slot_key)[idx];
+        if (k == IRM_EMPTY_KEY) {
+            k = atomicCAS((unsigned long long *)&ix.slot_key[idx], (unsigned long long)IRM_EMPTY_KEY,
+                          (unsigned long long)key);
+            if (k == IRM_EMPTY_KEY) {
+                atomicAdd((unsigned long long *)&ix.counters[0], 1ULL);
+                k = key;
+            }
+        }
+        if (k == key) {
+            atomicMin((long long *)&ix.slot_epoch[idx], (long long)epoch);
+            return;
+        }
+    }
+    atomicOr((unsigned long long *)&ix.counters[1], (unsigned long long)ERR_TABLE_FULL);
+}
+
+__global__ void reset_kernel(irm_prefix_view ix) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < ix.n_slots) {
+        ix.slot_key[i] = IRM_EMPTY_KEY;
+        ix.slot_epoch[i] = INT64_MAX;
+    }
+    if (i < 2) ix.counters[i] = 0;
+}
+
+// chunk_off[i] = exclusive scan of ceil(len_i / CH) (one CTA, tiles of PT sequences)
+__global__ void __launch_bounds__(PT) chunk_plan_kernel(const int64_t *__restrict__ seq_off, int32_t n_seq,
+                                                         int64_t *__restrict__ chunk_off) {
+    __shared__ int64_t carry, sm[PT / 32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n_seq; base += PT) {
+        const int i = base + threadIdx.x;
+        const int64_t c = i < n_seq ? (seq_off[i + 1] - seq_off[i] + CH - 1) / CH : 0;
+        int64_t total;
+        const int64_t ex = block_exclusive_scan<PT>(c, &total, sm);
+        if (i < n_seq) chunk_off[i] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) chunk_off[n_seq] = carry;
+}
+
+// which (sequence, chunk) this CTA owns; false past the last chunk
+__device__ __forceinline__ bool locate(const int64_t *chunk_off, int32_t n_seq, int64_t c, int &seq, int64_t &j) {
+    if (c >= chunk_off[n_seq]) return false;
+    int lo = 0, hi = n_seq - 1;  // last seq with chunk_off[seq] <= c
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (chunk_off[mid] <= c) lo = mid;
+        else hi = mid - 1;
+    }
+    seq = lo;
+    j = c - chunk_off[lo];
+    return true;
+}
+
+// block-wide exclusive scan of per-thread affine maps; returns this thread's exclusive
+// prefix and writes the block aggregate
+__device__ __forceinline__ Aff block_scan_aff(Aff v, Aff *agg) {
+    __shared__ Aff warp_tot[PT / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    Aff inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        Aff o;
+        o.a = __shfl_up_sync(0xffffffffu, inc.a, off);
+        o.b = __shfl_up_sync(0xffffffffu, inc.b, off);
+        if (lane >= off) inc = compose(o, inc);
+    }
+    if (lane == 31) warp_tot[w] = inc;
+    __syncthreads();
+    Aff wpre = {1, 0};
+    for (int k = 0; k < w; ++k) wpre = compose(wpre, warp_tot[k]);
+    Aff tot = {1, 0};
+    for (int k = 0; k < PT / 32; ++k) tot = compose(tot, warp_tot[k]);
+    Aff ex;
+    ex.a = __shfl_up_sync(0xffffffffu, inc.a, 1);
+    ex.b = __shfl_up_sync(0xffffffffu, inc.b, 1);
+    if (lane == 0) ex = {1, 0};
+    *agg = tot;
+    __syncthreads();
+    return compose(wpre, ex);
+}
+
+__device__ __forceinline__ Aff thread_aff(const uint32_t *tok, int64_t s0, int64_t len, int64_t j, uint32_t t[TPT]) {
+    Aff a = {1, 0};
+    const int64_t d0 = j * CH + (int64_t)threadIdx.x * TPT;
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+        const int64_t d = d0 + q;
+        t[q] = d < len ? tok[s0 + d] : 0;
+        if (d < len) a = compose(a, tok_aff(t[q]));
+    }
+    return a;
+}
+
+__global__ void __launch_bounds__(PT) aggregate_kernel(const uint32_t *__restrict__ tok,
+                                                        const int64_t *__restrict__ seq_off, int32_t n_seq,
+                                                        const int64_t *__restrict__ chunk_off, Aff *__restrict__ agg) {
+    int seq;
+    int64_t j;
+    if (!locate(chunk_off, n_seq, blockIdx.x, seq, j)) return;
+    const int64_t s0 = seq_off[seq], len = seq_off[seq + 1] - s0;
+    uint32_t t[TPT];
+    Aff a = thread_aff(tok, s0, len, j, t), tot;
+    block_scan_aff(a, &tot);
+    if (threadIdx.x == 0) agg[blockIdx.x] = tot;
+}
+
+// per sequence: exclusive prefix of its chunk aggregates (sequential; ~len/1024 steps)
+__global__ void carry_kernel(const int64_t *__restrict__ chunk_off, int32_t n_seq, const Aff *__restrict__ agg,
+                             Aff *__restrict__ carry) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_seq) return;
+    Aff c = {1, 0};
+    for (int64_t k = chunk_off[i]; k < chunk_off[i + 1]; ++k) {
+        carry[k] = c;
+        c = compose(c, agg[k]);
+    }
+}
+
+// keys of every depth (key[seq_off[s] + d - 1] = key of prefix length d), inserted
+// with the sequence's epoch when op_insert
+__global__ void __launch_bounds__(PT) keys_kernel(irm_prefix_view ix, const uint32_t *__restrict__ tok,
+                                                   const int64_t *__restrict__ seq_off, int32_t n_seq,
+                                                   const int64_t *__restrict__ chunk_off, const Aff *__restrict__ carry,
+                                                   const int64_t *__restrict__ op_epoch,
+                                                   const uint8_t *__restrict__ op_insert, uint64_t *__restrict__ key) {
+    int seq;
+    int64_t j;
+    if (!locate(chunk_off, n_seq, blockIdx.x, seq, j)) return;
+    const int64_t s0 = seq_off[seq], len = seq_off[seq + 1] - s0;
+    uint32_t t[TPT];
+    Aff a = thread_aff(tok, s0, len, j, t), tot;
+    Aff h = compose(carry[blockIdx.x], block_scan_aff(a, &tot));  // maps H(empty) = 0 to H before my tokens
+    const bool ins = op_insert && op_insert[seq];
+    const int64_t ep = op_epoch[seq];
+    const int64_t d0 = j * CH + (int64_t)threadIdx.x * TPT;
+    uint64_t H = h.b;  // hash of the prefix before my first token (applied to x = 0)
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+        const int64_t d = d0 + q;
+        if (d >= len) break;
+        H = addmod(mulmod(H, BASE), (uint64_t)t[q] + 1);
+        const uint64_t k = prefix_key(H, d + 1);
+        key[s0 + d] = k;
+        if (ins) insert(ix, k, ep);
+    }
+}
+
+__global__ void query_kernel(irm_prefix_view ix, const int64_t *__restrict__ seq_off, int32_t n_seq,
+                             const int64_t *__restrict__ op_epoch, const uint8_t *__restrict__ op_query,
+                             const uint64_t *__restrict__ key, int64_t *__restrict__ m_out,
+                             int64_t *__restrict__ wit_out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_seq) return;
+    if (op_query && !op_query[i]) {
+        m_out[i] = 0;
+        wit_out[i] = -1;
+        return;
+    }
+    const int64_t s0 = seq_off[i], len = seq_off[i + 1] - s0, e = op_epoch[i];
+    int64_t lo = 0, hi = len, wit = -1;
+    while (lo < hi) {  // largest d with a prefix of length d inserted before epoch e
+        const int64_t mid = (lo + hi + 1) >> 1;
+        const int64_t s = find(ix, key[s0 + mid - 1]);
+        const int64_t ep = s >= 0 ? ((volatile int64_t *)ix.slot_epoch)[s] : INT64_MAX;
+        if (ep < e) {
+            lo = mid;
+            wit = ep;
+        } else {
+            hi = mid - 1;
+        }
+    }
+    m_out[i] = lo;
+    wit_out[i] = lo > 0 ? wit : -1;
+}
+
+// token-by-token check of every answer against the witness's stored tokens
+__global__ void verify_kernel(irm_prefix_view ix, const uint32_t *__restrict__ tok, const int64_t *__restrict__ seq_off,
+                              int32_t n_seq, const uint32_t *__restrict__ arena, const int64_t *__restrict__ wit_off,
+                              const int64_t *__restrict__ wit_len, const int64_t *__restrict__ m,
+                              const int64_t *__restrict__ wit) {
+    const int i = blockIdx.x;
+    if (i >= n_seq) return;
+    const int64_t mi = m[i];
+    if (mi <= 0) return;
+    const int64_t w = wit[i];
+    const int64_t s0 = seq_off[i];
+    bool bad = w < 0 || wit_len[w] < mi;
+    if (!bad) {
+        const uint32_t *a = tok + s0, *b = arena + wit_off[w];
+        for (int64_t d = threadIdx.x; d < mi; d += blockDim.x) bad |= a[d] != b[d];
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0)
+        atomicOr((unsigned long long *)&ix.counters[1], (unsigned long long)ERR_VERIFY);
+}
+
+}  // namespace prefix
+}  // namespace irm
+
+using namespace irm;
+using prefix::Aff;
+
+extern "C" int irm_prefix_reset(const irm_prefix_view *ix, irm_stream_t stream) {
+    IRM_REQUIRE(ix && ix->slot_key && ix->slot_epoch && ix->counters, "null pointer");
+    IRM_REQUIRE(ix->n_slots >= 2 && (ix->n_slots & (ix->n_slots - 1)) == 0, "n_slots must be a power of two");
+    const int64_t n = ix->n_slots;
+    prefix::reset_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*ix);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+static int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+extern "C" int64_t irm_prefix_workspace_bytes(int64_t n_tokens, int32_t n_seq) {
+    const int64_t n_chunks = n_tokens / prefix::CH + n_seq + 1;
+    return align256((int64_t)(n_seq + 1) * 8) + 2 * align256(n_chunks * (int64_t)sizeof(Aff)) +
+           align256(n_tokens * 8);
+}
+
+extern "C" int irm_prefix_match_insert(const irm_prefix_view *ix, const uint32_t *tok, const int64_t *seq_off,
+                                       int32_t n_seq, int64_t n_tokens, const int64_t *op_epoch,
+                                       const uint8_t *op_insert, const uint8_t *op_query, const uint32_t *arena,
+                                       const int64_t *wit_off, const int64_t *wit_len, int64_t *m, int64_t *wit,
+                                       void *ws, int64_t ws_bytes, irm_stream_t stream) {
+    IRM_REQUIRE(ix && ix->slot_key && ix->slot_epoch && ix->counters, "null index");
+    IRM_REQUIRE(n_seq >= 0 && n_tokens >= 0, "bad sizes");
+    if (n_seq == 0) return IRM_OK;
+    IRM_REQUIRE(seq_off && op_epoch && m && wit && ws, "null pointer");
+    IRM_REQUIRE(n_tokens == 0 || tok, "null tokens");
+    IRM_REQUIRE(arena && wit_off && wit_len, "queries are verified against the arena: arena/wit_off/wit_len required");
+    IRM_REQUIRE(ws_bytes >= irm_prefix_workspace_bytes(n_tokens, n_seq), "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n_chunks_cap = n_tokens / prefix::CH + n_seq + 1;
+    uint8_t *w = (uint8_t *)ws;
+    int64_t *chunk_off = (int64_t *)w;
+    w += align256((int64_t)(n_seq + 1) * 8);
+    Aff *agg = (Aff *)w;
+    w += align256(n_chunks_cap * (int64_t)sizeof(Aff));
+    Aff *carry = (Aff *)w;
+    w += align256(n_chunks_cap * (int64_t)sizeof(Aff));
+    uint64_t *key = (uint64_t *)w;
+    prefix::chunk_plan_kernel<<<1, prefix::PT, 0, s>>>(seq_off, n_seq, chunk_off);
+    IRM_LAUNCH_CHECK();
+    // grid = an upper bound on the chunk count; CTAs past the real count exit
+    const unsigned grid = (unsigned)n_chunks_cap;
+    prefix::aggregate_kernel<<<grid, prefix::PT, 0, s>>>(tok, seq_off, n_seq, chunk_off, agg);
+    IRM_LAUNCH_CHECK();
+    prefix::carry_kernel<<<(n_seq + 127) / 128, 128, 0, s>>>(chunk_off, n_seq, agg, carry);
+    IRM_LAUNCH_CHECK();
+    prefix::keys_kernel<<<grid, prefix::PT, 0, s>>>(*ix, tok, seq_off, n_seq, chunk_off, carry, op_epoch, op_insert,
+                                                     key);
+    IRM_LAUNCH_CHECK();
+    prefix::query_kernel<<<(n_seq + 127) / 128, 128, 0, s>>>(*ix, seq_off, n_seq, op_epoch, op_query, key, m, wit);
+    IRM_LAUNCH_CHECK();
+    prefix::verify_kernel<<<n_seq, 256, 0, s>>>(*ix, tok, seq_off, n_seq, arena, wit_off, wit_len, m, wit);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}

@@ -28,7 +28,7 @@ from . import ops
 from .chunking import Chunk, ChunkerParams, cdc_chunk_batch, marker_pin_offsets
 from .fingerprint import fingerprint, fingerprint_spans
 from .model import Request, Trace, flatten, marker_spans
-from .radix import RadixTree
+from .radix import DeviceRadixTree
 from .registry import KvRegistry, SyntheticKvParams
 from .rotary import Precision, RotarySpec, make_spec, rotate_rows_device
 
@@ -112,9 +112,10 @@ class LiveVerificationError(AssertionError):
 class EngineState:
     """Mutable caches shared across the requests of one trace run."""
 
-    def __init__(self, config: ServeConfig, max_entries: int = 1 << 16):
+    def __init__(self, config: ServeConfig, max_entries: int = 1 << 16, max_prefixes: int = 1 << 22,
+                 max_tokens: int = 1 << 24):
         self.config = config
-        self.tree = RadixTree()
+        self.tree = DeviceRadixTree(max_prefixes=max_prefixes, max_tokens=max_tokens)  # K0
         self.registry = KvRegistry(config.kv, config.spec, max_entries=max_entries)
         self.subwindows: set[int] = set()
         self.request_counter = 0
@@ -156,19 +157,21 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
     reg = state.registry
     dev = ops._dev()
 
-    # ---- phase 1: exact-prefix match (host radix), sequential by construction
+    # ---- phase 1: exact-prefix match (K0): request i matches everything inserted before it,
+    # then is inserted (engine.py:170, 228), as one batched device operation
     plans: list[_Plan] = []
+    flats = []
     for r in requests:
         flat, _ = flatten(r)
         if len(flat) == 0:
             raise ValueError("request flattens to zero tokens")
-    for r in requests:
-        flat, _ = flatten(r)
-        m, _w = state.tree.match_prefix(flat)
+        flats.append(flat)
+    handles = list(range(state.request_counter, state.request_counter + len(requests)))
+    ms, _w = state.tree.match_insert(flats, handles)
+    state.request_counter += len(requests)
+    for r, flat, m in zip(requests, flats, ms):
         pins = marker_pin_offsets((max(s - m, 0), e - m) for s, e in marker_spans(r) if e - 1 >= m)
         plans.append(_Plan(flat, m, pins))
-        state.tree.insert(flat, state.request_counter)
-        state.request_counter += 1
 
     # ---- phase 2: one CDC + xxh64 launch over all tails (K1)
     tails = [p.flat[p.m:] for p in plans]

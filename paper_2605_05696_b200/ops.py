@@ -149,7 +149,7 @@ _DTYPE_CODE = {torch.float64: N.DTYPE_F64, torch.float32: N.DTYPE_F32, torch.bfl
 
 
 def inv_freq_device(inv_freq) -> torch.Tensor:
-    return torch.as_tensor(np.asarray(inv_freq, dtype=np.float64)).to(_dev())
+    return torch.from_numpy(np.array(inv_freq, dtype=np.float64)).to(_dev())
 
 
 def rotate_gather(pool: torch.Tensor, out: torch.Tensor, src_row: torch.Tensor, dst_row: torch.Tensor,

@@ -1,7 +1,8 @@
 """Exact-prefix index for phase 1 of the serve path (reference radix.py).
 
-Host-side and pointer-chasing by nature (kept off the GPU; a
-batched device prefix index is §8(f) item 1). Edges reference slices of the
+``RadixTree`` is the host form (pointer chasing); ``DeviceRadixTree`` is
+K0, the batched device prefix index of SURVEY §8(f) item 1, which the serve
+path uses. Edges reference slices of the
 inserted sequences (numpy views, no copies) and common-prefix lengths are
 computed with vectorised compares, so a 32K-token match is a handful of
 numpy calls instead of a per-token Python loop. Semantics follow
@@ -84,3 +85,126 @@ class RadixTree:
             node = child
             i += common
         return (matched, witness) if matched else (0, None)
+
+
+class DeviceRadixTree:
+    """K0: the exact-prefix index on the B200 (csrc/prefix.cu) behind the
+    RadixTree API (radix.py:31-89): ``insert(seq, handle)``,
+    ``match_prefix(seq) -> (m, handle)``, plus the batched forms the serve
+    path uses (``run_ops``, ``match_insert``), one launch sequence per batch.
+
+    Every prefix of every inserted sequence is a key of a device hash table
+    holding the earliest insert epoch that reaches it; a query is a binary
+    search over its own prefix keys, verified token by token against the
+    witness's stored tokens (``check()`` raises on a failed verification or
+    a full table). Inserted sequences are kept in a device token arena."""
+
+    def __init__(self, capacity_hint: int | None = None, max_prefixes: int = 1 << 22,
+                 max_tokens: int = 1 << 24, max_sequences: int = 1 << 16):
+        import torch
+
+        from . import _native as N
+        from . import ops
+
+        self._N, self._torch = N, torch
+        dev = ops._dev()
+        n_slots = 2
+        while n_slots < 2 * max_prefixes:
+            n_slots <<= 1
+        self.capacity_hint = capacity_hint
+        self.slot_key = torch.empty(n_slots, dtype=torch.int64, device=dev)
+        self.slot_epoch = torch.empty(n_slots, dtype=torch.int64, device=dev)
+        self.counters = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.view = N.PrefixView(N.ptr(self.slot_key), N.ptr(self.slot_epoch), n_slots, N.ptr(self.counters))
+        self.arena = torch.zeros(max_tokens, dtype=torch.int32, device=dev)
+        self.wit_off = torch.zeros(max_sequences, dtype=torch.int64, device=dev)
+        self.wit_len = torch.zeros(max_sequences, dtype=torch.int64, device=dev)
+        self.used = 0        # arena tokens in use
+        self._epoch = 0      # inserts so far (radix.py:34-35)
+        self.handles: list = []
+        self._ws = None
+        N.check(N.lib().irm_prefix_reset(self.view, N.stream_ptr()), "irm_prefix_reset")
+
+    def _workspace(self, n_tok, n_seq):
+        need = int(self._N.lib().irm_prefix_workspace_bytes(n_tok, n_seq))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = self._torch.empty(max(need, 256), dtype=self._torch.uint8, device=self.arena.device)
+        return self._ws
+
+    def run_ops(self, seqs, insert, query, handles=None):
+        """A batch of operations in order. ``seqs``: list of token sequences;
+        ``insert[i]`` / ``query[i]``: booleans. Returns device tensors
+        (m, witness epoch); a query sees every insert before it in the batch
+        and before the batch. ``handles[i]`` names inserted sequence i."""
+        torch, N = self._torch, self._N
+        arrs = [np.asarray(s, dtype=np.uint64).astype(np.uint32) if not isinstance(s, np.ndarray)
+                else s.astype(np.uint32, copy=False) for s in seqs]
+        n = len(arrs)
+        lens = np.array([a.size for a in arrs], np.int64)
+        off = np.zeros(n + 1, np.int64)
+        np.cumsum(lens, out=off[1:])
+        n_tok = int(off[-1])
+        ins = np.asarray(insert, bool)
+        qry = np.asarray(query, bool)
+        n_ins = int(ins.sum())
+        if self.used + n_tok > self.arena.numel():
+            raise ValueError("prefix index token arena is full: raise max_tokens")
+        if self._epoch + n_ins > self.wit_off.numel():
+            raise ValueError("prefix index holds max_sequences inserts: raise max_sequences")
+        before = np.cumsum(ins) - ins  # inserts earlier in the batch
+        # an insert's epoch is its insert index; a query's bound is the number of inserts before it
+        epoch = (self._epoch + before).astype(np.int64)
+        dev = self.arena.device
+        base = self.used
+        if n_tok:
+            flat = np.concatenate(arrs).view(np.int32)
+            self.arena[base:base + n_tok].copy_(torch.from_numpy(flat), non_blocking=False)
+        ep_ins = epoch[ins]
+        if n_ins:
+            self.wit_off[self._epoch:self._epoch + n_ins].copy_(torch.from_numpy(base + off[:-1][ins]))
+            self.wit_len[self._epoch:self._epoch + n_ins].copy_(torch.from_numpy(lens[ins]))
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        seq_off, op_epoch = d(off), d(epoch)
+        op_ins, op_q = d(ins.astype(np.uint8)), d(qry.astype(np.uint8))
+        m = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        wit = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        ws = self._workspace(n_tok, n)
+        rc = N.lib().irm_prefix_match_insert(
+            self.view, N.ptr(self.arena[base:]) if base < self.arena.numel() else None, N.ptr(seq_off), n,
+            n_tok, N.ptr(op_epoch), N.ptr(op_ins), N.ptr(op_q), N.ptr(self.arena), N.ptr(self.wit_off),
+            N.ptr(self.wit_len), N.ptr(m), N.ptr(wit), N.ptr(ws), ws.numel(), N.stream_ptr())
+        N.check(rc, "irm_prefix_match_insert")
+        self.used += n_tok
+        self._epoch += n_ins
+        hs = list(handles) if handles is not None else [None] * n
+        self.handles += [hs[i] for i in range(n) if ins[i]]
+        return m[:n], wit[:n]
+
+    def match_insert(self, seqs, handles):
+        """Each sequence is matched against everything inserted before it, then
+        inserted (engine.py:170 then :228). Returns host lists (m, witness handle)."""
+        n = len(seqs)
+        m, wit = self.run_ops(seqs, [True] * n, [True] * n, handles)
+        self.check()
+        mh, wh = m.cpu().tolist(), wit.cpu().tolist()
+        return mh, [self.handles[w] if w >= 0 else None for w in wh]
+
+    def insert(self, seq: Sequence[int], handle: Hashable) -> None:
+        self.run_ops([seq], [True], [False], [handle])
+
+    def match_prefix(self, seq: Sequence[int]) -> tuple[int, Hashable | None]:
+        m, wit = self.run_ops([seq], [False], [True])
+        self.check()
+        mm, w = int(m[0]), int(wit[0])
+        return (mm, self.handles[w]) if mm else (0, None)
+
+    def check(self):
+        flags = int(self.counters[1])
+        if flags & 1:
+            raise RuntimeError("device prefix index table is full: raise max_prefixes")
+        if flags & 2:
+            raise RuntimeError("device prefix index: a match failed token verification (hash collision)")
+
+    @property
+    def n_prefixes(self) -> int:
+        return int(self.counters[0])

@@ -49,3 +49,8 @@ def golden_registry():
 @pytest.fixture(scope="session")
 def golden_traces():
     return load_npz("traces")
+
+
+@pytest.fixture(scope="session")
+def golden_radix():
+    return load_npz("radix")

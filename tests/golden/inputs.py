@@ -131,3 +131,40 @@ TRACE_CASES = {
     "tool_variants": dict(pattern="tool_variants", n_req=12, body_len=2500, seed=5),
     "agent_meta_k5": dict(pattern="agent_meta", n_req=6, body_len=3000, seed=9, k=5),
 }
+
+
+# K0 / radix.py: operation sequences (insert or query, with a token sequence each)
+RADIX_CASES = {
+    # the reference's own randomized test shape (test_radix.py:75-90): alphabet 6, lengths 0..14
+    "small_alphabet": dict(kind="small", n_ops=3000, seed=2024),
+    # long sequences sharing prefixes that diverge at random depths (u32 tokens)
+    "long_shared": dict(kind="long", n_ops=160, seed=77),
+    # serve-loop shape: shared header, random metadata, shared body (engine.py:170, 228)
+    "agent_meta": dict(kind="agent", n_ops=48, seed=5),
+}
+
+
+def radix_case_inputs(case: dict):
+    """-> list of (is_insert, np.uint32 tokens)."""
+    rng = np.random.default_rng(case["seed"])
+    ops = []
+    if case["kind"] == "small":
+        for _ in range(case["n_ops"]):
+            seq = rng.integers(0, 6, size=int(rng.integers(0, 15))).astype(np.uint32)
+            ops.append((bool(rng.random() < 0.5), seq))
+    elif case["kind"] == "long":
+        bases = [rng.integers(0, 2**32, size=6000, dtype=np.uint64).astype(np.uint32) for _ in range(4)]
+        for _ in range(case["n_ops"]):
+            b = bases[int(rng.integers(0, 4))].copy()
+            n = int(rng.integers(1, 6000))
+            cut = int(rng.integers(0, n))
+            b[cut:n] = rng.integers(0, 2**32, size=n - cut, dtype=np.uint64).astype(np.uint32)
+            ops.append((bool(rng.random() < 0.6), b[:n].copy()))
+    else:
+        header = rng.integers(0, 2**32, size=200, dtype=np.uint64).astype(np.uint32)
+        body = rng.integers(0, 2**32, size=3000, dtype=np.uint64).astype(np.uint32)
+        for i in range(case["n_ops"]):
+            meta = rng.integers(0, 2**32, size=int(rng.integers(0, 40)), dtype=np.uint64).astype(np.uint32)
+            seq = np.concatenate([header[:int(rng.integers(150, 201))], meta, body[:int(rng.integers(0, 3000))]])
+            ops.append((i % 3 != 2, seq))  # two of three requests are inserted after matching
+    return ops

@@ -1,0 +1,111 @@
+"""GPU parity of K0 (csrc/prefix.cu, radix.DeviceRadixTree) against the
+reference RadixTree's own outputs (tests/golden/radix.npz, made by
+make_golden.py from radix.py:31-83) and the brute-force oracle the reference
+tests pin it with (test_radix.py:15-23): longest match m bit-exact and the
+earliest-inserted witness, for op sequences run as one batch, in small
+batches, and one op at a time through the scalar API."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_npz
+from inputs import RADIX_CASES, radix_case_inputs
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _tree(**kw):
+    from paper_2605_05696_b200.radix import DeviceRadixTree
+
+    args = dict(max_prefixes=1 << 20, max_tokens=1 << 22, max_sequences=1 << 14)
+    args.update(kw)
+    return DeviceRadixTree(**args)
+
+
+@pytest.mark.parametrize("batch", [None, 7, 1])
+@pytest.mark.parametrize("case", sorted(RADIX_CASES))
+def test_prefix_ops_golden(case, batch):
+    g = load_npz("radix")[case]
+    ops = radix_case_inputs(RADIX_CASES[case])
+    if batch == 1 and len(ops) > 500:
+        ops = ops[:500]
+    tree = _tree()
+    bs = batch or len(ops)
+    got_m, got_w = np.full(len(ops), -1), np.full(len(ops), -1)
+    for b0 in range(0, len(ops), bs):
+        part = ops[b0:b0 + bs]
+        ins = [o[0] for o in part]
+        m, w = tree.run_ops([o[1] for o in part], ins, [not x for x in ins], handles=list(range(b0, b0 + len(part))))
+        m, w = m.cpu().numpy(), w.cpu().numpy()
+        for k, (is_ins, _) in enumerate(part):
+            if not is_ins:
+                got_m[b0 + k] = m[k]
+                got_w[b0 + k] = tree.handles[w[k]] if m[k] > 0 else -1
+    tree.check()
+    q = np.array([not o[0] for o in ops])
+    assert np.array_equal(got_m[q], g["m"][:len(ops)][q])
+    assert np.array_equal(got_w[q], g["witness"][:len(ops)][q])
+
+
+def test_prefix_scalar_api():
+    """insert / match_prefix one call at a time, as RadixTree (radix.py:31-83)."""
+    tree = _tree()
+    assert tree.match_prefix([1, 2, 3]) == (0, None)  # test_radix.py:26-27
+    tree.insert([1, 2, 3], "a")
+    assert tree.match_prefix([]) == (0, None)
+    tree.insert([1, 2, 3, 4], "b")
+    tree.insert([1, 2], "c")
+    assert tree.match_prefix([1, 2, 3, 4, 5]) == (4, "b")
+    assert tree.match_prefix([1, 2, 3]) == (3, "a")  # earliest witness at depth 3
+    assert tree.match_prefix([1, 2, 9]) == (2, "a")
+    assert tree.match_prefix([9]) == (0, None)
+    tree.insert([], "empty")
+    assert tree.match_prefix([7]) == (0, None)
+    tree.check()
+
+
+def test_prefix_match_insert_sessions():
+    """The serve-loop form at scale: 256 agent sessions x 4 turns of 8K-16K tokens
+    (shared system header, per-session history growing turn by turn), each
+    request matched against every earlier one then inserted (engine.py:170,
+    228); checked against the host radix and, for a sample, the brute force."""
+    from paper_2605_05696_b200.radix import RadixTree
+
+    rng = np.random.default_rng(12)
+    header = rng.integers(0, 2**32, size=2000, dtype=np.uint64).astype(np.uint32)
+    hist = [np.concatenate([header, rng.integers(0, 2**32, size=int(rng.integers(6000, 14000)),
+                                                 dtype=np.uint64).astype(np.uint32)]) for _ in range(256)]
+    reqs = []
+    for turn in range(4):
+        for s in range(256):
+            if turn:
+                hist[s] = np.concatenate([hist[s], rng.integers(0, 2**32, size=int(rng.integers(50, 500)),
+                                                                dtype=np.uint64).astype(np.uint32)])
+            cut = hist[s].size - int(rng.integers(0, 64))  # sometimes an edited tail
+            reqs.append(hist[s][:cut].copy())
+    tree = _tree(max_prefixes=1 << 23, max_tokens=1 << 24)
+    torch.cuda.synchronize()
+    ms, ws = [], []
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for t in range(4):  # one batch per turn
+        part = reqs[t * 256:(t + 1) * 256]
+        ev[0].record()
+        m, w = tree.match_insert(part, list(range(t * 256, (t + 1) * 256)))
+        ev[1].record()
+        ms += m
+        ws += w
+    torch.cuda.synchronize()
+    host = RadixTree()
+    for i, r in enumerate(reqs):
+        hm, hw = host.match_prefix(r)
+        assert (ms[i], ws[i]) == (hm, hw), i
+        host.insert(r, i)
+    for i in rng.choice(len(reqs), size=24, replace=False):
+        bm, bw = O.prefix_match(list(enumerate(reqs[:i])), reqs[i])
+        assert (ms[i], ws[i]) == (bm, bw)
+    assert sum(m > 0 for m in ms) > 900
+    tree.check()
+    print(f"K0 match_insert: {sum(r.size for r in reqs[-256:])} tokens in {ev[0].elapsed_time(ev[1]):.3f} ms "
+          f"(last batch), {tree.n_prefixes} prefixes stored")

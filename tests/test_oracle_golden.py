@@ -10,7 +10,9 @@ import pytest
 
 from oracle import oracle as O
 from oracle import workloads as W
-from inputs import CDC_CASES, ROT_CASES, TRACE_CASES, cdc_case_inputs, rot_case_inputs, GEAR, marker_tokens
+from conftest import load_npz
+from inputs import (CDC_CASES, GEAR, RADIX_CASES, ROT_CASES, TRACE_CASES, cdc_case_inputs, marker_tokens,
+                    radix_case_inputs, rot_case_inputs)
 
 
 def test_gear_table_golden(constants):
@@ -132,3 +134,17 @@ def test_threaded_batch_matches_single():
         a = O.cdc_chunk(toks[off[s]:off[s + 1]], pins=pins[s])
         o, c = out_off[s], counts[s]
         assert np.array_equal(a[0], st[o:o + c]) and np.array_equal(a[2], fp[o:o + c])
+
+
+@pytest.mark.parametrize("case", sorted(RADIX_CASES))
+def test_prefix_match_oracle_golden(case):
+    """oracle.prefix_match (brute force) == the reference RadixTree on every query op."""
+    g = load_npz("radix")[case]
+    want_m, want_w = g["m"], g["witness"]
+    inserted = []
+    for i, (is_insert, seq) in enumerate(radix_case_inputs(RADIX_CASES[case])):
+        if is_insert:
+            inserted.append((i, seq))
+            continue
+        m, w = O.prefix_match(inserted, seq)
+        assert m == want_m[i] and (-1 if w is None else w) == want_w[i], (case, i)
