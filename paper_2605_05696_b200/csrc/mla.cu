@@ -66,6 +66,7 @@ struct Params {
     int64_t q_pos0;
     float scale_log2;         // softmax scale * log2(e)
     int dbg;                  // IRM_MLA_DEBUG: per-role cycle breakdown of CTA 0
+    int tgroup;               // pairs per shared key-tile order (IRM_MLA_TGROUP; 1 = every pair its own)
 };
 
 __device__ __forceinline__ uint32_t swz128(int row, int chunk) {  // SW128 byte offset (128-B rows)
@@ -92,6 +93,11 @@ __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 
 #define IRM_MLA_PROF_MASK 0
 #endif
 constexpr bool kProf = IRM_MLA_PROF_MASK != 0;
+// What-if builds (wrong results; cost attribution only): 1 = V loaded but never waited for,
+// 2 = V never loaded, 3 = K loaded for the first KST tiles only
+#ifndef IRM_MLA_WHATIF
+#define IRM_MLA_WHATIF 0
+#endif
 template <int ROLE>
 __device__ __forceinline__ long long prof_clock() {
     if constexpr ((IRM_MLA_PROF_MASK & ROLE) != 0) return clock64();
@@ -196,8 +202,27 @@ __device__ __forceinline__ void store_rope(const Params &p, uint8_t *tile, int p
     fence_proxy_async_smem();
 }
 
+// L2 policy of the pool loads (IRM_MLA_HINT: 0 none, 1 evict_last): the pool is re-read by
+// every CTA pair, the Q / O streams are touched once
+#ifndef IRM_MLA_HINT
+#define IRM_MLA_HINT 0
+#endif
+__device__ __forceinline__ uint64_t pool_policy() {
+    uint64_t pol = 0;
+    if constexpr (IRM_MLA_HINT == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 // BN consecutive pool rows x 64 columns -> one SW128 piece
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *tmap, int col, int row, uint64_t *bar) {
+    if constexpr (IRM_MLA_HINT != 0) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+            "l"(tmap), "r"(col), "r"(row), "r"(smem_u32(bar)), "l"(pool_policy())
+            : "memory");
+        return;
+    }
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
             dst),
@@ -205,9 +230,34 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *tma
         : "memory");
 }
 
+// 32 consecutive pool rows x several 64-column pieces in ONE TMA op (the pool seen as
+// [piece][row][64 cols] with a 128-B piece stride): smem gets one 4 KB SW128 piece after
+// another, exactly the layout of separate 2-D boxes, for 1/8 (K) or 1/4 (V) of the ops
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *tmap, int row, int piece, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(dst), "l"(tmap), "r"(0), "r"(row), "r"(piece), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *tmap, int row, int piece, int group,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+        ::"r"(dst), "l"(tmap), "r"(0), "r"(row), "r"(piece), "r"(group), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // 4 arbitrary pool rows x 64 columns (128 B each) -> 512 B of a SW128 piece
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tmap, int col, int r0, int r1, int r2,
                                             int r3, uint64_t *bar) {
+    if constexpr (IRM_MLA_HINT != 0) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+            "l"(tmap), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar)), "l"(pool_policy())
+            : "memory");
+        return;
+    }
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
@@ -574,7 +624,8 @@ __device__ __forceinline__ void tma_rows32(const Rows32 &r, const CUtensorMap *t
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
 mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
-                        const __grid_constant__ CUtensorMap tmap_tile) {
+                        const __grid_constant__ CUtensorMap tmap_tile, const __grid_constant__ CUtensorMap tmap_k8,
+                        const __grid_constant__ CUtensorMap tmap_v4) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     __shared__ __align__(8) uint64_t b_q, b_qpair, b_kfull[KST], b_kpair[KST], b_vfull[VST], b_vpair[VST],
@@ -591,7 +642,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
     const int64_t max_pos = p.q_pos0 + last_row / p.heads;
     const int n_keys = (int)min((int64_t)p.n_kv, max_pos + 1);
     const int T = (n_keys + PBN - 1) / PBN;
-    const int toff = (int)(((uint32_t)(blockIdx.x >> 1) * 2654435761u) % (uint32_t)T);
+    const int toff = (int)(((uint32_t)((blockIdx.x >> 1) / p.tgroup) * 2654435761u) % (uint32_t)T);
 
     if (threadIdx.x == 0) {
         mbar_init(&b_q, 128);
@@ -652,10 +703,19 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             long long a0 = prof_clock<1>();
             if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
             c_e += prof_clock<1>() - a0;
+            if (IRM_MLA_WHATIF == 3 && t >= KST) {
+                if (lane == 0) mbar_arrive(&b_kfull[st]);
+                continue;
+            }
             if (lane == 0) mbar_arrive_expect_tx(&b_kfull[st], CKV_TX);
             __syncwarp();
             const uint32_t dst = smem_u32(smem + S_K + st * KTILE);
-            for (int pc = 0; pc < 8; ++pc) tma_rows32(rr, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, lane, &b_kfull[st]);
+            if (rr.contig) {  // one op for the 8 c_KV pieces of 32 consecutive rows
+                if (lane == 0) tma_load_3d(dst, &tmap_k8, rr.row0, 0, &b_kfull[st]);
+            } else {
+                for (int pc = 0; pc < 8; ++pc)
+                    tma_rows32(rr, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, lane, &b_kfull[st]);
+            }
         }
         if (kProf && p.dbg && blockIdx.x < 2 && lane == 0)
             printf("2sm ktma cta%d: wait_empty %lld total %lld\n", (int)rank, c_e, prof_clock<1>() - c0);
@@ -663,19 +723,34 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         // ------------------------------------------------ V: all 64 keys x this CTA's 256 latent dims
         // key half-tiles u = 2t + a: keys [64 kt + 32a, +32), rows read one half-tile ahead
         int row_next = key_row(p, (toff % T) * PBN + lane);
+        long long c_ve = 0, c_vi = 0, c0v = prof_clock<1>();
         for (int u = 0; u < 2 * T; ++u) {
             const int st = u % VST;
             const Rows32 rr = rows32_resolve(row_next, lane);
             if (u + 1 < 2 * T) row_next = key_row(p, (((u + 1) / 2 + toff) % T) * PBN + 32 * ((u + 1) & 1) + lane);
+            if (IRM_MLA_WHATIF == 2) {
+                if (lane == 0) mbar_arrive(&b_vfull[st]);
+                continue;
+            }
+            long long a0 = prof_clock<1>();
             if (u >= VST) mbar_wait(&b_vempty[st], ((u / VST) - 1) & 1);
+            c_ve += prof_clock<1>() - a0;
+            long long a1 = prof_clock<1>();
             if (lane == 0) mbar_arrive_expect_tx(&b_vfull[st], (uint32_t)VTILE);
             __syncwarp();
             const uint32_t dst = smem_u32(smem + S_V + st * VTILE);
-            for (int j = 0; j < 4; ++j) {
-                const int cpiece = (j >> 1) * 4 + 2 * (int)rank + (j & 1);  // dims [256h + 128 rank, +128)
-                tma_rows32(rr, &tmap_pool, &tmap_tile, dst + j * VPIECE, cpiece, lane, &b_vfull[st]);
+            if (rr.contig) {  // one op: pieces 4h + 2 rank + i, (h, i) in {0,1}^2
+                if (lane == 0) tma_load_4d(dst, &tmap_v4, rr.row0, 2 * (int)rank, 0, &b_vfull[st]);
+            } else {
+                for (int j = 0; j < 4; ++j) {
+                    const int cpiece = (j >> 1) * 4 + 2 * (int)rank + (j & 1);  // dims [256h + 128 rank, +128)
+                    tma_rows32(rr, &tmap_pool, &tmap_tile, dst + j * VPIECE, cpiece, lane, &b_vfull[st]);
+                }
             }
+            c_vi += prof_clock<1>() - a1;
         }
+        if (kProf && p.dbg && blockIdx.x < 2 && lane == 0)
+            printf("2sm vtma cta%d: wait_empty %lld issue %lld total %lld\n", (int)rank, c_ve, c_vi, prof_clock<1>() - c0v);
     } else if (warp == W_MMA2) {
         if (rank != 0) {
             // ------------------------------------------------ peer: relay local data readiness to the leader
@@ -693,7 +768,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 if (t + 1 < T) relay_k(t + 1);
                 mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
                 if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_pfull[t & 1]), 0));
-                for (int u = 2 * t; u < 2 * t + 2; ++u) {
+                for (int u = 2 * t; u < 2 * t + 2 && (IRM_MLA_WHATIF == 0 || IRM_MLA_WHATIF == 3); ++u) {
                     mbar_wait(&b_vfull[u % VST], (u / VST) & 1);
                     if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_vpair[u % VST]), 0));
                 }
@@ -712,7 +787,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             const uint32_t p_lo = (uint32_t)p_desc, p_hi = (uint32_t)(p_desc >> 32);
             mbar_wait(&b_q, 0);
             mbar_wait(&b_qpair, 0);
-            long long c_k = 0, c_kp = 0, c_p = 0, c_v = 0, c0 = prof_clock<2>();
+            long long c_k = 0, c_kp = 0, c_p = 0, c_v = 0, c_vl = 0, c0 = prof_clock<2>();
             auto issue_qk = [&](int t) {
                 const int st = t % KST;
                 long long a0 = prof_clock<2>();
@@ -752,8 +827,11 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 for (int a = 0; a < 2; ++a) {  // PV over key half a, as soon as its V half-tile lands
                     const int u = 2 * t + a, vs = u % VST;
                     long long a1 = prof_clock<2>();
-                    mbar_wait(&b_vfull[vs], (u / VST) & 1);
-                    mbar_wait(&b_vpair[vs], (u / VST) & 1);
+                    if (IRM_MLA_WHATIF == 0 || IRM_MLA_WHATIF == 3) {
+                        mbar_wait(&b_vfull[vs], (u / VST) & 1);
+                        c_vl += prof_clock<2>() - a1;
+                        mbar_wait(&b_vpair[vs], (u / VST) & 1);
+                    }
                     c_v += prof_clock<2>() - a1;
                     tc::fence_after();
                     const uint32_t vd = v_lo + ((vs * VTILE) >> 4);
@@ -773,8 +851,8 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 }
             }
             if (kProf && p.dbg && blockIdx.x == 0 && lane == 0)
-                printf("2sm mma: wait_k %lld wait_kpair %lld wait_p %lld wait_v %lld total %lld T=%d\n", c_k, c_kp, c_p,
-                       c_v, prof_clock<2>() - c0, T);
+                printf("2sm mma: wait_k %lld wait_kpair %lld wait_p %lld wait_v %lld (local %lld) total %lld T=%d\n", c_k, c_kp,
+                       c_p, c_v, c_vl, prof_clock<2>() - c0, T);
         }
     } else {
         // ------------------------------------------------ softmax / correction (warps 0-3)
@@ -963,6 +1041,8 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
         return IRM_ECUDA;
     }
     CUtensorMap tmap, tmap_tile;
+    const int promo_env = getenv("IRM_MLA_PROMO") ? atoi(getenv("IRM_MLA_PROMO")) : 3;
+    const CUtensorMapL2promotion promo = (CUtensorMapL2promotion)(promo_env < 0 || promo_env > 3 ? 3 : promo_env);
     const cuuint64_t strides[1] = {(cuuint64_t)mla::DQK * 2};
     const cuuint32_t estr[2] = {1, 1};
     for (int which = 0; which < 2; ++which) {
@@ -973,10 +1053,36 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
         const cuuint32_t box[2] = {64, which == 0 ? 1u : (cuuint32_t)mla::BN};
         CUresult cr = encode(which == 0 ? &tmap : &tmap_tile, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                              const_cast<void *>(pool), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_SWIZZLE_128B, promo,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) {
             set_error("cuTensorMapEncodeTiled failed (%d)", (int)cr);
+            return IRM_ECUDA;
+        }
+    }
+    // multi-piece maps over the same rows as tmap_tile: [piece][row][64 cols], piece stride 128 B
+    //   k8: 8 pieces (the c_KV part of a row), box {64, 32, 8}
+    //   v4: pieces p + 4 g for p in [0, 4), g in [0, 2), box {64, 32, 2, 2}
+    CUtensorMap tmap_k8, tmap_v4;
+    {
+        const cuuint64_t rows = (cuuint64_t)(kv_rows ? pool_rows : n_kv);
+        const cuuint64_t dk[3] = {64, rows, 8};
+        const cuuint64_t sk[2] = {(cuuint64_t)mla::DQK * 2, 128};
+        const cuuint32_t bk[3] = {64, (cuuint32_t)mla::BN, 8};
+        const cuuint32_t ek[3] = {1, 1, 1};
+        CUresult cr = encode(&tmap_k8, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(pool), dk, sk, bk, ek,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const cuuint64_t dv[4] = {64, rows, 4, 2};
+        const cuuint64_t sv[3] = {(cuuint64_t)mla::DQK * 2, 128, 512};
+        const cuuint32_t bv[4] = {64, (cuuint32_t)mla::BN, 2, 2};
+        const cuuint32_t ev[4] = {1, 1, 1, 1};
+        if (cr == CUDA_SUCCESS)
+            cr = encode(&tmap_v4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(pool), dv, sv, bv, ev,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled (multi-piece) failed (%d)", (int)cr);
             return IRM_ECUDA;
         }
     }
@@ -995,11 +1101,14 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
     p.q_pos0 = q_pos0;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.dbg = getenv("IRM_MLA_DEBUG") != nullptr;
+    p.tgroup = getenv("IRM_MLA_TGROUP") ? atoi(getenv("IRM_MLA_TGROUP")) : 1;
+    if (p.tgroup < 1) p.tgroup = 1;
     if (getenv("IRM_MLA_1SM") == nullptr) {  // CTA-pair (cta_group::2) kernel: 128 rows per cluster
         const int smem = mla::p2::SMEM2 + 1024;
         IRM_CUDA_CHECK(cudaFuncSetAttribute(mla::p2::mla_reattach_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         const int64_t grid = 2 * ((p.n_rows + 127) / 128);
-        mla::p2::mla_reattach_2sm_kernel<<<(unsigned)grid, mla::p2::THREADS2, smem, (cudaStream_t)stream>>>(p, tmap, tmap_tile);
+        mla::p2::mla_reattach_2sm_kernel<<<(unsigned)grid, mla::p2::THREADS2, smem, (cudaStream_t)stream>>>(
+            p, tmap, tmap_tile, tmap_k8, tmap_v4);
         IRM_LAUNCH_CHECK();
         return IRM_OK;
     }
