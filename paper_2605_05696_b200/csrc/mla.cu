@@ -247,6 +247,31 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *tma
         : "memory");
 }
 
+// .cta_group::2 forms: the data lands in the issuing CTA's smem, the transaction bytes
+// complete on the LEADER CTA's mbarrier (bar = its shared::cluster address), so the peer's
+// loads need no relay
+__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap *tmap, int row, int piece, int group,
+                                                 uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst), "l"(tmap), "r"(0), "r"(row), "r"(piece), "r"(group), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_gather4_pair(uint32_t dst, const CUtensorMap *tmap, int col, int r0, int r1,
+                                                 int r2, int r3, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst), "l"(tmap), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *tmap, int col, int row, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst), "l"(tmap), "r"(col), "r"(row), "r"(bar)
+        : "memory");
+}
+
 // 4 arbitrary pool rows x 64 columns (128 B each) -> 512 B of a SW128 piece
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tmap, int col, int r0, int r1, int r2,
                                             int r3, uint64_t *bar) {
@@ -622,13 +647,26 @@ __device__ __forceinline__ void tma_rows32(const Rows32 &r, const CUtensorMap *t
     if (lane < 8) tma_gather4(dst + lane * 512, tm_g4, 64 * col_piece, r0, r1, r2, r3, bar);
 }
 
+// the same 32 rows, completing on the leader's barrier (bar: shared::cluster address)
+__device__ __forceinline__ void tma_rows32_pair(const Rows32 &r, const CUtensorMap *tm_g4, const CUtensorMap *tm_tile,
+                                                uint32_t dst, int col_piece, int lane, uint32_t bar) {
+    if (r.contig) {
+        if (lane == 0) tma_load_2d_pair(dst, tm_tile, 64 * col_piece, r.row0, bar);
+        return;
+    }
+    const int g = lane & 7;
+    const int r0 = __shfl_sync(0xffffffffu, r.row, 4 * g), r1 = __shfl_sync(0xffffffffu, r.row, 4 * g + 1);
+    const int r2 = __shfl_sync(0xffffffffu, r.row, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, r.row, 4 * g + 3);
+    if (lane < 8) tma_gather4_pair(dst + lane * 512, tm_g4, 64 * col_piece, r0, r1, r2, r3, bar);
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
 mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                         const __grid_constant__ CUtensorMap tmap_tile, const __grid_constant__ CUtensorMap tmap_k8,
                         const __grid_constant__ CUtensorMap tmap_v4) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    __shared__ __align__(8) uint64_t b_q, b_qpair, b_kfull[KST], b_kpair[KST], b_vfull[VST], b_vpair[VST],
+    __shared__ __align__(8) uint64_t b_q, b_qpair, b_kfull[KST], b_kpair[KST], b_vfull[VST],
         b_kempty[KST], b_vempty[VST], b_sfull[2], b_pfull[2], b_odone[2];
     __shared__ float sx[2][2][64];  // row-max exchange between the two key halves
     __shared__ float sl[2][64];     // final row-sum exchange
@@ -653,8 +691,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             mbar_init(&b_kempty[s], 1);
         }
         for (int s = 0; s < VST; ++s) {
-            mbar_init(&b_vfull[s], 1);
-            mbar_init(&b_vpair[s], 1);
+            mbar_init(&b_vfull[s], 1);  // leader: its expect_tx; the peer's bytes complete here too
             mbar_init(&b_vempty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -736,15 +773,18 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             if (u >= VST) mbar_wait(&b_vempty[st], ((u / VST) - 1) & 1);
             c_ve += prof_clock<1>() - a0;
             long long a1 = prof_clock<1>();
-            if (lane == 0) mbar_arrive_expect_tx(&b_vfull[st], (uint32_t)VTILE);
+            // the leader's b_vfull[st] completes when BOTH CTAs' half-tiles have landed: the
+            // leader expects 2 x VTILE bytes, the peer's TMA completes on that barrier directly
+            if (rank == 0 && lane == 0) mbar_arrive_expect_tx(&b_vfull[st], 2 * (uint32_t)VTILE);
             __syncwarp();
             const uint32_t dst = smem_u32(smem + S_V + st * VTILE);
+            const uint32_t vbar = cl::map_to(smem_u32(&b_vfull[st]), 0);
             if (rr.contig) {  // one op: pieces 4h + 2 rank + i, (h, i) in {0,1}^2
-                if (lane == 0) tma_load_4d(dst, &tmap_v4, rr.row0, 2 * (int)rank, 0, &b_vfull[st]);
+                if (lane == 0) tma_load_4d_pair(dst, &tmap_v4, rr.row0, 2 * (int)rank, 0, vbar);
             } else {
                 for (int j = 0; j < 4; ++j) {
                     const int cpiece = (j >> 1) * 4 + 2 * (int)rank + (j & 1);  // dims [256h + 128 rank, +128)
-                    tma_rows32(rr, &tmap_pool, &tmap_tile, dst + j * VPIECE, cpiece, lane, &b_vfull[st]);
+                    tma_rows32_pair(rr, &tmap_pool, &tmap_tile, dst + j * VPIECE, cpiece, lane, vbar);
                 }
             }
             c_vi += prof_clock<1>() - a1;
@@ -768,10 +808,6 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 if (t + 1 < T) relay_k(t + 1);
                 mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
                 if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_pfull[t & 1]), 0));
-                for (int u = 2 * t; u < 2 * t + 2 && (IRM_MLA_WHATIF == 0 || IRM_MLA_WHATIF == 3); ++u) {
-                    mbar_wait(&b_vfull[u % VST], (u / VST) & 1);
-                    if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_vpair[u % VST]), 0));
-                }
             }
         } else {
             // ------------------------------------------------ leader: MMA issue for the pair
@@ -828,9 +864,8 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                     const int u = 2 * t + a, vs = u % VST;
                     long long a1 = prof_clock<2>();
                     if (IRM_MLA_WHATIF == 0 || IRM_MLA_WHATIF == 3) {
-                        mbar_wait(&b_vfull[vs], (u / VST) & 1);
+                        mbar_wait(&b_vfull[vs], (u / VST) & 1);  // both CTAs' V half-tiles
                         c_vl += prof_clock<2>() - a1;
-                        mbar_wait(&b_vpair[vs], (u / VST) & 1);
                     }
                     c_v += prof_clock<2>() - a1;
                     tc::fence_after();
