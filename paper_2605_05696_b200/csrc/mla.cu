@@ -257,6 +257,13 @@ __device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap
         " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst), "l"(tmap), "r"(0), "r"(row), "r"(piece), "r"(group), "r"(bar)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap *tmap, int row, int piece,
+                                                 uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst), "l"(tmap), "r"(0), "r"(row), "r"(piece), "r"(bar)
+        : "memory");
+}
 __device__ __forceinline__ void tma_gather4_pair(uint32_t dst, const CUtensorMap *tmap, int col, int r0, int r1,
                                                  int r2, int r3, uint32_t bar) {
     asm volatile(
@@ -666,7 +673,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                         const __grid_constant__ CUtensorMap tmap_v4) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    __shared__ __align__(8) uint64_t b_q, b_qpair, b_kfull[KST], b_kpair[KST], b_vfull[VST],
+    __shared__ __align__(8) uint64_t b_q, b_qpair, b_kfull[KST], b_krope[KST], b_vfull[VST],
         b_kempty[KST], b_vempty[VST], b_sfull[2], b_pfull[2], b_odone[2];
     __shared__ float sx[2][2][64];  // row-max exchange between the two key halves
     __shared__ float sl[2][64];     // final row-sum exchange
@@ -686,8 +693,10 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         mbar_init(&b_q, 128);
         mbar_init(&b_qpair, 1);
         for (int s = 0; s < KST; ++s) {
-            mbar_init(&b_kfull[s], 1 + GROUP);  // TMA expect_tx + the rope group
-            mbar_init(&b_kpair[s], 1);
+            // leader: its TMA expect_tx (both CTAs' c_KV bytes land here) + its rope group + the
+            // peer's rope readiness (relayed); peer: b_krope collects its rope group
+            mbar_init(&b_kfull[s], 2 + GROUP);
+            mbar_init(&b_krope[s], GROUP);
             mbar_init(&b_kempty[s], 1);
         }
         for (int s = 0; s < VST; ++s) {
@@ -727,7 +736,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             rope_fetch(p, 2 * kt + (int)rank, gtid, rr);  // keys kt*64 + 32*rank + [0, 32)
             if (t >= KST) mbar_wait(&b_kempty[g], ((t / KST) - 1) & 1);
             store_rope(p, smem + S_K + g * KTILE, gtid, rr);
-            mbar_arrive(&b_kfull[g]);
+            mbar_arrive(rank == 0 ? &b_kfull[g] : &b_krope[g]);
         }
     } else if (warp == W_KTMA) {
         // ------------------------------------------------ c_KV of this CTA's 32 keys (QK operand)
@@ -741,17 +750,19 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
             c_e += prof_clock<1>() - a0;
             if (IRM_MLA_WHATIF == 3 && t >= KST) {
-                if (lane == 0) mbar_arrive(&b_kfull[st]);
+                if (lane == 0 && rank == 0) mbar_arrive(&b_kfull[st]);
                 continue;
             }
-            if (lane == 0) mbar_arrive_expect_tx(&b_kfull[st], CKV_TX);
+            // both CTAs' c_KV bytes complete on the leader's b_kfull (peer: .cta_group::2 TMA)
+            if (rank == 0 && lane == 0) mbar_arrive_expect_tx(&b_kfull[st], 2 * CKV_TX);
             __syncwarp();
             const uint32_t dst = smem_u32(smem + S_K + st * KTILE);
+            const uint32_t kbar = cl::map_to(smem_u32(&b_kfull[st]), 0);
             if (rr.contig) {  // one op for the 8 c_KV pieces of 32 consecutive rows
-                if (lane == 0) tma_load_3d(dst, &tmap_k8, rr.row0, 0, &b_kfull[st]);
+                if (lane == 0) tma_load_3d_pair(dst, &tmap_k8, rr.row0, 0, kbar);
             } else {
                 for (int pc = 0; pc < 8; ++pc)
-                    tma_rows32(rr, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, lane, &b_kfull[st]);
+                    tma_rows32_pair(rr, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, lane, kbar);
             }
         }
         if (kProf && p.dbg && blockIdx.x < 2 && lane == 0)
@@ -797,9 +808,9 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             const uint32_t q_l = cl::map_to(smem_u32(&b_qpair), 0);
             mbar_wait(&b_q, 0);
             if (lane == 0) cl::remote_arrive(q_l);
-            auto relay_k = [&](int t) {
-                mbar_wait(&b_kfull[t % KST], (t / KST) & 1);
-                if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_kpair[t % KST]), 0));
+            auto relay_k = [&](int t) {  // the peer's rotated k_r is in smem
+                mbar_wait(&b_krope[t % KST], (t / KST) & 1);
+                if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_kfull[t % KST]), 0));
             };
             relay_k(0);
             // forwarded in the leader's consumption order: K(t+1) for QK, then P(t) and V(t) for PV.
@@ -827,9 +838,8 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             auto issue_qk = [&](int t) {
                 const int st = t % KST;
                 long long a0 = prof_clock<2>();
-                mbar_wait(&b_kfull[st], (t / KST) & 1);
+                mbar_wait(&b_kfull[st], (t / KST) & 1);  // both CTAs' K tiles (bytes + rope)
                 long long a1 = prof_clock<2>();
-                mbar_wait(&b_kpair[st], (t / KST) & 1);
                 c_k += a1 - a0;
                 c_kp += prof_clock<2>() - a1;
                 tc::fence_after();
