@@ -86,6 +86,28 @@ int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_o
 int irm_xxh64_spans(const uint8_t *base, const int64_t *off, const int64_t *len, int64_t n,
                     uint64_t seed, uint64_t *out, irm_stream_t stream);
 
+/* ---- Ingest: JSONL traces -> flattened token CSR (host; model.py:80-170) ----
+ * Lines split on \n, \r\n and \r when universal_newlines (a text file), on \n
+ * only otherwise (an in-memory stream). irm_trace_scan validates every record
+ * exactly as model._parse_request does
+ * (same error precedence; on IRM_EINVAL err_line / err_field name the line and
+ * field, irm_last_error() the message) and writes sizes[4] = {requests, tokens,
+ * segments, string bytes}. irm_trace_fill then writes, in caller buffers:
+ *   tokens [tokens] u32           the flattened request tokens (flatten, :80-87)
+ *   req_tok_off / req_seg_off [requests + 1], req_turn [requests]
+ *   req_session [2 x requests]    (offset, length) of session_id in strings
+ *   seg_kind [segments]           index into system, header, history, tool, doc,
+ *                                 marker, body, other
+ *   seg_tok_off [segments]        start of the segment within its request
+ *   seg_shared [2 x segments]     (offset, length) of shared_id, offset -1 = null
+ *   strings [string bytes]        UTF-8 */
+int irm_trace_scan(const char *text, int64_t len, int32_t universal_newlines, int64_t *sizes, int64_t *err_line,
+                   char *err_field, int32_t field_cap);
+int irm_trace_fill(const char *text, int64_t len, int32_t universal_newlines, uint32_t *tokens, int64_t *req_tok_off,
+                   int64_t *req_seg_off,
+                   int64_t *req_turn, int64_t *req_session, uint8_t *seg_kind, int64_t *seg_tok_off,
+                   int64_t *seg_shared, char *strings);
+
 /* ---- K0: exact-prefix index (radix.py:31-89; engine.py:170, 228) -------
  * Every prefix of every inserted sequence is a key of an open-addressing
  * table holding the smallest insert epoch that reaches it (the radix tree's
