@@ -86,6 +86,19 @@ __device__ __forceinline__ void mma_bf16_ss_w(uint32_t d_tmem, uint32_t a_lo, ui
         : "memory");
 }
 
+// TS form: A from TMEM (a_tmem: column of the K-slice; rows duplicated across the lane
+// halves of each CTA), B from shared memory
+__device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t b_hi,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 b;\n\t"
+        "setp.ne.b32 p, %5, 0;\n\t"
+        "mov.b64 b, {%2, %3};\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], b, %4, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // arrive on the same mbarrier in both CTAs of the pair when the issued tcgen05 ops complete
 __device__ __forceinline__ void commit_both(uint64_t *bar) {
     asm volatile(

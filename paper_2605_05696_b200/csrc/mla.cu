@@ -608,13 +608,24 @@ namespace p2 {
 constexpr int PBN = 64;                     // keys per pair tile (QK N)
 constexpr int VPIECE = 32 * 128;            // 4 KB: 32 keys x 64 dims (SW128)
 constexpr int VTILE = 4 * VPIECE;           // V half-tile: 32 keys x this CTA's 256 latent dims
-constexpr int KST = 2, VST = 4;             // ring stages (V in half-tiles: PV(t) is two K=32 halves)
+#ifndef IRM_MLA_VST
+#define IRM_MLA_VST 4
+#endif
+constexpr int KST = 2, VST = IRM_MLA_VST;             // ring stages (V in half-tiles: PV(t) is two K=32 halves)
 constexpr int PTILE2 = 64 * 128;            // P [64 rows x 64 keys] bf16, SW128
-constexpr int S_Q = 0, S_K = NPIECE * QPIECE, S_V = S_K + KST * KTILE, S_P = S_V + VST * VTILE;
-constexpr int SMEM2 = S_P + 2 * PTILE2;     // 224 KB
+// Q pieces [0, QT) live in TMEM as the A operand of TS-mode QK MMAs (read by the tensor
+// core from TMEM, not shared memory); pieces [QT, 9) stay in shared memory (SS mode)
+#ifndef IRM_MLA_QT
+#define IRM_MLA_QT 6
+#endif
+constexpr int QT = IRM_MLA_QT;
+constexpr int S_Q = 0, S_K = (NPIECE - QT) * QPIECE, S_V = S_K + KST * KTILE, S_P = S_V + VST * VTILE;
+constexpr int SMEM2 = S_P + 2 * PTILE2;     // 224 KB - QT x 8 KB
 constexpr int W_KTMA = 8, W_MMA2 = 9, W_VTMA = 10;
 constexpr int THREADS2 = 32 * 11;
 constexpr uint32_t COL_S = 0, COL_O = 64;   // TMEM columns: S[2] x 32, O 2 x 128
+constexpr uint32_t COL_Q = 320;             // Q pieces [0, QT): 32 columns each (bf16 pairs)
+static_assert(COL_Q + 32 * QT <= 512, "TMEM holds at most 6 Q pieces next to S and O");
 
 __device__ __forceinline__ void arrive_leader(uint64_t *bar, uint32_t rank) {
     if (rank == 0) mbar_arrive(bar);
@@ -690,7 +701,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
     const int toff = (int)(((uint32_t)((blockIdx.x >> 1) / p.tgroup) * 2654435761u) % (uint32_t)T);
 
     if (threadIdx.x == 0) {
-        mbar_init(&b_q, 128);
+        mbar_init(&b_q, QT > 0 ? 256 : 128);  // smem Q (producers) + TMEM Q (softmax warps)
         mbar_init(&b_qpair, 1);
         for (int s = 0; s < KST; ++s) {
             // leader: its TMA expect_tx (both CTAs' c_KV bytes land here) + its rope group + the
@@ -720,11 +731,13 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         // ------------------------------------------------ Q (once) + rope of this CTA's 32 keys
         const int ptid = threadIdx.x - 128;
         const uint32_t qbase = smem_u32(smem + S_Q);
-        for (int i = ptid; i < 64 * 72; i += 128) {
-            const int r = i / 72, c = i % 72;
+        constexpr int QC = (NPIECE - QT) * 8;  // 16-byte chunks per row kept in smem
+        for (int i = ptid; i < 64 * QC; i += 128) {
+            const int r = i / QC, c = i % QC + QT * 8;
             const int64_t grow = row0 + r;
             const bool ok = grow < p.n_rows;
-            cp_async16(qbase + (c >> 3) * QPIECE + swz128(r, c & 7), p.q + (ok ? grow : 0) * DQK + c * 8, ok ? 16u : 0u);
+            cp_async16(qbase + ((c >> 3) - QT) * QPIECE + swz128(r, c & 7), p.q + (ok ? grow : 0) * DQK + c * 8,
+                       ok ? 16u : 0u);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         fence_proxy_async_smem();
@@ -848,9 +861,17 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 if (tc::elect_one()) {
                     // one 64-dim piece per iteration, descriptors advanced incrementally: a fully
                     // unrolled loop hoists all 72 descriptors into uniform registers and spills
-                    uint32_t qa = q_lo, kb = kd;
+                    uint32_t qa = q_lo, kb = kd, qt = tbase + COL_Q;
 #pragma unroll 1
-                    for (int pc = 0; pc < NPIECE; ++pc) {
+                    for (int pc = 0; pc < QT; ++pc) {  // A = Q from TMEM
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            tc2::mma_bf16_ts_w(ds, qt + 8 * k, kb + 2 * k, k_hi, idesc_qk, (pc | k) != 0);
+                        qt += 32;
+                        kb += KPIECE >> 4;
+                    }
+#pragma unroll 1
+                    for (int pc = QT; pc < NPIECE; ++pc) {  // A = Q from shared memory
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             tc2::mma_bf16_ss_w(ds, qa + 2 * k, q_hi, kb + 2 * k, k_hi, idesc_qk, (pc | k) != 0);
@@ -911,6 +932,28 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
         const uint32_t p_base = smem_u32(smem + S_P);
         const uint32_t pfull_leader0 = cl::map_to(smem_u32(&b_pfull[0]), 0);
         const uint32_t pfull_leader1 = cl::map_to(smem_u32(&b_pfull[1]), 0);
+        if constexpr (QT > 0) {
+            // this thread's row of Q, pieces [0, QT), into its TMEM lane (rows are duplicated
+            // across the lane halves: warps w and w + 2 hold the same rows, as the 2-SM TS
+            // A operand expects)
+            const uint4 *src = reinterpret_cast<const uint4 *>(p.q + (row_ok ? grow : 0) * DQK);
+#pragma unroll 1
+            for (int pc = 0; pc < QT; ++pc) {
+                uint32_t qv[32];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint4 x = row_ok ? __ldg(src + 8 * pc + j) : make_uint4(0, 0, 0, 0);
+                    qv[4 * j] = x.x;
+                    qv[4 * j + 1] = x.y;
+                    qv[4 * j + 2] = x.z;
+                    qv[4 * j + 3] = x.w;
+                }
+                tc2::st_32x32b_x32(lane_base + COL_Q + 32 * pc, qv);
+            }
+            tc::wait_st();
+            tc::fence_before();
+            mbar_arrive(&b_q);
+        }
         float m = -INFINITY, l = 0.f;
         long long c_s = 0, c_o = 0, c_x = 0, c_r = 0, c_e = 0, c_ld = 0, c_mx = 0, c_ex = 0, c0 = prof_clock<4>();
         for (int t = 0; t < T; ++t) {
@@ -1028,6 +1071,407 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
 
 }  // namespace p2
 
+// ============================================================================
+// v3: the CTA pair with V taken from the K tiles. Q pieces [0, QT3) in TMEM, 4 K stages,
+// 3 S buffers (QK runs two tiles ahead of PV), and per tile only the OTHER CTA's keys'
+// V pieces are loaded, straight into the K stage once QK(t) is done with it.
+namespace p3 {
+using namespace p2;
+#undef IRM_MLA_QT_V3
+constexpr int QT = 5;
+constexpr int KST = 4, NS = 3;
+constexpr int S_Q = 0, S_K = (NPIECE - QT) * QPIECE, S_P = S_K + KST * KTILE;
+constexpr int SMEM3 = S_P + 2 * PTILE2;  // 192 KB
+constexpr uint32_t COL_S = 0, COL_O = 32 * NS, COL_Q = COL_O + 256;
+static_assert(COL_Q + 32 * QT <= 512, "TMEM: S x 3, O, Q pieces");
+constexpr uint32_t FV_TX = 4 * KPIECE;  // foreign V bytes per CTA per tile
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
+mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
+                           const __grid_constant__ CUtensorMap tmap_tile, const __grid_constant__ CUtensorMap tmap_k8,
+                           const __grid_constant__ CUtensorMap tmap_k2) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t b_q, b_qpair, b_kfull[KST], b_krope[KST], b_qkdone[KST], b_vfull[KST],
+        b_kempty[KST], b_sfull[NS], b_pfull[2], b_odone[2];
+    __shared__ float sx[2][2][64];  // row-max exchange between the two key halves
+    __shared__ float sl[2][64];     // final row-sum exchange
+    __shared__ uint32_t tmem_base;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cl::cta_rank();
+    const int64_t prow0 = (int64_t)(blockIdx.x >> 1) * 128;  // first row of the pair
+    const int64_t row0 = prow0 + 64 * rank;                 // first row of this CTA
+    const int64_t last_row = min(p.n_rows, prow0 + 128) - 1;
+    const int64_t max_pos = p.q_pos0 + last_row / p.heads;
+    const int n_keys = (int)min((int64_t)p.n_kv, max_pos + 1);
+    const int T = (n_keys + PBN - 1) / PBN;
+    const int toff = (int)(((uint32_t)((blockIdx.x >> 1) / p.tgroup) * 2654435761u) % (uint32_t)T);
+
+    if (threadIdx.x == 0) {
+        mbar_init(&b_q, QT > 0 ? 256 : 128);  // smem Q (producers) + TMEM Q (softmax warps)
+        mbar_init(&b_qpair, 1);
+        for (int s = 0; s < KST; ++s) {
+            // leader: its TMA expect_tx (both CTAs' c_KV bytes land here) + its rope group + the
+            // peer's rope readiness (relayed); peer: b_krope collects its rope group
+            mbar_init(&b_kfull[s], 2 + GROUP);
+            mbar_init(&b_krope[s], GROUP);
+            mbar_init(&b_kempty[s], 1);
+        }
+        for (int s = 0; s < KST; ++s) {
+            mbar_init(&b_qkdone[s], 1);  // QK(t) done (multicast commit): the foreign V may overwrite
+            mbar_init(&b_vfull[s], 1);   // leader: its expect_tx; the peer's bytes complete here too
+        }
+        for (int s = 0; s < NS; ++s) mbar_init(&b_sfull[s], 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&b_pfull[s], rank == 0 ? 128 + 1 : 128);  // local softmax threads (+ the peer's relay)
+            mbar_init(&b_odone[s], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == W_MMA2) tc2::tmem_alloc(&tmem_base, 512);
+    tc::fence_before();
+    cl::cluster_sync();
+    tc::fence_after();
+    const uint32_t tbase = tmem_base;
+
+    if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------ Q (once) + rope of this CTA's 32 keys
+        const int ptid = threadIdx.x - 128;
+        const uint32_t qbase = smem_u32(smem + S_Q);
+        constexpr int QC = (NPIECE - QT) * 8;  // 16-byte chunks per row kept in smem
+        for (int i = ptid; i < 64 * QC; i += 128) {
+            const int r = i / QC, c = i % QC + QT * 8;
+            const int64_t grow = row0 + r;
+            const bool ok = grow < p.n_rows;
+            cp_async16(qbase + ((c >> 3) - QT) * QPIECE + swz128(r, c & 7), p.q + (ok ? grow : 0) * DQK + c * 8,
+                       ok ? 16u : 0u);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        fence_proxy_async_smem();
+        mbar_arrive(&b_q);
+        const int g = ptid / GROUP, gtid = ptid % GROUP;  // group g: tiles t = g (mod 2)
+        for (int t = g; t < T; t += 2) {
+            const int kt = (t + toff) % T, st = t % KST;
+            RopeRegs rr;
+            rope_fetch(p, 2 * kt + (int)rank, gtid, rr);  // keys kt*64 + 32*rank + [0, 32)
+            if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
+            store_rope(p, smem + S_K + st * KTILE, gtid, rr);
+            mbar_arrive(rank == 0 ? &b_kfull[st] : &b_krope[st]);
+        }
+    } else if (warp == W_KTMA) {
+        // ------------------------------------------------ c_KV of this CTA's 32 keys (QK operand)
+        long long c_e = 0, c0 = prof_clock<1>();
+        int row_next = key_row(p, (toff % T) * PBN + 32 * (int)rank + lane);  // rows read one tile ahead
+        for (int t = 0; t < T; ++t) {
+            const int st = t % KST;
+            const Rows32 rr = rows32_resolve(row_next, lane);
+            if (t + 1 < T) row_next = key_row(p, ((t + 1 + toff) % T) * PBN + 32 * (int)rank + lane);
+            long long a0 = prof_clock<1>();
+            if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
+            c_e += prof_clock<1>() - a0;
+            if (IRM_MLA_WHATIF == 3 && t >= KST) {
+                if (lane == 0 && rank == 0) mbar_arrive(&b_kfull[st]);
+                continue;
+            }
+            // both CTAs' c_KV bytes complete on the leader's b_kfull (peer: .cta_group::2 TMA)
+            if (rank == 0 && lane == 0) mbar_arrive_expect_tx(&b_kfull[st], 2 * CKV_TX);
+            __syncwarp();
+            const uint32_t dst = smem_u32(smem + S_K + st * KTILE);
+            const uint32_t kbar = cl::map_to(smem_u32(&b_kfull[st]), 0);
+            if (rr.contig) {  // one op for the 8 c_KV pieces of 32 consecutive rows
+                if (lane == 0) tma_load_3d_pair(dst, &tmap_k8, rr.row0, 0, kbar);
+            } else {
+                for (int pc = 0; pc < 8; ++pc)
+                    tma_rows32_pair(rr, &tmap_pool, &tmap_tile, dst + pc * KPIECE, pc, lane, kbar);
+            }
+        }
+        if (kProf && p.dbg && blockIdx.x < 2 && lane == 0)
+            printf("2sm-v3 ktma cta%d: wait_empty %lld total %lld\n", (int)rank, c_e, prof_clock<1>() - c0);
+    } else if (warp == W_VTMA) {
+        // ------------------------------------------------ foreign V: the other CTA's 32 keys x my dims
+        // PV over key half a reads, at K-stage slots 4h + 2a (+1), the half's own CTA's K pieces and,
+        // in the other CTA, the same keys' pieces of ITS latent dims. So once QK(t) no longer needs
+        // them, CTA r overwrites its slots 4h + 2(1 - r) (+1) with pieces 4h + 2r (+1) of the other
+        // CTA's keys: V is never loaded for the CTA's own keys (16 KB per tile instead of 32 KB)
+        int row_next = key_row(p, (toff % T) * PBN + 32 * (1 - (int)rank) + lane);
+        for (int t = 0; t < T; ++t) {
+            const int st = t % KST;
+            const Rows32 rr = rows32_resolve(row_next, lane);
+            if (t + 1 < T) row_next = key_row(p, ((t + 1 + toff) % T) * PBN + 32 * (1 - (int)rank) + lane);
+            mbar_wait(&b_qkdone[st], (t / KST) & 1);
+            if (rank == 0 && lane == 0) mbar_arrive_expect_tx(&b_vfull[st], 2 * FV_TX);
+            __syncwarp();
+            const uint32_t dst = smem_u32(smem + S_K + st * KTILE);
+            const uint32_t vbar = cl::map_to(smem_u32(&b_vfull[st]), 0);
+            const int src0 = 2 * (int)rank, dst0 = 2 * (1 - (int)rank);
+            if (rr.contig) {  // two ops: pieces src0 + {0, 1} and 4 + src0 + {0, 1}
+                if (lane == 0) {
+                    tma_load_3d_pair(dst + dst0 * KPIECE, &tmap_k2, rr.row0, src0, vbar);
+                    tma_load_3d_pair(dst + (4 + dst0) * KPIECE, &tmap_k2, rr.row0, 4 + src0, vbar);
+                }
+            } else {
+                for (int j = 0; j < 4; ++j) {
+                    const int off = (j >> 1) * 4 + (j & 1);
+                    tma_rows32_pair(rr, &tmap_pool, &tmap_tile, dst + (dst0 + off) * KPIECE, src0 + off, lane, vbar);
+                }
+            }
+        }
+    } else if (warp == W_MMA2) {
+        if (rank != 0) {
+            // ------------------------------------------------ peer: relay local data readiness to the leader
+            const uint32_t q_l = cl::map_to(smem_u32(&b_qpair), 0);
+            mbar_wait(&b_q, 0);
+            if (lane == 0) cl::remote_arrive(q_l);
+            auto relay_k = [&](int t) {  // the peer's rotated k_r is in smem
+                mbar_wait(&b_krope[t % KST], (t / KST) & 1);
+                if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_kfull[t % KST]), 0));
+            };
+            relay_k(0);
+            // forwarded in the leader's consumption order: K(t+1) for QK, then P(t) and V(t) for PV.
+            // A cluster-scope release costs ~1.5K cycles; doing it here keeps it off the softmax path.
+            for (int t = 0; t < T; ++t) {
+                if (t + 1 < T) relay_k(t + 1);
+                mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
+                if (lane == 0) cl::remote_arrive(cl::map_to(smem_u32(&b_pfull[t & 1]), 0));
+            }
+        } else {
+            // ------------------------------------------------ leader: MMA issue for the pair
+            const uint32_t idesc_qk = tc::idesc_bf16(128, PBN, false, false);
+            const uint32_t idesc_pv = tc::idesc_bf16(128, 256, false, true);
+            const uint64_t q_desc = tc::smem_desc_sw128(smem_u32(smem + S_Q), 16, 1024);
+            const uint64_t k_desc = tc::smem_desc_sw128(smem_u32(smem + S_K), 16, 1024);
+            const uint64_t kv_desc = tc::smem_desc_sw128(smem_u32(smem + S_K), KPIECE, 1024);  // MN-major view
+            const uint32_t kv_lo = (uint32_t)kv_desc, kv_hi = (uint32_t)(kv_desc >> 32);
+            const uint64_t p_desc = tc::smem_desc_sw128(smem_u32(smem + S_P), 16, 1024);
+            const uint32_t q_lo = (uint32_t)q_desc, q_hi = (uint32_t)(q_desc >> 32);
+            const uint32_t k_lo = (uint32_t)k_desc, k_hi = (uint32_t)(k_desc >> 32);
+            const uint32_t p_lo = (uint32_t)p_desc, p_hi = (uint32_t)(p_desc >> 32);
+            mbar_wait(&b_q, 0);
+            mbar_wait(&b_qpair, 0);
+            long long c_k = 0, c_kp = 0, c_p = 0, c_v = 0, c_vl = 0, c0 = prof_clock<2>();
+            auto issue_qk = [&](int t) {
+                const int st = t % KST;
+                long long a0 = prof_clock<2>();
+                mbar_wait(&b_kfull[st], (t / KST) & 1);  // both CTAs' K tiles (bytes + rope)
+                long long a1 = prof_clock<2>();
+                c_k += a1 - a0;
+                c_kp += prof_clock<2>() - a1;
+                tc::fence_after();
+                const uint32_t kd = k_lo + ((st * KTILE) >> 4);
+                const uint32_t ds = tbase + COL_S + (t % NS) * 32;
+                if (tc::elect_one()) {
+                    // one 64-dim piece per iteration, descriptors advanced incrementally: a fully
+                    // unrolled loop hoists all 72 descriptors into uniform registers and spills
+                    uint32_t qa = q_lo, kb = kd, qt = tbase + COL_Q;
+#pragma unroll 1
+                    for (int pc = 0; pc < QT; ++pc) {  // A = Q from TMEM
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            tc2::mma_bf16_ts_w(ds, qt + 8 * k, kb + 2 * k, k_hi, idesc_qk, (pc | k) != 0);
+                        qt += 32;
+                        kb += KPIECE >> 4;
+                    }
+#pragma unroll 1
+                    for (int pc = QT; pc < NPIECE; ++pc) {  // A = Q from shared memory
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            tc2::mma_bf16_ss_w(ds, qa + 2 * k, q_hi, kb + 2 * k, k_hi, idesc_qk, (pc | k) != 0);
+                        qa += QPIECE >> 4;
+                        kb += KPIECE >> 4;
+                    }
+                    tc2::commit_both(&b_sfull[t % NS]);
+                    tc2::commit_both(&b_qkdone[st]);
+                }
+                __syncwarp();
+            };
+            issue_qk(0);
+            if (T > 1) issue_qk(1);
+            for (int t = 0; t < T; ++t) {
+                if (t + 2 < T) issue_qk(t + 2);  // S(t+2) reuses the buffer softmax(t-1) has read
+                const int st = t % KST;
+                long long a0 = prof_clock<2>();
+                mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
+                long long a1 = prof_clock<2>();
+                c_p += a1 - a0;
+                mbar_wait(&b_vfull[st], (t / KST) & 1);  // both CTAs' foreign V in place
+                c_v += prof_clock<2>() - a1;
+                tc::fence_after();
+                const uint32_t pd = p_lo + (((t & 1) * PTILE2) >> 4);
+                const uint32_t kd = kv_lo + ((st * KTILE) >> 4);
+                if (tc::elect_one()) {
+#pragma unroll
+                    for (int a = 0; a < 2; ++a) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                            for (int k = 0; k < 2; ++k)
+                                tc2::mma_bf16_ss_w(tbase + COL_O + h * 128, pd + (((2 * a + k) * 32) >> 4), p_hi,
+                                                   kd + (((4 * h + 2 * a) * KPIECE + k * 2048) >> 4), kv_hi, idesc_pv,
+                                                   (t > 0 || a > 0 || k > 0) ? 1u : 0u);
+                        }
+                    }
+                    tc2::commit_both(&b_kempty[st]);
+                    tc2::commit_both(&b_odone[t & 1]);
+                }
+                __syncwarp();
+            }
+            if (kProf && p.dbg && blockIdx.x == 0 && lane == 0)
+                printf("2sm-v3 mma: wait_k %lld wait_kpair %lld wait_p %lld wait_v %lld (local %lld) total %lld T=%d\n", c_k, c_kp,
+                       c_p, c_v, c_vl, prof_clock<2>() - c0, T);
+        }
+    } else {
+        // ------------------------------------------------ softmax / correction (warps 0-3)
+        const int w = warp;
+        const int r = 32 * (w & 1) + lane;  // row of this CTA
+        const int kh = w >> 1;              // key half (S) / latent-dim half (O)
+        const int64_t grow = row0 + r;
+        const bool row_ok = grow < p.n_rows;
+        const int64_t qpos = p.q_pos0 + (row_ok ? grow / p.heads : 0);
+        const uint32_t lane_base = tbase + ((uint32_t)(32 * w) << 16);
+        const uint32_t p_base = smem_u32(smem + S_P);
+        const uint32_t pfull_leader0 = cl::map_to(smem_u32(&b_pfull[0]), 0);
+        const uint32_t pfull_leader1 = cl::map_to(smem_u32(&b_pfull[1]), 0);
+        if constexpr (QT > 0) {
+            // this thread's row of Q, pieces [0, QT), into its TMEM lane (rows are duplicated
+            // across the lane halves: warps w and w + 2 hold the same rows, as the 2-SM TS
+            // A operand expects)
+            const uint4 *src = reinterpret_cast<const uint4 *>(p.q + (row_ok ? grow : 0) * DQK);
+#pragma unroll 1
+            for (int pc = 0; pc < QT; ++pc) {
+                uint32_t qv[32];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint4 x = row_ok ? __ldg(src + 8 * pc + j) : make_uint4(0, 0, 0, 0);
+                    qv[4 * j] = x.x;
+                    qv[4 * j + 1] = x.y;
+                    qv[4 * j + 2] = x.z;
+                    qv[4 * j + 3] = x.w;
+                }
+                tc2::st_32x32b_x32(lane_base + COL_Q + 32 * pc, qv);
+            }
+            tc::wait_st();
+            tc::fence_before();
+            mbar_arrive(&b_q);
+        }
+        float m = -INFINITY, l = 0.f;
+        long long c_s = 0, c_o = 0, c_x = 0, c_r = 0, c_e = 0, c_ld = 0, c_mx = 0, c_ex = 0, c0 = prof_clock<4>();
+        for (int t = 0; t < T; ++t) {
+            long long a0 = prof_clock<4>();
+            mbar_wait(&b_sfull[t % NS], (t / NS) & 1);
+            c_s += prof_clock<4>() - a0;
+            tc::fence_after();
+            uint32_t v[32];
+            long long b0 = prof_clock<4>();
+            tc2::ld_32x32b_x32(lane_base + COL_S + (t % NS) * 32, v);
+            tc::wait_ld();
+            long long b1 = prof_clock<4>();
+            c_ld += b1 - b0;
+            const int64_t kbase = (int64_t)((t + toff) % T) * PBN + 32 * kh;
+            if (!__all_sync(0xffffffffu, row_ok && kbase + 31 <= qpos && kbase + 31 < p.n_kv)) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int64_t key = kbase + i;
+                    if (!(row_ok && key <= qpos && key < p.n_kv)) v[i] = NEG_INF_BITS;
+                }
+            }
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(v[i]));
+            float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
+            sx[t & 1][kh][r] = mt;  // exchange with the thread holding the other key half
+            long long a1 = prof_clock<4>();
+            c_mx += a1 - b1;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            c_x += prof_clock<4>() - a1;
+            mt = fmaxf(mt, sx[t & 1][kh ^ 1][r]);
+            float alpha = 1.f;
+            const float m_new = fmaxf(m, mt);
+            if (m_new > m + RESCALE_THRESHOLD) {
+                alpha = (m == -INFINITY) ? 0.f : ex2(m - m_new);
+                m = m_new;
+            }
+            const float nm = (m == -INFINITY) ? 0.f : -m;  // fully masked so far: every v is -inf
+            float ls[2] = {0.f, 0.f};
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+                const float e0 = ex2(fmaf(__uint_as_float(v[i]), p.scale_log2, nm));
+                const float e1 = ex2(fmaf(__uint_as_float(v[i + 1]), p.scale_log2, nm));
+                ls[(i >> 1) & 1] += e0 + e1;
+                pk[i >> 1] = pack_bf2(e0, e1);
+            }
+            l = l * alpha + (ls[0] + ls[1]);
+            long long a2 = prof_clock<4>();
+            c_ex += a2 - a1;
+            if (t >= 2) mbar_wait(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
+            c_o += prof_clock<4>() - a2;
+            long long a3 = prof_clock<4>();
+            if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
+                mbar_wait(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV(0..t-1)
+                tc::fence_after();
+#pragma unroll 1
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t o[32];
+                    const uint32_t a = lane_base + COL_O + (c >> 2) * 128 + (c & 3) * 32;
+                    tc2::ld_32x32b_x32(a, o);
+                    tc::wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    tc2::st_32x32b_x32(a, o);
+                }
+                tc::wait_st();
+            }
+            long long a4 = prof_clock<4>();
+            c_r += a4 - a3;
+            const uint32_t pt = p_base + (t & 1) * PTILE2;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                sts128(pt + swz128(r, 4 * kh + j), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
+            fence_proxy_async_smem();
+            tc::fence_before();
+            mbar_arrive(&b_pfull[t & 1]);  // local; the peer's relay forwards it to the leader
+            c_e += prof_clock<4>() - a4;
+        }
+        if (kProf && p.dbg && blockIdx.x < 2 && lane == 0 && w == 0)
+            printf("2sm-v3 softmax cta%d: wait_s %lld ld %lld mask %lld xchg+exp %lld wait_o %lld rescale %lld pstore %lld "
+                   "total %lld\n", (int)rank, c_s, c_ld, c_mx, c_ex, c_o, c_r, c_e, prof_clock<4>() - c0);
+        // epilogue: O / l -> bf16, lse (l summed over the two key halves)
+        sl[kh][r] = l;
+        mbar_wait(&b_odone[(T - 1) & 1], ((T - 1) >> 1) & 1);
+        tc::fence_after();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        l += sl[kh ^ 1][r];
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+            const int h = c >> 2, q = c & 3;
+            uint32_t o[32];
+            tc2::ld_32x32b_x32(lane_base + COL_O + h * 128 + q * 32, o);
+            tc::wait_ld();
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2)
+                pk[i >> 1] = pack_bf2(__uint_as_float(o[i]) * inv_l, __uint_as_float(o[i + 1]) * inv_l);
+            if (row_ok) {
+                uint4 *dst = reinterpret_cast<uint4 *>(p.out + grow * DV + 256 * h + 128 * kh + 32 * q);
+                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                dst[2] = make_uint4(pk[8], pk[9], pk[10], pk[11]);
+                dst[3] = make_uint4(pk[12], pk[13], pk[14], pk[15]);
+            }
+        }
+        if (row_ok && kh == 0 && p.lse) p.lse[grow] = (m + log2f(l)) * 0.69314718055994531f;
+    }
+    tc::fence_before();
+    cl::cluster_sync();
+    tc::fence_after();
+    if (warp == W_MMA2) tc2::tmem_dealloc(tbase, 512);
+}
+
+}  // namespace p3
+
+
 __global__ void cossin_kernel(const int64_t *__restrict__ delta, int64_t n_chunks,
                               const double *__restrict__ inv_freq, float2 *__restrict__ cs) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1108,7 +1552,7 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
     // multi-piece maps over the same rows as tmap_tile: [piece][row][64 cols], piece stride 128 B
     //   k8: 8 pieces (the c_KV part of a row), box {64, 32, 8}
     //   v4: pieces p + 4 g for p in [0, 4), g in [0, 2), box {64, 32, 2, 2}
-    CUtensorMap tmap_k8, tmap_v4;
+    CUtensorMap tmap_k8, tmap_v4, tmap_k2;
     {
         const cuuint64_t rows = (cuuint64_t)(kv_rows ? pool_rows : n_kv);
         const cuuint64_t dk[3] = {64, rows, 8};
@@ -1124,6 +1568,11 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
         const cuuint32_t ev[4] = {1, 1, 1, 1};
         if (cr == CUDA_SUCCESS)
             cr = encode(&tmap_v4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(pool), dv, sv, bv, ev,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const cuuint32_t b2[3] = {64, (cuuint32_t)mla::BN, 2};  // two adjacent pieces (v3 foreign V)
+        if (cr == CUDA_SUCCESS)
+            cr = encode(&tmap_k2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(pool), dk, sk, b2, ek,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) {
@@ -1148,6 +1597,18 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
     p.dbg = getenv("IRM_MLA_DEBUG") != nullptr;
     p.tgroup = getenv("IRM_MLA_TGROUP") ? atoi(getenv("IRM_MLA_TGROUP")) : 1;
     if (p.tgroup < 1) p.tgroup = 1;
+    // default: the CTA pair with V from the K tiles (v3); IRM_MLA_V2 = the pair with a separate
+    // V ring, IRM_MLA_1SM = the single-CTA kernel (both kept for comparison and tests)
+    if (getenv("IRM_MLA_1SM") == nullptr && getenv("IRM_MLA_V2") == nullptr) {
+        const int smem = mla::p3::SMEM3 + 1024;
+        IRM_CUDA_CHECK(cudaFuncSetAttribute(mla::p3::mla_reattach_2sm_v3_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        const int64_t grid = 2 * ((p.n_rows + 127) / 128);
+        mla::p3::mla_reattach_2sm_v3_kernel<<<(unsigned)grid, mla::p2::THREADS2, smem, (cudaStream_t)stream>>>(
+            p, tmap, tmap_tile, tmap_k8, tmap_k2);
+        IRM_LAUNCH_CHECK();
+        return IRM_OK;
+    }
     if (getenv("IRM_MLA_1SM") == nullptr) {  // CTA-pair (cta_group::2) kernel: 128 rows per cluster
         const int smem = mla::p2::SMEM2 + 1024;
         IRM_CUDA_CHECK(cudaFuncSetAttribute(mla::p2::mla_reattach_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -16,20 +16,22 @@ pytestmark = pytest.mark.gpu
 TOL = 4.7e-3
 
 
-@pytest.fixture(scope="module", params=["2sm", "1sm"])
+@pytest.fixture(scope="module", params=["2sm-v3", "2sm-v2", "1sm"])
 def ops(request):
-    """Both K5 kernels: the CTA-pair (cta_group::2, default) and the 1-SM one
-    (selected by IRM_MLA_1SM, read by the library on every call)."""
+    """All K5 kernels: the CTA pair with V from the K tiles (default), the CTA pair
+    with a separate V ring (IRM_MLA_V2) and the 1-SM one (IRM_MLA_1SM); the
+    library reads the selection on every call."""
     import os
 
     from paper_2605_05696_b200 import _native as N, ops
 
-    if request.param == "1sm":
-        os.environ["IRM_MLA_1SM"] = "1"
-    else:
-        os.environ.pop("IRM_MLA_1SM", None)
+    env = {"2sm-v3": {}, "2sm-v2": {"IRM_MLA_V2": "1"}, "1sm": {"IRM_MLA_1SM": "1"}}[request.param]
+    for k in ("IRM_MLA_V2", "IRM_MLA_1SM"):
+        os.environ.pop(k, None)
+    os.environ.update(env)
     yield ops, N
-    os.environ.pop("IRM_MLA_1SM", None)
+    for k in env:
+        os.environ.pop(k, None)
 
 
 def run_case(ops, N, n_kv, n_q, heads=16, q_pos0=None, rotate=False, paged=False, layout=0, q_gain=1.0, seed=0,
