@@ -366,6 +366,7 @@ def run_ours(args):
                          "launch_ms": k1, "tokens_per_launch": tok_per_wave,
                          "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm, "unit": "GB/s",
                                       "frac": k1_gbs / hbm}},
+            "cdc_hash_wide": cdc_wide_component(hbm),
             "fused_attn": fused_attn_component(args, tf_burst, peak_kind) if not args.no_attn else None,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo},
@@ -385,6 +386,40 @@ def run_sharded(pipe, n, load, wave0, graphs, after_front=None):
         pipe.run_overlapped(n, load, after_front=after_front, wave0=wave0)
     else:
         pipe.run_overlapped_sharded(n, load, wave0=wave0, k4_sms=K4_SMS, after_front=after_front)
+
+
+# ----------------------------------------------------------------- K1 with wide parallelism
+def cdc_wide_component(hbm, n_streams=296, n_tok=32768):
+    """K1 over a config-5-sized wave: 296 independent 32K-token session tails (2 per SM).
+    CDC is sequential within a pin-delimited region (one bit of carried state per
+    token, DESIGN.md K1), so K1's throughput is regions in flight x per-region rate;
+    the config-2 line above has only 8 long regions per wave."""
+    import torch
+
+    from paper_2605_05696_b200 import ops
+
+    rng = np.random.default_rng(21)
+    tok = torch.from_numpy(rng.integers(0, 2**32, size=n_streams * n_tok, dtype=np.uint64).astype(np.uint32)
+                           .view(np.int32)).cuda()
+    off = torch.arange(0, (n_streams + 1) * n_tok, n_tok, dtype=torch.int64, device="cuda")
+    ws = ops.CdcWorkspace()
+    run = lambda: ops.cdc_xxh64(tok, off, None, None, 7, 32, 512, True, ws=ws, n_tokens=tok.numel())
+    run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    a.record()
+    for _ in range(reps):
+        t = run()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    n_chunks = int(t.chunk_off[-1].item())
+    byt = tok.numel() * 4 + n_chunks * 24
+    return {"value": tok.numel() / (ms / 1e3), "unit": "tokens/s", "kernel": "irm_cdc_xxh64 (K1)",
+            "workload": f"{n_streams} streams x {n_tok} tokens (config-5 scale wave)", "launch_ms": ms,
+            "roofline": {"bound": "hbm", "achieved": byt / (ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": byt / (ms / 1e3) / 1e9 / hbm}}
 
 
 # ----------------------------------------------------------------- K5 component
