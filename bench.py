@@ -370,7 +370,10 @@ def run_ours(args):
             "fused_attn": fused_attn_component(args, tf_burst, peak_kind) if not args.no_attn else None,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo},
-        "gpu_launches": args.steps * 11,
+        # our kernels per wave (ncu launch list, profiles/r01e_launches.csv): K1 plan / offsets /
+        # region / compact, K3 claim / decide / blockscan / commit / resolve, K4 cossin + gather;
+        # sharded: + the replica map store's 5 and irm_copy_runs
+        "gpu_launches": args.steps * (17 if sharded else 11),
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu:
