@@ -66,7 +66,6 @@ struct Params {
     int64_t q_pos0;
     float scale_log2;         // softmax scale * log2(e)
     int dbg;                  // IRM_MLA_DEBUG: per-role cycle breakdown of CTA 0
-    int tgroup;               // pairs per shared key-tile order (IRM_MLA_TGROUP; 1 = every pair its own)
 };
 
 __device__ __forceinline__ uint32_t swz128(int row, int chunk) {  // SW128 byte offset (128-B rows)
@@ -217,27 +216,8 @@ __device__ __forceinline__ void store_rope(const Params &p, uint8_t *tile, int p
     fence_proxy_async_smem();
 }
 
-// L2 policy of the pool loads (IRM_MLA_HINT: 0 none, 1 evict_last): the pool is re-read by
-// every CTA pair, the Q / O streams are touched once
-#ifndef IRM_MLA_HINT
-#define IRM_MLA_HINT 0
-#endif
-__device__ __forceinline__ uint64_t pool_policy() {
-    uint64_t pol = 0;
-    if constexpr (IRM_MLA_HINT == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
 // BN consecutive pool rows x 64 columns -> one SW128 piece
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *tmap, int col, int row, uint64_t *bar) {
-    if constexpr (IRM_MLA_HINT != 0) {
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-            " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-            "l"(tmap), "r"(col), "r"(row), "r"(smem_u32(bar)), "l"(pool_policy())
-            : "memory");
-        return;
-    }
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
             dst),
@@ -297,14 +277,6 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
 // 4 arbitrary pool rows x 64 columns (128 B each) -> 512 B of a SW128 piece
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tmap, int col, int r0, int r1, int r2,
                                             int r3, uint64_t *bar) {
-    if constexpr (IRM_MLA_HINT != 0) {
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
-            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
-            "l"(tmap), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar)), "l"(pool_policy())
-            : "memory");
-        return;
-    }
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
@@ -713,7 +685,7 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
     const int64_t max_pos = p.q_pos0 + last_row / p.heads;
     const int n_keys = (int)min((int64_t)p.n_kv, max_pos + 1);
     const int T = (n_keys + PBN - 1) / PBN;
-    const int toff = (int)(((uint32_t)((blockIdx.x >> 1) / p.tgroup) * 2654435761u) % (uint32_t)T);
+    const int toff = (int)(((uint32_t)(blockIdx.x >> 1) * 2654435761u) % (uint32_t)T);
 
     if (threadIdx.x == 0) {
         mbar_init(&b_q, QT > 0 ? 256 : 128);  // smem Q (producers) + TMEM Q (softmax warps)
@@ -1121,7 +1093,7 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
     const int64_t max_pos = p.q_pos0 + last_row / p.heads;
     const int n_keys = (int)min((int64_t)p.n_kv, max_pos + 1);
     const int T = (n_keys + PBN - 1) / PBN;
-    const int toff = (int)(((uint32_t)((blockIdx.x >> 1) / p.tgroup) * 2654435761u) % (uint32_t)T);
+    const int toff = (int)(((uint32_t)(blockIdx.x >> 1) * 2654435761u) % (uint32_t)T);
 
     if (threadIdx.x == 0) {
         mbar_init(&b_q, QT > 0 ? 256 : 128);  // smem Q (producers) + TMEM Q (softmax warps)
@@ -1548,8 +1520,7 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
         return IRM_ECUDA;
     }
     CUtensorMap tmap, tmap_tile;
-    const int promo_env = getenv("IRM_MLA_PROMO") ? atoi(getenv("IRM_MLA_PROMO")) : 3;
-    const CUtensorMapL2promotion promo = (CUtensorMapL2promotion)(promo_env < 0 || promo_env > 3 ? 3 : promo_env);
+    const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // none / 64 / 128 B: no difference
     const cuuint64_t strides[1] = {(cuuint64_t)mla::DQK * 2};
     const cuuint32_t estr[2] = {1, 1};
     for (int which = 0; which < 2; ++which) {
@@ -1613,8 +1584,6 @@ extern "C" int irm_mla_reattach_prefill(const void *q, int64_t n_q, int32_t head
     p.q_pos0 = q_pos0;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.dbg = getenv("IRM_MLA_DEBUG") != nullptr;
-    p.tgroup = getenv("IRM_MLA_TGROUP") ? atoi(getenv("IRM_MLA_TGROUP")) : 1;
-    if (p.tgroup < 1) p.tgroup = 1;
     // default: the CTA pair with V from the K tiles (v3); IRM_MLA_V2 = the pair with a separate
     // V ring, IRM_MLA_1SM = the single-CTA kernel (both kept for comparison and tests)
     if (getenv("IRM_MLA_1SM") == nullptr && getenv("IRM_MLA_V2") == nullptr) {
