@@ -1072,6 +1072,11 @@ constexpr int SMEM3 = S_P + 2 * PTILE2;  // 192 KB
 constexpr uint32_t COL_S = 0, COL_O = 32 * NS, COL_Q = COL_O + 256;
 static_assert(COL_Q + 32 * QT <= 512, "TMEM: S x 3, O, Q pieces");
 constexpr uint32_t FV_TX = 4 * KPIECE;  // foreign V bytes per CTA per tile
+// CTA pairs per shared key-tile order (the walk starts at a hashed tile; any order is exact
+// under the online softmax)
+#ifndef IRM_MLA_TGRP
+#define IRM_MLA_TGRP 16
+#endif
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
 mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
@@ -1093,7 +1098,7 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
     const int64_t max_pos = p.q_pos0 + last_row / p.heads;
     const int n_keys = (int)min((int64_t)p.n_kv, max_pos + 1);
     const int T = (n_keys + PBN - 1) / PBN;
-    const int toff = (int)(((uint32_t)(blockIdx.x >> 1) * 2654435761u) % (uint32_t)T);
+    const int toff = (int)(((uint32_t)((blockIdx.x >> 1) / IRM_MLA_TGRP) * 2654435761u) % (uint32_t)T);
 
     if (threadIdx.x == 0) {
         mbar_init(&b_q, QT > 0 ? 256 : 128);  // smem Q (producers) + TMEM Q (softmax warps)
