@@ -104,3 +104,27 @@ def test_mla_validation(ops):
     kv = torch.zeros(8, 576, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError):
         o.mla_reattach_prefill(q, kv, 8, 6, 0.1)  # q_pos0 + n_q > n_kv
+
+
+def test_mla_vs_reference_materialize(ops):
+    """K5 on a reattached prompt whose k_r golden comes from the REFERENCE's
+    KvRegistry.materialize (tests/golden/mla.npz, make_golden.py): 4 cached documents
+    re-inserted in a permuted order (delta = p_dest - p_src per chunk), paged pool rows,
+    DSv3 half-split rotary theta 5e4; within the 4.7e-3 rel-L2 bound."""
+    from conftest import load_npz
+
+    o, N = ops
+    c = load_npz("mla")["case"]
+    q = torch.from_numpy(c["q_bf16"].view(np.int16)).view(torch.bfloat16).cuda()
+    pool = torch.from_numpy(c["pool"]).to(torch.bfloat16).cuda()
+    n_kv = c["kv_rows"].size
+    cs = o.chunk_cossin(torch.from_numpy(c["deltas"]).cuda(), o.inv_freq_device(O.make_inv_freq(float(c["theta"]))))
+    out, lse = o.mla_reattach_prefill(q, pool, n_kv, n_kv - q.shape[0], 192 ** -0.5,
+                                      kv_rows=torch.from_numpy(c["kv_rows"]).cuda(),
+                                      kv_chunk=torch.from_numpy(c["kv_chunk"]).cuda(), chunk_cs=cs,
+                                      layout=N.LAYOUT_HALF_SPLIT)
+    torch.cuda.synchronize()
+    ref = torch.from_numpy(c["out"]).double()
+    got = out.double().cpu()
+    assert float((got - ref).norm() / ref.norm()) <= TOL
+    assert float((lse.double().cpu() - torch.from_numpy(c["lse"])).abs().max()) <= 2e-2

@@ -148,3 +148,21 @@ def test_prefix_match_oracle_golden(case):
             continue
         m, w = O.prefix_match(inserted, seq)
         assert m == want_m[i] and (-1 if w is None else w) == want_w[i], (case, i)
+
+
+def test_mla_oracle_vs_reference_materialize():
+    """K5's fp64 restatement (oracle/mla_ref.py), on the bf16 inputs the kernel sees,
+    against attention over k_r rotated by the REFERENCE's KvRegistry.materialize
+    (tests/golden/mla.npz): within the 4.7e-3 bound (the gap is bf16 input rounding)."""
+    import torch
+
+    from oracle.mla_ref import mla_reattach_ref
+
+    c = load_npz("mla")["case"]
+    q = torch.from_numpy(c["q_bf16"].view(np.int16)).view(torch.bfloat16)
+    kv = torch.from_numpy(c["pool"][c["kv_rows"]]).to(torch.bfloat16)
+    out, lse = mla_reattach_ref(q, kv, kv.shape[0] - q.shape[0], 192 ** -0.5, c["deltas"][c["kv_chunk"]],
+                                O.make_inv_freq(float(c["theta"])))
+    ref = torch.from_numpy(c["out"]).double()
+    assert float((out - ref).norm() / ref.norm()) <= 4.7e-3
+    assert float((lse - torch.from_numpy(c["lse"])).abs().max()) <= 2e-2
