@@ -1,8 +1,10 @@
 """TEST INFRASTRUCTURE ONLY -- fp64 restatement of the fused reattach attention (K5).
 
 No reference implementation exists (the fused
-kernel is a "deliberate follow-up"); parity for K5 is therefore UNPINNED by
-the reference and this oracle restates the semantics from the paper:
+kernel is a "deliberate follow-up"); the attention is therefore UNPINNED by the
+reference and this oracle restates the semantics from the paper. Its rotation
+input is pinned: tests/golden/mla.npz (make_golden.py) feeds keys rotated by
+the reference's KvRegistry.materialize, checked in tests/test_oracle_golden.py.
   * absorbed MLA: attention runs on the 512-dim latent
     c_KV with the 64-dim decoupled rotary key, scores over the 576-wide key;
   * reattach: the cached k_r is kr_base rotated by
