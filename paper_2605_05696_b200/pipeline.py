@@ -127,6 +127,15 @@ class ReattachPipeline:
         all-to-alls between the kernels) but never wait for the host: every
         buffer is capacity-bounded, so the CPU runs ahead of the GPU."""
         self.sharded, self.replica, self.rank, self.world = sharded_store, replica_cache, rank, world
+        # the exchange has equal splits: every rank uses the largest chunk-table capacity
+        import torch.distributed as dist
+
+        k, mn, mx = self.params
+        cap = torch.tensor([max(int(N.lib().irm_cdc_chunk_bound(self.max_tokens, self.R, self.max_pins, mn)), 16)],
+                           dtype=torch.int64, device=self.pool.device)
+        if world > 1:
+            dist.all_reduce(cap, op=dist.ReduceOp.MAX, group=sharded_store.group)
+        sharded_store.slots = int(cap.item())
 
     def k3_sharded(self, wave: int):
         t = self.table

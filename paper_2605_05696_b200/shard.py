@@ -54,14 +54,18 @@ class ShardedStore:
     the same ``lookup_insert`` contract and an ``e_row`` entry array, e.g. a
     test dict store on CPU)."""
 
-    def __init__(self, local_store, novel_rows: int, group=None):
+    def __init__(self, local_store, novel_rows: int, group=None, slots: int | None = None):
         """novel_rows: rows [0, novel_rows) of every rank's latent pool hold the
         KV of chunks that rank writes first. Owner o hands out rows of the
         sub-range [o * novel_rows // G, (o + 1) * novel_rows // G) of each
         writer's pool, with one bump counter per writer, so a first writer's
-        rows are known in the same exchange that decides it is first."""
+        rows are known in the same exchange that decides it is first.
+        slots: queries per (rank, owner) bucket of the exchange; it must be the
+        same on every rank (the all-to-all has equal splits). None: the size of
+        each call's query array, which then must match across ranks."""
         self.local = local_store
         self.group = group
+        self.slots = slots
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         e_row = local_store.e_row
@@ -81,13 +85,15 @@ class ShardedStore:
         chunk). Returns (hit, p_src, row, owner); row is the global row
         (encode_row) of the entry's KV: for a novel query, where this rank must
         keep the chunk's KV (a row of its own pool, assigned by the owner).
-        No host synchronisation: every buffer has a fixed capacity of
-        q_fp.numel() slots per owner."""
+        No host synchronisation: every buffer has a fixed capacity of ``slots``
+        (default q_fp.numel()) queries per owner."""
         dev = q_fp.device
         n, G = q_fp.numel(), self.world
         i64 = dict(dtype=torch.int64, device=dev)
         probe = torch.ones(n, dtype=torch.bool, device=dev) if q_probe is None else q_probe.to(torch.bool)
-        cap = max(n, 1)
+        cap = self.slots if self.slots is not None else max(n, 1)
+        if n > cap:
+            raise ValueError(f"{n} queries exceed the exchange's {cap} slots per owner")
         own = torch.where(probe, owner_of(q_fp, G), torch.full_like(q_fp, G))  # bucket G: not probed
         perm = torch.argsort(own, stable=True)
         own_s = own[perm]

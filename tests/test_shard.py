@@ -134,3 +134,46 @@ def test_sharded_store_matches_sequential(seed):
     for ordk, i, rank, wave, k, h, ps, row, own in rows:
         if probe[i]:
             assert row == grow[first[int(fp[i])]], (i, row)  # every query reads its first writer's rows
+
+
+def _worker_uneven(rank, port, out_q):
+    """Ranks with different query counts per call: the exchange pads to a common slot count."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    from dict_store import DictStore
+
+    try:
+        g = torch.Generator().manual_seed(5)
+        fps = torch.randint(-(2**62), 2**62, (40,), generator=g, dtype=torch.int64)
+        n = 50 if rank == 0 else 70
+        q = fps[torch.randint(0, 40, (n,), generator=torch.Generator().manual_seed(10 + rank))]
+        order = torch.arange(n, dtype=torch.int64) * WORLD + rank
+        store = shard.ShardedStore(DictStore(), novel_rows=1 << 20, slots=80)
+        h, ps, row, own = store.lookup_insert(q, order, torch.arange(n) + 1000 * rank,
+                                              torch.full((n,), 4, dtype=torch.int32))
+        out_q.put((rank, q.tolist(), order.tolist(), h.tolist(), ps.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_store_uneven_batches():
+    from dict_store import DictStore
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_uneven, args=(r, port, q)) for r in range(WORLD)]
+    for pr in procs:
+        pr.start()
+    outs = [q.get(timeout=240) for _ in range(WORLD)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    rows = sorted((o, r, i, f, h, ps) for r, fs, orders, hs, pss in outs
+                  for i, (f, o, h, ps) in enumerate(zip(fs, orders, hs, pss)))
+    ref = DictStore()
+    for o, r, i, f, h, ps in rows:
+        eh, _, eps, _ = ref.lookup_insert(torch.tensor([f]), torch.tensor([o]), torch.tensor([i + 1000 * r]),
+                                          torch.tensor([4], dtype=torch.int32))
+        assert (h, ps) == (int(eh[0]), int(eps[0]))
