@@ -376,7 +376,7 @@ def run_ours(args):
         "gpu_launches": args.steps * (17 if sharded else 11),
         "clocks": clk.summary(),
     }
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU leg: rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline(args, packed[0], sample_requests=R - 1)
     if rank == 0:
         print(json.dumps(line))
