@@ -143,17 +143,24 @@ __device__ __forceinline__ void stage_tokens(const uint32_t *__restrict__ rt, in
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// G_t for tokens [tile_start, tile_start + RG_TILE) of a region into sGdst.
-__device__ __forceinline__ void produce_tile(const uint32_t *sTok, int32_t len, int32_t tile_start,
-                                             const uint64_t *__restrict__ gear, uint64_t *sGdst,
-                                             const uint64_t *sGprev, uint64_t *sS31, int pw, int lane) {
-    uint64_t g[RG_PER];
+// gear values g_t of this producer thread's tokens of a tile (the L2 lookups are issued one
+// tile ahead of their use, so their latency hides under the previous tile's scan)
+__device__ __forceinline__ void load_gear(const uint32_t *sTok, int32_t len, int32_t tile_start,
+                                          const uint64_t *__restrict__ gear, int pw, int lane,
+                                          uint64_t (&g)[RG_PER]) {
 #pragma unroll
     for (int q = 0; q < RG_PER; ++q) {
         const int c = pw + q * RG_PRODUCERS;
         const int32_t t = tile_start + c * 32 + lane;
         g[q] = (c < RG_SUB && t < len) ? __ldg(gear + (sTok[c * 32 + lane] & 0xFFFFu)) : 0ULL;
     }
+}
+
+// G_t for tokens [tile_start, tile_start + RG_TILE) of a region into sGdst, from the tile's
+// gear values g (load_gear).
+__device__ __forceinline__ void produce_tile(uint64_t (&g)[RG_PER], int32_t len, int32_t tile_start,
+                                             uint64_t *sGdst, const uint64_t *sGprev, uint64_t *sS31, int pw,
+                                             int lane) {
     // in-block windowed scan S_j = sum_{i<=j} g_i << (j-i), Kogge-Stone through
     // shared memory: the warp-shuffle unit is left to the chain/cand warps'
     // votes, which sit on the CTA's critical path
@@ -213,10 +220,18 @@ __device__ __forceinline__ void chain_tile(const uint64_t *sG, uint32_t *sBm, in
     const uint32_t Blo0 = Blo, Bhi0 = Bhi;
     uint32_t myW = 0;  // lane s keeps W_s
     bool amb = false;  // per lane: some step's high word sat at a carry boundary
-    uint32_t Ghn = (uint32_t)(sG[j] >> 32);
+    // G's high words are read CH_AHEAD steps ahead: the producers keep shared memory busy,
+    // so one step of lead does not cover the load latency
+    constexpr int CH_AHEAD = 4;
+    uint32_t Gq[CH_AHEAD];
+#pragma unroll
+    for (int a = 0; a < CH_AHEAD; ++a) Gq[a] = a < nsteps ? (uint32_t)(sG[a * 32 + j] >> 32) : 0u;
+#pragma unroll CH_AHEAD
     for (int s = 0; s < nsteps; ++s) {
-        const uint32_t Ghi = Ghn;
-        if (s + 1 < nsteps) Ghn = (uint32_t)(sG[(s + 1) * 32 + j] >> 32);
+        const uint32_t Ghi = Gq[0];
+#pragma unroll
+        for (int a = 0; a + 1 < CH_AHEAD; ++a) Gq[a] = Gq[a + 1];
+        Gq[CH_AHEAD - 1] = s + CH_AHEAD < nsteps ? (uint32_t)(sG[(s + CH_AHEAD) * 32 + j] >> 32) : 0u;
         const uint32_t hs = Ghi + __funnelshift_l(Blo, Bhi, j);  // high word of h, carry c in {0,1,2} pending
         const unsigned W = __ballot_sync(0xffffffffu, hs >> 31);
         amb |= (hs & 0x7FFFFFFEu) == 0x7FFFFFFEu;  // (past-the-end lanes may trigger a harmless redo)
@@ -350,9 +365,13 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
     // role warps take the HIGHEST warp ids: the SMSP arbiter issues
     // highest-warp-id-first, so the chain warp is never starved by producers
     const int pw = warp, ptid = threadIdx.x;
+    uint64_t gcur[RG_PER];  // producers: gear values of the tile being scanned
     if (warp < W_WALK) {
         stage_tokens(rt, R.len, 0, sTok[0], ptid);
         stage_tokens(rt, R.len, 1, sTok[1], ptid);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // tile 0's tokens landed
+        producer_bar();
+        load_gear(sTok[0], R.len, 0, gear, pw, lane, gcur);
     }
     long long t_work = 0, t_all = clock64();
     for (int i = 0; i <= ntiles + 2; ++i) {
@@ -370,10 +389,13 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
                           nch, sink, lane);
         } else if (i < ntiles && !(dbg & 2)) {
             stage_tokens(rt, R.len, i + 2, sTok[(i + 2) % 3], ptid);  // empty group past the end
-            asm volatile("cp.async.wait_group 2;" ::: "memory");       // tile i's tokens landed
+            asm volatile("cp.async.wait_group 1;" ::: "memory");       // tile i + 1's tokens landed
             producer_bar();
-            produce_tile(sTok[i % 3], R.len, i * RG_TILE, gear, sG[i % 3], i ? sG[(i - 1) % 3] : nullptr,
-                         sS31, pw, lane);
+            uint64_t gnext[RG_PER];
+            load_gear(sTok[(i + 1) % 3], R.len, (i + 1) * RG_TILE, gear, pw, lane, gnext);  // in flight
+            produce_tile(gcur, R.len, i * RG_TILE, sG[i % 3], i ? sG[(i - 1) % 3] : nullptr, sS31, pw, lane);
+#pragma unroll
+            for (int q = 0; q < RG_PER; ++q) gcur[q] = gnext[q];
         }
         t_work += clock64() - t0;
         __syncthreads();
@@ -401,7 +423,7 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
                                             0, lane);
         if (ok && (lane & 3) == 0) st_fp[cap + c] = h;
     }
-    if (dbg && (threadIdx.x & 31) == 0 && (warp >= W_WALK || warp == 0) && R.len > 10000)  // IRM_CDC_DEBUG=1
+    if (dbg && (threadIdx.x & 31) == 0 && (warp >= W_WALK || warp == 0 || warp == 3) && R.len > 10000)  // IRM_CDC_DEBUG=1
         printf("region %lld warp %d work %lld loop %lld with-hash %lld tiles %d\n", (long long)r, warp,
                t_work, t_loop, clock64() - t_all, ntiles);
 }
