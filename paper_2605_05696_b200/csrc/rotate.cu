@@ -274,8 +274,9 @@ static int launch_gather(const GatherArgs &a, void *ws, const int64_t *delta, co
     }
     const bool tma_ok = (a.row_bytes % 16 == 0) && (((uintptr_t)a.pool | (uintptr_t)a.out) % 16 == 0);
     if (tma_ok) {
-        // rows per tile so that one pipeline stage is ~18 KB
-        const int rows_fit = 18432 / a.row_bytes;
+        // rows per tile so that one pipeline stage is ~36 KB (4 stages: 144 KB, one CTA per SM;
+        // 18 KB stages with 3 CTAs per SM ran 2-5 % slower, tools/k4_tune.py)
+        const int rows_fit = 36864 / a.row_bytes;
         if (const char *v = getenv("IRM_RG_VARIANT")) {  // tuning hook: rows x stages
             const int var = atoi(v);
             if (var == 1) return launch_tma<T, 8, 8>(a, cs, st);
@@ -284,6 +285,11 @@ static int launch_gather(const GatherArgs &a, void *ws, const int64_t *delta, co
             if (var == 4) return launch_tma<T, 32, 4>(a, cs, st);
             if (var == 5) return launch_tma<T, 8, 12>(a, cs, st);
             if (var == 6) return launch_tma<T, 16, 8>(a, cs, st);
+            if (var == 7) return launch_tma<T, 32, 5>(a, cs, st);
+            if (var == 8) return launch_tma<T, 32, 6>(a, cs, st);
+            if (var == 9) return launch_tma<T, 64, 3>(a, cs, st);
+            if (var == 10) return launch_tma<T, 48, 4>(a, cs, st);
+            if (var == 11) return launch_tma<T, 24, 6>(a, cs, st);
         }
         if (rows_fit >= 32) return launch_tma<T, 32>(a, cs, st);
         if (rows_fit >= 16) return launch_tma<T, 16>(a, cs, st);

@@ -15,7 +15,7 @@ dst = torch.from_numpy(np.concatenate([[0], np.cumsum(lens[:-1])]).astype(np.int
 ln = torch.from_numpy(lens).cuda()
 delta = torch.from_numpy(rng.integers(-5000, 5000, size=lens.size)).cuda()
 inv = ops.inv_freq_device(np.power(1e4, -2.0 * np.arange(32) / 64))
-for v in ["0", "1", "2", "3", "4", "5", "6"]:
+for v in sys.argv[1:] or ["0", "1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11"]:
     if v == "0":
         os.environ.pop("IRM_RG_VARIANT", None)
     else:
