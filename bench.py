@@ -230,7 +230,20 @@ def run_ours(args):
     # (eager streams when the backend cannot be captured, e.g. the gloo one-device check)
     graphs = not sharded or backend == "nccl"
     if overlapped and sharded and graphs:
-        pipe.capture_overlapped(k4_sms=K4_SMS, sharded=True)
+        try:
+            pipe.capture_overlapped(k4_sms=K4_SMS, sharded=True)
+        except Exception as e:  # keep the N-rank run alive on the stream pipeline (same results)
+            print(f"bench: sharded graph capture failed ({type(e).__name__}: {e}); running on streams",
+                  file=sys.stderr)
+            graphs = False
+            pipe.wave_t = None
+            torch.cuda.synchronize()
+        if world > 1:  # every rank must take the same path
+            ok = torch.tensor([1 if graphs else 0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0 and graphs:
+                graphs = False
+                pipe.wave_t = None
     if overlapped and sharded:
         run_sharded(pipe, args.warmup, lambda i: pipe.load(*dev_in[i]), n_steps + 2, graphs)
     torch.cuda.synchronize()
