@@ -326,11 +326,12 @@ def run_ours(args):
         def d2h(i, slot):  # D2H of wave i's per-chunk service result
             res[i].copy_(pipe.slots[slot]["hit"], non_blocking=True)
 
-        if sharded:
-            run_sharded(pipe, args.steps, lambda i: pipe.load(*host_in[args.warmup + i]), 3 * n_steps + 6,
-                        graphs, after_front=d2h)
-        else:
-            pipe.run_overlapped(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]), after_front=d2h)
+        if sharded and not graphs:
+            pipe.run_overlapped_sharded(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]),
+                                        wave0=3 * n_steps + 6, k4_sms=K4_SMS, after_front=d2h)
+        else:  # the service maps come back on a side stream (readback), off the critical path
+            pipe.run_overlapped(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]), readback=res,
+                                wave0=3 * n_steps + 6)
         bo = pipe.slots[0]["hit"].numel() * pipe.slots[0]["hit"].element_size()
     else:
         for i in range(args.steps):

@@ -326,13 +326,17 @@ class ReattachPipeline:
         torch.cuda.synchronize()
         self.hit_tokens.zero_()
 
-    def run_overlapped(self, n_waves: int, load_wave, after_front=None, after_k4=None, wave0: int = 0):
+    def run_overlapped(self, n_waves: int, load_wave, after_front=None, after_k4=None, wave0: int = 0,
+                       readback=None):
         """Process waves 0..n_waves-1 through the two-wave pipeline.
         ``load_wave(i)`` copies wave i's inputs into the static buffers (called on
         the current stream, after the previous graph that read them);
         ``after_front(i, slot)`` is called once wave i's lookup results are in
         ``slots[slot]`` (stream-ordered), e.g. to read the service map back;
         ``after_k4(i, slot)`` once wave i's KV is in ``slots[slot]["out"]``.
+        ``readback[i]`` (pinned host tensors, optional): wave i's per-chunk
+        service map is copied there on a side stream, off the step's critical
+        path; the graph that next overwrites the slot waits for the copy.
         Sharded graphs number the waves ``wave0 + i`` in the global order key."""
         if n_waves <= 0:
             return
@@ -340,26 +344,44 @@ class ReattachPipeline:
         if getattr(self, "wave_t", None) is not None:
             self.wave_t.fill_(wave0)
         loader = _Loader(self, load_wave)
+        if readback is not None and getattr(self, "_d2h", None) is None:
+            self._d2h = torch.cuda.Stream()
+        rb_done = [None, None]
+
+        def read(j, slot):  # D2H of wave j's service map, after the graph that wrote it
+            if readback is not None:
+                ev = torch.cuda.Event()
+                ev.record(main)
+                self._d2h.wait_event(ev)
+                with torch.cuda.stream(self._d2h):
+                    readback[j].copy_(self.slots[slot]["hit"], non_blocking=True)
+                    rb_done[slot] = torch.cuda.Event()
+                    rb_done[slot].record(self._d2h)
+            if after_front:
+                after_front(j, slot)
+
         loader.load(0, main)
         self.g_front[0].replay()
         loader.read_done(0, main)
-        if after_front:
-            after_front(0, 0)
+        read(0, 0)
         if n_waves > 1:
             loader.load(1, main)
         for i in range(n_waves):
             s = i & 1
             if i + 1 < n_waves:
+                if rb_done[1 - s] is not None:
+                    main.wait_event(rb_done[1 - s])  # slot 1 - s is rewritten by this graph
                 self.g_overlap[s].replay()  # K4(i) || K1 + K3(i + 1) -> slot 1 - s
                 loader.read_done(i + 1, main)
                 if i + 2 < n_waves:
                     loader.load(i + 2, main)  # H2D under the next graph (other input set)
-                if after_front:
-                    after_front(i + 1, 1 - s)
+                read(i + 1, 1 - s)
             else:
                 self.g_drain[s].replay()
             if after_k4:
                 after_k4(i, s)
+        if readback is not None:
+            main.wait_stream(self._d2h)
 
     def load(self, tok, stream_off, pin_off, pins, m):
         """Copy one wave's inputs (device-resident or pinned host) into the static

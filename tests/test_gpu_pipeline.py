@@ -149,13 +149,17 @@ def test_pipeline_overlapped_matches_oracle(setup):
     torch.cuda.synchronize()
     pipe.capture_overlapped(k4_sms=100)
     hits, outs = {}, {}
+    # service maps read back on the pipeline's side stream (the e2e path of bench.py)
+    rb = [torch.empty(pipe.slots[0]["hit"].shape, dtype=pipe.slots[0]["hit"].dtype, pin_memory=True)
+          for _ in range(WAVES)]
     pipe.run_overlapped(WAVES, lambda i: pipe.load(*dev[1 + i]),
                         after_front=lambda i, s: hits.__setitem__(i, pipe.slots[s]["hit"].clone()),
-                        after_k4=lambda i, s: outs.__setitem__(i, pipe.slots[s]["out"].clone()))
+                        after_k4=lambda i, s: outs.__setitem__(i, pipe.slots[s]["out"].clone()), readback=rb)
     torch.cuda.synchronize()
     n_tok = 0
     for i in range(WAVES):
         check_wave(S, 1 + i, hits[i].cpu().numpy(), outs[i].cpu())
+        assert torch.equal(rb[i], hits[i].cpu())
         n_tok += sum(r[4] for r in S["ref"][1 + i] if r[0] == 1)
     assert int(pipe.hit_tokens.item()) == n_tok
 
