@@ -3,7 +3,6 @@ golden chunk tables and the oracle. Bit-exact (start, len, fp, forced)."""
 
 import numpy as np
 import pytest
-import torch
 
 from inputs import CDC_CASES, cdc_case_inputs
 from oracle import oracle as O

@@ -1,5 +1,5 @@
 """K4 (bf16, config-2 sized) HBM bandwidth vs the number of SMs it spreads over (irm_rotate_gather_set_sm_limit)."""
-import os, sys
+import sys
 import numpy as np, torch
 sys.path.insert(0, ".")
 from paper_2605_05696_b200 import ops

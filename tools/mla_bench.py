@@ -6,7 +6,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
-from paper_2605_05696_b200 import _native as N, ops  # noqa: E402
+from paper_2605_05696_b200 import ops  # noqa: E402
 
 
 def main(n_kv=65536, n_q=4096, heads=16, reps=5, theta=5e4):
