@@ -1066,9 +1066,16 @@ namespace p3 {
 using namespace p2;
 #undef IRM_MLA_QT_V3
 constexpr int QT = 5;
-constexpr int KST = 4, NS = 3;
+#ifndef IRM_MLA_V3_KST
+#define IRM_MLA_V3_KST 4
+#endif
+#ifndef IRM_MLA_V3_NP
+#define IRM_MLA_V3_NP 2
+#endif
+constexpr int KST = IRM_MLA_V3_KST, NS = 3;
+constexpr int NP = IRM_MLA_V3_NP;  // P buffers: 1 frees smem for a fifth K stage
 constexpr int S_Q = 0, S_K = (NPIECE - QT) * QPIECE, S_P = S_K + KST * KTILE;
-constexpr int SMEM3 = S_P + 2 * PTILE2;  // 192 KB
+constexpr int SMEM3 = S_P + NP * PTILE2;  // 192 KB (4 K stages, 2 P buffers)
 constexpr uint32_t COL_S = 0, COL_O = 32 * NS, COL_Q = COL_O + 256;
 static_assert(COL_Q + 32 * QT <= 512, "TMEM: S x 3, O, Q pieces");
 constexpr uint32_t FV_TX = 4 * KPIECE;  // foreign V bytes per CTA per tile
@@ -1289,7 +1296,7 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
                 mbar_wait(&b_vfull[st], (t / KST) & 1);  // both CTAs' foreign V in place
                 c_v += prof_clock<2>() - a1;
                 tc::fence_after();
-                const uint32_t pd = p_lo + (((t & 1) * PTILE2) >> 4);
+                const uint32_t pd = p_lo + ((((t & 1) % NP) * PTILE2) >> 4);
                 const uint32_t kd = kv_lo + ((st * KTILE) >> 4);
                 if (tc::elect_one()) {
 #pragma unroll
@@ -1399,7 +1406,8 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
             l = l * alpha + (ls[0] + ls[1]);
             long long a2 = prof_clock<4>();
             c_ex += a2 - a1;
-            if (t >= 2) mbar_wait(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
+            if (NP == 2 && t >= 2) mbar_wait(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
+            if (NP == 1 && t >= 1) mbar_wait(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);  // PV(t-1) read P
             c_o += prof_clock<4>() - a2;
             long long a3 = prof_clock<4>();
             if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
@@ -1419,7 +1427,7 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
             }
             long long a4 = prof_clock<4>();
             c_r += a4 - a3;
-            const uint32_t pt = p_base + (t & 1) * PTILE2;
+            const uint32_t pt = p_base + ((t & 1) % NP) * PTILE2;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 sts128(pt + swz128(r, 4 * kh + j), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
