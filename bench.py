@@ -382,6 +382,10 @@ def run_ours(args):
                                       "frac": k1_gbs / hbm}},
             "cdc_hash_wide": cdc_wide_component(hbm),
             "fused_attn": fused_attn_component(args, tf_burst, peak_kind) if not args.no_attn else None,
+            # the north star's "DeepSeek-V2-Lite shapes": config 2's 32K context, DSv2 interleaved rotary
+            "fused_attn_dsv2": fused_attn_component(args, tf_burst, peak_kind, n_ctx=32768, n_q=4096, theta=1e4,
+                                                    layout=N.LAYOUT_INTERLEAVED, shape="config 2")
+            if not args.no_attn else None,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo},
         # our kernels per wave (ncu launch list, profiles/r01e_launches.csv): K1 plan / offsets /
@@ -440,7 +444,8 @@ def cdc_wide_component(hbm, n_streams=296, n_tok=32768):
 
 
 # ----------------------------------------------------------------- K5 component
-def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=16, theta=5e4):
+def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=16, theta=5e4, layout=None,
+                         shape="config 3"):
     """BASELINE.json config 3 (Moonlight-16B-A3B shape, DSv3-form half-split
     rotary, theta 5e4): a 64K-token prompt = 512-token prefix + 63 marker-wrapped
     1K-token documents re-permuted relative to the cached order (the rerank
@@ -454,7 +459,9 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
     from paper_2605_05696_b200 import _native as N, ops
 
     rng = np.random.default_rng(35)
-    doc, n_docs, prefix = 960, 63, 512  # 63 x (960 + 64-token marker) + 512 = 65,024; 512 novel tail
+    layout = N.LAYOUT_HALF_SPLIT if layout is None else layout
+    doc, prefix = 960, 512  # 1K-token documents (960 + 64-token marker) after a 512-token prefix
+    n_docs = (n_ctx - prefix - 512) // (doc + 64)  # 63 at 64K (65,024 tokens + a 512-token novel tail)
     seg = doc + 64
     src_start = prefix + np.arange(n_docs) * seg  # cached layout
     perm = rng.permutation(n_docs)
@@ -476,14 +483,14 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
     rows_d = torch.from_numpy(kv_rows.astype(np.int32)).to(dev)
     chunk_d = torch.from_numpy(chunk_of_key).to(dev)
     out, lse = ops.mla_reattach_prefill(q, pool, n_ctx, n_ctx - n_q, 192 ** -0.5, kv_rows=rows_d,
-                                        kv_chunk=chunk_d, chunk_cs=cs, layout=N.LAYOUT_HALF_SPLIT)
+                                        kv_chunk=chunk_d, chunk_cs=cs, layout=layout)
     torch.cuda.synchronize()
     reps = 5
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps):
         ops.mla_reattach_prefill(q, pool, n_ctx, n_ctx - n_q, 192 ** -0.5, kv_rows=rows_d, kv_chunk=chunk_d,
-                                 chunk_cs=cs, layout=N.LAYOUT_HALF_SPLIT, out=out, lse=lse)
+                                 chunk_cs=cs, layout=layout, out=out, lse=lse)
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
@@ -491,8 +498,9 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
     flops = heads * float((pos + 1).sum()) * 2176  # (2*576 + 2*512) per visible (query, key, head)
     tflops = flops / (ms / 1e3) / 1e12
     return {"value": tflops, "unit": "TFLOP/s", "kernel": "irm_mla_reattach_prefill (K5, tcgen05/TMEM)",
-            "workload": f"config 3: {n_ctx} ctx, last {n_q} queries, {heads} heads, 63 re-permuted docs, "
-                        "DSv3 half-split theta 5e4, bf16", "launch_ms": ms, "flop_per_launch": flops,
+            "workload": f"{shape}: {n_ctx} ctx, last {n_q} queries, {heads} heads, {n_docs} re-permuted docs, "
+                        f"{'DSv2 interleaved' if layout == N.LAYOUT_INTERLEAVED else 'DSv3 half-split'} theta {theta:g}, bf16",
+            "launch_ms": ms, "flop_per_launch": flops,
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": tf_peak, "unit": "TFLOP/s",
                          "frac": tflops / tf_peak, "peak_kind": f"{peak_kind} bf16 burst"}}
 
