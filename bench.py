@@ -482,6 +482,11 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
     cs = ops.chunk_cossin(torch.tensor(deltas, dtype=torch.int64, device=dev), inv)
     rows_d = torch.from_numpy(kv_rows.astype(np.int32)).to(dev)
     chunk_d = torch.from_numpy(chunk_of_key).to(dev)
+    # start from an idle GPU (1 s): the power-managed clocks after the HBM-bound step or the
+    # previous component otherwise lower the first launches (1246 vs 1395 TFLOP/s measured at
+    # 32K right after a 64K run); the peak it is compared with is the burst figure too
+    torch.cuda.synchronize()
+    time.sleep(1.0)
     out, lse = ops.mla_reattach_prefill(q, pool, n_ctx, n_ctx - n_q, 192 ** -0.5, kv_rows=rows_d,
                                         kv_chunk=chunk_d, chunk_cs=cs, layout=layout)
     torch.cuda.synchronize()
