@@ -105,12 +105,19 @@ def check(rc: int, what: str = "") -> None:
     raise RuntimeError(f"{what}: CUDA error: {msg}")
 
 
+_cuda_ok = False
+
+
 def require_cuda():
+    global _cuda_ok
+    if _cuda_ok:  # checked once: torch.cuda.is_available() costs milliseconds per call
+        return
     import torch
 
     if not torch.cuda.is_available():
         raise RuntimeError("irminsul_b200 requires a CUDA device (B200, sm_100a); no CPU fallback")
     lib()
+    _cuda_ok = True
 
 
 def stream_ptr(stream=None):

@@ -68,17 +68,38 @@ class _SynthCache:
                 np.stack([self._rows[t][1] for t in tokens]))
 
 
-@dataclass(frozen=True)
 class RegistryEntry:
-    fingerprint: int
-    c_kv: np.ndarray
-    kr_base: np.ndarray
-    p_src: int
-    insert_epoch: int
+    """registry.py:73-84. ``c_kv`` / ``kr_base`` are produced on first use: the
+    synthetic prefill rows (PCG64 per token, registry.py:37-54) and their pool
+    write + rotation to p_src happen when something reads them (an attribute
+    access, materialize, the live tripwire), so observer-mode serving never pays
+    for KV it does not look at. The values are the same as an eager insert's."""
+
+    __slots__ = ("fingerprint", "p_src", "insert_epoch", "_reg", "_tokens", "_c_kv", "_kr_base")
+
+    def __init__(self, fingerprint: int, p_src: int, insert_epoch: int, reg, tokens, c_kv=None, kr_base=None):
+        self.fingerprint, self.p_src, self.insert_epoch = fingerprint, p_src, insert_epoch
+        self._reg, self._tokens, self._c_kv, self._kr_base = reg, tokens, c_kv, kr_base
+
+    @property
+    def c_kv(self) -> np.ndarray:
+        if self._c_kv is None:
+            self._reg._flush()
+        return self._c_kv
+
+    @property
+    def kr_base(self) -> np.ndarray:
+        if self._kr_base is None:
+            self._reg._flush()
+        return self._kr_base
 
     @property
     def chunk_len(self) -> int:
-        return self.kr_base.shape[0]
+        return len(self._tokens)
+
+    def __repr__(self) -> str:
+        return f"RegistryEntry(fingerprint={self.fingerprint:#x}, p_src={self.p_src}, len={self.chunk_len}, " \
+               f"insert_epoch={self.insert_epoch})"
 
 
 @dataclass
@@ -121,6 +142,7 @@ class KvRegistry:
         self._rows_used = 0
         self._order = 0
         self._gather_ws = None
+        self._pending: list[RegistryEntry] = []  # entries whose rows are not written yet
 
     # ------------------------------------------------------------ queries
     def __len__(self) -> int:
@@ -162,41 +184,49 @@ class KvRegistry:
         return self.commit_rows(fp, tokens, p_src, r)
 
     def commit_rows(self, fp: int, tokens: Sequence[int], p_src: int, row: int) -> RegistryEntry:
-        """Producer side: write synthetic prefill rows at pool row ``row`` and
-        rotate k_r to p_src + i on the device (registry.py:131-136)."""
-        n = len(tokens)
-        c_kv, kr_raw = self._synth.rows(tokens)
-        self.pool.ensure(row + n)
-        d = self.pool.data
-        ckv = self.kv_params.ckv_dim
-        dev = d.device
-        if n:
-            d[0, row:row + n, :ckv] = torch.from_numpy(c_kv).to(dev)
-            d[0, row:row + n, ckv:] = torch.from_numpy(kr_raw).to(dev)
-            pos = torch.arange(p_src, p_src + n, dtype=torch.float64, device=dev)
-            kr_view = d[0, row:row + n, ckv:]
-            ops.rotate_rows(kr_view, pos, inv_freq_device(self.spec), self.spec.layout_code,
-                            out=kr_view)
-            kr_base = kr_view.cpu().numpy().copy()
-        else:
-            kr_base = np.zeros((0, self.kv_params.kr_dim))
-        self._rows_used = max(self._rows_used, row + n)
-        c_kv = c_kv.copy()
-        c_kv.setflags(write=False)
-        kr_base.setflags(write=False)
-        entry = RegistryEntry(int(fp), c_kv, kr_base, int(p_src), len(self._entries))
+        """Producer side (registry.py:131-136): register the entry whose rows live at
+        pool row ``row``; the rows are synthesised and rotated to p_src + i on the
+        device at the next ``_flush`` (first read)."""
+        entry = RegistryEntry(int(fp), int(p_src), len(self._entries), self, tuple(tokens))
         self._entries.append(entry)
         self._entry_rows.append(row)
+        self._pending.append(entry)
+        self._rows_used = max(self._rows_used, row + len(tokens))
         return entry
+
+    def _flush(self):
+        """Synthesise, upload and rotate the rows of every entry not yet written."""
+        pending, self._pending = self._pending, []
+        ckv = self.kv_params.ckv_dim
+        for entry in pending:
+            row, n = self._entry_rows[entry.insert_epoch], entry.chunk_len
+            c_kv, kr_raw = self._synth.rows(entry._tokens)
+            self.pool.ensure(row + n)
+            d = self.pool.data
+            dev = d.device
+            if n:
+                d[0, row:row + n, :ckv] = torch.from_numpy(c_kv).to(dev)
+                d[0, row:row + n, ckv:] = torch.from_numpy(kr_raw).to(dev)
+                pos = torch.arange(entry.p_src, entry.p_src + n, dtype=torch.float64, device=dev)
+                kr_view = d[0, row:row + n, ckv:]
+                ops.rotate_rows(kr_view, pos, inv_freq_device(self.spec), self.spec.layout_code, out=kr_view)
+                kr_base = kr_view.cpu().numpy().copy()
+            else:
+                kr_base = np.zeros((0, self.kv_params.kr_dim))
+            c_kv = c_kv.copy()
+            c_kv.setflags(write=False)
+            kr_base.setflags(write=False)
+            entry._c_kv, entry._kr_base = c_kv, kr_base
 
     def pool_bytes(self) -> int:
         """Bytes of the shared latent pool as f64 c_kv rows (one copy per fingerprint)."""
-        return sum(e.c_kv.nbytes for e in self._entries)
+        return sum(e.chunk_len for e in self._entries) * self.kv_params.ckv_dim * 8
 
     # ------------------------------------------------------------ materialize
     def materialize_device(self, rows: torch.Tensor, lens: torch.Tensor, deltas: torch.Tensor,
                            precision: Precision = Precision.F64, out: torch.Tensor | None = None):
         """Batched K4 over the pool: chunk i -> out rows [sum(lens[:i]), +lens[i])."""
+        self._flush()
         n_rows = int(lens.sum().item()) if out is None else out.shape[1]
         if out is None:
             out = torch.empty(1, max(n_rows, 1), self.pool.data.shape[2], dtype=self.pool.data.dtype,
