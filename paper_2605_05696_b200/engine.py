@@ -162,7 +162,13 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
     plans: list[_Plan] = []
     flats = []
     for r in requests:
-        flat, _ = flatten(r)
+        flat = getattr(r, "_flat_u32", None)  # set by model.parse_trace (native ingest)
+        if flat is None:
+            t, _ = flatten(r)
+            flat = np.asarray(t, dtype=np.uint64)
+            if flat.size and int(flat.max()) > 0xFFFFFFFF:
+                raise ValueError("token ids must be unsigned 32-bit")
+            flat = flat.astype(np.uint32)
         if len(flat) == 0:
             raise ValueError("request flattens to zero tokens")
         flats.append(flat)

@@ -175,7 +175,11 @@ def trace_from_arrays(ta: TraceArrays) -> Trace:
             a = t0 + starts[j]
             b = t0 + starts[j + 1] if j + 1 < s1 else t1
             segs.append(Segment(KIND_NAMES[kinds[j]], tuple(toks[a:b]), ta.shared_ids[j]))
-        requests.append(Request(ta.sessions[i], int(ta.turns[i]), tuple(segs)))
+        req = Request(ta.sessions[i], int(ta.turns[i]), tuple(segs))
+        # the flattened u32 tokens ride along (a view of the ingest buffer), so the
+        # engine feeds K0 / K1 without converting Python ints back to an array
+        object.__setattr__(req, "_flat_u32", ta.tokens[t0:t1])
+        requests.append(req)
     return Trace(tuple(requests))
 
 

@@ -59,6 +59,7 @@ class _SynthCache:
         self._rows: dict[int, tuple[np.ndarray, np.ndarray]] = {}
 
     def rows(self, tokens: Sequence[int]) -> tuple[np.ndarray, np.ndarray]:
+        tokens = tokens.tolist() if isinstance(tokens, np.ndarray) else tokens  # Python ints (derive_seed)
         for t in tokens:
             if t not in self._rows:
                 self._rows[t] = synth_kv(t, 0, self.params)
@@ -187,7 +188,8 @@ class KvRegistry:
         """Producer side (registry.py:131-136): register the entry whose rows live at
         pool row ``row``; the rows are synthesised and rotated to p_src + i on the
         device at the next ``_flush`` (first read)."""
-        entry = RegistryEntry(int(fp), int(p_src), len(self._entries), self, tuple(tokens))
+        toks = tuple(tokens.tolist()) if isinstance(tokens, np.ndarray) else tuple(tokens)
+        entry = RegistryEntry(int(fp), int(p_src), len(self._entries), self, toks)
         self._entries.append(entry)
         self._entry_rows.append(row)
         self._pending.append(entry)
