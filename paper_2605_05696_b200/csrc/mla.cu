@@ -92,11 +92,6 @@ __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 
 #define IRM_MLA_PROF_MASK 0
 #endif
 constexpr bool kProf = IRM_MLA_PROF_MASK != 0;
-// What-if builds (wrong results; cost attribution only): 1 = V loaded but never waited for,
-// 2 = V never loaded, 3 = K loaded for the first KST tiles only
-#ifndef IRM_MLA_WHATIF
-#define IRM_MLA_WHATIF 0
-#endif
 template <int ROLE>
 __device__ __forceinline__ long long prof_clock() {
     if constexpr ((IRM_MLA_PROF_MASK & ROLE) != 0) return clock64();
@@ -109,20 +104,6 @@ __device__ __forceinline__ float ex2(float x) {  // 2^x, flush-to-zero; ex2(-inf
     return y;
 }
 
-// 2^x on the FMA pipe (FA4-style MUFU offload): 2^floor(x) by exponent arithmetic times a
-// degree-3 polynomial for 2^frac (max relative error 1.7e-4, far below bf16's 3.9e-3 for P)
-__device__ __forceinline__ float ex2_poly(float x) {
-    const float xc = fmaxf(x, -127.f);
-    const float xi = floorf(xc);
-    const float f = xc - xi;
-    const float q = fmaf(fmaf(fmaf(0.07632546f, f, 0.22830825f), f, 0.69503617f), f, 1.0f);
-    const float r = __int_as_float(__float_as_int(q) + ((int)xi << 23));
-    return x < -126.f ? 0.f : r;
-}
-// pairs of scores (of 16 per thread and tile) whose exponent runs on the FMA pipe
-#ifndef IRM_MLA_POLY
-#define IRM_MLA_POLY 0
-#endif
 
 // Row max of raw scores with masked keys forced to -inf. Scores are scaled after the
 // max (scale > 0), so the exponent is one FFMA per element: ex2(v * scale_log2 - m).
@@ -749,10 +730,6 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             long long a0 = prof_clock<1>();
             if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
             c_e += prof_clock<1>() - a0;
-            if (IRM_MLA_WHATIF == 3 && t >= KST) {
-                if (lane == 0 && rank == 0) mbar_arrive(&b_kfull[st]);
-                continue;
-            }
             // both CTAs' c_KV bytes complete on the leader's b_kfull (peer: .cta_group::2 TMA)
             if (rank == 0 && lane == 0) mbar_arrive_expect_tx(&b_kfull[st], 2 * CKV_TX);
             __syncwarp();
@@ -776,10 +753,6 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
             const int st = u % VST;
             const Rows32 rr = rows32_resolve(row_next, lane);
             if (u + 1 < 2 * T) row_next = key_row(p, (((u + 1) / 2 + toff) % T) * PBN + 32 * ((u + 1) & 1) + lane);
-            if (IRM_MLA_WHATIF == 2) {
-                if (lane == 0) mbar_arrive(&b_vfull[st]);
-                continue;
-            }
             long long a0 = prof_clock<1>();
             if (u >= VST) mbar_wait(&b_vempty[st], ((u / VST) - 1) & 1);
             c_ve += prof_clock<1>() - a0;
@@ -881,10 +854,8 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
                 for (int a = 0; a < 2; ++a) {  // PV over key half a, as soon as its V half-tile lands
                     const int u = 2 * t + a, vs = u % VST;
                     long long a1 = prof_clock<2>();
-                    if (IRM_MLA_WHATIF == 0 || IRM_MLA_WHATIF == 3) {
-                        mbar_wait(&b_vfull[vs], (u / VST) & 1);  // both CTAs' V half-tiles
-                        c_vl += prof_clock<2>() - a1;
-                    }
+                    mbar_wait(&b_vfull[vs], (u / VST) & 1);  // both CTAs' V half-tiles
+                    c_vl += prof_clock<2>() - a1;
                     c_v += prof_clock<2>() - a1;
                     tc::fence_after();
                     const uint32_t vd = v_lo + ((vs * VTILE) >> 4);
@@ -1169,10 +1140,6 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
             long long a0 = prof_clock<1>();
             if (t >= KST) mbar_wait(&b_kempty[st], ((t / KST) - 1) & 1);
             c_e += prof_clock<1>() - a0;
-            if (IRM_MLA_WHATIF == 3 && t >= KST) {
-                if (lane == 0 && rank == 0) mbar_arrive(&b_kfull[st]);
-                continue;
-            }
             // both CTAs' c_KV bytes complete on the leader's b_kfull (peer: .cta_group::2 TMA)
             if (rank == 0 && lane == 0) mbar_arrive_expect_tx(&b_kfull[st], 2 * CKV_TX);
             __syncwarp();
@@ -1397,9 +1364,8 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
             for (int i = 0; i < 32; i += 2) {
                 const float x0 = fmaf(__uint_as_float(v[i]), p.scale_log2, nm);
                 const float x1 = fmaf(__uint_as_float(v[i + 1]), p.scale_log2, nm);
-                const bool poly = ((i >> 1) * IRM_MLA_POLY) % 16 + IRM_MLA_POLY >= 16;  // spread over the pairs
-                const float e0 = poly ? ex2_poly(x0) : ex2(x0);
-                const float e1 = poly ? ex2_poly(x1) : ex2(x1);
+                const float e0 = ex2(x0);
+                const float e1 = ex2(x1);
                 ls[(i >> 1) & 1] += e0 + e1;
                 pk[i >> 1] = pack_bf2(e0, e1);
             }
