@@ -100,7 +100,11 @@ class DeviceRadixTree:
     a full table). Inserted sequences are kept in a device token arena."""
 
     def __init__(self, capacity_hint: int | None = None, max_prefixes: int = 1 << 22,
-                 max_tokens: int = 1 << 24, max_sequences: int = 1 << 16):
+                 max_tokens: int = 1 << 24, max_sequences: int = 1 << 16, grow: bool = True):
+        """Capacities are initial sizes; with ``grow`` (default) the arena, the
+        per-sequence arrays and the table are enlarged when a batch would not
+        fit (the table by rebuilding it from the arena, epochs unchanged), so a
+        long serve run never hits a limit the reference's tree does not have."""
         import torch
 
         from . import _native as N
@@ -108,22 +112,82 @@ class DeviceRadixTree:
 
         self._N, self._torch = N, torch
         dev = ops._dev()
-        n_slots = 2
-        while n_slots < 2 * max_prefixes:
-            n_slots <<= 1
         self.capacity_hint = capacity_hint
-        self.slot_key = torch.empty(n_slots, dtype=torch.int64, device=dev)
-        self.slot_epoch = torch.empty(n_slots, dtype=torch.int64, device=dev)
+        self.grow = grow
         self.counters = torch.zeros(2, dtype=torch.int64, device=dev)
-        self.view = N.PrefixView(N.ptr(self.slot_key), N.ptr(self.slot_epoch), n_slots, N.ptr(self.counters))
+        self._new_table(max_prefixes)
         self.arena = torch.zeros(max_tokens, dtype=torch.int32, device=dev)
         self.wit_off = torch.zeros(max_sequences, dtype=torch.int64, device=dev)
         self.wit_len = torch.zeros(max_sequences, dtype=torch.int64, device=dev)
         self.used = 0        # arena tokens in use
         self._epoch = 0      # inserts so far (radix.py:34-35)
+        self._prefix_bound = 0  # upper bound on stored prefixes (inserted tokens since the last count)
         self.handles: list = []
         self._ws = None
+
+    def _new_table(self, max_prefixes: int):
+        torch, N = self._torch, self._N
+        n_slots = 2
+        while n_slots < 2 * max_prefixes:
+            n_slots <<= 1
+        dev = self.counters.device
+        self.slot_key = torch.empty(n_slots, dtype=torch.int64, device=dev)
+        self.slot_epoch = torch.empty(n_slots, dtype=torch.int64, device=dev)
+        self.view = N.PrefixView(N.ptr(self.slot_key), N.ptr(self.slot_epoch), n_slots, N.ptr(self.counters))
         N.check(N.lib().irm_prefix_reset(self.view, N.stream_ptr()), "irm_prefix_reset")
+
+    def _reserve(self, n_tok: int, n_ins: int, ins_tok: int):
+        """Make room for a batch of n_tok tokens with n_ins inserts (ins_tok of their tokens)."""
+        torch = self._torch
+        if self.used + n_tok > self.arena.numel():
+            if not self.grow:
+                raise ValueError("prefix index token arena is full: raise max_tokens")
+            new = torch.zeros(max(2 * self.arena.numel(), self.used + n_tok), dtype=torch.int32,
+                              device=self.arena.device)
+            new[:self.used].copy_(self.arena[:self.used])
+            self.arena = new
+        if self._epoch + n_ins > self.wit_off.numel():
+            if not self.grow:
+                raise ValueError("prefix index holds max_sequences inserts: raise max_sequences")
+            cap = max(2 * self.wit_off.numel(), self._epoch + n_ins)
+            for name in ("wit_off", "wit_len"):
+                old = getattr(self, name)
+                new = torch.zeros(cap, dtype=torch.int64, device=old.device)
+                new[:self._epoch].copy_(old[:self._epoch])
+                setattr(self, name, new)
+        half = self.slot_key.numel() // 2
+        if self.grow and self._prefix_bound + ins_tok > half:
+            self.check()
+            used = int(self.counters[0])  # the real count (one sync, only near the load limit)
+            self._prefix_bound = used
+            if used + ins_tok > half:
+                self._rehash(used + ins_tok)
+
+    def _rehash(self, need: int):
+        """Rebuild the table 2x larger from the stored sequences, with their epochs."""
+        torch, N = self._torch, self._N
+        self.counters.zero_()
+        self._new_table(max(2 * need, self.slot_key.numel()))
+        n = self._epoch
+        if n == 0:
+            return
+        off, ln = self.wit_off[:n], self.wit_len[:n]
+        seq_off = torch.zeros(n + 1, dtype=torch.int64, device=off.device)
+        seq_off[1:] = torch.cumsum(ln, 0)
+        total = int(seq_off[-1])
+        idx = torch.repeat_interleave(off - seq_off[:-1], ln) + torch.arange(total, device=off.device)
+        tok = self.arena[idx].contiguous()  # every inserted sequence, compacted
+        epoch = torch.arange(n, dtype=torch.int64, device=off.device)
+        ones = torch.ones(n, dtype=torch.uint8, device=off.device)
+        m = torch.empty(n, dtype=torch.int64, device=off.device)
+        wit = torch.empty_like(m)
+        ws = self._workspace(total, n)
+        rc = N.lib().irm_prefix_match_insert(
+            self.view, N.ptr(tok), N.ptr(seq_off), n, total, N.ptr(epoch), N.ptr(ones), N.ptr(torch.zeros_like(ones)),
+            N.ptr(self.arena), N.ptr(self.wit_off), N.ptr(self.wit_len), N.ptr(m), N.ptr(wit), N.ptr(ws),
+            ws.numel(), N.stream_ptr())
+        N.check(rc, "irm_prefix_match_insert (rehash)")
+        self._prefix_bound = total
 
     def _workspace(self, n_tok, n_seq):
         need = int(self._N.lib().irm_prefix_workspace_bytes(n_tok, n_seq))
@@ -147,10 +211,8 @@ class DeviceRadixTree:
         ins = np.asarray(insert, bool)
         qry = np.asarray(query, bool)
         n_ins = int(ins.sum())
-        if self.used + n_tok > self.arena.numel():
-            raise ValueError("prefix index token arena is full: raise max_tokens")
-        if self._epoch + n_ins > self.wit_off.numel():
-            raise ValueError("prefix index holds max_sequences inserts: raise max_sequences")
+        ins_tok = int(lens[ins].sum()) if n else 0
+        self._reserve(n_tok, n_ins, ins_tok)
         before = np.cumsum(ins) - ins  # inserts earlier in the batch
         # an insert's epoch is its insert index; a query's bound is the number of inserts before it
         epoch = (self._epoch + before).astype(np.int64)
@@ -176,6 +238,7 @@ class DeviceRadixTree:
         N.check(rc, "irm_prefix_match_insert")
         self.used += n_tok
         self._epoch += n_ins
+        self._prefix_bound += ins_tok
         hs = list(handles) if handles is not None else [None] * n
         self.handles += [hs[i] for i in range(n) if ins[i]]
         return m[:n], wit[:n]

@@ -26,7 +26,7 @@ def test_store_entries_overflow_raises():
 def test_prefix_index_full_raises():
     from paper_2605_05696_b200.radix import DeviceRadixTree
 
-    tree = DeviceRadixTree(max_prefixes=64, max_tokens=1 << 14, max_sequences=16)  # 128 slots
+    tree = DeviceRadixTree(max_prefixes=64, max_tokens=1 << 14, max_sequences=16, grow=False)  # 128 slots
     rng = np.random.default_rng(1)
     tree.run_ops([rng.integers(0, 2**32, size=500, dtype=np.uint64).astype(np.uint32)], [True], [False])
     with pytest.raises(RuntimeError, match="full"):
@@ -36,7 +36,7 @@ def test_prefix_index_full_raises():
 def test_prefix_index_arena_capacity():
     from paper_2605_05696_b200.radix import DeviceRadixTree
 
-    tree = DeviceRadixTree(max_prefixes=1 << 10, max_tokens=100, max_sequences=4)
+    tree = DeviceRadixTree(max_prefixes=1 << 10, max_tokens=100, max_sequences=4, grow=False)
     with pytest.raises(ValueError, match="arena"):
         tree.insert(list(range(101)), "x")
     assert tree.run_ops([], [], [])[0].numel() == 0  # empty batch: nothing launched, nothing inserted

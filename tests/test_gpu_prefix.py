@@ -109,3 +109,28 @@ def test_prefix_match_insert_sessions():
     tree.check()
     print(f"K0 match_insert: {sum(r.size for r in reqs[-256:])} tokens in {ev[0].elapsed_time(ev[1]):.3f} ms "
           f"(last batch), {tree.n_prefixes} prefixes stored")
+
+
+@pytest.mark.parametrize("case", ["long_shared", "small_alphabet"])
+def test_prefix_growth_golden(case):
+    """Tiny initial capacities: the arena, the per-sequence arrays and the table
+    (rebuilt from the arena with the original epochs) grow as batches arrive;
+    results still equal the reference RadixTree's."""
+    g = load_npz("radix")[case]
+    ops = radix_case_inputs(RADIX_CASES[case])
+    tree = _tree(max_prefixes=8, max_tokens=64, max_sequences=2)
+    got_m, got_w = np.full(len(ops), -1), np.full(len(ops), -1)
+    bs = 13
+    for b0 in range(0, len(ops), bs):
+        part = ops[b0:b0 + bs]
+        ins = [o[0] for o in part]
+        m, w = tree.run_ops([o[1] for o in part], ins, [not x for x in ins], handles=list(range(b0, b0 + len(part))))
+        m, w = m.cpu().numpy(), w.cpu().numpy()
+        for k, (is_ins, _) in enumerate(part):
+            if not is_ins:
+                got_m[b0 + k] = m[k]
+                got_w[b0 + k] = tree.handles[w[k]] if m[k] > 0 else -1
+    tree.check()
+    q = np.array([not o[0] for o in ops])
+    assert np.array_equal(got_m[q], g["m"][q]) and np.array_equal(got_w[q], g["witness"][q])
+    assert tree.slot_key.numel() > 16 and tree.arena.numel() > 64
