@@ -196,6 +196,7 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
     # ---- phase 3: batched first-writer-wins lookup-or-insert (K3)
     order = reg._order + torch.arange(n_chunks, dtype=torch.int64, device=dev)
     reg._order += n_chunks
+    reg.ensure_capacity(n_chunks)  # every probed chunk could be novel
     hit, entry, p_src, row = reg.store.lookup_insert(table.fp[:n_chunks], order, p_abs, lens, probe)
 
     # one device->host copy of everything the events need

@@ -170,8 +170,29 @@ class KvRegistry:
         return self._synth.rows(tokens)
 
     # ------------------------------------------------------------ inserts
+    def ensure_capacity(self, n_new: int):
+        """Room for n_new more entries: the device store is rebuilt 2x larger from the
+        host mirror (same entry ids, rows and p_src; inserting in epoch order gives the
+        store's row scan the same rows), so the dict never fills up (registry.py:126)."""
+        need = len(self._entries) + n_new
+        if need <= self.store.max_entries:
+            return
+        cap = max(2 * self.store.max_entries, need)
+        new = ops.ChunkStore(cap)
+        n = len(self._entries)
+        if n:
+            dev = ops._dev()
+            fps = self._fp_tensor([e.fingerprint for e in self._entries])
+            order = torch.arange(n, dtype=torch.int64, device=dev)
+            p = torch.tensor([e.p_src for e in self._entries], dtype=torch.int64, device=dev)
+            ln = torch.tensor([e.chunk_len for e in self._entries], dtype=torch.int32, device=dev)
+            hit, entry, _, row = new.lookup_insert(fps, order, p, ln)
+            assert bool((hit == 0).all()) and row.cpu().tolist() == self._entry_rows, "store rebuild diverged"
+        self.store = new
+
     def insert(self, fp: int, tokens: Sequence[int], p_src: int) -> RegistryEntry:
         """Store a chunk's KV at p_src (no-op on duplicates, registry.py:126-140)."""
+        self.ensure_capacity(1)
         dev = ops._dev()
         hit, entry, _, row = self.store.lookup_insert(
             self._fp_tensor([fp]), torch.tensor([self._order], dtype=torch.int64, device=dev),

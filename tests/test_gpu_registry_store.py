@@ -189,3 +189,15 @@ def test_sharded_store_single_rank_nccl(M):
         sh.check()
     finally:
         dist.destroy_process_group()
+
+
+def test_registry_store_grows(M):
+    """A registry created with room for 4 entries keeps serving: the device store is
+    rebuilt larger (same ids, rows, p_src) and lookups still hit."""
+    registry, rotary, _, ops = M
+    reg = registry.KvRegistry(registry.SyntheticKvParams(), rotary.make_spec(1e4), max_entries=4)
+    entries = [reg.insert(1000 + i, [7 * i + j for j in range(3 + i)], 40 + i) for i in range(11)]
+    assert reg.store.max_entries >= 11 and len(reg) == 11
+    for i, e in enumerate(entries):
+        assert reg.lookup(1000 + i) is e and e.p_src == 40 + i and e.chunk_len == 3 + i
+    assert reg.insert(1003, [1, 2, 3], 999) is entries[3]  # first writer still wins
