@@ -17,6 +17,8 @@
 // the reported error is the first one in line order, as the sequential reference.
 #include <algorithm>
 #include <atomic>
+#include <charconv>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -356,18 +358,65 @@ struct Err {
 
 std::string repr_raw(const JNode &n) { return std::string(n.src, n.src_len); }
 
+// Python's repr of a float (the shortest round-trip digits, scientific when the decimal
+// point position is <= -4 or > 16, "inf" / "nan"), for messages that quote a JSON number
+std::string py_float_repr(const JNode &n) {
+    const std::string raw = repr_raw(n);
+    const double v = strtod(raw.c_str(), nullptr);
+    if (std::isnan(v)) return "nan";
+    if (std::isinf(v)) return v < 0 ? "-inf" : "inf";
+    char buf[64];
+    const auto r = std::to_chars(buf, buf + sizeof buf, std::fabs(v), std::chars_format::scientific);
+    const std::string sci(buf, r.ptr);
+    const size_t epos = sci.find('e');
+    std::string digits = sci.substr(0, epos);
+    digits.erase(std::remove(digits.begin(), digits.end(), '.'), digits.end());
+    const int exp10 = atoi(sci.c_str() + epos + 1);
+    const int decpt = exp10 + 1, nd = (int)digits.size();
+    std::string out = std::signbit(v) ? "-" : "";
+    if (decpt > -4 && decpt <= 16) {
+        if (decpt <= 0) out += "0." + std::string(-decpt, '0') + digits;
+        else if (decpt >= nd) out += digits + std::string(decpt - nd, '0') + ".0";
+        else out += digits.substr(0, decpt) + "." + digits.substr(decpt);
+    } else {
+        out += digits.substr(0, 1);
+        if (nd > 1) out += "." + digits.substr(1);
+        char e[16];
+        snprintf(e, sizeof e, "e%c%02d", exp10 < 0 ? '-' : '+', std::abs(exp10));
+        out += e;
+    }
+    return out;
+}
+
 // Python repr of a JSON value as the reference's f-strings print it (strings quoted)
 std::string py_repr(const Parser &P, const JNode &n) {
     switch (n.type) {
         case J_NULL: return "None";
         case J_TRUE: return "True";
         case J_FALSE: return "False";
+        case J_FLOAT: return py_float_repr(n);
         case J_STR: {
             const std::string s = P.sv(n);
             const bool dq = s.find('\'') != std::string::npos && s.find('"') == std::string::npos;
             return (dq ? "\"" : "'") + s + (dq ? "\"" : "'");
         }
-        default: return repr_raw(n);
+        case J_ARR: {
+            std::string o = "[";
+            for (uint32_t i = 0; i < n.count; ++i) {
+                if (i) o += ", ";
+                o += n.packed ? std::to_string(P.ints[n.first + i]) : py_repr(P, P.nodes[P.kids[n.first + i]]);
+            }
+            return o + "]";
+        }
+        case J_OBJ: {
+            std::string o = "{";
+            for (uint32_t i = 0; i < n.count; ++i) {  // (duplicate keys: Python keeps the last; rare here)
+                if (i) o += ", ";
+                o += py_repr(P, P.nodes[P.kids[n.first + 2 * i]]) + ": " + py_repr(P, P.nodes[P.kids[n.first + 2 * i + 1]]);
+            }
+            return o + "}";
+        }
+        default: return repr_raw(n);  // integers: their digits
     }
 }
 
