@@ -210,6 +210,16 @@ int irm_rotate_gather_set_sm_limit(int32_t n_sms);
 int irm_copy_runs(const int64_t *src_addr, int64_t src_layer_stride, void *dst, int64_t dst_layer_stride,
                   const int64_t *dst_row, const int32_t *len, int64_t n_runs, const int64_t *n_runs_dev,
                   int32_t layers, int32_t row_bytes, irm_stream_t stream);
+/* Peer pool mapping for irm_copy_runs: irm_peer_export writes the
+ * IRM_PEER_HANDLE_BYTES-byte IPC handle of the device allocation holding `ptr` and
+ * the byte offset of `ptr` in it; another process on any GPU of the node passes
+ * both to irm_peer_open, which maps the allocation on the caller's CURRENT device
+ * (peer access over NVLink enabled lazily) and returns the address of `ptr` there.
+ * Mappings live until the process exits. Replaces the reference's in-process
+ * sharing of registry rows (registry.py:126-140). */
+#define IRM_PEER_HANDLE_BYTES 64
+int irm_peer_export(const void *ptr, void *handle, int64_t *offset);
+int irm_peer_open(const void *handle, int64_t offset, void **ptr);
 /* Per-row absolute rotation (producer side of the store, registry.py:131-133
  * with rotary.py:98-108): out[i] = R(positions[i]) rows[i] for the dim-wide
  * rotary rows at rows + i*row_stride (elements). out may alias rows. */

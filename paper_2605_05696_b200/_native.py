@@ -18,6 +18,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "irminsul_b200.h")
 IRM_OK, IRM_EINVAL, IRM_ECUDA, IRM_ECAPACITY = 0, 1, 2, 3
 FORCED_NONE, FORCED_MAX_CLAMP, FORCED_MARKER, FORCED_STREAM_END = 0, 1, 2, 3
 LAYOUT_HALF_SPLIT, LAYOUT_INTERLEAVED = 0, 1
+PEER_HANDLE_BYTES = 64  # IRM_PEER_HANDLE_BYTES
 DTYPE_F64, DTYPE_F32, DTYPE_BF16 = 0, 1, 2
 ROUND_NONE, ROUND_F32, ROUND_BF16 = 0, 1, 2
 EMPTY_KEY = 0xFFFFFFFFFFFFFFFF
@@ -58,6 +59,8 @@ _SIGS = {
     "irm_rotate_gather_workspace_bytes": ([i64, i32], i64),
     "irm_rotate_gather_set_sm_limit": ([i32], i32),
     "irm_copy_runs": ([P, i64, P, i64, P, P, i64, P, i32, i32, P], i32),
+    "irm_peer_export": ([P, P, P], i32),
+    "irm_peer_open": ([P, i64, P], i32),
     "irm_rotate_gather": ([P, i64, P, i64, i32, i32, i32, P, P, P, P, i64, P, P, i32, i32, i32, P, i64, P], i32),
     "irm_rotate_rows": ([P, i64, P, i64, i64, i32, P, P, i32, i32, i32, P], i32),
     "irm_round_f64": ([P, P, i64, i32, P], i32),

@@ -12,6 +12,8 @@
 // chunk: fp32 angles fail the 1e-5 bar at |delta| ~ 2^20), and writes the tile
 // back with a bulk store. STAGES tiles are in flight per CTA.
 #include <algorithm>
+#include <cuda.h>
+#include <string.h>
 #include "common.cuh"
 #include "tma.cuh"
 #include <cuda_bf16.h>
@@ -438,5 +440,44 @@ extern "C" int irm_copy_runs(const int64_t *src_addr, int64_t src_layer_stride, 
     irm::copy_runs_kernel<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, (cudaStream_t)stream>>>(
         src_addr, src_layer_stride, (char *)dst, dst_layer_stride, dst_row, len, n_runs, n_runs_dev, layers, row_bytes);
     IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+// ---------------------------------------------------------------- peer pool mapping (K6)
+// The pool a peer process exports is mapped into this process on the CURRENT device with
+// lazy peer enabling, so kernels launched on this rank's GPU read the peer's HBM over
+// NVLink (the IPC handle is opened from the reader's device, not the owner's).
+extern "C" int irm_peer_export(const void *ptr, void *handle, int64_t *offset) {
+    IRM_REQUIRE(ptr && handle && offset, "null pointer");
+    // driver entry point fetched through the runtime: the library does not link libcuda
+    using range_fn = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+    static range_fn get_range = nullptr;
+    if (!get_range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        IRM_REQUIRE(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                        q == cudaDriverEntryPointSuccess && fn,
+                    "cuMemGetAddressRange unavailable");
+        get_range = (range_fn)fn;
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    CUresult r = get_range(&base, &size, (CUdeviceptr)ptr);
+    IRM_REQUIRE(r == CUDA_SUCCESS, "cuMemGetAddressRange failed (%d): not a device allocation", (int)r);
+    static_assert(sizeof(cudaIpcMemHandle_t) == IRM_PEER_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    IRM_CUDA_CHECK(cudaIpcGetMemHandle(&h, (void *)base));
+    memcpy(handle, &h, sizeof(h));
+    *offset = (int64_t)((CUdeviceptr)ptr - base);
+    return IRM_OK;
+}
+
+extern "C" int irm_peer_open(const void *handle, int64_t offset, void **ptr) {
+    IRM_REQUIRE(handle && ptr && offset >= 0, "bad arguments");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void *base = nullptr;
+    IRM_CUDA_CHECK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr = (char *)base + offset;
     return IRM_OK;
 }

@@ -27,6 +27,8 @@ then always reads local HBM.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 import torch.distributed as dist
 
@@ -152,17 +154,48 @@ class ShardedStore:
             raise RuntimeError("first-writer row range of the pool is full: raise novel_rows")
 
 
+class _PeerMapping:
+    """A peer allocation mapped into this process, exposed to torch through the
+    CUDA array interface (no copy; the mapping lives until the process exits)."""
+
+    def __init__(self, addr: int, shape, itemsize: int):
+        self.__cuda_array_interface__ = {"data": (addr, False), "shape": tuple(shape),
+                                         "typestr": f"<i{itemsize}", "strides": None, "version": 2}
+
+
 def map_peer_pools(pool: torch.Tensor, group=None) -> list[torch.Tensor]:
-    """Every rank's latent pool, mapped into this process (CUDA IPC; peer access
-    over NVLink is enabled lazily on first touch). Index = rank."""
-    from torch.multiprocessing.reductions import reduce_tensor
+    """Every rank's latent pool, mapped into this process. Index = rank.
+
+    Each rank exports its pool's allocation (``irm_peer_export``: CUDA IPC handle
+    + offset) and every other rank maps it on ITS OWN device
+    (``irm_peer_open``, peer access over NVLink enabled lazily), so K6's
+    ``irm_copy_runs`` on this rank's GPU reads the peer's HBM directly."""
+    from . import _native as N
 
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     if world == 1:
         return [pool]
+    assert pool.is_cuda and pool.is_contiguous()
+    L = N.lib()
+    handle = ctypes.create_string_buffer(N.PEER_HANDLE_BYTES)
+    offset = ctypes.c_int64(0)
+    N.check(L.irm_peer_export(ctypes.c_void_p(pool.data_ptr()), handle, ctypes.byref(offset)), "irm_peer_export")
     objs = [None] * world
-    dist.all_gather_object(objs, reduce_tensor(pool), group=group)
-    return [pool if r == rank else objs[r][0](*objs[r][1]) for r in range(world)]
+    dist.all_gather_object(objs, (handle.raw, offset.value, tuple(pool.shape)), group=group)
+    out = []
+    with torch.cuda.device(pool.device):
+        for r, (h, off, shape) in enumerate(objs):
+            if r == rank:
+                out.append(pool)
+                continue
+            assert tuple(shape) == tuple(pool.shape), "peer pools must have the same shape"
+            addr = ctypes.c_void_p(0)
+            N.check(L.irm_peer_open(ctypes.create_string_buffer(h, len(h)), int(off), ctypes.byref(addr)),
+                    "irm_peer_open")
+            item = pool.element_size()
+            t = torch.as_tensor(_PeerMapping(addr.value, shape, item))
+            out.append(t.view(pool.dtype))
+    return out
 
 
 class ReplicaCache:

@@ -33,7 +33,8 @@ def _worker(rank, port, out_q):
         from paper_2605_05696_b200 import ops, shard
 
         torch.cuda.set_device(0)
-        pool = torch.full((2, 256, 576), float(rank + 1), dtype=torch.bfloat16, device="cuda")
+        big = torch.full((3, 256, 576), float(rank + 1), dtype=torch.bfloat16, device="cuda")
+        pool = big[1:]  # not at its allocation's base: the exported offset is non-zero
         pool[:, :, 1] = torch.arange(256, device="cuda").to(torch.bfloat16)
         peers = shard.map_peer_pools(pool)
         cache = shard.ReplicaCache(pool, 128, peers, rank, ops.ChunkStore(1 << 10))
@@ -47,6 +48,9 @@ def _worker(rank, port, out_q):
         ok = ok and bool((p[:, local[0]:local[0] + 3, 0] == other + 1).all())
         ok = ok and bool((p[:, local[0]:local[0] + 3, 1] == torch.arange(5, 8).float()).all())
         ok = ok and bool((p[:, local[1]:local[1] + 7, 1] == torch.arange(40, 47).float()).all())
+        ok = ok and torch.equal(peers[other][:, 100:110, :2].float().cpu(),
+                                torch.stack([torch.full((2, 10), float(other + 1)),
+                                             torch.arange(100, 110).float().expand(2, 10)], -1))
         out_q.put((rank, ok))
         dist.barrier()  # keep both pools alive until both ranks have read
     finally:
@@ -65,3 +69,16 @@ def test_replica_fetch_across_processes():
         pr.join(timeout=60)
         assert pr.exitcode == 0
     assert outs == {0: True, 1: True}, outs
+
+
+def test_peer_export_rejects_host_memory():
+    import ctypes
+
+    from paper_2605_05696_b200 import _native as N
+
+    host = torch.zeros(16)
+    h = ctypes.create_string_buffer(N.PEER_HANDLE_BYTES)
+    off = ctypes.c_int64(0)
+    rc = N.lib().irm_peer_export(ctypes.c_void_p(host.data_ptr()), h, ctypes.byref(off))
+    with pytest.raises(ValueError, match="not a device allocation"):
+        N.check(rc, "irm_peer_export")
