@@ -23,6 +23,8 @@
 #include "common.cuh"
 #include "tma.cuh"
 #include <stdlib.h>
+#include <string.h>
+#include <algorithm>
 
 namespace irm {
 
@@ -428,6 +430,222 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
                t_work, t_loop, clock64() - t_all, ntiles);
 }
 
+// walker, scalar form (split K1): the warp builds next-candidate words once per tile
+// (suffix min over lanes), then lane 0 alone walks the boundary rule with two shared
+// loads per chunk: no vote / shuffle on the per-chunk dependency chain. Same rule as
+// walk_tile; walker state (start, nch) lives in lane 0.
+__device__ __forceinline__ void walk_tile_scalar(const unsigned *sCand, int32_t *sNext, int32_t tile_start,
+                                                 int32_t len, int32_t min_size, int32_t max_size, int32_t t_pin,
+                                                 int32_t &start, int32_t &nch, const ChunkSink &sink, int lane) {
+    const unsigned my_cand = sCand[lane];
+    int32_t nc = my_cand ? tile_start + 32 * lane + __ffs(my_cand) - 1 : INT32_MAX;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int32_t y = __shfl_down_sync(0xffffffffu, nc, d);
+        if (lane + d < 32) nc = min(nc, y);
+    }
+    sNext[lane] = nc;  // first candidate at or after word `lane`
+    if (lane == 0) sNext[32] = INT32_MAX;
+    __syncwarp();
+    if (lane != 0) return;
+    const int32_t tile_end = min(tile_start + RG_TILE, len);
+    while (true) {
+        const int32_t t_max = start + max_size - 1;
+        const int32_t rel = max(0, start + min_size - 1 - tile_start);
+        int32_t t_cand = INT32_MAX;
+        if (rel < RG_TILE) {
+            const int w = rel >> 5;
+            const unsigned cw = sCand[w] & (0xffffffffu << (rel & 31));
+            const int32_t nx = sNext[w + 1];
+            t_cand = cw ? tile_start + 32 * w + __ffs(cw) - 1 : nx;
+        }
+        const int32_t nxt = min(t_max, min(t_pin >= start ? t_pin : INT32_MAX, t_cand));
+        if (nxt >= tile_end) break;
+        sink.emit(0, nch, start, nxt - start + 1,
+                  nxt == t_pin ? IRM_FORCED_MARKER : nxt == t_max ? IRM_FORCED_MAX_CLAMP : IRM_FORCED_NONE);
+        ++nch;
+        start = nxt + 1;
+    }
+}
+
+// ---------------------------------------------------------------- K1 split form
+// G_t is windowed (64 tokens), so it need not sit on the per-region critical path:
+// gear_window_kernel computes it for the whole flat token array on every SM
+// (G over the flat array, ignoring region starts), and cdc_region_split_kernel only
+// stages it, corrects the first 63 tokens of its region
+//     G_local_t = G_flat_t - (G_flat_{rs-1} << (t - rs + 1))      (mod 2^64)
+// and runs the chain / cand / walker roles. Its tile time is the roles' own.
+constexpr int GW_THREADS = 256;
+constexpr int GW_PER = 8;                              // sub-blocks per warp, loads batched
+constexpr int GW_SUB = GW_THREADS / 32 * GW_PER - 2;   // output sub-blocks per CTA (+2 halo in front)
+
+__global__ void __launch_bounds__(GW_THREADS)
+gear_window_kernel(const uint32_t *__restrict__ tok, int64_t n, const uint64_t *__restrict__ gear,
+                   uint64_t *__restrict__ G) {
+    __shared__ uint64_t sS[(GW_SUB + 2) * 32];
+    __shared__ uint64_t sS31[GW_SUB + 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t base = (int64_t)blockIdx.x * GW_SUB * 32; base < n; base += (int64_t)gridDim.x * GW_SUB * 32) {
+        // in-sub-block scans S_j(l) = sum_{i<=l} g_i << (l - i); sub-block j covers base + 32 (j - 2) ..
+        // (all token loads of the warp in flight, then all gear lookups, then the scans)
+        uint32_t tk[GW_PER];
+        uint64_t g[GW_PER];
+#pragma unroll
+        for (int u = 0; u < GW_PER; ++u) {
+            const int64_t t = base + 32 * (warp * GW_PER + u - 2) + lane;
+            tk[u] = (t >= 0 && t < n) ? __ldg(tok + t) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < GW_PER; ++u) {
+            const int64_t t = base + 32 * (warp * GW_PER + u - 2) + lane;
+            g[u] = (t >= 0 && t < n) ? __ldg(gear + (tk[u] & 0xFFFFu)) : 0ULL;
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+            for (int u = 0; u < GW_PER; ++u) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, g[u], d);
+                if (lane >= d) g[u] += y << d;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < GW_PER; ++u) {
+            const int j = warp * GW_PER + u;
+            sS[j * 32 + lane] = g[u];
+            if (lane == 31) sS31[j] = g[u];
+        }
+        __syncthreads();
+        for (int j = 2 + warp; j < GW_SUB + 2; j += GW_THREADS / 32) {
+            const int64_t t = base + 32 * (j - 2) + lane;
+            // carry-in G_{first-1} = S31(j-1) + (S31(j-2) << 32)
+            const uint64_t gb = sS31[j - 1] + (sS31[j - 2] << 32);
+            if (t < n) G[t] = sS[j * 32 + lane] + (gb << (lane + 1));
+        }
+        __syncthreads();
+    }
+}
+
+#ifndef IRM_CDC2_THREADS
+#define IRM_CDC2_THREADS 256
+#endif
+constexpr int RG2_THREADS = IRM_CDC2_THREADS;
+constexpr int RG2_LOADERS = RG2_THREADS / 32 - 4;
+constexpr int W2_WALK = RG2_LOADERS, W2_CAND = RG2_LOADERS + 1, W2_CHAIN = RG2_LOADERS + 3;
+
+// G of tile `tile` into sGdst with 8-byte cp.async (zero-filled past the region end)
+__device__ __forceinline__ void stage_G(const uint64_t *__restrict__ rG, int32_t len, int32_t tile,
+                                        uint64_t *sGdst, int ptid) {
+    const int32_t base = tile * RG_TILE;
+    for (int i = ptid; i < RG_TILE; i += RG2_LOADERS * 32) {
+        const bool in = base + i < len;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(sGdst + i)),
+                     "l"(rG + (in ? base + i : 0)), "r"(in ? 8 : 0)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(RG2_THREADS)
+cdc_region_split_kernel(const uint32_t *__restrict__ tok, const uint64_t *__restrict__ Gflat,
+                   const Region *__restrict__ regions, const int64_t *__restrict__ n_regions_p, int32_t k,
+                   int32_t min_size, int32_t max_size, int32_t *__restrict__ st_start,
+                   int32_t *__restrict__ st_len, uint8_t *__restrict__ st_forced,
+                   uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count, int dbg) {
+    __shared__ uint64_t sG[4][RG_TILE];
+    __shared__ uint32_t sBm[2][RG_SUB];
+    __shared__ unsigned sCand[2][RG_SUB];
+    __shared__ int32_t sNext[RG_SUB + 1];
+
+    const int64_t r = blockIdx.x;
+    if (r >= *n_regions_p) return;  // uniform per CTA
+    const Region R = regions[r];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t *__restrict__ rG = Gflat + R.tok_begin;
+    const uint32_t mask = (1u << k) - 1;
+    const int32_t t_pin = R.ends_pin ? R.len - 1 : INT32_MAX;
+    const ChunkSink sink{st_start, st_len, st_forced, R.cap_off, (int32_t)(R.tok_begin - R.stream_begin)};
+    const int ntiles = (R.len + RG_TILE - 1) / RG_TILE;
+
+    uint32_t Blo = 0, Bhi = 0;
+    uint32_t Cprev_lo = 0;
+    int32_t start = 0, nch = 0;
+    const int ptid = threadIdx.x;
+    const uint64_t Gcut = R.tok_begin > 0 ? Gflat[R.tok_begin - 1] : 0ULL;  // G_flat_{rs-1}
+    if (warp < W2_WALK) stage_G(rG, R.len, 0, sG[0], ptid);
+    long long t_work = 0, t_all = clock64();
+    for (int i = 0; i <= ntiles + 2; ++i) {
+        const long long t0 = clock64();
+        if (warp == W2_CHAIN) {
+            if (i >= 1 && i <= ntiles && !(dbg & 4))
+                chain_tile(sG[(i - 1) & 3], sBm[(i - 1) & 1], (i - 1) * RG_TILE, R.len, Blo, Bhi, lane);
+        } else if (warp == W2_CAND || warp == W2_CAND + 1) {
+            if (i >= 2 && i <= ntiles + 1)
+                cand_tile(sG[(i - 2) & 3], sBm[i & 1], sCand[i & 1], (i - 2) * RG_TILE, R.len, mask,
+                          Cprev_lo, warp - W2_CAND, lane);
+        } else if (warp == W2_WALK) {
+            if (i >= 3)
+                walk_tile_scalar(sCand[(i - 3) & 1], sNext, (i - 3) * RG_TILE, R.len, min_size, max_size, t_pin,
+                                 start, nch, sink, lane);
+        } else {
+            if (i < ntiles) {
+                if (i + 1 < ntiles) stage_G(rG, R.len, i + 1, sG[(i + 1) & 3], ptid);
+                else asm volatile("cp.async.commit_group;" ::: "memory");
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // this thread's part of tile i landed
+                // the region's first 63 tokens: drop the window's part before the region start
+                // (each thread fixes the elements it staged itself)
+                if (i == 0 && Gcut)
+                    for (int t = ptid; t < 63 && t < R.len; t += RG2_LOADERS * 32) sG[0][t] -= Gcut << (t + 1);
+            }
+        }
+        t_work += clock64() - t0;
+        __syncthreads();
+    }
+    const long long t_loop = clock64() - t_all;
+    if (warp == W2_WALK) {
+        if (start < R.len) {
+            sink.emit(lane, nch, start, R.len - start, IRM_FORCED_STREAM_END);
+            ++nch;
+        }
+        if (lane == 0) r_count[r] = nch;
+    }
+    if (dbg && (threadIdx.x & 31) == 0 && (warp >= W2_WALK || warp == 0) && R.len > 10000)
+        printf("region-split %lld warp %d work %lld loop %lld tiles %d\n", (long long)r, warp, t_work, t_loop, ntiles);
+}
+
+// fingerprints + compaction (split K1), over every chunk of the batch on every SM: a quad
+// of lanes per chunk (fingerprint.py:28-30), the chunk's region found by binary search
+// over the regions' output offsets r_out (cdc_offsets_kernel)
+__global__ void __launch_bounds__(256)
+cdc_hash_compact_kernel(const uint32_t *__restrict__ tok, const int64_t *__restrict__ n_regions_p,
+                        const Region *__restrict__ regions, const int64_t *__restrict__ r_out,
+                        const int32_t *__restrict__ st_start, const int32_t *__restrict__ st_len,
+                        const uint8_t *__restrict__ st_forced, int32_t *__restrict__ c_start,
+                        int32_t *__restrict__ c_len, uint64_t *__restrict__ c_fp, uint8_t *__restrict__ c_forced) {
+    const int64_t nr = *n_regions_p;
+    const int64_t total = r_out[nr];
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * 64;
+    for (int64_t q0 = (int64_t)blockIdx.x * 64 + (threadIdx.x >> 5) * 8; q0 < total; q0 += stride) {
+        const int64_t q = q0 + (lane >> 2);
+        const bool ok = q < total;
+        int64_t lo = 0, hi = nr - 1;  // last region with r_out[r] <= q
+        while (ok && lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(r_out + mid) <= q) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t src = ok ? regions[lo].cap_off + (q - r_out[lo]) : 0;
+        const int32_t st = ok ? st_start[src] : 0, ln = ok ? st_len[src] : 0;
+        const uint64_t h = xxh64_words_quad(tok + (ok ? regions[lo].stream_begin : 0) + st, ln, 0, lane);
+        if (ok && (lane & 3) == 0) {
+            c_start[q] = st;
+            c_len[q] = ln;
+            c_fp[q] = h;
+            c_forced[q] = st_forced[src];
+        }
+    }
+}
+
 __global__ void __launch_bounds__(PLAN_BLOCK)
 cdc_offsets_kernel(const int64_t *__restrict__ n_regions_p, const int32_t *__restrict__ r_count,
                    int64_t *__restrict__ r_out, const int64_t *__restrict__ r_first,
@@ -488,6 +706,7 @@ struct CdcWs {
     int32_t *r_count, *st_start, *st_len;
     uint8_t *st_forced;
     uint64_t *st_fp;
+    uint64_t *G;
     int64_t bytes;
 };
 
@@ -514,6 +733,7 @@ static CdcWs carve_cdc_ws(void *ws, int64_t n_tokens, int32_t n_streams, int64_t
     w.st_len = (int32_t *)take(smax * sizeof(int32_t));
     w.st_fp = (uint64_t *)take(smax * sizeof(uint64_t));
     w.st_forced = (uint8_t *)take(smax);
+    w.G = (uint64_t *)take(n_tokens * sizeof(uint64_t));
     w.bytes = o;
     return w;
 }
@@ -578,16 +798,39 @@ extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_
                                               min_size, w.regions, w.r_first, w.n_regions);
     IRM_LAUNCH_CHECK();
     const int64_t rmax = (int64_t)n_streams + np;
-    cdc_region_kernel<<<(unsigned)rmax, RG_THREADS, 0, st>>>(
-        tok, w.regions, w.n_regions, gear, mask_exponent, min_size, max_size, w.st_start, w.st_len,
-        w.st_forced, w.st_fp, w.r_count, getenv("IRM_CDC_DEBUG") ? atoi(getenv("IRM_CDC_DEBUG")) : 0);
+    const int dbg = getenv("IRM_CDC_DEBUG") ? atoi(getenv("IRM_CDC_DEBUG")) : 0;
+    // two forms, same results: "fused" (G computed inside the region kernel; many regions in
+    // flight hide its latency) and "split" (G on every SM first, hashing on every SM after;
+    // shortest critical path when a few long regions leave most SMs idle)
+    const char *form = getenv("IRM_CDC_FORM");
+    const bool v1 = form ? strcmp(form, "fused") == 0 : rmax >= sm_count();
+    if (v1) {
+        cdc_region_kernel<<<(unsigned)rmax, RG_THREADS, 0, st>>>(
+            tok, w.regions, w.n_regions, gear, mask_exponent, min_size, max_size, w.st_start, w.st_len,
+            w.st_forced, w.st_fp, w.r_count, dbg);
+    } else {
+        const int64_t gw_tiles = (n_tokens + GW_SUB * 32 - 1) / (GW_SUB * 32);
+        gear_window_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(gw_tiles, (int64_t)sm_count() * 8)),
+                             GW_THREADS, 0, st>>>(tok, n_tokens, gear, w.G);
+        IRM_LAUNCH_CHECK();
+        cdc_region_split_kernel<<<(unsigned)rmax, RG2_THREADS, 0, st>>>(
+            tok, w.G, w.regions, w.n_regions, mask_exponent, min_size, max_size, w.st_start, w.st_len,
+            w.st_forced, w.st_fp, w.r_count, dbg);
+    }
     IRM_LAUNCH_CHECK();
     cdc_offsets_kernel<<<1, PLAN_BLOCK, 0, st>>>(w.n_regions, w.r_count, w.r_out, w.r_first,
                                                  n_streams, chunk_off);
     IRM_LAUNCH_CHECK();
-    cdc_compact_kernel<<<(unsigned)((rmax + 3) / 4), 128, 0, st>>>(
-        w.n_regions, w.regions, w.r_count, w.r_out, w.st_start, w.st_len, w.st_forced, w.st_fp,
-        c_start, c_len, c_fp, c_forced);
+    if (v1) {
+        cdc_compact_kernel<<<(unsigned)((rmax + 3) / 4), 128, 0, st>>>(
+            w.n_regions, w.regions, w.r_count, w.r_out, w.st_start, w.st_len, w.st_forced, w.st_fp,
+            c_start, c_len, c_fp, c_forced);
+    } else {
+        const int64_t blocks = std::min<int64_t>((bound + 63) / 64, (int64_t)sm_count() * 8);
+        cdc_hash_compact_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(
+            tok, w.n_regions, w.regions, w.r_out, w.st_start, w.st_len, w.st_forced, c_start, c_len, c_fp,
+            c_forced);
+    }
     IRM_LAUNCH_CHECK();
     return IRM_OK;
 }

@@ -121,6 +121,13 @@ __device__ __forceinline__ uint64_t xxh64_words_quad(const uint32_t *__restrict_
         return (uint64_t)__ldg(p + 8 * s) | ((uint64_t)__ldg(p + 8 * s + 1) << 32);
     };
     int64_t s = 0;
+    for (; s + 8 <= stripes; s += 8) {  // 8 stripes of loads in flight per lane
+        uint64_t d[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d[u] = rd(s + u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v = xxh_round(v, d[u]);
+    }
     for (; s + 4 <= stripes; s += 4) {
         const uint64_t d0 = rd(s), d1 = rd(s + 1), d2 = rd(s + 2), d3 = rd(s + 3);
         v = xxh_round(v, d0);

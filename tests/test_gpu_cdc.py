@@ -10,11 +10,18 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def pkg():
+@pytest.fixture(scope="module", params=["auto", "fused", "split"])
+def pkg(request):
+    """Both K1 forms (IRM_CDC_FORM, read on every call) and the size-based default."""
+    import os
+
     from paper_2605_05696_b200 import chunking, fingerprint, ops
 
-    return chunking, fingerprint, ops
+    os.environ.pop("IRM_CDC_FORM", None)
+    if request.param != "auto":
+        os.environ["IRM_CDC_FORM"] = request.param
+    yield chunking, fingerprint, ops
+    os.environ.pop("IRM_CDC_FORM", None)
 
 
 def test_gear_table_device(pkg, constants):
