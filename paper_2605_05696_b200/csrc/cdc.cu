@@ -68,14 +68,29 @@ __device__ __forceinline__ int64_t for_each_region(int64_t n, const int64_t *pin
 
 constexpr int PLAN_BLOCK = 1024;
 
-__global__ void __launch_bounds__(PLAN_BLOCK)
-cdc_plan_kernel(const int64_t *__restrict__ stream_off, int32_t n_streams,
-                const int64_t *__restrict__ pin_off, const int64_t *__restrict__ pins,
-                int32_t use_pins, int32_t min_size, Region *__restrict__ regions,
-                int64_t *__restrict__ r_first, int64_t *__restrict__ n_regions) {
-    __shared__ int64_t sm[PLAN_BLOCK / 32];
+struct PlanArgs {
+    const int64_t *stream_off;
+    int32_t n_streams;
+    const int64_t *pin_off, *pins;
+    int32_t use_pins, min_size;
+    Region *regions;
+    int64_t *r_first, *n_regions;
+};
+
+// the region plan of a batch (one CTA of BLOCK threads): regions per stream, their
+// exclusive scan, then one Region record per pin-delimited region
+template <int BLOCK>
+__device__ __forceinline__ void plan_regions(const PlanArgs &a) {
+    const int64_t *__restrict__ stream_off = a.stream_off;
+    const int32_t n_streams = a.n_streams;
+    const int64_t *__restrict__ pin_off = a.pin_off;
+    const int64_t *__restrict__ pins = a.pins;
+    const int32_t use_pins = a.use_pins, min_size = a.min_size;
+    Region *__restrict__ regions = a.regions;
+    int64_t *__restrict__ r_first = a.r_first;
+    __shared__ int64_t sm[BLOCK / 32];
     int64_t carry = 0;
-    for (int32_t s0 = 0; s0 < n_streams; s0 += PLAN_BLOCK) {
+    for (int32_t s0 = 0; s0 < n_streams; s0 += BLOCK) {
         const int32_t s = s0 + threadIdx.x;
         int64_t cnt = 0, n = 0, p0 = 0, np = 0, sb = 0;
         if (s < n_streams) {
@@ -88,7 +103,7 @@ cdc_plan_kernel(const int64_t *__restrict__ stream_off, int32_t n_streams,
             cnt = for_each_region(n, pins + p0, np, [](int64_t, int64_t, int, int64_t) {});
         }
         int64_t tot;
-        const int64_t ex = block_exclusive_scan<PLAN_BLOCK>(cnt, &tot, sm);
+        const int64_t ex = block_exclusive_scan<BLOCK>(cnt, &tot, sm);
         if (s < n_streams) {
             const int64_t rbase = carry + ex;
             r_first[s] = rbase;
@@ -106,9 +121,11 @@ cdc_plan_kernel(const int64_t *__restrict__ stream_off, int32_t n_streams,
     }
     if (threadIdx.x == 0) {
         r_first[n_streams] = carry;
-        *n_regions = carry;
+        *a.n_regions = carry;
     }
 }
+
+__global__ void __launch_bounds__(PLAN_BLOCK) cdc_plan_kernel(PlanArgs a) { plan_regions<PLAN_BLOCK>(a); }
 
 // One CTA per region, four warp roles pipelined over 1024-token tiles:
 //   producers (warps 3..15): windowed G_t of tile i (tokens staged by cp.async
@@ -479,13 +496,19 @@ constexpr int GW_THREADS = 256;
 constexpr int GW_PER = 8;                              // sub-blocks per warp, loads batched
 constexpr int GW_SUB = GW_THREADS / 32 * GW_PER - 2;   // output sub-blocks per CTA (+2 halo in front)
 
+// (its last CTA plans the regions meanwhile: one launch instead of two)
 __global__ void __launch_bounds__(GW_THREADS)
 gear_window_kernel(const uint32_t *__restrict__ tok, int64_t n, const uint64_t *__restrict__ gear,
-                   uint64_t *__restrict__ G) {
+                   uint64_t *__restrict__ G, PlanArgs plan) {
+    if (blockIdx.x == gridDim.x - 1) {
+        plan_regions<GW_THREADS>(plan);
+        return;
+    }
     __shared__ uint64_t sS[(GW_SUB + 2) * 32];
     __shared__ uint64_t sS31[GW_SUB + 2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int64_t base = (int64_t)blockIdx.x * GW_SUB * 32; base < n; base += (int64_t)gridDim.x * GW_SUB * 32) {
+    const int64_t nblk = gridDim.x - 1;
+    for (int64_t base = (int64_t)blockIdx.x * GW_SUB * 32; base < n; base += nblk * GW_SUB * 32) {
         // in-sub-block scans S_j(l) = sum_{i<=l} g_i << (l - i); sub-block j covers base + 32 (j - 2) ..
         // (all token loads of the warp in flight, then all gear lookups, then the scans)
         uint32_t tk[GW_PER];
@@ -615,13 +638,31 @@ cdc_region_split_kernel(const uint32_t *__restrict__ tok, const uint64_t *__rest
 // fingerprints + compaction (split K1), over every chunk of the batch on every SM: a quad
 // of lanes per chunk (fingerprint.py:28-30), the chunk's region found by binary search
 // over the regions' output offsets r_out (cdc_offsets_kernel)
-__global__ void __launch_bounds__(256)
+// The split form runs only for batches of fewer regions than SMs (< HC_THREADS), so every
+// CTA scans the region chunk counts itself (the offsets pass folded in; CTA 0 publishes
+// chunk_off).
+constexpr int HC_THREADS = 256;
+
+__global__ void __launch_bounds__(HC_THREADS)
 cdc_hash_compact_kernel(const uint32_t *__restrict__ tok, const int64_t *__restrict__ n_regions_p,
-                        const Region *__restrict__ regions, const int64_t *__restrict__ r_out,
+                        const Region *__restrict__ regions, const int32_t *__restrict__ r_count,
+                        const int64_t *__restrict__ r_first, int32_t n_streams, int64_t *__restrict__ chunk_off,
                         const int32_t *__restrict__ st_start, const int32_t *__restrict__ st_len,
                         const uint8_t *__restrict__ st_forced, int32_t *__restrict__ c_start,
                         int32_t *__restrict__ c_len, uint64_t *__restrict__ c_fp, uint8_t *__restrict__ c_forced) {
-    const int64_t nr = *n_regions_p;
+    __shared__ int64_t sScan[HC_THREADS / 32];
+    __shared__ int64_t r_out[HC_THREADS + 1];
+    const int64_t nr = *n_regions_p;  // <= HC_THREADS (host-checked bound)
+    {
+        const int64_t c = threadIdx.x < nr ? r_count[threadIdx.x] : 0;
+        int64_t tot;
+        const int64_t ex = block_exclusive_scan<HC_THREADS>(c, &tot, sScan);
+        if (threadIdx.x < nr) r_out[threadIdx.x] = ex;
+        if (threadIdx.x == 0) r_out[nr] = tot;
+        __syncthreads();
+        if (blockIdx.x == 0)
+            for (int32_t s = threadIdx.x; s <= n_streams; s += HC_THREADS) chunk_off[s] = r_out[r_first[s]];
+    }
     const int64_t total = r_out[nr];
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * 64;
@@ -631,7 +672,7 @@ cdc_hash_compact_kernel(const uint32_t *__restrict__ tok, const int64_t *__restr
         int64_t lo = 0, hi = nr - 1;  // last region with r_out[r] <= q
         while (ok && lo < hi) {
             const int64_t mid = (lo + hi + 1) >> 1;
-            if (__ldg(r_out + mid) <= q) lo = mid;
+            if (r_out[mid] <= q) lo = mid;
             else hi = mid - 1;
         }
         const int64_t src = ok ? regions[lo].cap_off + (q - r_out[lo]) : 0;
@@ -794,42 +835,42 @@ extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_
         return IRM_OK;
     }
     const int32_t use_pins = marker_pinned && n_pins > 0;
-    cdc_plan_kernel<<<1, PLAN_BLOCK, 0, st>>>(stream_off, n_streams, pin_off, pins, use_pins,
-                                              min_size, w.regions, w.r_first, w.n_regions);
-    IRM_LAUNCH_CHECK();
+    const PlanArgs plan{stream_off, n_streams, pin_off, pins, use_pins, min_size, w.regions, w.r_first, w.n_regions};
     const int64_t rmax = (int64_t)n_streams + np;
     const int dbg = getenv("IRM_CDC_DEBUG") ? atoi(getenv("IRM_CDC_DEBUG")) : 0;
     // two forms, same results: "fused" (G computed inside the region kernel; many regions in
     // flight hide its latency) and "split" (G on every SM first, hashing on every SM after;
     // shortest critical path when a few long regions leave most SMs idle)
     const char *form = getenv("IRM_CDC_FORM");
-    const bool v1 = form ? strcmp(form, "fused") == 0 : rmax >= sm_count();
+    const bool v1 = (form ? strcmp(form, "fused") == 0 : rmax >= sm_count()) || rmax > HC_THREADS;
     if (v1) {
+        cdc_plan_kernel<<<1, PLAN_BLOCK, 0, st>>>(plan);
+        IRM_LAUNCH_CHECK();
         cdc_region_kernel<<<(unsigned)rmax, RG_THREADS, 0, st>>>(
             tok, w.regions, w.n_regions, gear, mask_exponent, min_size, max_size, w.st_start, w.st_len,
             w.st_forced, w.st_fp, w.r_count, dbg);
     } else {
         const int64_t gw_tiles = (n_tokens + GW_SUB * 32 - 1) / (GW_SUB * 32);
-        gear_window_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(gw_tiles, (int64_t)sm_count() * 8)),
-                             GW_THREADS, 0, st>>>(tok, n_tokens, gear, w.G);
+        gear_window_kernel<<<(unsigned)(std::max<int64_t>(1, std::min<int64_t>(gw_tiles, (int64_t)sm_count() * 8)) + 1),
+                             GW_THREADS, 0, st>>>(tok, n_tokens, gear, w.G, plan);
         IRM_LAUNCH_CHECK();
         cdc_region_split_kernel<<<(unsigned)rmax, RG2_THREADS, 0, st>>>(
             tok, w.G, w.regions, w.n_regions, mask_exponent, min_size, max_size, w.st_start, w.st_len,
             w.st_forced, w.st_fp, w.r_count, dbg);
     }
     IRM_LAUNCH_CHECK();
-    cdc_offsets_kernel<<<1, PLAN_BLOCK, 0, st>>>(w.n_regions, w.r_count, w.r_out, w.r_first,
-                                                 n_streams, chunk_off);
-    IRM_LAUNCH_CHECK();
     if (v1) {
+        cdc_offsets_kernel<<<1, PLAN_BLOCK, 0, st>>>(w.n_regions, w.r_count, w.r_out, w.r_first,
+                                                     n_streams, chunk_off);
+        IRM_LAUNCH_CHECK();
         cdc_compact_kernel<<<(unsigned)((rmax + 3) / 4), 128, 0, st>>>(
             w.n_regions, w.regions, w.r_count, w.r_out, w.st_start, w.st_len, w.st_forced, w.st_fp,
             c_start, c_len, c_fp, c_forced);
     } else {
         const int64_t blocks = std::min<int64_t>((bound + 63) / 64, (int64_t)sm_count() * 8);
-        cdc_hash_compact_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(
-            tok, w.n_regions, w.regions, w.r_out, w.st_start, w.st_len, w.st_forced, c_start, c_len, c_fp,
-            c_forced);
+        cdc_hash_compact_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), HC_THREADS, 0, st>>>(
+            tok, w.n_regions, w.regions, w.r_count, w.r_first, n_streams, chunk_off, w.st_start, w.st_len,
+            w.st_forced, c_start, c_len, c_fp, c_forced);
     }
     IRM_LAUNCH_CHECK();
     return IRM_OK;
