@@ -215,8 +215,12 @@ def run_ours(args):
         step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_sharded(i))
     else:
         step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_eager() if cold else pipe.replay())
-    # cold request wave: inserts the body (its pool rows hold the random latents)
+    # cold request wave: inserts the body (its pool rows hold the random latents); the
+    # library's launch counter around this eager wave = our kernels per wave (the graphs
+    # replay the same launches)
+    lc0 = ops.launch_count()
     step(len(dev_in) - 1, cold=True)
+    launches_per_wave = ops.launch_count() - lc0
     torch.cuda.synchronize()
     overlapped = not args.serial
     if not sharded:
@@ -391,7 +395,7 @@ def run_ours(args):
         # our kernels per wave (ncu launch list, profiles/r01e_launches.csv): K1 plan / offsets /
         # region / compact, K3 claim / decide / blockscan / commit / resolve, K4 cossin + gather;
         # sharded: + the replica map store's 5 and irm_copy_runs
-        "gpu_launches": args.steps * (17 if sharded else 11),
+        "gpu_launches": args.steps * launches_per_wave,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:  # the CPU leg: rank 0 at N = 1 only

@@ -54,6 +54,9 @@ typedef struct CUstream_st *irm_stream_t; /* == cudaStream_t */
 int irm_abi_version(void);
 const char *irm_last_error(void);
 int irm_device_sm_count(void);
+/* Kernels this library has launched (or recorded into a CUDA graph being
+ * captured) in this process: the caller's evidence of its own GPU launches. */
+int64_t irm_launch_count(void);
 
 /* ---- constants (rng.py:17-38, chunking.py:64-86) ---------------------- */
 /* Gear table: out[i] = splitmix64 output i+1 of `seed`, 65,536 entries.

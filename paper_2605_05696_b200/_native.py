@@ -47,6 +47,7 @@ _SIGS = {
     "irm_abi_version": ([], i32),
     "irm_last_error": ([], ctypes.c_char_p),
     "irm_device_sm_count": ([], i32),
+    "irm_launch_count": ([], i64),
     "irm_gear_table": ([u64, P, P], i32),
     "irm_cdc_chunk_bound": ([i64, i32, i64, i32], i64),
     "irm_cdc_workspace_bytes": ([i64, i32, i64, i32], i64),

@@ -30,7 +30,13 @@ void set_error(const char *fmt, ...);
         }                                                                           \
     } while (0)
 
-#define IRM_LAUNCH_CHECK() IRM_CUDA_CHECK(cudaGetLastError())
+// after every kernel launch of the library (one per launch): counts it, checks it
+void count_launch();
+#define IRM_LAUNCH_CHECK()          \
+    do {                            \
+        ::irm::count_launch();      \
+        IRM_CUDA_CHECK(cudaGetLastError()); \
+    } while (0)
 
 int sm_count();
 

@@ -185,6 +185,11 @@ def copy_runs(src_addr: torch.Tensor, src_layer_stride: int, dst_pool: torch.Ten
     N.check(rc, "irm_copy_runs")
 
 
+def launch_count() -> int:
+    """Kernels the library has launched or recorded into a captured graph (process-wide)."""
+    return int(N.lib().irm_launch_count())
+
+
 def set_rotate_gather_sm_limit(n_sms: int) -> None:
     """Spread later K4 launches over at most ``n_sms`` SMs (0 = all)."""
     N.check(N.lib().irm_rotate_gather_set_sm_limit(int(n_sms)), "irm_rotate_gather_set_sm_limit")
