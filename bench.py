@@ -385,7 +385,9 @@ def run_ours(args):
                          "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm, "unit": "GB/s",
                                       "frac": k1_gbs / hbm}},
             "cdc_hash_wide": cdc_wide_component(hbm),
-            "fused_attn": fused_attn_component(args, tf_burst, peak_kind) if not args.no_attn else None,
+            "fused_attn": fused_attn_component(args, tf_burst, peak_kind,
+                                               cpu=rank == 0 and world == 1 and not args.no_cpu)
+            if not args.no_attn else None,
             # the north star's "DeepSeek-V2-Lite shapes": config 2's 32K context, DSv2 interleaved rotary
             "fused_attn_dsv2": fused_attn_component(args, tf_burst, peak_kind, n_ctx=32768, n_q=4096, theta=1e4,
                                                     layout=N.LAYOUT_INTERLEAVED, shape="config 2")
@@ -449,7 +451,7 @@ def cdc_wide_component(hbm, n_streams=296, n_tok=32768):
 
 # ----------------------------------------------------------------- K5 component
 def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=16, theta=5e4, layout=None,
-                         shape="config 3"):
+                         shape="config 3", cpu=False):
     """BASELINE.json config 3 (Moonlight-16B-A3B shape, DSv3-form half-split
     rotary, theta 5e4): a 64K-token prompt = 512-token prefix + 63 marker-wrapped
     1K-token documents re-permuted relative to the cached order (the rerank
@@ -506,7 +508,11 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
     pos = np.arange(n_ctx - n_q, n_ctx, dtype=np.float64)
     flops = heads * float((pos + 1).sum()) * 2176  # (2*576 + 2*512) per visible (query, key, head)
     tflops = flops / (ms / 1e3) / 1e12
-    return {"value": tflops, "unit": "TFLOP/s", "kernel": "irm_mla_reattach_prefill (K5, tcgen05/TMEM)",
+    extra = {}
+    if cpu:
+        extra["cpu_baseline"] = attn_cpu_baseline(q, pool, kv_rows, chunk_of_key, np.array(deltas, np.int64), theta,
+                                                  layout == N.LAYOUT_INTERLEAVED, n_ctx, n_q)
+    return {**extra, "value": tflops, "unit": "TFLOP/s", "kernel": "irm_mla_reattach_prefill (K5, tcgen05/TMEM)",
             "workload": f"{shape}: {n_ctx} ctx, last {n_q} queries, {heads} heads, {n_docs} re-permuted docs, "
                         f"{'DSv2 interleaved' if layout == N.LAYOUT_INTERLEAVED else 'DSv3 half-split'} theta {theta:g}, bf16",
             "launch_ms": ms, "flop_per_launch": flops,
@@ -515,6 +521,42 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
 
 
 # ----------------------------------------------------------------- CPU legs
+def attn_cpu_baseline(q, pool, kv_rows, chunk_of_key, deltas, theta, interleaved, n_ctx, n_q, sample_q=64):
+    """K5 has no reference CPU path: the restated absorbed MLA
+    reattach prefill in torch-CPU fp32 on all host threads, for the last
+    `sample_q` queries of the same workload (same bf16 inputs, keys gathered
+    from the pool and their k_r rotated by each document's delta). TFLOP/s
+    counts the same causally visible FLOPs as the kernel's figure."""
+    import torch
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    kv = pool.float().cpu()[torch.from_numpy(kv_rows)]  # [n_ctx, 576] in request order
+    inv = torch.from_numpy(np.power(theta, -2.0 * np.arange(32) / 64))
+    ang = (torch.from_numpy(deltas[chunk_of_key]).double()[:, None] * inv[None, :]).float()
+    c, s_ = torch.cos(ang), torch.sin(ang)
+    kr = kv[:, 512:]
+    lo, hi = (kr[:, 0::2], kr[:, 1::2]) if interleaved else (kr[:, :32], kr[:, 32:])
+    rlo, rhi = lo * c - hi * s_, lo * s_ + hi * c
+    if interleaved:
+        kr = torch.stack([rlo, rhi], dim=-1).reshape(-1, 64)
+    else:
+        kr = torch.cat([rlo, rhi], dim=1)
+    k = torch.cat([kv[:, :512], kr], dim=1)
+    qs = q[n_q - sample_q:].float().cpu()  # [sample_q, H, 576], positions n_ctx - sample_q ..
+    heads = qs.shape[1]
+    sc = torch.einsum("qhd,kd->qhk", qs, k) * 192 ** -0.5
+    pos = torch.arange(n_ctx - sample_q, n_ctx)
+    sc.masked_fill_(torch.arange(n_ctx)[None, None, :] > pos[:, None, None], float("-inf"))
+    out = torch.einsum("qhk,kd->qhd", torch.softmax(sc, dim=-1), kv[:, :512])
+    dt = time.perf_counter() - t0
+    flops = heads * float((pos + 1).sum()) * 2176
+    assert torch.isfinite(out).all()
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": torch.get_num_threads(), "kind": "restated",
+            "sample": f"last {sample_q} of {n_q} queries x {heads} heads over {n_ctx} keys, torch-CPU fp32 "
+                      f"(gather, delta rotation, causal softmax; {dt:.2f} s)"}
+
+
 def cpu_baseline(args, packed, sample_requests=1, n_threads=0):
     """The oracle port (restated reference, oracle/irm_oracle.c) on host cores:
     CDC + xxh64, dict lookup, bf16 rotate+gather for `sample_requests` requests
