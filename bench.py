@@ -304,19 +304,24 @@ def run_ours(args):
     step(args.warmup)
     torch.cuda.synchronize()
     k4_rows = int(pipe.length.sum().item()) * LAYERS
+    n_queries = int(pipe.table.chunk_off[-1].item())  # K3 probes per wave (chunks of the wave)
     if sharded:
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         ev[0].record()
         pipe.k1()
         ev[1].record()
         ev[2].record()
         pipe.k4()
         ev[3].record()
+        ev[4].record()
+        pipe.k3_sharded(10**6)  # the same chunks again under fresh order keys: all hits
+        ev[5].record()
         torch.cuda.synchronize()
-        k1, k4 = ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])
+        k1, k4, k3 = ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3]), ev[4].elapsed_time(ev[5])
     else:
         k1 = time_graph(pipe.graph_k1)
         k4 = time_graph(pipe.graph_k4)
+        k3 = time_graph(pipe.graph_k3)
 
     # -------- e2e: the same pipeline fed from pinned host buffers, result read back
     bi = sum(t.numel() * t.element_size() for t in host_in[0])
@@ -385,6 +390,12 @@ def run_ours(args):
                          "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm, "unit": "GB/s",
                                       "frac": k1_gbs / hbm}},
             "cdc_hash_wide": cdc_wide_component(hbm),
+            # K3 / K6 are latency-bound: queries/s and the step's ms, no roofline
+            "store_lookup": {"value": n_queries / (k3 / 1e3), "unit": "queries/s", "launch_ms": k3,
+                             "queries_per_launch": n_queries,
+                             "kernel": "irm_store_lookup_insert (K3)" + (
+                                 f" + 2 NCCL all-to-alls over {world} rank(s) (K6)" if sharded else ""),
+                             "note": "a re-probe of a stored wave (all hits), per-chunk glue included"},
             "fused_attn": fused_attn_component(args, tf_burst, peak_kind,
                                                cpu=rank == 0 and world == 1 and not args.no_cpu)
             if not args.no_attn else None,

@@ -213,7 +213,7 @@ class ReattachPipeline:
 
     # ------------------------------------------------------------ graphs
     def capture(self, warmup: int = 2):
-        """Capture the step (and K1-only / K4-only graphs for component timing)."""
+        """Capture the step (and K1-, K3- and K4-only graphs for component timing)."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -231,6 +231,11 @@ class ReattachPipeline:
         self.graph_k4 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph_k4, pool=pool):
             self.k4()
+        self.graph_k3 = torch.cuda.CUDAGraph()  # replays re-probe the same wave: all hits, no inserts
+        live = dict(self.__dict__)
+        with torch.cuda.graph(self.graph_k3, pool=pool):
+            self.k3()
+        self.__dict__.update(live)  # k3 rebinds its outputs: the step graph's buffers stay the live ones
         torch.cuda.synchronize()
 
     def _alloc_slots(self):
