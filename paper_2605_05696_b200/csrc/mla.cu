@@ -1036,14 +1036,20 @@ mla_reattach_2sm_kernel(Params p, const __grid_constant__ CUtensorMap tmap_pool,
 namespace p3 {
 using namespace p2;
 #undef IRM_MLA_QT_V3
-constexpr int QT = 5;
+#ifndef IRM_MLA_V3_QT
+#define IRM_MLA_V3_QT 5
+#endif
+#ifndef IRM_MLA_V3_NS
+#define IRM_MLA_V3_NS 3
+#endif
+constexpr int QT = IRM_MLA_V3_QT;
 #ifndef IRM_MLA_V3_KST
 #define IRM_MLA_V3_KST 4
 #endif
 #ifndef IRM_MLA_V3_NP
 #define IRM_MLA_V3_NP 2
 #endif
-constexpr int KST = IRM_MLA_V3_KST, NS = 3;
+constexpr int KST = IRM_MLA_V3_KST, NS = IRM_MLA_V3_NS;  // S buffers: QK runs NS - 1 tiles ahead
 constexpr int NP = IRM_MLA_V3_NP;  // P buffers: 1 frees smem for a fifth K stage
 constexpr int S_Q = 0, S_K = (NPIECE - QT) * QPIECE, S_P = S_K + KST * KTILE;
 constexpr int SMEM3 = S_P + NP * PTILE2;  // 192 KB (4 K stages, 2 P buffers)
@@ -1251,10 +1257,9 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
                 }
                 __syncwarp();
             };
-            issue_qk(0);
-            if (T > 1) issue_qk(1);
+            for (int t = 0; t < NS - 1 && t < T; ++t) issue_qk(t);
             for (int t = 0; t < T; ++t) {
-                if (t + 2 < T) issue_qk(t + 2);  // S(t+2) reuses the buffer softmax(t-1) has read
+                if (t + NS - 1 < T) issue_qk(t + NS - 1);  // reuses the S buffer softmax(t-1) has read
                 const int st = t % KST;
                 long long a0 = prof_clock<2>();
                 mbar_wait(&b_pfull[t & 1], (t >> 1) & 1);
