@@ -394,7 +394,7 @@ def run_ours(args):
             "store_lookup": {"value": n_queries / (k3 / 1e3), "unit": "queries/s", "launch_ms": k3,
                              "queries_per_launch": n_queries,
                              "kernel": "irm_store_lookup_insert (K3)" + (
-                                 f" + 2 NCCL all-to-alls over {world} rank(s) (K6)" if sharded else ""),
+                                 f" + 2 {backend} all-to-alls over {world} rank(s) (K6)" if sharded else ""),
                              "note": "a re-probe of a stored wave (all hits), per-chunk glue included"},
             "fused_attn": fused_attn_component(args, tf_burst, peak_kind,
                                                cpu=rank == 0 and world == 1 and not args.no_cpu)
