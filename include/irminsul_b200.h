@@ -180,6 +180,22 @@ int irm_store_lookup_insert(const irm_store_view *st, const uint64_t *q_fp,
 /* Read-only batched lookup (registry.py:116-117): q_entry = -1 on miss. */
 int irm_store_lookup(const irm_store_view *st, const uint64_t *q_fp, int64_t n, int64_t *q_entry,
                      irm_stream_t stream);
+/* Warm-serve step glue around K3 (engine.py:181-223 batched over a wave of
+ * n_req requests whose chunk table is CSR chunk_off[n_req+1], cap slots):
+ * irm_wave_plan gives, per slot i < cap, req[i] = the owning request (clamped
+ * to n_req-1 past the end), p_abs[i] = meta_len[req] + start[i], probe[i] =
+ * (i < chunk_off[n_req] && p_abs >= carve) (the carve-out, engine.py:186-189),
+ * order[i] = order0 + i. irm_wave_compact lists the slots with hit[i] == 1 in
+ * slot order as K4 work (src = row, dst = req*req_stride + p_abs, len,
+ * delta = p_abs - p_src), n_hit[0] = their count, length_out[i] = len if hit
+ * else 0, and adds the hit tokens to *hit_tokens (if not null). */
+int irm_wave_plan(const int64_t *chunk_off, int32_t n_req, const int32_t *start, const int64_t *meta_len,
+                  int64_t cap, int64_t carve, int64_t order0, int64_t *req, int64_t *p_abs, uint8_t *probe,
+                  int64_t *order, irm_stream_t stream);
+int irm_wave_compact(const int32_t *hit, const int64_t *row, const int64_t *req, const int64_t *p_abs,
+                     const int64_t *p_src, const int32_t *len, int64_t cap, int64_t req_stride, int64_t *src_out,
+                     int64_t *dst_out, int32_t *len_out, int64_t *delta_out, int64_t *n_hit, int32_t *length_out,
+                     int64_t *hit_tokens, irm_stream_t stream);
 
 /* ---- K4: delta-rotation rotate + gather (registry.py:146-166) ----------
  * For each chunk c and layer l: rows [src_row[c], +len[c]) of the pool are

@@ -11,6 +11,7 @@
 // pool rows of new entries are assigned by an exclusive scan in query order,
 // so insert_epoch (registry.py:83,137) and pool layout are deterministic.
 #include "common.cuh"
+#include <algorithm>
 
 namespace irm {
 
@@ -294,6 +295,100 @@ extern "C" int irm_store_lookup(const irm_store_view *st, const uint64_t *q_fp, 
     IRM_REQUIRE(q_fp && q_entry, "null query arrays");
     store_lookup_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*st, q_fp, n,
                                                                                       q_entry);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+// ---------------------------------------------------------------- wave plan / hit compaction
+// The per-chunk glue around K3 in the warm-serve step (engine.py:181-223 batched over a
+// wave): which request owns each chunk slot, its absolute position, whether it is probed
+// (carve-out, engine.py:186-189), its global order key; and after the lookup, the hits
+// compacted in slot order into K4's work list with their count left on the device.
+namespace irm {
+
+__global__ void wave_plan_kernel(const int64_t *__restrict__ chunk_off, int32_t n_req,
+                                 const int32_t *__restrict__ start, const int64_t *__restrict__ meta_len,
+                                 int64_t cap, int64_t carve, int64_t order0, int64_t *__restrict__ req,
+                                 int64_t *__restrict__ p_abs, uint8_t *__restrict__ probe,
+                                 int64_t *__restrict__ order) {
+    const int64_t total = chunk_off[n_req];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = n_req - 1;  // the last request with chunk_off[r] <= i (clamped)
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(chunk_off + mid) <= i) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t p = __ldg(meta_len + lo) + start[i];
+        req[i] = lo;
+        p_abs[i] = p;
+        probe[i] = (i < total && p >= carve) ? 1 : 0;
+        order[i] = order0 + i;
+    }
+}
+
+constexpr int WC_BLOCK = 1024;
+
+__global__ void __launch_bounds__(WC_BLOCK)
+wave_compact_kernel(const int32_t *__restrict__ hit, const int64_t *__restrict__ row,
+                    const int64_t *__restrict__ req, const int64_t *__restrict__ p_abs,
+                    const int64_t *__restrict__ p_src, const int32_t *__restrict__ len, int64_t cap,
+                    int64_t req_stride, int64_t *__restrict__ src_out, int64_t *__restrict__ dst_out,
+                    int32_t *__restrict__ len_out, int64_t *__restrict__ delta_out, int64_t *__restrict__ n_hit,
+                    int32_t *__restrict__ length_out, int64_t *__restrict__ hit_tokens) {
+    __shared__ int64_t sm[WC_BLOCK / 32];
+    int64_t base = 0, tokens = 0;
+    for (int64_t i0 = 0; i0 < cap; i0 += WC_BLOCK) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool h = i < cap && hit[i] == 1;
+        const int32_t l = i < cap ? len[i] : 0;
+        if (i < cap) length_out[i] = h ? l : 0;
+        int64_t tot;
+        const int64_t k = base + block_exclusive_scan<WC_BLOCK>(h ? 1 : 0, &tot, sm);
+        if (h) {
+            const int64_t pa = p_abs[i];
+            src_out[k] = row[i];
+            dst_out[k] = req[i] * req_stride + pa;
+            len_out[k] = l;
+            delta_out[k] = pa - p_src[i];
+            tokens += l;
+        }
+        base += tot;
+    }
+    int64_t ttot;
+    block_exclusive_scan<WC_BLOCK>(tokens, &ttot, sm);
+    if (threadIdx.x == 0) {
+        *n_hit = base;
+        if (hit_tokens) *hit_tokens += ttot;
+    }
+}
+
+}  // namespace irm
+
+extern "C" int irm_wave_plan(const int64_t *chunk_off, int32_t n_req, const int32_t *start,
+                             const int64_t *meta_len, int64_t cap, int64_t carve, int64_t order0, int64_t *req,
+                             int64_t *p_abs, uint8_t *probe, int64_t *order, irm_stream_t stream) {
+    IRM_REQUIRE(n_req >= 1 && cap >= 0, "bad sizes");
+    if (cap == 0) return IRM_OK;
+    IRM_REQUIRE(chunk_off && start && meta_len && req && p_abs && probe && order, "null pointer");
+    const int64_t grid = std::min<int64_t>((cap + 255) / 256, (int64_t)irm::sm_count() * 4);
+    irm::wave_plan_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(chunk_off, n_req, start, meta_len, cap,
+                                                                            carve, order0, req, p_abs, probe, order);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+extern "C" int irm_wave_compact(const int32_t *hit, const int64_t *row, const int64_t *req, const int64_t *p_abs,
+                                const int64_t *p_src, const int32_t *len, int64_t cap, int64_t req_stride,
+                                int64_t *src_out, int64_t *dst_out, int32_t *len_out, int64_t *delta_out,
+                                int64_t *n_hit, int32_t *length_out, int64_t *hit_tokens, irm_stream_t stream) {
+    IRM_REQUIRE(cap >= 0 && req_stride >= 0, "bad sizes");
+    IRM_REQUIRE(n_hit && (cap == 0 || (hit && row && req && p_abs && p_src && len && src_out && dst_out &&
+                                       len_out && delta_out && length_out)),
+                "null pointer");
+    irm::wave_compact_kernel<<<1, irm::WC_BLOCK, 0, (cudaStream_t)stream>>>(
+        hit, row, req, p_abs, p_src, len, cap, req_stride, src_out, dst_out, len_out, delta_out, n_hit, length_out,
+        hit_tokens);
     IRM_LAUNCH_CHECK();
     return IRM_OK;
 }

@@ -283,6 +283,25 @@ class ChunkStore:
         return c[0], c[1], c[2]
 
 
+def wave_plan(chunk_off: torch.Tensor, n_req: int, start: torch.Tensor, meta_len: torch.Tensor, carve: int,
+              order0: int, req: torch.Tensor, p_abs: torch.Tensor, probe: torch.Tensor, order: torch.Tensor) -> None:
+    """irm_wave_plan: per chunk slot, owning request, absolute position, probe flag, order key."""
+    N.check(N.lib().irm_wave_plan(N.ptr(chunk_off), int(n_req), N.ptr(start), N.ptr(meta_len), start.numel(),
+                                  int(carve), int(order0), N.ptr(req), N.ptr(p_abs), N.ptr(probe), N.ptr(order),
+                                  N.stream_ptr()), "irm_wave_plan")
+
+
+def wave_compact(hit: torch.Tensor, row: torch.Tensor, req: torch.Tensor, p_abs: torch.Tensor, p_src: torch.Tensor,
+                 length: torch.Tensor, req_stride: int, src_out: torch.Tensor, dst_out: torch.Tensor,
+                 len_out: torch.Tensor, delta_out: torch.Tensor, n_hit: torch.Tensor, length_out: torch.Tensor,
+                 hit_tokens: torch.Tensor | None = None) -> None:
+    """irm_wave_compact: the hit slots, in slot order, as K4 work; their count on the device."""
+    N.check(N.lib().irm_wave_compact(N.ptr(hit), N.ptr(row), N.ptr(req), N.ptr(p_abs), N.ptr(p_src), N.ptr(length),
+                                     hit.numel(), int(req_stride), N.ptr(src_out), N.ptr(dst_out), N.ptr(len_out),
+                                     N.ptr(delta_out), N.ptr(n_hit), N.ptr(length_out), N.ptr(hit_tokens),
+                                     N.stream_ptr()), "irm_wave_compact")
+
+
 # ------------------------------------------------------------------ K5: fused MLA reattach prefill
 def chunk_cossin(delta: torch.Tensor, inv_freq: torch.Tensor) -> torch.Tensor:
     """Per-chunk (cos, sin)(delta * inv_freq[j]) from fp64 angles -> float32 [n_chunks, 32, 2]."""

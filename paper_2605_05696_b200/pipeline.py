@@ -72,39 +72,49 @@ class ReattachPipeline:
         self.table = ops.cdc_xxh64(self.tok, self.stream_off, self.pin_off, self.pins, k, mn, mx, True,
                                    ws=self.cdc_ws, n_tokens=self.max_tokens, n_pins=self.max_pins)
 
-    def k3(self):
+    def _plan(self):
+        """Per-slot request / absolute position / probe flag / order key of the wave
+        (irm_wave_plan: the glue of engine.py:181-189, one launch)."""
         t = self.table
         cap = t.start.numel()
-        idx = torch.arange(cap, device=t.start.device)
-        req = torch.searchsorted(t.chunk_off[1:], idx, right=True)
-        valid = idx < t.chunk_off[-1]
-        self.reqc = torch.clamp(req, max=self.R - 1)
-        self.p_abs = self.m[self.reqc] + t.start.to(torch.int64)
-        probe = (valid & (self.p_abs >= self.carve)).to(torch.uint8)
-        order = self.order0 + idx
+        dev = t.start.device
+        self.reqc = torch.empty(cap, dtype=torch.int64, device=dev)
+        self.p_abs = torch.empty(cap, dtype=torch.int64, device=dev)
+        probe = torch.empty(cap, dtype=torch.uint8, device=dev)
+        order = torch.empty(cap, dtype=torch.int64, device=dev)
+        ops.wave_plan(t.chunk_off, self.R, t.start, self.m, self.carve, self.order0, self.reqc, self.p_abs, probe,
+                      order)
+        return probe, order
+
+    def k3(self):
+        t = self.table
+        probe, order = self._plan()
         self.hit, self.entry, self.p_src, self.row = self.store.lookup_insert(t.fp, order, self.p_abs,
                                                                               t.length, probe)
-        is_hit = self.hit == 1
-        self.length = torch.where(is_hit, t.length, torch.zeros_like(t.length))
-        self._compact(is_hit, self.row, self.reqc * self.req_stride + self.p_abs, self.p_abs - self.p_src)
+        self._compact(self.row)
 
-    def _compact(self, is_hit, src, dst, delta):
-        """PIC hits first (stable), with their count left on the device: K4 then
-        walks only real work and the step stays free of host synchronisation."""
-        perm = torch.argsort((~is_hit).to(torch.int8), stable=True)
+    def _compact(self, src):
+        """PIC hits first, in slot order, with their count left on the device
+        (irm_wave_compact, one launch): K4 then walks only real work and the step
+        stays free of host synchronisation."""
+        t = self.table
+        cap = t.start.numel()
+        dev = t.start.device
+        self.length = torch.empty(cap, dtype=torch.int32, device=dev)
         if self.fill_slot is None:
-            self.k4_src, self.k4_dst = src[perm], dst[perm]
-            self.k4_len, self.k4_delta = self.length[perm], delta[perm]
-            self.n_hit = is_hit.sum().reshape(1).to(torch.int64)
+            self.k4_src = torch.empty(cap, dtype=torch.int64, device=dev)
+            self.k4_dst = torch.empty(cap, dtype=torch.int64, device=dev)
+            self.k4_len = torch.empty(cap, dtype=torch.int32, device=dev)
+            self.k4_delta = torch.empty(cap, dtype=torch.int64, device=dev)
+            self.n_hit = torch.empty(1, dtype=torch.int64, device=dev)
+            ops.wave_compact(self.hit, src, self.reqc, self.p_abs, self.p_src, t.length, self.req_stride,
+                             self.k4_src, self.k4_dst, self.k4_len, self.k4_delta, self.n_hit, self.length)
             return
         sl = self.slots[self.fill_slot]  # overlapped mode: static per-slot buffers
-        torch.index_select(src, 0, perm, out=sl["src"])
-        torch.index_select(dst, 0, perm, out=sl["dst"])
-        torch.index_select(self.length, 0, perm, out=sl["len"])
-        torch.index_select(delta, 0, perm, out=sl["delta"])
-        sl["n_hit"].copy_(is_hit.sum().reshape(1))
+        ops.wave_compact(self.hit, src, self.reqc, self.p_abs, self.p_src, t.length, self.req_stride,
+                         sl["src"], sl["dst"], sl["len"], sl["delta"], sl["n_hit"], self.length,
+                         hit_tokens=self.hit_tokens)
         sl["hit"].copy_(self.hit)
-        self.hit_tokens += self.length.sum(dtype=torch.int64)
 
     def k4(self, slot: int | None = None):
         if slot is None:
@@ -142,11 +152,8 @@ class ReattachPipeline:
         cap = t.start.numel()
         dev = t.start.device
         idx = torch.arange(cap, device=dev)
-        req = torch.searchsorted(t.chunk_off[1:], idx, right=True)
-        valid = idx < t.chunk_off[-1]
-        self.reqc = torch.clamp(req, max=self.R - 1)
-        self.p_abs = self.m[self.reqc] + t.start.to(torch.int64)
-        probe = valid & (self.p_abs >= self.carve)
+        probe, _ = self._plan()
+        probe = probe.to(torch.bool)
         # global order: (global request = (wave * R + r) * G + rank, chunk index within the request);
         # wave: an int, or a device scalar (graph-captured fronts advance it on the device)
         g_req = (wave * self.R + self.reqc) * self.world + self.rank
@@ -155,9 +162,9 @@ class ReattachPipeline:
         self.hit = hit
         self.grow = grow  # novel chunks: the rows of this rank's pool that keep their KV (prefill writes them)
         is_hit = hit == 1
-        self.length = torch.where(is_hit, t.length, torch.zeros_like(t.length))
-        src = self.replica.localize(torch.where(is_hit, grow, torch.full_like(grow, -1)), self.length)
-        self._compact(is_hit, src, self.reqc * self.req_stride + self.p_abs, self.p_abs - self.p_src)
+        src = self.replica.localize(torch.where(is_hit, grow, torch.full_like(grow, -1)),
+                                    torch.where(is_hit, t.length, torch.zeros_like(t.length)))
+        self._compact(src)
 
     def step_sharded(self, wave: int):
         self.k1()
