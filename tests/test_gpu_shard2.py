@@ -1,15 +1,15 @@
-"""GPU, world size 2 on one B200 (two processes on cuda:0, gloo carrying the
+"""GPU, world sizes 2 and 4 on one B200 (processes on cuda:0, gloo carrying the
 all-to-alls on CUDA tensors; NCCL cannot put two ranks on one GPU): the
 sharded production step (pipeline.ReattachPipeline.run_overlapped_sharded, the
 path bench.py times at N > 1) against one sequential first-writer-wins oracle
-over both ranks' requests in global order (wave, request, rank), with the
+over all ranks' requests in global order (wave, request, rank), with the
 chunks of each request in order (engine.py:181-226).
 
 Checked on every rank and wave: the per-chunk service map (hit / novel /
 carve-out) bit-exact, and every hit row of the per-request KV output against
 the oracle's bf16 rotate+gather (registry.py:146-166) of the FIRST WRITER's
 pool rows, c_KV bit-exact and k_r within bf16 rounding. Hits whose first
-writer is the other rank read rows fetched peer-to-peer into the replica
+writer is another rank read rows fetched peer-to-peer into the replica
 region (CUDA IPC mapping of the peer pool, irm_copy_runs)."""
 
 import os
@@ -21,7 +21,6 @@ import torch
 import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
-WORLD = 2
 
 
 def _free_port():
@@ -32,7 +31,7 @@ def _free_port():
     return port
 
 
-def global_oracle(all_waves, novel_rows):
+def global_oracle(all_waves, novel_rows, WORLD):
     """Per rank, per wave: chunk records (code, writer, row, p_src, p, len, request)."""
     from oracle import oracle as O
     from test_gpu_pipeline import CARVE
@@ -82,7 +81,7 @@ def global_oracle(all_waves, novel_rows):
     return out
 
 
-def _worker(rank, port, out_q):
+def _worker(rank, WORLD, port, out_q):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -97,8 +96,8 @@ def _worker(rank, port, out_q):
         from paper_2605_05696_b200.pipeline import ReattachPipeline
 
         all_waves = [make_waves(seed=11 + k) for k in range(WORLD)]
-        novel_rows = 2 * 12000
-        ref = global_oracle(all_waves, novel_rows)
+        novel_rows = WORLD * 12000  # 12K first-writer rows per (owner, writer) sub-range
+        ref = global_oracle(all_waves, novel_rows, WORLD)
         waves = all_waves[rank]
         gen = torch.Generator(device="cuda").manual_seed(3 + rank)
         pool = torch.randn(LAYERS, novel_rows + 8192, 576, device="cuda", generator=gen).to(torch.bfloat16)
@@ -115,7 +114,7 @@ def _worker(rank, port, out_q):
                              rank, WORLD)
         dev = [to_dev(w) for w in waves]
         pipe.load(*dev[0])
-        pipe.step_sharded(0)  # cold wave: rank 0 writes the body first, rank 1 fetches it
+        pipe.step_sharded(0)  # cold wave: rank 0 writes the body first, the others fetch it
         hits, outs = {}, {}
         pipe.run_overlapped_sharded(WAVES, lambda i: pipe.load(*dev[1 + i]), wave0=1, k4_sms=100,
                                     after_front=lambda i, s: hits.__setitem__(i, pipe.slots[s]["hit"].clone()),
@@ -149,7 +148,7 @@ def _worker(rank, port, out_q):
                 f = lambda u: (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
                 g, e = f(out_u16[:, rws, 512:]), f(exp[:, rws, 512:])
                 assert np.abs(g - e).max() <= 2.0 ** -7 * np.abs(e).max(), (rank, i, writer)
-        # rank 1's hits on the body were first written by rank 0: they went through the replica
+        # the other ranks' hits on the body were first written by rank 0: they went through the replica
         assert rank == 0 or n_remote > 0
         out_q.put((rank, "ok", int(pipe.replica.fetched_rows)))
     except Exception as e:  # report, then still meet the other rank at the barrier
@@ -157,24 +156,25 @@ def _worker(rank, port, out_q):
 
         out_q.put((rank, traceback.format_exc()[-2000:], -1))
     finally:
-        dist.barrier()  # keep both pools mapped until both ranks have read
+        dist.barrier()  # keep every pool mapped until every rank has read
         dist.destroy_process_group()
 
 
-def test_sharded_pipeline_world2_one_gpu():
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_pipeline_one_gpu(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
     outs = {}
-    for _ in range(WORLD):
+    for _ in range(world):
         rank, msg, fetched = q.get(timeout=600)
         outs[rank] = (msg, fetched)
     for pr in procs:
         pr.join(timeout=120)
     assert all(m == "ok" for m, _ in outs.values()), outs
-    assert outs[1][1] > 0, "rank 1 must have fetched the body from rank 0's pool"
+    assert all(outs[r][1] > 0 for r in range(1, world)), "ranks > 0 must fetch the body from rank 0's pool"
     for pr in procs:
         assert pr.exitcode == 0
