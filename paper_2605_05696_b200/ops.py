@@ -283,9 +283,21 @@ class ChunkStore:
         return c[0], c[1], c[2]
 
 
+def _expect(pairs, what: str) -> None:
+    for t, dt in pairs:
+        if t.dtype != dt or not t.is_contiguous() or not t.is_cuda:
+            raise ValueError(f"{what}: expected a contiguous CUDA {dt} tensor, got {t.dtype} "
+                             f"(contiguous={t.is_contiguous()}, device={t.device})")
+
+
 def wave_plan(chunk_off: torch.Tensor, n_req: int, start: torch.Tensor, meta_len: torch.Tensor, carve: int,
               order0: int, req: torch.Tensor, p_abs: torch.Tensor, probe: torch.Tensor, order: torch.Tensor) -> None:
     """irm_wave_plan: per chunk slot, owning request, absolute position, probe flag, order key."""
+    _expect([(chunk_off, torch.int64), (start, torch.int32), (meta_len, torch.int64), (req, torch.int64),
+             (p_abs, torch.int64), (probe, torch.uint8), (order, torch.int64)], "wave_plan")
+    if meta_len.numel() < n_req or chunk_off.numel() < n_req + 1 or min(req.numel(), p_abs.numel(), probe.numel(),
+                                                                         order.numel()) < start.numel():
+        raise ValueError("wave_plan: buffer too small")
     N.check(N.lib().irm_wave_plan(N.ptr(chunk_off), int(n_req), N.ptr(start), N.ptr(meta_len), start.numel(),
                                   int(carve), int(order0), N.ptr(req), N.ptr(p_abs), N.ptr(probe), N.ptr(order),
                                   N.stream_ptr()), "irm_wave_plan")
@@ -296,6 +308,14 @@ def wave_compact(hit: torch.Tensor, row: torch.Tensor, req: torch.Tensor, p_abs:
                  len_out: torch.Tensor, delta_out: torch.Tensor, n_hit: torch.Tensor, length_out: torch.Tensor,
                  hit_tokens: torch.Tensor | None = None) -> None:
     """irm_wave_compact: the hit slots, in slot order, as K4 work; their count on the device."""
+    _expect([(hit, torch.int32), (row, torch.int64), (req, torch.int64), (p_abs, torch.int64), (p_src, torch.int64),
+             (length, torch.int32), (src_out, torch.int64), (dst_out, torch.int64), (len_out, torch.int32),
+             (delta_out, torch.int64), (n_hit, torch.int64), (length_out, torch.int32)]
+            + ([(hit_tokens, torch.int64)] if hit_tokens is not None else []), "wave_compact")
+    n = hit.numel()
+    if min(t.numel() for t in (row, req, p_abs, p_src, length, src_out, dst_out, len_out, delta_out,
+                               length_out)) < n:
+        raise ValueError("wave_compact: buffer too small")
     N.check(N.lib().irm_wave_compact(N.ptr(hit), N.ptr(row), N.ptr(req), N.ptr(p_abs), N.ptr(p_src), N.ptr(length),
                                      hit.numel(), int(req_stride), N.ptr(src_out), N.ptr(dst_out), N.ptr(len_out),
                                      N.ptr(delta_out), N.ptr(n_hit), N.ptr(length_out), N.ptr(hit_tokens),

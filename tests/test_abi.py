@@ -63,3 +63,18 @@ def test_store_view_validation():
     v.n_slots = 3  # not a power of two
     assert L.irm_store_reset(ctypes.byref(v), None) == N.IRM_EINVAL
     assert b"power of two" in L.irm_last_error()
+
+
+def test_wave_ops_reject_wrong_tensors():
+    """The wave glue wrappers check dtypes / devices before any library call."""
+    import pytest
+    import torch
+
+    from paper_2605_05696_b200 import ops
+
+    z64 = torch.zeros(4, dtype=torch.int64)
+    z32 = torch.zeros(4, dtype=torch.int32)
+    with pytest.raises(ValueError, match="wave_plan"):
+        ops.wave_plan(z64, 2, z32, z64, 32, 0, z64, z64, torch.zeros(4, dtype=torch.uint8), z64)  # CPU tensors
+    with pytest.raises(ValueError, match="wave_compact"):
+        ops.wave_compact(z64, z64, z64, z64, z64, z32, 1, z64, z64, z32, z64, z64[:1], z32)  # hit must be int32
