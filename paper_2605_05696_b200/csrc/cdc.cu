@@ -20,6 +20,8 @@
 // independent regions; one CTA scans one region (producer / chain / walker
 // warps, see cdc_region_kernel), walks the boundary rule with ballot/ffs over
 // the candidate words, then hashes its chunks (XXH64 from L2-resident tokens).
+// That is the fused form; the split form (further below) computes G on every
+// SM first and hashes on every SM after, for batches of few long regions.
 #include "common.cuh"
 #include "tma.cuh"
 #include <stdlib.h>
@@ -637,10 +639,9 @@ cdc_region_split_kernel(const uint32_t *__restrict__ tok, const uint64_t *__rest
 
 // fingerprints + compaction (split K1), over every chunk of the batch on every SM: a quad
 // of lanes per chunk (fingerprint.py:28-30), the chunk's region found by binary search
-// over the regions' output offsets r_out (cdc_offsets_kernel)
-// The split form runs only for batches of fewer regions than SMs (< HC_THREADS), so every
-// CTA scans the region chunk counts itself (the offsets pass folded in; CTA 0 publishes
-// chunk_off).
+// over the regions' output offsets. The split form runs only for batches of at most
+// HC_THREADS regions, so every CTA scans the region chunk counts itself (the offsets pass
+// folded in; CTA 0 publishes chunk_off).
 constexpr int HC_THREADS = 256;
 
 __global__ void __launch_bounds__(HC_THREADS)
