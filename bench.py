@@ -387,6 +387,8 @@ def run_ours(args):
         "components": {
             "cdc_hash": {"value": tok_per_wave / (k1 / 1e3), "unit": "tokens/s", "kernel": "irm_cdc_xxh64 (K1)",
                          "launch_ms": k1, "tokens_per_launch": tok_per_wave,
+                         "note": "latency-bound: one carried bit per token within a pin-delimited region, "
+                                 "8 long regions in this wave (split form, DESIGN.md K1)",
                          "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm, "unit": "GB/s",
                                       "frac": k1_gbs / hbm}},
             "cdc_hash_wide": cdc_wide_component(hbm),
