@@ -168,7 +168,9 @@ def run_ours(args):
     marker = np.array(canonical_marker(), np.uint32)
     R = args.requests
     n_steps = args.warmup + args.steps
-    waves = [make_wave(rng, header, marker, body, R) for _ in range(n_steps + 1)]
+    # waves[0 .. n_steps-1]: warm-up + timed; waves[n_steps]: the parity check wave (run once,
+    # after every timed region); waves[-1]: the cold request wave that stores the body
+    waves = [make_wave(rng, header, marker, body, R) for _ in range(n_steps + 2)]
 
     def pack(wave):
         streams, pins, ms = wave
@@ -194,7 +196,7 @@ def run_ours(args):
 
     store = ops.ChunkStore(max_entries=1 << 16)
     sharded = world > 1 or args.sharded
-    pool_rows = BODY + 2048 * (n_steps + 2)  # body + the novel header/meta chunks of every wave
+    pool_rows = BODY + 2048 * (n_steps + 3)  # body + the novel header/meta chunks of every wave
     if sharded:
         # rows [0, novel) hold first-writer KV (split among the G owners), [novel, pool_rows) the replicas
         n_waves_total = 3 * n_steps + 8
@@ -359,6 +361,12 @@ def run_ours(args):
     if sharded:  # host checks, outside the timed regions: first-writer rows and replicas all fit
         pipe.sharded.check()
         pipe.replica.check()
+    # -------- in-run parity (the checker, after every timed region): one fresh wave through the
+    # production path vs the sequential oracle over every wave this run served
+    parity = None
+    if world == 1:
+        parity = pipeline_parity(pipe, packed, n_steps, overlapped, sharded, graphs if sharded else True, pool,
+                                 dev_in, req_stride, wave0=5 * n_steps + 12)
 
     # -------- roofline of the dominant kernel (K4) and K1
     rows_per_launch = k4_rows
@@ -405,8 +413,14 @@ def run_ours(args):
             "fused_attn_dsv2": fused_attn_component(args, tf_burst, peak_kind, n_ctx=32768, n_q=4096, theta=1e4,
                                                     layout=N.LAYOUT_INTERLEAVED, shape="config 2")
             if not args.no_attn else None,
+            # config 4 (JoyAI-Flash shape): 128K context, 8K queries, theta 3.2e7; pool > L2
+            "fused_attn_config4": fused_attn_component(args, tf_burst, peak_kind, n_ctx=131072, n_q=8192,
+                                                       theta=3.2e7, shape="config 4")
+            if not args.no_attn else None,
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo},
+        "parity": parity if parity is not None else {"checked": False,
+                                                     "why": "N > 1: the global oracle needs every rank's waves"},
         # our kernels per wave (ncu launch list, profiles/r01e_launches.csv): K1 plan / offsets /
         # region / compact, K3 claim / decide / blockscan / commit / resolve, K4 cossin + gather;
         # sharded: + the replica map store's 5 and irm_copy_runs
@@ -419,6 +433,98 @@ def run_ours(args):
         print(json.dumps(line))
     if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def pipeline_parity(pipe, packed, n_steps, overlapped, sharded, graphs, pool, dev_in, req_stride, wave0,
+                    chunks_per_request=3):
+    """The checker for the timed path. Runs the never-served
+    check wave (packed[n_steps]) through the same production path the timed
+    region used (overlapped graphs / serial graph / sharded), then replays the
+    sequential oracle over every wave this process served, in serve order (the
+    cold wave, then waves 0 .. n_steps-1; re-served waves insert nothing new):
+    oracle/irm_oracle.c CDC + xxh64 per request, a first-writer-wins dict with
+    the carve-out (engine.py:181-226) and pool rows handed out in query order
+    (store.cu). Checked: the check wave's per-chunk service map, bit-exact; and,
+    for a stratified sample of hit chunks (first, middle, last of every
+    request), every row in all layers against oracle rotate+gather
+    (registry.py:146-166) of the GPU pool's own bytes: c_KV bit-exact, k_r
+    within bf16 rounding."""
+    import torch
+
+    from oracle import oracle as O
+
+    check = n_steps
+    hit_map = {}
+    load = lambda i: pipe.load(*dev_in[check])
+    if overlapped:
+        grab = lambda i, s: hit_map.__setitem__("hit", pipe.slots[s]["hit"].clone())
+        if sharded:
+            run_sharded(pipe, 1, load, wave0, graphs, after_front=grab)
+        else:
+            pipe.run_overlapped(1, load, after_front=grab)
+        torch.cuda.synchronize()
+        out = pipe.slots[0]["out"]
+    else:
+        pipe.load(*dev_in[check])
+        pipe.step_sharded(wave0) if sharded else pipe.replay()
+        torch.cuda.synchronize()
+        hit_map["hit"] = pipe.hit.clone()
+        out = pipe.out
+    got_hit = hit_map["hit"].cpu().numpy().astype(np.int64)
+
+    t0 = time.perf_counter()
+    reg, rows_next = {}, 0
+    order = [len(packed) - 1] + list(range(n_steps)) + [check]
+    for w in order:
+        tok, off, poff, pins, ms = packed[w]
+        recs = []
+        for r in range(off.size - 1):
+            st, ln, fp, _ = O.cdc_chunk(tok[off[r]:off[r + 1]], pins=pins[poff[r]:poff[r + 1]])
+            for s_, l_, f_ in zip(st.tolist(), ln.tolist(), fp.tolist()):
+                p = int(ms[r]) + s_
+                if p < CARVE:
+                    recs.append((-1, 0, -1, p, l_, r))
+                elif f_ in reg:
+                    recs.append((1, reg[f_][0], reg[f_][1], p, l_, r))
+                else:
+                    reg[f_] = (p, rows_next)
+                    recs.append((0, p, rows_next, p, l_, r))
+                    rows_next += l_
+    want = np.array([x[0] for x in recs], np.int64)
+    n = want.size
+    map_ok = bool(np.array_equal(got_hit[:n], want) and (got_hit[n:] == -1).all())
+    # stratified KV sample: first / middle / last hit chunk of every request, all rows, all layers
+    sample = []
+    for r in range(pipe.R):
+        hr = [x for x in recs if x[0] == 1 and x[5] == r]
+        if hr:
+            idx = sorted({0, len(hr) // 2, len(hr) - 1})[:chunks_per_request]
+            sample += [hr[i] for i in idx]
+    src = np.array([x[2] for x in sample], np.int64)
+    ln = np.array([x[4] for x in sample], np.int32)
+    delta = np.array([x[3] - x[1] for x in sample], np.int64)
+    dst_rows = np.concatenate([x[5] * req_stride + x[3] + np.arange(x[4]) for x in sample])
+    src_rows = np.concatenate([x[2] + np.arange(x[4]) for x in sample])
+    got = out[:, torch.from_numpy(dst_rows).to(out.device)].view(torch.int16).cpu().numpy().view(np.uint16)
+    mini = pool[:, torch.from_numpy(src_rows).to(pool.device)].view(torch.int16).cpu().numpy().view(np.uint16)
+    mini = np.ascontiguousarray(mini)
+    starts = np.concatenate([[0], np.cumsum(ln)[:-1]]).astype(np.int64)
+    exp = np.zeros_like(got)
+    inv = np.power(THETA, -2.0 * np.arange(KR // 2) / KR)
+    O.rotate_gather_bf16(mini, exp, starts, starts, ln, delta, inv, interleaved=True)
+    ckv_ok = bool(np.array_equal(got[..., :CKV], exp[..., :CKV]))
+    f = lambda u: (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    g, e = f(got[..., CKV:]), f(exp[..., CKV:])
+    kr_err = float(np.abs(g - e).max() / max(np.abs(e).max(), 1e-30))
+    rel = O.rel_l2(g, e)
+    return {"ok": bool(map_ok and ckv_ok and kr_err <= 2.0 ** -7 and rel <= 4.7e-3 and len(sample) > 0),
+            "service_map_bit_exact": map_ok, "chunks": int(n), "hits": int((want == 1).sum()),
+            "kv_rows_checked": int(dst_rows.size), "layers": int(got.shape[0]), "ckv_bit_exact": ckv_ok,
+            "kr_max_rel": kr_err, "kr_rel_l2": rel, "bound": "c_KV bit-exact; k_r within bf16 rounding (2^-7 of max), "
+                                                          "rel-L2 <= 4.7e-3",
+            "sample": f"check wave ({pipe.R} fresh requests, never served before) through the timed path; oracle "
+                      f"replayed over {len(order)} waves ({time.perf_counter() - t0:.1f} s); KV: first/middle/last "
+                      f"hit chunk per request x all layers"}
 
 
 def run_sharded(pipe, n, load, wave0, graphs, after_front=None):
@@ -463,21 +569,20 @@ def cdc_wide_component(hbm, n_streams=296, n_tok=32768):
 
 
 # ----------------------------------------------------------------- K5 component
-def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=16, theta=5e4, layout=None,
-                         shape="config 3", cpu=False):
-    """BASELINE.json config 3 (Moonlight-16B-A3B shape, DSv3-form half-split
-    rotary, theta 5e4): a 64K-token prompt = 512-token prefix + 63 marker-wrapped
-    1K-token documents re-permuted relative to the cached order (the rerank
-    shape of workloads.py:142-162, scaled). Its KV lives in the latent pool in
-    SOURCE order with k_r entangled at the source positions; the fused kernel
-    gathers the rows (contiguous runs -> tiled TMA, seams -> gather4), rotates
-    each document's k_r by its delta in shared memory, and runs the absorbed
-    causal prefill of the last 4,096 (novel) query tokens over all 64K keys."""
+def attn_workload(n_ctx=65536, n_q=4096, heads=16, theta=5e4, layout=None, seed=35):
+    """The reattached prompt of BASELINE.json configs 2-4 for K5: a
+    ``n_ctx``-token prompt = 512-token prefix + marker-wrapped 1K-token documents
+    re-permuted relative to the cached order (the rerank shape of
+    workloads.py:142-162, scaled) + a novel tail holding the ``n_q`` queries.
+    Its KV lives in the latent pool in SOURCE order with k_r entangled at the
+    source positions; ``kv_rows`` maps request order -> pool row, ``kv_chunk``
+    each key to its document (chunk 0 = delta 0). Shared by bench.py and the
+    benchmarked-shape parity tests (tests/test_gpu_mla_shapes.py)."""
     import torch
 
     from paper_2605_05696_b200 import _native as N, ops
 
-    rng = np.random.default_rng(35)
+    rng = np.random.default_rng(seed)
     layout = N.LAYOUT_HALF_SPLIT if layout is None else layout
     doc, prefix = 960, 512  # 1K-token documents (960 + 64-token marker) after a 512-token prefix
     n_docs = (n_ctx - prefix - 512) // (doc + 64)  # 63 at 64K (65,024 tokens + a 512-token novel tail)
@@ -495,12 +600,59 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
     tail = prefix + n_docs * seg  # the novel tail holds the queries
     chunk_of_key[tail:] = 0
     dev = torch.device("cuda")
-    pool = torch.randn(n_ctx, 576, device=dev).to(torch.bfloat16)
-    q = torch.randn(n_q, heads, 576, device=dev).to(torch.bfloat16)
-    inv = ops.inv_freq_device(np.power(theta, -2.0 * np.arange(32) / 64))
-    cs = ops.chunk_cossin(torch.tensor(deltas, dtype=torch.int64, device=dev), inv)
-    rows_d = torch.from_numpy(kv_rows.astype(np.int32)).to(dev)
-    chunk_d = torch.from_numpy(chunk_of_key).to(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    pool = torch.randn(n_ctx, 576, device=dev, generator=g).to(torch.bfloat16)
+    q = torch.randn(n_q, heads, 576, device=dev, generator=g).to(torch.bfloat16)
+    inv_np = np.power(theta, -2.0 * np.arange(32) / 64)
+    inv = ops.inv_freq_device(inv_np)
+    deltas = np.array(deltas, np.int64)
+    cs = ops.chunk_cossin(torch.from_numpy(deltas).to(dev), inv)
+    return dict(pool=pool, q=q, cs=cs, rows_d=torch.from_numpy(kv_rows.astype(np.int32)).to(dev),
+                chunk_d=torch.from_numpy(chunk_of_key).to(dev), kv_rows=kv_rows, chunk_of_key=chunk_of_key,
+                deltas=deltas, inv=inv_np, n_docs=n_docs, layout=layout, n_ctx=n_ctx, n_q=n_q, heads=heads,
+                theta=theta)
+
+
+def attn_parity(w, out, lse, sample=64, device="cuda"):
+    """The checker, after the timed region: the first, a middle and the last
+    ``sample`` query rows x all heads of the kernel's output against the fp64
+    restatement (oracle/mla_ref.py) over their full causal context, on the
+    same bf16 inputs. Bound: the north star's 4.7e-3 rel-L2; lse within 2e-2."""
+    import torch
+
+    from oracle.mla_ref import mla_reattach_ref
+
+    n_q, n_ctx = w["n_q"], w["n_ctx"]
+    mid = n_q // 2 - sample // 2
+    idx = np.concatenate([np.arange(sample), np.arange(mid, mid + sample), np.arange(n_q - sample, n_q)])
+    kv = w["pool"][torch.from_numpy(w["kv_rows"]).to(w["pool"].device)]  # request order
+    ref, ref_lse = mla_reattach_ref(w["q"], kv, n_ctx - n_q, 192 ** -0.5, w["deltas"][w["chunk_of_key"]], w["inv"],
+                                    interleaved=bool(w["layout"]), q_index=idx, device=device)
+    got = out[torch.from_numpy(idx).to(out.device)].double().cpu()
+    rel = float((got - ref).norm() / ref.norm())
+    row = float(((got - ref).norm(dim=-1) / ref.norm(dim=-1).clamp_min(1e-30)).max())
+    lerr = float((lse[torch.from_numpy(idx).to(lse.device)].double().cpu() - ref_lse).abs().max())
+    return {"rel_l2": rel, "max_row_rel_l2": row, "lse_max_abs": lerr, "bound": 4.7e-3,
+            "ok": bool(rel <= 4.7e-3 and lerr <= 2e-2),
+            "sample": f"query rows [0,{sample}) [{mid},{mid + sample}) [{n_q - sample},{n_q}) x {out.shape[1]} heads, "
+                      f"full causal context each, vs the fp64 restatement (oracle/mla_ref.py)"}
+
+
+def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=16, theta=5e4, layout=None,
+                         shape="config 3", cpu=False):
+    """BASELINE.json config 3 (Moonlight-16B-A3B shape, DSv3-form half-split
+    rotary, theta 5e4) by default: attn_workload's re-permuted 64K prompt. The
+    fused kernel gathers the rows (contiguous runs -> tiled TMA, seams ->
+    gather4), rotates each document's k_r by its delta in shared memory, and
+    runs the absorbed causal prefill of the last 4,096 (novel) query tokens
+    over all 64K keys."""
+    import torch
+
+    from paper_2605_05696_b200 import _native as N, ops
+
+    w = attn_workload(n_ctx, n_q, heads, theta, layout)
+    q, pool, cs, rows_d, chunk_d, layout = w["q"], w["pool"], w["cs"], w["rows_d"], w["chunk_d"], w["layout"]
     # start from an idle GPU (1 s): the power-managed clocks after the HBM-bound step or the
     # previous component otherwise lower the first launches (1246 vs 1395 TFLOP/s measured at
     # 32K right after a 64K run); the peak it is compared with is the burst figure too
@@ -521,12 +673,12 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
     pos = np.arange(n_ctx - n_q, n_ctx, dtype=np.float64)
     flops = heads * float((pos + 1).sum()) * 2176  # (2*576 + 2*512) per visible (query, key, head)
     tflops = flops / (ms / 1e3) / 1e12
-    extra = {}
+    extra = {"parity": attn_parity(w, out, lse)}
     if cpu:
-        extra["cpu_baseline"] = attn_cpu_baseline(q, pool, kv_rows, chunk_of_key, np.array(deltas, np.int64), theta,
+        extra["cpu_baseline"] = attn_cpu_baseline(q, pool, w["kv_rows"], w["chunk_of_key"], w["deltas"], theta,
                                                   layout == N.LAYOUT_INTERLEAVED, n_ctx, n_q)
     return {**extra, "value": tflops, "unit": "TFLOP/s", "kernel": "irm_mla_reattach_prefill (K5, tcgen05/TMEM)",
-            "workload": f"{shape}: {n_ctx} ctx, last {n_q} queries, {heads} heads, {n_docs} re-permuted docs, "
+            "workload": f"{shape}: {n_ctx} ctx, last {n_q} queries, {heads} heads, {w['n_docs']} re-permuted docs, "
                         f"{'DSv2 interleaved' if layout == N.LAYOUT_INTERLEAVED else 'DSv3 half-split'} theta {theta:g}, bf16",
             "launch_ms": ms, "flop_per_launch": flops,
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": tf_peak, "unit": "TFLOP/s",

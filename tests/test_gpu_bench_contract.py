@@ -13,10 +13,11 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_bench_json_line():
+@pytest.mark.parametrize("mode", [[], ["--serial"], ["--sharded"]])
+def test_bench_json_line(mode):
     import bench
 
-    p = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-attn"], cwd=ROOT,
+    p = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-attn"] + mode, cwd=ROOT,
                        capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     lines = [l for l in p.stdout.splitlines() if l.strip()]
@@ -35,3 +36,6 @@ def test_bench_json_line():
     c = d["cpu_baseline"]
     assert c["value"] > 0 and c["kind"] == "port" and c["cores"] >= 1
     assert {"cdc_hash", "cdc_hash_wide", "store_lookup"} <= set(d["components"])
+    # in-run parity of the timed path: a fresh wave vs the sequential oracle
+    par = d["parity"]
+    assert par["ok"] and par["service_map_bit_exact"] and par["ckv_bit_exact"] and par["kv_rows_checked"] > 0, par
