@@ -52,12 +52,14 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def ncu_traffic():
+def ncu_traffic(kernel_prefix: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per K4 launch, from the committed
-    ncu --set full capture of this same workload (profiles/ncu_traffic.json)."""
+    ncu --set full capture of this same workload (profiles/ncu_traffic.json), when
+    that capture is of the kernel this run's roofline names."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return float(json.load(f)["dram_bytes_per_launch"])
+            d = json.load(f)
+        return float(d["dram_bytes_per_launch"]) if d["kernel"].startswith(kernel_prefix) else None
     except Exception:
         return None
 
@@ -206,7 +208,8 @@ def run_ours(args):
     inv = ops.inv_freq_device(np.power(THETA, -2.0 * np.arange(KR // 2) / KR))
     max_tok = max(int(p[1][-1]) for p in packed)
     max_pins = max(int(p[2][-1]) for p in packed)
-    pipe = ReattachPipeline(store, pool, inv, R, max_tok, max_pins, req_stride, layout=N.LAYOUT_INTERLEAVED)
+    pipe = ReattachPipeline(store, pool, inv, R, max_tok, max_pins, req_stride, layout=N.LAYOUT_INTERLEAVED,
+                            fanout=not args.no_fanout)
 
     if sharded:  # K6: hash-sharded store (fixed-capacity NCCL all-to-all) + peer replica cache
         from paper_2605_05696_b200 import shard
@@ -305,7 +308,12 @@ def run_ours(args):
 
     step(args.warmup)
     torch.cuda.synchronize()
-    k4_rows = int(pipe.length.sum().item()) * LAYERS
+    k4_rows = int(pipe.length.sum().item()) * LAYERS  # reattached rows written per launch
+    if pipe.fanout:  # each distinct source run is read once per launch (K4 fan-out)
+        ng = int(pipe.groups.n_groups.item())
+        src_rows = int(pipe.groups.g_len[:ng].to(torch.int64).sum().item()) * LAYERS
+    else:
+        src_rows = k4_rows
     n_queries = int(pipe.table.chunk_off[-1].item())  # K3 probes per wave (chunks of the wave)
     if sharded:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
@@ -369,8 +377,7 @@ def run_ours(args):
                                  dev_in, req_stride, wave0=5 * n_steps + 12)
 
     # -------- roofline of the dominant kernel (K4) and K1
-    rows_per_launch = k4_rows
-    k4_bytes = rows_per_launch * 2 * (CKV + KR) * 2
+    k4_bytes = (src_rows + k4_rows) * (CKV + KR) * 2  # bf16 rows: unique source reads + destination writes
     k4_gbs = k4_bytes / (k4 / 1e3) / 1e9
     k1_bytes = tok_per_wave * 4 + (tok_per_wave // 128) * 24
     k1_gbs = k1_bytes / (k1 / 1e3) / 1e9
@@ -389,9 +396,14 @@ def run_ours(args):
                                    " (streams; sharded lookup + peer replica fetch)" if sharded else " (CUDA graphs)"))
                                if overlapped else "serial K1 -> K3 -> K4 per wave",
                    "parallelism": f"sessions s mod G over {world} GPU(s)" + (", store sharded by fp prefix, NCCL all-to-all lookup" if sharded else "")},
-        "roofline": {"bound": "hbm", "kernel": "irm_rotate_gather (K4)", "achieved": k4_gbs,
-                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": ncu_traffic(),
-                     "peak_kind": peak_kind, "launch_ms": k4, "algorithmic_bytes": k4_bytes},
+        "roofline": {"bound": "hbm", "kernel": ("irm_rotate_gather_fanout (K4 fan-out)" if pipe.fanout
+                                                else "irm_rotate_gather (K4)"), "achieved": k4_gbs,
+                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": ncu_traffic("rotate_gather_fanout_kernel" if pipe.fanout
+                                                                          else "rotate_gather_tma_kernel"),
+                     "peak_kind": peak_kind, "launch_ms": k4, "algorithmic_bytes": k4_bytes,
+                     "source_rows_read": src_rows, "rows_written": k4_rows,
+                     "bytes_rule": "1152 B per distinct source row read (once per launch) + 1152 B per reattached "
+                                   "row written, x 27 layers"},
         "components": {
             "cdc_hash": {"value": tok_per_wave / (k1 / 1e3), "unit": "tokens/s", "kernel": "irm_cdc_xxh64 (K1)",
                          "launch_ms": k1, "tokens_per_launch": tok_per_wave,
@@ -816,6 +828,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-attn", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="K6 sharded-store path even at N=1")
+    ap.add_argument("--no-fanout", action="store_true",
+                    help="K4 reads every hit's source rows (default: one read per distinct source run per wave)")
     ap.add_argument("--serial", action="store_true",
                     help="one graph per wave, K1 -> K3 -> K4 in series (default: wave i's K4 overlaps "
                          "K1 + K3 of wave i + 1)")

@@ -157,7 +157,11 @@ typedef struct {
     int64_t *e_row;       /* [max_entries] first row in the latent pool         */
     int64_t max_entries;
     int64_t *counters;    /* [4]: n_entries, pool rows used, error flags (1 table
-                           full, 2 entries full; sticky), reserved            */
+                           full, 2 entries full, 4 pool rows exhausted; sticky),
+                           reserved                                            */
+    int64_t pool_rows;    /* rows of the latent pool new entries are allocated in;
+                           an entry whose rows would pass it is not published
+                           (flag 4, q_row = -1). 0: unbounded                  */
 } irm_store_view;
 #define IRM_EMPTY_KEY 0xFFFFFFFFFFFFFFFFULL
 
@@ -188,14 +192,16 @@ int irm_store_lookup(const irm_store_view *st, const uint64_t *q_fp, int64_t n, 
  * order[i] = order0 + i. irm_wave_compact lists the slots with hit[i] == 1 in
  * slot order as K4 work (src = row, dst = req*req_stride + p_abs, len,
  * delta = p_abs - p_src), n_hit[0] = their count, length_out[i] = len if hit
- * else 0, and adds the hit tokens to *hit_tokens (if not null). */
+ * else 0, and adds the hit tokens to *hit_tokens (if not null). A hit whose
+ * rows [p_abs, p_abs + len) leave [0, req_stride) is not listed (it would
+ * write into the next request's rows) and sets bit 4 of *status (nullable). */
 int irm_wave_plan(const int64_t *chunk_off, int32_t n_req, const int32_t *start, const int64_t *meta_len,
                   int64_t cap, int64_t carve, int64_t order0, int64_t *req, int64_t *p_abs, uint8_t *probe,
                   int64_t *order, irm_stream_t stream);
 int irm_wave_compact(const int32_t *hit, const int64_t *row, const int64_t *req, const int64_t *p_abs,
                      const int64_t *p_src, const int32_t *len, int64_t cap, int64_t req_stride, int64_t *src_out,
                      int64_t *dst_out, int32_t *len_out, int64_t *delta_out, int64_t *n_hit, int32_t *length_out,
-                     int64_t *hit_tokens, irm_stream_t stream);
+                     int64_t *hit_tokens, uint64_t *status, irm_stream_t stream);
 
 /* ---- K4: delta-rotation rotate + gather (registry.py:146-166) ----------
  * For each chunk c and layer l: rows [src_row[c], +len[c]) of the pool are
@@ -206,20 +212,52 @@ int irm_wave_compact(const int32_t *hit, const int64_t *row, const int64_t *req,
  * dtype: element type of pool and out. out_round: IRM_ROUND_* applied to
  * the rotated values (f64 pools only; BF16E/F32 store emulation).
  * n_chunks_dev (nullable): device-side count of the leading chunks to process
- * (<= n_chunks), so a compacted hit list needs no host synchronisation. */
+ * (<= n_chunks), so a compacted hit list needs no host synchronisation.
+ * Bounds: pool_layer_stride / out_layer_stride are the row counts of one layer;
+ * a chunk whose source run leaves the pool or whose destination run leaves out
+ * is skipped and reported in *status (nullable, sticky OR: 1 source, 2
+ * destination) -- never read or written out of range.
+ * max_sms: spread the persistent CTAs over at most this many SMs (0 = all), per
+ * call, so a CUDA graph captures it with its launch (the reattach pipeline
+ * leaves ~20 SMs to CDC/lookup of the next wave running concurrently; the
+ * gather holds the HBM roofline down to ~120 SMs, profiles/r01d_k4_sms.md). */
 int64_t irm_rotate_gather_workspace_bytes(int64_t n_chunks, int32_t kr_dim);
 int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, void *out,
                       int64_t out_layer_stride, int32_t layers, int32_t ckv_dim, int32_t kr_dim,
                       const int64_t *src_row, const int64_t *dst_row, const int32_t *len,
                       const int64_t *delta, int64_t n_chunks, const int64_t *n_chunks_dev,
                       const double *inv_freq, int32_t layout, int32_t dtype, int32_t out_round,
-                      void *ws, int64_t ws_bytes, irm_stream_t stream);
-/* Limit the SMs a subsequent irm_rotate_gather launch spreads its persistent
- * CTAs over (0 = all SMs; process-wide, read at launch, so a captured CUDA graph
- * keeps the value it was captured with). The reattach pipeline leaves ~20 SMs to
- * CDC/lookup of the next wave running concurrently; the gather stays at the HBM
- * roofline down to ~128 SMs (profiles/r01d_k4_sms.md). */
-int irm_rotate_gather_set_sm_limit(int32_t n_sms);
+                      int32_t max_sms, uint64_t *status, void *ws, int64_t ws_bytes, irm_stream_t stream);
+/* K4 fan-out form. materialize (registry.py:146-166) is a pure function of
+ * (entry, p_dest): when several hits of a wave share a source run, its rows are
+ * read from HBM once and written once per destination.
+ * irm_group_by_source: the first n = min(n, *n_dev) (n_dev nullable) K4 work
+ * items (src_row, dst_row, len, delta, e.g. irm_wave_compact's output) grouped
+ * by source run (src_row, len): group g = (g_src, g_len, g_first, g_count), its
+ * members m_dst / m_delta[g_first .. g_first + g_count); groups in the order of
+ * their first item; *n_groups = the group count (device). ws: at least
+ * irm_group_workspace_bytes(n) bytes, ZERO-FILLED before the first call; every
+ * call leaves it zeroed. n < 2^31.
+ * irm_rotate_gather_fanout: for each group g < min(n_groups, *n_groups_dev),
+ * layer l and member m: rows [g_src, +g_len) of the pool -> rows [m_dst,
+ * +g_len) of out, c_KV verbatim, k_r rotated by R(m_delta) (fp64 angle, fp32
+ * rotation), bf16 or f32 pools, kr_dim a multiple of 4. n_members(_dev) bounds
+ * the member table; ws at
+ * least irm_fanout_workspace_bytes(n_members, kr_dim). Bounds, status and
+ * max_sms as irm_rotate_gather. */
+int64_t irm_group_workspace_bytes(int64_t n);
+int irm_group_by_source(const int64_t *src_row, const int64_t *dst_row, const int32_t *len, const int64_t *delta,
+                        int64_t n, const int64_t *n_dev, int64_t *g_src, int32_t *g_len, int32_t *g_first,
+                        int32_t *g_count, int64_t *m_dst, int64_t *m_delta, int64_t *n_groups, void *ws,
+                        int64_t ws_bytes, irm_stream_t stream);
+int64_t irm_fanout_workspace_bytes(int64_t n_members, int32_t kr_dim);
+int irm_rotate_gather_fanout(const void *pool, int64_t pool_layer_stride, void *out, int64_t out_layer_stride,
+                             int32_t layers, int32_t ckv_dim, int32_t kr_dim, const int64_t *g_src,
+                             const int32_t *g_len, const int32_t *g_first, const int32_t *g_count, int64_t n_groups,
+                             const int64_t *n_groups_dev, const int64_t *m_dst, const int64_t *m_delta,
+                             int64_t n_members, const int64_t *n_members_dev, const double *inv_freq,
+                             int32_t layout, int32_t dtype, int32_t max_sms, uint64_t *status, void *ws,
+                             int64_t ws_bytes, irm_stream_t stream);
 /* K6 replica fetch: for run c < min(n_runs, *n_runs_dev), copy len[c] rows of
  * row_bytes from src_addr[c] + l * src_layer_stride (a device address, normally
  * inside a peer GPU's pool mapped through CUDA IPC over NVLink) to

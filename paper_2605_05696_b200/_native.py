@@ -33,7 +33,7 @@ class StoreView(ctypes.Structure):
     _fields_ = [
         ("slot_key", P), ("slot_order", P), ("slot_entry", P), ("n_slots", i64),
         ("e_fp", P), ("e_p_src", P), ("e_len", P), ("e_row", P), ("max_entries", i64),
-        ("counters", P),
+        ("counters", P), ("pool_rows", i64),
     ]
 
 
@@ -58,13 +58,18 @@ _SIGS = {
     "irm_store_lookup_insert": ([ctypes.POINTER(StoreView), P, P, P, P, P, i64, P, P, P, P, P, i64, P], i32),
     "irm_store_lookup": ([ctypes.POINTER(StoreView), P, i64, P, P], i32),
     "irm_wave_plan": ([P, i32, P, P, i64, i64, i64, P, P, P, P, P], i32),
-    "irm_wave_compact": ([P, P, P, P, P, P, i64, i64, P, P, P, P, P, P, P, P], i32),
+    "irm_wave_compact": ([P, P, P, P, P, P, i64, i64, P, P, P, P, P, P, P, P, P], i32),
     "irm_rotate_gather_workspace_bytes": ([i64, i32], i64),
-    "irm_rotate_gather_set_sm_limit": ([i32], i32),
+    "irm_group_workspace_bytes": ([i64], i64),
+    "irm_group_by_source": ([P, P, P, P, i64, P, P, P, P, P, P, P, P, P, i64, P], i32),
+    "irm_fanout_workspace_bytes": ([i64, i32], i64),
+    "irm_rotate_gather_fanout": ([P, i64, P, i64, i32, i32, i32, P, P, P, P, i64, P, P, P, i64, P, P, i32, i32, i32,
+                                  P, P, i64, P], i32),
     "irm_copy_runs": ([P, i64, P, i64, P, P, i64, P, i32, i32, P], i32),
     "irm_peer_export": ([P, P, P], i32),
     "irm_peer_open": ([P, i64, P], i32),
-    "irm_rotate_gather": ([P, i64, P, i64, i32, i32, i32, P, P, P, P, i64, P, P, i32, i32, i32, P, i64, P], i32),
+    "irm_rotate_gather": ([P, i64, P, i64, i32, i32, i32, P, P, P, P, i64, P, P, i32, i32, i32, i32, P, P, i64, P],
+                          i32),
     "irm_rotate_rows": ([P, i64, P, i64, i64, i32, P, P, i32, i32, i32, P], i32),
     "irm_round_f64": ([P, P, i64, i32, P], i32),
     "irm_chunk_cossin": ([P, i64, P, P, P], i32),

@@ -219,6 +219,18 @@ __device__ __forceinline__ uint64_t xxh64_bytes(const uint8_t *__restrict__ p, i
 
 // ---------------------------------------------------------------- block scan
 // Exclusive scan of one int64 per thread across a block of BLOCK threads.
+// The rotation of one (lo, hi) pair, rounded exactly as the oracle's C restatement
+// (oracle/irm_oracle.c: lo*c - hi*s, lo*s + hi*c in separately rounded fp32
+// products, no FMA contraction), so every K4 form agrees bit for bit.
+__device__ __forceinline__ float rot_lo(float lo, float hi, float c, float s) {
+    return __fsub_rn(__fmul_rn(lo, c), __fmul_rn(hi, s));
+}
+__device__ __forceinline__ float rot_hi(float lo, float hi, float c, float s) {
+    return __fadd_rn(__fmul_rn(lo, s), __fmul_rn(hi, c));
+}
+__device__ __forceinline__ double rot_lo(double lo, double hi, double c, double s) { return lo * c - hi * s; }
+__device__ __forceinline__ double rot_hi(double lo, double hi, double c, double s) { return lo * s + hi * c; }
+
 template <int BLOCK>
 __device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t *total,
                                                         int64_t *smem /*[BLOCK/32]*/) {

@@ -92,8 +92,8 @@ __device__ __forceinline__ void rotate_pair(T *row_kr, int j, int half, int layo
     const A lo = Elem<T>::load(row_kr[ilo]);
     const A hi = Elem<T>::load(row_kr[ihi]);
     const A c = (A)cs.x, s = (A)cs.y;
-    row_kr[ilo] = Elem<T>::store(lo * c - hi * s, round);
-    row_kr[ihi] = Elem<T>::store(lo * s + hi * c, round);
+    row_kr[ilo] = Elem<T>::store(rot_lo(lo, hi, c, s), round);
+    row_kr[ihi] = Elem<T>::store(rot_hi(lo, hi, c, s), round);
 }
 
 // ------------------------------------------------------------ TMA-staged kernel
@@ -107,31 +107,43 @@ struct GatherArgs {
     int64_t n_chunks, n_items;
     const int64_t *n_dev;  // optional device-side chunk count (<= n_chunks): graph-friendly compaction
     int32_t layout, round;
+    unsigned long long *status;  // optional sticky flags: 1 source run outside the pool, 2 destination outside out
 };
+
+// A chunk's rows must lie inside the pool and the output (the layer strides are the row
+// counts): out-of-range work is skipped and reported, never read or written.
+__device__ __forceinline__ bool chunk_in_bounds(const GatherArgs &a, int64_t c, bool report) {
+    const int64_t len = __ldg(a.len + c), s = __ldg(a.src_row + c), d = __ldg(a.dst_row + c);
+    const bool src_ok = s >= 0 && len >= 0 && s + len <= a.pool_ls;
+    const bool dst_ok = d >= 0 && d + len <= a.out_ls;
+    if (report && a.status && !(src_ok && dst_ok))
+        atomicOr(a.status, (src_ok ? 0ULL : 1ULL) | (dst_ok ? 0ULL : 2ULL));
+    return src_ok && dst_ok;
+}
 
 template <int ROWS>
 struct TileIter {
     int64_t item, c;
     int32_t l, tile, ntiles;
-    __device__ __forceinline__ void load(const GatherArgs &a) {
+    __device__ __forceinline__ void load(const GatherArgs &a, bool report) {
         while (item < a.n_items) {
             c = item / a.layers;
             l = (int32_t)(item - c * a.layers);
-            ntiles = (__ldg(a.len + c) + ROWS - 1) / ROWS;
+            ntiles = chunk_in_bounds(a, c, report && l == 0) ? (__ldg(a.len + c) + ROWS - 1) / ROWS : 0;
             if (ntiles > 0) return;
             item += gridDim.x;
         }
     }
-    __device__ __forceinline__ void start(const GatherArgs &a) {
+    __device__ __forceinline__ void start(const GatherArgs &a, bool report) {
         item = blockIdx.x;
         tile = 0;
-        load(a);
+        load(a, report);
     }
-    __device__ __forceinline__ void next(const GatherArgs &a) {
+    __device__ __forceinline__ void next(const GatherArgs &a, bool report) {
         if (++tile >= ntiles) {
             tile = 0;
             item += gridDim.x;
-            load(a);
+            load(a, report);
         }
     }
     __device__ __forceinline__ bool valid(const GatherArgs &a) const { return item < a.n_items; }
@@ -164,12 +176,12 @@ rotate_gather_tma_kernel(GatherArgs a, const typename Elem<T>::CS *__restrict__ 
 
     // producer iterator (thread 0) runs STAGES-1 tiles ahead of the consumers
     TileIter<ROWS> prod, cons;
-    cons.start(a);
+    cons.start(a, threadIdx.x == 0);
     if (threadIdx.x == 0) {
-        prod.start(a);
+        prod.start(a, false);
         for (int s = 0; s < STAGES && prod.valid(a); ++s) {
             issue(prod, s);
-            prod.next(a);
+            prod.next(a, false);
         }
     }
     for (int64_t t = 0; cons.valid(a); ++t) {
@@ -192,10 +204,10 @@ rotate_gather_tma_kernel(GatherArgs a, const typename Elem<T>::CS *__restrict__ 
             if (t >= 1 && prod.valid(a)) {
                 bulk_wait_read<1>();  // the store of tile t-1 has left its stage
                 issue(prod, (int)((t - 1) % STAGES));
-                prod.next(a);
+                prod.next(a, false);
             }
         }
-        cons.next(a);
+        cons.next(a, threadIdx.x == 0);
     }
     if (threadIdx.x == 0) bulk_wait<0>();
 }
@@ -210,6 +222,7 @@ __global__ void rotate_gather_generic_kernel(GatherArgs a, const typename Elem<T
     for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         const int64_t c = item / a.layers;
         const int32_t l = (int32_t)(item - c * a.layers);
+        if (!chunk_in_bounds(a, c, threadIdx.x == 0 && l == 0)) continue;
         for (int32_t r = warp; r < a.len[c]; r += nwarp) {
             const T *src = reinterpret_cast<const T *>(a.pool) + ((int64_t)l * a.pool_ls + a.src_row[c] + r) * row_elems;
             T *dst = reinterpret_cast<T *>(a.out) + ((int64_t)l * a.out_ls + a.dst_row[c] + r) * row_elems;
@@ -236,17 +249,16 @@ __global__ void rotate_rows_kernel(const T *__restrict__ rows, int64_t rs, T *__
     using A = typename Elem<T>::Acc;
     const auto cs = make_cs<typename Elem<T>::CS>(pos[r] * inv_freq[j]);
     const A lo = Elem<T>::load(rows[r * rs + ilo]), hi = Elem<T>::load(rows[r * rs + ihi]);
-    out[r * os + ilo] = Elem<T>::store(lo * (A)cs.x - hi * (A)cs.y, round);
-    out[r * os + ihi] = Elem<T>::store(lo * (A)cs.y + hi * (A)cs.x, round);
+    out[r * os + ilo] = Elem<T>::store(rot_lo(lo, hi, (A)cs.x, (A)cs.y), round);
+    out[r * os + ihi] = Elem<T>::store(rot_hi(lo, hi, (A)cs.x, (A)cs.y), round);
 }
 
 // ------------------------------------------------------------ host launchers
-static int g_rg_sm_limit = 0;  // irm_rotate_gather_set_sm_limit
 constexpr int RG_THREADS = 256;
 constexpr int RG_STAGES = 4;
 
 template <typename T, int ROWS, int STAGES = RG_STAGES>
-static int launch_tma(const GatherArgs &a, const typename Elem<T>::CS *cs, cudaStream_t st) {
+static int launch_tma(const GatherArgs &a, const typename Elem<T>::CS *cs, int max_sms, cudaStream_t st) {
     auto kern = rotate_gather_tma_kernel<T, ROWS, STAGES, RG_THREADS>;
     const int smem = STAGES * ROWS * a.row_bytes;
     IRM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -254,7 +266,7 @@ static int launch_tma(const GatherArgs &a, const typename Elem<T>::CS *cs, cudaS
     IRM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RG_THREADS, smem));
     if (per_sm < 1) per_sm = 1;
     int sms = sm_count();
-    if (g_rg_sm_limit > 0) sms = std::min(sms, g_rg_sm_limit);
+    if (max_sms > 0) sms = std::min(sms, max_sms);
     int64_t grid = (int64_t)sms * per_sm;
     if (grid > a.n_items) grid = a.n_items;
     if (grid < 1) grid = 1;
@@ -265,7 +277,7 @@ static int launch_tma(const GatherArgs &a, const typename Elem<T>::CS *cs, cudaS
 
 template <typename T>
 static int launch_gather(const GatherArgs &a, void *ws, const int64_t *delta, const double *inv_freq,
-                         cudaStream_t st) {
+                         int max_sms, cudaStream_t st) {
     using CS = typename Elem<T>::CS;
     const int half = a.kr / 2;
     CS *cs = reinterpret_cast<CS *>(ws);
@@ -281,22 +293,22 @@ static int launch_gather(const GatherArgs &a, void *ws, const int64_t *delta, co
         const int rows_fit = 36864 / a.row_bytes;
         if (const char *v = getenv("IRM_RG_VARIANT")) {  // tuning hook: rows x stages
             const int var = atoi(v);
-            if (var == 1) return launch_tma<T, 8, 8>(a, cs, st);
-            if (var == 2) return launch_tma<T, 16, 6>(a, cs, st);
-            if (var == 3) return launch_tma<T, 32, 3>(a, cs, st);
-            if (var == 4) return launch_tma<T, 32, 4>(a, cs, st);
-            if (var == 5) return launch_tma<T, 8, 12>(a, cs, st);
-            if (var == 6) return launch_tma<T, 16, 8>(a, cs, st);
-            if (var == 7) return launch_tma<T, 32, 5>(a, cs, st);
-            if (var == 8) return launch_tma<T, 32, 6>(a, cs, st);
-            if (var == 9) return launch_tma<T, 64, 3>(a, cs, st);
-            if (var == 10) return launch_tma<T, 48, 4>(a, cs, st);
-            if (var == 11) return launch_tma<T, 24, 6>(a, cs, st);
+            if (var == 1) return launch_tma<T, 8, 8>(a, cs, max_sms, st);
+            if (var == 2) return launch_tma<T, 16, 6>(a, cs, max_sms, st);
+            if (var == 3) return launch_tma<T, 32, 3>(a, cs, max_sms, st);
+            if (var == 4) return launch_tma<T, 32, 4>(a, cs, max_sms, st);
+            if (var == 5) return launch_tma<T, 8, 12>(a, cs, max_sms, st);
+            if (var == 6) return launch_tma<T, 16, 8>(a, cs, max_sms, st);
+            if (var == 7) return launch_tma<T, 32, 5>(a, cs, max_sms, st);
+            if (var == 8) return launch_tma<T, 32, 6>(a, cs, max_sms, st);
+            if (var == 9) return launch_tma<T, 64, 3>(a, cs, max_sms, st);
+            if (var == 10) return launch_tma<T, 48, 4>(a, cs, max_sms, st);
+            if (var == 11) return launch_tma<T, 24, 6>(a, cs, max_sms, st);
         }
-        if (rows_fit >= 32) return launch_tma<T, 32>(a, cs, st);
-        if (rows_fit >= 16) return launch_tma<T, 16>(a, cs, st);
-        if (rows_fit >= 8) return launch_tma<T, 8>(a, cs, st);
-        if (a.row_bytes <= 49152) return launch_tma<T, 1>(a, cs, st);
+        if (rows_fit >= 32) return launch_tma<T, 32>(a, cs, max_sms, st);
+        if (rows_fit >= 16) return launch_tma<T, 16>(a, cs, max_sms, st);
+        if (rows_fit >= 8) return launch_tma<T, 8>(a, cs, max_sms, st);
+        if (a.row_bytes <= 49152) return launch_tma<T, 1>(a, cs, max_sms, st);
     }
     int64_t grid = (int64_t)sm_count() * 8;
     if (grid > a.n_items) grid = a.n_items;
@@ -309,12 +321,6 @@ static int launch_gather(const GatherArgs &a, void *ws, const int64_t *delta, co
 
 using namespace irm;
 
-extern "C" int irm_rotate_gather_set_sm_limit(int32_t n_sms) {
-    IRM_REQUIRE(n_sms >= 0, "n_sms must be >= 0");
-    g_rg_sm_limit = n_sms;
-    return IRM_OK;
-}
-
 extern "C" int64_t irm_rotate_gather_workspace_bytes(int64_t n_chunks, int32_t kr_dim) {
     if (n_chunks < 0 || kr_dim < 0) return -1;
     const int64_t cs = ((n_chunks * (kr_dim / 2) * (int64_t)sizeof(double2) + 255) / 256) * 256;
@@ -326,8 +332,8 @@ extern "C" int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, vo
                                  int32_t kr_dim, const int64_t *src_row, const int64_t *dst_row,
                                  const int32_t *len, const int64_t *delta, int64_t n_chunks,
                                  const int64_t *n_chunks_dev, const double *inv_freq, int32_t layout,
-                                 int32_t dtype, int32_t out_round, void *ws, int64_t ws_bytes,
-                                 irm_stream_t stream) {
+                                 int32_t dtype, int32_t out_round, int32_t max_sms, uint64_t *status, void *ws,
+                                 int64_t ws_bytes, irm_stream_t stream) {
     IRM_REQUIRE(n_chunks >= 0 && layers >= 1 && ckv_dim >= 0 && kr_dim >= 0 && kr_dim % 2 == 0,
                 "bad sizes (layers >= 1, kr_dim even)");
     IRM_REQUIRE(layout == IRM_LAYOUT_HALF_SPLIT || layout == IRM_LAYOUT_INTERLEAVED, "bad layout");
@@ -335,6 +341,7 @@ extern "C" int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, vo
     IRM_REQUIRE(out_round == IRM_ROUND_NONE || dtype == IRM_DTYPE_F64,
                 "out_round applies to f64 pools only");
     IRM_REQUIRE(out_round >= 0 && out_round <= 2, "bad out_round");
+    IRM_REQUIRE(max_sms >= 0, "max_sms must be >= 0");
     if (n_chunks == 0) return IRM_OK;
     IRM_REQUIRE(pool && out && src_row && dst_row && len && delta && inv_freq && ws, "null pointer");
     if (ws_bytes < irm_rotate_gather_workspace_bytes(n_chunks, kr_dim)) {
@@ -360,10 +367,11 @@ extern "C" int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, vo
     a.n_dev = n_chunks_dev;
     a.layout = layout;
     a.round = out_round;
+    a.status = (unsigned long long *)status;
     cudaStream_t st = (cudaStream_t)stream;
-    if (dtype == IRM_DTYPE_BF16) return launch_gather<__nv_bfloat16>(a, ws, delta, inv_freq, st);
-    if (dtype == IRM_DTYPE_F32) return launch_gather<float>(a, ws, delta, inv_freq, st);
-    return launch_gather<double>(a, ws, delta, inv_freq, st);
+    if (dtype == IRM_DTYPE_BF16) return launch_gather<__nv_bfloat16>(a, ws, delta, inv_freq, max_sms, st);
+    if (dtype == IRM_DTYPE_F32) return launch_gather<float>(a, ws, delta, inv_freq, max_sms, st);
+    return launch_gather<double>(a, ws, delta, inv_freq, max_sms, st);
 }
 
 extern "C" int irm_rotate_rows(const void *rows, int64_t row_stride, void *out, int64_t out_stride,

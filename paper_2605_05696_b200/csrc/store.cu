@@ -17,7 +17,7 @@ namespace irm {
 
 constexpr int ST_BLOCK = 512;
 enum : int8_t { Q_NOVEL = 0, Q_HIT_OLD = 1, Q_HIT_BATCH = 2, Q_SKIP = 3 };
-enum : int64_t { ERR_TABLE_FULL = 1, ERR_ENTRIES_FULL = 2 };
+enum : int64_t { ERR_TABLE_FULL = 1, ERR_ENTRIES_FULL = 2, ERR_POOL_FULL = 4 };
 
 __device__ __forceinline__ uint64_t slot_hash(uint64_t fp) {
     // fingerprints are already xxh64 outputs; fold the high bits in anyway
@@ -145,20 +145,24 @@ store_commit_kernel(irm_store_view st, const uint64_t *__restrict__ q_fp,
         const int64_t e = n_before + blk_cnt[blockIdx.x] + ec;
         const int64_t row = rows_before + blk_rows[blockIdx.x] + er;
         const int64_t s = q_slot[i];
-        if (e < st.max_entries) {
+        // the entry's rows must fit the latent pool (pool_rows 0: unbounded); an entry that
+        // does not fit is never published, so nothing ever reads past the pool
+        const bool fits = st.pool_rows <= 0 || row + q_len[i] <= st.pool_rows;
+        if (e < st.max_entries && fits) {
             st.e_fp[e] = q_fp[i];
             st.e_p_src[e] = q_p[i];
             st.e_len[e] = q_len[i];
             st.e_row[e] = row;
             st.slot_entry[s] = e;
         } else {
-            atomicOr((unsigned long long *)&st.counters[2], (unsigned long long)ERR_ENTRIES_FULL);
+            atomicOr((unsigned long long *)&st.counters[2],
+                     (unsigned long long)(fits ? ERR_ENTRIES_FULL : ERR_POOL_FULL));
         }
         st.slot_order[s] = INT64_MAX;
         q_hit[i] = 0;
         q_entry[i] = e;
         q_p_src[i] = q_p[i];
-        q_row[i] = row;
+        q_row[i] = fits ? row : -1;
     } else if (state == Q_SKIP) {
         q_hit[i] = -1;
         q_entry[i] = -1;
@@ -335,13 +339,18 @@ wave_compact_kernel(const int32_t *__restrict__ hit, const int64_t *__restrict__
                     const int64_t *__restrict__ p_src, const int32_t *__restrict__ len, int64_t cap,
                     int64_t req_stride, int64_t *__restrict__ src_out, int64_t *__restrict__ dst_out,
                     int32_t *__restrict__ len_out, int64_t *__restrict__ delta_out, int64_t *__restrict__ n_hit,
-                    int32_t *__restrict__ length_out, int64_t *__restrict__ hit_tokens) {
+                    int32_t *__restrict__ length_out, int64_t *__restrict__ hit_tokens,
+                    unsigned long long *__restrict__ status) {
     __shared__ int64_t sm[WC_BLOCK / 32];
     int64_t base = 0, tokens = 0;
     for (int64_t i0 = 0; i0 < cap; i0 += WC_BLOCK) {
         const int64_t i = i0 + threadIdx.x;
-        const bool h = i < cap && hit[i] == 1;
         const int32_t l = i < cap ? len[i] : 0;
+        bool h = i < cap && hit[i] == 1;
+        if (h && (p_abs[i] < 0 || p_abs[i] + l > req_stride)) {  // would spill into the next request's rows
+            h = false;
+            if (status) atomicOr(status, 4ULL);
+        }
         if (i < cap) length_out[i] = h ? l : 0;
         int64_t tot;
         const int64_t k = base + block_exclusive_scan<WC_BLOCK>(h ? 1 : 0, &tot, sm);
@@ -381,14 +390,15 @@ extern "C" int irm_wave_plan(const int64_t *chunk_off, int32_t n_req, const int3
 extern "C" int irm_wave_compact(const int32_t *hit, const int64_t *row, const int64_t *req, const int64_t *p_abs,
                                 const int64_t *p_src, const int32_t *len, int64_t cap, int64_t req_stride,
                                 int64_t *src_out, int64_t *dst_out, int32_t *len_out, int64_t *delta_out,
-                                int64_t *n_hit, int32_t *length_out, int64_t *hit_tokens, irm_stream_t stream) {
+                                int64_t *n_hit, int32_t *length_out, int64_t *hit_tokens, uint64_t *status,
+                                irm_stream_t stream) {
     IRM_REQUIRE(cap >= 0 && req_stride >= 0, "bad sizes");
     IRM_REQUIRE(n_hit && (cap == 0 || (hit && row && req && p_abs && p_src && len && src_out && dst_out &&
                                        len_out && delta_out && length_out)),
                 "null pointer");
     irm::wave_compact_kernel<<<1, irm::WC_BLOCK, 0, (cudaStream_t)stream>>>(
         hit, row, req, p_abs, p_src, len, cap, req_stride, src_out, dst_out, len_out, delta_out, n_hit, length_out,
-        hit_tokens);
+        hit_tokens, (unsigned long long *)status);
     IRM_LAUNCH_CHECK();
     return IRM_OK;
 }

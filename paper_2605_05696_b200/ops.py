@@ -80,11 +80,18 @@ class ChunkTable:
 
 
 class CdcWorkspace:
-    """Reusable device scratch for irm_cdc_xxh64 (grown on demand). Output
-    tables are allocated per call, so results never alias a later call."""
+    """Reusable device scratch for irm_cdc_xxh64 (grown on demand until
+    ``freeze()``). Output tables are allocated per call, so results never alias
+    a later call."""
 
     def __init__(self):
         self.ws = None
+        self.frozen = False
+
+    def freeze(self):
+        """No growth from now on (a captured CUDA graph holds the buffer's
+        address): a call needing more scratch raises instead of reallocating."""
+        self.frozen = True
 
     def get(self, n_tokens, n_streams, n_pins, min_size):
         L = N.lib()
@@ -92,6 +99,8 @@ class CdcWorkspace:
         cap = max(int(L.irm_cdc_chunk_bound(n_tokens, n_streams, n_pins, min_size)), 16)
         dev = _dev()
         if self.ws is None or self.ws.numel() < wb:
+            if self.frozen:
+                raise ValueError("CdcWorkspace: the call exceeds the frozen (graph-captured) workspace")
             self.ws = torch.empty(max(wb, 256), dtype=torch.uint8, device=dev)
         bufs = (torch.empty(cap, dtype=torch.int32, device=dev),
                 torch.empty(cap, dtype=torch.int32, device=dev),
@@ -156,9 +165,14 @@ def rotate_gather(pool: torch.Tensor, out: torch.Tensor, src_row: torch.Tensor, 
                   length: torch.Tensor, delta: torch.Tensor, inv_freq: torch.Tensor,
                   ckv_dim: int = 512, kr_dim: int = 64, layout: int = N.LAYOUT_HALF_SPLIT,
                   out_round: int = N.ROUND_NONE, ws: torch.Tensor | None = None,
-                  n_dev: torch.Tensor | None = None) -> None:
+                  n_dev: torch.Tensor | None = None, max_sms: int = 0,
+                  status: torch.Tensor | None = None) -> None:
     """K4. pool [layers, pool_rows, ckv+kr], out [layers, out_rows, ckv+kr] (same dtype).
-    ``n_dev`` (int64 [1], device): process only the first n_dev[0] chunks."""
+    ``n_dev`` (int64 [1], device): process only the first n_dev[0] chunks.
+    ``max_sms``: spread over at most this many SMs (0 = all). ``status`` (int64 [1],
+    device, optional): sticky OR of 1 (a source run outside the pool) / 2 (a
+    destination run outside ``out``); such chunks are skipped. Without ``status``
+    the call checks nothing on the host (bench / graph use); see ``check_status``."""
     assert pool.dtype == out.dtype and pool.is_contiguous() and out.is_contiguous()
     assert pool.dim() == 3 and out.dim() == 3 and pool.shape[0] == out.shape[0]
     assert pool.shape[2] == ckv_dim + kr_dim == out.shape[2]
@@ -169,8 +183,80 @@ def rotate_gather(pool: torch.Tensor, out: torch.Tensor, src_row: torch.Tensor, 
     rc = N.lib().irm_rotate_gather(
         N.ptr(pool), pool.shape[1], N.ptr(out), out.shape[1], pool.shape[0], ckv_dim, kr_dim,
         N.ptr(src_row), N.ptr(dst_row), N.ptr(length), N.ptr(delta), n, N.ptr(n_dev), N.ptr(inv_freq), layout,
-        _DTYPE_CODE[pool.dtype], out_round, N.ptr(ws), ws.numel(), N.stream_ptr())
+        _DTYPE_CODE[pool.dtype], out_round, int(max_sms), N.ptr(status), N.ptr(ws), ws.numel(), N.stream_ptr())
     N.check(rc, "irm_rotate_gather")
+
+
+def check_status(status: torch.Tensor, what: str = "rotate_gather") -> None:
+    """Raise if a K4 status word reports skipped out-of-range work (host sync)."""
+    v = int(status.item())
+    if v:
+        parts = [m for b, m in ((1, "a source run outside the latent pool"),
+                                (2, "a destination run outside the output"),
+                                (4, "a hit past its request's req_stride rows")) if v & b]
+        raise ValueError(f"{what}: skipped {' and '.join(parts)} (status {v})")
+
+
+@dataclass
+class SourceGroups:
+    """irm_group_by_source output: groups of K4 work sharing a source run."""
+
+    g_src: torch.Tensor     # int64 [cap]
+    g_len: torch.Tensor     # int32 [cap]
+    g_first: torch.Tensor   # int32 [cap]
+    g_count: torch.Tensor   # int32 [cap]
+    m_dst: torch.Tensor     # int64 [cap]
+    m_delta: torch.Tensor   # int64 [cap]
+    n_groups: torch.Tensor  # int64 [1] (device)
+    ws: torch.Tensor        # zero-filled group workspace (left zeroed by every call)
+
+    @staticmethod
+    def alloc(cap: int, device) -> "SourceGroups":
+        i64 = dict(dtype=torch.int64, device=device)
+        i32 = dict(dtype=torch.int32, device=device)
+        wsb = int(N.lib().irm_group_workspace_bytes(cap))
+        return SourceGroups(torch.zeros(cap, **i64), torch.zeros(cap, **i32), torch.zeros(cap, **i32),
+                            torch.zeros(cap, **i32), torch.zeros(cap, **i64), torch.zeros(cap, **i64),
+                            torch.zeros(1, **i64), torch.zeros(max(wsb, 256), dtype=torch.uint8, device=device))
+
+
+def group_by_source(src_row: torch.Tensor, dst_row: torch.Tensor, length: torch.Tensor, delta: torch.Tensor,
+                    groups: SourceGroups, n_dev: torch.Tensor | None = None) -> SourceGroups:
+    """Group K4 work items by source run (irm_group_by_source), into ``groups``'
+    static buffers (graph-capturable: nothing is allocated per call)."""
+    n = src_row.numel()
+    if groups.g_src.numel() < n:
+        raise ValueError("group_by_source: group buffers smaller than the work list")
+    _expect([(src_row, torch.int64), (dst_row, torch.int64), (length, torch.int32), (delta, torch.int64)],
+            "group_by_source")
+    rc = N.lib().irm_group_by_source(
+        N.ptr(src_row), N.ptr(dst_row), N.ptr(length), N.ptr(delta), n, N.ptr(n_dev), N.ptr(groups.g_src),
+        N.ptr(groups.g_len), N.ptr(groups.g_first), N.ptr(groups.g_count), N.ptr(groups.m_dst),
+        N.ptr(groups.m_delta), N.ptr(groups.n_groups), N.ptr(groups.ws), groups.ws.numel(), N.stream_ptr())
+    N.check(rc, "irm_group_by_source")
+    return groups
+
+
+def rotate_gather_fanout(pool: torch.Tensor, out: torch.Tensor, groups: SourceGroups, inv_freq: torch.Tensor,
+                         ckv_dim: int = 512, kr_dim: int = 64, layout: int = N.LAYOUT_HALF_SPLIT,
+                         ws: torch.Tensor | None = None, n_members_dev: torch.Tensor | None = None,
+                         max_sms: int = 0, status: torch.Tensor | None = None) -> None:
+    """K4 fan-out (irm_rotate_gather_fanout): each group's source rows are read
+    once and written, rotated by each member's delta, to every member's rows."""
+    assert pool.dtype == out.dtype and pool.is_contiguous() and out.is_contiguous()
+    assert pool.dim() == 3 and out.dim() == 3 and pool.shape[0] == out.shape[0]
+    assert pool.shape[2] == ckv_dim + kr_dim == out.shape[2]
+    cap = groups.m_dst.numel()
+    need = int(N.lib().irm_fanout_workspace_bytes(cap, kr_dim))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 256), dtype=torch.uint8, device=pool.device)
+    rc = N.lib().irm_rotate_gather_fanout(
+        N.ptr(pool), pool.shape[1], N.ptr(out), out.shape[1], pool.shape[0], ckv_dim, kr_dim, N.ptr(groups.g_src),
+        N.ptr(groups.g_len), N.ptr(groups.g_first), N.ptr(groups.g_count), groups.g_src.numel(),
+        N.ptr(groups.n_groups), N.ptr(groups.m_dst), N.ptr(groups.m_delta), cap, N.ptr(n_members_dev),
+        N.ptr(inv_freq), layout, _DTYPE_CODE[pool.dtype], int(max_sms), N.ptr(status), N.ptr(ws), ws.numel(),
+        N.stream_ptr())
+    N.check(rc, "irm_rotate_gather_fanout")
 
 
 def copy_runs(src_addr: torch.Tensor, src_layer_stride: int, dst_pool: torch.Tensor, dst_row: torch.Tensor,
@@ -188,11 +274,6 @@ def copy_runs(src_addr: torch.Tensor, src_layer_stride: int, dst_pool: torch.Ten
 def launch_count() -> int:
     """Kernels the library has launched or recorded into a captured graph (process-wide)."""
     return int(N.lib().irm_launch_count())
-
-
-def set_rotate_gather_sm_limit(n_sms: int) -> None:
-    """Spread later K4 launches over at most ``n_sms`` SMs (0 = all)."""
-    N.check(N.lib().irm_rotate_gather_set_sm_limit(int(n_sms)), "irm_rotate_gather_set_sm_limit")
 
 
 def rotate_rows(rows: torch.Tensor, positions: torch.Tensor, inv_freq: torch.Tensor,
@@ -224,7 +305,10 @@ class ChunkStore:
     Host state is only the ctypes view; tables and entries are torch tensors.
     """
 
-    def __init__(self, max_entries: int = 1 << 16, load_factor: float = 0.5):
+    def __init__(self, max_entries: int = 1 << 16, load_factor: float = 0.5, pool_rows: int = 0):
+        """pool_rows: rows of the latent pool that new entries' rows are bump-allocated
+        in (0 = unbounded); an insert that would pass it is not published and sets
+        the sticky pool-full flag that ``counts()`` raises on."""
         dev = _dev()
         n_slots = 1
         while n_slots < max(2, int(max_entries / load_factor)):
@@ -241,16 +325,37 @@ class ChunkStore:
         self.view = N.StoreView(
             N.ptr(self.slot_key), N.ptr(self.slot_order), N.ptr(self.slot_entry), n_slots,
             N.ptr(self.e_fp), N.ptr(self.e_p_src), N.ptr(self.e_len), N.ptr(self.e_row),
-            max_entries, N.ptr(self.counters))
+            max_entries, N.ptr(self.counters), int(pool_rows))
         self._ws = None
+        self._ws_frozen = False
         self.reset()
+
+    @property
+    def pool_rows(self) -> int:
+        return int(self.view.pool_rows)
+
+    def set_pool_rows(self, rows: int) -> None:
+        """Bound later inserts to ``rows`` pool rows (0 = unbounded). Read at launch:
+        a captured CUDA graph keeps the bound it was captured with."""
+        self.view.pool_rows = int(rows)
 
     def reset(self):
         N.check(N.lib().irm_store_reset(self.view, N.stream_ptr()), "irm_store_reset")
 
+    def reserve(self, n: int) -> None:
+        """Size the lookup workspace for batches of up to ``n`` queries once and
+        freeze it: a CUDA graph that captured ``lookup_insert`` keeps the buffer's
+        address, so it must never be replaced afterwards (a larger call raises).
+        An explicit ``reserve`` may still grow it: call it before capturing."""
+        self._ws_frozen = False
+        self._workspace(n)
+        self._ws_frozen = True
+
     def _workspace(self, n):
         need = int(N.lib().irm_store_workspace_bytes(n))
         if self._ws is None or self._ws.numel() < need:
+            if self._ws_frozen:
+                raise ValueError(f"ChunkStore: {n} queries exceed the reserved (graph-captured) workspace")
             self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.slot_key.device)
         return self._ws
 
@@ -279,7 +384,9 @@ class ChunkStore:
     def counts(self) -> tuple[int, int, int]:
         c = self.counters.cpu().tolist()
         if c[2]:
-            raise RuntimeError(f"chunk store overflow (flags {c[2]}): raise max_entries")
+            what = [m for b, m in ((1, "hash table full"), (2, "max_entries reached"),
+                                   (4, "latent pool rows exhausted")) if c[2] & b]
+            raise RuntimeError(f"chunk store overflow (flags {c[2]}: {', '.join(what)})")
         return c[0], c[1], c[2]
 
 
@@ -306,8 +413,10 @@ def wave_plan(chunk_off: torch.Tensor, n_req: int, start: torch.Tensor, meta_len
 def wave_compact(hit: torch.Tensor, row: torch.Tensor, req: torch.Tensor, p_abs: torch.Tensor, p_src: torch.Tensor,
                  length: torch.Tensor, req_stride: int, src_out: torch.Tensor, dst_out: torch.Tensor,
                  len_out: torch.Tensor, delta_out: torch.Tensor, n_hit: torch.Tensor, length_out: torch.Tensor,
-                 hit_tokens: torch.Tensor | None = None) -> None:
-    """irm_wave_compact: the hit slots, in slot order, as K4 work; their count on the device."""
+                 hit_tokens: torch.Tensor | None = None, status: torch.Tensor | None = None) -> None:
+    """irm_wave_compact: the hit slots, in slot order, as K4 work; their count on the device.
+    A hit whose rows would leave its request's ``req_stride`` rows is dropped and
+    sets bit 4 of ``status`` (int64 [1], device, optional)."""
     _expect([(hit, torch.int32), (row, torch.int64), (req, torch.int64), (p_abs, torch.int64), (p_src, torch.int64),
              (length, torch.int32), (src_out, torch.int64), (dst_out, torch.int64), (len_out, torch.int32),
              (delta_out, torch.int64), (n_hit, torch.int64), (length_out, torch.int32)]
@@ -319,7 +428,7 @@ def wave_compact(hit: torch.Tensor, row: torch.Tensor, req: torch.Tensor, p_abs:
     N.check(N.lib().irm_wave_compact(N.ptr(hit), N.ptr(row), N.ptr(req), N.ptr(p_abs), N.ptr(p_src), N.ptr(length),
                                      hit.numel(), int(req_stride), N.ptr(src_out), N.ptr(dst_out), N.ptr(len_out),
                                      N.ptr(delta_out), N.ptr(n_hit), N.ptr(length_out), N.ptr(hit_tokens),
-                                     N.stream_ptr()), "irm_wave_compact")
+                                     N.ptr(status), N.stream_ptr()), "irm_wave_compact")
 
 
 # ------------------------------------------------------------------ K5: fused MLA reattach prefill

@@ -16,9 +16,21 @@ single CUDA graph (no tracing compiler), replayed per wave after the inputs
 are copied into the static buffers.
 
 ``capture_overlapped`` adds a two-wave software pipeline: one graph per slot
-runs K4 of wave i (slot i % 2, on ~128 SMs) while K1 + K3 of wave i + 1 run on
+runs K4 of wave i (slot i % 2, on ~120 SMs) while K1 + K3 of wave i + 1 run on
 a forked stream over the remaining SMs and fill the other slot. K3 waves stay
 in order on that stream, so first-writer-wins across waves is unchanged.
+
+K4 runs in its fan-out form by default (``fanout=True``): the compacted hits
+are grouped by source run on the device (``irm_group_by_source``) and every
+(entry, layer) slab is read from HBM once for all the requests of the wave that
+reattach it (``irm_rotate_gather_fanout``; registry.py:146-166 is a pure
+function of (entry, p_dest)). ``fanout=False`` keeps the one-read-per-hit
+gather (``irm_rotate_gather``).
+
+Bounds: K4 skips (and reports in ``status``) any source run outside the pool
+or destination run outside the output, and the hit compaction refuses a hit
+whose request row range would spill past ``req_stride``; ``check()`` raises on
+any flag, the store's included (call it outside timed regions).
 """
 
 from __future__ import annotations
@@ -33,8 +45,12 @@ class ReattachPipeline:
     def __init__(self, store: ops.ChunkStore, pool: torch.Tensor, inv_freq: torch.Tensor,
                  max_requests: int, max_tokens: int, max_pins: int, req_stride: int,
                  layout: int = N.LAYOUT_INTERLEAVED, mask_exponent: int = 7, min_size: int = 32,
-                 max_size: int = 512, carve: int = 32, ckv_dim: int = 512, kr_dim: int = 64):
+                 max_size: int = 512, carve: int = 32, ckv_dim: int = 512, kr_dim: int = 64,
+                 fanout: bool = True):
         dev = pool.device
+        self.fanout = fanout
+        self.k4_sms = 0  # SMs K4 spreads over (0 = all); per launch, captured with it
+        self.status = torch.zeros(1, dtype=torch.int64, device=dev)  # sticky K4 / compaction bound flags
         self.store, self.pool, self.inv = store, pool, inv_freq
         self.R, self.req_stride, self.carve = max_requests, req_stride, carve
         self.params = (mask_exponent, min_size, max_size)
@@ -54,6 +70,15 @@ class ReattachPipeline:
         bound = int(N.lib().irm_cdc_chunk_bound(max_tokens, max_requests, max_pins, min_size))
         self.gather_ws = torch.empty(int(N.lib().irm_rotate_gather_workspace_bytes(bound, kr_dim)),
                                      dtype=torch.uint8, device=dev)
+        self.fan_ws = torch.empty(int(N.lib().irm_fanout_workspace_bytes(max(bound, 16), kr_dim)),
+                                  dtype=torch.uint8, device=dev)
+        # workspaces sized once for the static capacity and frozen: captured graphs keep their addresses
+        self.cdc_ws.get(max_tokens, max_requests, max_pins, max(min_size, 1))
+        self.cdc_ws.freeze()
+        store.reserve(max(bound, 16))
+        if store.pool_rows == 0:  # new entries' rows must fit this pool (sticky flag, check())
+            store.set_pool_rows(pool.shape[1])
+        self.groups = None  # serial mode's source groups (static: graph-captured)
         self.order0 = 0
         self.fill_slot = None  # overlapped mode: the slot K3 compacts into
         self.slots = None
@@ -108,22 +133,43 @@ class ReattachPipeline:
             self.k4_delta = torch.empty(cap, dtype=torch.int64, device=dev)
             self.n_hit = torch.empty(1, dtype=torch.int64, device=dev)
             ops.wave_compact(self.hit, src, self.reqc, self.p_abs, self.p_src, t.length, self.req_stride,
-                             self.k4_src, self.k4_dst, self.k4_len, self.k4_delta, self.n_hit, self.length)
+                             self.k4_src, self.k4_dst, self.k4_len, self.k4_delta, self.n_hit, self.length,
+                             status=self.status)
+            if self.fanout:
+                if self.groups is None or self.groups.g_src.numel() < cap:
+                    self.groups = ops.SourceGroups.alloc(cap, dev)
+                ops.group_by_source(self.k4_src, self.k4_dst, self.k4_len, self.k4_delta, self.groups,
+                                    n_dev=self.n_hit)
             return
         sl = self.slots[self.fill_slot]  # overlapped mode: static per-slot buffers
         ops.wave_compact(self.hit, src, self.reqc, self.p_abs, self.p_src, t.length, self.req_stride,
                          sl["src"], sl["dst"], sl["len"], sl["delta"], sl["n_hit"], self.length,
-                         hit_tokens=self.hit_tokens)
+                         hit_tokens=self.hit_tokens, status=self.status)
+        if self.fanout:
+            ops.group_by_source(sl["src"], sl["dst"], sl["len"], sl["delta"], sl["groups"], n_dev=sl["n_hit"])
         sl["hit"].copy_(self.hit)
 
-    def k4(self, slot: int | None = None):
+    def k4(self, slot: int | None = None, max_sms: int | None = None):
+        sms = self.k4_sms if max_sms is None else max_sms
         if slot is None:
-            ops.rotate_gather(self.pool, self.out, self.k4_src, self.k4_dst, self.k4_len, self.k4_delta, self.inv,
-                              self.ckv, self.kr, self.layout, ws=self.gather_ws, n_dev=self.n_hit)
-            return
-        sl = self.slots[slot]
-        ops.rotate_gather(self.pool, sl["out"], sl["src"], sl["dst"], sl["len"], sl["delta"], self.inv, self.ckv,
-                          self.kr, self.layout, ws=self.gather_ws, n_dev=sl["n_hit"])
+            out, src, dst, ln, delta, n_hit, groups = (self.out, self.k4_src, self.k4_dst, self.k4_len,
+                                                       self.k4_delta, self.n_hit, self.groups)
+        else:
+            sl = self.slots[slot]
+            out, src, dst, ln, delta, n_hit, groups = (sl["out"], sl["src"], sl["dst"], sl["len"], sl["delta"],
+                                                       sl["n_hit"], sl["groups"])
+        if self.fanout:
+            ops.rotate_gather_fanout(self.pool, out, groups, self.inv, self.ckv, self.kr, self.layout,
+                                     ws=self.fan_ws, n_members_dev=n_hit, max_sms=sms, status=self.status)
+        else:
+            ops.rotate_gather(self.pool, out, src, dst, ln, delta, self.inv, self.ckv, self.kr, self.layout,
+                              ws=self.gather_ws, n_dev=n_hit, max_sms=sms, status=self.status)
+
+    def check(self):
+        """Host check (outside timed regions): no K4 / compaction bound was hit and
+        the store did not overflow (raises ValueError / RuntimeError)."""
+        ops.check_status(self.status, "reattach pipeline")
+        self.store.counts()
 
     def step_eager(self):
         self.k1()
@@ -146,6 +192,11 @@ class ReattachPipeline:
         if world > 1:
             dist.all_reduce(cap, op=dist.ReduceOp.MAX, group=sharded_store.group)
         sharded_store.slots = int(cap.item())
+        # the owner allocates first-writer rows itself (ShardedStore): the shard's own row counter is unused
+        self.store.set_pool_rows(0)
+        self.store.reserve(world * sharded_store.slots)
+        if hasattr(replica_cache.map, "reserve"):
+            replica_cache.map.reserve(sharded_store.slots)
 
     def k3_sharded(self, wave: int):
         t = self.table
@@ -191,7 +242,7 @@ class ReattachPipeline:
             self.fill_slot, self.cur_in = None, 0
 
         loader = _Loader(self, load_wave)
-        ops.set_rotate_gather_sm_limit(k4_sms)
+        self.k4_sms = k4_sms
         try:
             loader.load(0, main)
             front(0, 0)
@@ -216,7 +267,7 @@ class ReattachPipeline:
                 if after_k4:
                     after_k4(i, s)
         finally:
-            ops.set_rotate_gather_sm_limit(0)
+            self.k4_sms = 0
 
     # ------------------------------------------------------------ graphs
     def capture(self, warmup: int = 2):
@@ -259,6 +310,7 @@ class ReattachPipeline:
                 src=torch.zeros(cap, **i64), dst=torch.zeros(cap, **i64), delta=torch.zeros(cap, **i64),
                 len=torch.zeros(cap, dtype=torch.int32, device=dev), n_hit=torch.zeros(1, **i64),
                 hit=torch.zeros(cap, dtype=torch.int32, device=dev),
+                groups=ops.SourceGroups.alloc(cap, dev) if self.fanout else None,
                 out=self.out if s == 0 else torch.empty_like(self.out)))
         self.hit_tokens = torch.zeros((), **i64)
 
@@ -292,7 +344,7 @@ class ReattachPipeline:
         def overlap(s):
             cur = torch.cuda.current_stream()
             side.wait_stream(cur)
-            self.k4(s)
+            self.k4(s, max_sms=k4_sms)  # the rest of the SMs run the next wave's front
             with torch.cuda.stream(side):
                 front(1 - s)
             cur.wait_stream(side)
@@ -305,7 +357,6 @@ class ReattachPipeline:
             ins["pin_off"].zero_()
         s0 = torch.cuda.Stream()
         s0.wait_stream(torch.cuda.current_stream())
-        ops.set_rotate_gather_sm_limit(k4_sms)
         try:
             with torch.cuda.stream(s0):
                 for _ in range(warmup):
@@ -330,7 +381,6 @@ class ReattachPipeline:
                     self.k4(s)
                 self.g_drain.append(g)
         finally:
-            ops.set_rotate_gather_sm_limit(0)
             torch.cuda.synchronize()
             for ins, (so, po) in zip(self.inputs, saved):
                 ins["stream_off"].copy_(so)
@@ -397,10 +447,17 @@ class ReattachPipeline:
 
     def load(self, tok, stream_off, pin_off, pins, m):
         """Copy one wave's inputs (device-resident or pinned host) into the static
-        buffers of the current input set (``cur_in``), on the current stream."""
+        buffers of the current input set (``cur_in``), on the current stream.
+        Host inputs are validated here (every request's m + tail fits its
+        ``req_stride`` rows); device inputs are checked by the compaction on the
+        device (``status``), so loading never waits for the GPU."""
         n = tok.numel()
         if n > self.max_tokens or pins.numel() > self.max_pins or m.numel() > self.R:
             raise ValueError("wave exceeds the pipeline's static capacity")
+        if not stream_off.is_cuda and not m.is_cuda and m.numel():
+            span = (stream_off[1:m.numel() + 1] - stream_off[:m.numel()]) + m
+            if int(span.max()) > self.req_stride:
+                raise ValueError(f"a request of {int(span.max())} tokens exceeds req_stride {self.req_stride}")
         self.tok[:n].copy_(tok, non_blocking=True)
         r = stream_off.numel()
         self.stream_off[:r].copy_(stream_off, non_blocking=True)

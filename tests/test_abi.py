@@ -49,12 +49,31 @@ def test_cdc_capacity_error():
 def test_rotate_validation():
     L = N.lib()
     # odd rotary dim, bad layout, rounding on a non-f64 pool
-    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 63, None, None, None, None, 1, None, None, 0, 0, 0, None, 0, None) == N.IRM_EINVAL
-    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 1, None, None, 7, 0, 0, None, 0, None) == N.IRM_EINVAL
-    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 1, None, None, 0, N.DTYPE_BF16, N.ROUND_BF16, None, 0, None) == N.IRM_EINVAL
+    g = lambda kr, layout, dtype, rnd, n=1, sms=0: L.irm_rotate_gather(
+        None, 0, None, 0, 1, 512, kr, None, None, None, None, n, None, None, layout, dtype, rnd, sms, None, None, 0,
+        None)
+    assert g(63, 0, 0, 0) == N.IRM_EINVAL
+    assert g(64, 7, 0, 0) == N.IRM_EINVAL
+    assert g(64, 0, N.DTYPE_BF16, N.ROUND_BF16) == N.IRM_EINVAL
+    assert g(64, 0, 0, 0, sms=-1) == N.IRM_EINVAL  # per-call SM limit
     assert L.irm_rotate_rows(None, 0, None, 0, 4, 63, None, None, 0, 0, 0, None) == N.IRM_EINVAL
     # zero work is a no-op success
-    assert L.irm_rotate_gather(None, 0, None, 0, 1, 512, 64, None, None, None, None, 0, None, None, 0, 0, 0, None, 0, None) == N.IRM_OK
+    assert g(64, 0, 0, 0, n=0) == N.IRM_OK
+
+
+def test_fanout_validation():
+    L = N.lib()
+    f = lambda kr, layout, dtype, ng=1, sms=0: L.irm_rotate_gather_fanout(
+        None, 0, None, 0, 1, 512, kr, None, None, None, None, ng, None, None, None, 4, None, None, layout, dtype,
+        sms, None, None, 0, None)
+    assert f(63, 0, N.DTYPE_BF16) == N.IRM_EINVAL
+    assert f(64, 3, N.DTYPE_BF16) == N.IRM_EINVAL
+    assert f(64, 0, N.DTYPE_F64) == N.IRM_EINVAL  # bf16 / f32 pools only
+    assert f(64, 0, N.DTYPE_BF16, ng=0) == N.IRM_OK
+    assert L.irm_group_workspace_bytes(1000) >= 2048 * 20
+    buf = ctypes.create_string_buffer(64)
+    assert L.irm_group_by_source(buf, buf, buf, buf, 100, None, buf, buf, buf, buf, buf, buf, buf, buf, 64,
+                                 None) == N.IRM_ECAPACITY
 
 
 def test_store_view_validation():

@@ -106,3 +106,51 @@ def test_mla_degenerate_sizes():
     assert float((out[0].float() - ref).abs().max()) <= 1e-2 * float(ref.abs().max())
     e_out, e_lse = ops.mla_reattach_prefill(q[:0], kv, 1, 0, 192 ** -0.5)  # no queries: nothing launched
     assert e_out.shape[0] == 0
+
+
+def test_store_pool_rows_bound():
+    """An insert whose rows would pass the latent pool is never published: its row
+    is -1, later lookups miss it, and the sticky pool-full flag raises."""
+    from paper_2605_05696_b200 import ops
+
+    store = ops.ChunkStore(max_entries=64, pool_rows=100)
+    n = 4
+    fp = torch.arange(1, n + 1, dtype=torch.int64, device="cuda") * 0x9E3779B97F4A7C15
+    hit, entry, p_src, row = store.lookup_insert(fp, torch.arange(n, device="cuda"),
+                                                 torch.arange(n, device="cuda") + 100,
+                                                 torch.full((n,), 40, dtype=torch.int32, device="cuda"))
+    assert row.tolist() == [0, 40, -1, -1]  # 80 rows fit, the third chunk would end at 120
+    assert store.lookup(fp).tolist()[:2] == [0, 1] and store.lookup(fp).tolist()[2:] == [-1, -1]
+    with pytest.raises(RuntimeError, match="pool rows exhausted"):
+        store.counts()
+
+
+def test_frozen_workspaces_refuse_to_grow():
+    """A graph-captured workspace is never replaced: a larger call raises."""
+    from paper_2605_05696_b200 import ops
+
+    store = ops.ChunkStore(max_entries=1 << 10)
+    store.reserve(16)
+    fp = torch.arange(1, 1001, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError, match="reserved"):
+        store.lookup_insert(fp, torch.arange(1000, device="cuda"), torch.zeros(1000, dtype=torch.int64, device="cuda"),
+                            torch.ones(1000, dtype=torch.int32, device="cuda"))
+    ws = ops.CdcWorkspace()
+    ws.get(1000, 2, 0, 32)
+    ws.freeze()
+    with pytest.raises(ValueError, match="frozen"):
+        ws.get(1 << 20, 2, 0, 32)
+
+
+def test_pipeline_request_longer_than_stride():
+    """A host-loaded wave whose request would spill past req_stride is refused."""
+    from paper_2605_05696_b200 import ops
+    from paper_2605_05696_b200.pipeline import ReattachPipeline
+
+    pool = torch.zeros(1, 4096, 576, dtype=torch.bfloat16, device="cuda")
+    pipe = ReattachPipeline(ops.ChunkStore(1 << 10), pool, ops.inv_freq_device(np.power(1e4, -np.arange(32) / 32)),
+                            2, 4096, 4, req_stride=1000)
+    tok = torch.zeros(1500, dtype=torch.int32)
+    with pytest.raises(ValueError, match="req_stride"):
+        pipe.load(tok, torch.tensor([0, 900, 1500]), torch.zeros(3, dtype=torch.int64),
+                  torch.zeros(1, dtype=torch.int64), torch.tensor([200, 0]))

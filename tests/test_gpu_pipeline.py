@@ -92,13 +92,13 @@ def setup():
                 req_stride=req_stride)
 
 
-def new_pipe(S):
+def new_pipe(S, fanout=True):
     from paper_2605_05696_b200.pipeline import ReattachPipeline
 
     ops = S["ops"]
     store = ops.ChunkStore(max_entries=1 << 12)
     return ReattachPipeline(store, S["pool"], ops.inv_freq_device(S["inv"]), R, S["max_tok"], S["max_pins"],
-                            S["req_stride"], layout=S["N"].LAYOUT_INTERLEAVED)
+                            S["req_stride"], layout=S["N"].LAYOUT_INTERLEAVED, fanout=fanout)
 
 
 def check_wave(S, w, hit, out):
@@ -125,9 +125,10 @@ def check_wave(S, w, hit, out):
     assert np.abs(g - e).max() <= 2.0 ** -7 * np.abs(e).max(), "k_r beyond bf16 rounding"
 
 
-def test_pipeline_serial_graph(setup):
+@pytest.mark.parametrize("fanout", [True, False])
+def test_pipeline_serial_graph(setup, fanout):
     S = setup
-    pipe = new_pipe(S)
+    pipe = new_pipe(S, fanout)
     dev = [to_dev(w) for w in S["waves"]]
     pipe.load(*dev[0])
     pipe.step_eager()  # cold wave: inserts the body
@@ -138,11 +139,13 @@ def test_pipeline_serial_graph(setup):
         pipe.replay()
         torch.cuda.synchronize()
         check_wave(S, w, pipe.hit.cpu().numpy(), pipe.out.cpu())
+    pipe.check()
 
 
-def test_pipeline_overlapped_matches_oracle(setup):
+@pytest.mark.parametrize("fanout", [True, False])
+def test_pipeline_overlapped_matches_oracle(setup, fanout):
     S = setup
-    pipe = new_pipe(S)
+    pipe = new_pipe(S, fanout)
     dev = [to_dev(w) for w in S["waves"]]
     pipe.load(*dev[0])
     pipe.step_eager()
@@ -162,6 +165,7 @@ def test_pipeline_overlapped_matches_oracle(setup):
         assert torch.equal(rb[i], hits[i].cpu())
         n_tok += sum(r[4] for r in S["ref"][1 + i] if r[0] == 1)
     assert int(pipe.hit_tokens.item()) == n_tok
+    pipe.check()
 
 
 def test_replica_fetch_peer_pools():

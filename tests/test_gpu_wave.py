@@ -55,13 +55,18 @@ def test_wave_plan_and_compact(seed, n_req, cap, empty_every):
         n_hit = torch.zeros(1, dtype=torch.int64, device=dev)
         length = torch.empty(cap, dtype=torch.int32, device=dev)
         tokens = torch.full((), 5, dtype=torch.int64, device=dev)
-        ops.wave_compact(hit, row, req, p_abs, p_src, ln, 4096, outs[0], outs[1], len_out, delta_out, n_hit, length,
-                         hit_tokens=tokens)
-        is_hit = hit == 1
-        k = int(is_hit.sum())
-        assert int(n_hit) == k
-        assert torch.equal(outs[0][:k], row[is_hit])
-        assert torch.equal(outs[1][:k], (req * 4096 + p_abs)[is_hit])
-        assert torch.equal(len_out[:k], ln[is_hit]) and torch.equal(delta_out[:k], (p_abs - p_src)[is_hit])
-        assert torch.equal(length, torch.where(is_hit, ln, torch.zeros_like(ln)))
-        assert int(tokens) == 5 + int(ln[is_hit].sum())
+        for stride in (8192, 2048):  # 2048: some hits would spill past their request's rows
+            status = torch.zeros(1, dtype=torch.int64, device=dev)
+            tokens.fill_(5)
+            ops.wave_compact(hit, row, req, p_abs, p_src, ln, stride, outs[0], outs[1], len_out, delta_out, n_hit,
+                             length, hit_tokens=tokens, status=status)
+            fits = p_abs + ln.to(torch.int64) <= stride
+            is_hit = (hit == 1) & fits
+            k = int(is_hit.sum())
+            assert int(n_hit) == k
+            assert torch.equal(outs[0][:k], row[is_hit])
+            assert torch.equal(outs[1][:k], (req * stride + p_abs)[is_hit])
+            assert torch.equal(len_out[:k], ln[is_hit]) and torch.equal(delta_out[:k], (p_abs - p_src)[is_hit])
+            assert torch.equal(length, torch.where(is_hit, ln, torch.zeros_like(ln)))
+            assert int(tokens) == 5 + int(ln[is_hit].sum())
+            assert int(status) == (4 if bool(((hit == 1) & ~fits).any()) else 0)

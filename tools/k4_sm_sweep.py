@@ -1,4 +1,4 @@
-"""K4 (bf16, config-2 sized) HBM bandwidth vs the number of SMs it spreads over (irm_rotate_gather_set_sm_limit)."""
+"""K4 (bf16, config-2 sized) HBM bandwidth vs the number of SMs it spreads over (irm_rotate_gather's max_sms)."""
 import sys
 import numpy as np, torch
 sys.path.insert(0, ".")
@@ -15,14 +15,13 @@ ln = torch.from_numpy(lens).cuda()
 delta = torch.from_numpy(rng.integers(-5000, 5000, size=lens.size)).cuda()
 inv = ops.inv_freq_device(np.power(1e4, -2.0 * np.arange(32) / 64))
 for sms in [148, 144, 140, 136, 132, 128, 120, 112]:
-    ops.set_rotate_gather_sm_limit(sms)
     for _ in range(3):
-        ops.rotate_gather(pool, out, src, dst, ln, delta, inv, layout=1)
+        ops.rotate_gather(pool, out, src, dst, ln, delta, inv, layout=1, max_sms=sms)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(10):
-        ops.rotate_gather(pool, out, src, dst, ln, delta, inv, layout=1)
+        ops.rotate_gather(pool, out, src, dst, ln, delta, inv, layout=1, max_sms=sms)
     b.record(); torch.cuda.synchronize()
     ms = a.elapsed_time(b) / 10
     print(sms, f"{ms:.3f} ms", f"{n_out * L * 2304 / ms / 1e6:.0f} GB/s")
