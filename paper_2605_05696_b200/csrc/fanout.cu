@@ -27,10 +27,15 @@
 // x row bytes), against 2 x all destination rows for the plain gather. The
 // launch is then bound by HBM WRITE bandwidth (8.15 of its 9.2 GB are writes
 // on the config-2 wave): ~4.9 TB/s of writes, where a 1:1 copy reaches 6.5
-// TB/s combined (tools/k4_fan_bench.py, profiles/r02_k4_fanout.md). A
-// thread-copy form (one smem source stage, threads copying c_KV into output
-// stages) measured 2.7 ms against 1.68 ms here: its per-tile copy and the
-// barriers around it, not HBM, set its pace.
+// TB/s combined (tools/k4_fan_bench.py, profiles/r02_k4_fanout.md). Two
+// source-once forms measured slower: threads copying the source tile into
+// per-member output stages (2.7 ms against 1.68 ms here) and the TMA engine
+// copying it shared -> shared inside the CTA (2.63 ms): an SM moves 36 KB
+// between its own stages more slowly than it re-reads them from L2. A third,
+// round-robin source-once form (each stage serves all members of its tile,
+// the pristine k_r kept aside, stages interleaved so a stage is rewritten only
+// after its previous store left) ran 1.67-1.73 ms: no faster than this form,
+// so L2 re-reads are not what holds the launch at ~5.4 TB/s combined.
 #include <algorithm>
 #include <cuda_bf16.h>
 #include <stdlib.h>
