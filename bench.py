@@ -398,7 +398,7 @@ def run_ours(args):
                    "parallelism": f"sessions s mod G over {world} GPU(s)" + (", store sharded by fp prefix, NCCL all-to-all lookup" if sharded else "")},
         "roofline": {"bound": "hbm", "kernel": ("irm_rotate_gather_fanout (K4 fan-out)" if pipe.fanout
                                                 else "irm_rotate_gather (K4)"), "achieved": k4_gbs,
-                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": ncu_traffic("rotate_gather_fanout_kernel" if pipe.fanout
+                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": ncu_traffic("rotate_gather_ws_kernel" if pipe.fanout
                                                                           else "rotate_gather_tma_kernel"),
                      "peak_kind": peak_kind, "launch_ms": k4, "algorithmic_bytes": k4_bytes,
                      "source_rows_read": src_rows, "rows_written": k4_rows,

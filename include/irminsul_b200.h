@@ -119,8 +119,13 @@ typedef struct {
     uint64_t *slot_key;   /* [n_slots] prefix key or IRM_EMPTY_KEY               */
     int64_t *slot_epoch;  /* [n_slots] smallest insert epoch with this prefix    */
     int64_t n_slots;      /* power of two, >= 2 x the distinct prefixes stored  */
-    int64_t *counters;    /* [2]: slots used, error flags (1 table full, 2 a
-                           match failed token verification; sticky)            */
+    int64_t *counters;    /* [2]: slots used, flags (1 table full: error; 4 a hash
+                           collision was resolved by an exact scan: informational;
+                           sticky)                                             */
+    uint64_t hash_key;    /* keys the prefix hash (polynomial base and mixing);
+                           fixed for the index's life. 1 = degenerate keys (every
+                           prefix of one length collides): a test hook for the
+                           exact fallback                                      */
 } irm_prefix_view;
 
 int irm_prefix_reset(const irm_prefix_view *ix, irm_stream_t stream);
@@ -135,7 +140,9 @@ int64_t irm_prefix_workspace_bytes(int64_t n_tokens, int32_t n_seq);
  *     m[i]; m = 0, wit = -1 when nothing matches (match_prefix, radix.py:60-83).
  * Every answer is checked token by token against the witness's tokens at
  * arena + wit_off[wit] (wit_len[wit] tokens; the caller keeps each inserted
- * sequence there, including this batch's); a mismatch sets error flag 2. */
+ * sequence there, including this batch's, indexed by epoch); a mismatch (hash
+ * collision) is answered again by an exact scan of the sequences with epochs
+ * < op_epoch[i] and sets flag 4: answers are always exact. */
 int irm_prefix_match_insert(const irm_prefix_view *ix, const uint32_t *tok, const int64_t *seq_off,
                             int32_t n_seq, int64_t n_tokens, const int64_t *op_epoch,
                             const uint8_t *op_insert, const uint8_t *op_query, const uint32_t *arena,

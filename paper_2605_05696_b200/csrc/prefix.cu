@@ -16,21 +16,28 @@
 // All prefix hashes of a batch come from one segmented scan of affine maps
 // x -> B x + (t + 1) (mod 2^61 - 1), so the work is O(tokens) and parallel.
 //
+// The hash is keyed per index (irm_prefix_view.hash_key: the polynomial base
+// and the key mixing both derive from it; the Python index draws it from
+// os.urandom), so colliding token sequences cannot be prepared offline.
+//
 // Exactness: a hash collision could only make a prefix look present. The
 // final answer of every query is verified token by token against the
-// witness's stored tokens; a mismatch raises error flag 2 (loud, never a
-// silent wrong answer). Deeper-prefix false negatives cannot happen.
+// witness's stored tokens; on a mismatch the query is answered again by an
+// exact scan of every sequence inserted before it (longest common prefix,
+// earliest epoch on ties, radix.py:60-89) and flag 4 records that a collision
+// was resolved. A colliding slot therefore costs a scan, never a wrong answer
+// and never an error. Deeper-prefix false negatives cannot happen.
 #include "common.cuh"
 
 namespace irm {
 namespace prefix {
 
 constexpr uint64_t P61 = (1ULL << 61) - 1;
-constexpr uint64_t BASE = 0x0F3D5B79A2C4E68DULL % P61;  // fixed odd base < p
 constexpr int CH = 1024;       // tokens per chunk (one CTA)
 constexpr int PT = 256;        // threads per CTA
 constexpr int TPT = CH / PT;   // tokens per thread
-enum : int64_t { ERR_TABLE_FULL = 1, ERR_VERIFY = 2 };
+enum : int64_t { ERR_TABLE_FULL = 1, ERR_VERIFY = 2, COLLISION_RESOLVED = 4 };
+constexpr uint64_t DEGENERATE_KEY = 1;  // test hook: every prefix of one length collides
 
 struct Aff {  // x -> a x + b (mod p)
     uint64_t a, b;
@@ -48,7 +55,16 @@ __device__ __forceinline__ uint64_t addmod(uint64_t x, uint64_t y) {
 }
 // f then g
 __device__ __forceinline__ Aff compose(Aff f, Aff g) { return {mulmod(f.a, g.a), addmod(mulmod(g.a, f.b), g.b)}; }
-__device__ __forceinline__ Aff tok_aff(uint32_t t) { return {BASE, (uint64_t)t + 1}; }
+__device__ __forceinline__ Aff tok_aff(uint32_t t, uint64_t base) { return {base, (uint64_t)t + 1}; }
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+// the polynomial base of this index, in [2, p - 1)
+__device__ __forceinline__ uint64_t key_base(uint64_t hash_key) { return 2 + splitmix(hash_key) % (P61 - 3); }
 
 __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
     k ^= k >> 33;
@@ -58,8 +74,9 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
     k ^= k >> 33;
     return k;
 }
-__device__ __forceinline__ uint64_t prefix_key(uint64_t h, int64_t d) {
-    const uint64_t k = fmix64(h + (uint64_t)d * 0x9E3779B97F4A7C15ULL);
+__device__ __forceinline__ uint64_t prefix_key(uint64_t h, int64_t d, uint64_t hash_key) {
+    if (hash_key == DEGENERATE_KEY) h = 0;
+    const uint64_t k = fmix64((h ^ splitmix(hash_key ^ 0x5851F42D4C957F2DULL)) + (uint64_t)d * 0x9E3779B97F4A7C15ULL);
     return k == IRM_EMPTY_KEY ? k - 1 : k;
 }
 
@@ -165,27 +182,29 @@ __device__ __forceinline__ Aff block_scan_aff(Aff v, Aff *agg) {
     return compose(wpre, ex);
 }
 
-__device__ __forceinline__ Aff thread_aff(const uint32_t *tok, int64_t s0, int64_t len, int64_t j, uint32_t t[TPT]) {
+__device__ __forceinline__ Aff thread_aff(const uint32_t *tok, int64_t s0, int64_t len, int64_t j, uint32_t t[TPT],
+                                          uint64_t base) {
     Aff a = {1, 0};
     const int64_t d0 = j * CH + (int64_t)threadIdx.x * TPT;
 #pragma unroll
     for (int q = 0; q < TPT; ++q) {
         const int64_t d = d0 + q;
         t[q] = d < len ? tok[s0 + d] : 0;
-        if (d < len) a = compose(a, tok_aff(t[q]));
+        if (d < len) a = compose(a, tok_aff(t[q], base));
     }
     return a;
 }
 
 __global__ void __launch_bounds__(PT) aggregate_kernel(const uint32_t *__restrict__ tok,
                                                         const int64_t *__restrict__ seq_off, int32_t n_seq,
-                                                        const int64_t *__restrict__ chunk_off, Aff *__restrict__ agg) {
+                                                        const int64_t *__restrict__ chunk_off, Aff *__restrict__ agg,
+                                                        uint64_t base) {
     int seq;
     int64_t j;
     if (!locate(chunk_off, n_seq, blockIdx.x, seq, j)) return;
     const int64_t s0 = seq_off[seq], len = seq_off[seq + 1] - s0;
     uint32_t t[TPT];
-    Aff a = thread_aff(tok, s0, len, j, t), tot;
+    Aff a = thread_aff(tok, s0, len, j, t, base), tot;
     block_scan_aff(a, &tot);
     if (threadIdx.x == 0) agg[blockIdx.x] = tot;
 }
@@ -213,8 +232,9 @@ __global__ void __launch_bounds__(PT) keys_kernel(irm_prefix_view ix, const uint
     int64_t j;
     if (!locate(chunk_off, n_seq, blockIdx.x, seq, j)) return;
     const int64_t s0 = seq_off[seq], len = seq_off[seq + 1] - s0;
+    const uint64_t base = key_base(ix.hash_key);
     uint32_t t[TPT];
-    Aff a = thread_aff(tok, s0, len, j, t), tot;
+    Aff a = thread_aff(tok, s0, len, j, t, base), tot;
     Aff h = compose(carry[blockIdx.x], block_scan_aff(a, &tot));  // maps H(empty) = 0 to H before my tokens
     const bool ins = op_insert && op_insert[seq];
     const int64_t ep = op_epoch[seq];
@@ -224,8 +244,8 @@ __global__ void __launch_bounds__(PT) keys_kernel(irm_prefix_view ix, const uint
     for (int q = 0; q < TPT; ++q) {
         const int64_t d = d0 + q;
         if (d >= len) break;
-        H = addmod(mulmod(H, BASE), (uint64_t)t[q] + 1);
-        const uint64_t k = prefix_key(H, d + 1);
+        H = addmod(mulmod(H, base), (uint64_t)t[q] + 1);
+        const uint64_t k = prefix_key(H, d + 1, ix.hash_key);
         key[s0 + d] = k;
         if (ins) insert(ix, k, ep);
     }
@@ -259,26 +279,68 @@ __global__ void query_kernel(irm_prefix_view ix, const int64_t *__restrict__ seq
     wit_out[i] = lo > 0 ? wit : -1;
 }
 
-// token-by-token check of every answer against the witness's stored tokens
+// token-by-token check of every answer against the witness's stored tokens; a
+// mismatch (a hash collision) is answered again by an exact scan of every sequence
+// inserted before the query: the longest common prefix, the earliest epoch on ties
 __global__ void verify_kernel(irm_prefix_view ix, const uint32_t *__restrict__ tok, const int64_t *__restrict__ seq_off,
-                              int32_t n_seq, const uint32_t *__restrict__ arena, const int64_t *__restrict__ wit_off,
-                              const int64_t *__restrict__ wit_len, const int64_t *__restrict__ m,
-                              const int64_t *__restrict__ wit) {
+                              int32_t n_seq, const int64_t *__restrict__ op_epoch, const uint8_t *__restrict__ op_query,
+                              const uint32_t *__restrict__ arena, const int64_t *__restrict__ wit_off,
+                              const int64_t *__restrict__ wit_len, int64_t *__restrict__ m,
+                              int64_t *__restrict__ wit) {
+    __shared__ unsigned long long first_diff;
     const int i = blockIdx.x;
-    if (i >= n_seq) return;
+    if (i >= n_seq || (op_query && !op_query[i])) return;
     const int64_t mi = m[i];
-    if (mi <= 0) return;
     const int64_t w = wit[i];
-    const int64_t s0 = seq_off[i];
-    bool bad = w < 0 || wit_len[w] < mi;
-    if (!bad) {
-        const uint32_t *a = tok + s0, *b = arena + wit_off[w];
+    const int64_t s0 = seq_off[i], len = seq_off[i + 1] - s0;
+    const uint32_t *a = tok + s0;
+    bool bad = mi > 0 && (w < 0 || wit_len[w] < mi);
+    if (mi > 0 && !bad) {
+        const uint32_t *b = arena + wit_off[w];
         for (int64_t d = threadIdx.x; d < mi; d += blockDim.x) bad |= a[d] != b[d];
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0)
-        atomicOr((unsigned long long *)&ix.counters[1], (unsigned long long)ERR_VERIFY);
+    if (!__syncthreads_or(bad)) return;
+    int64_t best = 0, best_w = -1;
+    const int64_t e = op_epoch[i];
+    for (int64_t v = 0; v < e; ++v) {
+        const int64_t L = min(len, wit_len[v]);
+        if (L <= best) continue;  // cannot beat the current answer (uniform: same values in every thread)
+        if (threadIdx.x == 0) first_diff = (unsigned long long)L;
+        __syncthreads();
+        const uint32_t *b = arena + wit_off[v];
+        for (int64_t d = threadIdx.x; d < L; d += blockDim.x)
+            if (a[d] != b[d]) {
+                atomicMin(&first_diff, (unsigned long long)d);
+                break;
+            }
+        __syncthreads();
+        const int64_t lcp = (int64_t)first_diff;
+        __syncthreads();
+        if (lcp > best) {
+            best = lcp;
+            best_w = v;
+        }
+    }
+    if (threadIdx.x == 0) {
+        m[i] = best;
+        wit[i] = best > 0 ? best_w : -1;
+        atomicOr((unsigned long long *)&ix.counters[1], (unsigned long long)COLLISION_RESOLVED);
+    }
 }
 
+}  // namespace prefix
+}  // namespace irm
+
+namespace irm {
+namespace prefix {
+// host copy of key_base (the aggregate kernel takes the base as an argument)
+static uint64_t key_base_host(uint64_t hash_key) {
+    uint64_t x = hash_key + 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    x ^= x >> 31;
+    return 2 + x % (P61 - 3);
+}
 }  // namespace prefix
 }  // namespace irm
 
@@ -328,7 +390,8 @@ extern "C" int irm_prefix_match_insert(const irm_prefix_view *ix, const uint32_t
     IRM_LAUNCH_CHECK();
     // grid = an upper bound on the chunk count; CTAs past the real count exit
     const unsigned grid = (unsigned)n_chunks_cap;
-    prefix::aggregate_kernel<<<grid, prefix::PT, 0, s>>>(tok, seq_off, n_seq, chunk_off, agg);
+    prefix::aggregate_kernel<<<grid, prefix::PT, 0, s>>>(tok, seq_off, n_seq, chunk_off, agg,
+                                                          prefix::key_base_host(ix->hash_key));
     IRM_LAUNCH_CHECK();
     prefix::carry_kernel<<<(n_seq + 127) / 128, 128, 0, s>>>(chunk_off, n_seq, agg, carry);
     IRM_LAUNCH_CHECK();
@@ -337,7 +400,8 @@ extern "C" int irm_prefix_match_insert(const irm_prefix_view *ix, const uint32_t
     IRM_LAUNCH_CHECK();
     prefix::query_kernel<<<(n_seq + 127) / 128, 128, 0, s>>>(*ix, seq_off, n_seq, op_epoch, op_query, key, m, wit);
     IRM_LAUNCH_CHECK();
-    prefix::verify_kernel<<<n_seq, 256, 0, s>>>(*ix, tok, seq_off, n_seq, arena, wit_off, wit_len, m, wit);
+    prefix::verify_kernel<<<n_seq, 256, 0, s>>>(*ix, tok, seq_off, n_seq, op_epoch, op_query, arena, wit_off, wit_len,
+                                                 m, wit);
     IRM_LAUNCH_CHECK();
     return IRM_OK;
 }

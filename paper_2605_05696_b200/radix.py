@@ -11,6 +11,8 @@ radix.py:31-89: longest match, earliest-inserted witness.
 
 from __future__ import annotations
 
+import os
+
 from typing import Hashable, Sequence
 
 import numpy as np
@@ -96,11 +98,15 @@ class DeviceRadixTree:
     Every prefix of every inserted sequence is a key of a device hash table
     holding the earliest insert epoch that reaches it; a query is a binary
     search over its own prefix keys, verified token by token against the
-    witness's stored tokens (``check()`` raises on a failed verification or
-    a full table). Inserted sequences are kept in a device token arena."""
+    witness's stored tokens. The hash is keyed per index (``hash_key``, drawn
+    from os.urandom), and a verification failure (a collision) is answered by
+    an exact scan on the device: answers are always the reference tree's.
+    ``check()`` raises only on a full table. Inserted sequences are kept in a
+    device token arena."""
 
     def __init__(self, capacity_hint: int | None = None, max_prefixes: int = 1 << 22,
-                 max_tokens: int = 1 << 24, max_sequences: int = 1 << 16, grow: bool = True):
+                 max_tokens: int = 1 << 24, max_sequences: int = 1 << 16, grow: bool = True,
+                 hash_key: int | None = None):
         """Capacities are initial sizes; with ``grow`` (default) the arena, the
         per-sequence arrays and the table are enlarged when a batch would not
         fit (the table by rebuilding it from the arena, epochs unchanged), so a
@@ -112,6 +118,7 @@ class DeviceRadixTree:
 
         self._N, self._torch = N, torch
         dev = ops._dev()
+        self.hash_key = int.from_bytes(os.urandom(8), "little") if hash_key is None else int(hash_key)
         self.capacity_hint = capacity_hint
         self.grow = grow
         self.counters = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -133,7 +140,8 @@ class DeviceRadixTree:
         dev = self.counters.device
         self.slot_key = torch.empty(n_slots, dtype=torch.int64, device=dev)
         self.slot_epoch = torch.empty(n_slots, dtype=torch.int64, device=dev)
-        self.view = N.PrefixView(N.ptr(self.slot_key), N.ptr(self.slot_epoch), n_slots, N.ptr(self.counters))
+        self.view = N.PrefixView(N.ptr(self.slot_key), N.ptr(self.slot_epoch), n_slots, N.ptr(self.counters),
+                                 self.hash_key & (2**64 - 1))
         N.check(N.lib().irm_prefix_reset(self.view, N.stream_ptr()), "irm_prefix_reset")
 
     def _reserve(self, n_tok: int, n_ins: int, ins_tok: int):
@@ -265,8 +273,11 @@ class DeviceRadixTree:
         flags = int(self.counters[1])
         if flags & 1:
             raise RuntimeError("device prefix index table is full: raise max_prefixes")
-        if flags & 2:
-            raise RuntimeError("device prefix index: a match failed token verification (hash collision)")
+
+    @property
+    def collisions_resolved(self) -> bool:
+        """True once some query met a hash collision (answered by the exact scan)."""
+        return bool(int(self.counters[1]) & 4)
 
     @property
     def n_prefixes(self) -> int:

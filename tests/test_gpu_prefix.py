@@ -134,3 +134,30 @@ def test_prefix_growth_golden(case):
     q = np.array([not o[0] for o in ops])
     assert np.array_equal(got_m[q], g["m"][q]) and np.array_equal(got_w[q], g["witness"][q])
     assert tree.slot_key.numel() > 16 and tree.arena.numel() > 64
+
+
+@pytest.mark.parametrize("case", sorted(RADIX_CASES))
+def test_prefix_collisions_answered_exactly(case):
+    """With degenerate hash keys (hash_key 1: every prefix of one length collides,
+    the worst an adversary could do) every query still gets the reference tree's
+    answer: the verification catches each false match and the exact on-device
+    scan answers it (a collision must not poison later queries)."""
+    g = load_npz("radix")[case]
+    ops = radix_case_inputs(RADIX_CASES[case])[:300]
+    tree = _tree(hash_key=1)
+    for b0 in range(0, len(ops), 37):
+        part = ops[b0:b0 + 37]
+        ins = [o[0] for o in part]
+        m, w = tree.run_ops([o[1] for o in part], ins, [not x for x in ins], handles=list(range(b0, b0 + len(part))))
+        m, w = m.cpu().numpy(), w.cpu().numpy()
+        for j, (is_ins, _seq) in enumerate(part):
+            if not is_ins:
+                assert m[j] == g["m"][b0 + j], (case, b0 + j)
+                assert (tree.handles[w[j]] if m[j] > 0 else -1) == g["witness"][b0 + j], (case, b0 + j)
+    tree.check()  # no error: collisions are resolved, not raised
+    assert tree.collisions_resolved or not any(not o[0] for o in ops)
+
+
+def test_prefix_keyed_hash_differs_per_index():
+    a, b = _tree(), _tree()
+    assert a.hash_key != b.hash_key

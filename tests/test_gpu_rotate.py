@@ -138,3 +138,23 @@ def test_delta_precision_sweep(R, theta):
             truth = O.rotate_rows(raw, np.full(n, p_src + dl), inv)
             worst = max(worst, O.rel_l2(got[i], truth))
         assert worst <= tol, (dt, theta, worst)
+
+
+def test_rotate_rows_uses_the_specs_own_frequencies():
+    """A spec carrying its own (e.g. scaled) inv_freq rotates by THOSE frequencies
+    on the device paths, as the reference's rotate_rows reads spec.inv_freq
+    (rotary.py:98-108) -- not make_spec's frequencies for the same theta."""
+    import dataclasses
+
+    from paper_2605_05696_b200 import rotary
+
+    base = rotary.make_spec(1e4)
+    scaled = dataclasses.replace(base, inv_freq=base.inv_freq * 0.25)
+    rng = np.random.default_rng(3)
+    rows = rng.standard_normal((7, 64))
+    pos = np.arange(7, dtype=np.float64) * 1000
+    got_base = rotary.rotate_rows(rows, pos, base)
+    got_scaled = rotary.rotate_rows(rows, pos, scaled)
+    assert O.rel_l2(got_base, O.rotate_rows(rows, pos, base.inv_freq)) <= 1e-12
+    assert O.rel_l2(got_scaled, O.rotate_rows(rows, pos, scaled.inv_freq)) <= 1e-12
+    assert O.rel_l2(got_scaled, got_base) > 1e-3
