@@ -412,6 +412,7 @@ def run_ours(args):
                          "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm, "unit": "GB/s",
                                       "frac": k1_gbs / hbm}},
             "cdc_hash_wide": cdc_wide_component(hbm),
+            "producer_rotate": producer_component(hbm),
             # K3 / K6 are latency-bound: queries/s and the step's ms, no roofline
             "store_lookup": {"value": n_queries / (k3 / 1e3), "unit": "queries/s", "launch_ms": k3,
                              "queries_per_launch": n_queries,
@@ -544,6 +545,50 @@ def run_sharded(pipe, n, load, wave0, graphs, after_front=None):
         pipe.run_overlapped(n, load, after_front=after_front, wave0=wave0)
     else:
         pipe.run_overlapped_sharded(n, load, wave0=wave0, k4_sms=K4_SMS, after_front=after_front)
+
+
+# ----------------------------------------------------------------- producer rotation
+def producer_component(hbm, n_rows=BODY):
+    """The producer side of the store (registry.py:126-140) at the
+    config-2 shape: the cold request's 32,768 novel rows, kr_raw of all 27 layers
+    rotated in place to p_src + i by ONE irm_rotate_rows_layered launch (cos/sin
+    per (row, frequency) once, applied to every layer). HBM-bound: the 128-byte
+    k_r slice of each 1,152-byte bf16 row is read and written."""
+    import torch
+
+    from paper_2605_05696_b200 import _native as N, ops
+
+    rng = np.random.default_rng(41)
+    pool = torch.randn(LAYERS, n_rows + 64, CKV + KR, device="cuda").to(torch.bfloat16)
+    kr = pool[:, :n_rows, CKV:]
+    lens, pos = [], []
+    while sum(lens) < n_rows:
+        lens.append(min(int(rng.integers(32, 400)), n_rows - sum(lens)))
+    p0 = 50 + 64
+    for ln in lens:
+        pos.append(np.arange(p0, p0 + ln))
+        p0 += ln
+    positions = torch.from_numpy(np.concatenate(pos).astype(np.float64)).cuda()
+    inv = ops.inv_freq_device(np.power(THETA, -2.0 * np.arange(KR // 2) / KR))
+    run = lambda: ops.rotate_rows_layered(kr, positions, inv, N.LAYOUT_INTERLEAVED, out=kr)
+    run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    a.record()
+    for _ in range(reps):
+        run()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    rows = n_rows * LAYERS
+    byt = rows * KR * 2 * 2
+    return {"value": rows / (ms / 1e3), "unit": "rows/s", "kernel": "irm_rotate_rows_layered (producer)",
+            "workload": f"{n_rows} novel rows x {LAYERS} layers, bf16 k_r rotated in place to p_src + i "
+                        f"({len(lens)} chunks), DSv2 interleaved theta {THETA:g}",
+            "launch_ms": ms, "roofline": {"bound": "hbm", "achieved": byt / (ms / 1e3) / 1e9, "peak": hbm,
+                                          "unit": "GB/s", "frac": byt / (ms / 1e3) / 1e9 / hbm,
+                                          "bytes_rule": "128 B of k_r read + written per (row, layer)"}}
 
 
 # ----------------------------------------------------------------- K1 with wide parallelism

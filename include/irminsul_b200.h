@@ -286,10 +286,18 @@ int irm_peer_export(const void *ptr, void *handle, int64_t *offset);
 int irm_peer_open(const void *handle, int64_t offset, void **ptr);
 /* Per-row absolute rotation (producer side of the store, registry.py:131-133
  * with rotary.py:98-108): out[i] = R(positions[i]) rows[i] for the dim-wide
- * rotary rows at rows + i*row_stride (elements). out may alias rows. */
+ * rotary rows at rows + i*row_stride (elements). out may alias rows. fp64 rows
+ * use correctly rounded cos/sin (the reference's f64 values bit for bit). */
 int irm_rotate_rows(const void *rows, int64_t row_stride, void *out, int64_t out_stride,
                     int64_t n, int32_t dim, const double *positions, const double *inv_freq,
                     int32_t layout, int32_t dtype, int32_t out_round, irm_stream_t stream);
+/* The same over `layers` layers at rows + l*rows_layer_stride (out: out_layer_stride),
+ * every layer's row i rotated by positions[i]: cos/sin evaluated once per (row,
+ * frequency) -- the batched producer of a multi-layer latent pool. */
+int irm_rotate_rows_layered(const void *rows, int64_t row_stride, int64_t rows_layer_stride, void *out,
+                            int64_t out_stride, int64_t out_layer_stride, int32_t layers, int64_t n, int32_t dim,
+                            const double *positions, const double *inv_freq, int32_t layout, int32_t dtype,
+                            int32_t out_round, irm_stream_t stream);
 /* Elementwise store rounding of f64 values: IRM_ROUND_F32 (f32 cast) or
  * IRM_ROUND_BF16 (rotary.py:63-87 round_bf16, single RNE incl. subnormals). */
 int irm_round_f64(const double *x, double *y, int64_t n, int32_t mode, irm_stream_t stream);

@@ -125,10 +125,15 @@ def marker_spans(req) -> list[tuple[int, int]]:
 KLASS = ("prefix_hit", "pic_hit", "s1_hit", "carveout_prefill", "novel_prefill")
 
 
-def serve_trace(reqs, k: int = 7, min_size: int = 32, max_size: int = 512, carve: int = 32):
-    """Sequential observer-mode serve; returns events (req, start, len, klass, fp, delta)."""
+def serve_trace(reqs, k: int = 7, min_size: int = 32, max_size: int = 512, carve: int = 32,
+                s1: bool = False, window: int = 128):
+    """Sequential observer-mode serve (engine.py:158-238); returns events
+    (req, start, len, klass, fp, delta). ``s1``: the sub-window fallback
+    (engine.py:116-139, 211-226): a missed chunk's aligned full windows are
+    probed against the fingerprints of every earlier novel chunk's windows."""
     seen: list[np.ndarray] = []
     registry: dict[int, int] = {}  # fp -> p_src
+    subwindows: set[int] = set()
     events = []
     for ri, req in enumerate(reqs):
         flat = flatten(req)
@@ -154,7 +159,23 @@ def serve_trace(reqs, k: int = 7, min_size: int = 32, max_size: int = 512, carve
             if f in registry:
                 events.append((ri, p, l, 1, f, p - registry[f]))
                 continue
-            events.append((ri, p, l, 4, -1, None))
+            novel = [(p, l)]
+            if s1:
+                chunk = tail[p - m:p - m + l]
+                wins = [(o, O.fingerprint(chunk[o:o + window])) for o in range(0, l - window + 1, window)]
+                hits = [(p + o, wf) for o, wf in wins if wf in subwindows]
+                for hs, wf in hits:
+                    events.append((ri, hs, window, 2, wf, None))
+                novel, pos = [], p
+                for hs, _ in hits:  # _subtract_spans (engine.py:211-226)
+                    if hs > pos:
+                        novel.append((pos, hs - pos))
+                    pos = hs + window
+                if pos < p + l:
+                    novel.append((pos, p + l - pos))
+                subwindows.update(wf for _, wf in wins)
+            for s_, l_ in novel:
+                events.append((ri, s_, l_, 4, -1, None))
             registry[f] = p
         seen.append(arr)
     return events, len(registry)

@@ -71,6 +71,7 @@ _SIGS = {
     "irm_rotate_gather": ([P, i64, P, i64, i32, i32, i32, P, P, P, P, i64, P, P, i32, i32, i32, i32, P, P, i64, P],
                           i32),
     "irm_rotate_rows": ([P, i64, P, i64, i64, i32, P, P, i32, i32, i32, P], i32),
+    "irm_rotate_rows_layered": ([P, i64, i64, P, i64, i64, i32, i64, i32, P, P, i32, i32, i32, P], i32),
     "irm_round_f64": ([P, P, i64, i32, P], i32),
     "irm_chunk_cossin": ([P, i64, P, P, P], i32),
     "irm_trace_scan": ([P, i64, i32, P, P, P, i32], i32),

@@ -228,8 +228,92 @@ __device__ __forceinline__ float rot_lo(float lo, float hi, float c, float s) {
 __device__ __forceinline__ float rot_hi(float lo, float hi, float c, float s) {
     return __fadd_rn(__fmul_rn(lo, s), __fmul_rn(hi, c));
 }
-__device__ __forceinline__ double rot_lo(double lo, double hi, double c, double s) { return lo * c - hi * s; }
-__device__ __forceinline__ double rot_hi(double lo, double hi, double c, double s) { return lo * s + hi * c; }
+// fp64: the reference's numpy expression, lo*cos - hi*sin / lo*sin + hi*cos, with every
+// product rounded on its own (rotary.py:107) -- no FMA contraction
+__device__ __forceinline__ double rot_lo(double lo, double hi, double c, double s) {
+    return __dsub_rn(__dmul_rn(lo, c), __dmul_rn(hi, s));
+}
+__device__ __forceinline__ double rot_hi(double lo, double hi, double c, double s) {
+    return __dadd_rn(__dmul_rn(lo, s), __dmul_rn(hi, c));
+}
+
+// ---------------------------------------------------------------- correctly rounded sincos
+// sin / cos of an fp64 angle evaluated in double-double (~100 bits) and rounded once, so
+// they equal the correctly rounded values the reference's rotary golden file holds
+// (rotary_reference.csv, rotary.py:104: numpy/libm cos, sin; all 384 rotated golden values
+// reproduce with correctly rounded cos/sin). CUDA's sincos is within 2 ulp, which left
+// 1-ulp differences in fp64 rotations. Cost: ~1k fp64 flops per angle, evaluated per
+// (chunk, frequency) -- not per row.
+struct ddouble {
+    double hi, lo;
+};
+__device__ __forceinline__ ddouble dd_two_sum(double a, double b) {
+    const double s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    return {s, __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb))};
+}
+__device__ __forceinline__ ddouble dd_fast(double a, double b) {  // |a| >= |b|
+    const double s = __dadd_rn(a, b);
+    return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ ddouble dd_add(ddouble a, ddouble b) {
+    ddouble s = dd_two_sum(a.hi, b.hi);
+    const ddouble t = dd_two_sum(a.lo, b.lo);
+    s = dd_fast(s.hi, __dadd_rn(s.lo, t.hi));
+    return dd_fast(s.hi, __dadd_rn(s.lo, t.lo));
+}
+__device__ __forceinline__ ddouble dd_mul(ddouble a, ddouble b) {
+    const double p = __dmul_rn(a.hi, b.hi);
+    const double e = __fma_rn(a.hi, b.hi, -p);
+    return dd_fast(p, __fma_rn(a.hi, b.lo, __fma_rn(a.lo, b.hi, e)));
+}
+
+__device__ __forceinline__ void sincos_cr(double x, double *sn, double *cs) {
+    // 1/n! as double-double, n = 0 .. 29
+    constexpr double IF_HI[30] = {
+        0x1.0p+0, 0x1.0p+0, 0x1.0p-1, 0x1.5555555555555p-3, 0x1.5555555555555p-5, 0x1.1111111111111p-7,
+        0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13, 0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19,
+        0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33,
+        0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-41, 0x1.ae7f3e733b81fp-45, 0x1.952c77030ad4ap-49,
+        0x1.6827863b97d97p-53, 0x1.2f49b46814157p-57, 0x1.e542ba4020225p-62, 0x1.71b8ef6dcf572p-66,
+        0x1.0ce396db7f853p-70, 0x1.761b41316381ap-75, 0x1.f2cf01972f578p-80, 0x1.3f3ccdd165fa9p-84,
+        0x1.88e85fc6a4e5ap-89, 0x1.d1ab1c2dccea3p-94, 0x1.0a18a2635085dp-98, 0x1.259f98b4358adp-103};
+    constexpr double IF_LO[30] = {
+        0.0, 0.0, 0.0, 0x1.5555555555555p-57, 0x1.5555555555555p-59, 0x1.1111111111111p-63,
+        -0x1.f49f49f49f49fp-65, 0x1.a01a01a01a01ap-73, 0x1.a01a01a01a01ap-76, -0x1.c154f8ddc6c00p-73,
+        0x1.cbbc05b4fa99ap-76, -0x1.c062e06d1f209p-80, -0x1.2aec959e14c06p-83, 0x1.f28e0cc748ebep-87,
+        0x1.05d6f8a2efd1fp-92, 0x1.1d8656b0ee8cbp-97, 0x1.1d8656b0ee8cbp-101, 0x1.ac981465ddc6cp-103,
+        0x1.eec01221a8b0bp-107, 0x1.2650f61dbdcb4p-112, 0x1.ea72b4afe3c2fp-120, -0x1.d043ae40c4647p-120,
+        -0x1.aebcdbd20331cp-124, -0x1.3423c7d91404fp-130, -0x1.9ada5fcc1ab14p-135, -0x1.58ddadf344487p-139,
+        -0x1.71c37ebd16540p-143, 0x1.054d0c78aea14p-149, 0x1.b9e2e28e1aa54p-153, 0x1.eaf8c39dd9bc5p-157};
+    // pi/2 in four doubles; reduction r = x - k pi/2 (|x| < 2^40: k fits, the first step is exact)
+    constexpr double P1 = 0x1.921fb54442d18p+0, P2 = 0x1.1a62633145c07p-54, P3 = -0x1.f1976b7ed8fbcp-110,
+                     P4 = 0x1.4cf98e804177dp-164;
+    const double k = rint(x * 0x1.45f306dc9c883p-1);
+    const double p = __dmul_rn(k, P1);
+    const double pe = __fma_rn(k, P1, -p);
+    ddouble r = dd_fast(__dsub_rn(x, p), -pe);  // x - p exact (Sterbenz), -pe its correction
+    const double q2 = __dmul_rn(k, P2);
+    r = dd_add(r, {-q2, -__fma_rn(k, P2, -q2)});
+    const double q3 = __dmul_rn(k, P3);
+    r = dd_add(r, {-q3, -__fma_rn(k, P3, -q3)});
+    r = dd_add(r, {-__dmul_rn(k, P4), 0.0});
+    const ddouble z = dd_mul(r, r);
+    ddouble s = {IF_HI[29], IF_LO[29]}, c = {IF_HI[28], IF_LO[28]};
+    for (int n = 27; n >= 1; n -= 2) {  // sin: sum (-1)^i r^(2i+1)/(2i+1)!
+        const ddouble t = dd_mul(z, s);
+        s = dd_add({IF_HI[n], IF_LO[n]}, {-t.hi, -t.lo});
+    }
+    for (int n = 26; n >= 0; n -= 2) {  // cos: sum (-1)^i r^(2i)/(2i)!
+        const ddouble t = dd_mul(z, c);
+        c = dd_add({IF_HI[n], IF_LO[n]}, {-t.hi, -t.lo});
+    }
+    s = dd_mul(s, r);
+    const int q = (int)(((long long)k % 4 + 4) % 4);
+    const double sv = s.hi, cv = c.hi;
+    *sn = q == 0 ? sv : q == 1 ? cv : q == 2 ? -sv : -cv;
+    *cs = q == 0 ? cv : q == 1 ? -sv : q == 2 ? -cv : sv;
+}
 
 template <int BLOCK>
 __device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t *total,

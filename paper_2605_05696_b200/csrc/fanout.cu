@@ -180,7 +180,7 @@ __global__ void member_cossin_kernel(const int64_t *__restrict__ delta, int64_t 
         const int64_t c = i / half;
         const int j = (int)(i - c * half);
         double s, co;
-        sincos((double)delta[c] * inv_freq[j], &s, &co);  // fp64 angle
+        sincos_cr((double)delta[c] * inv_freq[j], &s, &co);  // fp64 angle
         cs[i] = make_float2((float)co, (float)s);
     }
 }

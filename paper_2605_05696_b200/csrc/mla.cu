@@ -1451,7 +1451,7 @@ __global__ void cossin_kernel(const int64_t *__restrict__ delta, int64_t n_chunk
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_chunks * 32) return;
     double s, c;
-    sincos((double)delta[i / 32] * inv_freq[i % 32], &s, &c);  // fp64 angle (|delta| up to 2^20)
+    sincos_cr((double)delta[i / 32] * inv_freq[i % 32], &s, &c);  // fp64 angle (|delta| up to 2^20)
     cs[i] = make_float2((float)c, (float)s);
 }
 

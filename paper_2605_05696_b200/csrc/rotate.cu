@@ -63,12 +63,12 @@ template <typename CS>
 __device__ __forceinline__ CS make_cs(double a);
 template <> __device__ __forceinline__ float2 make_cs<float2>(double a) {
     double s, c;
-    sincos(a, &s, &c);
+    sincos_cr(a, &s, &c);
     return make_float2((float)c, (float)s);
 }
 template <> __device__ __forceinline__ double2 make_cs<double2>(double a) {
     double s, c;
-    sincos(a, &s, &c);
+    sincos_cr(a, &s, &c);
     return make_double2(c, s);
 }
 
@@ -235,9 +235,26 @@ __global__ void rotate_gather_generic_kernel(GatherArgs a, const typename Elem<T
 }
 
 // ------------------------------------------------------------ per-row rotation
+// One thread per (row, frequency): the angle's cos/sin are computed once and applied to
+// the row in every layer (the producer rotates kr_raw of all layers by the same p_src + i,
+// registry.py:131-133). fp64 rows take correctly rounded cos/sin (sincos_cr: the
+// reference's f64 values bit for bit); fp32/bf16 rows round CUDA's fp64 sincos to fp32.
+template <typename CS>
+__device__ __forceinline__ CS row_cs(double a);
+template <> __device__ __forceinline__ double2 row_cs<double2>(double a) {
+    double s, c;
+    sincos_cr(a, &s, &c);
+    return make_double2(c, s);
+}
+template <> __device__ __forceinline__ float2 row_cs<float2>(double a) {
+    double s, c;
+    sincos(a, &s, &c);
+    return make_float2((float)c, (float)s);
+}
+
 template <typename T>
-__global__ void rotate_rows_kernel(const T *__restrict__ rows, int64_t rs, T *__restrict__ out,
-                                   int64_t os, int64_t n, int half,
+__global__ void rotate_rows_kernel(const T *__restrict__ rows, int64_t rs, int64_t rls, T *__restrict__ out,
+                                   int64_t os, int64_t ols, int64_t n, int half, int layers,
                                    const double *__restrict__ pos, const double *__restrict__ inv_freq,
                                    int layout, int round) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -247,10 +264,14 @@ __global__ void rotate_rows_kernel(const T *__restrict__ rows, int64_t rs, T *__
     const int ilo = layout == IRM_LAYOUT_INTERLEAVED ? 2 * j : j;
     const int ihi = layout == IRM_LAYOUT_INTERLEAVED ? 2 * j + 1 : j + half;
     using A = typename Elem<T>::Acc;
-    const auto cs = make_cs<typename Elem<T>::CS>(pos[r] * inv_freq[j]);
-    const A lo = Elem<T>::load(rows[r * rs + ilo]), hi = Elem<T>::load(rows[r * rs + ihi]);
-    out[r * os + ilo] = Elem<T>::store(rot_lo(lo, hi, (A)cs.x, (A)cs.y), round);
-    out[r * os + ihi] = Elem<T>::store(rot_hi(lo, hi, (A)cs.x, (A)cs.y), round);
+    const auto cs = row_cs<typename Elem<T>::CS>(pos[r] * inv_freq[j]);
+    for (int l = 0; l < layers; ++l) {
+        const T *src = rows + l * rls + r * rs;
+        T *dst = out + l * ols + r * os;
+        const A lo = Elem<T>::load(src[ilo]), hi = Elem<T>::load(src[ihi]);
+        dst[ilo] = Elem<T>::store(rot_lo(lo, hi, (A)cs.x, (A)cs.y), round);
+        dst[ihi] = Elem<T>::store(rot_hi(lo, hi, (A)cs.x, (A)cs.y), round);
+    }
 }
 
 // ------------------------------------------------------------ host launchers
@@ -374,11 +395,11 @@ extern "C" int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, vo
     return launch_gather<double>(a, ws, delta, inv_freq, max_sms, st);
 }
 
-extern "C" int irm_rotate_rows(const void *rows, int64_t row_stride, void *out, int64_t out_stride,
-                               int64_t n, int32_t dim, const double *positions,
-                               const double *inv_freq, int32_t layout, int32_t dtype,
-                               int32_t out_round, irm_stream_t stream) {
-    IRM_REQUIRE(n >= 0 && dim >= 0 && dim % 2 == 0, "bad sizes (dim even)");
+extern "C" int irm_rotate_rows_layered(const void *rows, int64_t row_stride, int64_t rows_layer_stride, void *out,
+                                       int64_t out_stride, int64_t out_layer_stride, int32_t layers, int64_t n,
+                                       int32_t dim, const double *positions, const double *inv_freq, int32_t layout,
+                                       int32_t dtype, int32_t out_round, irm_stream_t stream) {
+    IRM_REQUIRE(n >= 0 && dim >= 0 && dim % 2 == 0 && layers >= 1, "bad sizes (dim even, layers >= 1)");
     IRM_REQUIRE(layout == IRM_LAYOUT_HALF_SPLIT || layout == IRM_LAYOUT_INTERLEAVED, "bad layout");
     IRM_REQUIRE(out_round == IRM_ROUND_NONE || dtype == IRM_DTYPE_F64, "out_round applies to f64 only");
     if (n == 0 || dim == 0) return IRM_OK;
@@ -387,15 +408,29 @@ extern "C" int irm_rotate_rows(const void *rows, int64_t row_stride, void *out, 
     const unsigned grid = (unsigned)((n * half + 255) / 256);
     cudaStream_t st = (cudaStream_t)stream;
     if (dtype == IRM_DTYPE_BF16)
-        rotate_rows_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16 *)rows, row_stride, (__nv_bfloat16 *)out, out_stride, n, half, positions, inv_freq, layout, out_round);
+        rotate_rows_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+            (const __nv_bfloat16 *)rows, row_stride, rows_layer_stride, (__nv_bfloat16 *)out, out_stride,
+            out_layer_stride, n, half, layers, positions, inv_freq, layout, out_round);
     else if (dtype == IRM_DTYPE_F32)
-        rotate_rows_kernel<float><<<grid, 256, 0, st>>>((const float *)rows, row_stride, (float *)out, out_stride, n, half, positions, inv_freq, layout, out_round);
+        rotate_rows_kernel<float><<<grid, 256, 0, st>>>((const float *)rows, row_stride, rows_layer_stride,
+                                                        (float *)out, out_stride, out_layer_stride, n, half,
+                                                        layers, positions, inv_freq, layout, out_round);
     else if (dtype == IRM_DTYPE_F64)
-        rotate_rows_kernel<double><<<grid, 256, 0, st>>>((const double *)rows, row_stride, (double *)out, out_stride, n, half, positions, inv_freq, layout, out_round);
+        rotate_rows_kernel<double><<<grid, 256, 0, st>>>((const double *)rows, row_stride, rows_layer_stride,
+                                                         (double *)out, out_stride, out_layer_stride, n, half,
+                                                         layers, positions, inv_freq, layout, out_round);
     else
         IRM_REQUIRE(false, "bad dtype");
     IRM_LAUNCH_CHECK();
     return IRM_OK;
+}
+
+extern "C" int irm_rotate_rows(const void *rows, int64_t row_stride, void *out, int64_t out_stride,
+                               int64_t n, int32_t dim, const double *positions,
+                               const double *inv_freq, int32_t layout, int32_t dtype,
+                               int32_t out_round, irm_stream_t stream) {
+    return irm_rotate_rows_layered(rows, row_stride, 0, out, out_stride, 0, 1, n, dim, positions, inv_freq, layout,
+                                   dtype, out_round, stream);
 }
 
 // Elementwise store rounding of f64 values (rotary.py:63-95: round_bf16 / f32 cast).

@@ -215,6 +215,14 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
         assert int(h_entry[c]) == len(reg), "device store and host mirror diverged"
         reg.commit_rows(int(h_fp_u[c]), toks, plans[ri].m + s, int(h_row[c]))
 
+    # ---- S1 sub-window fallback (engine.py:116-139, 211-226), batched: every aligned full
+    # window of every novel chunk is fingerprinted by ONE K2 launch; in the sequential order
+    # a window hits iff its fingerprint was indexed before the batch or by a window of an
+    # earlier novel chunk (a chunk is indexed only after its own probe)
+    s1_hits: dict[int, list[tuple[int, int]]] = {}
+    if config.s1_enabled:
+        s1_hits = _s1_batch(state, tails, [p.m for p in plans], off, h_hit, h_start, h_len)
+
     # ---- events, per request in chunk order
     results: list[ServeResult] = []
     live_hits = []  # (request, chunk index)
@@ -247,23 +255,16 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
                     live_hits.append((ri, c, len(events) - 1))
                 continue
             novel_spans = [(p, ln)]
-            if config.s1_enabled:
-                toks = plan.flat[p:p + ln]
-                hits = s1_probe(toks, p, state.subwindows, config.s1_window)
-                for hs, hl in hits:
-                    counts[ServiceClass.S1_HIT] += hl
-                    events.append(SegmentEvent(hs, hl, ServiceClass.S1_HIT, fingerprint(plan.flat[hs:hs + hl])))
-                novel_spans = _subtract_spans((p, ln), hits)
+            hits = s1_hits.get(c)
+            if hits:
+                w = config.s1_window
+                for hs, hf in hits:
+                    counts[ServiceClass.S1_HIT] += w
+                    events.append(SegmentEvent(hs, w, ServiceClass.S1_HIT, hf))
+                novel_spans = _subtract_spans((p, ln), [(hs, w) for hs, _ in hits])
             for s, l in novel_spans:
                 counts[ServiceClass.NOVEL_PREFILL] += l
                 events.append(SegmentEvent(s, l, ServiceClass.NOVEL_PREFILL))
-            if config.s1_enabled:
-                w = config.s1_window
-                toks = plan.flat[p:p + ln]
-                offs = list(range(0, ln - w + 1, w))
-                if offs:
-                    fps = fingerprint_spans(toks, np.array(offs, np.int64), np.full(len(offs), w, np.int64))
-                    state.subwindows.update(int(f) for f in fps)
             live_rows += ln
         assert sum(counts.values()) == n, "service classes must tile the request"
         results.append(ServeResult(counts, events, n, live_rows if config.mode == Mode.LIVE else None, 0))
@@ -271,6 +272,39 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
     if config.mode == Mode.LIVE and live_hits:
         _verify_hits(state, plans, live_hits, h_start, h_len, h_entry, h_psrc, results)
     return results
+
+
+def _s1_batch(state, tails, ms, off, h_hit, h_start, h_len) -> dict[int, list[tuple[int, int]]]:
+    """All S1 probes and sub-window indexing of a batch: one fingerprint launch.
+    Returns {chunk index: [(absolute window start, window fingerprint), ...]} for
+    the windows that hit, in window order; state.subwindows gains every window."""
+    w = state.config.s1_window
+    nov = np.nonzero(h_hit == 0)[0]  # probed misses (the inserted chunks), in sequential order
+    nwin = h_len[nov] // w
+    total = int(nwin.sum())
+    if total == 0:
+        return {}
+    win_chunk = np.repeat(nov, nwin)
+    j = np.arange(total) - np.repeat(np.cumsum(nwin) - nwin, nwin)
+    req = np.searchsorted(off, win_chunk, side="right") - 1
+    tail_base = np.concatenate([[0], np.cumsum([len(t) for t in tails])])
+    start_tail = h_start[win_chunk] + j * w
+    fps = fingerprint_spans(np.concatenate(tails), tail_base[req] + start_tail, np.full(total, w, np.int64))
+    prior = np.fromiter(state.subwindows, dtype=np.uint64, count=len(state.subwindows))
+    hit = np.isin(fps, prior)
+    # the first novel chunk (in order) carrying each fingerprint; a later chunk's window hits it
+    order = np.lexsort((win_chunk, fps))
+    fs = fps[order]
+    head = np.maximum.accumulate(np.where(np.r_[True, fs[1:] != fs[:-1]], np.arange(total), 0))
+    first_chunk = np.empty(total, np.int64)
+    first_chunk[order] = win_chunk[order][head]
+    hit |= first_chunk < win_chunk
+    state.subwindows.update(fps.tolist())
+    ms = np.asarray(ms, np.int64)
+    out: dict[int, list[tuple[int, int]]] = {}
+    for k in np.nonzero(hit)[0]:
+        out.setdefault(int(win_chunk[k]), []).append((int(ms[req[k]] + start_tail[k]), int(fps[k])))
+    return out
 
 
 def _verify_hits(state, plans, live_hits, h_start, h_len, h_entry, h_psrc, results):

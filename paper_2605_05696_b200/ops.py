@@ -291,6 +291,24 @@ def rotate_rows(rows: torch.Tensor, positions: torch.Tensor, inv_freq: torch.Ten
     return out
 
 
+def rotate_rows_layered(rows: torch.Tensor, positions: torch.Tensor, inv_freq: torch.Tensor,
+                        layout: int = N.LAYOUT_HALF_SPLIT, out: torch.Tensor | None = None) -> torch.Tensor:
+    """irm_rotate_rows_layered: rows [layers, n, dim] (any row / layer stride, unit
+    element stride), every layer's row i rotated by positions[i]; in place when
+    ``out`` is ``rows``."""
+    assert rows.dim() == 3 and rows.stride(2) == 1
+    if out is None:
+        out = torch.empty(rows.shape, dtype=rows.dtype, device=rows.device)
+    assert out.shape == rows.shape and out.stride(2) == 1
+    pos = positions.to(device=rows.device, dtype=torch.float64).contiguous()
+    rc = N.lib().irm_rotate_rows_layered(N.ptr(rows), rows.stride(1), rows.stride(0), N.ptr(out), out.stride(1),
+                                         out.stride(0), rows.shape[0], rows.shape[1], rows.shape[2], N.ptr(pos),
+                                         N.ptr(inv_freq), layout, _DTYPE_CODE[rows.dtype], N.ROUND_NONE,
+                                         N.stream_ptr())
+    N.check(rc, "irm_rotate_rows_layered")
+    return out
+
+
 def round_f64(x: torch.Tensor, mode: int) -> torch.Tensor:
     x = x.contiguous()
     y = torch.empty_like(x)

@@ -218,25 +218,36 @@ class KvRegistry:
         return entry
 
     def _flush(self):
-        """Synthesise, upload and rotate the rows of every entry not yet written."""
+        """Producer (registry.py:131-136), batched: the synthetic rows of every entry
+        not yet written go up in ONE host->device copy, k_r is rotated to p_src + i
+        for all of them by ONE irm_rotate_rows launch, the rows land in the pool by
+        one scatter, and kr_base comes back in one copy."""
         pending, self._pending = self._pending, []
-        ckv = self.kv_params.ckv_dim
-        for entry in pending:
-            row, n = self._entry_rows[entry.insert_epoch], entry.chunk_len
-            c_kv, kr_raw = self._synth.rows(entry._tokens)
-            self.pool.ensure(row + n)
-            d = self.pool.data
-            dev = d.device
-            if n:
-                d[0, row:row + n, :ckv] = torch.from_numpy(c_kv).to(dev)
-                d[0, row:row + n, ckv:] = torch.from_numpy(kr_raw).to(dev)
-                pos = torch.arange(entry.p_src, entry.p_src + n, dtype=torch.float64, device=dev)
-                kr_view = d[0, row:row + n, ckv:]
-                ops.rotate_rows(kr_view, pos, inv_freq_device(self.spec), self.spec.layout_code, out=kr_view)
-                kr_base = kr_view.cpu().numpy().copy()
-            else:
-                kr_base = np.zeros((0, self.kv_params.kr_dim))
-            c_kv = c_kv.copy()
+        if not pending:
+            return
+        ckv, kr = self.kv_params.ckv_dim, self.kv_params.kr_dim
+        rows = [self._synth.rows(e._tokens) for e in pending]
+        lens = np.array([e.chunk_len for e in pending], np.int64)
+        total = int(lens.sum())
+        c_all = [r[0] for r in rows]
+        if total:
+            starts = np.array([self._entry_rows[e.insert_epoch] for e in pending], np.int64)
+            self.pool.ensure(int((starts + lens).max()))
+            dev = self.pool.data.device
+            stage = np.empty((total, ckv + kr), np.float64)
+            stage[:, :ckv] = np.concatenate([r[0] for r in rows if len(r[0])])
+            stage[:, ckv:] = np.concatenate([r[1] for r in rows if len(r[1])])
+            pos = np.concatenate([np.arange(e.p_src, e.p_src + e.chunk_len, dtype=np.float64) for e in pending])
+            st = torch.from_numpy(stage).to(dev)
+            ops.rotate_rows(st[:, ckv:], torch.from_numpy(pos).to(dev), inv_freq_device(self.spec),
+                            self.spec.layout_code, out=st[:, ckv:])
+            dst = torch.from_numpy(np.repeat(starts, lens) + (np.arange(total) - np.repeat(np.cumsum(lens) - lens, lens)))
+            self.pool.data[0].index_copy_(0, dst.to(dev), st)
+            kr_all = st[:, ckv:].cpu().numpy()
+        bounds = np.concatenate([[0], np.cumsum(lens)])
+        for k, entry in enumerate(pending):
+            c_kv = c_all[k].copy()
+            kr_base = kr_all[bounds[k]:bounds[k + 1]].copy() if entry.chunk_len else np.zeros((0, kr))
             c_kv.setflags(write=False)
             kr_base.setflags(write=False)
             entry._c_kv, entry._kr_base = c_kv, kr_base

@@ -16,13 +16,7 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
 
 
-def load_npz(name: str) -> dict[str, dict[str, np.ndarray]]:
-    z = np.load(os.path.join(GOLDEN, f"{name}.npz"))
-    out: dict[str, dict[str, np.ndarray]] = {}
-    for key in z.files:
-        case, field = key.split("/", 1)
-        out.setdefault(case, {})[field] = z[key]
-    return out
+from goldens import load_npz  # noqa: E402  (tests/golden/goldens.py)
 
 
 @pytest.fixture(scope="session")

@@ -130,7 +130,31 @@ TRACE_CASES = {
     "rerank": dict(pattern="rerank", n_req=20, body_len=2500, seed=4),
     "tool_variants": dict(pattern="tool_variants", n_req=12, body_len=2500, seed=5),
     "agent_meta_k5": dict(pattern="agent_meta", n_req=6, body_len=3000, seed=9, k=5),
+    # S1 sub-window fallback (engine.py:116-139, 211-226): s1_enabled serve configs
+    "compact_s1": dict(pattern="compact", n_req=10, body_len=3000, seed=11, s1=True),
+    "compact_s1_k20": dict(pattern="compact", n_req=10, body_len=3000, seed=11, s1=True, k=20),
+    "rerank_s1": dict(pattern="rerank", n_req=12, body_len=2500, seed=4, s1=True),
+    "tool_variants_s1_k20": dict(pattern="tool_variants", n_req=10, body_len=2500, seed=5, s1=True, k=20),
+    # a shared body behind per-request headers whose lengths differ by multiples of the window
+    # but not of the 512-token max-clamp chunk (k=20): chunks miss, aligned sub-windows hit
+    "s1_shift": dict(custom="s1_shift", n_req=10, body_len=4000, seed=21, s1=True, k=20, window=128),
+    "s1_shift_w64": dict(custom="s1_shift", n_req=10, body_len=3000, seed=22, s1=True, k=20, window=64),
+    "s1_shift_k7": dict(custom="s1_shift", n_req=8, body_len=3000, seed=23, s1=True, k=7, window=128),
 }
+
+
+def custom_trace(case: dict):
+    """Requests (lists of (kind, tokens, shared_id) segments) of the custom trace cases."""
+    assert case["custom"] == "s1_shift"
+    rng = np.random.default_rng(case["seed"])
+    w = case["window"]
+    body = [int(t) for t in rng.integers(0, 2**32, size=case["body_len"], dtype=np.uint64)]
+    reqs = []
+    for i in range(case["n_req"]):
+        hdr_len = 100 + w * (i % 5) + 512 * (i // 5)  # i and i + 5: same shift mod 512 -> PIC hits
+        hdr = [int(t) for t in rng.integers(0, 2**32, size=hdr_len, dtype=np.uint64)]
+        reqs.append([("header", hdr, None), ("body", body, "s1_body")])
+    return reqs
 
 
 # K0 / radix.py: operation sequences (insert or query, with a token sequence each)

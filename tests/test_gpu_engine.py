@@ -5,7 +5,7 @@ live mode passes / trips the rotation check like engine.py:142-155."""
 import numpy as np
 import pytest
 
-from inputs import TRACE_CASES
+from inputs import TRACE_CASES, custom_trace
 from oracle import workloads as W
 
 pytestmark = pytest.mark.gpu
@@ -29,8 +29,9 @@ def test_trace_events_golden(E, name, batch, golden_traces):
     engine, model, chunking, _ = E
     case = dict(TRACE_CASES[name])
     k = case.pop("k", 7)
-    reqs = to_requests(model, W.generate(**case))
-    cfg = engine.ServeConfig(chunker=chunking.ChunkerParams(mask_exponent=k))
+    s1, window = case.pop("s1", False), case.pop("window", 128)
+    reqs = to_requests(model, custom_trace(TRACE_CASES[name]) if "custom" in case else W.generate(**case))
+    cfg = engine.ServeConfig(chunker=chunking.ChunkerParams(mask_exponent=k), s1_enabled=s1, s1_window=window)
     state = engine.EngineState(cfg)
     results, _ = engine.run_trace(state, model.Trace(tuple(reqs)), batch=batch)
     g = golden_traces[name]
@@ -39,10 +40,12 @@ def test_trace_events_golden(E, name, batch, golden_traces):
     assert len(ev) == g["req"].size
     for i, (ri, s, l, kl, fp, d) in enumerate(ev):
         assert (ri, s, l, kl) == (g["req"][i], g["start"][i], g["length"][i], g["klass"][i]), i
+        want_fp = None if int(g["fp"][i]) == 2**64 - 1 else int(g["fp"][i])  # -1 encodes None
+        assert fp == want_fp, i
         if g["has_delta"][i]:
-            assert fp == int(g["fp"][i]) and d == int(g["delta"][i])
+            assert d == int(g["delta"][i])
         else:
-            assert fp is None and d is None
+            assert d is None
     counts = np.array([[r.counts[k] for k in engine.ServiceClass] for r in results])
     assert np.array_equal(counts, g["counts"])
     assert len(state.registry) == int(g["registry_len"][0])

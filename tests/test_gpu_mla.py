@@ -111,7 +111,7 @@ def test_mla_vs_reference_materialize(ops):
     KvRegistry.materialize (tests/golden/mla.npz, make_golden.py): 4 cached documents
     re-inserted in a permuted order (delta = p_dest - p_src per chunk), paged pool rows,
     DSv3 half-split rotary theta 5e4; within the 4.7e-3 rel-L2 bound."""
-    from conftest import load_npz
+    from goldens import load_npz
 
     o, N = ops
     c = load_npz("mla")["case"]

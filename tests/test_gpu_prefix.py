@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import load_npz
+from goldens import load_npz
 from inputs import RADIX_CASES, radix_case_inputs
 from oracle import oracle as O
 

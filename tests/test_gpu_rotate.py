@@ -158,3 +158,72 @@ def test_rotate_rows_uses_the_specs_own_frequencies():
     assert O.rel_l2(got_base, O.rotate_rows(rows, pos, base.inv_freq)) <= 1e-12
     assert O.rel_l2(got_scaled, O.rotate_rows(rows, pos, scaled.inv_freq)) <= 1e-12
     assert O.rel_l2(got_scaled, got_base) > 1e-3
+
+
+def _cr_sincos(x: float):
+    """Correctly rounded (sin, cos) of a double via 60-digit Decimal arithmetic."""
+    from decimal import Decimal, getcontext
+
+    getcontext().prec = 60
+    pi = Decimal("3.14159265358979323846264338327950288419716939937510582097494459230781640628620899")
+    d = Decimal(x)
+    k = (d / (pi / 2)).to_integral_value()
+    r = d - k * (pi / 2)
+    s = c = Decimal(0)
+    term, n = r, 1
+    while abs(term) > Decimal(10) ** -55:
+        s, n, term = s + term, n + 2, -term * r * r / ((n + 1) * (n + 2))
+    term, n = Decimal(1), 0
+    while abs(term) > Decimal(10) ** -55:
+        c, n, term = c + term, n + 2, -term * r * r / ((n + 1) * (n + 2))
+    q = int(k) % 4
+    s, c = [(s, c), (c, -s), (-s, -c), (-c, s)][q]
+    return float(s), float(c)
+
+
+def test_f64_rotation_bit_exact_with_correctly_rounded_trig():
+    """fp64 rotations use correctly rounded cos/sin (double-double, common.cuh
+    sincos_cr) and separately rounded products -- the arithmetic that
+    reproduces every value of the reference's rotary golden file
+    (rotary_reference.csv; rotary.py:104-108): bit-exact against that
+    arithmetic on random rows and positions up to 2^20, three thetas."""
+    from paper_2605_05696_b200 import rotary
+
+    rng = np.random.default_rng(11)
+    rows = rng.standard_normal((150, 64))
+    pos = rng.integers(-(2**20), 2**20, size=150).astype(np.float64)
+    for theta in (1e4, 5e4, 3.2e7):
+        spec = rotary.make_spec(theta)
+        got = rotary.rotate_rows(rows, pos, spec)
+        ang = pos[:, None] * spec.inv_freq[None, :]
+        sc = np.array([[_cr_sincos(float(a)) for a in row] for row in ang])
+        s, c = sc[..., 0], sc[..., 1]
+        lo, hi = rows[:, :32], rows[:, 32:]
+        ref = np.concatenate([lo * c - hi * s, lo * s + hi * c], axis=1)
+        assert np.array_equal(got, ref), (theta, np.mean(got == ref))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "f64"])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_rotate_rows_layered_matches_per_layer(dtype, layout):
+    """irm_rotate_rows_layered (the batched producer: cos/sin once per (row,
+    frequency), every layer rotated) equals irm_rotate_rows layer by layer,
+    in place on the k_r slice of a [layers, rows, 576] pool, bit for bit."""
+    import torch
+
+    from paper_2605_05696_b200 import ops
+
+    dt = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[dtype]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    pool = torch.randn(5, 700, 576, device="cuda", generator=g, dtype=torch.float64).to(dt)
+    pos = torch.from_numpy(np.random.default_rng(1).integers(-(2**20), 2**20, size=600).astype(np.float64)).cuda()
+    inv = ops.inv_freq_device(O.make_inv_freq(5e4))
+    ref = pool.clone()
+    for l in range(5):
+        ops.rotate_rows(ref[l, :600, 512:], pos, inv, layout, out=ref[l, :600, 512:])
+    got = pool.clone()
+    kr = got[:, :600, 512:]
+    ops.rotate_rows_layered(kr, pos, inv, layout, out=kr)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    assert not torch.equal(got[:, :600, 512:], pool[:, :600, 512:])

@@ -16,7 +16,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN
+from goldens import GOLDEN
 
 from paper_2605_05696_b200 import model as M
 

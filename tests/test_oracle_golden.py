@@ -10,8 +10,8 @@ import pytest
 
 from oracle import oracle as O
 from oracle import workloads as W
-from conftest import load_npz
-from inputs import (CDC_CASES, GEAR, RADIX_CASES, ROT_CASES, TRACE_CASES, cdc_case_inputs, marker_tokens,
+from goldens import load_npz
+from inputs import (CDC_CASES, GEAR, RADIX_CASES, ROT_CASES, TRACE_CASES, cdc_case_inputs, custom_trace, marker_tokens,
                     radix_case_inputs, rot_case_inputs)
 
 
@@ -110,8 +110,9 @@ def test_registry_materialize_oracle(golden_registry):
 def test_trace_events_golden(name, golden_traces):
     case = dict(TRACE_CASES[name])
     k = case.pop("k", 7)
-    reqs = W.generate(**case)
-    events, n_entries = W.serve_trace(reqs, k=k)
+    s1, window = case.pop("s1", False), case.pop("window", 128)
+    reqs = custom_trace(TRACE_CASES[name]) if "custom" in case else W.generate(**case)
+    events, n_entries = W.serve_trace(reqs, k=k, s1=s1, window=window)
     g = golden_traces[name]
     assert n_entries == int(g["registry_len"][0])
     assert len(events) == g["req"].size
@@ -119,6 +120,8 @@ def test_trace_events_golden(name, golden_traces):
         assert (ri, s, l, kl) == (g["req"][i], g["start"][i], g["length"][i], g["klass"][i])
         if kl == 1:
             assert fp == int(g["fp"][i]) and d == int(g["delta"][i]) and g["has_delta"][i]
+        if kl == 2:  # S1 hit: the window's fingerprint, no delta
+            assert fp == int(g["fp"][i]) and not g["has_delta"][i]
 
 
 def test_threaded_batch_matches_single():
