@@ -373,8 +373,8 @@ def run_ours(args):
     # production path vs the sequential oracle over every wave this run served
     parity = None
     if world == 1:
-        parity = pipeline_parity(pipe, packed, n_steps, overlapped, sharded, graphs if sharded else True, pool,
-                                 dev_in, req_stride, wave0=5 * n_steps + 12)
+        parity = pipeline_parity(pipe, [packed[-1]] + packed[:n_steps], packed[n_steps], dev_in[n_steps], overlapped,
+                                 sharded, graphs if sharded else True, pool, req_stride, wave0=5 * n_steps + 12)
 
     # -------- roofline of the dominant kernel (K4) and K1
     k4_bytes = (src_rows + k4_rows) * (CKV + KR) * 2  # bf16 rows: unique source reads + destination writes
@@ -448,13 +448,14 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def pipeline_parity(pipe, packed, n_steps, overlapped, sharded, graphs, pool, dev_in, req_stride, wave0,
-                    chunks_per_request=3):
+def pipeline_parity(pipe, served, check_packed, check_dev, overlapped, sharded, graphs, pool, req_stride, wave0,
+                    chunks_per_request=3, theta=THETA):
     """The checker for the timed path. Runs the never-served
-    check wave (packed[n_steps]) through the same production path the timed
-    region used (overlapped graphs / serial graph / sharded), then replays the
-    sequential oracle over every wave this process served, in serve order (the
-    cold wave, then waves 0 .. n_steps-1; re-served waves insert nothing new):
+    check wave (``check_packed`` / its device copy ``check_dev``) through the same
+    production path the timed region used (overlapped graphs / serial graph /
+    sharded), then replays the sequential oracle over every wave this process
+    served, in serve order (``served``: packed waves; re-served waves insert
+    nothing new):
     oracle/irm_oracle.c CDC + xxh64 per request, a first-writer-wins dict with
     the carve-out (engine.py:181-226) and pool rows handed out in query order
     (store.cu). Checked: the check wave's per-chunk service map, bit-exact; and,
@@ -466,9 +467,8 @@ def pipeline_parity(pipe, packed, n_steps, overlapped, sharded, graphs, pool, de
 
     from oracle import oracle as O
 
-    check = n_steps
     hit_map = {}
-    load = lambda i: pipe.load(*dev_in[check])
+    load = lambda i: pipe.load(*check_dev)
     if overlapped:
         grab = lambda i, s: hit_map.__setitem__("hit", pipe.slots[s]["hit"].clone())
         if sharded:
@@ -478,7 +478,7 @@ def pipeline_parity(pipe, packed, n_steps, overlapped, sharded, graphs, pool, de
         torch.cuda.synchronize()
         out = pipe.slots[0]["out"]
     else:
-        pipe.load(*dev_in[check])
+        pipe.load(*check_dev)
         pipe.step_sharded(wave0) if sharded else pipe.replay()
         torch.cuda.synchronize()
         hit_map["hit"] = pipe.hit.clone()
@@ -487,9 +487,9 @@ def pipeline_parity(pipe, packed, n_steps, overlapped, sharded, graphs, pool, de
 
     t0 = time.perf_counter()
     reg, rows_next = {}, 0
-    order = [len(packed) - 1] + list(range(n_steps)) + [check]
-    for w in order:
-        tok, off, poff, pins, ms = packed[w]
+    order = list(served) + [check_packed]
+    for wave in order:
+        tok, off, poff, pins, ms = wave
         recs = []
         for r in range(off.size - 1):
             st, ln, fp, _ = O.cdc_chunk(tok[off[r]:off[r + 1]], pins=pins[poff[r]:poff[r + 1]])
@@ -523,7 +523,7 @@ def pipeline_parity(pipe, packed, n_steps, overlapped, sharded, graphs, pool, de
     mini = np.ascontiguousarray(mini)
     starts = np.concatenate([[0], np.cumsum(ln)[:-1]]).astype(np.int64)
     exp = np.zeros_like(got)
-    inv = np.power(THETA, -2.0 * np.arange(KR // 2) / KR)
+    inv = np.power(theta, -2.0 * np.arange(KR // 2) / KR)
     O.rotate_gather_bf16(mini, exp, starts, starts, ln, delta, inv, interleaved=True)
     ckv_ok = bool(np.array_equal(got[..., :CKV], exp[..., :CKV]))
     f = lambda u: (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
@@ -538,6 +538,211 @@ def pipeline_parity(pipe, packed, n_steps, overlapped, sharded, graphs, pool, de
             "sample": f"check wave ({pipe.R} fresh requests, never served before) through the timed path; oracle "
                       f"replayed over {len(order)} waves ({time.perf_counter() - t0:.1f} s); KV: first/middle/last "
                       f"hit chunk per request x all layers"}
+
+
+# ----------------------------------------------------------------- config 5: sharded sessions
+C5_SESSIONS_PER_GPU, C5_R, C5_BODY, C5_DOC, C5_HEADER = 64, 16, 16384, 2048, 64
+
+
+def c5_request(s, t, header, doc, marker):
+    """Session s, turn t of the config-5 agent workload (the agent_meta shape of
+    workloads.py:85-100 per session): the fleet-wide system header, the turn's
+    metadata, the marker, a tool document shared by every session, and the
+    session's own 16K-token context. Returns (tail after the header, pins, m)."""
+    srng = np.random.default_rng(1_000_003 * (s + 1))
+    body = srng.integers(0, 2**32, size=C5_BODY, dtype=np.uint64).astype(np.uint32)
+    trng = np.random.default_rng(7_919 * (s + 1) + t)
+    meta = trng.integers(0, 2**32, size=int(trng.integers(30, 71)), dtype=np.uint64).astype(np.uint32)
+    tail = np.concatenate([meta, marker, doc, body])
+    return tail, sorted({meta.size - 1, meta.size + 63}), C5_HEADER
+
+
+def c5_wave(rank, world, sessions, block, turn, header, doc, marker):
+    """R requests of this rank: local sessions [block*R, (block+1)*R) at `turn`
+    (global session id = rank + world * local index: sessions s mod G)."""
+    streams, pins, ms = [], [], []
+    for i in range(block * C5_R, (block + 1) * C5_R):
+        tail, p, m = c5_request(rank + world * (i % sessions), turn, header, doc, marker)
+        streams.append(tail)
+        pins.append(p)
+        ms.append(m)
+    off = np.zeros(len(streams) + 1, np.int64)
+    np.cumsum([x.size for x in streams], out=off[1:])
+    poff = np.zeros(len(streams) + 1, np.int64)
+    np.cumsum([len(p) for p in pins], out=poff[1:])
+    return (np.concatenate(streams), off, poff, np.array([x for p in pins for x in p], np.int64),
+            np.array(ms, np.int64))
+
+
+def run_config5(args):
+    """BASELINE.json configs[4]: agent sessions partitioned s mod G over the GPUs
+    (64 per GPU: 512 at 8 GPUs, weak scaling), the chunk store sharded by
+    fingerprint prefix with the NCCL all-to-all lookup and peer replica fetch
+    (shard.py) captured in the two-wave CUDA graphs. A step = one wave of 16
+    session turns per GPU (~18.6K tokens each). Turn 0 of every session (cold:
+    inserts the contexts) runs untimed; warm-up and timed waves are later turns
+    (new metadata, contexts and the shared tool document reattached)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_05696_b200 import _native as N, ops, shard
+    from paper_2605_05696_b200.chunking import canonical_marker
+    from paper_2605_05696_b200.pipeline import ReattachPipeline
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("IRM_BENCH_ONE_DEVICE") == "1":
+        local = 0
+    backend = os.environ.get("IRM_BENCH_BACKEND", "nccl")
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    os.environ.setdefault("RANK", "0")
+    os.environ.setdefault("WORLD_SIZE", "1")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    dev = torch.device("cuda", local)
+    hbm, _tf, _tfs, peak_kind = peaks()
+    sessions = args.sessions_per_gpu
+    assert sessions % C5_R == 0, "sessions per GPU must be a multiple of the wave size"
+    blocks = sessions // C5_R
+    shared = np.random.default_rng(77)
+    header = shared.integers(0, 2**32, size=C5_HEADER, dtype=np.uint64).astype(np.uint32)
+    doc = shared.integers(0, 2**32, size=C5_DOC, dtype=np.uint64).astype(np.uint32)
+    marker = np.array(canonical_marker(), np.uint32)
+    # schedule: turn-major over the blocks of R sessions; turn 0 = cold
+    n_cold = blocks
+    n_steps = args.warmup + args.steps
+    sched = [(b % blocks, 1 + b // blocks) for b in range(2 * n_steps + 1)]
+    cold = [c5_wave(rank, world, sessions, b, 0, header, doc, marker) for b in range(n_cold)]
+    warm = [c5_wave(rank, world, sessions, b, t, header, doc, marker) for b, t in sched]
+    to_dev = lambda p: tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(dev) for a in p)
+    to_pin = lambda p: tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).pin_memory()
+                             for a in p)
+    cold_dev = [to_dev(p) for p in cold]
+    warm_dev = [to_dev(p) for p in warm[:n_steps + 1]]
+    warm_host = [to_pin(p) for p in warm[n_steps + 1:]]
+    max_tok = max(int(p[1][-1]) for p in cold + warm)
+    max_pins = max(int(p[2][-1]) for p in cold + warm)
+    req_stride = max(int(np.diff(p[1]).max()) for p in cold + warm) + C5_HEADER
+
+    # pool: [0, novel) first-writer rows (one sub-range per owner), then replicas, then scratch
+    n_waves_total = n_cold + 2 * n_steps + 4
+    novel_est = sessions * C5_BODY + C5_DOC + C5_R * 80 * n_waves_total + 1024  # contexts + every turn's metadata
+    sub = (int(1.25 * novel_est / world) + 4096) if world > 1 else novel_est + 4096
+    novel_rows = sub * world
+    replica_rows = 4 * C5_DOC + 16384
+    scratch = 2 * C5_DOC + 4096
+    pool_rows = novel_rows + replica_rows + 2 * scratch
+    pool = torch.empty(LAYERS, pool_rows, CKV + KR, dtype=torch.bfloat16, device=dev)
+    for l in range(LAYERS):  # random-init latents, one layer at a time (no fp32 temporary)
+        pool[l].normal_()
+    inv = ops.inv_freq_device(np.power(THETA, -2.0 * np.arange(KR // 2) / KR))
+    store = ops.ChunkStore(max_entries=1 << 20)
+    pipe = ReattachPipeline(store, pool, inv, C5_R, max_tok, max_pins, req_stride, layout=N.LAYOUT_INTERLEAVED)
+    cache = shard.ReplicaCache(pool, novel_rows, shard.map_peer_pools(pool), rank, ops.ChunkStore(max_entries=1 << 14),
+                               scratch_rows=scratch)
+    sharded = shard.ShardedStore(store, novel_rows)
+    pipe.enable_sharding(sharded, cache, rank, world)
+
+    graphs = backend == "nccl"
+    lc0 = ops.launch_count()
+    pipe.load(*cold_dev[0])
+    pipe.step_sharded(0)  # one eager wave: our kernels per wave (the graphs replay the same launches)
+    launches_per_wave = ops.launch_count() - lc0
+    if graphs:
+        pipe.capture_overlapped(k4_sms=K4_SMS, sharded=True)
+    run_sharded(pipe, n_cold - 1, lambda i: pipe.load(*cold_dev[1 + i]), 1, graphs)
+    wave = n_cold
+    run_sharded(pipe, args.warmup, lambda i: pipe.load(*warm_dev[i]), wave, graphs)
+    wave += args.warmup
+    torch.cuda.synchronize()
+    dist.barrier()
+
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        pipe.hit_tokens.zero_()
+        t0.record()
+        run_sharded(pipe, args.steps, lambda i: pipe.load(*warm_dev[args.warmup + i]), wave, graphs)
+        t1.record()
+        torch.cuda.synchronize()
+    wave += args.steps
+    ms_total = t0.elapsed_time(t1)
+    hit_tok = int(pipe.hit_tokens.item())
+    t = torch.tensor([ms_total], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ht = torch.tensor([hit_tok], device=dev, dtype=torch.int64)
+    dist.all_reduce(ht)
+    hit_all = int(ht.item())
+    value = hit_all / (ms_total / 1e3)
+
+    # e2e: the next turns from pinned host buffers, service maps read back
+    n_e2e = min(args.steps, len(warm_host))
+    res = [torch.empty(pipe.slots[0]["hit"].shape, dtype=pipe.slots[0]["hit"].dtype, pin_memory=True)
+           for _ in range(n_e2e)]
+    pipe.hit_tokens.zero_()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    if graphs:
+        pipe.run_overlapped(n_e2e, lambda i: pipe.load(*warm_host[i]), readback=res, wave0=wave)
+    else:
+        pipe.run_overlapped_sharded(n_e2e, lambda i: pipe.load(*warm_host[i]), wave0=wave, k4_sms=K4_SMS,
+                                    after_front=lambda i, sl: res[i].copy_(pipe.slots[sl]["hit"], non_blocking=True))
+    e1.record()
+    torch.cuda.synchronize()
+    wave += n_e2e
+    e2e_ms = e0.elapsed_time(e1)
+    t = torch.tensor([e2e_ms], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ht = torch.tensor([int(pipe.hit_tokens.item())], device=dev, dtype=torch.int64)
+    dist.all_reduce(ht)
+    e2e_value = int(ht.item()) / (float(t.item()) / 1e3)
+    bi = sum(x.numel() * x.element_size() for x in warm_host[0])
+    bo = res[0].numel() * res[0].element_size() if n_e2e else 0
+    sharded.check()
+    cache.check()
+    pipe.check()
+    fetched = torch.stack([cache.fetched_runs, cache.fetched_rows]).to(torch.int64)
+    dist.all_reduce(fetched)
+    fetched = fetched.tolist()
+
+    parity = {"checked": False, "why": "N > 1: the global oracle needs every rank's waves"}
+    if world == 1:
+        check = c5_wave(rank, world, sessions, 0, 10_000, header, doc, marker)
+        served = cold + warm[:n_steps] + warm[n_steps + 1:n_steps + 1 + n_e2e]
+        parity = pipeline_parity(pipe, served, check, to_dev(check), True, True, graphs, pool, req_stride, wave0=wave)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"config 5: {sessions * world} agent sessions ({sessions} per GPU, s mod G), "
+                               f"27 layers, DSv2 interleaved theta 1e4, ~{C5_BODY // 1024 + 2}K-token turns",
+                   "sessions": sessions * world, "sessions_per_gpu": sessions, "requests_per_step": C5_R,
+                   "tokens_per_request": int(np.mean(np.diff(warm[0][1]))) + C5_HEADER, "layers": LAYERS,
+                   "l2": "inputs larger than L2 (pool of %.0f GB per GPU)" % (pool.numel() * 2 / 1e9),
+                   "pipeline": "two-wave overlap, K4 on %d SMs; sharded lookup (%s all-to-alls%s) + peer replica fetch"
+                               % (K4_SMS, backend, " captured in the CUDA graphs" if graphs else ", streams"),
+                   "parallelism": f"sessions s mod G over {world} GPU(s), store sharded by fingerprint prefix"},
+        "exchange": {"bytes_per_lookup": sharded.last_exchange_bytes, "owner_slots": sharded.owner_slots or
+                     (sharded.slots if world == 1 else min(sharded.slots, (5 * sharded.slots) // (4 * world) + 64)),
+                     "query_capacity": sharded.slots, "replica_runs_fetched_all_ranks": fetched[0],
+                     "replica_rows_fetched_all_ranks": fetched[1]},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo},
+        "parity": parity,
+        "gpu_launches": args.steps * launches_per_wave,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    dist.destroy_process_group()
 
 
 def run_sharded(pipe, n, load, wave0, graphs, after_front=None):
@@ -873,6 +1078,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-attn", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="K6 sharded-store path even at N=1")
+    ap.add_argument("--workload", default="config2", choices=["config2", "config5"],
+                    help="config2: DeepSeek-V2-Lite 8 x 32K wave (default); config5: sharded agent sessions")
+    ap.add_argument("--sessions-per-gpu", type=int, default=C5_SESSIONS_PER_GPU)
     ap.add_argument("--no-fanout", action="store_true",
                     help="K4 reads every hit's source rows (default: one read per distinct source run per wave)")
     ap.add_argument("--serial", action="store_true",
@@ -881,6 +1089,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "config5":
+        run_config5(args)
     else:
         run_ours(args)
 

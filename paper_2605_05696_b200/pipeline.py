@@ -213,8 +213,12 @@ class ReattachPipeline:
         self.hit = hit
         self.grow = grow  # novel chunks: the rows of this rank's pool that keep their KV (prefill writes them)
         is_hit = hit == 1
+        # hits on entries this very exchange created (another rank's same-wave first write) are
+        # fetched for this wave only: the writer has not produced those rows yet
         src = self.replica.localize(torch.where(is_hit, grow, torch.full_like(grow, -1)),
-                                    torch.where(is_hit, t.length, torch.zeros_like(t.length)))
+                                    torch.where(is_hit, t.length, torch.zeros_like(t.length)),
+                                    fresh=self.sharded.fresh & is_hit,
+                                    scratch_half=self.fill_slot if self.fill_slot is not None else None)
         self._compact(src)
 
     def step_sharded(self, wave: int):

@@ -8,21 +8,28 @@ tests), with fixed-capacity buffers so nothing on the path waits for the host:
 
   1. every probed query goes to slot (owner, position in the owner's bucket)
      of a [G, cap, 4] send buffer (fp, order key, p, len); unused
-     slots carry padding order keys that sort after every real key
+     slots carry padding order keys that sort after every real key. ``cap``
+     is a per-owner bound (fingerprints are uniform, so an owner receives
+     ~1/G of a wave: 1.25/G of the wave's capacity + 64 slots); a bucket that
+     would overflow sets a sticky flag that ``check()`` raises on
   2. all-to-all of equal splits
   3. the owner sorts what it received by the global order key (request,
      chunk) and runs the first-writer-wins batch on its shard (K3), so the
      winner is the globally earliest query, exactly as the sequential
      reference (engine.py:197-223); a new entry's rows are allocated by the
      owner in its sub-range of the first writer's pool
-  4. reverse all-to-all of (hit, p_src, row) into the same slots
+  4. reverse all-to-all of (hit, p_src, row, fresh) into the same slots;
+     fresh = the entry was created by this very exchange (its KV is written
+     by the first writer's prefill of this wave, not yet)
 
 Rows are named globally: ``row = rank << 40 | local_row``. A hit whose rows
 live on another rank is fetched once into this rank's replica region of its
 pool (``ReplicaCache``): the peer pools are mapped into every process (CUDA
 IPC over NVLink), a second store keyed by the global row dedupes runs and
 assigns replica rows, and ``irm_copy_runs`` pulls the rows peer-to-peer. K4
-then always reads local HBM.
+then always reads local HBM. A hit on an entry created in the same exchange
+(``fresh``) is fetched into a per-wave scratch region and never cached: the
+writer has not produced those rows yet, so a cached copy would stay stale.
 """
 
 from __future__ import annotations
@@ -56,18 +63,22 @@ class ShardedStore:
     the same ``lookup_insert`` contract and an ``e_row`` entry array, e.g. a
     test dict store on CPU)."""
 
-    def __init__(self, local_store, novel_rows: int, group=None, slots: int | None = None):
+    def __init__(self, local_store, novel_rows: int, group=None, slots: int | None = None,
+                 owner_slots: int | None = None):
         """novel_rows: rows [0, novel_rows) of every rank's latent pool hold the
         KV of chunks that rank writes first. Owner o hands out rows of the
         sub-range [o * novel_rows // G, (o + 1) * novel_rows // G) of each
         writer's pool, with one bump counter per writer, so a first writer's
         rows are known in the same exchange that decides it is first.
-        slots: queries per (rank, owner) bucket of the exchange; it must be the
-        same on every rank (the all-to-all has equal splits). None: the size of
-        each call's query array, which then must match across ranks."""
+        slots: the most queries one call may carry; it must be the same on every
+        rank (the all-to-all has equal splits). None: the size of each call's
+        query array, which then must match across ranks. owner_slots: queries
+        per (rank, owner) bucket (default: 1.25 x slots / G + 64, at most slots);
+        an overflowing bucket raises in ``check()``."""
         self.local = local_store
         self.group = group
         self.slots = slots
+        self.owner_slots = owner_slots
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         e_row = local_store.e_row
@@ -78,7 +89,9 @@ class ShardedStore:
         self.base = self.rank * self.region
         self.next = torch.zeros(self.world, dtype=torch.int64, device=dev)  # per-writer bump counters
         self.overflow = torch.zeros((), dtype=torch.bool, device=dev)
+        self.bucket_overflow = torch.zeros((), dtype=torch.bool, device=dev)
         self.last_exchange_bytes = 0
+        self.fresh = None  # per query of the last call: hit on an entry this exchange created
 
     def lookup_insert(self, q_fp, q_order, q_p, q_len, q_probe=None):
         """Same contract as ops.ChunkStore.lookup_insert, over the sharded store.
@@ -93,16 +106,19 @@ class ShardedStore:
         n, G = q_fp.numel(), self.world
         i64 = dict(dtype=torch.int64, device=dev)
         probe = torch.ones(n, dtype=torch.bool, device=dev) if q_probe is None else q_probe.to(torch.bool)
-        cap = self.slots if self.slots is not None else max(n, 1)
-        if n > cap:
-            raise ValueError(f"{n} queries exceed the exchange's {cap} slots per owner")
+        total = self.slots if self.slots is not None else max(n, 1)
+        if n > total:
+            raise ValueError(f"{n} queries exceed the exchange's {total} slots")
+        cap = self.owner_slots or (total if G == 1 else min(total, (5 * total) // (4 * G) + 64))
         own = torch.where(probe, owner_of(q_fp, G), torch.full_like(q_fp, G))  # bucket G: not probed
         perm = torch.argsort(own, stable=True)
         own_s = own[perm]
         counts = torch.zeros(G + 1, **i64).scatter_add_(0, own, torch.ones(n, **i64))
         start = torch.cumsum(counts, 0) - counts
-        valid = own_s < G
-        dest = torch.where(valid, own_s * cap + torch.arange(n, **i64) - start[own_s], G * cap)
+        pos = torch.arange(n, **i64) - start[own_s]
+        self.bucket_overflow |= (counts[:G] > cap).any()  # sticky; check() raises
+        valid = (own_s < G) & (pos < cap)
+        dest = torch.where(valid, own_s * cap + pos, G * cap)
         send = torch.zeros(G * cap + 1, 4, **i64)  # last row: sink for unprobed queries
         send[:, 1] = PAD_ORDER + self.rank * G * cap + torch.arange(G * cap + 1, **i64)  # unique padding keys
         send.index_copy_(0, dest, torch.stack([q_fp, q_order, q_p.to(torch.int64), q_len.to(torch.int64)],
@@ -115,6 +131,7 @@ class ShardedStore:
         o = torch.argsort(recv[:, 1])
         r = recv[o]
         real = r[:, 1] < PAD_ORDER
+        n_before = self._entry_count()  # entries of this shard before the exchange (device)
         hit, entry, p_src, _row = self.local.lookup_insert(
             r[:, 0].contiguous(), r[:, 1].contiguous(), r[:, 2].contiguous(), r[:, 3].to(torch.int32).contiguous(),
             real)
@@ -131,11 +148,12 @@ class ShardedStore:
         # each entry has exactly one novel query
         self.e_grow.index_copy_(0, torch.where(novel, entry, torch.full_like(entry, sink)), grow)
         rows = torch.where(entry >= 0, self.e_grow[entry.clamp_min(0)], torch.full_like(entry, -1))
-        reply = torch.empty(G * cap, 3, **i64)
-        reply.index_copy_(0, o, torch.stack([hit.to(torch.int64), p_src.to(torch.int64), rows], dim=1))
+        fresh = ((hit == 1) & (entry >= n_before)).to(torch.int64)
+        reply = torch.empty(G * cap, 4, **i64)
+        reply.index_copy_(0, o, torch.stack([hit.to(torch.int64), p_src.to(torch.int64), rows, fresh], dim=1))
         back = torch.empty_like(reply)
         dist.all_to_all_single(back, reply, group=self.group)
-        self.last_exchange_bytes = 2 * G * cap * (4 + 3) * 8
+        self.last_exchange_bytes = 2 * G * cap * (4 + 4) * 8
 
         res = back[torch.where(valid, dest, torch.zeros_like(dest))]  # sorted position k -> its slot
         out_hit = torch.full((n,), -1, dtype=torch.int32, device=dev)
@@ -146,12 +164,24 @@ class ShardedStore:
         out_psrc.index_copy_(0, perm, torch.where(valid, res[:, 1], 0))
         out_row.index_copy_(0, perm, torch.where(valid, res[:, 2], -1))
         out_owner.index_copy_(0, perm, torch.where(valid, own_s, -1))
+        out_fresh = torch.zeros(n, dtype=torch.bool, device=dev)
+        out_fresh.index_copy_(0, perm, valid & (res[:, 3] == 1))
+        self.fresh = out_fresh
         return out_hit, out_psrc, out_row, out_owner
 
+    def _entry_count(self) -> torch.Tensor:
+        c = getattr(self.local, "counters", None)
+        if c is not None:
+            return c[0].clone()
+        return torch.tensor(len(getattr(self.local, "map", ())), dtype=torch.int64)
+
     def check(self):
-        """Host check (call outside timed regions): every first writer got its rows."""
+        """Host check (call outside timed regions): every first writer got its rows and no
+        owner bucket of the exchange overflowed."""
         if bool(self.overflow):
             raise RuntimeError("first-writer row range of the pool is full: raise novel_rows")
+        if bool(self.bucket_overflow):
+            raise RuntimeError("an owner bucket of the lookup exchange overflowed: raise owner_slots")
 
 
 class _PeerMapping:
@@ -210,8 +240,18 @@ class ReplicaCache:
     that dedupes runs within and across waves."""
 
     def __init__(self, pool: torch.Tensor, replica_base: int, peer_pools: list[torch.Tensor], rank: int,
-                 map_store):
+                 map_store, scratch_rows: int | None = None):
+        """scratch_rows: the last 2 x scratch_rows rows of the pool are a double-buffered
+        per-wave scratch for fresh remote hits (rows their writer has not produced yet:
+        fetched for this wave, never cached; default: 1/8 of the replica region per
+        half). The replica region is [replica_base, pool rows - 2 x scratch_rows)."""
+        if scratch_rows is None:
+            scratch_rows = max(pool.shape[1] - replica_base, 0) // 8
         self.pool, self.base, self.peers, self.rank, self.map = pool, replica_base, peer_pools, rank, map_store
+        self.scratch_rows = scratch_rows
+        self.scratch_base = pool.shape[1] - 2 * scratch_rows
+        self.limit = self.scratch_base  # replica rows end here
+        self._half = 0
         for pp in peer_pools:
             assert pp.shape == pool.shape and pp.dtype == pool.dtype and pp.is_contiguous()
         dev = pool.device
@@ -222,9 +262,13 @@ class ReplicaCache:
         self.fetched_runs = torch.zeros((), dtype=torch.int64, device=dev)
         self.fetched_rows = torch.zeros((), dtype=torch.int64, device=dev)
 
-    def localize(self, grow: torch.Tensor, length: torch.Tensor) -> torch.Tensor:
+    def localize(self, grow: torch.Tensor, length: torch.Tensor, fresh: torch.Tensor | None = None,
+                 scratch_half: int | None = None) -> torch.Tensor:
         """grow [n] global rows (or -1), length [n] -> local rows (int64).
-        Missing remote runs are fetched peer-to-peer first (stream-ordered)."""
+        Missing remote runs are fetched peer-to-peer first (stream-ordered).
+        ``fresh`` [n] (bool, optional): remote hits whose entry was created in this
+        wave -- fetched into scratch half ``scratch_half`` (default: alternating per
+        call; the two-wave pipeline passes its slot) and NOT cached."""
         dev = grow.device
         n = grow.numel()
         i64 = dict(dtype=torch.int64, device=dev)
@@ -232,13 +276,36 @@ class ReplicaCache:
         ln = length.to(torch.int64)
         src_rank = gt >> ROW_SHIFT
         remote = (gt >= 0) & (src_rank != self.rank)
+        fresh_remote = remote & fresh if fresh is not None else torch.zeros_like(remote)
+        cached = remote & ~fresh_remote
         hit, _e, _p, row = self.map.lookup_insert(gt.contiguous(), torch.arange(n, **i64), torch.zeros(n, **i64),
-                                                  ln.to(torch.int32).contiguous(), remote)
+                                                  ln.to(torch.int32).contiguous(), cached)
         local = self.base + row
-        fits = local + ln <= self.pool.shape[1]
-        new = remote & (hit == 0)
+        fits = local + ln <= self.limit
+        new = cached & (hit == 0)
         self.overflow |= (new & ~fits).any()
         fetch = new & fits
+        if fresh is not None:
+            half = self._half if scratch_half is None else scratch_half
+            if scratch_half is None:
+                self._half ^= 1
+            # one scratch copy per distinct fresh run of the wave (fixed-size sort, no host sync)
+            big = torch.iinfo(torch.int64).max
+            sk, sp = torch.sort(torch.where(fresh_remote, gt, torch.full_like(gt, big)))
+            first = torch.ones_like(fresh_remote)
+            first[1:] = sk[1:] != sk[:-1]
+            first &= sk != big
+            sl = ln[sp] * first
+            off = torch.cumsum(sl, 0) - sl
+            head = torch.cummax(torch.where(first, torch.arange(n, **i64), torch.zeros_like(sp)), 0).values
+            srow = torch.empty_like(gt)
+            srow[sp] = self.scratch_base + half * self.scratch_rows + off[head]
+            lead = torch.zeros_like(fresh_remote)
+            lead[sp] = first
+            sfits = srow + ln <= self.scratch_base + (half + 1) * self.scratch_rows
+            self.overflow |= (fresh_remote & ~sfits).any()
+            local = torch.where(fresh_remote, srow, local)
+            fetch = fetch | (lead & sfits)
         perm = torch.argsort((~fetch).to(torch.int8), stable=True)  # runs to fetch first
         n_fetch = fetch.sum().reshape(1)
         self.fetched_runs += n_fetch[0]

@@ -100,7 +100,9 @@ def _worker(rank, WORLD, port, out_q):
         ref = global_oracle(all_waves, novel_rows, WORLD)
         waves = all_waves[rank]
         gen = torch.Generator(device="cuda").manual_seed(3 + rank)
-        pool = torch.randn(LAYERS, novel_rows + 8192, 576, device="cuda", generator=gen).to(torch.bfloat16)
+        # replica region 8192 rows + a 2 x 6000-row scratch: the cold wave's body is fresh for every
+        # rank but its first writer (same exchange), so it is fetched into scratch, uncached
+        pool = torch.randn(LAYERS, novel_rows + 8192 + 12000, 576, device="cuda", generator=gen).to(torch.bfloat16)
         peers = shard.map_peer_pools(pool)
         inv = O.make_inv_freq(1e4)
         max_tok = max(int(w[1][-1]) for ws in all_waves for w in ws)
@@ -110,7 +112,8 @@ def _worker(rank, WORLD, port, out_q):
         pipe = ReattachPipeline(store, pool, ops.inv_freq_device(inv), R, max_tok, max_pins, req_stride,
                                 layout=N.LAYOUT_INTERLEAVED)
         pipe.enable_sharding(shard.ShardedStore(store, novel_rows),
-                             shard.ReplicaCache(pool, novel_rows, peers, rank, ops.ChunkStore(1 << 10)),
+                             shard.ReplicaCache(pool, novel_rows, peers, rank, ops.ChunkStore(1 << 10),
+                                                scratch_rows=6000),
                              rank, WORLD)
         dev = [to_dev(w) for w in waves]
         pipe.load(*dev[0])

@@ -177,3 +177,59 @@ def test_sharded_store_uneven_batches():
         eh, _, eps, _ = ref.lookup_insert(torch.tensor([f]), torch.tensor([o]), torch.tensor([i + 1000 * r]),
                                           torch.tensor([4], dtype=torch.int32))
         assert (h, ps) == (int(eh[0]), int(eps[0]))
+
+
+def _worker_fresh(rank, port, out_q, pools):
+    """Rank 0 writes fp X first; rank 1 hits X in the SAME exchange (fresh: the
+    writer has not produced the rows yet) and again one wave later."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    from dict_store import DictStore
+
+    try:
+        store = shard.ShardedStore(DictStore(), novel_rows=32)
+        cache = shard.ReplicaCache(pools[rank], 32, pools, rank, DictStore(), scratch_rows=8)
+        fp = torch.tensor([0x1234567], dtype=torch.int64)
+        ln = torch.tensor([3], dtype=torch.int32)
+        seen = []
+        for wave in range(2):
+            order = torch.tensor([(wave * 2 + rank)], dtype=torch.int64)  # rank 0 first in each wave
+            h, ps, row, own = store.lookup_insert(fp, order, torch.tensor([100 + rank]), ln)
+            fresh = store.fresh
+            local = cache.localize(torch.where(h == 1, row, torch.full_like(row, -1)),
+                                   torch.where(h == 1, ln, torch.zeros_like(ln)), fresh=fresh & (h == 1))
+            seen.append((int(h[0]), bool(fresh[0]), int(local[0]), len(cache.map.map)))
+        cache.check()
+        store.check()
+        out_q.put((rank, seen))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fresh_remote_hits_are_not_cached():
+    """a same-exchange hit on another rank's first write is fetched into
+    the per-wave scratch and never published in the replica map; one wave later
+    (the writer's rows produced) it is fetched once and cached."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    pools = []
+    for r in range(WORLD):
+        pool = torch.zeros(1, 64, 3)
+        pool[:, :, 0] = r
+        pools.append(pool.share_memory_())
+    procs = [ctx.Process(target=_worker_fresh, args=(r, port, q, pools)) for r in range(WORLD)]
+    for pr in procs:
+        pr.start()
+    outs = dict(q.get(timeout=240) for _ in range(WORLD))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    (h0, f0, _, n0), (h0b, f0b, _, n0b) = outs[0]
+    assert (h0, f0, n0) == (0, False, 0) and (h0b, f0b, n0b) == (1, False, 0)  # the writer never fetches
+    (h1, f1, l1, n1), (h1b, f1b, l1b, n1b) = outs[1]
+    assert (h1, f1, n1) == (1, True, 0), outs[1]  # same exchange: fresh, scratch, not cached
+    assert l1 >= 64 - 2 * 8  # a scratch row
+    assert (h1b, f1b, n1b) == (1, False, 1) and 32 <= l1b < 64 - 2 * 8  # next wave: cached replica row
+    assert bool((pools[1][0, l1b:l1b + 3, 0] == 0).all())  # rank 0's rows
