@@ -149,6 +149,18 @@ int irm_prefix_match_insert(const irm_prefix_view *ix, const uint32_t *tok, cons
                             const int64_t *wit_off, const int64_t *wit_len, int64_t *m, int64_t *wit,
                             void *ws, int64_t ws_bytes, irm_stream_t stream);
 
+/* Graph-capturable wave form of phase 1 (engine.py:170, 228): append the n_seq
+ * sequences tok[seq_off[r], seq_off[r+1]) to the token arena at *arena_used,
+ * record wit_off / wit_len for epochs *epoch_next + r, write those epochs to
+ * op_epoch (for irm_prefix_match_insert with every op inserting and querying),
+ * then advance *arena_used and *epoch_next -- all on the device. A wave that
+ * would overflow the arena (arena_cap tokens) or the epoch arrays (wit_cap) is
+ * not appended: op_epoch = -1 (nothing matched or inserted) and flag 1. */
+int irm_prefix_wave_prepare(const irm_prefix_view *ix, uint32_t *arena, int64_t arena_cap, int64_t *arena_used,
+                            int64_t *wit_off, int64_t *wit_len, int64_t wit_cap, int64_t *epoch_next,
+                            const uint32_t *tok, const int64_t *seq_off, int32_t n_seq, int64_t *op_epoch,
+                            irm_stream_t stream);
+
 /* ---- K3: content-hash chunk store (registry.py:113-140) ----------------
  * Open-addressing table fingerprint -> entry, plus entry arrays, all caller
  * owned. Initialise with irm_store_reset(). First writer wins by the
@@ -202,6 +214,17 @@ int irm_store_lookup(const irm_store_view *st, const uint64_t *q_fp, int64_t n, 
  * else 0, and adds the hit tokens to *hit_tokens (if not null). A hit whose
  * rows [p_abs, p_abs + len) leave [0, req_stride) is not listed (it would
  * write into the next request's rows) and sets bit 4 of *status (nullable). */
+/* Phase 1 -> phase 2 glue (engine.py:170-179): with m[r] the prefix match of
+ * request r = tok[off[r], off[r+1]), packs the tails tok[off[r] + m[r], off[r+1])
+ * into `tail` (CSR tail_off[n_req+1]; cap = the token capacity of tok) and
+ * rebases the request's marker spans (span_off[n_req+1], spans[2k], [2k+1] =
+ * request-relative [start, end), ascending) into tail-relative pins (pin_off = 2 span_off):
+ * spans with end - 1 >= m only, as (max(start - m, 0), end - m), each pinning
+ * start - 1 (if > 0) and end - 1 (marker_pin_offsets, chunking.py:149-161);
+ * dropped pins are -1 (ignored by K1). */
+int irm_wave_rebase(const uint32_t *tok, const int64_t *off, const int64_t *m, int32_t n_req, int64_t cap,
+                    const int64_t *span_off, const int64_t *spans, uint32_t *tail, int64_t *tail_off,
+                    int64_t *pin_off, int64_t *pins, irm_stream_t stream);
 int irm_wave_plan(const int64_t *chunk_off, int32_t n_req, const int32_t *start, const int64_t *meta_len,
                   int64_t cap, int64_t carve, int64_t order0, int64_t *req, int64_t *p_abs, uint8_t *probe,
                   int64_t *order, irm_stream_t stream);

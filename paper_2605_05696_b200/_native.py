@@ -57,6 +57,8 @@ _SIGS = {
     "irm_store_workspace_bytes": ([i64], i64),
     "irm_store_lookup_insert": ([ctypes.POINTER(StoreView), P, P, P, P, P, i64, P, P, P, P, P, i64, P], i32),
     "irm_store_lookup": ([ctypes.POINTER(StoreView), P, i64, P, P], i32),
+    "irm_wave_rebase": ([P, P, P, i32, i64, P, P, P, P, P, P, P], i32),
+    "irm_prefix_wave_prepare": ([ctypes.POINTER(PrefixView), P, i64, P, P, P, i64, P, P, P, i32, P, P], i32),
     "irm_wave_plan": ([P, i32, P, P, i64, i64, i64, P, P, P, P, P], i32),
     "irm_wave_compact": ([P, P, P, P, P, P, i64, i64, P, P, P, P, P, P, P, P, P], i32),
     "irm_rotate_gather_workspace_bytes": ([i64, i32], i64),

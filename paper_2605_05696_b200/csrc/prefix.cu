@@ -236,8 +236,8 @@ __global__ void __launch_bounds__(PT) keys_kernel(irm_prefix_view ix, const uint
     uint32_t t[TPT];
     Aff a = thread_aff(tok, s0, len, j, t, base), tot;
     Aff h = compose(carry[blockIdx.x], block_scan_aff(a, &tot));  // maps H(empty) = 0 to H before my tokens
-    const bool ins = op_insert && op_insert[seq];
     const int64_t ep = op_epoch[seq];
+    const bool ins = op_insert && op_insert[seq] && ep >= 0;  // epoch -1: a wave that did not fit
     const int64_t d0 = j * CH + (int64_t)threadIdx.x * TPT;
     uint64_t H = h.b;  // hash of the prefix before my first token (applied to x = 0)
 #pragma unroll
@@ -328,6 +328,43 @@ __global__ void verify_kernel(irm_prefix_view ix, const uint32_t *__restrict__ t
     }
 }
 
+// Graph-capturable wave form (the serve pipeline's phase 1): append the wave's
+// sequences to the token arena at the device-side fill level, give sequence r
+// the insert epoch epoch_next + r, then bump both counters. No host involvement.
+__global__ void wave_arena_kernel(uint32_t *__restrict__ arena, int64_t arena_cap,
+                                  const int64_t *__restrict__ arena_used, int64_t *__restrict__ wit_off,
+                                  int64_t *__restrict__ wit_len, int64_t wit_cap,
+                                  const int64_t *__restrict__ epoch_next, const uint32_t *__restrict__ tok,
+                                  const int64_t *__restrict__ seq_off, int32_t n_seq, int64_t *__restrict__ op_epoch,
+                                  int64_t *__restrict__ counters) {
+    const int64_t used = *arena_used, e0 = *epoch_next;
+    const int64_t n_tok = seq_off[n_seq] - seq_off[0];
+    const bool fits = used + n_tok <= arena_cap && e0 + n_seq <= wit_cap;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (!fits) {
+        if (g == 0) atomicOr((unsigned long long *)&counters[1], (unsigned long long)ERR_TABLE_FULL);
+        for (int64_t r = g; r < n_seq; r += stride) op_epoch[r] = -1;  // nothing inserted or matched
+        return;
+    }
+    for (int64_t r = g; r < n_seq; r += stride) {
+        op_epoch[r] = e0 + r;
+        wit_off[e0 + r] = used + seq_off[r] - seq_off[0];
+        wit_len[e0 + r] = seq_off[r + 1] - seq_off[r];
+    }
+    for (int64_t i = g; i < n_tok; i += stride) arena[used + i] = tok[seq_off[0] + i];
+}
+
+__global__ void wave_bump_kernel(int64_t arena_cap, int64_t *__restrict__ arena_used, int64_t wit_cap,
+                                 int64_t *__restrict__ epoch_next, const int64_t *__restrict__ seq_off,
+                                 int32_t n_seq) {
+    const int64_t n_tok = seq_off[n_seq] - seq_off[0];
+    if (*arena_used + n_tok <= arena_cap && *epoch_next + n_seq <= wit_cap) {
+        *arena_used += n_tok;
+        *epoch_next += n_seq;
+    }
+}
+
 }  // namespace prefix
 }  // namespace irm
 
@@ -402,6 +439,25 @@ extern "C" int irm_prefix_match_insert(const irm_prefix_view *ix, const uint32_t
     IRM_LAUNCH_CHECK();
     prefix::verify_kernel<<<n_seq, 256, 0, s>>>(*ix, tok, seq_off, n_seq, op_epoch, op_query, arena, wit_off, wit_len,
                                                  m, wit);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
+
+extern "C" int irm_prefix_wave_prepare(const irm_prefix_view *ix, uint32_t *arena, int64_t arena_cap,
+                                       int64_t *arena_used, int64_t *wit_off, int64_t *wit_len, int64_t wit_cap,
+                                       int64_t *epoch_next, const uint32_t *tok, const int64_t *seq_off,
+                                       int32_t n_seq, int64_t *op_epoch, irm_stream_t stream) {
+    IRM_REQUIRE(ix && ix->counters, "null index");
+    IRM_REQUIRE(n_seq >= 0 && arena_cap >= 0 && wit_cap >= 0, "bad sizes");
+    if (n_seq == 0) return IRM_OK;
+    IRM_REQUIRE(arena && arena_used && wit_off && wit_len && epoch_next && tok && seq_off && op_epoch,
+                "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int grid = irm::sm_count() * 4;
+    prefix::wave_arena_kernel<<<grid, 256, 0, s>>>(arena, arena_cap, arena_used, wit_off, wit_len, wit_cap,
+                                                    epoch_next, tok, seq_off, n_seq, op_epoch, ix->counters);
+    IRM_LAUNCH_CHECK();
+    prefix::wave_bump_kernel<<<1, 1, 0, s>>>(arena_cap, arena_used, wit_cap, epoch_next, seq_off, n_seq);
     IRM_LAUNCH_CHECK();
     return IRM_OK;
 }

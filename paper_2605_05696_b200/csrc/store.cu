@@ -372,7 +372,76 @@ wave_compact_kernel(const int32_t *__restrict__ hit, const int64_t *__restrict__
     }
 }
 
+// Phase 1 -> phase 2 on the device (engine.py:170-179): request r's tail is
+// tok[off[r] + m[r], off[r+1]) where m[r] is the K0 prefix match; the tails are
+// packed into one CSR stream set for K1, and the request's marker spans
+// (request-relative [s, e)) become tail-relative pins: spans with e - 1 >= m only, rebased to
+// (max(s - m, 0), e - m), each pinning start - 1 (if > 0) and end - 1
+// (chunking.py:149-161); a dropped pin is -1, which K1 ignores.
+__global__ void __launch_bounds__(WC_BLOCK)
+wave_rebase_plan_kernel(const int64_t *__restrict__ off, const int64_t *__restrict__ m, int32_t n_req,
+                        const int64_t *__restrict__ span_off, const int64_t *__restrict__ spans,
+                        int64_t *__restrict__ tail_off, int64_t *__restrict__ pin_off, int64_t *__restrict__ pins) {
+    __shared__ int64_t sm[WC_BLOCK / 32];
+    int64_t base = 0;
+    for (int32_t r0 = 0; r0 < n_req; r0 += WC_BLOCK) {
+        const int32_t r = r0 + threadIdx.x;
+        const int64_t len = r < n_req ? max(off[r + 1] - off[r] - m[r], (int64_t)0) : 0;
+        int64_t tot;
+        const int64_t ex = block_exclusive_scan<WC_BLOCK>(len, &tot, sm);
+        if (r < n_req) {
+            tail_off[r] = base + ex;
+            pin_off[r] = 2 * span_off[r];
+            const int64_t mr = m[r];
+            for (int64_t k = span_off[r]; k < span_off[r + 1]; ++k) {
+                const int64_t s = spans[2 * k], e = spans[2 * k + 1];  // request-relative [s, e)
+                const bool keep = e - 1 >= mr;
+                const int64_t rs = max(s - mr, (int64_t)0), re = e - mr;
+                pins[2 * k] = keep && rs > 0 ? rs - 1 : -1;
+                pins[2 * k + 1] = keep ? re - 1 : -1;
+            }
+        }
+        base += tot;
+    }
+    if (threadIdx.x == 0) {
+        tail_off[n_req] = base;
+        pin_off[n_req] = 2 * span_off[n_req];
+    }
+}
+
+__global__ void wave_rebase_copy_kernel(const uint32_t *__restrict__ tok, const int64_t *__restrict__ off,
+                                        const int64_t *__restrict__ m, int32_t n_req, int64_t cap,
+                                        const int64_t *__restrict__ tail_off, uint32_t *__restrict__ tail) {
+    const int64_t total = off[n_req];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < min(total, cap);
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = n_req - 1;  // the request holding token i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(off + mid) <= i) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t j = i - off[lo] - m[lo];
+        if (j >= 0) tail[tail_off[lo] + j] = tok[i];
+    }
+}
+
 }  // namespace irm
+
+extern "C" int irm_wave_rebase(const uint32_t *tok, const int64_t *off, const int64_t *m, int32_t n_req, int64_t cap,
+                               const int64_t *span_off, const int64_t *spans, uint32_t *tail, int64_t *tail_off,
+                               int64_t *pin_off, int64_t *pins, irm_stream_t stream) {
+    IRM_REQUIRE(n_req >= 1 && cap >= 0, "bad sizes");
+    IRM_REQUIRE(tok && off && m && span_off && tail && tail_off && pin_off, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    irm::wave_rebase_plan_kernel<<<1, irm::WC_BLOCK, 0, s>>>(off, m, n_req, span_off, spans, tail_off, pin_off, pins);
+    IRM_LAUNCH_CHECK();
+    const int64_t grid = std::min<int64_t>((cap + 255) / 256, (int64_t)irm::sm_count() * 8);
+    irm::wave_rebase_copy_kernel<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, s>>>(tok, off, m, n_req, cap, tail_off,
+                                                                                      tail);
+    IRM_LAUNCH_CHECK();
+    return IRM_OK;
+}
 
 extern "C" int irm_wave_plan(const int64_t *chunk_off, int32_t n_req, const int32_t *start,
                              const int64_t *meta_len, int64_t cap, int64_t carve, int64_t order0, int64_t *req,

@@ -428,6 +428,23 @@ def wave_plan(chunk_off: torch.Tensor, n_req: int, start: torch.Tensor, meta_len
                                   N.stream_ptr()), "irm_wave_plan")
 
 
+def wave_rebase(tok: torch.Tensor, off: torch.Tensor, m: torch.Tensor, n_req: int, span_off: torch.Tensor,
+                spans: torch.Tensor, tail: torch.Tensor, tail_off: torch.Tensor, pin_off: torch.Tensor,
+                pins: torch.Tensor) -> None:
+    """irm_wave_rebase: pack the tails tok[off[r] + m[r], off[r+1]) into ``tail``
+    (CSR ``tail_off``) and rebase the requests' marker spans (request-relative
+    [start, end) pairs, CSR ``span_off``) into tail-relative pins."""
+    _expect([(tok, torch.int32), (off, torch.int64), (m, torch.int64), (span_off, torch.int64),
+             (spans, torch.int64), (tail, torch.int32), (tail_off, torch.int64), (pin_off, torch.int64),
+             (pins, torch.int64)], "wave_rebase")
+    if tail.numel() < tok.numel() or tail_off.numel() < n_req + 1 or pin_off.numel() < n_req + 1 \
+            or pins.numel() < spans.numel():
+        raise ValueError("wave_rebase: output buffers too small")
+    N.check(N.lib().irm_wave_rebase(N.ptr(tok), N.ptr(off), N.ptr(m), int(n_req), tok.numel(), N.ptr(span_off),
+                                    N.ptr(spans), N.ptr(tail), N.ptr(tail_off), N.ptr(pin_off), N.ptr(pins),
+                                    N.stream_ptr()), "irm_wave_rebase")
+
+
 def wave_compact(hit: torch.Tensor, row: torch.Tensor, req: torch.Tensor, p_abs: torch.Tensor, p_src: torch.Tensor,
                  length: torch.Tensor, req_stride: int, src_out: torch.Tensor, dst_out: torch.Tensor,
                  len_out: torch.Tensor, delta_out: torch.Tensor, n_hit: torch.Tensor, length_out: torch.Tensor,

@@ -46,8 +46,15 @@ class ReattachPipeline:
                  max_requests: int, max_tokens: int, max_pins: int, req_stride: int,
                  layout: int = N.LAYOUT_INTERLEAVED, mask_exponent: int = 7, min_size: int = 32,
                  max_size: int = 512, carve: int = 32, ckv_dim: int = 512, kr_dim: int = 64,
-                 fanout: bool = True):
+                 fanout: bool = True, prefix_index=None, max_spans: int = 0):
+        """prefix_index (radix.WavePrefixIndex): phase 1 runs on the device inside the
+        step -- waves are then loaded as WHOLE requests with their marker spans
+        (``load_requests``); K0 matches each request against every earlier one,
+        ``irm_wave_rebase`` packs the tails and rebases the pins, then K1 / K3 / K4
+        as before. Without it, waves are loaded as tails with a host-known m
+        (``load``). max_spans: marker spans per wave (prefix mode)."""
         dev = pool.device
+        self.prefix_index = prefix_index
         self.fanout = fanout
         self.k4_sms = 0  # SMs K4 spreads over (0 = all); per launch, captured with it
         self.status = torch.zeros(1, dtype=torch.int64, device=dev)  # sticky K4 / compaction bound flags
@@ -62,6 +69,13 @@ class ReattachPipeline:
                             pin_off=torch.zeros(max_requests + 1, dtype=torch.int64, device=dev),
                             pins=torch.zeros(max(max_pins, 1), dtype=torch.int64, device=dev),
                             m=torch.zeros(max_requests, dtype=torch.int64, device=dev)) for _ in range(2)]
+        if prefix_index is not None:  # whole requests + request-relative marker spans, per input set
+            assert max_pins >= 2 * max_spans, "two pins per marker span"
+            for ins in self.inputs:
+                ins.update(full_tok=torch.zeros(max_tokens, dtype=torch.int32, device=dev),
+                           full_off=torch.zeros(max_requests + 1, dtype=torch.int64, device=dev),
+                           span_off=torch.zeros(max_requests + 1, dtype=torch.int64, device=dev),
+                           spans=torch.zeros(max(2 * max_spans, 2), dtype=torch.int64, device=dev))
         self.cur_in = 0  # the input set K1 / K3 read and load() writes
         # static outputs: per-request KV and the chunk service table
         self.out = torch.empty(pool.shape[0], max_requests * req_stride, pool.shape[2], dtype=pool.dtype,
@@ -92,6 +106,16 @@ class ReattachPipeline:
     m = property(lambda self: self.inputs[self.cur_in]["m"])
 
     # ------------------------------------------------------------ device step
+    def k0(self):
+        """Phase 1 on the device: m of every request of the wave (K0), then the
+        tails and their pins for K1 (irm_wave_rebase). No-op without a prefix index."""
+        if self.prefix_index is None:
+            return
+        ins = self.inputs[self.cur_in]
+        self.prefix_index.match_insert_wave(ins["full_tok"], ins["full_off"], self.R, ins["m"])
+        ops.wave_rebase(ins["full_tok"], ins["full_off"], ins["m"], self.R, ins["span_off"], ins["spans"],
+                        ins["tok"], ins["stream_off"], ins["pin_off"], ins["pins"])
+
     def k1(self):
         k, mn, mx = self.params
         self.table = ops.cdc_xxh64(self.tok, self.stream_off, self.pin_off, self.pins, k, mn, mx, True,
@@ -167,11 +191,15 @@ class ReattachPipeline:
 
     def check(self):
         """Host check (outside timed regions): no K4 / compaction bound was hit and
-        the store did not overflow (raises ValueError / RuntimeError)."""
+        the store (and the prefix index) did not overflow (raises ValueError /
+        RuntimeError)."""
         ops.check_status(self.status, "reattach pipeline")
         self.store.counts()
+        if self.prefix_index is not None:
+            self.prefix_index.check()
 
     def step_eager(self):
+        self.k0()
         self.k1()
         self.k3()
         self.k4()
@@ -222,6 +250,7 @@ class ReattachPipeline:
         self._compact(src)
 
     def step_sharded(self, wave: int):
+        self.k0()
         self.k1()
         self.k3_sharded(wave)
         self.k4()
@@ -241,6 +270,7 @@ class ReattachPipeline:
 
         def front(i, s):
             self.fill_slot, self.cur_in = s, s
+            self.k0()
             self.k1()
             self.k3_sharded(wave0 + i)
             self.fill_slot, self.cur_in = None, 0
@@ -274,8 +304,27 @@ class ReattachPipeline:
             self.k4_sms = 0
 
     # ------------------------------------------------------------ graphs
+    def _empty_inputs(self):
+        """Zero the CSR offsets of both input sets (every request empty) and return
+        a restore function: warm-ups before a capture then touch no store or index."""
+        keys = ("full_off", "span_off") if self.prefix_index is not None else ("stream_off", "pin_off")
+        saved = [tuple(ins[k].clone() for k in keys) for ins in self.inputs]
+        for ins in self.inputs:
+            for k in keys:
+                ins[k].zero_()
+
+        def restore():
+            torch.cuda.synchronize()
+            for ins, sv in zip(self.inputs, saved):
+                for k, v in zip(keys, sv):
+                    ins[k].copy_(v)
+            torch.cuda.synchronize()
+        return restore
+
     def capture(self, warmup: int = 2):
-        """Capture the step (and K1-, K3- and K4-only graphs for component timing)."""
+        """Capture the step (and K1-, K3- and K4-only graphs for component timing).
+        Prefix mode warms up on empty requests (re-serving a wave would match it whole)."""
+        restore = self._empty_inputs() if self.prefix_index is not None else None
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -283,6 +332,8 @@ class ReattachPipeline:
                 self.step_eager()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
+        if restore:
+            restore()
         pool = torch.cuda.graph_pool_handle()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, pool=pool):
@@ -337,6 +388,7 @@ class ReattachPipeline:
 
         def front(s):
             self.fill_slot, self.cur_in = s, s
+            self.k0()
             self.k1()
             if sharded:
                 self.k3_sharded(self.wave_t)
@@ -355,10 +407,7 @@ class ReattachPipeline:
 
         # warm up and capture over empty streams: no store side effects (nothing is
         # probed or inserted), and every shape is capacity-bounded anyway
-        saved = [(ins["stream_off"].clone(), ins["pin_off"].clone()) for ins in self.inputs]
-        for ins in self.inputs:
-            ins["stream_off"].zero_()
-            ins["pin_off"].zero_()
+        restore = self._empty_inputs()
         s0 = torch.cuda.Stream()
         s0.wait_stream(torch.cuda.current_stream())
         try:
@@ -385,11 +434,7 @@ class ReattachPipeline:
                     self.k4(s)
                 self.g_drain.append(g)
         finally:
-            torch.cuda.synchronize()
-            for ins, (so, po) in zip(self.inputs, saved):
-                ins["stream_off"].copy_(so)
-                ins["pin_off"].copy_(po)
-        torch.cuda.synchronize()
+            restore()
         self.hit_tokens.zero_()
 
     def run_overlapped(self, n_waves: int, load_wave, after_front=None, after_k4=None, wave0: int = 0,
@@ -471,6 +516,23 @@ class ReattachPipeline:
             self.pin_off[r:].copy_(self.pin_off[r - 1:r].expand(self.R + 1 - r))
         self.pins[:pins.numel()].copy_(pins, non_blocking=True)
         self.m[:m.numel()].copy_(m, non_blocking=True)
+
+    def load_requests(self, tok, off, span_off, spans):
+        """Prefix mode: copy one wave of WHOLE requests (u32 tokens as int32, CSR
+        ``off``) and their request-relative marker spans ([start, end) pairs, CSR
+        ``span_off``) into the current input set, on the current stream."""
+        assert self.prefix_index is not None, "load_requests needs a prefix index (else: load)"
+        ins = self.inputs[self.cur_in]
+        n, r = tok.numel(), off.numel()
+        if n > ins["full_tok"].numel() or spans.numel() > ins["spans"].numel() or r > self.R + 1:
+            raise ValueError("wave exceeds the pipeline's static capacity")
+        ins["full_tok"][:n].copy_(tok, non_blocking=True)
+        ins["full_off"][:r].copy_(off, non_blocking=True)
+        ins["span_off"][:r].copy_(span_off, non_blocking=True)
+        if r < self.R + 1:  # unused request slots are empty requests
+            ins["full_off"][r:].copy_(ins["full_off"][r - 1:r].expand(self.R + 1 - r))
+            ins["span_off"][r:].copy_(ins["span_off"][r - 1:r].expand(self.R + 1 - r))
+        ins["spans"][:spans.numel()].copy_(spans, non_blocking=True)
 
     def replay(self):
         self.graph.replay()

@@ -282,3 +282,69 @@ class DeviceRadixTree:
     @property
     def n_prefixes(self) -> int:
         return int(self.counters[0])
+
+
+class WavePrefixIndex:
+    """Phase 1 of the warm-serve step as device work a CUDA graph can capture
+    (engine.py:170, 228: every request is matched against everything inserted
+    before it -- earlier waves and earlier requests of its own wave -- then
+    inserted). The K0 table, token arena and epoch arrays of DeviceRadixTree,
+    but with the arena fill level and the next insert epoch as DEVICE counters
+    (``irm_prefix_wave_prepare``), so a wave needs no host round trip. Sized
+    once; a wave that would overflow is skipped and flagged (``check()``).
+    Answers are exact (keyed hash, verified, collisions rescanned)."""
+
+    def __init__(self, max_prefixes: int, arena_tokens: int, max_sequences: int, hash_key: int | None = None):
+        import torch
+
+        from . import _native as N
+        from . import ops
+
+        self._N, self._torch = N, torch
+        dev = ops._dev()
+        self.hash_key = int.from_bytes(os.urandom(8), "little") if hash_key is None else int(hash_key)
+        n_slots = 2
+        while n_slots < 2 * max_prefixes:
+            n_slots <<= 1
+        self.counters = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.slot_key = torch.empty(n_slots, dtype=torch.int64, device=dev)
+        self.slot_epoch = torch.empty(n_slots, dtype=torch.int64, device=dev)
+        self.view = N.PrefixView(N.ptr(self.slot_key), N.ptr(self.slot_epoch), n_slots, N.ptr(self.counters),
+                                 self.hash_key & (2**64 - 1))
+        N.check(N.lib().irm_prefix_reset(self.view, N.stream_ptr()), "irm_prefix_reset")
+        self.arena = torch.zeros(arena_tokens, dtype=torch.int32, device=dev)
+        self.wit_off = torch.zeros(max_sequences, dtype=torch.int64, device=dev)
+        self.wit_len = torch.zeros(max_sequences, dtype=torch.int64, device=dev)
+        self.arena_used = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.epoch_next = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._ws = None
+        self._bufs = {}
+
+    def match_insert_wave(self, tok, seq_off, n_seq: int, m_out, wit_out=None) -> None:
+        """tok: int32 [cap] (the wave's requests, CSR ``seq_off`` [n_seq + 1], both on
+        the device); m_out int64 [n_seq] <- each request's longest prefix shared with
+        an earlier request; then every request is inserted. No host synchronisation."""
+        torch, N = self._torch, self._N
+        cap = tok.numel()
+        key = (cap, n_seq)
+        if key not in self._bufs:  # static per shape: a captured graph keeps the addresses
+            need = int(N.lib().irm_prefix_workspace_bytes(cap, n_seq))
+            self._bufs[key] = (torch.empty(max(need, 256), dtype=torch.uint8, device=tok.device),
+                               torch.empty(n_seq, dtype=torch.int64, device=tok.device),
+                               torch.ones(n_seq, dtype=torch.uint8, device=tok.device),
+                               torch.empty(n_seq, dtype=torch.int64, device=tok.device))
+        ws, op_epoch, ones, wit = self._bufs[key]
+        wit = wit if wit_out is None else wit_out
+        L = N.lib()
+        N.check(L.irm_prefix_wave_prepare(self.view, N.ptr(self.arena), self.arena.numel(), N.ptr(self.arena_used),
+                                          N.ptr(self.wit_off), N.ptr(self.wit_len), self.wit_off.numel(),
+                                          N.ptr(self.epoch_next), N.ptr(tok), N.ptr(seq_off), n_seq, N.ptr(op_epoch),
+                                          N.stream_ptr()), "irm_prefix_wave_prepare")
+        N.check(L.irm_prefix_match_insert(self.view, N.ptr(tok), N.ptr(seq_off), n_seq, cap, N.ptr(op_epoch),
+                                          N.ptr(ones), None, N.ptr(self.arena), N.ptr(self.wit_off),
+                                          N.ptr(self.wit_len), N.ptr(m_out), N.ptr(wit), N.ptr(ws), ws.numel(),
+                                          N.stream_ptr()), "irm_prefix_match_insert")
+
+    def check(self):
+        if int(self.counters[1]) & 1:
+            raise RuntimeError("wave prefix index full (table, token arena or epochs): raise its capacities")

