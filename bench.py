@@ -65,6 +65,39 @@ def ncu_traffic(kernel_prefix: str):
 
 
 # ----------------------------------------------------------------- workload
+def make_requests(rng, header, marker, body, n_req):
+    """One wave of whole agent_meta requests (workloads.py:85-100 shape): the shared
+    header, 30..70 random metadata tokens, the marker, the shared body. Returns
+    the token arrays and each request's marker span [start, end)."""
+    reqs, spans = [], []
+    for _ in range(n_req):
+        meta = rng.integers(0, 2**32, size=int(rng.integers(30, 71)), dtype=np.uint64).astype(np.uint32)
+        reqs.append(np.concatenate([header, meta, marker, body]))
+        spans.append([(HEADER + meta.size, HEADER + meta.size + marker.size)])
+    return reqs, spans
+
+
+def pack_requests(reqs, spans):
+    """-> (tokens u32, off [n+1], span_off [n+1], spans [2 x n_spans] request-relative)."""
+    off = np.zeros(len(reqs) + 1, np.int64)
+    np.cumsum([r.size for r in reqs], out=off[1:])
+    soff = np.zeros(len(reqs) + 1, np.int64)
+    np.cumsum([len(s) for s in spans], out=soff[1:])
+    flat = np.array([x for s in spans for sp in s for x in sp], np.int64)
+    return np.concatenate(reqs), off, soff, flat
+
+
+def pack_tails(wave):
+    """make_wave's (tails, pins, m) -> (tokens u32, off, pin_off, pins, m) arrays."""
+    streams, pins, ms = wave
+    off = np.zeros(len(streams) + 1, np.int64)
+    np.cumsum([x.size for x in streams], out=off[1:])
+    poff = np.zeros(len(streams) + 1, np.int64)
+    np.cumsum([len(p) for p in pins], out=poff[1:])
+    return (np.concatenate(streams), off, poff, np.array([x for p in pins for x in p], np.int64),
+            np.array(ms, np.int64))
+
+
 def make_wave(rng, header, marker, body, n_req):
     """Token streams of one wave plus the host-side phase-1 prefix length m
     (the shared header; exact-prefix matching is host radix work, §8(f))."""
@@ -162,82 +195,97 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     hbm, tf_burst, tf_sust, peak_kind = peaks()
 
-    # -------- inputs (seeded, per rank: sessions s mod G)
+    # -------- inputs (seeded, per rank: sessions s mod G). Every serve takes a FRESH wave:
+    # phase 1 runs on the device (K0) against every request served before, so a re-served
+    # wave would match whole. Serve order: cold, serial warm-up (graph path), overlapped
+    # warm-up, timed, component probe, e2e (pinned host), parity check.
     rng = np.random.default_rng(1000 + rank)
     shared = np.random.default_rng(7)
     header = shared.integers(0, 2**32, size=HEADER, dtype=np.uint64).astype(np.uint32)
     body = shared.integers(0, 2**32, size=BODY, dtype=np.uint64).astype(np.uint32)
     marker = np.array(canonical_marker(), np.uint32)
     R = args.requests
-    n_steps = args.warmup + args.steps
-    # waves[0 .. n_steps-1]: warm-up + timed; waves[n_steps]: the parity check wave (run once,
-    # after every timed region); waves[-1]: the cold request wave that stores the body
-    waves = [make_wave(rng, header, marker, body, R) for _ in range(n_steps + 2)]
+    overlapped = not args.serial
+    sharded = world > 1 or args.sharded
+    W, K = args.warmup, args.steps
+    n_serial_warm = W if not sharded else 0
+    n_ovl_warm = W if overlapped else 0
+    plan = dict(cold=1, serial_warm=n_serial_warm, ovl_warm=n_ovl_warm, timed=K, comp=1, e2e=K, check=1)
+    waves = {k: [pack_requests(*make_requests(rng, header, marker, body, R)) for _ in range(n)]
+             for k, n in plan.items()}
+    all_waves = [w for k in plan for w in waves[k]]
+    max_tok = max(int(w[1][-1]) for w in all_waves)
+    max_spans = max(int(w[2][-1]) for w in all_waves)
+    req_stride = max(int(np.diff(w[1]).max()) for w in all_waves)  # rows per request in the KV out
+    tok_per_wave = int(waves["timed"][0][1][-1]) - R * HEADER  # the tails K1 scans (m = the shared header)
+    to_dev = lambda p: tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(dev) for a in p)
+    to_pin = lambda p: tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).pin_memory()
+                             for a in p)
+    dev_in = {k: [to_dev(w) for w in waves[k]] for k in plan if k != "e2e"}
+    host_in = [to_pin(w) for w in waves["e2e"]]
+    served = []  # whole-request waves in serve order (the parity oracle replays them)
 
-    def pack(wave):
-        streams, pins, ms = wave
-        off = np.zeros(len(streams) + 1, np.int64)
-        np.cumsum([s.size for s in streams], out=off[1:])
-        poff = np.zeros(len(streams) + 1, np.int64)
-        np.cumsum([len(p) for p in pins], out=poff[1:])
-        return (np.concatenate(streams), off, poff, np.array([x for p in pins for x in p], np.int64),
-                np.array(ms, np.int64))
-
-    packed = [pack(w) for w in waves]
-    max_tail = max(int(p[1][-1]) for p in packed)
-    req_stride = max(int(np.diff(p[1]).max()) + HEADER for p in packed)  # rows per request in the KV out
-
-    # device-resident inputs (value) and pinned host copies (e2e)
-    dev_in = [tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(dev) for a in p)
-              for p in packed]
-    host_in = [tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).pin_memory() for a in p)
-               for p in packed]
-
-    # -------- store + latent pool, populated by the cold request (untimed)
+    # -------- store, prefix index + latent pool, populated by the cold request (untimed)
     from paper_2605_05696_b200.pipeline import ReattachPipeline
+    from paper_2605_05696_b200.radix import WavePrefixIndex
 
     store = ops.ChunkStore(max_entries=1 << 16)
-    sharded = world > 1 or args.sharded
-    pool_rows = BODY + 2048 * (n_steps + 3)  # body + the novel header/meta chunks of every wave
+    n_served = sum(plan.values())
+    pool_rows = BODY + HEADER + 2048 * (n_served + 2)  # body + the novel meta chunks of every wave
     if sharded:
         # rows [0, novel) hold first-writer KV (split among the G owners), [novel, pool_rows) the replicas
-        n_waves_total = 3 * n_steps + 8
-        novel_rows = 2 * (BODY + 80 * R * n_waves_total)
-        pool_rows = novel_rows + BODY + 80 * R * n_waves_total + 4096
-    pool = torch.randn(LAYERS, pool_rows, CKV + KR, device=dev).to(torch.bfloat16)  # random-init latents
+        novel_rows = 2 * (BODY + HEADER + 80 * R * (n_served + 4))
+        scratch_rows = BODY + 4096  # per half: a cold body first written by another rank in the same wave
+        pool_rows = novel_rows + BODY + 80 * R * (n_served + 4) + 4096 + 2 * scratch_rows
+    pool = torch.empty(LAYERS, pool_rows, CKV + KR, dtype=torch.bfloat16, device=dev)
+    for l in range(LAYERS):  # random-init latents, a layer at a time
+        pool[l].normal_()
     inv = ops.inv_freq_device(np.power(THETA, -2.0 * np.arange(KR // 2) / KR))
-    max_tok = max(int(p[1][-1]) for p in packed)
-    max_pins = max(int(p[2][-1]) for p in packed)
-    pipe = ReattachPipeline(store, pool, inv, R, max_tok, max_pins, req_stride, layout=N.LAYOUT_INTERLEAVED,
-                            fanout=not args.no_fanout)
+    n_tok_all = sum(int(w[1][-1]) for w in all_waves)
+    index = WavePrefixIndex(max_prefixes=n_tok_all + 4096, arena_tokens=n_tok_all + 4096,
+                            max_sequences=R * (n_served + 4) + 64)
+    pipe = ReattachPipeline(store, pool, inv, R, max_tok, 2 * max_spans, req_stride, layout=N.LAYOUT_INTERLEAVED,
+                            fanout=not args.no_fanout, prefix_index=index, max_spans=max_spans)
+
+    def load(kind, i, host=False):
+        w = host_in[i] if host else dev_in[kind][i]
+        pipe.load_requests(*w)
+        served.append(waves[kind][i])
 
     if sharded:  # K6: hash-sharded store (fixed-capacity NCCL all-to-all) + peer replica cache
         from paper_2605_05696_b200 import shard
 
         cache = shard.ReplicaCache(pool, novel_rows, shard.map_peer_pools(pool), rank,
-                                   ops.ChunkStore(max_entries=1 << 16))
+                                   ops.ChunkStore(max_entries=1 << 16), scratch_rows=scratch_rows)
         pipe.enable_sharding(shard.ShardedStore(store, novel_rows), cache, rank, world)
-        step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_sharded(i))
-    else:
-        step = lambda i, cold=False: (pipe.load(*dev_in[i]), pipe.step_eager() if cold else pipe.replay())
+    wave_no = [0]  # global wave counter of the sharded order key
+
+    def step(kind, i, cold=False):  # one wave on the serial path (eager or the serial graph)
+        load(kind, i)
+        if sharded:
+            pipe.step_sharded(wave_no[0])
+        elif cold:
+            pipe.step_eager()
+        else:
+            pipe.replay()
+        wave_no[0] += 1
+
     # cold request wave: inserts the body (its pool rows hold the random latents); the
     # library's launch counter around this eager wave = our kernels per wave (the graphs
     # replay the same launches)
     lc0 = ops.launch_count()
-    step(len(dev_in) - 1, cold=True)
+    step("cold", 0, cold=True)
     launches_per_wave = ops.launch_count() - lc0
     torch.cuda.synchronize()
-    overlapped = not args.serial
     if not sharded:
         pipe.capture()  # one CUDA graph per step (+ K1-only / K4-only graphs for component timing)
-    for i in range(args.warmup):
-        step(i)
-    if overlapped and not sharded:  # two-wave pipeline graphs (K4 on 128 SMs || K1 + K3 of the next wave)
-        pipe.capture_overlapped(k4_sms=K4_SMS)
-        pipe.run_overlapped(args.warmup, lambda i: pipe.load(*dev_in[i]))
-    # sharded: the same two-wave graphs with the NCCL all-to-alls captured inside the front
+    for i in range(n_serial_warm):
+        step("serial_warm", i)
+    # sharded: the two-wave graphs with the NCCL all-to-alls captured inside the front
     # (eager streams when the backend cannot be captured, e.g. the gloo one-device check)
     graphs = not sharded or backend == "nccl"
+    if overlapped and not sharded:  # two-wave pipeline graphs (K4 on 120 SMs || K0 + K1 + K3 of the next wave)
+        pipe.capture_overlapped(k4_sms=K4_SMS)
     if overlapped and sharded and graphs:
         try:
             pipe.capture_overlapped(k4_sms=K4_SMS, sharded=True)
@@ -253,8 +301,16 @@ def run_ours(args):
             if int(ok.item()) == 0 and graphs:
                 graphs = False
                 pipe.wave_t = None
-    if overlapped and sharded:
-        run_sharded(pipe, args.warmup, lambda i: pipe.load(*dev_in[i]), n_steps + 2, graphs)
+
+    def run_waves(kind, n, host=False, **kw):
+        if sharded:
+            run_sharded(pipe, n, lambda i: load(kind, i, host), wave_no[0], graphs, **kw)
+        else:
+            pipe.run_overlapped(n, lambda i: load(kind, i, host), **kw)
+        wave_no[0] += n
+
+    if overlapped:
+        run_waves("ovl_warm", n_ovl_warm)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -269,16 +325,12 @@ def run_ours(args):
         if overlapped:
             pipe.hit_tokens.zero_()
             t0.record()
-            if sharded:
-                run_sharded(pipe, args.steps, lambda i: pipe.load(*dev_in[args.warmup + i]), 2 * n_steps + 4,
-                            graphs)
-            else:
-                pipe.run_overlapped(args.steps, lambda i: pipe.load(*dev_in[args.warmup + i]))
+            run_waves("timed", K)
             t1.record()
         else:
             t0.record()
-            for i in range(args.steps):
-                step(args.warmup + i)
+            for i in range(K):
+                step("timed", i)
                 lens.append(pipe.length.sum())  # device-side reduction, read after the timed region
             t1.record()
         torch.cuda.synchronize()
@@ -292,8 +344,7 @@ def run_ours(args):
         dist.all_reduce(ht)
         hit_tok = int(ht.item())
     value = hit_tok / (ms_total / 1e3)  # whole-job reattached tokens/s
-    ms_step = ms_total / args.steps
-    tok_per_wave = int(packed[0][1][-1])
+    ms_step = ms_total / K
 
     # -------- per-launch K1 / K4 durations: graph replays between events (no host gaps)
     def time_graph(g, n=20):
@@ -306,7 +357,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / n
 
-    step(args.warmup)
+    step("comp", 0)  # a fresh wave through the serial path: its K1 / K3 / K4 are re-timed below
     torch.cuda.synchronize()
     k4_rows = int(pipe.length.sum().item()) * LAYERS  # reattached rows written per launch
     if pipe.fanout:  # each distinct source run is read once per launch (K4 fan-out)
@@ -333,48 +384,58 @@ def run_ours(args):
         k4 = time_graph(pipe.graph_k4)
         k3 = time_graph(pipe.graph_k3)
 
-    # -------- e2e: the same pipeline fed from pinned host buffers, result read back
+    # -------- e2e: the pipeline fed from pinned host buffers (fresh waves), results read back
     bi = sum(t.numel() * t.element_size() for t in host_in[0])
     bo = 0
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     hit_src = pipe.slots[0]["hit"] if overlapped else pipe.hit
-    res = [torch.empty(hit_src.shape, dtype=hit_src.dtype, pin_memory=True) for _ in range(args.steps)]
+    res = [torch.empty(hit_src.shape, dtype=hit_src.dtype, pin_memory=True) for _ in range(K)]
+    e_lens = []
+    if overlapped:
+        pipe.hit_tokens.zero_()
     e0.record()
     if overlapped:
         def d2h(i, slot):  # D2H of wave i's per-chunk service result
             res[i].copy_(pipe.slots[slot]["hit"], non_blocking=True)
 
         if sharded and not graphs:
-            pipe.run_overlapped_sharded(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]),
-                                        wave0=3 * n_steps + 6, k4_sms=K4_SMS, after_front=d2h)
+            run_waves("e2e", K, host=True, after_front=d2h)
         else:  # the service maps come back on a side stream (readback), off the critical path
-            pipe.run_overlapped(args.steps, lambda i: pipe.load(*host_in[args.warmup + i]), readback=res,
-                                wave0=3 * n_steps + 6)
+            run_waves("e2e", K, host=True, readback=res)
         bo = pipe.slots[0]["hit"].numel() * pipe.slots[0]["hit"].element_size()
     else:
-        for i in range(args.steps):
-            pipe.load(*host_in[args.warmup + i])  # H2D from pinned memory
-            pipe.step_sharded(args.warmup + i) if sharded else pipe.replay()
+        for i in range(K):
+            load("e2e", i, host=True)  # H2D from pinned memory
+            pipe.step_sharded(wave_no[0]) if sharded else pipe.replay()
+            wave_no[0] += 1
             res[i].copy_(pipe.hit, non_blocking=True)  # D2H of the per-chunk service result
+            e_lens.append(pipe.length.sum())
             bo = pipe.hit.numel() * pipe.hit.element_size()
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
+    e2e_tok = int(pipe.hit_tokens.item()) if overlapped else int(torch.stack(e_lens).sum().item())
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = hit_tok / (e2e_ms / 1e3)
+        ht = torch.tensor([e2e_tok], device=dev, dtype=torch.int64)
+        dist.all_reduce(ht)
+        e2e_tok = int(ht.item())
+    e2e_value = e2e_tok / (e2e_ms / 1e3)
     if sharded:  # host checks, outside the timed regions: first-writer rows and replicas all fit
         pipe.sharded.check()
         pipe.replica.check()
+    pipe.check()
     # -------- in-run parity (the checker, after every timed region): one fresh wave through the
     # production path vs the sequential oracle over every wave this run served
     parity = None
     if world == 1:
-        parity = pipeline_parity(pipe, [packed[-1]] + packed[:n_steps], packed[n_steps], dev_in[n_steps], overlapped,
-                                 sharded, graphs if sharded else True, pool, req_stride, wave0=5 * n_steps + 12)
+        parity = pipeline_parity(pipe, list(served), waves["check"][0], dev_in["check"][0], overlapped, sharded,
+                                 graphs if sharded else True, pool, req_stride, wave0=wave_no[0], prefix=True)
 
     # -------- roofline of the dominant kernel (K4) and K1
     k4_bytes = (src_rows + k4_rows) * (CKV + KR) * 2  # bf16 rows: unique source reads + destination writes
@@ -441,15 +502,44 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:  # the CPU leg: rank 0 at N = 1 only
-        line["cpu_baseline"] = cpu_baseline(args, packed[0], sample_requests=R - 1)
+        sample = pack_tails(make_wave(np.random.default_rng(1000), header, marker, body, R))
+        line["cpu_baseline"] = cpu_baseline(args, sample, sample_requests=R - 1)
     if rank == 0:
         print(json.dumps(line))
     if dist.is_initialized():
         dist.destroy_process_group()
 
 
+def whole_to_tails(waves):
+    """Whole-request waves (tokens, off, span_off, spans) in serve order -> the
+    (tails, off, pin_off, pins, m) form, with m the exact phase-1 answer of every
+    request against all earlier ones (oracle.prefix_lengths_sequential) and the
+    pins of its marker spans rebased to the tail (engine.py:170-179)."""
+    from oracle import oracle as O
+
+    reqs, spans = [], []
+    for tok, off, soff, sp in waves:
+        for r in range(off.size - 1):
+            reqs.append(tok[off[r]:off[r + 1]])
+            spans.append(sp[2 * soff[r]:2 * soff[r + 1]].reshape(-1, 2))
+    ms = O.prefix_lengths_sequential(reqs)
+    out, k = [], 0
+    for tok, off, soff, sp in waves:
+        n = off.size - 1
+        streams, pins, mm = [], [], []
+        for r in range(n):
+            m = ms[k]
+            streams.append(reqs[k][m:])
+            pins.append(sorted(O.marker_pin_offsets((max(int(a) - m, 0), int(b) - m) for a, b in spans[k]
+                                                    if int(b) - 1 >= m)))
+            mm.append(m)
+            k += 1
+        out.append(pack_tails((streams, pins, mm)))
+    return out
+
+
 def pipeline_parity(pipe, served, check_packed, check_dev, overlapped, sharded, graphs, pool, req_stride, wave0,
-                    chunks_per_request=3, theta=THETA):
+                    chunks_per_request=3, theta=THETA, prefix=False):
     """The checker for the timed path. Runs the never-served
     check wave (``check_packed`` / its device copy ``check_dev``) through the same
     production path the timed region used (overlapped graphs / serial graph /
@@ -468,7 +558,7 @@ def pipeline_parity(pipe, served, check_packed, check_dev, overlapped, sharded, 
     from oracle import oracle as O
 
     hit_map = {}
-    load = lambda i: pipe.load(*check_dev)
+    load = lambda i: pipe.load_requests(*check_dev) if prefix else pipe.load(*check_dev)
     if overlapped:
         grab = lambda i, s: hit_map.__setitem__("hit", pipe.slots[s]["hit"].clone())
         if sharded:
@@ -478,7 +568,7 @@ def pipeline_parity(pipe, served, check_packed, check_dev, overlapped, sharded, 
         torch.cuda.synchronize()
         out = pipe.slots[0]["out"]
     else:
-        pipe.load(*check_dev)
+        load(0)
         pipe.step_sharded(wave0) if sharded else pipe.replay()
         torch.cuda.synchronize()
         hit_map["hit"] = pipe.hit.clone()
@@ -488,6 +578,8 @@ def pipeline_parity(pipe, served, check_packed, check_dev, overlapped, sharded, 
     t0 = time.perf_counter()
     reg, rows_next = {}, 0
     order = list(served) + [check_packed]
+    if prefix:  # whole requests: phase 1 replayed exactly (K0 ran on the device)
+        order = whole_to_tails(order)
     for wave in order:
         tok, off, poff, pins, ms = wave
         recs = []
@@ -745,10 +837,11 @@ def run_config5(args):
     dist.destroy_process_group()
 
 
-def run_sharded(pipe, n, load, wave0, graphs, after_front=None):
+def run_sharded(pipe, n, load, wave0, graphs, after_front=None, readback=None):
     if graphs:
-        pipe.run_overlapped(n, load, after_front=after_front, wave0=wave0)
+        pipe.run_overlapped(n, load, after_front=after_front, wave0=wave0, readback=readback)
     else:
+        assert readback is None, "the stream pipeline reads service maps back in after_front"
         pipe.run_overlapped_sharded(n, load, wave0=wave0, k4_sms=K4_SMS, after_front=after_front)
 
 

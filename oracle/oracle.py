@@ -271,3 +271,36 @@ def prefix_match(inserted, seq):
         if m > best:
             best, who = m, handle
     return best, who
+
+
+def prefix_lengths_sequential(seqs, probe: int = 64):
+    """m[i] = the longest common prefix of seqs[i] with any seqs[j], j < i -- the
+    phase-1 answer of the serve loop (engine.py:170, 228; radix.py:60-83), exact
+    and fast for long sequences: an LCP below ``probe`` is found by comparing
+    every earlier sequence's first ``probe`` tokens at once; only sequences
+    sharing all ``probe`` first tokens are compared in full."""
+    seqs = [np.asarray(s, dtype=np.uint32) for s in seqs]
+    heads = np.zeros((len(seqs), probe), np.uint64)
+    hlen = np.zeros(len(seqs), np.int64)
+    groups: dict[bytes, list[int]] = {}
+    out = []
+    for i, s in enumerate(seqs):
+        h = s[:probe].astype(np.uint64)
+        m = 0
+        if i:
+            n = np.minimum(hlen[:i], h.size)
+            eq = heads[:i, :h.size] == h[None, :]
+            first_diff = np.where(eq.all(axis=1), h.size, np.argmin(eq, axis=1))
+            m = int(np.minimum(first_diff, n).max())
+            if h.size == probe:
+                for j in groups.get(h.tobytes(), []):  # candidates for an LCP of probe or more
+                    t = seqs[j]
+                    k = min(t.size, s.size)
+                    neq = np.nonzero(t[:k] != s[:k])[0]
+                    m = max(m, int(neq[0]) if neq.size else k)
+        out.append(m)
+        heads[i, :h.size] = h
+        hlen[i] = h.size
+        if h.size == probe:
+            groups.setdefault(h.tobytes(), []).append(i)
+    return out

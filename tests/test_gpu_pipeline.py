@@ -276,7 +276,10 @@ def test_pipeline_device_prefix_matches_oracle(setup, mode):
     whole = [_whole(w, header) for w in S["waves"]]
     max_tok = max(int(w[1][-1]) for w in whole)
     index = WavePrefixIndex(max_prefixes=1 << 20, arena_tokens=1 << 21, max_sequences=1 << 10)
-    pipe = ReattachPipeline(ops.ChunkStore(max_entries=1 << 12), S["pool"], ops.inv_freq_device(S["inv"]), R,
+    # the cold request stores its header chunks too here (m = 0): a pool with room for them
+    pool = torch.cat([S["pool"], torch.zeros_like(S["pool"][:, :4096])], dim=1)
+    S = dict(S, pool=pool)
+    pipe = ReattachPipeline(ops.ChunkStore(max_entries=1 << 12), pool, ops.inv_freq_device(S["inv"]), R,
                             max_tok, S["max_pins"], S["req_stride"], layout=S["N"].LAYOUT_INTERLEAVED,
                             prefix_index=index, max_spans=R)
     dev = [tuple(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).cuda() for a in w[:4])
@@ -299,13 +302,29 @@ def test_pipeline_device_prefix_matches_oracle(setup, mode):
                                                       ms.__setitem__(i, pipe.inputs[s]["m"].clone())),
                             after_k4=lambda i, s: outs.__setitem__(i, pipe.slots[s]["out"].clone()))
         torch.cuda.synchronize()
-    inserted = [(k, s) for k, s in enumerate(whole[0][4])]
-    for i in range(WAVES):
-        want_m = []
-        for s_ in whole[1 + i][4]:
-            want_m.append(O.prefix_match(inserted, s_)[0])
+    # the oracle: m by brute force over every earlier whole request (the cold one has m = 0),
+    # then the sequential serve over tails whose pins are the rebased marker spans
+    inserted, o_waves = [], []
+    for wi, w in enumerate(whole):
+        streams, pins, m_list = [], [], []
+        spans = w[3].reshape(-1, 2)
+        for r, s_ in enumerate(w[4]):
+            m_ = O.prefix_match(inserted, s_)[0]
             inserted.append((len(inserted), s_))
-        assert ms[i].cpu().tolist()[:len(want_m)] == want_m, (i, want_m)
-        assert all(m_ == HEADER for m_ in want_m)  # the workload's metadata diverges right after the header
-        check_wave(S, 1 + i, hits[i].cpu().numpy(), outs[i].cpu())
+            sp = [(int(a), int(b)) for a, b in spans[w[2][r]:w[2][r + 1]]]
+            pins.append(sorted(O.marker_pin_offsets((max(a - m_, 0), b - m_) for a, b in sp if b - 1 >= m_)))
+            streams.append(s_[m_:])
+            m_list.append(m_)
+        off = np.zeros(len(streams) + 1, np.int64)
+        np.cumsum([x.size for x in streams], out=off[1:])
+        poff = np.zeros(len(streams) + 1, np.int64)
+        np.cumsum([len(p) for p in pins], out=poff[1:])
+        o_waves.append((np.concatenate(streams), off, poff, np.array([x for p in pins for x in p], np.int64),
+                        np.array(m_list, np.int64)))
+        if wi > 0:
+            assert ms[wi - 1].cpu().tolist()[:len(m_list)] == m_list, (wi, m_list)
+    ref, _ = oracle_waves(o_waves)
+    S2 = dict(S, ref=ref)
+    for i in range(WAVES):
+        check_wave(S2, 1 + i, hits[i].cpu().numpy(), outs[i].cpu())
     pipe.check()

@@ -169,3 +169,18 @@ def test_mla_oracle_vs_reference_materialize():
     ref = torch.from_numpy(c["out"]).double()
     assert float((out - ref).norm() / ref.norm()) <= 4.7e-3
     assert float((lse - torch.from_numpy(c["lse"])).abs().max()) <= 2e-2
+
+
+def test_prefix_lengths_sequential_matches_brute_force():
+    """The checker's fast phase-1 oracle (bench.py parity) equals the brute force
+    the reference pins RadixTree with (tests/test_radix.py:15-23)."""
+    rng = np.random.default_rng(3)
+    base = rng.integers(0, 4, size=400).astype(np.uint32)
+    seqs = []
+    for _ in range(250):
+        n, cut = int(rng.integers(0, 400)), int(rng.integers(0, 400))
+        s = base[:n].copy()
+        s[min(cut, n):] = rng.integers(0, 4, size=max(n - cut, 0))
+        seqs.append(s)
+    fast = O.prefix_lengths_sequential(seqs, probe=16)
+    assert fast == [O.prefix_match([(j, seqs[j]) for j in range(i)], seqs[i])[0] for i in range(len(seqs))]
