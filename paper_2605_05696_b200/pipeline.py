@@ -1,8 +1,12 @@
 """The warm-serve reattach step as one CUDA graph (B200 production path).
 
-For a wave of requests whose phase-1 prefix lengths ``m`` are known (host
-radix, engine.py:170), one step is
+For a wave of requests, one step is
 
+    K0  phase 1 on the device (engine.py:170, 228): every request's longest
+        prefix match against all earlier requests, then its insert
+        (radix.WavePrefixIndex), and the tails + rebased marker pins packed for
+        K1 (irm_wave_rebase) -- when the pipeline has a prefix index; otherwise
+        the wave arrives as tails with a host-known m
     K1  CDC + xxh64 over every request tail          (irm_cdc_xxh64)
     K3  first-writer-wins lookup/insert of all chunks (irm_store_lookup_insert)
         -- carve-out chunks (p < 32) neither probed nor inserted (engine.py:184-196)
