@@ -265,23 +265,12 @@ __global__ void rotate_rows_kernel(const T *rows, int64_t rs, int64_t rls, T *ou
     const int ihi = layout == IRM_LAYOUT_INTERLEAVED ? 2 * j + 1 : j + half;
     using A = typename Elem<T>::Acc;
     const auto cs = row_cs<typename Elem<T>::CS>(pos[r] * inv_freq[j]);
-    constexpr int U = 8;  // layers in flight per thread: their loads issue back to back
-    for (int l0 = 0; l0 < layers; l0 += U) {
-        A lo[U], hi[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (l0 + u < layers) {
-                const T *src = rows + (l0 + u) * rls + r * rs;
-                lo[u] = Elem<T>::load(src[ilo]);
-                hi[u] = Elem<T>::load(src[ihi]);
-            }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (l0 + u < layers) {
-                T *dst = out + (l0 + u) * ols + r * os;
-                dst[ilo] = Elem<T>::store(rot_lo(lo[u], hi[u], (A)cs.x, (A)cs.y), round);
-                dst[ihi] = Elem<T>::store(rot_hi(lo[u], hi[u], (A)cs.x, (A)cs.y), round);
-            }
+    for (int l = 0; l < layers; ++l) {
+        const T *src = rows + l * rls + r * rs;
+        T *dst = out + l * ols + r * os;
+        const A lo = Elem<T>::load(src[ilo]), hi = Elem<T>::load(src[ihi]);
+        dst[ilo] = Elem<T>::store(rot_lo(lo, hi, (A)cs.x, (A)cs.y), round);
+        dst[ihi] = Elem<T>::store(rot_hi(lo, hi, (A)cs.x, (A)cs.y), round);
     }
 }
 
