@@ -442,6 +442,16 @@ def run_ours(args):
     k4_gbs = k4_bytes / (k4 / 1e3) / 1e9
     k1_bytes = tok_per_wave * 4 + (tok_per_wave // 128) * 24
     k1_gbs = k1_bytes / (k1 / 1e3) / 1e9
+    # K1's real bound: the longest pin-delimited region walks its one-bit chain serially
+    longest_region = 0  # tail regions between marker pins (span start - 1, span end - 1), after m = HEADER
+    _tk, w_off, w_soff, w_spans = waves["comp"][0]
+    for r in range(w_off.size - 1):
+        sp = w_spans[2 * w_soff[r]:2 * w_soff[r + 1]].reshape(-1, 2) - HEADER
+        cuts = [-1] + sorted(int(x) for a, b in sp for x in (a - 1, b - 1)) + [int(w_off[r + 1] - w_off[r]) - HEADER - 1]
+        longest_region = max([longest_region] + [b - a for a, b in zip(cuts[:-1], cuts[1:])])
+    sm_mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0)) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
+    chain_floor_us = -(-longest_region // 32) * 85 / sm_mhz
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -468,10 +478,14 @@ def run_ours(args):
         "components": {
             "cdc_hash": {"value": tok_per_wave / (k1 / 1e3), "unit": "tokens/s", "kernel": "irm_cdc_xxh64 (K1)",
                          "launch_ms": k1, "tokens_per_launch": tok_per_wave,
-                         "note": "latency-bound: one carried bit per token within a pin-delimited region, "
-                                 "8 long regions in this wave (split form, DESIGN.md K1)",
-                         "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm, "unit": "GB/s",
-                                      "frac": k1_gbs / hbm}},
+                         "note": "bound by the one-bit carried chain of the longest pin-delimited region "
+                                 "(DESIGN.md K1), not by HBM",
+                         "roofline": {"bound": "chain", "achieved": chain_floor_us / (k1 * 1e3), "peak": 1.0,
+                                      "unit": "fraction of the chain floor", "frac": chain_floor_us / (k1 * 1e3),
+                                      "chain_floor_us": chain_floor_us, "longest_region_tokens": longest_region,
+                                      "floor_rule": "ceil(tokens / 32) x 85 cycles (tools/chain_microbench.cu) "
+                                                    "at the max SM clock",
+                                      "hbm_frac": k1_gbs / hbm}},
             "cdc_hash_wide": cdc_wide_component(hbm),
             "producer_rotate": producer_component(hbm),
             "serve_api": serve_api_component(),

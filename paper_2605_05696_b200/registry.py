@@ -16,6 +16,7 @@ in the reference (registry.py:37-70); it is the input generator, not the path.
 
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -77,10 +78,37 @@ class RegistryEntry:
     for KV it does not look at. The values are the same as an eager insert's."""
 
     __slots__ = ("fingerprint", "p_src", "insert_epoch", "_reg", "_tokens", "_c_kv", "_kr_base")
+    _FROZEN = ("fingerprint", "p_src", "insert_epoch", "c_kv", "kr_base")
 
     def __init__(self, fingerprint: int, p_src: int, insert_epoch: int, reg, tokens, c_kv=None, kr_base=None):
-        self.fingerprint, self.p_src, self.insert_epoch = fingerprint, p_src, insert_epoch
-        self._reg, self._tokens, self._c_kv, self._kr_base = reg, tokens, c_kv, kr_base
+        sa = object.__setattr__
+        sa(self, "fingerprint", fingerprint)
+        sa(self, "p_src", p_src)
+        sa(self, "insert_epoch", insert_epoch)
+        sa(self, "_reg", reg)
+        sa(self, "_tokens", tokens)
+        sa(self, "_c_kv", c_kv)
+        sa(self, "_kr_base", kr_base)
+
+    def __setattr__(self, name, value):
+        # frozen like the reference's dataclass (registry.py:73): its public fields never change
+        if name in self._FROZEN:
+            raise dataclasses.FrozenInstanceError(f"cannot assign to field {name!r}")
+        object.__setattr__(self, name, value)
+
+    def __delattr__(self, name):
+        if name in self._FROZEN:
+            raise dataclasses.FrozenInstanceError(f"cannot delete field {name!r}")
+        object.__delattr__(self, name)
+
+    def __eq__(self, other):
+        if not isinstance(other, RegistryEntry):
+            return NotImplemented
+        return (self.fingerprint, self.p_src, self.insert_epoch) == (other.fingerprint, other.p_src,
+                                                                     other.insert_epoch) and self._reg is other._reg
+
+    def __hash__(self):
+        return hash((self.fingerprint, self.p_src, self.insert_epoch))
 
     @property
     def c_kv(self) -> np.ndarray:

@@ -97,3 +97,19 @@ def test_wave_ops_reject_wrong_tensors():
         ops.wave_plan(z64, 2, z32, z64, 32, 0, z64, z64, torch.zeros(4, dtype=torch.uint8), z64)  # CPU tensors
     with pytest.raises(ValueError, match="wave_compact"):
         ops.wave_compact(z64, z64, z64, z64, z64, z32, 1, z64, z64, z32, z64, z64[:1], z32)  # hit must be int32
+
+
+def test_registry_entry_is_frozen():
+    """RegistryEntry keeps the reference's frozen-dataclass contract (registry.py:73)
+    while its rows are produced lazily."""
+    import dataclasses
+
+    import pytest
+
+    from paper_2605_05696_b200.registry import RegistryEntry
+
+    e = RegistryEntry(0xABC, 64, 0, None, (1, 2, 3))
+    for field in ("fingerprint", "p_src", "insert_epoch", "c_kv", "kr_base"):
+        with pytest.raises(dataclasses.FrozenInstanceError):
+            setattr(e, field, 1)
+    assert e.chunk_len == 3 and e == RegistryEntry(0xABC, 64, 0, None, (1, 2, 3))
