@@ -173,7 +173,9 @@ template <> struct FanElem<float> {
 
 __global__ void member_cossin_kernel(const int64_t *__restrict__ delta, int64_t n_cap,
                                      const int64_t *__restrict__ n_dev, int half,
-                                     const double *__restrict__ inv_freq, float2 *__restrict__ cs) {
+                                     const double *__restrict__ inv_freq, float2 *__restrict__ cs,
+                                     unsigned long long *__restrict__ work) {
+    if (work && blockIdx.x == 0 && threadIdx.x == 0) *work = 0;  // the gather's item counter, per launch
     const int64_t n = n_dev ? min(n_cap, *n_dev) : n_cap;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * half;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -198,6 +200,7 @@ struct FanArgs {
     const int64_t *n_groups_dev;
     int32_t layout;
     unsigned long long *status;  // sticky: 1 source run out of the pool, 2 destination run out of `out`
+    unsigned long long *work;    // dynamic item counter (nullable: static round robin)
 };
 
 // Reload form: the same fan-out, but every member's tile is brought in by its own
@@ -233,8 +236,15 @@ struct ReloadIter {
                 m = 0;
                 if (next_member(a, report)) return;
             }
-            item += gridDim.x;
+            advance(a);
         }
+    }
+    // the next (group, layer) item: first blockIdx.x, then dynamically from the shared
+    // counter when the launch has one (items vary 1..16 tiles x members: a static round
+    // robin left the slowest CTA ~25 % behind the mean)
+    __device__ __forceinline__ void advance(const FanArgs &a) {
+        if (a.work) item = (int64_t)atomicAdd(a.work, 1ULL) + gridDim.x;
+        else item += gridDim.x;
     }
     __device__ __forceinline__ void start(const FanArgs &a, bool report) {
         item = blockIdx.x;
@@ -247,7 +257,7 @@ struct ReloadIter {
             m = 0;
             if (next_member(a, report)) return;
         }
-        item += gridDim.x;
+        advance(a);
         load_item(a, report);
     }
     __device__ __forceinline__ bool valid(const FanArgs &a) const { return item < a.n_items; }
@@ -521,7 +531,9 @@ static int launch_ws(const FanArgs &a, int max_sms, cudaStream_t st) {
 }
 
 template <typename T, int ROWS, int STAGES, int D>
-static int launch_reload(const FanArgs &a, int max_sms, cudaStream_t st) {
+static int launch_reload(const FanArgs &a_in, int max_sms, cudaStream_t st) {
+    FanArgs a = a_in;
+    a.work = nullptr;  // producer and consumers walk the item sequence independently: static schedule
     // the vectorised k_r path: bf16, 64-wide k_r, 16-byte aligned c_KV
     const bool vec = std::is_same<T, __nv_bfloat16>::value && a.kr == 64 && a.ckv_bytes % 16 == 0 &&
                      ROWS * 4 <= 256;
@@ -636,8 +648,10 @@ extern "C" int irm_rotate_gather_fanout(const void *pool, int64_t pool_layer_str
     float2 *cs = reinterpret_cast<float2 *>(ws);
     const int half = kr_dim / 2;
     const int64_t grid = std::min<int64_t>((n_members * half + 255) / 256, (int64_t)sm_count() * 8);
+    const int64_t cs_bytes = ((n_members * half * (int64_t)sizeof(float2) + 255) / 256) * 256;
+    unsigned long long *work = reinterpret_cast<unsigned long long *>((char *)ws + cs_bytes);  // the spare 256 B
     member_cossin_kernel<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, st>>>(m_delta, n_members, n_members_dev,
-                                                                               half, inv_freq, cs);
+                                                                               half, inv_freq, cs, work);
     IRM_LAUNCH_CHECK();
     FanArgs a{};
     a.pool = (const char *)pool;
@@ -660,6 +674,7 @@ extern "C" int irm_rotate_gather_fanout(const void *pool, int64_t pool_layer_str
     a.n_groups_dev = n_groups_dev;
     a.layout = layout;
     a.status = (unsigned long long *)status;
+    a.work = getenv("IRM_FAN_STATIC") ? nullptr : work;  // tuning hook: the static round robin
     if (dtype == IRM_DTYPE_BF16) return dispatch_fanout<__nv_bfloat16>(a, max_sms, st);
     return dispatch_fanout<float>(a, max_sms, st);
 }

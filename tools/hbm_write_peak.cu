@@ -62,6 +62,39 @@ __global__ void __launch_bounds__(128) bulk_mix(char *out, const char *in, int64
     bulk_wait<0>();
 }
 
+// every store preceded by a bulk load of its tile; 8 consecutive stores of a CTA share one source tile
+// (the first load of a group misses to HBM, the rest hit L2): the K4 fan-out reload pattern, no math
+__global__ void __launch_bounds__(128) bulk_reload(char *out, const char *in, int64_t tiles, int group) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar[STAGES];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x) return;
+    const int64_t mine = (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    auto src_of = [&](int64_t k) { return in + (((blockIdx.x + k * gridDim.x) / group) % tiles) * (int64_t)TILE; };
+    constexpr int AHEAD = 3;  // loads in flight; STAGES - AHEAD stores in flight
+    for (int64_t k = 0; k < AHEAD && k < mine; ++k) {
+        mbar_arrive_expect_tx(&bar[k % STAGES], TILE);
+        bulk_g2s(smem + (k % STAGES) * TILE, src_of(k), TILE, &bar[k % STAGES]);
+    }
+    for (int64_t k = 0; k < mine; ++k) {
+        const int s = (int)(k % STAGES);
+        mbar_wait(&bar[s], (uint32_t)((k / STAGES) & 1));
+        bulk_s2g(out + (blockIdx.x + k * gridDim.x) * (int64_t)TILE, smem + s * TILE, TILE);
+        bulk_commit();
+        const int64_t nk = k + AHEAD;
+        if (nk < mine) {
+            bulk_wait_read<STAGES - AHEAD - 1>();  // store nk - STAGES has left stage nk % STAGES
+            mbar_arrive_expect_tx(&bar[nk % STAGES], TILE);
+            bulk_g2s(smem + (nk % STAGES) * TILE, src_of(nk), TILE, &bar[nk % STAGES]);
+        }
+    }
+    bulk_wait<0>();
+}
+
 __global__ void vec_write(uint4 *out, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = make_uint4((uint32_t)i, 1, 2, 3);
@@ -116,6 +149,12 @@ int main() {
         ms = time_ms([&] { bulk_mix<<<sms, 128, smem>>>(buf, src, tiles, ratio); });
         printf("bulk  %d stores : 1 load : %.0f GB/s write + %.0f GB/s read\n", ratio, gb / ms * 1e3,
                gb / ratio / ms * 1e3);
+    }
+    cudaFuncSetAttribute(bulk_reload, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int group : {8, 1}) {
+        ms = time_ms([&] { bulk_reload<<<sms, 128, smem>>>(buf, src, tiles, group); });
+        printf("bulk  load+store per tile, %d stores per source tile : %.0f GB/s write (+%.0f GB/s HBM read)\n",
+               group, gb / ms * 1e3, gb / group / ms * 1e3);
     }
     const int64_t n16 = tiles * TILE / 16;
     ms = time_ms([&] { vec_write<<<sms * 8, 512>>>((uint4 *)buf, n16); });
