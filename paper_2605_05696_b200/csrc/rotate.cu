@@ -253,7 +253,9 @@ template <> __device__ __forceinline__ float2 row_cs<float2>(double a) {
 }
 
 template <typename T>
-__global__ void rotate_rows_kernel(const T *rows, int64_t rs, int64_t rls, T *out,  // may alias (in place)
+// rows / out may be the same buffer (in place): every element is read, then written, by one
+// thread only, so the non-aliasing promise holds for every access the compiler may reorder
+__global__ void rotate_rows_kernel(const T *__restrict__ rows, int64_t rs, int64_t rls, T *__restrict__ out,
                                    int64_t os, int64_t ols, int64_t n, int half, int layers,
                                    const double *__restrict__ pos, const double *__restrict__ inv_freq,
                                    int layout, int round) {
