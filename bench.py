@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 METRIC = "reattached KV tokens/s/GPU (rotate+gather); CDC+hash tokens/s; fused-attn TFLOPS"
 UNIT = "tokens/s"
 LAYERS, CKV, KR, THETA = 27, 512, 64, 1e4
-K4_SMS = int(os.environ.get("IRM_K4_SMS", "120"))  # SMs the gather spreads over while the next wave's CDC + lookup run beside it
+K4_SMS = int(os.environ.get("IRM_K4_SMS", "140"))  # SMs the gather spreads over while the next wave's K0 + K1 + K3 run beside it (swept 112-148: profiles/r02_k4_sms.md)
 BODY, HEADER, R_PER_WAVE = 32768, 50, 8
 CARVE = 32
 
