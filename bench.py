@@ -38,7 +38,11 @@ sys.path.insert(0, ROOT)
 METRIC = "reattached KV tokens/s/GPU (rotate+gather); CDC+hash tokens/s; fused-attn TFLOPS"
 UNIT = "tokens/s"
 LAYERS, CKV, KR, THETA = 27, 512, 64, 1e4
-K4_SMS = int(os.environ.get("IRM_K4_SMS", "140"))  # SMs the gather spreads over while the next wave's K0 + K1 + K3 run beside it (swept 112-148: profiles/r02_k4_sms.md)
+# SMs the gather of wave i spreads over while K0 + K1 + K3 of wave i + 1 run beside it; 0 = all of them, in 4
+# retiring CTA rounds, with the front on a high-priority stream (swept: profiles/r02_k4_sms.md)
+K4_SMS = int(os.environ.get("IRM_K4_SMS", "0"))
+K4_PLACEMENT = ("K4 of wave i on all SMs in 4 retiring CTA rounds, wave i+1's front on a high-priority stream"
+                if K4_SMS == 0 else "K4 of wave i on %d SMs" % K4_SMS)
 BODY, HEADER, R_PER_WAVE = 32768, 50, 8
 CARVE = 32
 
@@ -461,7 +465,7 @@ def run_ours(args):
                                "DSv2 interleaved rotary theta 1e4, 32K-token agent_meta prompts",
                    "requests_per_step": R, "tokens_per_request": tok_per_wave // R + HEADER,
                    "layers": LAYERS, "l2": "inputs larger than L2 (1.0 GB pool, 8 GB KV out per step)",
-                   "pipeline": ("two-wave overlap: K4 of wave i on %d SMs || K1 + K3 of wave i+1" % K4_SMS
+                   "pipeline": ("two-wave overlap: %s || K0 + K1 + K3 of wave i+1" % K4_PLACEMENT
                                 + (" (CUDA graphs; sharded lookup: NCCL all-to-alls captured in the graph, peer replica fetch)"
                                    if sharded and graphs else
                                    " (streams; sharded lookup + peer replica fetch)" if sharded else " (CUDA graphs)"))
@@ -835,8 +839,8 @@ def run_config5(args):
                    "sessions": sessions * world, "sessions_per_gpu": sessions, "requests_per_step": C5_R,
                    "tokens_per_request": int(np.mean(np.diff(warm[0][1]))) + C5_HEADER, "layers": LAYERS,
                    "l2": "inputs larger than L2 (pool of %.0f GB per GPU)" % (pool.numel() * 2 / 1e9),
-                   "pipeline": "two-wave overlap, K4 on %d SMs; sharded lookup (%s all-to-alls%s) + peer replica fetch"
-                               % (K4_SMS, backend, " captured in the CUDA graphs" if graphs else ", streams"),
+                   "pipeline": "two-wave overlap (%s); sharded lookup (%s all-to-alls%s) + peer replica fetch"
+                               % (K4_PLACEMENT, backend, " captured in the CUDA graphs" if graphs else ", streams"),
                    "parallelism": f"sessions s mod G over {world} GPU(s), store sharded by fingerprint prefix"},
         "exchange": {"bytes_per_lookup": sharded.last_exchange_bytes, "owner_slots": sharded.owner_slots or
                      (sharded.slots if world == 1 else min(sharded.slots, (5 * sharded.slots) // (4 * world) + 64)),

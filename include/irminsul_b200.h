@@ -274,7 +274,10 @@ int irm_rotate_gather(const void *pool, int64_t pool_layer_stride, void *out,
  * rotation), bf16 or f32 pools, kr_dim a multiple of 4. n_members(_dev) bounds
  * the member table; ws at
  * least irm_fanout_workspace_bytes(n_members, kr_dim). Bounds, status and
- * max_sms as irm_rotate_gather. */
+ * max_sms as irm_rotate_gather. Items are handed out dynamically (an atomic
+ * counter in ws). cta_rounds > 1: the grid is cta_rounds x the resident CTAs and
+ * each CTA retires after its share of the items, so kernels of a higher-priority
+ * stream (the next wave's front in the reattach pipeline) get SMs in between. */
 int64_t irm_group_workspace_bytes(int64_t n);
 int irm_group_by_source(const int64_t *src_row, const int64_t *dst_row, const int32_t *len, const int64_t *delta,
                         int64_t n, const int64_t *n_dev, int64_t *g_src, int32_t *g_len, int32_t *g_first,
@@ -286,8 +289,8 @@ int irm_rotate_gather_fanout(const void *pool, int64_t pool_layer_stride, void *
                              const int32_t *g_len, const int32_t *g_first, const int32_t *g_count, int64_t n_groups,
                              const int64_t *n_groups_dev, const int64_t *m_dst, const int64_t *m_delta,
                              int64_t n_members, const int64_t *n_members_dev, const double *inv_freq,
-                             int32_t layout, int32_t dtype, int32_t max_sms, uint64_t *status, void *ws,
-                             int64_t ws_bytes, irm_stream_t stream);
+                             int32_t layout, int32_t dtype, int32_t max_sms, int32_t cta_rounds, uint64_t *status,
+                             void *ws, int64_t ws_bytes, irm_stream_t stream);
 /* K6 replica fetch: for run c < min(n_runs, *n_runs_dev), copy len[c] rows of
  * row_bytes from src_addr[c] + l * src_layer_stride (a device address, normally
  * inside a peer GPU's pool mapped through CUDA IPC over NVLink) to

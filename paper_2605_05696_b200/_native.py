@@ -66,7 +66,7 @@ _SIGS = {
     "irm_group_by_source": ([P, P, P, P, i64, P, P, P, P, P, P, P, P, P, i64, P], i32),
     "irm_fanout_workspace_bytes": ([i64, i32], i64),
     "irm_rotate_gather_fanout": ([P, i64, P, i64, i32, i32, i32, P, P, P, P, i64, P, P, P, i64, P, P, i32, i32, i32,
-                                  P, P, i64, P], i32),
+                                  i32, P, P, i64, P], i32),
     "irm_copy_runs": ([P, i64, P, i64, P, P, i64, P, i32, i32, P], i32),
     "irm_peer_export": ([P, P, P], i32),
     "irm_peer_open": ([P, i64, P], i32),

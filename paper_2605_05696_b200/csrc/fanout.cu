@@ -201,6 +201,8 @@ struct FanArgs {
     int32_t layout;
     unsigned long long *status;  // sticky: 1 source run out of the pool, 2 destination run out of `out`
     unsigned long long *work;    // dynamic item counter (nullable: static round robin)
+    int32_t rounds;              // > 1: the grid is rounds x the resident CTAs and each CTA retires after
+                                 // its share of the items, so kernels of other streams get SMs in between
 };
 
 // Reload form: the same fan-out, but every member's tile is brought in by its own
@@ -208,7 +210,7 @@ struct FanArgs {
 // tile back to back) and rotated in place, so the SM threads only touch k_r.
 template <int ROWS>
 struct ReloadIter {
-    int64_t item, g, src, dst;
+    int64_t item, g, src, dst, quota = INT64_MAX;
     int32_t l, tile, ntiles, len, m, m0, mc;
     __device__ __forceinline__ bool member_ok(const FanArgs &a, bool report) {
         dst = __ldg(a.m_dst + m0 + m);
@@ -243,11 +245,13 @@ struct ReloadIter {
     // counter when the launch has one (items vary 1..16 tiles x members: a static round
     // robin left the slowest CTA ~25 % behind the mean)
     __device__ __forceinline__ void advance(const FanArgs &a) {
-        if (a.work) item = (int64_t)atomicAdd(a.work, 1ULL) + gridDim.x;
+        if (--quota <= 0) item = a.n_items;  // this CTA's share is done: retire
+        else if (a.work) item = (int64_t)atomicAdd(a.work, 1ULL) + gridDim.x;
         else item += gridDim.x;
     }
     __device__ __forceinline__ void start(const FanArgs &a, bool report) {
         item = blockIdx.x;
+        if (a.rounds > 1) quota = (a.n_items + gridDim.x - 1) / gridDim.x;
         load_item(a, report);
     }
     __device__ __forceinline__ void next(const FanArgs &a, bool report) {
@@ -522,7 +526,7 @@ static int launch_ws(const FanArgs &a, int max_sms, cudaStream_t st) {
     if (per_sm < 1) per_sm = 1;
     int sms = sm_count();
     if (max_sms > 0) sms = std::min(sms, max_sms);
-    int64_t grid = (int64_t)sms * per_sm;
+    int64_t grid = (int64_t)sms * per_sm * (a.rounds > 1 ? a.rounds : 1);
     if (grid > a.n_items) grid = a.n_items;
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, threads, smem, st>>>(a);
@@ -534,6 +538,7 @@ template <typename T, int ROWS, int STAGES, int D>
 static int launch_reload(const FanArgs &a_in, int max_sms, cudaStream_t st) {
     FanArgs a = a_in;
     a.work = nullptr;  // producer and consumers walk the item sequence independently: static schedule
+    a.rounds = 1;
     // the vectorised k_r path: bf16, 64-wide k_r, 16-byte aligned c_KV
     const bool vec = std::is_same<T, __nv_bfloat16>::value && a.kr == 64 && a.ckv_bytes % 16 == 0 &&
                      ROWS * 4 <= 256;
@@ -626,13 +631,14 @@ extern "C" int irm_rotate_gather_fanout(const void *pool, int64_t pool_layer_str
                                         const int32_t *g_count, int64_t n_groups, const int64_t *n_groups_dev,
                                         const int64_t *m_dst, const int64_t *m_delta, int64_t n_members,
                                         const int64_t *n_members_dev, const double *inv_freq, int32_t layout,
-                                        int32_t dtype, int32_t max_sms, uint64_t *status, void *ws,
+                                        int32_t dtype, int32_t max_sms, int32_t cta_rounds, uint64_t *status, void *ws,
                                         int64_t ws_bytes, irm_stream_t stream) {
     IRM_REQUIRE(n_groups >= 0 && n_members >= 0 && layers >= 1 && ckv_dim >= 0 && kr_dim >= 4 && kr_dim % 4 == 0,
                 "bad sizes (layers >= 1, kr_dim a multiple of 4)");
     IRM_REQUIRE(layout == IRM_LAYOUT_HALF_SPLIT || layout == IRM_LAYOUT_INTERLEAVED, "bad layout");
     IRM_REQUIRE(dtype == IRM_DTYPE_BF16 || dtype == IRM_DTYPE_F32, "fan-out gather: bf16 or f32 pools");
     IRM_REQUIRE(max_sms >= 0, "max_sms must be >= 0");
+    IRM_REQUIRE(cta_rounds >= 1, "cta_rounds must be >= 1");
     if (n_groups == 0 || n_members == 0) return IRM_OK;
     IRM_REQUIRE(pool && out && g_src && g_len && g_first && g_count && m_dst && m_delta && inv_freq && ws,
                 "null pointer");
@@ -675,6 +681,7 @@ extern "C" int irm_rotate_gather_fanout(const void *pool, int64_t pool_layer_str
     a.layout = layout;
     a.status = (unsigned long long *)status;
     a.work = getenv("IRM_FAN_STATIC") ? nullptr : work;  // tuning hook: the static round robin
+    a.rounds = cta_rounds;
     if (dtype == IRM_DTYPE_BF16) return dispatch_fanout<__nv_bfloat16>(a, max_sms, st);
     return dispatch_fanout<float>(a, max_sms, st);
 }

@@ -240,9 +240,11 @@ def group_by_source(src_row: torch.Tensor, dst_row: torch.Tensor, length: torch.
 def rotate_gather_fanout(pool: torch.Tensor, out: torch.Tensor, groups: SourceGroups, inv_freq: torch.Tensor,
                          ckv_dim: int = 512, kr_dim: int = 64, layout: int = N.LAYOUT_HALF_SPLIT,
                          ws: torch.Tensor | None = None, n_members_dev: torch.Tensor | None = None,
-                         max_sms: int = 0, status: torch.Tensor | None = None) -> None:
+                         max_sms: int = 0, status: torch.Tensor | None = None, cta_rounds: int = 1) -> None:
     """K4 fan-out (irm_rotate_gather_fanout): each group's source rows are read
-    once and written, rotated by each member's delta, to every member's rows."""
+    once and written, rotated by each member's delta, to every member's rows.
+    ``cta_rounds`` > 1: CTAs retire after their share so a concurrent
+    high-priority stream gets SMs (the overlapped reattach step)."""
     assert pool.dtype == out.dtype and pool.is_contiguous() and out.is_contiguous()
     assert pool.dim() == 3 and out.dim() == 3 and pool.shape[0] == out.shape[0]
     assert pool.shape[2] == ckv_dim + kr_dim == out.shape[2]
@@ -254,8 +256,8 @@ def rotate_gather_fanout(pool: torch.Tensor, out: torch.Tensor, groups: SourceGr
         N.ptr(pool), pool.shape[1], N.ptr(out), out.shape[1], pool.shape[0], ckv_dim, kr_dim, N.ptr(groups.g_src),
         N.ptr(groups.g_len), N.ptr(groups.g_first), N.ptr(groups.g_count), groups.g_src.numel(),
         N.ptr(groups.n_groups), N.ptr(groups.m_dst), N.ptr(groups.m_delta), cap, N.ptr(n_members_dev),
-        N.ptr(inv_freq), layout, _DTYPE_CODE[pool.dtype], int(max_sms), N.ptr(status), N.ptr(ws), ws.numel(),
-        N.stream_ptr())
+        N.ptr(inv_freq), layout, _DTYPE_CODE[pool.dtype], int(max_sms), int(cta_rounds), N.ptr(status), N.ptr(ws),
+        ws.numel(), N.stream_ptr())
     N.check(rc, "irm_rotate_gather_fanout")
 
 

@@ -39,6 +39,7 @@ any flag, the store's included (call it outside timed regions).
 
 from __future__ import annotations
 
+
 import torch
 
 from . import _native as N
@@ -177,7 +178,7 @@ class ReattachPipeline:
             ops.group_by_source(sl["src"], sl["dst"], sl["len"], sl["delta"], sl["groups"], n_dev=sl["n_hit"])
         sl["hit"].copy_(self.hit)
 
-    def k4(self, slot: int | None = None, max_sms: int | None = None):
+    def k4(self, slot: int | None = None, max_sms: int | None = None, cta_rounds: int = 1):
         sms = self.k4_sms if max_sms is None else max_sms
         if slot is None:
             out, src, dst, ln, delta, n_hit, groups = (self.out, self.k4_src, self.k4_dst, self.k4_len,
@@ -188,7 +189,8 @@ class ReattachPipeline:
                                                        sl["n_hit"], sl["groups"])
         if self.fanout:
             ops.rotate_gather_fanout(self.pool, out, groups, self.inv, self.ckv, self.kr, self.layout,
-                                     ws=self.fan_ws, n_members_dev=n_hit, max_sms=sms, status=self.status)
+                                     ws=self.fan_ws, n_members_dev=n_hit, max_sms=sms, status=self.status,
+                                     cta_rounds=cta_rounds)
         else:
             ops.rotate_gather(self.pool, out, src, dst, ln, delta, self.inv, self.ckv, self.kr, self.layout,
                               ws=self.gather_ws, n_dev=n_hit, max_sms=sms, status=self.status)
@@ -269,7 +271,7 @@ class ReattachPipeline:
             return
         self._alloc_slots()
         main = torch.cuda.current_stream()
-        side = self._side if getattr(self, "_side", None) is not None else torch.cuda.Stream()
+        side = self._side if getattr(self, "_side", None) is not None else torch.cuda.Stream(priority=-1)
         self._side = side
 
         def front(i, s):
@@ -296,7 +298,7 @@ class ReattachPipeline:
                     with torch.cuda.stream(side):
                         front(i + 1, 1 - s)
                         loader.read_done(i + 1, side)
-                self.k4(s)
+                self.k4(s, cta_rounds=4 if k4_sms == 0 else 1)
                 main.wait_stream(side)
                 if i + 2 < n_waves:
                     loader.load(i + 2, side)  # H2D under K4(i + 1); front(i + 2) waits for it
@@ -386,7 +388,9 @@ class ReattachPipeline:
         device scalar (``wave_t``) each front advances. Every rank captures the
         same sequence of collectives, so replays stay matched across ranks."""
         self._alloc_slots()
-        side = torch.cuda.Stream()
+        # the next wave's front on a high-priority stream: its kernels take SMs as K4's CTAs retire
+        # (K4 runs in cta_rounds=4 rounds of CTAs when it has every SM; profiles/r02_k4_sms.md)
+        side = torch.cuda.Stream(priority=-1)
         if sharded:
             self.wave_t = torch.zeros((), dtype=torch.int64, device=self.pool.device)
 
@@ -404,7 +408,8 @@ class ReattachPipeline:
         def overlap(s):
             cur = torch.cuda.current_stream()
             side.wait_stream(cur)
-            self.k4(s, max_sms=k4_sms)  # the rest of the SMs run the next wave's front
+            # the rest of the SMs (k4_sms < all), or SMs freed between K4's CTA rounds, run the next front
+            self.k4(s, max_sms=k4_sms, cta_rounds=4 if k4_sms == 0 else 1)
             with torch.cuda.stream(side):
                 front(1 - s)
             cur.wait_stream(side)

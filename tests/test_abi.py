@@ -63,12 +63,13 @@ def test_rotate_validation():
 
 def test_fanout_validation():
     L = N.lib()
-    f = lambda kr, layout, dtype, ng=1, sms=0: L.irm_rotate_gather_fanout(
+    f = lambda kr, layout, dtype, ng=1, sms=0, rounds=1: L.irm_rotate_gather_fanout(
         None, 0, None, 0, 1, 512, kr, None, None, None, None, ng, None, None, None, 4, None, None, layout, dtype,
-        sms, None, None, 0, None)
+        sms, rounds, None, None, 0, None)
     assert f(63, 0, N.DTYPE_BF16) == N.IRM_EINVAL
     assert f(64, 3, N.DTYPE_BF16) == N.IRM_EINVAL
     assert f(64, 0, N.DTYPE_F64) == N.IRM_EINVAL  # bf16 / f32 pools only
+    assert f(64, 0, N.DTYPE_BF16, rounds=0) == N.IRM_EINVAL
     assert f(64, 0, N.DTYPE_BF16, ng=0) == N.IRM_OK
     assert L.irm_group_workspace_bytes(1000) >= 2048 * 20
     buf = ctypes.create_string_buffer(64)
