@@ -47,6 +47,15 @@ BODY, HEADER, R_PER_WAVE = 32768, 50, 8
 CARVE = 32
 
 
+def nccl_logs_to_stderr(world):
+    """N > 1: NCCL's communicator lines (ranks, NVLink / NVLS paths) stay visible, on stderr,
+    so stdout keeps exactly one JSON line."""
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,COLL")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -193,6 +202,7 @@ def run_ours(args):
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
         if backend == "nccl":
+            nccl_logs_to_stderr(world)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -712,6 +722,7 @@ def run_config5(args):
     os.environ.setdefault("RANK", "0")
     os.environ.setdefault("WORLD_SIZE", "1")
     if backend == "nccl":
+        nccl_logs_to_stderr(world)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         dist.init_process_group(backend)

@@ -163,7 +163,7 @@ def _worker(rank, WORLD, port, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_sharded_pipeline_one_gpu(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
