@@ -240,15 +240,46 @@ __global__ void __launch_bounds__(PT) keys_kernel(irm_prefix_view ix, const uint
     const bool ins = op_insert && op_insert[seq] && ep >= 0;  // epoch -1: a wave that did not fit
     const int64_t d0 = j * CH + (int64_t)threadIdx.x * TPT;
     uint64_t H = h.b;  // hash of the prefix before my first token (applied to x = 0)
+    uint64_t k[TPT];
+    int nk = 0;
 #pragma unroll
     for (int q = 0; q < TPT; ++q) {
         const int64_t d = d0 + q;
-        if (d >= len) break;
-        H = addmod(mulmod(H, base), (uint64_t)t[q] + 1);
-        const uint64_t k = prefix_key(H, d + 1, ix.hash_key);
-        key[s0 + d] = k;
-        if (ins) insert(ix, k, ep);
+        if (d < len) {
+            H = addmod(mulmod(H, base), (uint64_t)t[q] + 1);
+            k[q] = prefix_key(H, d + 1, ix.hash_key);
+            key[s0 + d] = k[q];
+            nk = q + 1;
+        }
     }
+    if (!ins) return;
+    // inserts: the first probe of every key in flight at once (claim by CAS), then every epoch
+    // min at once; a key whose home slot holds another key falls back to the probe loop
+    const uint64_t m = (uint64_t)ix.n_slots - 1;
+    int64_t slot[TPT];
+    unsigned claimed = 0;
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+        slot[q] = -1;
+        if (q < nk) {
+            const uint64_t idx = (k[q] >> 20) & m;
+            const unsigned long long old = atomicCAS((unsigned long long *)&ix.slot_key[idx],
+                                                     (unsigned long long)IRM_EMPTY_KEY, (unsigned long long)k[q]);
+            if (old == IRM_EMPTY_KEY) claimed++;
+            if (old == IRM_EMPTY_KEY || old == k[q]) slot[q] = (int64_t)idx;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+        if (q >= nk) continue;
+        if (slot[q] >= 0) atomicMin((long long *)&ix.slot_epoch[slot[q]], (long long)ep);
+        else insert(ix, k[q], ep);  // collision at the home slot: linear probing (counts its own claim)
+    }
+    // slots used: one atomic per warp
+    unsigned c = claimed;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)&ix.counters[0], (unsigned long long)c);
 }
 
 __global__ void query_kernel(irm_prefix_view ix, const int64_t *__restrict__ seq_off, int32_t n_seq,
