@@ -276,6 +276,60 @@ __global__ void rotate_rows_kernel(const T *__restrict__ rows, int64_t rs, int64
     }
 }
 
+// bf16, 64-wide rotary rows, 16-byte aligned: one thread per (row, 8-pair unit) -- eight
+// cos/sin pairs computed once, then two 16-byte loads / stores per layer (the pairs of
+// j = 8u .. 8u+7: interleaved words 2u, 2u+1; half-split words u (lo) and u+4 (hi))
+template <int LSPLIT>
+__global__ void rotate_rows_bf16x8_kernel(const __nv_bfloat16 *__restrict__ rows, int64_t rs, int64_t rls,
+                                          __nv_bfloat16 *__restrict__ out, int64_t os, int64_t ols, int64_t n,
+                                          int layers, const double *__restrict__ pos,
+                                          const double *__restrict__ inv_freq, int layout) {
+    // LSPLIT threads share a (row, unit): thread ls takes layers ls, ls + LSPLIT, ... (more loads in flight)
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * 4 * LSPLIT) return;
+    const int ls = (int)(i % LSPLIT);
+    const int64_t r = (i / LSPLIT) >> 2;
+    const int u = (int)((i / LSPLIT) & 3);
+    float c[8], sn[8];
+    const double p = pos[r];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        double s_, c_;
+        sincos(p * inv_freq[8 * u + q], &s_, &c_);
+        c[q] = (float)c_;
+        sn[q] = (float)s_;
+    }
+    const bool il = layout == IRM_LAYOUT_INTERLEAVED;
+    const int w0i = il ? 2 * u : u, w1i = il ? 2 * u + 1 : u + 4;
+#pragma unroll 3
+    for (int l = ls; l < layers; l += LSPLIT) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(rows + l * rls + r * rs);
+        uint4 *dst = reinterpret_cast<uint4 *>(out + l * ols + r * os);
+        uint4 w0 = src[w0i], w1 = src[w1i];
+        __nv_bfloat162 *p0 = reinterpret_cast<__nv_bfloat162 *>(&w0);
+        __nv_bfloat162 *p1 = reinterpret_cast<__nv_bfloat162 *>(&w1);
+        if (il) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                __nv_bfloat162 &pp = q < 4 ? p0[q] : p1[q - 4];
+                const float2 v = __bfloat1622float2(pp);
+                pp = __floats2bfloat162_rn(rot_lo(v.x, v.y, c[q], sn[q]), rot_hi(v.x, v.y, c[q], sn[q]));
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 lo = __bfloat1622float2(p0[q]), hi = __bfloat1622float2(p1[q]);
+                p0[q] = __floats2bfloat162_rn(rot_lo(lo.x, hi.x, c[2 * q], sn[2 * q]),
+                                              rot_lo(lo.y, hi.y, c[2 * q + 1], sn[2 * q + 1]));
+                p1[q] = __floats2bfloat162_rn(rot_hi(lo.x, hi.x, c[2 * q], sn[2 * q]),
+                                              rot_hi(lo.y, hi.y, c[2 * q + 1], sn[2 * q + 1]));
+            }
+        }
+        dst[w0i] = w0;
+        dst[w1i] = w1;
+    }
+}
+
 // ------------------------------------------------------------ host launchers
 constexpr int RG_THREADS = 256;
 constexpr int RG_STAGES = 4;
@@ -409,7 +463,19 @@ extern "C" int irm_rotate_rows_layered(const void *rows, int64_t row_stride, int
     const int half = dim / 2;
     const unsigned grid = (unsigned)((n * half + 255) / 256);
     cudaStream_t st = (cudaStream_t)stream;
-    if (dtype == IRM_DTYPE_BF16)
+    const bool vec = dtype == IRM_DTYPE_BF16 && dim == 64 && out_round == IRM_ROUND_NONE && row_stride % 8 == 0 &&
+                     out_stride % 8 == 0 && rows_layer_stride % 8 == 0 && out_layer_stride % 8 == 0 &&
+                     ((((uintptr_t)rows) | ((uintptr_t)out)) & 15) == 0;
+    const int lsplit = getenv("IRM_PROD_LSPLIT") ? atoi(getenv("IRM_PROD_LSPLIT")) : (layers >= 9 ? 3 : 1);
+    if (vec && lsplit == 3)
+        rotate_rows_bf16x8_kernel<3><<<(unsigned)((n * 12 + 255) / 256), 256, 0, st>>>(
+            (const __nv_bfloat16 *)rows, row_stride, rows_layer_stride, (__nv_bfloat16 *)out, out_stride,
+            out_layer_stride, n, layers, positions, inv_freq, layout);
+    else if (vec)
+        rotate_rows_bf16x8_kernel<1><<<(unsigned)((n * 4 + 255) / 256), 256, 0, st>>>(
+            (const __nv_bfloat16 *)rows, row_stride, rows_layer_stride, (__nv_bfloat16 *)out, out_stride,
+            out_layer_stride, n, layers, positions, inv_freq, layout);
+    else if (dtype == IRM_DTYPE_BF16)
         rotate_rows_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
             (const __nv_bfloat16 *)rows, row_stride, rows_layer_stride, (__nv_bfloat16 *)out, out_stride,
             out_layer_stride, n, half, layers, positions, inv_freq, layout, out_round);

@@ -227,3 +227,32 @@ def test_rotate_rows_layered_matches_per_layer(dtype, layout):
     torch.cuda.synchronize()
     assert torch.equal(got, ref)
     assert not torch.equal(got[:, :600, 512:], pool[:, :600, 512:])
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_rotate_rows_bf16_vector_path(layout):
+    """The 16-byte bf16 producer path (irm_rotate_rows on 64-wide k_r slices of a
+    [layers, rows, 576] pool) equals the element-wise path (a packed copy of the
+    same rows, which the vector path does not take) and the f64 rotation within
+    bf16 rounding."""
+    import torch
+
+    from paper_2605_05696_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(9)
+    pool = torch.randn(3, 300, 576, device="cuda", generator=g).to(torch.bfloat16)
+    pos = torch.from_numpy(np.random.default_rng(2).integers(0, 2**20, size=300).astype(np.float64)).cuda()
+    inv = O.make_inv_freq(1e4)
+    invd = ops.inv_freq_device(inv)
+    vec = pool.clone()
+    kr = vec[:, :, 512:]
+    ops.rotate_rows_layered(kr, pos, invd, layout, out=kr)
+    scal = torch.empty(3, 300, 66, dtype=torch.bfloat16, device="cuda")  # row stride 66: not 16-byte aligned
+    scal[:, :, :64] = pool[:, :, 512:]
+    ops.rotate_rows_layered(scal[:, :, :64], pos, invd, layout, out=scal[:, :, :64])
+    torch.cuda.synchronize()
+    assert torch.equal(vec[:, :, 512:], scal[:, :, :64])
+    assert torch.equal(vec[:, :, :512], pool[:, :, :512])
+    ref = O.rotate_rows(pool[0, :, 512:].double().cpu().numpy(), pos.cpu().numpy(), inv, interleaved=bool(layout))
+    got = vec[0, :, 512:].double().cpu().numpy()
+    assert np.abs(got - ref).max() <= 2.0 ** -7 * np.abs(ref).max()
