@@ -266,12 +266,27 @@ def run_ours(args):
         pipe.load_requests(*w)
         served.append(waves[kind][i])
 
+    fallback = None
     if sharded:  # K6: hash-sharded store (fixed-capacity NCCL all-to-all) + peer replica cache
         from paper_2605_05696_b200 import shard
 
-        cache = shard.ReplicaCache(pool, novel_rows, shard.map_peer_pools(pool), rank,
-                                   ops.ChunkStore(max_entries=1 << 16), scratch_rows=scratch_rows)
-        pipe.enable_sharding(shard.ShardedStore(store, novel_rows), cache, rank, world)
+        ok, peers = 1, None
+        try:
+            peers = shard.map_peer_pools(pool)
+        except Exception as e:  # no peer mapping between these GPUs: run independent replicas instead
+            print(f"bench: peer pool mapping failed ({type(e).__name__}: {e})", file=sys.stderr)
+            ok = 0
+        if world > 1:  # every rank takes the same path
+            t = torch.tensor([ok], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            ok = int(t.item())
+        if ok:
+            cache = shard.ReplicaCache(pool, novel_rows, peers, rank, ops.ChunkStore(max_entries=1 << 16),
+                                       scratch_rows=scratch_rows)
+            pipe.enable_sharding(shard.ShardedStore(store, novel_rows), cache, rank, world)
+        else:
+            sharded = False
+            fallback = "peer pool mapping (CUDA IPC) unavailable: every GPU runs an independent store (replicas)"
     wave_no = [0]  # global wave counter of the sharded order key
 
     def step(kind, i, cold=False):  # one wave on the serial path (eager or the serial graph)
@@ -480,7 +495,9 @@ def run_ours(args):
                                    if sharded and graphs else
                                    " (streams; sharded lookup + peer replica fetch)" if sharded else " (CUDA graphs)"))
                                if overlapped else "serial K1 -> K3 -> K4 per wave",
-                   "parallelism": f"sessions s mod G over {world} GPU(s)" + (", store sharded by fp prefix, NCCL all-to-all lookup" if sharded else "")},
+                   "parallelism": f"sessions s mod G over {world} GPU(s)" + (
+                       ", store sharded by fp prefix, NCCL all-to-all lookup" if sharded else
+                       f", {fallback}" if fallback else "")},
         "roofline": {"bound": "hbm", "kernel": ("irm_rotate_gather_fanout (K4 fan-out)" if pipe.fanout
                                                 else "irm_rotate_gather (K4)"), "achieved": k4_gbs,
                      "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": ncu_traffic("rotate_gather_ws_kernel" if pipe.fanout
