@@ -47,6 +47,29 @@ BODY, HEADER, R_PER_WAVE = 32768, 50, 8
 CARVE = 32
 
 
+_FLUSH = None
+
+
+def timed_flushed(fn, reps):
+    """Mean device time of ``fn`` over ``reps`` launches, each timed alone with CUDA
+    events and preceded (outside its events) by a 256 MB write that evicts the 126 MB
+    L2: component inputs smaller than L2 never start warm."""
+    import torch
+
+    global _FLUSH
+    if _FLUSH is None:
+        _FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda.synchronize()
+    for a, b in ev:
+        _FLUSH.fill_(1)
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev) / reps
+
+
 def nccl_logs_to_stderr(world):
     """N > 1: NCCL's communicator lines (ranks, NVLink / NVLS paths) stay visible, on stderr,
     so stdout keeps exactly one JSON line."""
@@ -376,15 +399,8 @@ def run_ours(args):
     ms_step = ms_total / K
 
     # -------- per-launch K1 / K4 durations: graph replays between events (no host gaps)
-    def time_graph(g, n=20):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        a.record()
-        for _ in range(n):
-            g.replay()
-        b.record()
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / n
+    def time_graph(g, n=20):  # each replay timed alone after an L2 flush
+        return timed_flushed(g.replay, n)
 
     step("comp", 0)  # a fresh wave through the serial path: its K1 / K3 / K4 are re-timed below
     torch.cuda.synchronize()
@@ -489,7 +505,8 @@ def run_ours(args):
         "config": {"workload": "DeepSeek-V2-Lite reattach (config 2): 27 layers, kv_lora 512 + rope 64, "
                                "DSv2 interleaved rotary theta 1e4, 32K-token agent_meta prompts",
                    "requests_per_step": R, "tokens_per_request": tok_per_wave // R + HEADER,
-                   "layers": LAYERS, "l2": "inputs larger than L2 (1.0 GB pool, 8 GB KV out per step)",
+                   "layers": LAYERS, "l2": "inputs larger than L2 (1.0 GB pool, 8 GB KV out per step); "
+                                           "components: L2 flushed (256 MB write) before every timed launch",
                    "pipeline": ("two-wave overlap: %s || K0 + K1 + K3 of wave i+1" % K4_PLACEMENT
                                 + (" (CUDA graphs; sharded lookup: NCCL all-to-alls captured in the graph, peer replica fetch)"
                                    if sharded and graphs else
@@ -963,15 +980,7 @@ def producer_component(hbm, n_rows=BODY):
     inv = ops.inv_freq_device(np.power(THETA, -2.0 * np.arange(KR // 2) / KR))
     run = lambda: ops.rotate_rows_layered(kr, positions, inv, N.LAYOUT_INTERLEAVED, out=kr)
     run()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 20
-    a.record()
-    for _ in range(reps):
-        run()
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / reps
+    ms = timed_flushed(run, 20)
     rows = n_rows * LAYERS
     byt = rows * KR * 2 * 2
     return {"value": rows / (ms / 1e3), "unit": "rows/s", "kernel": "irm_rotate_rows_layered (producer)",
@@ -998,16 +1007,8 @@ def cdc_wide_component(hbm, n_streams=296, n_tok=32768):
     off = torch.arange(0, (n_streams + 1) * n_tok, n_tok, dtype=torch.int64, device="cuda")
     ws = ops.CdcWorkspace()
     run = lambda: ops.cdc_xxh64(tok, off, None, None, 7, 32, 512, True, ws=ws, n_tokens=tok.numel())
-    run()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
-    a.record()
-    for _ in range(reps):
-        t = run()
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / reps
+    t = run()
+    ms = timed_flushed(run, 10)
     n_chunks = int(t.chunk_off[-1].item())
     byt = tok.numel() * 4 + n_chunks * 24
     return {"value": tok.numel() / (ms / 1e3), "unit": "tokens/s", "kernel": "irm_cdc_xxh64 (K1)",
@@ -1109,15 +1110,10 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
     out, lse = ops.mla_reattach_prefill(q, pool, n_ctx, n_ctx - n_q, 192 ** -0.5, kv_rows=rows_d,
                                         kv_chunk=chunk_d, chunk_cs=cs, layout=layout)
     torch.cuda.synchronize()
-    reps = 5
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(reps):
-        ops.mla_reattach_prefill(q, pool, n_ctx, n_ctx - n_q, 192 ** -0.5, kv_rows=rows_d, kv_chunk=chunk_d,
-                                 chunk_cs=cs, layout=layout, out=out, lse=lse)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / reps
+    # each launch timed alone after an L2 flush (the 64K pool, 75 MB, would otherwise stay in L2)
+    ms = timed_flushed(lambda: ops.mla_reattach_prefill(q, pool, n_ctx, n_ctx - n_q, 192 ** -0.5, kv_rows=rows_d,
+                                                        kv_chunk=chunk_d, chunk_cs=cs, layout=layout, out=out,
+                                                        lse=lse), 5)
     pos = np.arange(n_ctx - n_q, n_ctx, dtype=np.float64)
     flops = heads * float((pos + 1).sum()) * 2176  # (2*576 + 2*512) per visible (query, key, head)
     tflops = flops / (ms / 1e3) / 1e12
