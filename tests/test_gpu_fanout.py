@@ -62,9 +62,10 @@ def test_group_by_source(seed, n_items):
         assert got == want
 
 
+@pytest.mark.parametrize("rounds", [1, 4])
 @pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("seed,max_len", [(5, 300), (6, 40), (7, 513)])
-def test_fanout_matches_oracle_and_plain_gather(layout, seed, max_len):
+def test_fanout_matches_oracle_and_plain_gather(layout, seed, max_len, rounds):
     from paper_2605_05696_b200 import ops
 
     L, pool_rows = 3, 6000
@@ -77,7 +78,8 @@ def test_fanout_matches_oracle_and_plain_gather(layout, seed, max_len):
     ops.group_by_source(_d(src), _d(dst), _d(ln), _d(delta), groups)
     status = torch.zeros(1, dtype=torch.int64, device="cuda")
     out = torch.zeros(L, out_rows, 576, dtype=torch.bfloat16, device="cuda")
-    ops.rotate_gather_fanout(pool, out, groups, invd, layout=layout, status=status)
+    ops.rotate_gather_fanout(pool, out, groups, invd, layout=layout, status=status, cta_rounds=rounds,
+                             max_sms=0 if rounds > 1 else 17)  # retiring CTA rounds / a partial grid
     plain = torch.zeros_like(out)
     ops.rotate_gather(pool, plain, _d(src), _d(dst), _d(ln), _d(delta), invd, layout=layout)
     torch.cuda.synchronize()
