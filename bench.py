@@ -481,6 +481,9 @@ def run_ours(args):
     if world == 1:
         parity = pipeline_parity(pipe, list(served), waves["check"][0], dev_in["check"][0], overlapped, sharded,
                                  graphs if sharded else True, pool, req_stride, wave0=wave_no[0], prefix=True)
+    elif sharded and overlapped:  # every rank serves its check wave (the exchange is collective); rank 0 checks
+        parity = sharded_parity(pipe, plan, R, header, marker, body, dev_in["check"][0], graphs, peers, novel_rows,
+                                req_stride, wave_no[0], rank, world)
 
     # -------- roofline of the dominant kernel (K4) and K1
     k4_bytes = (src_rows + k4_rows) * (CKV + KR) * 2  # bf16 rows: unique source reads + destination writes
@@ -557,7 +560,7 @@ def run_ours(args):
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo},
         "parity": parity if parity is not None else {"checked": False,
-                                                     "why": "N > 1: the global oracle needs every rank's waves"},
+                                                     "why": "N > 1 without the sharded overlapped path"},
         # our kernels per wave (ncu launch list, profiles/r01e_launches.csv): K1 plan / offsets /
         # region / compact, K3 claim / decide / blockscan / commit / resolve, K4 cossin + gather;
         # sharded: + the replica map store's 5 and irm_copy_runs
@@ -599,6 +602,110 @@ def whole_to_tails(waves):
             k += 1
         out.append(pack_tails((streams, pins, mm)))
     return out
+
+
+def sharded_parity(pipe, plan, R, header, marker, body, check_dev, graphs, peers, novel_rows, req_stride, wave0,
+                   rank, world, chunks_per_request=3):
+    """The checker at N > 1 (after every timed region). Every rank serves its
+    never-served check wave through the sharded production path; rank 0 then
+    rebuilds EVERY rank's waves (each rank's generator is seeded by its rank) and
+    replays one global sequential oracle: phase 1 per rank (a rank's sessions are
+    its own), then first-writer-wins over all ranks' chunks in the exchange's
+    global order (wave, request, rank), with first-writer rows handed out by the
+    fingerprint's owner in its sub-range of the writer's pool (shard.py). Checked
+    on EVERY rank (results gathered to rank 0): its check wave's service map,
+    bit-exact, and a stratified sample of its hit rows against the oracle's
+    rotate+gather of the WRITER's pool bytes (peer pools read through their
+    CUDA-IPC mappings) -- ranks other than the body's first writer read rows
+    fetched from another GPU."""
+    import torch
+
+    from oracle import oracle as O
+
+    grab = {}
+    run_sharded(pipe, 1, lambda i: pipe.load_requests(*check_dev), wave0, graphs,
+                after_front=lambda i, s: grab.__setitem__("hit", pipe.slots[s]["hit"].clone()))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    # every rank's waves in serve order (the plan's order; the same generator calls as run_ours)
+    per_rank = []
+    for k in range(world):
+        rng = np.random.default_rng(1000 + k)
+        ws = {kind: [pack_requests(*make_requests(rng, header, marker, body, R)) for _ in range(n)]
+              for kind, n in plan.items()}
+        per_rank.append(whole_to_tails([w for kind in plan for w in ws[kind]]))
+    n_waves = len(per_rank[0])
+    chunks = [[None] * n_waves for _ in range(world)]
+    for k in range(world):
+        for w, (tok, off, poff, pins, ms) in enumerate(per_rank[k]):
+            recs = []
+            for r in range(off.size - 1):
+                st, ln, fp, _ = O.cdc_chunk(tok[off[r]:off[r + 1]], pins=pins[poff[r]:poff[r + 1]])
+                recs += [(int(ms[r]) + s_, l_, f_, r) for s_, l_, f_ in zip(st.tolist(), ln.tolist(), fp.tolist())]
+            chunks[k][w] = recs
+    reg, novel = {}, set()
+    for w in range(n_waves):  # the exchange's global order: (wave, request, rank), chunks in order
+        for r in range(R):
+            for k in range(world):
+                for j, (p, l, f, rr) in enumerate(chunks[k][w]):
+                    if rr == r and p >= CARVE and f not in reg:
+                        reg[f] = (k, w, j, p)
+                        novel.add((k, w, j))
+    region, nxt, rows = novel_rows // world, {}, {}
+    for k in range(world):  # owner o bump-allocates in its sub-range of writer k's pool, in k's query order
+        for w in range(n_waves):
+            for j, (p, l, f, r) in enumerate(chunks[k][w]):
+                if (k, w, j) in novel:
+                    o = ((f >> 32) * world) >> 32
+                    rows[(k, w, j)] = o * region + nxt.get((o, k), 0)
+                    nxt[(o, k)] = nxt.get((o, k), 0) + l
+    recs = []
+    for j, (p, l, f, r) in enumerate(chunks[rank][n_waves - 1]):  # this rank's check wave
+        if p < CARVE:
+            recs.append((-1, -1, -1, 0, p, l, r))
+        else:
+            wk, ww, wj, p_src = reg[f]
+            recs.append((0 if (wk, ww, wj) == (rank, n_waves - 1, j) else 1, wk, rows[(wk, ww, wj)], p_src, p, l,
+                         r))
+    want = np.array([x[0] for x in recs], np.int64)
+    got_hit = grab["hit"].cpu().numpy().astype(np.int64)
+    map_ok = bool(np.array_equal(got_hit[:want.size], want) and (got_hit[want.size:] == -1).all())
+    out = pipe.slots[0]["out"]
+    sample = []
+    for r in range(R):
+        hr = [x for x in recs if x[0] == 1 and x[6] == r]
+        if hr:
+            sample += [hr[i] for i in sorted({0, len(hr) // 2, len(hr) - 1})[:chunks_per_request]]
+    ckv_ok, kr_err, n_rows, remote = True, 0.0, 0, 0
+    inv = np.power(THETA, -2.0 * np.arange(KR // 2) / KR)
+    f32 = lambda u: (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    for code, wk, row, p_src, p, l, r in sample:
+        got = out[:, r * req_stride + p:r * req_stride + p + l].view(torch.int16).cpu().numpy().view(np.uint16)
+        src = peers[wk][:, row:row + l].view(torch.int16).cpu().numpy().view(np.uint16)
+        exp = np.zeros_like(got)
+        O.rotate_gather_bf16(np.ascontiguousarray(src), exp, np.zeros(1, np.int64), np.zeros(1, np.int64),
+                             np.array([l], np.int32), np.array([p - p_src], np.int64), inv, interleaved=True)
+        ckv_ok &= bool(np.array_equal(got[..., :CKV], exp[..., :CKV]))
+        e = f32(exp[..., CKV:])
+        kr_err = max(kr_err, float(np.abs(f32(got[..., CKV:]) - e).max() / max(np.abs(e).max(), 1e-30)))
+        n_rows += l
+        remote += l if wk != rank else 0
+    mine = {"ok": bool(map_ok and ckv_ok and kr_err <= 2.0 ** -7 and sample), "service_map_bit_exact": map_ok,
+            "chunks": int(want.size), "hits": int((want == 1).sum()), "kv_rows_checked": n_rows,
+            "kv_rows_first_written_by_another_gpu": remote, "ckv_bit_exact": ckv_ok, "kr_max_rel": kr_err}
+    import torch.distributed as dist
+
+    every = [None] * world
+    dist.all_gather_object(every, mine)
+    return {"ok": all(x["ok"] for x in every),
+            "service_map_bit_exact": all(x["service_map_bit_exact"] for x in every),
+            "ckv_bit_exact": all(x["ckv_bit_exact"] for x in every), "kr_max_rel": max(x["kr_max_rel"] for x in every),
+            "kv_rows_checked": sum(x["kv_rows_checked"] for x in every),
+            "kv_rows_first_written_by_another_gpu": sum(x["kv_rows_first_written_by_another_gpu"] for x in every),
+            "per_rank": every,
+            "sample": f"every rank's check wave ({R} fresh requests) through the sharded timed path vs one global "
+                      f"sequential oracle over {world} ranks x {n_waves} waves ({time.perf_counter() - t0:.1f} s); "
+                      f"KV: first/middle/last hit chunk per request x all layers, from the writer's pool"}
 
 
 def pipeline_parity(pipe, served, check_packed, check_dev, overlapped, sharded, graphs, pool, req_stride, wave0,
