@@ -1017,13 +1017,37 @@ def run_sharded(pipe, n, load, wave0, graphs, after_front=None, readback=None):
 
 
 # ----------------------------------------------------------------- the reference-facing serve API
+_REF_SERVE = r"""
+import hashlib, json, sys, time
+sys.path.insert(0, sys.argv[1])
+from irminsul import engine, model
+text = open(sys.argv[2]).read()
+t0 = time.perf_counter()
+import io
+trace = model.parse_trace(io.StringIO(text))
+state = engine.EngineState(engine.ServeConfig())
+results, row = engine.run_trace(state, trace)
+dt = time.perf_counter() - t0
+h = hashlib.sha256()
+for ri, r in enumerate(results):
+    for e in r.events:
+        h.update(repr((ri, e.start, e.length, e.klass.value, e.fingerprint, e.delta)).encode())
+print(json.dumps({"seconds": dt, "digest": h.hexdigest()[:16], "tokens": sum(r.num_tokens for r in results)}))
+"""
+
+
 def serve_api_component(n_warm=8):
     """The drop-in's public serve API end to end (engine.run_trace, engine.py:283-306)
     on a config-2 trace: one cold + ``n_warm`` warm 32.9K-token agent_meta requests
     as JSONL text -> model.parse_trace (native ingest) -> run_trace in one batch:
     K0 prefix match/insert, K1 CDC + xxh64, K3 first-writer-wins store, per-request
-    events on the host (observer mode). Tokens served per second, all included."""
+    events on the host (observer mode). Tokens served per second, all included.
+    When the reference is installed (baseline/_ref, the offline pip install), the
+    reference's own parse_trace + run_trace runs the same text on the same host and
+    the two event streams are compared by digest."""
+    import hashlib
     import io
+    import tempfile
 
     import torch
 
@@ -1054,12 +1078,31 @@ def serve_api_component(n_warm=8):
     dt = times[-1]
     n_tok = sum(r.num_tokens for r in results)
     pic = sum(r.counts[engine.ServiceClass.PIC_HIT] for r in results)
-    return {"value": n_tok / dt, "unit": "tokens/s", "api": "model.parse_trace + engine.run_trace (observer)",
-            "workload": f"{1 + n_warm} x {n_tok // (1 + n_warm)}-token agent_meta requests as JSONL "
-                        f"({len(text) / 1e6:.1f} MB), one serve batch", "seconds": dt,
-            "pic_hit_tokens": pic, "warm_total_cached": row.warm_total,
-            "note": "host-side per-request event lists included; the reference's own parse_trace + run_trace "
-                    "(Python) measured 0.30 M tok/s on this trace shape (profiles/r01_serve_api.md)"}
+    h = hashlib.sha256()
+    for ri, r in enumerate(results):
+        for e in r.events:
+            h.update(repr((ri, e.start, e.length, e.klass.value, e.fingerprint, e.delta)).encode())
+    out = {"value": n_tok / dt, "unit": "tokens/s", "api": "model.parse_trace + engine.run_trace (observer)",
+           "workload": f"{1 + n_warm} x {n_tok // (1 + n_warm)}-token agent_meta requests as JSONL "
+                       f"({len(text) / 1e6:.1f} MB), one serve batch", "seconds": dt,
+           "pic_hit_tokens": pic, "warm_total_cached": row.warm_total, "events_digest": h.hexdigest()[:16]}
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "irminsul")):
+        with tempfile.NamedTemporaryFile("w", suffix=".jsonl", delete=False) as f:
+            f.write(text)
+        try:
+            p = subprocess.run([sys.executable, "-c", _REF_SERVE, ref_dir, f.name], capture_output=True, text=True,
+                               timeout=600)
+            r = json.loads(p.stdout.strip().splitlines()[-1])
+            out["reference"] = {"value": r["tokens"] / r["seconds"], "unit": "tokens/s", "seconds": r["seconds"],
+                                "events_digest": r["digest"], "events_identical": r["digest"] == out["events_digest"],
+                                "what": "the reference package itself (baseline/_ref: irminsul 0.1.0, pure Python), "
+                                        "same JSONL text, same host, one process"}
+        except Exception as e:  # the comparison is informational; never fail the bench line on it
+            out["reference"] = {"unavailable": f"{type(e).__name__}: {e}"}
+        finally:
+            os.unlink(f.name)
+    return out
 
 
 # ----------------------------------------------------------------- producer rotation
