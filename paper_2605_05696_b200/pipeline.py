@@ -46,6 +46,21 @@ from . import _native as N
 from . import ops
 
 
+def _nvtx(name):
+    """NVTX range around a pipeline phase (visible to ncu --nvtx / Nsight on eager runs;
+    a captured graph replays without host ranges)."""
+    def wrap(fn):
+        def inner(*a, **kw):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*a, **kw)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        inner.__name__, inner.__doc__ = fn.__name__, fn.__doc__
+        return inner
+    return wrap
+
+
 class ReattachPipeline:
     def __init__(self, store: ops.ChunkStore, pool: torch.Tensor, inv_freq: torch.Tensor,
                  max_requests: int, max_tokens: int, max_pins: int, req_stride: int,
@@ -111,6 +126,7 @@ class ReattachPipeline:
     m = property(lambda self: self.inputs[self.cur_in]["m"])
 
     # ------------------------------------------------------------ device step
+    @_nvtx("irm.K0 phase 1 + rebase")
     def k0(self):
         """Phase 1 on the device: m of every request of the wave (K0), then the
         tails and their pins for K1 (irm_wave_rebase). No-op without a prefix index."""
@@ -121,6 +137,7 @@ class ReattachPipeline:
         ops.wave_rebase(ins["full_tok"], ins["full_off"], ins["m"], self.R, ins["span_off"], ins["spans"],
                         ins["tok"], ins["stream_off"], ins["pin_off"], ins["pins"])
 
+    @_nvtx("irm.K1 cdc+xxh64")
     def k1(self):
         k, mn, mx = self.params
         self.table = ops.cdc_xxh64(self.tok, self.stream_off, self.pin_off, self.pins, k, mn, mx, True,
@@ -140,6 +157,7 @@ class ReattachPipeline:
                       order)
         return probe, order
 
+    @_nvtx("irm.K3 store")
     def k3(self):
         t = self.table
         probe, order = self._plan()
@@ -178,6 +196,7 @@ class ReattachPipeline:
             ops.group_by_source(sl["src"], sl["dst"], sl["len"], sl["delta"], sl["groups"], n_dev=sl["n_hit"])
         sl["hit"].copy_(self.hit)
 
+    @_nvtx("irm.K4 rotate+gather")
     def k4(self, slot: int | None = None, max_sms: int | None = None, cta_rounds: int = 1):
         sms = self.k4_sms if max_sms is None else max_sms
         if slot is None:
@@ -232,6 +251,7 @@ class ReattachPipeline:
         if hasattr(replica_cache.map, "reserve"):
             replica_cache.map.reserve(sharded_store.slots)
 
+    @_nvtx("irm.K3+K6 sharded store")
     def k3_sharded(self, wave: int):
         t = self.table
         cap = t.start.numel()
