@@ -976,6 +976,24 @@ def run_config5(args):
     fetched = torch.stack([cache.fetched_runs, cache.fetched_rows]).to(torch.int64)
     dist.all_reduce(fetched)
     fetched = fetched.tolist()
+    # the exchange alone: K1 of a served wave, then its sharded lookup again (all hits), timed per rank
+    pipe.load(*warm_dev[0])
+    pipe.k1()
+    torch.cuda.synchronize()
+    dist.barrier()
+    for _ in range(2):  # warm (first calls allocate)
+        pipe.k3_sharded(10**6)
+    torch.cuda.synchronize()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record()
+    for _ in range(3):
+        pipe.k3_sharded(10**6)
+    x1.record()
+    torch.cuda.synchronize()
+    xt = torch.tensor([x0.elapsed_time(x1) * 1e3 / 3], device=dev)
+    every_us = [torch.zeros_like(xt) for _ in range(world)]
+    dist.all_gather(every_us, xt)
+    exchange_us = [float(x.item()) for x in every_us]
 
     parity = {"checked": False, "why": "N > 1: the global oracle needs every rank's waves"}
     if world == 1:
@@ -994,7 +1012,11 @@ def run_config5(args):
                    "pipeline": "two-wave overlap (%s); sharded lookup (%s all-to-alls%s) + peer replica fetch"
                                % (K4_PLACEMENT, backend, " captured in the CUDA graphs" if graphs else ", streams"),
                    "parallelism": f"sessions s mod G over {world} GPU(s), store sharded by fingerprint prefix"},
-        "exchange": {"bytes_per_lookup": sharded.last_exchange_bytes, "owner_slots": sharded.owner_slots or
+        "exchange": {"lookup_us_per_rank": exchange_us,
+                     "lookup_note": "eager (host-launched) K3 + both all-to-alls + owner sort + replica lookup of "
+                                    "one wave (re-probe, all hits), CUDA events per rank; in the timed step the same "
+                                    "work is replayed from the front's CUDA graph",
+                     "bytes_per_lookup": sharded.last_exchange_bytes, "owner_slots": sharded.owner_slots or
                      (sharded.slots if world == 1 else min(sharded.slots, (5 * sharded.slots) // (4 * world) + 64)),
                      "query_capacity": sharded.slots, "replica_runs_fetched_all_ranks": fetched[0],
                      "replica_rows_fetched_all_ranks": fetched[1]},
