@@ -1051,8 +1051,18 @@ constexpr int QT = IRM_MLA_V3_QT;
 #endif
 constexpr int KST = IRM_MLA_V3_KST, NS = IRM_MLA_V3_NS;  // S buffers: QK runs NS - 1 tiles ahead
 constexpr int NP = IRM_MLA_V3_NP;  // P buffers: 1 frees smem for a fifth K stage
+// P as the TMEM A operand of PV (TS mode), written over its own S buffer: the tensor core then
+// reads only V from shared memory in PV. The 2-SM TS layout wants each row's 64 keys in both
+// lane halves, so the two softmax warps holding a row's key halves swap them through shared
+// memory (8 KB written + read per CTA per tile, instead of 8 KB of P written and 16 KB read by
+// the MMAs)
+#ifndef IRM_MLA_V3_PT
+#define IRM_MLA_V3_PT 1
+#endif
+constexpr bool PT = IRM_MLA_V3_PT != 0;
+constexpr int XBUF = 2 * 2 * 64 * 64;  // P-half swap: [t & 1][key half][4 x 16 B][64 rows]
 constexpr int S_Q = 0, S_K = (NPIECE - QT) * QPIECE, S_P = S_K + KST * KTILE;
-constexpr int SMEM3 = S_P + NP * PTILE2;  // 192 KB (4 K stages, 2 P buffers)
+constexpr int SMEM3 = S_P + (PT ? XBUF : NP * PTILE2);  // 192 KB (4 K stages, 2 P buffers)
 constexpr uint32_t COL_S = 0, COL_O = 32 * NS, COL_Q = COL_O + 256;
 static_assert(COL_Q + 32 * QT <= 512, "TMEM: S x 3, O, Q pieces");
 constexpr uint32_t FV_TX = 4 * KPIECE;  // foreign V bytes per CTA per tile
@@ -1269,6 +1279,7 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
                 c_v += prof_clock<2>() - a1;
                 tc::fence_after();
                 const uint32_t pd = p_lo + ((((t & 1) % NP) * PTILE2) >> 4);
+                const uint32_t pt_col = tbase + COL_S + (t % NS) * 32;  // PT: P(t) over S(t)
                 const uint32_t kd = kv_lo + ((st * KTILE) >> 4);
                 if (tc::elect_one()) {
 #pragma unroll
@@ -1276,10 +1287,16 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
 #pragma unroll
-                            for (int k = 0; k < 2; ++k)
-                                tc2::mma_bf16_ss_w(tbase + COL_O + h * 128, pd + (((2 * a + k) * 32) >> 4), p_hi,
-                                                   kd + (((4 * h + 2 * a) * KPIECE + k * 2048) >> 4), kv_hi, idesc_pv,
-                                                   (t > 0 || a > 0 || k > 0) ? 1u : 0u);
+                            for (int k = 0; k < 2; ++k) {
+                                const uint32_t vb = kd + (((4 * h + 2 * a) * KPIECE + k * 2048) >> 4);
+                                const uint32_t acc = (t > 0 || a > 0 || k > 0) ? 1u : 0u;
+                                if constexpr (PT)  // keys 16 (2a + k) .. + 15: 8 bf16-pair columns
+                                    tc2::mma_bf16_ts_w(tbase + COL_O + h * 128, pt_col + 8 * (2 * a + k), vb, kv_hi,
+                                                       idesc_pv, acc);
+                                else
+                                    tc2::mma_bf16_ss_w(tbase + COL_O + h * 128, pd + (((2 * a + k) * 32) >> 4), p_hi,
+                                                       vb, kv_hi, idesc_pv, acc);
+                            }
                         }
                     }
                     tc2::commit_both(&b_kempty[st]);
@@ -1377,8 +1394,9 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
             l = l * alpha + (ls[0] + ls[1]);
             long long a2 = prof_clock<4>();
             c_ex += a2 - a1;
-            if (NP == 2 && t >= 2) mbar_wait(&b_odone[t & 1], ((t >> 1) - 1) & 1);  // P buffer free
-            if (NP == 1 && t >= 1) mbar_wait(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);  // PV(t-1) read P
+            // P buffer free (PT: S(t)'s buffer, read by PV(t - NS) before QK(t) overwrote it)
+            if (!PT && NP == 2 && t >= 2) mbar_wait(&b_odone[t & 1], ((t >> 1) - 1) & 1);
+            if (!PT && NP == 1 && t >= 1) mbar_wait(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);  // PV(t-1) read P
             c_o += prof_clock<4>() - a2;
             long long a3 = prof_clock<4>();
             if (t >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
@@ -1398,11 +1416,33 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
             }
             long long a4 = prof_clock<4>();
             c_r += a4 - a3;
-            const uint32_t pt = p_base + ((t & 1) % NP) * PTILE2;
+            if constexpr (PT) {
+                // swap key halves with warp w ^ 2 (same rows), then the row's 64 keys as 32 bf16-pair
+                // columns over S(t) in this lane
+                const uint32_t xb = p_base + (t & 1) * (XBUF / 2);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                sts128(pt + swz128(r, 4 * kh + j), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
-            fence_proxy_async_smem();
+                for (int j = 0; j < 4; ++j)
+                    sts128(xb + ((kh * 4 + j) * 64 + r) * 16,
+                           make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
+                asm volatile("bar.sync %0, 64;" ::"r"(2 + (w & 1)) : "memory");
+                uint32_t px[16];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(px[4 * j]), "=r"(px[4 * j + 1]), "=r"(px[4 * j + 2]), "=r"(px[4 * j + 3])
+                                 : "r"(xb + (((kh ^ 1) * 4 + j) * 64 + r) * 16));
+                const uint32_t pcol = lane_base + COL_S + (t % NS) * 32;
+                tc2::st_32x32b_x16(pcol + 16 * kh, pk);
+                tc2::st_32x32b_x16(pcol + 16 * (kh ^ 1), px);
+                tc::wait_st();
+            } else {
+                const uint32_t pt = p_base + ((t & 1) % NP) * PTILE2;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    sts128(pt + swz128(r, 4 * kh + j),
+                           make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
+                fence_proxy_async_smem();
+            }
             tc::fence_before();
             mbar_arrive(&b_pfull[t & 1]);  // local; the peer's relay forwards it to the leader
             c_e += prof_clock<4>() - a4;
