@@ -116,8 +116,10 @@ int irm_trace_fill(const char *text, int64_t len, int32_t universal_newlines, ui
  * table holding the smallest insert epoch that reaches it (the radix tree's
  * earliest-inserted witness). Caller-owned; initialise with irm_prefix_reset(). */
 typedef struct {
-    uint64_t *slot_key;   /* [n_slots] prefix key or IRM_EMPTY_KEY               */
-    int64_t *slot_epoch;  /* [n_slots] smallest insert epoch with this prefix    */
+    uint64_t *slots;      /* [2 x n_slots] slot i = (slots[2i] prefix key or
+                           IRM_EMPTY_KEY, slots[2i+1] (int64) the smallest insert
+                           epoch with this prefix): key and epoch share one 32-B
+                           sector, so an insert is one random DRAM access        */
     int64_t n_slots;      /* power of two, >= 2 x the distinct prefixes stored  */
     int64_t *counters;    /* [2]: slots used, flags (1 table full: error; 4 a hash
                            collision was resolved by an exact scan: informational;

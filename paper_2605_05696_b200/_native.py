@@ -40,7 +40,7 @@ class StoreView(ctypes.Structure):
 class PrefixView(ctypes.Structure):
     """irm_prefix_view (include/irminsul_b200.h)."""
 
-    _fields_ = [("slot_key", P), ("slot_epoch", P), ("n_slots", i64), ("counters", P), ("hash_key", u64)]
+    _fields_ = [("slots", P), ("n_slots", i64), ("counters", P), ("hash_key", u64)]
 
 
 _SIGS = {

@@ -80,11 +80,16 @@ __device__ __forceinline__ uint64_t prefix_key(uint64_t h, int64_t d, uint64_t h
     return k == IRM_EMPTY_KEY ? k - 1 : k;
 }
 
+__device__ __forceinline__ uint64_t *slot_key(const irm_prefix_view &ix, uint64_t i) { return ix.slots + 2 * i; }
+__device__ __forceinline__ long long *slot_epoch(const irm_prefix_view &ix, uint64_t i) {
+    return reinterpret_cast<long long *>(ix.slots + 2 * i + 1);
+}
+
 __device__ __forceinline__ int64_t find(const irm_prefix_view &ix, uint64_t key) {
     const uint64_t m = (uint64_t)ix.n_slots - 1;
     uint64_t idx = (key >> 20) & m;
     for (int64_t probe = 0; probe < ix.n_slots; ++probe, idx = (idx + 1) & m) {
-        const uint64_t k = ((volatile uint64_t *)ix.slot_key)[idx];
+        const uint64_t k = *(volatile uint64_t *)slot_key(ix, idx);
         if (k == key) return (int64_t)idx;
         if (k == IRM_EMPTY_KEY) return -1;
     }
@@ -95,9 +100,9 @@ __device__ __forceinline__ void insert(const irm_prefix_view &ix, uint64_t key, 
     const uint64_t m = (uint64_t)ix.n_slots - 1;
     uint64_t idx = (key >> 20) & m;
     for (int64_t probe = 0; probe < ix.n_slots; ++probe, idx = (idx + 1) & m) {
-        uint64_t k = ((volatile uint64_t *)ix.slot_key)[idx];
+        uint64_t k = *(volatile uint64_t *)slot_key(ix, idx);
         if (k == IRM_EMPTY_KEY) {
-            k = atomicCAS((unsigned long long *)&ix.slot_key[idx], (unsigned long long)IRM_EMPTY_KEY,
+            k = atomicCAS((unsigned long long *)slot_key(ix, idx), (unsigned long long)IRM_EMPTY_KEY,
                           (unsigned long long)key);
             if (k == IRM_EMPTY_KEY) {
                 atomicAdd((unsigned long long *)&ix.counters[0], 1ULL);
@@ -105,7 +110,7 @@ __device__ __forceinline__ void insert(const irm_prefix_view &ix, uint64_t key, 
             }
         }
         if (k == key) {
-            atomicMin((long long *)&ix.slot_epoch[idx], (long long)epoch);
+            atomicMin(slot_epoch(ix, idx), (long long)epoch);
             return;
         }
     }
@@ -115,8 +120,8 @@ __device__ __forceinline__ void insert(const irm_prefix_view &ix, uint64_t key, 
 __global__ void reset_kernel(irm_prefix_view ix) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < ix.n_slots) {
-        ix.slot_key[i] = IRM_EMPTY_KEY;
-        ix.slot_epoch[i] = INT64_MAX;
+        *slot_key(ix, i) = IRM_EMPTY_KEY;
+        *slot_epoch(ix, i) = INT64_MAX;
     }
     if (i < 2) ix.counters[i] = 0;
 }
@@ -263,7 +268,7 @@ __global__ void __launch_bounds__(PT) keys_kernel(irm_prefix_view ix, const uint
         slot[q] = -1;
         if (q < nk) {
             const uint64_t idx = (k[q] >> 20) & m;
-            const unsigned long long old = atomicCAS((unsigned long long *)&ix.slot_key[idx],
+            const unsigned long long old = atomicCAS((unsigned long long *)slot_key(ix, idx),
                                                      (unsigned long long)IRM_EMPTY_KEY, (unsigned long long)k[q]);
             if (old == IRM_EMPTY_KEY) claimed++;
             if (old == IRM_EMPTY_KEY || old == k[q]) slot[q] = (int64_t)idx;
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(PT) keys_kernel(irm_prefix_view ix, const uint
 #pragma unroll
     for (int q = 0; q < TPT; ++q) {
         if (q >= nk) continue;
-        if (slot[q] >= 0) atomicMin((long long *)&ix.slot_epoch[slot[q]], (long long)ep);
+        if (slot[q] >= 0) atomicMin(slot_epoch(ix, slot[q]), (long long)ep);
         else insert(ix, k[q], ep);  // collision at the home slot: linear probing (counts its own claim)
     }
     // slots used: one atomic per warp
@@ -298,7 +303,7 @@ __global__ void query_kernel(irm_prefix_view ix, const int64_t *__restrict__ seq
     while (lo < hi) {  // largest d with a prefix of length d inserted before epoch e
         const int64_t mid = (lo + hi + 1) >> 1;
         const int64_t s = find(ix, key[s0 + mid - 1]);
-        const int64_t ep = s >= 0 ? ((volatile int64_t *)ix.slot_epoch)[s] : INT64_MAX;
+        const int64_t ep = s >= 0 ? *(volatile int64_t *)slot_epoch(ix, s) : INT64_MAX;
         if (ep < e) {
             lo = mid;
             wit = ep;
@@ -416,7 +421,7 @@ using namespace irm;
 using prefix::Aff;
 
 extern "C" int irm_prefix_reset(const irm_prefix_view *ix, irm_stream_t stream) {
-    IRM_REQUIRE(ix && ix->slot_key && ix->slot_epoch && ix->counters, "null pointer");
+    IRM_REQUIRE(ix && ix->slots && ix->counters, "null pointer");
     IRM_REQUIRE(ix->n_slots >= 2 && (ix->n_slots & (ix->n_slots - 1)) == 0, "n_slots must be a power of two");
     const int64_t n = ix->n_slots;
     prefix::reset_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*ix);
@@ -437,7 +442,7 @@ extern "C" int irm_prefix_match_insert(const irm_prefix_view *ix, const uint32_t
                                        const uint8_t *op_insert, const uint8_t *op_query, const uint32_t *arena,
                                        const int64_t *wit_off, const int64_t *wit_len, int64_t *m, int64_t *wit,
                                        void *ws, int64_t ws_bytes, irm_stream_t stream) {
-    IRM_REQUIRE(ix && ix->slot_key && ix->slot_epoch && ix->counters, "null index");
+    IRM_REQUIRE(ix && ix->slots && ix->counters, "null index");
     IRM_REQUIRE(n_seq >= 0 && n_tokens >= 0, "bad sizes");
     if (n_seq == 0) return IRM_OK;
     IRM_REQUIRE(seq_off && op_epoch && m && wit && ws, "null pointer");

@@ -138,9 +138,9 @@ class DeviceRadixTree:
         while n_slots < 2 * max_prefixes:
             n_slots <<= 1
         dev = self.counters.device
-        self.slot_key = torch.empty(n_slots, dtype=torch.int64, device=dev)
-        self.slot_epoch = torch.empty(n_slots, dtype=torch.int64, device=dev)
-        self.view = N.PrefixView(N.ptr(self.slot_key), N.ptr(self.slot_epoch), n_slots, N.ptr(self.counters),
+        self.n_slots = n_slots
+        self.slots = torch.empty(2 * n_slots, dtype=torch.int64, device=dev)  # (key, epoch) pairs
+        self.view = N.PrefixView(N.ptr(self.slots), n_slots, N.ptr(self.counters),
                                  self.hash_key & (2**64 - 1))
         N.check(N.lib().irm_prefix_reset(self.view, N.stream_ptr()), "irm_prefix_reset")
 
@@ -163,7 +163,7 @@ class DeviceRadixTree:
                 new = torch.zeros(cap, dtype=torch.int64, device=old.device)
                 new[:self._epoch].copy_(old[:self._epoch])
                 setattr(self, name, new)
-        half = self.slot_key.numel() // 2
+        half = self.n_slots // 2
         if self.grow and self._prefix_bound + ins_tok > half:
             self.check()
             used = int(self.counters[0])  # the real count (one sync, only near the load limit)
@@ -175,7 +175,7 @@ class DeviceRadixTree:
         """Rebuild the table 2x larger from the stored sequences, with their epochs."""
         torch, N = self._torch, self._N
         self.counters.zero_()
-        self._new_table(max(2 * need, self.slot_key.numel()))
+        self._new_table(max(2 * need, self.n_slots))
         n = self._epoch
         if n == 0:
             return
@@ -307,9 +307,9 @@ class WavePrefixIndex:
         while n_slots < 2 * max_prefixes:
             n_slots <<= 1
         self.counters = torch.zeros(2, dtype=torch.int64, device=dev)
-        self.slot_key = torch.empty(n_slots, dtype=torch.int64, device=dev)
-        self.slot_epoch = torch.empty(n_slots, dtype=torch.int64, device=dev)
-        self.view = N.PrefixView(N.ptr(self.slot_key), N.ptr(self.slot_epoch), n_slots, N.ptr(self.counters),
+        self.n_slots = n_slots
+        self.slots = torch.empty(2 * n_slots, dtype=torch.int64, device=dev)  # (key, epoch) pairs
+        self.view = N.PrefixView(N.ptr(self.slots), n_slots, N.ptr(self.counters),
                                  self.hash_key & (2**64 - 1))
         N.check(N.lib().irm_prefix_reset(self.view, N.stream_ptr()), "irm_prefix_reset")
         self.arena = torch.zeros(arena_tokens, dtype=torch.int32, device=dev)

@@ -133,7 +133,7 @@ def test_prefix_growth_golden(case):
     tree.check()
     q = np.array([not o[0] for o in ops])
     assert np.array_equal(got_m[q], g["m"][q]) and np.array_equal(got_w[q], g["witness"][q])
-    assert tree.slot_key.numel() > 16 and tree.arena.numel() > 64
+    assert tree.n_slots > 16 and tree.arena.numel() > 64
 
 
 @pytest.mark.parametrize("case", sorted(RADIX_CASES))
