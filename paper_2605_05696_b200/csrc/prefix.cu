@@ -85,24 +85,58 @@ __device__ __forceinline__ long long *slot_epoch(const irm_prefix_view &ix, uint
     return reinterpret_cast<long long *>(ix.slots + 2 * i + 1);
 }
 
-__device__ __forceinline__ int64_t find(const irm_prefix_view &ix, uint64_t key) {
+// Slot placement. The keys of depths 64b + 1 .. 64b + 64 of a sequence share the home
+// region of the key of its prefix of length 64b (a constant for b = 0): home(d) = region +
+// (d - 1) % 64, a 1 KB run of slots, so inserting a sequence writes consecutive slots (DRAM
+// rows, not one random sector per token) and a query's binary search lands in the same runs.
+// Probe sequence of a key: its home slot, then the same offset in a second region chosen by
+// the region key (another block that took the home region: the block's keys move on together
+// and stay contiguous), then double hashing by the key itself (sequences diverging inside
+// one block -- e.g. every request after a shared header -- scatter instead of queueing behind
+// each other). The sequence is fixed by (region key, depth, key), so lookups follow the
+// inserts exactly; the first empty slot ends a search (there are no deletions).
+constexpr int REGION = 64;
+__device__ __forceinline__ uint64_t region_base0(uint64_t hash_key) { return splitmix(hash_key ^ 0xD1B54A32D192ED03ULL); }
+__device__ __forceinline__ uint64_t home_slot(const irm_prefix_view &ix, uint64_t base_key, int64_t d) {
     const uint64_t m = (uint64_t)ix.n_slots - 1;
-    uint64_t idx = (key >> 20) & m;
-    for (int64_t probe = 0; probe < ix.n_slots; ++probe, idx = (idx + 1) & m) {
-        const uint64_t k = *(volatile uint64_t *)slot_key(ix, idx);
-        if (k == key) return (int64_t)idx;
+    const uint64_t region = (fmix64(base_key) & m) & ~(uint64_t)(REGION - 1);
+    return (region + (uint64_t)((d - 1) & (REGION - 1))) & m;
+}
+// offset of the second probe: an odd number of regions
+__device__ __forceinline__ uint64_t region_step(uint64_t base_key) {
+    return ((fmix64(base_key ^ 0x9E3779B97F4A7C15ULL) >> 20) | 1) * REGION;
+}
+struct Probe {  // probe i of a key: home, home + rstep, then + kstep per further probe
+    uint64_t idx, kstep, m;
+    __device__ __forceinline__ Probe(const irm_prefix_view &ix, uint64_t home, uint64_t base_key, uint64_t key)
+        : idx(home), kstep((key >> 7) | 1), m((uint64_t)ix.n_slots - 1) {
+        rstep = region_step(base_key);
+    }
+    uint64_t rstep;
+    __device__ __forceinline__ void next(int64_t i) {  // from probe i to i + 1
+        idx = (idx + (i == 0 ? rstep : kstep)) & m;
+    }
+};
+
+__device__ __forceinline__ int64_t find(const irm_prefix_view &ix, uint64_t key, uint64_t home, uint64_t base_key) {
+    Probe p(ix, home, base_key, key);
+    for (int64_t probe = 0; probe < ix.n_slots; p.next(probe++)) {
+        const uint64_t k = *(volatile uint64_t *)slot_key(ix, p.idx);
+        if (k == key) return (int64_t)p.idx;
         if (k == IRM_EMPTY_KEY) return -1;
     }
     return -1;
 }
 
-__device__ __forceinline__ void insert(const irm_prefix_view &ix, uint64_t key, int64_t epoch) {
-    const uint64_t m = (uint64_t)ix.n_slots - 1;
-    uint64_t idx = (key >> 20) & m;
-    for (int64_t probe = 0; probe < ix.n_slots; ++probe, idx = (idx + 1) & m) {
-        uint64_t k = *(volatile uint64_t *)slot_key(ix, idx);
+// from the second probe on (the caller tried the home slot itself)
+__device__ __forceinline__ void insert_probe(const irm_prefix_view &ix, uint64_t key, uint64_t home,
+                                             uint64_t base_key, int64_t epoch) {
+    Probe p(ix, home, base_key, key);
+    p.next(0);
+    for (int64_t probe = 1; probe < ix.n_slots; p.next(probe++)) {
+        uint64_t k = *(volatile uint64_t *)slot_key(ix, p.idx);
         if (k == IRM_EMPTY_KEY) {
-            k = atomicCAS((unsigned long long *)slot_key(ix, idx), (unsigned long long)IRM_EMPTY_KEY,
+            k = atomicCAS((unsigned long long *)slot_key(ix, p.idx), (unsigned long long)IRM_EMPTY_KEY,
                           (unsigned long long)key);
             if (k == IRM_EMPTY_KEY) {
                 atomicAdd((unsigned long long *)&ix.counters[0], 1ULL);
@@ -110,7 +144,7 @@ __device__ __forceinline__ void insert(const irm_prefix_view &ix, uint64_t key, 
             }
         }
         if (k == key) {
-            atomicMin(slot_epoch(ix, idx), (long long)epoch);
+            atomicMin(slot_epoch(ix, p.idx), (long long)epoch);
             return;
         }
     }
@@ -258,27 +292,38 @@ __global__ void __launch_bounds__(PT) keys_kernel(irm_prefix_view ix, const uint
         }
     }
     if (!ins) return;
-    // inserts: the first probe of every key in flight at once (claim by CAS), then every epoch
-    // min at once; a key whose home slot holds another key falls back to the probe loop
-    const uint64_t m = (uint64_t)ix.n_slots - 1;
+    // the region key of each 64-depth block of the chunk: the key of the prefix ending just
+    // before it (the previous chunk's last depth for the first block, from the carry)
+    static_assert(CH % REGION == 0 && REGION % TPT == 0, "blocks align with chunks and threads");
+    __shared__ uint64_t sbase[CH / REGION];
+    constexpr int TPB = REGION / TPT;  // threads per block
+    if (threadIdx.x == 0)
+        sbase[0] = j == 0 ? region_base0(ix.hash_key) : prefix_key(carry[blockIdx.x].b, j * CH, ix.hash_key);
+    if ((threadIdx.x + 1) % TPB == 0 && (threadIdx.x + 1) / TPB < CH / REGION && nk == TPT)
+        sbase[(threadIdx.x + 1) / TPB] = k[TPT - 1];
+    __syncthreads();
+    const uint64_t bkey = sbase[threadIdx.x / TPB];
+    // inserts: the home probe of every key in flight at once (claim by CAS), then every epoch
+    // min at once; a key whose home slot holds another key goes on to its probe sequence
+    uint64_t home[TPT];
     int64_t slot[TPT];
     unsigned claimed = 0;
 #pragma unroll
     for (int q = 0; q < TPT; ++q) {
         slot[q] = -1;
         if (q < nk) {
-            const uint64_t idx = (k[q] >> 20) & m;
-            const unsigned long long old = atomicCAS((unsigned long long *)slot_key(ix, idx),
+            home[q] = home_slot(ix, bkey, d0 + q + 1);
+            const unsigned long long old = atomicCAS((unsigned long long *)slot_key(ix, home[q]),
                                                      (unsigned long long)IRM_EMPTY_KEY, (unsigned long long)k[q]);
             if (old == IRM_EMPTY_KEY) claimed++;
-            if (old == IRM_EMPTY_KEY || old == k[q]) slot[q] = (int64_t)idx;
+            if (old == IRM_EMPTY_KEY || old == k[q]) slot[q] = (int64_t)home[q];
         }
     }
 #pragma unroll
     for (int q = 0; q < TPT; ++q) {
         if (q >= nk) continue;
         if (slot[q] >= 0) atomicMin(slot_epoch(ix, slot[q]), (long long)ep);
-        else insert(ix, k[q], ep);  // collision at the home slot: linear probing (counts its own claim)
+        else insert_probe(ix, k[q], home[q], bkey, ep);  // home slot taken: the probe sequence
     }
     // slots used: one atomic per warp
     unsigned c = claimed;
@@ -302,7 +347,9 @@ __global__ void query_kernel(irm_prefix_view ix, const int64_t *__restrict__ seq
     int64_t lo = 0, hi = len, wit = -1;
     while (lo < hi) {  // largest d with a prefix of length d inserted before epoch e
         const int64_t mid = (lo + hi + 1) >> 1;
-        const int64_t s = find(ix, key[s0 + mid - 1]);
+        const int64_t blk = (mid - 1) / REGION * REGION;  // prefix length of the region key
+        const uint64_t bkey = blk == 0 ? region_base0(ix.hash_key) : key[s0 + blk - 1];
+        const int64_t s = find(ix, key[s0 + mid - 1], home_slot(ix, bkey, mid), bkey);
         const int64_t ep = s >= 0 ? *(volatile int64_t *)slot_epoch(ix, s) : INT64_MAX;
         if (ep < e) {
             lo = mid;

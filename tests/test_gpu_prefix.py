@@ -111,6 +111,37 @@ def test_prefix_match_insert_sessions():
           f"(last batch), {tree.n_prefixes} prefixes stored")
 
 
+def test_prefix_region_boundaries():
+    """The K0 table places the keys of depths 64b + 1 .. 64b + 64 of a sequence in one
+    region chosen by its prefix of length 64b, with a region step and then per-key double
+    hashing on collisions: 1,800 sequences diverging from a shared trunk at and around the
+    region boundaries (and from each other inside blocks, over a 3-letter alphabet), plus
+    duplicates and strict prefixes, all match the host radix tree exactly, batch after batch."""
+    from paper_2605_05696_b200.radix import RadixTree
+
+    rng = np.random.default_rng(64)
+    trunk = rng.integers(0, 2**32, size=5000, dtype=np.uint64).astype(np.uint32)
+    cuts = [0, 1, 50, 62, 63, 64, 65, 127, 128, 129, 1023, 1024, 1025, 2048, 4999, 5000]
+    reqs = []
+    for i in range(1800):
+        p = cuts[i % len(cuts)] if i % 3 else int(rng.integers(0, 5000))
+        tail = rng.integers(0, 3, size=int(rng.integers(0, 200))).astype(np.uint32)
+        r = np.concatenate([trunk[:p], tail])
+        if i % 97 == 5 and reqs:  # an exact repeat or a strict prefix of an earlier sequence
+            prev = reqs[int(rng.integers(0, len(reqs)))]
+            r = prev[:int(rng.integers(0, prev.size + 1))].copy()
+        reqs.append(r)
+    tree = _tree(max_prefixes=1 << 22, max_tokens=1 << 23)
+    host = RadixTree()
+    for b0 in range(0, len(reqs), 300):
+        part = reqs[b0:b0 + 300]
+        m, w = tree.match_insert(part, list(range(b0, b0 + len(part))))
+        for k, r in enumerate(part):
+            assert (m[k], w[k]) == host.match_prefix(r), b0 + k
+            host.insert(r, b0 + k)
+    tree.check()
+
+
 @pytest.mark.parametrize("case", ["long_shared", "small_alphabet"])
 def test_prefix_growth_golden(case):
     """Tiny initial capacities: the arena, the per-sequence arrays and the table
