@@ -41,8 +41,18 @@ LAYERS, CKV, KR, THETA = 27, 512, 64, 1e4
 # SMs the gather of wave i spreads over while K0 + K1 + K3 of wave i + 1 run beside it; 0 = all of them, in 4
 # retiring CTA rounds, with the front on a high-priority stream (swept: profiles/r02_k4_sms.md)
 K4_SMS = int(os.environ.get("IRM_K4_SMS", "0"))
-K4_PLACEMENT = ("K4 of wave i on all SMs in 4 retiring CTA rounds, wave i+1's front on a high-priority stream"
-                if K4_SMS == 0 else "K4 of wave i on %d SMs" % K4_SMS)
+# the sharded path's front launches NCCL kernels (the lookup all-to-alls), which need SMs that K4
+# does not hold: there K4 keeps to 112 SMs (N = 1 sweep, profiles/r02_k4_sms.md: config 5 113.0 M
+# tok/s vs 90.0 with all SMs in rounds; config 2 sharded 159.7 at 120 SMs vs 117.2)
+K4_SMS_SHARDED = int(os.environ.get("IRM_K4_SMS", "112"))
+
+
+def k4_placement(sms):
+    return ("K4 of wave i on all SMs in 4 retiring CTA rounds, wave i+1's front on a high-priority stream"
+            if sms == 0 else "K4 of wave i on %d SMs" % sms)
+
+
+K4_PLACEMENT = k4_placement(K4_SMS)
 BODY, HEADER, R_PER_WAVE = 32768, 50, 8
 CARVE = 32
 
@@ -340,7 +350,7 @@ def run_ours(args):
         pipe.capture_overlapped(k4_sms=K4_SMS)
     if overlapped and sharded and graphs:
         try:
-            pipe.capture_overlapped(k4_sms=K4_SMS, sharded=True)
+            pipe.capture_overlapped(k4_sms=K4_SMS_SHARDED, sharded=True)
         except Exception as e:  # keep the N-rank run alive on the stream pipeline (same results)
             print(f"bench: sharded graph capture failed ({type(e).__name__}: {e}); running on streams",
                   file=sys.stderr)
@@ -510,7 +520,8 @@ def run_ours(args):
                    "requests_per_step": R, "tokens_per_request": tok_per_wave // R + HEADER,
                    "layers": LAYERS, "l2": "inputs larger than L2 (1.0 GB pool, 8 GB KV out per step); "
                                            "components: L2 flushed (256 MB write) before every timed launch",
-                   "pipeline": ("two-wave overlap: %s || K0 + K1 + K3 of wave i+1" % K4_PLACEMENT
+                   "pipeline": ("two-wave overlap: %s || K0 + K1 + K3 of wave i+1"
+                                % k4_placement(K4_SMS_SHARDED if sharded else K4_SMS)
                                 + (" (CUDA graphs; sharded lookup: NCCL all-to-alls captured in the graph, peer replica fetch)"
                                    if sharded and graphs else
                                    " (streams; sharded lookup + peer replica fetch)" if sharded else " (CUDA graphs)"))
@@ -917,7 +928,7 @@ def run_config5(args):
     pipe.step_sharded(0)  # one eager wave: our kernels per wave (the graphs replay the same launches)
     launches_per_wave = ops.launch_count() - lc0
     if graphs:
-        pipe.capture_overlapped(k4_sms=K4_SMS, sharded=True)
+        pipe.capture_overlapped(k4_sms=K4_SMS_SHARDED, sharded=True)
     run_sharded(pipe, n_cold - 1, lambda i: pipe.load(*cold_dev[1 + i]), 1, graphs)
     wave = n_cold
     run_sharded(pipe, args.warmup, lambda i: pipe.load(*warm_dev[i]), wave, graphs)
@@ -957,7 +968,7 @@ def run_config5(args):
     if graphs:
         pipe.run_overlapped(n_e2e, lambda i: pipe.load(*warm_host[i]), readback=res, wave0=wave)
     else:
-        pipe.run_overlapped_sharded(n_e2e, lambda i: pipe.load(*warm_host[i]), wave0=wave, k4_sms=K4_SMS,
+        pipe.run_overlapped_sharded(n_e2e, lambda i: pipe.load(*warm_host[i]), wave0=wave, k4_sms=K4_SMS_SHARDED,
                                     after_front=lambda i, sl: res[i].copy_(pipe.slots[sl]["hit"], non_blocking=True))
     e1.record()
     torch.cuda.synchronize()
@@ -1010,7 +1021,8 @@ def run_config5(args):
                    "tokens_per_request": int(np.mean(np.diff(warm[0][1]))) + C5_HEADER, "layers": LAYERS,
                    "l2": "inputs larger than L2 (pool of %.0f GB per GPU)" % (pool.numel() * 2 / 1e9),
                    "pipeline": "two-wave overlap (%s); sharded lookup (%s all-to-alls%s) + peer replica fetch"
-                               % (K4_PLACEMENT, backend, " captured in the CUDA graphs" if graphs else ", streams"),
+                               % (k4_placement(K4_SMS_SHARDED), backend,
+                                  " captured in the CUDA graphs" if graphs else ", streams"),
                    "parallelism": f"sessions s mod G over {world} GPU(s), store sharded by fingerprint prefix"},
         "exchange": {"lookup_us_per_rank": exchange_us,
                      "lookup_note": "eager (host-launched) K3 + both all-to-alls + owner sort + replica lookup of "
@@ -1035,7 +1047,7 @@ def run_sharded(pipe, n, load, wave0, graphs, after_front=None, readback=None):
         pipe.run_overlapped(n, load, after_front=after_front, wave0=wave0, readback=readback)
     else:
         assert readback is None, "the stream pipeline reads service maps back in after_front"
-        pipe.run_overlapped_sharded(n, load, wave0=wave0, k4_sms=K4_SMS, after_front=after_front)
+        pipe.run_overlapped_sharded(n, load, wave0=wave0, k4_sms=K4_SMS_SHARDED, after_front=after_front)
 
 
 # ----------------------------------------------------------------- the reference-facing serve API
