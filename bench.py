@@ -44,7 +44,7 @@ K4_SMS = int(os.environ.get("IRM_K4_SMS", "0"))
 # the sharded path's front launches NCCL kernels (the lookup all-to-alls), which need SMs that K4
 # does not hold: there K4 keeps to 112 SMs (N = 1 sweep, profiles/r02_k4_sms.md: config 5 113.0 M
 # tok/s vs 90.0 with all SMs in rounds; config 2 sharded 159.7 at 120 SMs vs 117.2)
-K4_SMS_SHARDED = int(os.environ.get("IRM_K4_SMS", "112"))
+K4_SMS_SHARDED = int(os.environ.get("IRM_K4_SMS", "140"))
 
 
 def k4_placement(sms):
@@ -1005,6 +1005,13 @@ def run_config5(args):
     every_us = [torch.zeros_like(xt) for _ in range(world)]
     dist.all_gather(every_us, xt)
     exchange_us = [float(x.item()) for x in every_us]
+    # K4 of that re-probed wave (every chunk a hit), timed alone after an L2 flush: the roofline
+    k4_rows = int(pipe.length.sum().item()) * LAYERS
+    ng = int(pipe.groups.n_groups.item())
+    src_rows = int(pipe.groups.g_len[:ng].to(torch.int64).sum().item()) * LAYERS
+    k4_ms = timed_flushed(pipe.k4, 10)
+    k4_bytes = (k4_rows + src_rows) * (CKV + KR) * 2
+    k4_gbs = k4_bytes / (k4_ms / 1e3) / 1e9
 
     parity = {"checked": False, "why": "N > 1: the global oracle needs every rank's waves"}
     if world == 1:
@@ -1025,13 +1032,22 @@ def run_config5(args):
                                   " captured in the CUDA graphs" if graphs else ", streams"),
                    "parallelism": f"sessions s mod G over {world} GPU(s), store sharded by fingerprint prefix"},
         "exchange": {"lookup_us_per_rank": exchange_us,
-                     "lookup_note": "eager (host-launched) K3 + both all-to-alls + owner sort + replica lookup of "
-                                    "one wave (re-probe, all hits), CUDA events per rank; in the timed step the same "
-                                    "work is replayed from the front's CUDA graph",
+                     "lookup_note": "eager (host-launched) exchange of one wave (re-probe, all hits): irm_exchange_pack, "
+                                    "all-to-all, split, K3 on the owner's shard, reply, reverse all-to-all, unpack, "
+                                    "replica lookup; CUDA events per rank; in the timed step the same work is "
+                                    "replayed from the front's CUDA graph",
                      "bytes_per_lookup": sharded.last_exchange_bytes, "owner_slots": sharded.owner_slots or
                      (sharded.slots if world == 1 else min(sharded.slots, (5 * sharded.slots) // (4 * world) + 64)),
                      "query_capacity": sharded.slots, "replica_runs_fetched_all_ranks": fetched[0],
                      "replica_rows_fetched_all_ranks": fetched[1]},
+        "roofline": {"bound": "hbm", "kernel": "irm_rotate_gather_fanout (K4 fan-out)", "achieved": k4_gbs,
+                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "launch_ms": k4_ms, "algorithmic_bytes": k4_bytes, "source_rows_read": src_rows,
+                     "rows_written": k4_rows, "wave": "a served wave re-probed (every chunk a hit), rank 0",
+                     "peak_note": "the peak is MEASURED_PEAKS.json's torch copy (1:1 read:write); at this wave's "
+                                  "~0.9:1 mix K4's bulk TMA streams can move more (frac > 1 is possible)",
+                     "bytes_rule": "1152 B per distinct source row read (once per launch) + 1152 B per reattached "
+                                   "row written, x 27 layers"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo},
         "parity": parity,
         "gpu_launches": args.steps * launches_per_wave,
@@ -1109,6 +1125,10 @@ def serve_api_component(n_warm=8):
         results, row = engine.run_trace(state, trace)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
+        # a server keeps one state; here each pass builds its own, so the previous pass's device
+        # tables are released first and the caching allocator hands their blocks to the next
+        # pass instead of cudaMalloc-ing a second set while the first is still referenced
+        del state, trace
     dt = times[-1]
     n_tok = sum(r.num_tokens for r in results)
     pic = sum(r.counts[engine.ServiceClass.PIC_HIT] for r in results)

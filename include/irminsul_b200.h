@@ -312,6 +312,35 @@ int irm_copy_runs(const int64_t *src_addr, int64_t src_layer_stride, void *dst, 
 #define IRM_PEER_HANDLE_BYTES 64
 int irm_peer_export(const void *ptr, void *handle, int64_t *offset);
 int irm_peer_open(const void *handle, int64_t offset, void **ptr);
+/* K6 lookup exchange over the hash-sharded store (replaces the in-process dict
+ * of registry.py:113-140 across G GPUs; first writer = smallest order key, as
+ * engine.py:197-223 inserts in order). One wave:
+ *   irm_exchange_pack: probed query i (q_probe nullptr: all) goes to slot
+ *     owner * cap + k of send [world * cap, 4] = (fp, order, p, len), owner =
+ *     ((fp >> 32) * world) >> 32, k = its rank among this rank's queries to that
+ *     owner (query order); dest[i] = the slot, or -1 (not probed, or the bucket
+ *     is full: flags |= 1). Unused slots: order = 2^62 + rank * world * cap + slot.
+ *   (all-to-all of the send buffers: recv [world * cap, 4])
+ *   irm_exchange_split: recv -> K3 query arrays (real = order < 2^62).
+ *   (irm_store_lookup_insert on this rank's shard)
+ *   irm_exchange_reply: novel slots of writer w get rows base_row + next[w] + ...
+ *     (lengths scanned in slot order; next[w] advances; past region: flags |= 2);
+ *     e_grow[entry] = w << 40 | row; reply [world * cap, 4] = (hit, p_src,
+ *     e_grow[entry] or -1, fresh = hit on an entry >= *n_before).
+ *   (reverse all-to-all: back)
+ *   irm_exchange_unpack: back[dest[i]] -> hit / p_src / row / owner / fresh of
+ *     query i (dest -1: hit -1, row -1, owner -1).
+ * world <= 32. One CTA for pack and reply (deterministic slot order). */
+int irm_exchange_pack(const uint64_t *q_fp, const int64_t *q_order, const int64_t *q_p, const int32_t *q_len,
+                      const uint8_t *q_probe, int64_t n, int32_t world, int32_t rank, int64_t cap, int64_t *send,
+                      int64_t *dest, uint64_t *flags, irm_stream_t stream);
+int irm_exchange_split(const int64_t *recv, int64_t m, uint64_t *fp, int64_t *order, int64_t *p, int32_t *len,
+                       uint8_t *real, irm_stream_t stream);
+int irm_exchange_reply(const int64_t *recv, int32_t world, int64_t cap, const int32_t *hit, const int64_t *entry,
+                       const int64_t *p_src, const int64_t *n_before, int64_t base_row, int64_t region, int64_t *next,
+                       int64_t *e_grow, int64_t n_egrow, uint64_t *flags, int64_t *reply, irm_stream_t stream);
+int irm_exchange_unpack(const int64_t *back, const int64_t *dest, int64_t n, int64_t cap, int32_t *hit,
+                        int64_t *p_src, int64_t *row, int64_t *owner, uint8_t *fresh, irm_stream_t stream);
 /* Per-row absolute rotation (producer side of the store, registry.py:131-133
  * with rotary.py:98-108): out[i] = R(positions[i]) rows[i] for the dim-wide
  * rotary rows at rows + i*row_stride (elements). out may alias rows. fp64 rows

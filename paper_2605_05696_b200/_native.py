@@ -70,6 +70,10 @@ _SIGS = {
     "irm_copy_runs": ([P, i64, P, i64, P, P, i64, P, i32, i32, P], i32),
     "irm_peer_export": ([P, P, P], i32),
     "irm_peer_open": ([P, i64, P], i32),
+    "irm_exchange_pack": ([P, P, P, P, P, i64, i32, i32, i64, P, P, P, P], i32),
+    "irm_exchange_split": ([P, i64, P, P, P, P, P, P], i32),
+    "irm_exchange_reply": ([P, i32, i64, P, P, P, P, i64, i64, P, P, i64, P, P, P], i32),
+    "irm_exchange_unpack": ([P, P, i64, i64, P, P, P, P, P, P], i32),
     "irm_rotate_gather": ([P, i64, P, i64, i32, i32, i32, P, P, P, P, i64, P, P, i32, i32, i32, i32, P, P, i64, P],
                           i32),
     "irm_rotate_rows": ([P, i64, P, i64, i64, i32, P, P, i32, i32, i32, P], i32),

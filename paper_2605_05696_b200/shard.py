@@ -90,6 +90,7 @@ class ShardedStore:
         self.next = torch.zeros(self.world, dtype=torch.int64, device=dev)  # per-writer bump counters
         self.overflow = torch.zeros((), dtype=torch.bool, device=dev)
         self.bucket_overflow = torch.zeros((), dtype=torch.bool, device=dev)
+        self.flags = torch.zeros(1, dtype=torch.int64, device=dev)  # device path: 1 bucket full, 2 rows full
         self.last_exchange_bytes = 0
         self.fresh = None  # per query of the last call: hit on an entry this exchange created
 
@@ -105,11 +106,14 @@ class ShardedStore:
         dev = q_fp.device
         n, G = q_fp.numel(), self.world
         i64 = dict(dtype=torch.int64, device=dev)
-        probe = torch.ones(n, dtype=torch.bool, device=dev) if q_probe is None else q_probe.to(torch.bool)
         total = self.slots if self.slots is not None else max(n, 1)
         if n > total:
             raise ValueError(f"{n} queries exceed the exchange's {total} slots")
         cap = self.owner_slots or (total if G == 1 else min(total, (5 * total) // (4 * G) + 64))
+        if q_fp.is_cuda:
+            return self._lookup_insert_device(q_fp, q_order, q_p, q_len, q_probe, cap)
+        # CPU tensors (the gloo tests): the same exchange in torch ops
+        probe = torch.ones(n, dtype=torch.bool, device=dev) if q_probe is None else q_probe.to(torch.bool)
         own = torch.where(probe, owner_of(q_fp, G), torch.full_like(q_fp, G))  # bucket G: not probed
         perm = torch.argsort(own, stable=True)
         own_s = own[perm]
@@ -169,6 +173,49 @@ class ShardedStore:
         self.fresh = out_fresh
         return out_hit, out_psrc, out_row, out_owner
 
+    def _lookup_insert_device(self, q_fp, q_order, q_p, q_len, q_probe, cap):
+        """The exchange on the GPU: four native launches (irm_exchange_*) around K3 and
+        the two all-to-alls, no host synchronisation (captured whole into the
+        pipeline's CUDA graphs)."""
+        from . import _native as N
+
+        L, st = N.lib(), N.stream_ptr()
+        dev, n, G = q_fp.device, q_fp.numel(), self.world
+        m = G * cap
+        i64 = dict(dtype=torch.int64, device=dev)
+        q_fp, q_order = q_fp.contiguous(), q_order.to(torch.int64).contiguous()
+        q_p, q_len = q_p.to(torch.int64).contiguous(), q_len.to(torch.int32).contiguous()
+        probe = q_probe.to(torch.uint8).contiguous() if q_probe is not None else None
+        send = torch.empty(m, 4, **i64)
+        dest = torch.empty(n, **i64)
+        N.check(L.irm_exchange_pack(N.ptr(q_fp), N.ptr(q_order), N.ptr(q_p), N.ptr(q_len), N.ptr(probe), n, G,
+                                    self.rank, cap, N.ptr(send), N.ptr(dest), N.ptr(self.flags), st),
+                "irm_exchange_pack")
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=self.group)
+        r_fp, r_order, r_p = torch.empty(m, **i64), torch.empty(m, **i64), torch.empty(m, **i64)
+        r_len = torch.empty(m, dtype=torch.int32, device=dev)
+        r_real = torch.empty(m, dtype=torch.uint8, device=dev)
+        N.check(L.irm_exchange_split(N.ptr(recv), m, N.ptr(r_fp), N.ptr(r_order), N.ptr(r_p), N.ptr(r_len),
+                                     N.ptr(r_real), st), "irm_exchange_split")
+        n_before = self._entry_count()  # entries of this shard before the exchange (device)
+        hit, entry, p_src, _row = self.local.lookup_insert(r_fp, r_order, r_p, r_len, r_real)
+        reply = torch.empty(m, 4, **i64)
+        N.check(L.irm_exchange_reply(N.ptr(recv), G, cap, N.ptr(hit), N.ptr(entry), N.ptr(p_src), N.ptr(n_before),
+                                     self.base, self.region, N.ptr(self.next), N.ptr(self.e_grow),
+                                     self.e_grow.numel() - 1, N.ptr(self.flags), N.ptr(reply), st),
+                "irm_exchange_reply")
+        back = torch.empty_like(reply)
+        dist.all_to_all_single(back, reply, group=self.group)
+        self.last_exchange_bytes = 2 * m * 4 * 8
+        out_hit = torch.empty(n, dtype=torch.int32, device=dev)
+        out_psrc, out_row, out_owner = torch.empty(n, **i64), torch.empty(n, **i64), torch.empty(n, **i64)
+        fresh = torch.empty(n, dtype=torch.uint8, device=dev)
+        N.check(L.irm_exchange_unpack(N.ptr(back), N.ptr(dest), n, cap, N.ptr(out_hit), N.ptr(out_psrc),
+                                      N.ptr(out_row), N.ptr(out_owner), N.ptr(fresh), st), "irm_exchange_unpack")
+        self.fresh = fresh.view(torch.bool)
+        return out_hit, out_psrc, out_row, out_owner
+
     def _entry_count(self) -> torch.Tensor:
         c = getattr(self.local, "counters", None)
         if c is not None:
@@ -178,9 +225,10 @@ class ShardedStore:
     def check(self):
         """Host check (call outside timed regions): every first writer got its rows and no
         owner bucket of the exchange overflowed."""
-        if bool(self.overflow):
+        f = int(self.flags[0])
+        if bool(self.overflow) or f & 2:
             raise RuntimeError("first-writer row range of the pool is full: raise novel_rows")
-        if bool(self.bucket_overflow):
+        if bool(self.bucket_overflow) or f & 1:
             raise RuntimeError("an owner bucket of the lookup exchange overflowed: raise owner_slots")
 
 
