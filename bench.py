@@ -98,13 +98,13 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def ncu_traffic(kernel_prefix: str):
+def ncu_traffic(kernel_prefix: str, workload: str = "config2"):
     """dram__bytes_read.sum + dram__bytes_write.sum per K4 launch, from the committed
     ncu --set full capture of this same workload (profiles/ncu_traffic.json), when
     that capture is of the kernel this run's roofline names."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            d = json.load(f)
+            d = json.load(f)[workload]
         return float(d["dram_bytes_per_launch"]) if d["kernel"].startswith(kernel_prefix) else None
     except Exception:
         return None
@@ -1041,7 +1041,9 @@ def run_config5(args):
                      "query_capacity": sharded.slots, "replica_runs_fetched_all_ranks": fetched[0],
                      "replica_rows_fetched_all_ranks": fetched[1]},
         "roofline": {"bound": "hbm", "kernel": "irm_rotate_gather_fanout (K4 fan-out)", "achieved": k4_gbs,
-                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "peak": hbm, "unit": "GB/s", "frac": k4_gbs / hbm,
+                     "traffic": ncu_traffic("rotate_gather_ws_kernel" if pipe.fanout else "rotate_gather_tma", "config5"),
+                     "peak_kind": peak_kind,
                      "launch_ms": k4_ms, "algorithmic_bytes": k4_bytes, "source_rows_read": src_rows,
                      "rows_written": k4_rows, "wave": "a served wave re-probed (every chunk a hit), rank 0",
                      "peak_note": "the peak is MEASURED_PEAKS.json's torch copy (1:1 read:write); at this wave's "
