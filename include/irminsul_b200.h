@@ -83,6 +83,15 @@ int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_o
                   const uint64_t *gear, int32_t *c_start, int32_t *c_len, uint64_t *c_fp,
                   uint8_t *c_forced, int64_t *chunk_off, int64_t cap, void *ws, int64_t ws_bytes,
                   irm_stream_t stream);
+/* The same, with the Gear table given by its generating seed (ChunkerParams.gear_seed,
+ * chunking.py:42,64-66): g_t = splitmix64 output (tok & 0xFFFF) + 1 of gear_seed is
+ * computed in the kernel instead of read from a table (identical results). */
+int irm_cdc_xxh64_seeded(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_off,
+                         int32_t n_streams, const int64_t *pin_off, const int64_t *pins, int64_t n_pins,
+                         int32_t mask_exponent, int32_t min_size, int32_t max_size, int32_t marker_pinned,
+                         uint64_t gear_seed, int32_t *c_start, int32_t *c_len, uint64_t *c_fp,
+                         uint8_t *c_forced, int64_t *chunk_off, int64_t cap, void *ws, int64_t ws_bytes,
+                         irm_stream_t stream);
 
 /* ---- K2: batched xxh64 over byte spans (fingerprint.py:24-50) ----------
  * out[i] = XXH64(base + off[i], len[i] bytes, seed). Token spans: off/len x4. */

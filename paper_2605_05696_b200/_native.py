@@ -52,6 +52,7 @@ _SIGS = {
     "irm_cdc_chunk_bound": ([i64, i32, i64, i32], i64),
     "irm_cdc_workspace_bytes": ([i64, i32, i64, i32], i64),
     "irm_cdc_xxh64": ([P, i64, P, i32, P, P, i64, i32, i32, i32, i32, P, P, P, P, P, P, i64, P, i64, P], i32),
+    "irm_cdc_xxh64_seeded": ([P, i64, P, i32, P, P, i64, i32, i32, i32, i32, u64, P, P, P, P, P, i64, P, i64, P], i32),
     "irm_xxh64_spans": ([P, P, P, i64, u64, P, P], i32),
     "irm_store_reset": ([ctypes.POINTER(StoreView), P], i32),
     "irm_store_workspace_bytes": ([i64], i64),

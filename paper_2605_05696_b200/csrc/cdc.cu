@@ -38,14 +38,34 @@ struct Region {
     int32_t ends_pin;      // last token carries a marker pin
 };
 
-__global__ void gear_table_kernel(uint64_t seed, uint64_t *out) {
-    // splitmix64 (rng.py:17-24): state_i = seed + (i+1) * gamma, then mix.
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 65536) return;
+// gear[i] = splitmix64 output i + 1 of `seed` (rng.py:17-24: state_i = seed + (i+1) * gamma,
+// then mix; chunking.py:64-66). A closed form of the index, so the K1 kernels can
+// compute it instead of looking it up: ~20 integer instructions against a random
+// 8-byte L1/L2 read per token (one L1 wavefront per lane).
+__device__ __forceinline__ uint64_t gear_splitmix(uint64_t seed, uint32_t i) {
     uint64_t z = seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    out[i] = z ^ (z >> 31);
+    return z ^ (z >> 31);
+}
+
+__global__ void gear_table_kernel(uint64_t seed, uint64_t *out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 65536) return;
+    out[i] = gear_splitmix(seed, (uint32_t)i);
+}
+
+// where K1 takes g_t from: the caller's 65,536-entry table, or (SEEDED) the
+// table's generating seed
+struct GearSrc {
+    const uint64_t *table;
+    uint64_t seed;
+};
+
+template <bool SEEDED>
+__device__ __forceinline__ uint64_t gear_of(const GearSrc &gs, uint32_t tok) {
+    if constexpr (SEEDED) return gear_splitmix(gs.seed, tok & 0xFFFFu);
+    else return __ldg(gs.table + (tok & 0xFFFFu));
 }
 
 // Walk one stream's sorted pins: calls emit(start, last, ends_pin) per region.
@@ -130,8 +150,10 @@ __device__ __forceinline__ void plan_regions(const PlanArgs &a) {
 __global__ void __launch_bounds__(PLAN_BLOCK) cdc_plan_kernel(PlanArgs a) { plan_regions<PLAN_BLOCK>(a); }
 
 // One CTA per region, four warp roles pipelined over 1024-token tiles:
-//   producers (warps 3..15): windowed G_t of tile i (tokens staged by cp.async
-//                            two tiles ahead)
+//   producers (warps 0..7):  windowed G_t of tile i (lane-serial over 4 tokens per
+//                            thread + a 4-round warp scan; tokens loaded two tiles
+//                            ahead, Gear values computed from the seed or looked up
+//                            one tile ahead)
 //   chain     (warp 0):      the sequential MSB recurrence over tile i-1 -- ONLY
 //                            m_t, ~6 dependent instructions per 32 tokens
 //   cand      (warp 1):      h_t and the mask candidates of tile i-2 (parallel
@@ -139,11 +161,30 @@ __global__ void __launch_bounds__(PLAN_BLOCK) cdc_plan_kernel(PlanArgs a) { plan
 //   walker    (warp 2):      the boundary rule over the candidate words of tile i-3
 // msb(h) is decided on the high 32-bit words alone (the low words carry at
 // most 2 into them); the rare ambiguous lanes are resolved exactly in lane order.
-constexpr int RG_THREADS = 512;
+#ifndef IRM_CDC_PRODUCE
+#define IRM_CDC_PRODUCE 1  // fused-form producers: 1 = lane-serial G (4 tokens per thread), 0 = Kogge-Stone
+#endif
+#ifndef IRM_CDC_NPROD
+#define IRM_CDC_NPROD 8  // producer warps of the lane-serial form
+#endif
+constexpr int RG_THREADS = IRM_CDC_PRODUCE ? (IRM_CDC_NPROD + 4) * 32 : 512;
 constexpr int RG_TILE = 1024;                 // tokens per pipeline tile
 constexpr int RG_SUB = RG_TILE / 32;          // 32-token sub-blocks (chain steps) per tile
 constexpr int RG_PRODUCERS = RG_THREADS / 32 - 4;  // warps 0..11
-constexpr int W_WALK = RG_PRODUCERS, W_CAND = RG_PRODUCERS + 1, W_CHAIN = RG_PRODUCERS + 3;
+#ifndef IRM_CDC_ROLEMAP
+#define IRM_CDC_ROLEMAP 0
+#endif
+#if IRM_CDC_PRODUCE && IRM_CDC_ROLEMAP && IRM_CDC_NPROD == 8
+// (A/B only, slower on the B200: IRM_CDC_ROLEMAP=1 puts the three latency-bound roles of a
+// region -- chain, walker, one cand warp -- on SMSP 3 (warp id mod 4) and the producers on
+// SMSPs 0-2; the default keeps the roles on the highest warp ids)
+constexpr int W_CHAIN = 11, W_WALK = 7, W_CAND0 = 3, W_CAND1 = 10;
+__device__ __forceinline__ int producer_index(int w) { return w < 3 ? w : w < 7 ? w - 1 : w - 2; }
+#else
+constexpr int W_WALK = RG_PRODUCERS, W_CAND0 = RG_PRODUCERS + 1, W_CAND1 = RG_PRODUCERS + 2,
+              W_CHAIN = RG_PRODUCERS + 3;
+__device__ __forceinline__ int producer_index(int w) { return w; }
+#endif
 constexpr int RG_PER = (RG_SUB + RG_PRODUCERS - 1) / RG_PRODUCERS;
 
 __device__ __forceinline__ void producer_bar() {
@@ -166,14 +207,15 @@ __device__ __forceinline__ void stage_tokens(const uint32_t *__restrict__ rt, in
 
 // gear values g_t of this producer thread's tokens of a tile (the L2 lookups are issued one
 // tile ahead of their use, so their latency hides under the previous tile's scan)
+template <bool SEEDED>
 __device__ __forceinline__ void load_gear(const uint32_t *sTok, int32_t len, int32_t tile_start,
-                                          const uint64_t *__restrict__ gear, int pw, int lane,
+                                          const GearSrc &gear, int pw, int lane,
                                           uint64_t (&g)[RG_PER]) {
 #pragma unroll
     for (int q = 0; q < RG_PER; ++q) {
         const int c = pw + q * RG_PRODUCERS;
         const int32_t t = tile_start + c * 32 + lane;
-        g[q] = (c < RG_SUB && t < len) ? __ldg(gear + (sTok[c * 32 + lane] & 0xFFFFu)) : 0ULL;
+        g[q] = (c < RG_SUB && t < len) ? gear_of<SEEDED>(gear, sTok[c * 32 + lane]) : 0ULL;
     }
 }
 
@@ -225,6 +267,58 @@ __device__ __forceinline__ void produce_tile(uint64_t (&g)[RG_PER], int32_t len,
                                    : sS31[c - 1] + (sS31[c - 2] << 32);
         sGdst[c * 32 + lane] += gb << (lane + 1);
     }
+}
+
+// producers, lane-serial form (IRM_CDC_PRODUCE=1): thread p of the RG_PRODUCERS warps owns
+// tokens PT*p .. PT*p+PT-1 of a tile. Its local G over those tokens is a serial shift-add
+// (L_j = 2 L_{j-1} + g_j); the warp then scans the per-thread ends e with
+// x_i = e_i + (x_{i-1} << PT) in four shuffle rounds -- 16 threads span 64 tokens, so lane
+// 31's x is complete without any carry-in, and lanes < 15 add the carry C (G at the token
+// before the warp) shifted by their distance. About 40 integer instructions per token
+// against ~115 for a Kogge-Stone over 64-bit values in shared memory.
+constexpr int PT = RG_TILE / (RG_PRODUCERS * 32);
+static_assert(!IRM_CDC_PRODUCE || (PT * RG_PRODUCERS * 32 == RG_TILE && PT % 2 == 0), "tile split");
+
+__device__ __forceinline__ void load_tok_pt(const uint32_t *__restrict__ rt, int32_t len, int32_t tile,
+                                            int ptid, uint32_t (&tk)[PT]) {
+    const int32_t t0 = tile * RG_TILE + PT * ptid;
+#pragma unroll
+    for (int j = 0; j < PT; ++j) tk[j] = t0 + j < len ? __ldg(rt + t0 + j) : 0u;
+}
+
+template <bool SEEDED>
+__device__ __forceinline__ void gear_pt(const GearSrc &gear, const uint32_t (&tk)[PT], uint64_t (&g)[PT]) {
+#pragma unroll
+    for (int j = 0; j < PT; ++j) g[j] = gear_of<SEEDED>(gear, tk[j]);
+}
+
+// sX[2][RG_PRODUCERS]: each warp's complete G at its last token, by tile parity
+__device__ __forceinline__ void produce_tile_serial(const uint64_t (&g)[PT], int32_t tile, uint64_t *sGdst,
+                                                    uint64_t *sX, int pw, int lane, int ptid) {
+    uint64_t L[PT];
+    uint64_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+        acc = (acc << 1) + g[j];
+        L[j] = acc;
+    }
+    uint64_t x = acc;
+#pragma unroll
+    for (int d = 1; d * PT < 64; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y << (PT * d);
+    }
+    if (lane == 31) sX[(tile & 1) * RG_PRODUCERS + pw] = x;
+    producer_bar();
+    const uint64_t C = pw > 0 ? sX[(tile & 1) * RG_PRODUCERS + pw - 1]
+                     : tile > 0 ? sX[((tile - 1) & 1) * RG_PRODUCERS + RG_PRODUCERS - 1] : 0ULL;
+    if (PT * (lane + 1) < 64) x += C << (PT * (lane + 1));
+    uint64_t gp = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) gp = C;
+    ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(sGdst + PT * ptid);
+#pragma unroll
+    for (int j = 0; j < PT; j += 2)
+        dst[j / 2] = make_ulonglong2(L[j] + (gp << (j + 1)), L[j + 1] + (gp << (j + 2)));
 }
 
 // chain warp: sBm[s] = W_s, the low word of B after step s of one tile
@@ -358,97 +452,6 @@ __device__ __forceinline__ void walk_tile(const unsigned *sCand, int32_t tile_st
     }
 }
 
-__global__ void __launch_bounds__(RG_THREADS)
-cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ regions,
-                  const int64_t *__restrict__ n_regions_p, const uint64_t *__restrict__ gear,
-                  int32_t k, int32_t min_size, int32_t max_size, int32_t *__restrict__ st_start,
-                  int32_t *__restrict__ st_len, uint8_t *__restrict__ st_forced,
-                  uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count, int dbg) {
-    __shared__ uint64_t sG[3][RG_TILE];
-    __shared__ uint32_t sTok[3][RG_TILE];
-    __shared__ uint64_t sS31[RG_SUB];
-    __shared__ uint32_t sBm[2][RG_SUB];
-    __shared__ unsigned sCand[2][RG_SUB];
-    __shared__ int32_t sCount;
-    const int64_t r = blockIdx.x;
-    if (r >= *n_regions_p) return;  // uniform per CTA
-    const Region R = regions[r];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t *__restrict__ rt = tok + R.tok_begin;
-    const uint32_t mask = (1u << k) - 1;  // k <= 20: the low word of h decides
-    const int32_t t_pin = R.ends_pin ? R.len - 1 : INT32_MAX;
-    const ChunkSink sink{st_start, st_len, st_forced, R.cap_off, (int32_t)(R.tok_begin - R.stream_begin)};
-    const int ntiles = (R.len + RG_TILE - 1) / RG_TILE;
-
-    uint32_t Blo = 0, Bhi = 0;  // chain: the previous 64 MSBs
-    uint32_t Cprev_lo = 0;      // cand: B low word at the end of the previous tile
-    int32_t start = 0, nch = 0; // walker
-    // role warps take the HIGHEST warp ids: the SMSP arbiter issues
-    // highest-warp-id-first, so the chain warp is never starved by producers
-    const int pw = warp, ptid = threadIdx.x;
-    uint64_t gcur[RG_PER];  // producers: gear values of the tile being scanned
-    if (warp < W_WALK) {
-        stage_tokens(rt, R.len, 0, sTok[0], ptid);
-        stage_tokens(rt, R.len, 1, sTok[1], ptid);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");  // tile 0's tokens landed
-        producer_bar();
-        load_gear(sTok[0], R.len, 0, gear, pw, lane, gcur);
-    }
-    long long t_work = 0, t_all = clock64();
-    for (int i = 0; i <= ntiles + 2; ++i) {
-        const long long t0 = clock64();
-        if (warp == W_CHAIN) {
-            if (i >= 1 && i <= ntiles && !(dbg & 4))
-                chain_tile(sG[(i - 1) % 3], sBm[(i - 1) & 1], (i - 1) * RG_TILE, R.len, Blo, Bhi, lane);
-        } else if (warp == W_CAND || warp == W_CAND + 1) {
-            if (i >= 2 && i <= ntiles + 1)
-                cand_tile(sG[(i - 2) % 3], sBm[i & 1], sCand[i & 1], (i - 2) * RG_TILE, R.len, mask,
-                          Cprev_lo, warp - W_CAND, lane);
-        } else if (warp == W_WALK) {
-            if (i >= 3)
-                walk_tile(sCand[(i - 3) & 1], (i - 3) * RG_TILE, R.len, min_size, max_size, t_pin, start,
-                          nch, sink, lane);
-        } else if (i < ntiles && !(dbg & 2)) {
-            stage_tokens(rt, R.len, i + 2, sTok[(i + 2) % 3], ptid);  // empty group past the end
-            asm volatile("cp.async.wait_group 1;" ::: "memory");       // tile i + 1's tokens landed
-            producer_bar();
-            uint64_t gnext[RG_PER];
-            load_gear(sTok[(i + 1) % 3], R.len, (i + 1) * RG_TILE, gear, pw, lane, gnext);  // in flight
-            produce_tile(gcur, R.len, i * RG_TILE, sG[i % 3], i ? sG[(i - 1) % 3] : nullptr, sS31, pw, lane);
-#pragma unroll
-            for (int q = 0; q < RG_PER; ++q) gcur[q] = gnext[q];
-        }
-        t_work += clock64() - t0;
-        __syncthreads();
-    }
-    const long long t_loop = clock64() - t_all;
-    if (warp == W_WALK) {
-        if (start < R.len) {  // only when the region ends at the stream end
-            sink.emit(lane, nch, start, R.len - start, IRM_FORCED_STREAM_END);
-            ++nch;
-        }
-        if (lane == 0) {
-            sCount = nch;
-            r_count[r] = nch;
-        }
-    }
-    __syncthreads();
-    // fingerprints (fingerprint.py:28-30): a quad of lanes per chunk, tokens from L2
-    const uint32_t *__restrict__ sbase = tok + R.stream_begin;
-    const int64_t cap = R.cap_off;
-    const int n_chunks = sCount;
-    for (int c0 = warp * 8; c0 < n_chunks; c0 += RG_THREADS / 4) {  // warp-uniform trip count
-        const int c = c0 + (lane >> 2);
-        const bool ok = c < n_chunks;
-        const uint64_t h = xxh64_words_quad(sbase + (ok ? st_start[cap + c] : 0), ok ? st_len[cap + c] : 0,
-                                            0, lane);
-        if (ok && (lane & 3) == 0) st_fp[cap + c] = h;
-    }
-    if (dbg && (threadIdx.x & 31) == 0 && (warp >= W_WALK || warp == 0 || warp == 3) && R.len > 10000)  // IRM_CDC_DEBUG=1
-        printf("region %lld warp %d work %lld loop %lld with-hash %lld tiles %d\n", (long long)r, warp,
-               t_work, t_loop, clock64() - t_all, ntiles);
-}
-
 // walker, scalar form (split K1): the warp builds next-candidate words once per tile
 // (suffix min over lanes), then lane 0 alone walks the boundary rule with two shared
 // loads per chunk: no vote / shuffle on the per-chunk dependency chain. Same rule as
@@ -487,6 +490,132 @@ __device__ __forceinline__ void walk_tile_scalar(const unsigned *sCand, int32_t 
     }
 }
 
+#ifndef IRM_CDC_FUSED_WALK
+#define IRM_CDC_FUSED_WALK 1  // fused-form walker: 1 = lane-0 scalar (walk_tile_scalar), 0 = warp vote per chunk
+#endif
+
+template <bool SEEDED>
+__global__ void __launch_bounds__(RG_THREADS)
+cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ regions,
+                  const int64_t *__restrict__ n_regions_p, const GearSrc gear,
+                  int32_t k, int32_t min_size, int32_t max_size, int32_t *__restrict__ st_start,
+                  int32_t *__restrict__ st_len, uint8_t *__restrict__ st_forced,
+                  uint64_t *__restrict__ st_fp, int32_t *__restrict__ r_count, int dbg) {
+    __shared__ __align__(16) uint64_t sG[3][RG_TILE];
+#if IRM_CDC_PRODUCE
+    __shared__ uint64_t sX[2 * RG_PRODUCERS];
+#else
+    __shared__ uint32_t sTok[3][RG_TILE];
+    __shared__ uint64_t sS31[RG_SUB];
+#endif
+    __shared__ uint32_t sBm[2][RG_SUB];
+    __shared__ unsigned sCand[2][RG_SUB];
+    __shared__ int32_t sNext[RG_SUB + 1];
+    __shared__ int32_t sCount;
+    const int64_t r = blockIdx.x;
+    if (r >= *n_regions_p) return;  // uniform per CTA
+    const Region R = regions[r];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t *__restrict__ rt = tok + R.tok_begin;
+    const uint32_t mask = (1u << k) - 1;  // k <= 20: the low word of h decides
+    const int32_t t_pin = R.ends_pin ? R.len - 1 : INT32_MAX;
+    const ChunkSink sink{st_start, st_len, st_forced, R.cap_off, (int32_t)(R.tok_begin - R.stream_begin)};
+    const int ntiles = (R.len + RG_TILE - 1) / RG_TILE;
+
+    uint32_t Blo = 0, Bhi = 0;  // chain: the previous 64 MSBs
+    uint32_t Cprev_lo = 0;      // cand: B low word at the end of the previous tile
+    int32_t start = 0, nch = 0; // walker
+    const bool producer = warp != W_CHAIN && warp != W_WALK && warp != W_CAND0 && warp != W_CAND1;
+    const int pw = producer_index(warp), ptid = pw * 32 + lane;
+#if IRM_CDC_PRODUCE
+    // producers: gear values of tile i (gcur), of tile i + 1 in flight, tokens of tile i + 2 in flight
+    uint64_t gcur[PT];
+    uint32_t tk1[PT];
+    if (producer) {
+        uint32_t tk0[PT];
+        load_tok_pt(rt, R.len, 0, ptid, tk0);
+        load_tok_pt(rt, R.len, 1, ptid, tk1);
+        gear_pt<SEEDED>(gear, tk0, gcur);
+    }
+#else
+    uint64_t gcur[RG_PER];  // producers: gear values of the tile being scanned
+    if (producer) {
+        stage_tokens(rt, R.len, 0, sTok[0], ptid);
+        stage_tokens(rt, R.len, 1, sTok[1], ptid);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // tile 0's tokens landed
+        producer_bar();
+        load_gear<SEEDED>(sTok[0], R.len, 0, gear, pw, lane, gcur);
+    }
+#endif
+    long long t_work = 0, t_all = clock64();
+    for (int i = 0; i <= ntiles + 2; ++i) {
+        const long long t0 = clock64();
+        if (warp == W_CHAIN) {
+            if (i >= 1 && i <= ntiles && !(dbg & 4))
+                chain_tile(sG[(i - 1) % 3], sBm[(i - 1) & 1], (i - 1) * RG_TILE, R.len, Blo, Bhi, lane);
+        } else if (warp == W_CAND0 || warp == W_CAND1) {
+            if (i >= 2 && i <= ntiles + 1)
+                cand_tile(sG[(i - 2) % 3], sBm[i & 1], sCand[i & 1], (i - 2) * RG_TILE, R.len, mask,
+                          Cprev_lo, warp == W_CAND1, lane);
+        } else if (warp == W_WALK) {
+            if (i >= 3)
+#if IRM_CDC_FUSED_WALK
+                walk_tile_scalar(sCand[(i - 3) & 1], sNext, (i - 3) * RG_TILE, R.len, min_size, max_size, t_pin,
+                                 start, nch, sink, lane);
+#else
+                walk_tile(sCand[(i - 3) & 1], (i - 3) * RG_TILE, R.len, min_size, max_size, t_pin, start,
+                          nch, sink, lane);
+#endif
+        } else if (i < ntiles && !(dbg & 2)) {
+#if IRM_CDC_PRODUCE
+            uint64_t gnext[PT];
+            gear_pt<SEEDED>(gear, tk1, gnext);           // tile i + 1 (table form: lookups in flight)
+            load_tok_pt(rt, R.len, i + 2, ptid, tk1);    // tile i + 2
+            produce_tile_serial(gcur, i, sG[i % 3], sX, pw, lane, ptid);
+#pragma unroll
+            for (int q = 0; q < PT; ++q) gcur[q] = gnext[q];
+#else
+            stage_tokens(rt, R.len, i + 2, sTok[(i + 2) % 3], ptid);  // empty group past the end
+            asm volatile("cp.async.wait_group 1;" ::: "memory");       // tile i + 1's tokens landed
+            producer_bar();
+            uint64_t gnext[RG_PER];
+            load_gear<SEEDED>(sTok[(i + 1) % 3], R.len, (i + 1) * RG_TILE, gear, pw, lane, gnext);  // in flight
+            produce_tile(gcur, R.len, i * RG_TILE, sG[i % 3], i ? sG[(i - 1) % 3] : nullptr, sS31, pw, lane);
+#pragma unroll
+            for (int q = 0; q < RG_PER; ++q) gcur[q] = gnext[q];
+#endif
+        }
+        t_work += clock64() - t0;
+        __syncthreads();
+    }
+    const long long t_loop = clock64() - t_all;
+    if (warp == W_WALK) {
+        if (start < R.len) {  // only when the region ends at the stream end
+            sink.emit(lane, nch, start, R.len - start, IRM_FORCED_STREAM_END);
+            ++nch;
+        }
+        if (lane == 0) {
+            sCount = nch;
+            r_count[r] = nch;
+        }
+    }
+    __syncthreads();
+    // fingerprints (fingerprint.py:28-30): a quad of lanes per chunk, tokens from L2
+    const uint32_t *__restrict__ sbase = tok + R.stream_begin;
+    const int64_t cap = R.cap_off;
+    const int n_chunks = sCount;
+    for (int c0 = warp * 8; c0 < n_chunks; c0 += RG_THREADS / 4) {  // warp-uniform trip count
+        const int c = c0 + (lane >> 2);
+        const bool ok = c < n_chunks;
+        const uint64_t h = xxh64_words_quad(sbase + (ok ? st_start[cap + c] : 0), ok ? st_len[cap + c] : 0,
+                                            0, lane);
+        if (ok && (lane & 3) == 0) st_fp[cap + c] = h;
+    }
+    if (dbg && (threadIdx.x & 31) == 0 && (!producer || pw == 0 || pw == 3) && R.len > 10000)  // IRM_CDC_DEBUG=1
+        printf("region %lld warp %d work %lld loop %lld with-hash %lld tiles %d\n", (long long)r, warp,
+               t_work, t_loop, clock64() - t_all, ntiles);
+}
+
 // ---------------------------------------------------------------- K1 split form
 // G_t is windowed (64 tokens), so it need not sit on the per-region critical path:
 // gear_window_kernel computes it for the whole flat token array on every SM
@@ -499,8 +628,9 @@ constexpr int GW_PER = 8;                              // sub-blocks per warp, l
 constexpr int GW_SUB = GW_THREADS / 32 * GW_PER - 2;   // output sub-blocks per CTA (+2 halo in front)
 
 // (its last CTA plans the regions meanwhile: one launch instead of two)
+template <bool SEEDED>
 __global__ void __launch_bounds__(GW_THREADS)
-gear_window_kernel(const uint32_t *__restrict__ tok, int64_t n, const uint64_t *__restrict__ gear,
+gear_window_kernel(const uint32_t *__restrict__ tok, int64_t n, const GearSrc gear,
                    uint64_t *__restrict__ G, PlanArgs plan) {
     if (blockIdx.x == gridDim.x - 1) {
         plan_regions<GW_THREADS>(plan);
@@ -523,7 +653,7 @@ gear_window_kernel(const uint32_t *__restrict__ tok, int64_t n, const uint64_t *
 #pragma unroll
         for (int u = 0; u < GW_PER; ++u) {
             const int64_t t = base + 32 * (warp * GW_PER + u - 2) + lane;
-            g[u] = (t >= 0 && t < n) ? __ldg(gear + (tk[u] & 0xFFFFu)) : 0ULL;
+            g[u] = (t >= 0 && t < n) ? gear_of<SEEDED>(gear, tk[u]) : 0ULL;
         }
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -803,20 +933,20 @@ extern "C" int64_t irm_cdc_workspace_bytes(int64_t n_tokens, int32_t n_streams, 
     return carve_cdc_ws(nullptr, n_tokens, n_streams, n_pins, min_size).bytes;
 }
 
-extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_off,
-                             int32_t n_streams, const int64_t *pin_off, const int64_t *pins,
-                             int64_t n_pins, int32_t mask_exponent, int32_t min_size,
-                             int32_t max_size, int32_t marker_pinned, const uint64_t *gear,
-                             int32_t *c_start, int32_t *c_len, uint64_t *c_fp, uint8_t *c_forced,
-                             int64_t *chunk_off, int64_t cap, void *ws, int64_t ws_bytes,
-                             irm_stream_t stream) {
+static int cdc_xxh64_impl(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_off,
+                          int32_t n_streams, const int64_t *pin_off, const int64_t *pins,
+                          int64_t n_pins, int32_t mask_exponent, int32_t min_size,
+                          int32_t max_size, int32_t marker_pinned, const GearSrc gear, bool seeded,
+                          int32_t *c_start, int32_t *c_len, uint64_t *c_fp, uint8_t *c_forced,
+                          int64_t *chunk_off, int64_t cap, void *ws, int64_t ws_bytes,
+                          irm_stream_t stream) {
     // ChunkerParams validation, chunking.py:45-49
     IRM_REQUIRE(mask_exponent >= 1 && mask_exponent <= 20, "mask_exponent must be in [1, 20]");
     IRM_REQUIRE(min_size >= 1 && min_size < max_size, "need 1 <= min_size < max_size");
     IRM_REQUIRE(n_streams >= 0 && n_tokens >= 0 && n_pins >= 0, "negative sizes");
     IRM_REQUIRE(n_tokens < (int64_t)1 << 40, "n_tokens too large");
     IRM_REQUIRE(stream_off && chunk_off, "null stream_off/chunk_off");
-    IRM_REQUIRE(n_tokens == 0 || (tok && gear), "null tok/gear");
+    IRM_REQUIRE(n_tokens == 0 || (tok && (seeded || gear.table)), "null tok/gear");
     if (marker_pinned && n_pins > 0) IRM_REQUIRE(pin_off && pins, "null pins");
     const int64_t bound = irm_cdc_chunk_bound(n_tokens, n_streams, marker_pinned ? n_pins : 0,
                                               min_size);
@@ -847,13 +977,14 @@ extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_
     if (v1) {
         cdc_plan_kernel<<<1, PLAN_BLOCK, 0, st>>>(plan);
         IRM_LAUNCH_CHECK();
-        cdc_region_kernel<<<(unsigned)rmax, RG_THREADS, 0, st>>>(
+        (seeded ? cdc_region_kernel<true> : cdc_region_kernel<false>)<<<(unsigned)rmax, RG_THREADS, 0, st>>>(
             tok, w.regions, w.n_regions, gear, mask_exponent, min_size, max_size, w.st_start, w.st_len,
             w.st_forced, w.st_fp, w.r_count, dbg);
     } else {
         const int64_t gw_tiles = (n_tokens + GW_SUB * 32 - 1) / (GW_SUB * 32);
-        gear_window_kernel<<<(unsigned)(std::max<int64_t>(1, std::min<int64_t>(gw_tiles, (int64_t)sm_count() * 8)) + 1),
-                             GW_THREADS, 0, st>>>(tok, n_tokens, gear, w.G, plan);
+        (seeded ? gear_window_kernel<true> : gear_window_kernel<false>)
+            <<<(unsigned)(std::max<int64_t>(1, std::min<int64_t>(gw_tiles, (int64_t)sm_count() * 8)) + 1),
+               GW_THREADS, 0, st>>>(tok, n_tokens, gear, w.G, plan);
         IRM_LAUNCH_CHECK();
         cdc_region_split_kernel<<<(unsigned)rmax, RG2_THREADS, 0, st>>>(
             tok, w.G, w.regions, w.n_regions, mask_exponent, min_size, max_size, w.st_start, w.st_len,
@@ -875,6 +1006,30 @@ extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_
     }
     IRM_LAUNCH_CHECK();
     return IRM_OK;
+}
+
+extern "C" int irm_cdc_xxh64(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_off,
+                             int32_t n_streams, const int64_t *pin_off, const int64_t *pins,
+                             int64_t n_pins, int32_t mask_exponent, int32_t min_size,
+                             int32_t max_size, int32_t marker_pinned, const uint64_t *gear,
+                             int32_t *c_start, int32_t *c_len, uint64_t *c_fp, uint8_t *c_forced,
+                             int64_t *chunk_off, int64_t cap, void *ws, int64_t ws_bytes,
+                             irm_stream_t stream) {
+    return cdc_xxh64_impl(tok, n_tokens, stream_off, n_streams, pin_off, pins, n_pins, mask_exponent, min_size,
+                          max_size, marker_pinned, GearSrc{gear, 0}, false, c_start, c_len, c_fp, c_forced,
+                          chunk_off, cap, ws, ws_bytes, stream);
+}
+
+extern "C" int irm_cdc_xxh64_seeded(const uint32_t *tok, int64_t n_tokens, const int64_t *stream_off,
+                                    int32_t n_streams, const int64_t *pin_off, const int64_t *pins,
+                                    int64_t n_pins, int32_t mask_exponent, int32_t min_size,
+                                    int32_t max_size, int32_t marker_pinned, uint64_t gear_seed,
+                                    int32_t *c_start, int32_t *c_len, uint64_t *c_fp, uint8_t *c_forced,
+                                    int64_t *chunk_off, int64_t cap, void *ws, int64_t ws_bytes,
+                                    irm_stream_t stream) {
+    return cdc_xxh64_impl(tok, n_tokens, stream_off, n_streams, pin_off, pins, n_pins, mask_exponent, min_size,
+                          max_size, marker_pinned, GearSrc{nullptr, gear_seed}, true, c_start, c_len, c_fp,
+                          c_forced, chunk_off, cap, ws, ws_bytes, stream);
 }
 
 extern "C" int irm_xxh64_spans(const uint8_t *base, const int64_t *off, const int64_t *len,

@@ -116,11 +116,15 @@ def cdc_xxh64(tok: torch.Tensor, stream_off: torch.Tensor, pin_off: torch.Tensor
               pins: torch.Tensor | None, mask_exponent: int = 7, min_size: int = 32,
               max_size: int = 512, marker_pinned: bool = True,
               gear_seed: int = DEFAULT_GEAR_SEED, ws: CdcWorkspace | None = None,
-              n_tokens: int | None = None, n_pins: int | None = None) -> ChunkTable:
+              n_tokens: int | None = None, n_pins: int | None = None,
+              gear_from_table: bool = False) -> ChunkTable:
     """Batched CDC + fingerprints over CSR token streams (K1).
 
     ``tok`` int32 [n_tokens]; ``stream_off`` int64 [n_streams+1]; ``pins``
     int64 sorted per stream (CSR ``pin_off``). Outputs stay on the device.
+    The Gear values are computed from ``gear_seed`` in the kernel
+    (``irm_cdc_xxh64_seeded``); ``gear_from_table`` reads the device table
+    instead (``irm_cdc_xxh64``, same results).
     """
     ws = ws or _DEFAULT_CDC_WS
     n_streams = stream_off.numel() - 1
@@ -133,11 +137,14 @@ def cdc_xxh64(tok: torch.Tensor, stream_off: torch.Tensor, pin_off: torch.Tensor
     wsbuf, (st, ln, fp, fo), cap = ws.get(n_tokens, n_streams, n_pins if marker_pinned else 0,
                                           max(min_size, 1))
     chunk_off = torch.empty(n_streams + 1, dtype=torch.int64, device=tok.device)
-    rc = N.lib().irm_cdc_xxh64(
-        N.ptr(tok), n_tokens, N.ptr(stream_off), n_streams, N.ptr(pin_off), N.ptr(pins), n_pins,
-        mask_exponent, min_size, max_size, int(bool(marker_pinned)), N.ptr(gear_table_device(gear_seed)),
-        N.ptr(st), N.ptr(ln), N.ptr(fp), N.ptr(fo), N.ptr(chunk_off), cap, N.ptr(wsbuf),
-        wsbuf.numel(), N.stream_ptr())
+    if gear_from_table:
+        fn, gear = N.lib().irm_cdc_xxh64, N.ptr(gear_table_device(gear_seed))
+    else:
+        fn, gear = N.lib().irm_cdc_xxh64_seeded, gear_seed & (2**64 - 1)
+    rc = fn(N.ptr(tok), n_tokens, N.ptr(stream_off), n_streams, N.ptr(pin_off), N.ptr(pins), n_pins,
+            mask_exponent, min_size, max_size, int(bool(marker_pinned)), gear,
+            N.ptr(st), N.ptr(ln), N.ptr(fp), N.ptr(fo), N.ptr(chunk_off), cap, N.ptr(wsbuf),
+            wsbuf.numel(), N.stream_ptr())
     N.check(rc, "irm_cdc_xxh64")
     return ChunkTable(st, ln, fp, fo, chunk_off)
 

@@ -10,17 +10,24 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=["auto", "fused", "split"])
+@pytest.fixture(scope="module", params=["auto", "fused", "split", "fused-table", "split-table"])
 def pkg(request):
-    """Both K1 forms (IRM_CDC_FORM, read on every call) and the size-based default."""
+    """Both K1 forms (IRM_CDC_FORM, read on every call) and the size-based default, with
+    the Gear values computed from the seed (default) or read from the device table."""
+    import functools
     import os
 
     from paper_2605_05696_b200 import chunking, fingerprint, ops
 
     os.environ.pop("IRM_CDC_FORM", None)
-    if request.param != "auto":
-        os.environ["IRM_CDC_FORM"] = request.param
+    form, _, table = request.param.partition("-")
+    if form != "auto":
+        os.environ["IRM_CDC_FORM"] = form
+    orig = ops.cdc_xxh64
+    if table:
+        ops.cdc_xxh64 = functools.partial(orig, gear_from_table=True)
     yield chunking, fingerprint, ops
+    ops.cdc_xxh64 = orig
     os.environ.pop("IRM_CDC_FORM", None)
 
 

@@ -1,6 +1,7 @@
 """K1 timing: irm_cdc_xxh64 over n_streams random streams, eager launches between
 CUDA events (v1 = IRM_CDC_FORM=fused, v2 = split; the library reads it per call, so both forms time in one
-process). Usage: python tools/k1_bench.py [n_streams n_tok ...]"""
+process; t1 / t2 = the same forms reading the Gear table instead of computing it from the seed).
+Usage: python tools/k1_bench.py [n_streams n_tok ...]"""
 
 import os
 import sys
@@ -18,10 +19,13 @@ def time_k1(n_streams, n_tok, reps=int(os.environ.get("K1_REPS", "20")), forms=o
                            .view(np.int32)).cuda()
     off = torch.arange(0, (n_streams + 1) * n_tok, n_tok, dtype=torch.int64, device="cuda")
     ws = ops.CdcWorkspace()
-    run = lambda: ops.cdc_xxh64(tok, off, None, None, 7, 32, 512, True, ws=ws, n_tokens=tok.numel())
+    table = [False]
+    run = lambda: ops.cdc_xxh64(tok, off, None, None, 7, 32, 512, True, ws=ws, n_tokens=tok.numel(),
+                                gear_from_table=table[0])
     out = {}
     for form in forms.split(","):
-        os.environ["IRM_CDC_FORM"] = {"v1": "fused", "v2": "split"}[form]
+        os.environ["IRM_CDC_FORM"] = {"1": "fused", "2": "split"}[form[1]]
+        table[0] = form[0] == "t"
         t = run()
         torch.cuda.synchronize()
         ref = (t.start.clone(), t.fp.clone(), int(t.chunk_off[-1].item()))
@@ -33,9 +37,11 @@ def time_k1(n_streams, n_tok, reps=int(os.environ.get("K1_REPS", "20")), forms=o
         torch.cuda.synchronize()
         out[form] = (a.elapsed_time(b) / reps, ref)
     same = None
-    if "v1" in out and "v2" in out:
-        (_, r1), (_, r2) = out["v1"], out["v2"]
-        same = r1[2] == r2[2] and torch.equal(r1[0][:r1[2]], r2[0][:r2[2]]) and torch.equal(r1[1][:r1[2]], r2[1][:r2[2]])
+    if len(out) > 1:
+        same = True
+        (_, r1) = next(iter(out.values()))
+        for _, r2 in out.values():
+            same &= r1[2] == r2[2] and torch.equal(r1[0][:r1[2]], r2[0][:r2[2]]) and torch.equal(r1[1][:r1[2]], r2[1][:r2[2]])
     for form in out:
         ms = out[form][0]
         print(f"{n_streams:4d} x {n_tok:6d} {form}: {ms * 1e3:8.1f} us  {n_streams * n_tok / ms / 1e6:8.2f} G tok/s"
