@@ -167,24 +167,20 @@ __global__ void __launch_bounds__(PLAN_BLOCK) cdc_plan_kernel(PlanArgs a) { plan
 #ifndef IRM_CDC_NPROD
 #define IRM_CDC_NPROD 8  // producer warps of the lane-serial form
 #endif
-constexpr int RG_THREADS = IRM_CDC_PRODUCE ? (IRM_CDC_NPROD + 4) * 32 : 512;
+#ifndef IRM_CDC_HASHERS
+// warps fingerprinting, inside the tile loop, the chunks the walker emitted one tile earlier.
+// 0 (default): measured slower at 1, 2 and 4 (296 x 32K: 97 -> 150-207 us) -- a quad's XXH64
+// walks its chunk by dependent L2 round trips, which stretch the lock-step tile period; the
+// tail after the loop hashes every chunk of the region with all warps at once instead
+#define IRM_CDC_HASHERS 0
+#endif
+constexpr int RG_HASHERS = IRM_CDC_PRODUCE ? IRM_CDC_HASHERS : 0;
+constexpr int RG_THREADS = IRM_CDC_PRODUCE ? (IRM_CDC_NPROD + 4 + RG_HASHERS) * 32 : 512;
 constexpr int RG_TILE = 1024;                 // tokens per pipeline tile
 constexpr int RG_SUB = RG_TILE / 32;          // 32-token sub-blocks (chain steps) per tile
-constexpr int RG_PRODUCERS = RG_THREADS / 32 - 4;  // warps 0..11
-#ifndef IRM_CDC_ROLEMAP
-#define IRM_CDC_ROLEMAP 0
-#endif
-#if IRM_CDC_PRODUCE && IRM_CDC_ROLEMAP && IRM_CDC_NPROD == 8
-// (A/B only, slower on the B200: IRM_CDC_ROLEMAP=1 puts the three latency-bound roles of a
-// region -- chain, walker, one cand warp -- on SMSP 3 (warp id mod 4) and the producers on
-// SMSPs 0-2; the default keeps the roles on the highest warp ids)
-constexpr int W_CHAIN = 11, W_WALK = 7, W_CAND0 = 3, W_CAND1 = 10;
-__device__ __forceinline__ int producer_index(int w) { return w < 3 ? w : w < 7 ? w - 1 : w - 2; }
-#else
+constexpr int RG_PRODUCERS = RG_THREADS / 32 - 4 - RG_HASHERS;  // warps 0 .. RG_PRODUCERS - 1
 constexpr int W_WALK = RG_PRODUCERS, W_CAND0 = RG_PRODUCERS + 1, W_CAND1 = RG_PRODUCERS + 2,
-              W_CHAIN = RG_PRODUCERS + 3;
-__device__ __forceinline__ int producer_index(int w) { return w; }
-#endif
+              W_CHAIN = RG_PRODUCERS + 3, W_HASH = RG_PRODUCERS + 4;
 constexpr int RG_PER = (RG_SUB + RG_PRODUCERS - 1) / RG_PRODUCERS;
 
 __device__ __forceinline__ void producer_bar() {
@@ -511,6 +507,7 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
     __shared__ uint32_t sBm[2][RG_SUB];
     __shared__ unsigned sCand[2][RG_SUB];
     __shared__ int32_t sNext[RG_SUB + 1];
+    __shared__ int32_t sEmit[2];  // chunks emitted by the walker up to iteration i (by parity)
     __shared__ int32_t sCount;
     const int64_t r = blockIdx.x;
     if (r >= *n_regions_p) return;  // uniform per CTA
@@ -525,8 +522,12 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
     uint32_t Blo = 0, Bhi = 0;  // chain: the previous 64 MSBs
     uint32_t Cprev_lo = 0;      // cand: B low word at the end of the previous tile
     int32_t start = 0, nch = 0; // walker
-    const bool producer = warp != W_CHAIN && warp != W_WALK && warp != W_CAND0 && warp != W_CAND1;
-    const int pw = producer_index(warp), ptid = pw * 32 + lane;
+    // role warps take the highest warp ids
+    const bool producer = warp < RG_PRODUCERS;
+    const int pw = warp, ptid = threadIdx.x;
+    int32_t hashed = 0;  // hashers: chunks [0, hashed) fingerprinted
+    if (threadIdx.x == 0) sEmit[0] = sEmit[1] = 0;
+    __syncthreads();
 #if IRM_CDC_PRODUCE
     // producers: gear values of tile i (gcur), of tile i + 1 in flight, tokens of tile i + 2 in flight
     uint64_t gcur[PT];
@@ -558,7 +559,7 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
                 cand_tile(sG[(i - 2) % 3], sBm[i & 1], sCand[i & 1], (i - 2) * RG_TILE, R.len, mask,
                           Cprev_lo, warp == W_CAND1, lane);
         } else if (warp == W_WALK) {
-            if (i >= 3)
+            if (i >= 3) {
 #if IRM_CDC_FUSED_WALK
                 walk_tile_scalar(sCand[(i - 3) & 1], sNext, (i - 3) * RG_TILE, R.len, min_size, max_size, t_pin,
                                  start, nch, sink, lane);
@@ -566,6 +567,21 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
                 walk_tile(sCand[(i - 3) & 1], (i - 3) * RG_TILE, R.len, min_size, max_size, t_pin, start,
                           nch, sink, lane);
 #endif
+                if (lane == 0) sEmit[i & 1] = nch;
+            }
+        } else if (warp >= W_HASH) {
+            // the chunks emitted up to iteration i - 1 (their (start, len) were stored before the
+            // barrier that closed it); tokens from L2, a quad of lanes per chunk
+            const int32_t upto = sEmit[(i - 1) & 1];
+            const uint32_t *__restrict__ sbase = tok + R.stream_begin;
+            for (int c0 = hashed + (warp - W_HASH) * 8; c0 < upto; c0 += RG_HASHERS * 8) {  // warp-uniform
+                const int c = c0 + (lane >> 2);
+                const bool ok = c < upto;
+                const uint64_t h = xxh64_words_quad(sbase + (ok ? st_start[R.cap_off + c] : 0),
+                                                    ok ? st_len[R.cap_off + c] : 0, 0, lane);
+                if (ok && (lane & 3) == 0) st_fp[R.cap_off + c] = h;
+            }
+            hashed = upto;
         } else if (i < ntiles && !(dbg & 2)) {
 #if IRM_CDC_PRODUCE
             uint64_t gnext[PT];
@@ -600,11 +616,13 @@ cdc_region_kernel(const uint32_t *__restrict__ tok, const Region *__restrict__ r
         }
     }
     __syncthreads();
-    // fingerprints (fingerprint.py:28-30): a quad of lanes per chunk, tokens from L2
+    // fingerprints (fingerprint.py:28-30) of the chunks the hashers have not taken: a quad of
+    // lanes per chunk, tokens from L2
     const uint32_t *__restrict__ sbase = tok + R.stream_begin;
     const int64_t cap = R.cap_off;
     const int n_chunks = sCount;
-    for (int c0 = warp * 8; c0 < n_chunks; c0 += RG_THREADS / 4) {  // warp-uniform trip count
+    const int first = RG_HASHERS ? sEmit[(ntiles + 1) & 1] : 0;
+    for (int c0 = first + warp * 8; c0 < n_chunks; c0 += RG_THREADS / 4) {  // warp-uniform trip count
         const int c = c0 + (lane >> 2);
         const bool ok = c < n_chunks;
         const uint64_t h = xxh64_words_quad(sbase + (ok ? st_start[cap + c] : 0), ok ? st_len[cap + c] : 0,
@@ -774,25 +792,29 @@ cdc_region_split_kernel(const uint32_t *__restrict__ tok, const uint64_t *__rest
 // folded in; CTA 0 publishes chunk_off).
 constexpr int HC_THREADS = 256;
 
+// r_out_g == nullptr: at most HC_THREADS regions, every CTA scans their counts itself;
+// otherwise the region offsets come from cdc_offsets_kernel (r_out_g, chunk_off written).
 __global__ void __launch_bounds__(HC_THREADS)
 cdc_hash_compact_kernel(const uint32_t *__restrict__ tok, const int64_t *__restrict__ n_regions_p,
                         const Region *__restrict__ regions, const int32_t *__restrict__ r_count,
                         const int64_t *__restrict__ r_first, int32_t n_streams, int64_t *__restrict__ chunk_off,
                         const int32_t *__restrict__ st_start, const int32_t *__restrict__ st_len,
                         const uint8_t *__restrict__ st_forced, int32_t *__restrict__ c_start,
-                        int32_t *__restrict__ c_len, uint64_t *__restrict__ c_fp, uint8_t *__restrict__ c_forced) {
+                        int32_t *__restrict__ c_len, uint64_t *__restrict__ c_fp, uint8_t *__restrict__ c_forced,
+                        const int64_t *__restrict__ r_out_g) {
     __shared__ int64_t sScan[HC_THREADS / 32];
-    __shared__ int64_t r_out[HC_THREADS + 1];
-    const int64_t nr = *n_regions_p;  // <= HC_THREADS (host-checked bound)
-    {
+    __shared__ int64_t r_out_s[HC_THREADS + 1];
+    const int64_t nr = *n_regions_p;
+    const int64_t *r_out = r_out_g ? r_out_g : r_out_s;
+    if (!r_out_g) {  // nr <= HC_THREADS (host-checked bound)
         const int64_t c = threadIdx.x < nr ? r_count[threadIdx.x] : 0;
         int64_t tot;
         const int64_t ex = block_exclusive_scan<HC_THREADS>(c, &tot, sScan);
-        if (threadIdx.x < nr) r_out[threadIdx.x] = ex;
-        if (threadIdx.x == 0) r_out[nr] = tot;
+        if (threadIdx.x < nr) r_out_s[threadIdx.x] = ex;
+        if (threadIdx.x == 0) r_out_s[nr] = tot;
         __syncthreads();
         if (blockIdx.x == 0)
-            for (int32_t s = threadIdx.x; s <= n_streams; s += HC_THREADS) chunk_off[s] = r_out[r_first[s]];
+            for (int32_t s = threadIdx.x; s <= n_streams; s += HC_THREADS) chunk_off[s] = r_out_s[r_first[s]];
     }
     const int64_t total = r_out[nr];
     const int lane = threadIdx.x & 31;
@@ -973,7 +995,7 @@ static int cdc_xxh64_impl(const uint32_t *tok, int64_t n_tokens, const int64_t *
     // flight hide its latency) and "split" (G on every SM first, hashing on every SM after;
     // shortest critical path when a few long regions leave most SMs idle)
     const char *form = getenv("IRM_CDC_FORM");
-    const bool v1 = (form ? strcmp(form, "fused") == 0 : rmax >= sm_count()) || rmax > HC_THREADS;
+    const bool v1 = form ? strcmp(form, "fused") == 0 : rmax >= sm_count();
     if (v1) {
         cdc_plan_kernel<<<1, PLAN_BLOCK, 0, st>>>(plan);
         IRM_LAUNCH_CHECK();
@@ -999,10 +1021,16 @@ static int cdc_xxh64_impl(const uint32_t *tok, int64_t n_tokens, const int64_t *
             w.n_regions, w.regions, w.r_count, w.r_out, w.st_start, w.st_len, w.st_forced, w.st_fp,
             c_start, c_len, c_fp, c_forced);
     } else {
+        const bool many = rmax > HC_THREADS;
+        if (many) {
+            cdc_offsets_kernel<<<1, PLAN_BLOCK, 0, st>>>(w.n_regions, w.r_count, w.r_out, w.r_first, n_streams,
+                                                         chunk_off);
+            IRM_LAUNCH_CHECK();
+        }
         const int64_t blocks = std::min<int64_t>((bound + 63) / 64, (int64_t)sm_count() * 8);
         cdc_hash_compact_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), HC_THREADS, 0, st>>>(
             tok, w.n_regions, w.regions, w.r_count, w.r_first, n_streams, chunk_off, w.st_start, w.st_len,
-            w.st_forced, c_start, c_len, c_fp, c_forced);
+            w.st_forced, c_start, c_len, c_fp, c_forced, many ? w.r_out : nullptr);
     }
     IRM_LAUNCH_CHECK();
     return IRM_OK;
