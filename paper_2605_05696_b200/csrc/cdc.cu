@@ -317,6 +317,10 @@ __device__ __forceinline__ void produce_tile_serial(const uint64_t (&g)[PT], int
         dst[j / 2] = make_ulonglong2(L[j] + (gp << (j + 1)), L[j + 1] + (gp << (j + 2)));
 }
 
+#ifndef IRM_CDC_CHAIN_LEAN
+#define IRM_CDC_CHAIN_LEAN 1
+#endif
+
 // chain warp: sBm[s] = W_s, the low word of B after step s of one tile
 // (bit 31-i = m_i of the step's token i). Lane L handles token j = 31 - L, so
 // the ballot itself is the bit-reversed word and the loop-carried path is
@@ -334,6 +338,30 @@ __device__ __forceinline__ void chain_tile(const uint64_t *sG, uint32_t *sBm, in
     // G's high words are read CH_AHEAD steps ahead: the producers keep shared memory busy,
     // so one step of lead does not cover the load latency
     constexpr int CH_AHEAD = 4;
+#if IRM_CDC_CHAIN_LEAN
+    // lean step (~9 issue slots): 32-bit loads of G's high word only; ambiguity as bit 31 of
+    // an OR of (hs + 2) ^ hs -- adding the pending carry (<= 2) flips bit 31 exactly at a carry
+    // boundary; lane 0 stores W_s (no per-step select)
+    const uint32_t *sGhi = reinterpret_cast<const uint32_t *>(sG) + 1;
+    uint32_t amb_acc = 0;
+    uint32_t Gq[CH_AHEAD];
+#pragma unroll
+    for (int a = 0; a < CH_AHEAD; ++a) Gq[a] = a < nsteps ? sGhi[2 * (a * 32 + j)] : 0u;
+#pragma unroll CH_AHEAD
+    for (int s = 0; s < nsteps; ++s) {
+        const uint32_t Ghi = Gq[0];
+#pragma unroll
+        for (int a = 0; a + 1 < CH_AHEAD; ++a) Gq[a] = Gq[a + 1];
+        Gq[CH_AHEAD - 1] = s + CH_AHEAD < nsteps ? sGhi[2 * ((s + CH_AHEAD) * 32 + j)] : 0u;
+        const uint32_t hs = Ghi + __funnelshift_l(Blo, Bhi, j);  // high word of h, carry c in {0,1,2} pending
+        const unsigned W = __ballot_sync(0xffffffffu, (int32_t)hs < 0);
+        amb_acc |= (hs + 2u) ^ hs;  // (past-the-end lanes may trigger a harmless redo)
+        if (lane == 0) sBm[s] = W;
+        Bhi = Blo;
+        Blo = W;
+    }
+    amb = (int32_t)amb_acc < 0;
+#else
     uint32_t Gq[CH_AHEAD];
 #pragma unroll
     for (int a = 0; a < CH_AHEAD; ++a) Gq[a] = a < nsteps ? (uint32_t)(sG[a * 32 + j] >> 32) : 0u;
@@ -350,6 +378,7 @@ __device__ __forceinline__ void chain_tile(const uint64_t *sG, uint32_t *sBm, in
         Bhi = Blo;
         Blo = W;
     }
+#endif
     if (__any_sync(0xffffffffu, amb)) {  // rare: redo the tile with exact 64-bit arithmetic, lanes in token order
         Blo = Blo0;
         Bhi = Bhi0;
@@ -375,8 +404,14 @@ __device__ __forceinline__ void chain_tile(const uint64_t *sG, uint32_t *sBm, in
             Bhi = Blo;
             Blo = W;
         }
+#if IRM_CDC_CHAIN_LEAN
+        __syncwarp();
+        if (lane < nsteps) sBm[lane] = myW;
+#endif
     }
+#if !IRM_CDC_CHAIN_LEAN
     sBm[lane] = myW;
+#endif
 }
 
 // cand warp: candidate words ((h & mask) == 0, chunking.py:121) of one tile.
