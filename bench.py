@@ -1220,7 +1220,10 @@ def cdc_wide_component(hbm, n_streams=296, n_tok=32768):
     return {"value": tok.numel() / (ms / 1e3), "unit": "tokens/s", "kernel": "irm_cdc_xxh64 (K1)",
             "workload": f"{n_streams} streams x {n_tok} tokens (config-5 scale wave)", "launch_ms": ms,
             "roofline": {"bound": "hbm", "achieved": byt / (ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-                         "frac": byt / (ms / 1e3) / 1e9 / hbm}}
+                         "frac": byt / (ms / 1e3) / 1e9 / hbm},
+            "note": "nominal HBM bound only: the launch is set by each region's serial chain and walker "
+                    "(~1,024 dependent 32-token steps and ~205 dependent chunk decisions per region, 2 regions "
+                    "per SM; profiles/r02_k1_wide.md)"}
 
 
 # ----------------------------------------------------------------- K5 component
