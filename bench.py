@@ -80,6 +80,16 @@ def timed_flushed(fn, reps):
     return sum(a.elapsed_time(b) for a, b in ev) / reps
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    """The one JSON line on stdout (see ``main``: everything else written to fd 1 goes to stderr)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def nccl_logs_to_stderr(world):
     """N > 1: NCCL's communicator lines (ranks, NVLink / NVLS paths) stay visible, on stderr,
     so stdout keeps exactly one JSON line."""
@@ -582,7 +592,7 @@ def run_ours(args):
         sample = pack_tails(make_wave(np.random.default_rng(1000), header, marker, body, R))
         line["cpu_baseline"] = cpu_baseline(args, sample, sample_requests=R - 1)
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
     if dist.is_initialized():
         dist.destroy_process_group()
 
@@ -1005,6 +1015,31 @@ def run_config5(args):
     every_us = [torch.zeros_like(xt) for _ in range(world)]
     dist.all_gather(every_us, xt)
     exchange_us = [float(x.item()) for x in every_us]
+    # the same exchange as the timed step runs it: captured once in a CUDA graph, replayed
+    exchange_graph_us = None
+    if graphs:
+        gx = torch.cuda.CUDAGraph()
+        sx = torch.cuda.Stream()
+        sx.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(sx):
+            pipe.k3_sharded(10**6)
+        torch.cuda.current_stream().wait_stream(sx)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gx):
+            pipe.k3_sharded(10**6)
+        gx.replay()
+        torch.cuda.synchronize()
+        dist.barrier()
+        x0.record()
+        for _ in range(10):
+            gx.replay()
+        x1.record()
+        torch.cuda.synchronize()
+        xt = torch.tensor([x0.elapsed_time(x1) * 1e3 / 10], device=dev)
+        every_us = [torch.zeros_like(xt) for _ in range(world)]
+        dist.all_gather(every_us, xt)
+        exchange_graph_us = [float(x.item()) for x in every_us]
+        del gx
     # K4 of that re-probed wave (every chunk a hit), timed alone after an L2 flush: the roofline
     k4_rows = int(pipe.length.sum().item()) * LAYERS
     ng = int(pipe.groups.n_groups.item())
@@ -1031,7 +1066,9 @@ def run_config5(args):
                                % (k4_placement(K4_SMS_SHARDED), backend,
                                   " captured in the CUDA graphs" if graphs else ", streams"),
                    "parallelism": f"sessions s mod G over {world} GPU(s), store sharded by fingerprint prefix"},
-        "exchange": {"lookup_us_per_rank": exchange_us,
+        "exchange": {"lookup_us_per_rank": exchange_us, "lookup_graph_us_per_rank": exchange_graph_us,
+                     "lookup_graph_note": "the same exchange captured in one CUDA graph and replayed (10 replays, "
+                                          "CUDA events per rank): the form the timed step runs",
                      "lookup_note": "eager (host-launched) exchange of one wave (re-probe, all hits): irm_exchange_pack, "
                                     "all-to-all, split, K3 on the owner's shard, reply, reverse all-to-all, unpack, "
                                     "replica lookup; CUDA events per rank; in the timed step the same work is "
@@ -1056,7 +1093,7 @@ def run_config5(args):
         "clocks": clk.summary(),
     }
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
     dist.destroy_process_group()
 
 
@@ -1456,7 +1493,7 @@ def run_reference(args):
                        "requests_per_step": n_sample},
             "cpu_baseline": {**vals[-1], "value": v},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
 
 
 def main():
@@ -1478,6 +1515,12 @@ def main():
                     help="one graph per wave, K1 -> K3 -> K4 in series (default: wave i's K4 overlaps "
                          "K1 + K3 of wave i + 1)")
     args = ap.parse_args()
+    # stdout carries exactly one JSON line: libraries that print to fd 1 from C (NCCL's
+    # "NCCL version" banner, for one) are sent to stderr, the line goes to a dup of the real stdout
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "config5":
