@@ -4,7 +4,7 @@
   compute-sanitizer --tool memcheck --target-processes all python tools/sanitize_cases.py [names]
 
 Each case checks its own result against the oracle so a sanitizer run is also a
-parity run. Cases: k1_fused k1_split k2 k3 k4 k4_fanout k0 rebase producer k5_v3 k5_v2 k5_1sm"""
+parity run. Cases: k1_fused k1_split k1_fused_table k1_split_table k2 k3 k4 k4_fanout k0 rebase producer k5_v3 k5_v2 k5_1sm"""
 import os
 import sys
 
@@ -17,14 +17,22 @@ from oracle import oracle as O  # noqa: E402
 from paper_2605_05696_b200 import _native as N, ops  # noqa: E402
 
 
-def k1(form):
+def k1(form, table=False):
+    import functools
+
     os.environ["IRM_CDC_FORM"] = form
     rng = np.random.default_rng(1)
     streams = [rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32) for n in (3000, 1, 777, 5000)]
     pins = [[100, 101, 2000], [], [5], [4095]]
     from paper_2605_05696_b200 import chunking
 
-    t = chunking.cdc_chunk_batch(streams, chunking.ChunkerParams(), [set(p) for p in pins])
+    orig = ops.cdc_xxh64
+    if table:  # the Gear table read from memory instead of computed from the seed
+        ops.cdc_xxh64 = functools.partial(orig, gear_from_table=True)
+    try:
+        t = chunking.cdc_chunk_batch(streams, chunking.ChunkerParams(), [set(p) for p in pins])
+    finally:
+        ops.cdc_xxh64 = orig
     st, ln, fp, fo, off = t.to_host()
     for i, s in enumerate(streams):
         o = O.cdc_chunk(s, pins=pins[i])
@@ -132,7 +140,8 @@ def k5(kind):
         os.environ.pop(k, None)
 
 
-CASES = {"k1_fused": lambda: k1("fused"), "k1_split": lambda: k1("split"), "k2": k2, "k3": k3,
+CASES = {"k1_fused": lambda: k1("fused"), "k1_split": lambda: k1("split"),
+         "k1_fused_table": lambda: k1("fused", True), "k1_split_table": lambda: k1("split", True), "k2": k2, "k3": k3,
          "k4": lambda: k4(False), "k4_fanout": lambda: k4(True), "k0": k0, "rebase": rebase, "producer": producer,
          "k5_v3": lambda: k5("v3"), "k5_v2": lambda: k5("v2"), "k5_1sm": lambda: k5("1sm")}
 
