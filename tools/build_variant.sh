@@ -10,5 +10,5 @@ nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-c
   -c paper_2605_05696_b200/csrc/mla.cu -o _variants/obj/mla_$name.o 2> _variants/obj/mla_$name.ptxas.txt
 O=paper_2605_05696_b200/_lib/obj
 nvcc $ARCH -shared -o _variants/$name.so $O/runtime.o $O/cdc.o $O/store.o $O/rotate.o $O/fanout.o \
-  _variants/obj/mla_$name.o $O/prefix.o $O/ingest.o -lcuda -lpthread
+  _variants/obj/mla_$name.o $O/prefix.o $O/ingest.o $O/exchange.o -lcuda -lpthread
 grep -A2 "mla_reattach_2sm_v3" _variants/obj/mla_$name.ptxas.txt | grep -o "Used [0-9]* registers\|[0-9]* bytes spill stores" | tr '\n' ' '; echo " -> _variants/$name.so"
