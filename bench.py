@@ -519,7 +519,13 @@ def run_ours(args):
         longest_region = max([longest_region] + [b - a for a, b in zip(cuts[:-1], cuts[1:])])
     sm_mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0)) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
-    chain_floor_us = -(-longest_region // 32) * 85 / sm_mhz
+    # serial floors of one region, each measured alone on one warp: the shipped chain step
+    # (tools/chain_microbench.cu "shipped lean step": 33.8 cycles per 32 tokens) and the walker
+    # (tools/walker_microbench.cu: 228 cycles per chunk at this chunk density, stores included)
+    chain_floor_us = -(-longest_region // 32) * 33.8 / sm_mhz
+    walker_chunks = longest_region * n_queries / max(tok_per_wave, 1)
+    walker_floor_us = walker_chunks * 228 / sm_mhz
+    serial_floor_us = max(chain_floor_us, walker_floor_us)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -550,13 +556,17 @@ def run_ours(args):
         "components": {
             "cdc_hash": {"value": tok_per_wave / (k1 / 1e3), "unit": "tokens/s", "kernel": "irm_cdc_xxh64 (K1)",
                          "launch_ms": k1, "tokens_per_launch": tok_per_wave,
-                         "note": "bound by the one-bit carried chain of the longest pin-delimited region "
-                                 "(DESIGN.md K1), not by HBM",
-                         "roofline": {"bound": "chain", "achieved": chain_floor_us / (k1 * 1e3), "peak": 1.0,
-                                      "unit": "fraction of the chain floor", "frac": chain_floor_us / (k1 * 1e3),
-                                      "chain_floor_us": chain_floor_us, "longest_region_tokens": longest_region,
-                                      "floor_rule": "ceil(tokens / 32) x 85 cycles (tools/chain_microbench.cu) "
-                                                    "at the max SM clock",
+                         "note": "bound by the serial work of the longest pin-delimited region: the one-bit "
+                                 "carried chain and the boundary walker (DESIGN.md K1), not by HBM",
+                         "roofline": {"bound": "serial", "achieved": serial_floor_us / (k1 * 1e3), "peak": 1.0,
+                                      "unit": "fraction of the region's serial floor",
+                                      "frac": serial_floor_us / (k1 * 1e3), "serial_floor_us": serial_floor_us,
+                                      "chain_floor_us": chain_floor_us, "walker_floor_us": walker_floor_us,
+                                      "longest_region_tokens": longest_region,
+                                      "floor_rule": "max(chain: ceil(tokens / 32) x 33.8 cycles, walker: chunks x 228 "
+                                                    "cycles), each the shipped step timed alone on one warp "
+                                                    "(tools/chain_microbench.cu, tools/walker_microbench.cu), at "
+                                                    "the max SM clock; the launch adds G, hashing and planning",
                                       "hbm_frac": k1_gbs / hbm}},
             "cdc_hash_wide": cdc_wide_component(hbm),
             "producer_rotate": producer_component(hbm),

@@ -94,6 +94,34 @@ __global__ void bench(const uint64_t *G, uint32_t *out, long long *cyc, int step
     t1 = clock64();
     if (lane == 0) cyc[6] = t1 - t0;
     out[192 + lane] = Blo;
+    // variant 7: the shipped chain step (cdc.cu chain_tile, IRM_CDC_CHAIN_LEAN): lane j = 31 - lane so
+    // the ballot is already bit-reversed, G's high word by a 32-bit load 4 steps ahead, carry-boundary
+    // test OR-accumulated, lane 0 stores W
+    {
+        const int j = 31 - lane;
+        const uint32_t *sGhi = reinterpret_cast<const uint32_t *>(sG) + 1;
+        uint32_t Blo7 = 0, Bhi7 = 0, acc = 0;
+        uint32_t Gq[4];
+        for (int a = 0; a < 4; ++a) Gq[a] = sGhi[2 * (a * 32 + j)];
+        t0 = clock64();
+#pragma unroll 4
+        for (int s = 0; s < steps; ++s) {
+            const uint32_t Ghi = Gq[0];
+            Gq[0] = Gq[1];
+            Gq[1] = Gq[2];
+            Gq[2] = Gq[3];
+            Gq[3] = sGhi[2 * (((s + 4) & 31) * 32 + j)];
+            const uint32_t hs = Ghi + __funnelshift_l(Blo7, Bhi7, j);
+            const unsigned W = __ballot_sync(0xffffffffu, (int32_t)hs < 0);
+            acc |= (hs + 2u) ^ hs;
+            if (lane == 0) sBm[s & 1023] = W;
+            Bhi7 = Blo7;
+            Blo7 = W;
+        }
+        t1 = clock64();
+        if (lane == 0) cyc[7] = t1 - t0;
+        out[224 + lane] = Blo7 ^ acc;
+    }
 }
 
 int main() {
@@ -107,9 +135,9 @@ int main() {
     const int steps = 4096;
     for (int rep = 0; rep < 2; ++rep) bench<<<1, 32>>>(G, out, cyc, steps);
     long long h[8];
-    cudaMemcpy(h, cyc, 56, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h, cyc, 64, cudaMemcpyDeviceToHost);
     const char *names[] = {"ballot+brev core", "+und ballot+branch", "+all-lane STS", "+lane0 STS",
-                           "ballot-only chain", "brev-only chain", "shfl-only chain"};
-    for (int i = 0; i < 7; ++i) printf("%-22s %.1f cycles/step\n", names[i], (double)h[i] / steps);
+                           "ballot-only chain", "brev-only chain", "shfl-only chain", "shipped lean step"};
+    for (int i = 0; i < 8; ++i) printf("%-22s %.1f cycles/step\n", names[i], (double)h[i] / steps);
     return 0;
 }
