@@ -210,12 +210,12 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
 
     # ---- producer: novel chunks, in entry order (== insert epoch order)
     novel = np.nonzero(h_hit == 0)[0]
-    for c in novel[np.argsort(h_entry[novel], kind="stable")]:
-        ri = int(np.searchsorted(off, c, side="right") - 1)
-        s, l = int(h_start[c]), int(h_len[c])
-        toks = tails[ri][s:s + l]
-        assert int(h_entry[c]) == len(reg), "device store and host mirror diverged"
-        reg.commit_rows(int(h_fp_u[c]), toks, plans[ri].m + s, int(h_row[c]))
+    novel = novel[np.argsort(h_entry[novel], kind="stable")]
+    nov_req = (np.searchsorted(off, novel, side="right") - 1).tolist()
+    for c, ri, s, l, e, f, rw in zip(novel.tolist(), nov_req, h_start[novel].tolist(), h_len[novel].tolist(),
+                                     h_entry[novel].tolist(), h_fp_u[novel].tolist(), h_row[novel].tolist()):
+        assert e == len(reg), "device store and host mirror diverged"
+        reg.commit_rows(f, tails[ri][s:s + l], plans[ri].m + s, rw)
 
     # ---- S1 sub-window fallback (engine.py:116-139, 211-226), batched: every aligned full
     # window of every novel chunk is fingerprinted by ONE K2 launch; in the sequential order
@@ -225,7 +225,9 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
     if config.s1_enabled:
         s1_hits = _s1_batch(state, tails, [p.m for p in plans], off, h_hit, h_start, h_len)
 
-    # ---- events, per request in chunk order
+    # ---- events, per request in chunk order (Python lists: no numpy scalar per field access)
+    l_start, l_len, l_hit, l_psrc, l_fp, l_off = (h_start.tolist(), h_len.tolist(), h_hit.tolist(),
+                                                  h_psrc.tolist(), h_fp_u.tolist(), off.tolist())
     results: list[ServeResult] = []
     live_hits = []  # (request, chunk index)
     for ri, plan in enumerate(plans):
@@ -238,9 +240,9 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
             counts[ServiceClass.PREFIX_HIT] = m
             events.append(SegmentEvent(0, m, ServiceClass.PREFIX_HIT))
             live_rows += m
-        for c in range(int(off[ri]), int(off[ri + 1])):
-            p = m + int(h_start[c])
-            ln = int(h_len[c])
+        for c in range(l_off[ri], l_off[ri + 1]):
+            p = m + l_start[c]
+            ln = l_len[c]
             if p < carve:
                 carved = min(carve - p, ln)
                 counts[ServiceClass.CARVEOUT_PREFILL] += carved
@@ -250,9 +252,9 @@ def serve_batch(state: EngineState, requests: Sequence[Request]) -> list[ServeRe
                     events.append(SegmentEvent(p + carved, ln - carved, ServiceClass.NOVEL_PREFILL))
                 live_rows += ln
                 continue
-            if h_hit[c] == 1:
+            if l_hit[c] == 1:
                 counts[ServiceClass.PIC_HIT] += ln
-                events.append(SegmentEvent(p, ln, ServiceClass.PIC_HIT, int(h_fp_u[c]), p - int(h_psrc[c])))
+                events.append(SegmentEvent(p, ln, ServiceClass.PIC_HIT, l_fp[c], p - l_psrc[c]))
                 if config.mode == Mode.LIVE:
                     live_hits.append((ri, c, len(events) - 1))
                 continue
