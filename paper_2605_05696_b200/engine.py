@@ -112,10 +112,11 @@ class LiveVerificationError(AssertionError):
 class EngineState:
     """Mutable caches shared across the requests of one trace run."""
 
-    def __init__(self, config: ServeConfig, max_entries: int = 1 << 16, max_prefixes: int = 1 << 18,
-                 max_tokens: int = 1 << 21):
-        """Device capacities are initial sizes (the prefix index grows on demand): a
-        state costs ~10 MB of device memory until a trace needs more."""
+    def __init__(self, config: ServeConfig, max_entries: int = 1 << 16, max_prefixes: int = 1 << 22,
+                 max_tokens: int = 1 << 24):
+        """Device capacities are initial sizes (the prefix index grows on demand). Sized
+        for a few million tokens up front: growing inside a serve (a table rebuild and
+        fresh device allocations) cost more than the allocation (serve API: 28 -> 92 ms)."""
         self.config = config
         self.tree = DeviceRadixTree(max_prefixes=max_prefixes, max_tokens=max_tokens)  # K0
         self.registry = KvRegistry(config.kv, config.spec, max_entries=max_entries)
