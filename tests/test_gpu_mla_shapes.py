@@ -52,3 +52,35 @@ def test_mla_benchmarked_shape(name, kernel, monkeypatch):
     # the documents really were re-permuted (seams and non-zero deltas exercised; a few
     # documents may land in their cached slot, delta 0)
     assert np.count_nonzero(w["deltas"]) >= w["n_docs"] // 2
+
+
+@pytest.mark.parametrize("name", ["config2_32k_dsv2", "config4_128k"])
+@pytest.mark.parametrize("kernel", ["2sm-v3", "2sm-v2", "1sm"])
+def test_mla_repeat_launches_bit_identical(name, kernel, monkeypatch):
+    """The same launch repeated back to back gives bit-identical output and lse: the online
+    softmax walks a fixed per-pair tile order, so any difference is a race (P in TMEM showed
+    one: ~1-2K differing elements per 128K/8K launch and occasional faults)."""
+    import torch
+
+    import bench
+    from paper_2605_05696_b200 import _native as N, ops
+
+    monkeypatch.delenv("IRM_MLA_1SM", raising=False)
+    monkeypatch.delenv("IRM_MLA_V2", raising=False)
+    if kernel == "1sm":
+        monkeypatch.setenv("IRM_MLA_1SM", "1")
+    elif kernel == "2sm-v2":
+        monkeypatch.setenv("IRM_MLA_V2", "1")
+    c = SHAPES[name]
+    # the bench's own workload (default seed): the P-in-TMEM race showed on it at 128K / 8K
+    w = bench.attn_workload(c["n_ctx"], c["n_q"], 16, c["theta"],
+                            N.LAYOUT_INTERLEAVED if c["interleaved"] else N.LAYOUT_HALF_SPLIT)
+    run = lambda: ops.mla_reattach_prefill(w["q"], w["pool"], w["n_ctx"], w["n_ctx"] - w["n_q"], 192 ** -0.5,
+                                           kv_rows=w["rows_d"], kv_chunk=w["chunk_d"], chunk_cs=w["cs"],
+                                           layout=w["layout"])
+    out0, lse0 = run()
+    torch.cuda.synchronize()
+    for _ in range(6):
+        out, lse = run()
+        torch.cuda.synchronize()
+        assert torch.equal(out, out0) and torch.equal(lse, lse0)
