@@ -146,3 +146,34 @@ def test_fanout_bounds_are_skipped_and_flagged():
         assert o[:, 20:].abs().sum() == 0  # nothing else written
         with pytest.raises(ValueError, match="source run outside"):
             ops.check_status(status)
+
+
+def test_fanout_repeat_launches_bit_identical():
+    """K4 fan-out relaunched back to back on a 27-layer wave (8 members per source run, all SMs
+    and the 4-round retiring grid) writes bit-identical rows, equal to the plain gather's."""
+    from paper_2605_05696_b200 import _native as N, ops
+
+    rng = np.random.default_rng(11)
+    L, rows, n_src, members = 27, 12000, 60, 8
+    lens = rng.integers(32, 300, size=n_src).astype(np.int32)
+    starts = rng.integers(0, rows - 300, size=n_src).astype(np.int64)
+    perm = rng.permutation(n_src * members)
+    src, ln = np.repeat(starts, members)[perm], np.repeat(lens, members)[perm]
+    dst = np.concatenate([[0], np.cumsum(ln)[:-1]]).astype(np.int64)
+    delta = rng.integers(-(2**17), 2**17, size=src.size).astype(np.int64)
+    pool = torch.randn(L, rows, 576, device="cuda").to(torch.bfloat16)
+    out = torch.zeros(L, int(dst[-1] + ln[-1]), 576, dtype=torch.bfloat16, device="cuda")
+    src_d, dst_d, ln_d, delta_d = _d(src), _d(dst), _d(ln), _d(delta)
+    inv = ops.inv_freq_device(np.power(1e4, -2.0 * np.arange(32) / 64))
+    groups = ops.SourceGroups.alloc(src.size, "cuda")
+    n_dev = torch.tensor([src.size], dtype=torch.int64, device="cuda")
+    ops.rotate_gather(pool, out, src_d, dst_d, ln_d, delta_d, inv, layout=N.LAYOUT_INTERLEAVED)
+    torch.cuda.synchronize()
+    ref = out.clone()
+    for max_sms, rounds in [(0, 1)] * 4 + [(140, 4)] * 4:
+        out.zero_()
+        ops.group_by_source(src_d, dst_d, ln_d, delta_d, groups, n_dev=n_dev)
+        ops.rotate_gather_fanout(pool, out, groups, inv, layout=N.LAYOUT_INTERLEAVED, n_members_dev=n_dev,
+                                 max_sms=max_sms, cta_rounds=rounds)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
