@@ -1272,6 +1272,14 @@ mla_reattach_2sm_v3_kernel(Params p, const __grid_constant__ CUtensorMap tmap_po
             };
             for (int t = 0; t < NS - 1 && t < T; ++t) issue_qk(t);
             for (int t = 0; t < T; ++t) {
+#ifdef IRM_MLA_PT_WAIT_PV
+                // experiment: with P in TMEM, QK(t + NS - 1) overwrites the columns PV(t - 1) reads P from;
+                // wait for PV(t - 1) to complete before issuing it
+                if (PT && t >= 1 && t + NS - 1 < T) {
+                    mbar_wait(&b_odone[(t - 1) & 1], ((t - 1) >> 1) & 1);
+                    tc::fence_after();
+                }
+#endif
                 if (t + NS - 1 < T) issue_qk(t + NS - 1);  // reuses the S buffer softmax(t-1) has read
                 const int st = t % KST;
                 long long a0 = prof_clock<2>();
