@@ -1166,7 +1166,7 @@ def serve_api_component(n_warm=8):
                                                model.Segment("body", body, "agent_body"))))
     text = model.serialize_trace(model.Trace(tuple(reqs)))
     times = []
-    for _ in range(4):  # the first pass pays one-time library / allocator set-up; median of the other 3
+    for _ in range(6):  # the first pass pays one-time library / allocator set-up; median of the other 5
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         trace = model.parse_trace(io.StringIO(text))
@@ -1192,7 +1192,7 @@ def serve_api_component(n_warm=8):
             h.update(repr((ri, e.start, e.length, e.klass.value, e.fingerprint, e.delta)).encode())
     out = {"value": n_tok / dt, "unit": "tokens/s", "api": "model.parse_trace + engine.run_trace (observer)",
            "workload": f"{1 + n_warm} x {n_tok // (1 + n_warm)}-token agent_meta requests as JSONL "
-                       f"({len(text) / 1e6:.1f} MB), one serve batch; median of 3 timed passes, each with a "
+                       f"({len(text) / 1e6:.1f} MB), one serve batch; median of 5 timed passes, each with a "
                        f"fresh EngineState", "seconds": dt,
            "pic_hit_tokens": pic, "warm_total_cached": row.warm_total, "events_digest": h.hexdigest()[:16]}
     ref_dir = os.path.join(ROOT, "baseline", "_ref")
