@@ -649,22 +649,37 @@ def sharded_parity(pipe, plan, R, header, marker, body, check_dev, graphs, peers
     rotate+gather of the WRITER's pool bytes (peer pools read through their
     CUDA-IPC mappings) -- ranks other than the body's first writer read rows
     fetched from another GPU."""
+    # every rank's waves in serve order (the plan's order; the same generator calls as run_ours)
+    def waves_of(k):
+        rng = np.random.default_rng(1000 + k)
+        ws = {kind: [pack_requests(*make_requests(rng, header, marker, body, R)) for _ in range(n)]
+              for kind, n in plan.items()}
+        return [w for kind in plan for w in ws[kind]]
+
+    return sharded_check(pipe, waves_of, R, check_dev, graphs, peers, novel_rows, req_stride, wave0, rank, world,
+                         chunks_per_request)
+
+
+def sharded_check(pipe, waves_of, R, check_dev, graphs, peers, novel_rows, req_stride, wave0, rank, world,
+                  chunks_per_request=3, prefix=True):
+    """The common part of the N > 1 checkers: serve this rank's check wave (``check_dev``)
+    through the sharded path, then replay one global sequential oracle over ``waves_of(k)``
+    (rank k's whole-request waves in serve order, its check wave last) for every rank k:
+    phase 1 per rank, first-writer-wins across ranks in the exchange's order (wave, request,
+    rank), owner-allocated rows; check this rank's service map and a KV sample against the
+    writer's pool bytes; gather every rank's verdict. ``prefix``: the waves are whole
+    requests (phase 1 on the device, replayed exactly here) -- else tails with their m."""
     import torch
 
     from oracle import oracle as O
 
     grab = {}
-    run_sharded(pipe, 1, lambda i: pipe.load_requests(*check_dev), wave0, graphs,
+    load = (lambda i: pipe.load_requests(*check_dev)) if prefix else (lambda i: pipe.load(*check_dev))
+    run_sharded(pipe, 1, load, wave0, graphs,
                 after_front=lambda i, s: grab.__setitem__("hit", pipe.slots[s]["hit"].clone()))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    # every rank's waves in serve order (the plan's order; the same generator calls as run_ours)
-    per_rank = []
-    for k in range(world):
-        rng = np.random.default_rng(1000 + k)
-        ws = {kind: [pack_requests(*make_requests(rng, header, marker, body, R)) for _ in range(n)]
-              for kind, n in plan.items()}
-        per_rank.append(whole_to_tails([w for kind in plan for w in ws[kind]]))
+    per_rank = [whole_to_tails(waves_of(k)) if prefix else waves_of(k) for k in range(world)]
     n_waves = len(per_rank[0])
     chunks = [[None] * n_waves for _ in range(world)]
     for k in range(world):
@@ -919,9 +934,11 @@ def run_config5(args):
     cold_dev = [to_dev(p) for p in cold]
     warm_dev = [to_dev(p) for p in warm[:n_steps + 1]]
     warm_host = [to_pin(p) for p in warm[n_steps + 1:]]
-    max_tok = max(int(p[1][-1]) for p in cold + warm)
-    max_pins = max(int(p[2][-1]) for p in cold + warm)
-    req_stride = max(int(np.diff(p[1]).max()) for p in cold + warm) + C5_HEADER
+    check_wave = c5_wave(rank, world, sessions, 0, 10_000, header, doc, marker)  # the in-run checker's wave
+    sized = cold + warm + [check_wave]
+    max_tok = max(int(p[1][-1]) for p in sized)
+    max_pins = max(int(p[2][-1]) for p in sized)
+    req_stride = max(int(np.diff(p[1]).max()) for p in sized) + C5_HEADER
 
     # pool: [0, novel) first-writer rows (one sub-range per owner), then replicas, then scratch
     n_waves_total = n_cold + 2 * n_steps + 4
@@ -937,7 +954,8 @@ def run_config5(args):
     inv = ops.inv_freq_device(np.power(THETA, -2.0 * np.arange(KR // 2) / KR))
     store = ops.ChunkStore(max_entries=1 << 20)
     pipe = ReattachPipeline(store, pool, inv, C5_R, max_tok, max_pins, req_stride, layout=N.LAYOUT_INTERLEAVED)
-    cache = shard.ReplicaCache(pool, novel_rows, shard.map_peer_pools(pool), rank, ops.ChunkStore(max_entries=1 << 14),
+    peers = shard.map_peer_pools(pool)
+    cache = shard.ReplicaCache(pool, novel_rows, peers, rank, ops.ChunkStore(max_entries=1 << 14),
                                scratch_rows=scratch)
     sharded = shard.ShardedStore(store, novel_rows)
     pipe.enable_sharding(sharded, cache, rank, world)
@@ -1058,11 +1076,20 @@ def run_config5(args):
     k4_bytes = (k4_rows + src_rows) * (CKV + KR) * 2
     k4_gbs = k4_bytes / (k4_ms / 1e3) / 1e9
 
-    parity = {"checked": False, "why": "N > 1: the global oracle needs every rank's waves"}
     if world == 1:
-        check = c5_wave(rank, world, sessions, 0, 10_000, header, doc, marker)
+        check = check_wave
         served = cold + warm[:n_steps] + warm[n_steps + 1:n_steps + 1 + n_e2e]
         parity = pipeline_parity(pipe, served, check, to_dev(check), True, True, graphs, pool, req_stride, wave0=wave)
+    else:  # every rank's check wave vs one global oracle over all ranks' waves (rebuilt per rank k)
+        def waves_of(k):
+            c = [c5_wave(k, world, sessions, b, 0, header, doc, marker) for b in range(n_cold)]
+            wk = [c5_wave(k, world, sessions, b, t, header, doc, marker) for b, t in sched]
+            return (c + wk[:n_steps] + wk[n_steps + 1:n_steps + 1 + n_e2e]
+                    + [c5_wave(k, world, sessions, 0, 10_000, header, doc, marker)])
+
+        check = check_wave
+        parity = sharded_check(pipe, waves_of, C5_R, to_dev(check), graphs, peers, novel_rows, req_stride, wave,
+                               rank, world, prefix=False)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
