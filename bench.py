@@ -1415,7 +1415,10 @@ def fused_attn_component(args, tf_peak, peak_kind, n_ctx=65536, n_q=4096, heads=
                         f"{'DSv2 interleaved' if layout == N.LAYOUT_INTERLEAVED else 'DSv3 half-split'} theta {theta:g}, bf16",
             "launch_ms": ms, "flop_per_launch": flops,
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": tf_peak, "unit": "TFLOP/s",
-                         "frac": tflops / tf_peak, "peak_kind": f"{peak_kind} bf16 burst"}}
+                         "frac": tflops / tf_peak, "peak_kind": f"{peak_kind} bf16 burst",
+                         "frac_vs_sustained": tflops / peaks()[2],
+                         "note": "a multi-ms launch runs into the 1 kW cap like cuBLAS's sustained loop "
+                                 "(profiles/r02_k5_bound.md §3); frac is against the burst figure"}}
 
 
 # ----------------------------------------------------------------- CPU legs
